@@ -1,0 +1,176 @@
+/*
+ * sbx.h — C-ABI of the B200-native refined-wall Stokes solver.
+ *
+ * Drop-in boundary for the reference's C++ solver API
+ * (/root/reference/proj/include/stokesbie/*.hpp).  The reference exposes
+ * Eigen value types and exceptions and has no C ABI or FFI of its own (its
+ * python/ binding is an empty stub, proj/python/CMakeLists.txt:1); each entry
+ * point below names the reference call it replaces.  Plain pointers and sizes
+ * only — no torch or CUDA types in the signatures (streams are `void*`
+ * aliases of cudaStream_t, NULL = the library stream).
+ *
+ * Conventions (mirroring proj/include/stokesbie/common.hpp:11-15,
+ * geometry.hpp:60-62):
+ *   - unknowns are interleaved per node: scalar index = 2*node + component;
+ *   - multi-RHS blocks are n x nrhs, column-major with leading dimension ld;
+ *   - handles are immutable after build, so concurrent solves on distinct
+ *     streams are legal;
+ *   - every function returns a status code (SBX_OK ...) and, on failure, a
+ *     thread-local message is available from sbx_last_error() (the
+ *     reference's exception text, including SingularMatrixError::where).
+ */
+#ifndef SBX_H_
+#define SBX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (exception classes of common.hpp:20-52, CLI exit codes of
+ * tools/bench_main.cpp:42-55). */
+enum {
+  SBX_OK = 0,
+  SBX_INVALID_ARGUMENT = 1,   /* std::invalid_argument from require()        */
+  SBX_NONCONVERGENCE = 2,     /* ConvergenceError (reserved)                  */
+  SBX_GEOMETRY_ERROR = 3,     /* GeometryError                                */
+  SBX_SINGULAR_MATRIX = 4,    /* SingularMatrixError{where}                   */
+  SBX_PROXY_VIOLATION = 5,    /* ProxyViolationError                          */
+  SBX_CUDA_ERROR = 6,         /* CUDA / NCCL failure (no CPU fallback)        */
+  SBX_RUNTIME_ERROR = 7       /* any other std::runtime_error (e.g. HBS1 I/O) */
+};
+
+/* Curve kinds (geometry.hpp:10 CurveKind) and formulations (kernels.hpp:35). */
+enum { SBX_CIRCLE = 0, SBX_ELLIPSE = 1, SBX_STAR = 2, SBX_FOURIER = 3 };
+enum { SBX_INTERIOR_DIRICHLET = 0, SBX_EXTERIOR_COMBINED = 1, SBX_MIXED = 2 };
+
+/* Sweep flags. */
+enum {
+  SBX_TRANSPOSE = 1,     /* hbs_solve_t / hbs_apply_t                        */
+  SBX_DEVICE_PTRS = 2    /* b / x are device pointers (else host, pinned or
+                            pageable; copies are issued on the stream)     */
+};
+
+typedef struct sbx_geom_s* sbx_geom;     /* Discretization           */
+typedef struct sbx_plan_s* sbx_plan;     /* RefinementPlan           */
+typedef struct sbx_hbs_s* sbx_hbs;       /* HbsOperator (device)     */
+typedef struct sbx_update_s* sbx_update; /* LowRankUpdate (device)   */
+typedef struct sbx_els_s* sbx_els;       /* ElsSolver (device)       */
+
+/* CurveParams (geometry.hpp:14-26). */
+typedef struct {
+  int32_t kind;
+  double center_x, center_y, scale;
+  int32_t flip_normal, n_prongs;
+  double amplitude, aspect;
+  int32_t n_cos, n_sin;          /* fourier coefficient counts (<= 16 each) */
+  double cos_coef[16], sin_coef[16];
+} sbx_curve;
+
+/* HbsOptions (hbs.hpp:39-46). n_proxy is accepted and, as in the reference
+ * (hbs.cpp:276-279), ignored: compression always starts at 64 samples. */
+typedef struct {
+  double eps;          /* 1e-10 */
+  int64_t leaf_nodes;  /* 64    */
+  int32_t n_proxy;     /* 64    */
+  double bas_factor;   /* 1.5   */
+  double div_factor;   /* 3.0   */
+} sbx_hbs_options;
+
+const char* sbx_last_error(void);
+int sbx_init(int device);                  /* selects the CUDA device */
+int sbx_sync(void);                        /* waits for the library stream */
+
+/* ---------------------------------------------------------- geometry
+ * panelize (geometry.hpp:103), build_discretization + add_holes
+ * (geometry.hpp:104-106,134-135), refine (:120-121), coarsen (:124),
+ * panels_near_point (:139-140).  Node generation is O(N) host work. */
+int sbx_geom_create(const sbx_curve* curve, int n_panels, int q, sbx_geom* out);
+int sbx_geom_add_holes(sbx_geom wall, int n_holes, const sbx_curve* holes,
+                       const int32_t* n_panels, const int32_t* q, sbx_geom* out,
+                       sbx_plan* plan);
+int sbx_geom_destroy(sbx_geom g);
+int sbx_geom_info(sbx_geom g, int64_t* n_nodes, int64_t* n_panels, int64_t* n_components);
+/* 9*n doubles: x, y, nx, ny, tx, ty, w, curvature, param; panel_of n int64 */
+int sbx_geom_nodes(sbx_geom g, double* out9, int64_t* panel_of);
+int sbx_panels_near_point(sbx_geom g, double px, double py, double radius,
+                          int64_t* out, int64_t cap, int64_t* count);
+int sbx_refine(sbx_geom g, const int64_t* panel_ids, int64_t n, int m, sbx_geom* out,
+               sbx_plan* plan);
+int sbx_coarsen(sbx_geom g, sbx_plan plan, sbx_geom* out);
+int sbx_plan_destroy(sbx_plan p);
+int sbx_plan_sizes(sbx_plan p, int64_t* n_k, int64_t* n_c, int64_t* n_p);
+int sbx_plan_maps(sbx_plan p, int64_t* kept_old, int64_t* kept_new, int64_t* cut_old,
+                  int64_t* added_new);
+
+/* ---------------------------------------------------------- entries / data
+ * BieAssembler::submatrix (nystrom.hpp:30) evaluated on the device;
+ * boundary_data (nystrom.hpp:116-117). Host in/out buffers. */
+int sbx_submatrix(sbx_geom g, int formulation, double mu, const int64_t* rows, int64_t nr,
+                  const int64_t* cols, int64_t nc, double* out);
+int sbx_boundary_data(sbx_geom g, int64_t n_src, const double* src_xyf, double mu,
+                      double* out);
+
+/* ---------------------------------------------------------- HBS
+ * hbs_compress (hbs.hpp:80, on the device), hbs_invert (:85),
+ * hbs_solve/_t, hbs_apply/_t (:87-94), hbs_save/hbs_load "HBS1" (:97-98). */
+int sbx_hbs_compress(sbx_geom g, int formulation, double mu, const sbx_hbs_options* opts,
+                     sbx_hbs* out);
+int sbx_hbs_compress_subset(sbx_geom g, int formulation, double mu, const int64_t* nodes,
+                            int64_t n_nodes, const sbx_hbs_options* opts, sbx_hbs* out);
+int sbx_hbs_invert(sbx_hbs h);
+int sbx_hbs_destroy(sbx_hbs h);
+int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double* x,
+                  int64_t ldx, int flags, void* stream);
+int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double* y,
+                  int64_t ldy, int flags, void* stream);
+int sbx_hbs_save_hbs1(sbx_hbs h, const char* path);
+int sbx_hbs_load_hbs1(const char* path, sbx_hbs* out);
+/* info[0..9]: n, nodes, total_skeleton, max_block_drawn, has_inverse,
+ * solve_factor_doubles, max_depth, max_k, apply_factor_doubles, leaf_nodes */
+int sbx_hbs_info(sbx_hbs h, int64_t* info);
+int sbx_hbs_node_ranks(sbx_hbs h, int64_t* k, int64_t cap);
+
+/* ---------------------------------------------------------- low-rank update
+ * compress_update(blocks, proxy, eps, TwoStepId, {seed}) (lowrank.hpp:59-62),
+ * with BlockSource(old, new, plan) and make_proxy_geometry(new, plan) built
+ * internally (nystrom.hpp:75-76, proxy.hpp:48-49). */
+int sbx_update_compress(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formulation,
+                        double mu, double eps, uint64_t seed, sbx_update* out);
+int sbx_update_destroy(sbx_update u);
+/* info: k, k1, kc.k, kp.k, pk.k, n_ext, nk2, nc2, np2 */
+int sbx_update_info(sbx_update u, int64_t* info);
+/* which: 0 L (n_ext x k), 1 R (k x n_ext); column-major host copies */
+int sbx_update_factor(sbx_update u, int which, double* out);
+/* Tier-1 injection of externally computed factors (dump_matrix exchange,
+ * nystrom.hpp:141-143). */
+int sbx_update_from_factors(sbx_plan plan, const double* L, const double* R, int64_t n_ext,
+                            int64_t k, sbx_update* out);
+
+/* ---------------------------------------------------------- ELS / Woodbury
+ * els_build (els.hpp:42-44), els_solve / els_solve_raw (els.hpp:57,65),
+ * density_on_refined (els.hpp:69). */
+int sbx_els_build(sbx_hbs a_oo, sbx_geom old_g, sbx_geom new_g, sbx_plan plan,
+                  sbx_update upd, int formulation, double mu, sbx_els* out);
+int sbx_els_destroy(sbx_els e);
+/* info: n_k, n_c, n_p (scalars), k, app_is_hbs */
+int sbx_els_info(sbx_els e, int64_t* info);
+/* g_n: (n_k + n_p) x nrhs (kept, added); tau_n same shape. */
+int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, double* tau_n,
+                  int64_t ldt, int flags, void* stream);
+/* g_ext: n_ext x nrhs (kept, cut, added). */
+int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
+                      int64_t ldy, int flags, void* stream);
+int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out);
+/* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
+int sbx_els_xw(sbx_els e, double* X, double* W);
+
+/* ---------------------------------------------------------- diagnostics
+ * Number of sbx kernels launched since the last reset (bench evidence). */
+int64_t sbx_kernel_launches(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBX_H_ */

@@ -116,8 +116,8 @@ void make_householder(double* x, Index n, double& tau, double& beta) {
   } else {
     beta = std::sqrt(c0 * c0 + tail);
     if (c0 >= 0) beta = -beta;
-    const double s = 1.0 / (c0 - beta);
-    for (Index i = 1; i < n; ++i) x[i] *= s;  // Eigen: tail / (c0 - beta)
+    const double s = c0 - beta;
+    for (Index i = 1; i < n; ++i) x[i] /= s;  // Eigen: tail / (c0 - beta)
     tau = (beta - c0) / beta;
   }
 }

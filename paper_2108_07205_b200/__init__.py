@@ -1,0 +1,17 @@
+"""B200-native refined-wall Stokes solver (arXiv 2108.07205 per-time-step path).
+
+Public API mirrors the reference C++ solver (proj/include/stokesbie): see
+``api.py``.  Everything numerical runs in ``_lib/libsbx.so`` (sm_100a CUDA
+kernels behind the C-ABI of ``include/sbx.h``).
+"""
+from .api import (  # noqa: F401
+    CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR,
+    CurveParams, Discretization, ElsSolver, HbsOperator, HbsOptions, LowRankUpdate,
+    RefinementPlan, add_holes, boundary_data, circle, coarsen, compress_update, density_on_refined,
+    ellipse, els_build, els_solve, els_solve_raw, gather_kept_added, hbs_apply, hbs_compress,
+    hbs_invert, hbs_load, hbs_save, hbs_solve, init, kernel_launches, panelize, refine, star,
+    submatrix, update_from_factors,
+)
+from ._sbx import (  # noqa: F401
+    ConvergenceError, CudaError, GeometryError, ProxyViolationError, SbxError, SingularMatrixError,
+)

@@ -1,0 +1,474 @@
+"""Host-side mirror of the reference solver API (proj/include/stokesbie/*.hpp)
+over the sbx C-ABI.  Names, argument meaning and error behaviour follow the
+reference so that code written against it ports line by line:
+
+  reference (C++)                          here
+  ---------------------------------------  ------------------------------------
+  panelize(ParametricCurve(cp), n, q)      panelize(CurveParams(...), n, q)
+  refine(d, panel_ids, m)                  refine(d, panel_ids, m) -> (d1, plan)
+  coarsen(d, plan)                         coarsen(d, plan)
+  add_holes(d, holes)                      add_holes(d, holes) -> (d1, plan)
+  hbs_compress(make_hbs_source(a), opts)   hbs_compress(d, formulation, opts)
+  hbs_invert(op)                           hbs_invert(op)
+  hbs_solve / hbs_apply                    hbs_solve / hbs_apply
+  hbs_save / hbs_load                      hbs_save / hbs_load (HBS1, bit compatible)
+  compress_update(blocks, proxy, eps, ..)  compress_update(d0, d1, plan, eps, ...)
+  els_build(a_oo, blocks, plan, update)    els_build(a_oo, d0, d1, plan, update)
+  els_solve / els_solve_raw                els_solve / els_solve_raw
+  density_on_refined                       density_on_refined
+  boundary_data(d, sources, mu)            boundary_data(d, sources, mu)
+
+Exceptions: ValueError (std::invalid_argument), GeometryError,
+SingularMatrixError (message carries `where`), ProxyViolationError.
+Arrays are numpy float64 (host) or torch CUDA float64 tensors (device, no
+host round trip).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _sbx
+from ._sbx import F64P, I64P, VP, check, lib
+
+CIRCLE, ELLIPSE, STAR, FOURIER = 0, 1, 2, 3
+INTERIOR_DIRICHLET, EXTERIOR_COMBINED, MIXED = 0, 1, 2
+
+_initialized = False
+
+
+def init(device: int = 0):
+    global _initialized
+    check(lib().sbx_init(device))
+    _initialized = True
+
+
+def _ensure():
+    if not _initialized:
+        init(0)
+
+
+@dataclass
+class CurveParams:
+    """geometry.hpp:14-26."""
+    kind: int = CIRCLE
+    center: tuple = (0.0, 0.0)
+    scale: float = 1.0
+    flip_normal: bool = False
+    n_prongs: int = 0
+    amplitude: float = 0.0
+    aspect: float = 1.0
+    cos_coef: Sequence[float] = field(default_factory=list)
+    sin_coef: Sequence[float] = field(default_factory=list)
+
+    def to_c(self) -> _sbx.sbx_curve:
+        c = _sbx.sbx_curve()
+        c.kind = self.kind
+        c.center_x, c.center_y = float(self.center[0]), float(self.center[1])
+        c.scale = self.scale
+        c.flip_normal = int(self.flip_normal)
+        c.n_prongs = self.n_prongs
+        c.amplitude = self.amplitude
+        c.aspect = self.aspect
+        c.n_cos, c.n_sin = len(self.cos_coef), len(self.sin_coef)
+        for i, v in enumerate(self.cos_coef):
+            c.cos_coef[i] = v
+        for i, v in enumerate(self.sin_coef):
+            c.sin_coef[i] = v
+        return c
+
+
+def ellipse(a: float, b: float, center=(0.0, 0.0)) -> CurveParams:
+    return CurveParams(kind=ELLIPSE, center=center, scale=a, aspect=b / a)
+
+
+def star(n_prongs: int, amplitude: float, scale=1.0, center=(0.0, 0.0)) -> CurveParams:
+    return CurveParams(kind=STAR, center=center, scale=scale, n_prongs=n_prongs, amplitude=amplitude)
+
+
+def circle(radius=1.0, center=(0.0, 0.0)) -> CurveParams:
+    return CurveParams(kind=CIRCLE, center=center, scale=radius)
+
+
+class _Handle:
+    _destroy = None
+
+    def __init__(self, ptr):
+        self._ptr = VP(ptr) if not isinstance(ptr, VP) else ptr
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def __del__(self):
+        try:
+            if self._ptr and self._ptr.value and self._destroy and _sbx._lib is not None:
+                getattr(_sbx._lib, self._destroy)(self._ptr)
+                self._ptr = VP()
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class Discretization(_Handle):
+    """geometry.hpp:60-101 (SoA node arrays, interleaved unknowns)."""
+    _destroy = "sbx_geom_destroy"
+
+    def info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().sbx_geom_info(self.ptr, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def n_nodes(self):
+        return self.info()[0]
+
+    def n_unknowns(self):
+        return 2 * self.n_nodes()
+
+    def n_panels(self):
+        return self.info()[1]
+
+    def nodes(self) -> dict:
+        n = self.n_nodes()
+        out = np.zeros(9 * n)
+        pan = np.zeros(n, dtype=np.int64)
+        check(lib().sbx_geom_nodes(self.ptr, out.ctypes.data_as(F64P), pan.ctypes.data_as(I64P)))
+        o = out.reshape(9, n)
+        keys = ("x", "y", "nx", "ny", "tx", "ty", "w", "curvature", "param")
+        d = {k: o[i].copy() for i, k in enumerate(keys)}
+        d["panel_of"] = pan
+        return d
+
+    def panels_near_point(self, point, radius) -> np.ndarray:
+        cap = self.n_panels()
+        out = np.zeros(cap, dtype=np.int64)
+        cnt = C.c_int64()
+        check(lib().sbx_panels_near_point(self.ptr, float(point[0]), float(point[1]), float(radius),
+                                          out.ctypes.data_as(I64P), cap, C.byref(cnt)))
+        return out[: cnt.value]
+
+
+class RefinementPlan(_Handle):
+    """geometry.hpp:105-116."""
+    _destroy = "sbx_plan_destroy"
+
+    def sizes(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().sbx_plan_sizes(self.ptr, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def n_k(self):
+        return self.sizes()[0]
+
+    def n_c(self):
+        return self.sizes()[1]
+
+    def n_p(self):
+        return self.sizes()[2]
+
+    def maps(self) -> dict:
+        nk, nc, npp = self.sizes()
+        ko, kn = np.zeros(nk, np.int64), np.zeros(nk, np.int64)
+        co, an = np.zeros(nc, np.int64), np.zeros(npp, np.int64)
+        check(lib().sbx_plan_maps(self.ptr, ko.ctypes.data_as(I64P), kn.ctypes.data_as(I64P),
+                                  co.ctypes.data_as(I64P), an.ctypes.data_as(I64P)))
+        return {"kept_old": ko, "kept_new": kn, "cut_old": co, "added_new": an}
+
+
+def panelize(curve: CurveParams, n_panels: int, q: int = 16) -> Discretization:
+    _ensure()
+    out = VP()
+    c = curve.to_c()
+    check(lib().sbx_geom_create(C.byref(c), n_panels, q, C.byref(out)))
+    return Discretization(out)
+
+
+def refine(d: Discretization, panel_ids, m: int):
+    ids = np.ascontiguousarray(np.asarray(panel_ids, dtype=np.int64))
+    g, p = VP(), VP()
+    check(lib().sbx_refine(d.ptr, ids.ctypes.data_as(I64P), len(ids), m, C.byref(g), C.byref(p)))
+    return Discretization(g), RefinementPlan(p)
+
+
+def coarsen(d: Discretization, plan: RefinementPlan) -> Discretization:
+    g = VP()
+    check(lib().sbx_coarsen(d.ptr, plan.ptr, C.byref(g)))
+    return Discretization(g)
+
+
+def add_holes(d: Discretization, holes):
+    """holes: iterable of (CurveParams, n_panels, q)."""
+    holes = list(holes)
+    arr = (_sbx.sbx_curve * len(holes))(*[h[0].to_c() for h in holes])
+    npn = (C.c_int32 * len(holes))(*[h[1] for h in holes])
+    qs = (C.c_int32 * len(holes))(*[h[2] for h in holes])
+    g, p = VP(), VP()
+    check(lib().sbx_geom_add_holes(d.ptr, len(holes), arr, npn, qs, C.byref(g), C.byref(p)))
+    return Discretization(g), RefinementPlan(p)
+
+
+def boundary_data(d: Discretization, sources, mu: float = 1.0) -> np.ndarray:
+    """nystrom.cpp:383-392; sources rows (x, y, fx, fy)."""
+    s = np.ascontiguousarray(np.asarray(sources, dtype=np.float64).reshape(-1, 4))
+    out = np.zeros(d.n_unknowns())
+    check(lib().sbx_boundary_data(d.ptr, len(s), s.ctypes.data_as(F64P), mu, out.ctypes.data_as(F64P)))
+    return out
+
+
+def submatrix(d: Discretization, rows, cols, formulation=INTERIOR_DIRICHLET, mu=1.0) -> np.ndarray:
+    """BieAssembler::submatrix (nystrom.cpp:200-217), evaluated on the device."""
+    r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    c = np.ascontiguousarray(np.asarray(cols, dtype=np.int64))
+    out = np.zeros((len(r), len(c)), order="F")
+    check(lib().sbx_submatrix(d.ptr, formulation, mu, r.ctypes.data_as(I64P), len(r),
+                              c.ctypes.data_as(I64P), len(c), out.ctypes.data_as(F64P)))
+    return out
+
+
+@dataclass
+class HbsOptions:
+    """hbs.hpp:39-46."""
+    eps: float = 1e-10
+    leaf_nodes: int = 64
+    n_proxy: int = 64
+    bas_factor: float = 1.5
+    div_factor: float = 3.0
+
+    def to_c(self):
+        o = _sbx.sbx_hbs_options()
+        o.eps, o.leaf_nodes, o.n_proxy = self.eps, self.leaf_nodes, self.n_proxy
+        o.bas_factor, o.div_factor = self.bas_factor, self.div_factor
+        return o
+
+
+class HbsOperator(_Handle):
+    """hbs.hpp:64-74; factors live in a device arena."""
+    _destroy = "sbx_hbs_destroy"
+
+    def info(self) -> dict:
+        out = np.zeros(10, dtype=np.int64)
+        check(lib().sbx_hbs_info(self.ptr, out.ctypes.data_as(I64P)))
+        keys = ("n", "nodes", "total_skeleton", "max_block_drawn", "has_inverse",
+                "factor_doubles", "max_depth", "max_k", "apply_factor_doubles", "leaf_nodes")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    @property
+    def n(self):
+        return self.info()["n"]
+
+    def node_ranks(self) -> np.ndarray:
+        n = self.info()["nodes"]
+        out = np.zeros(n, dtype=np.int64)
+        check(lib().sbx_hbs_node_ranks(self.ptr, out.ctypes.data_as(I64P), n))
+        return out
+
+
+def hbs_compress(d: Discretization, formulation=INTERIOR_DIRICHLET, opts: HbsOptions | None = None,
+                 mu: float = 1.0, subset=None) -> HbsOperator:
+    o = (opts or HbsOptions()).to_c()
+    out = VP()
+    if subset is None:
+        check(lib().sbx_hbs_compress(d.ptr, formulation, mu, C.byref(o), C.byref(out)))
+    else:
+        s = np.ascontiguousarray(np.asarray(subset, dtype=np.int64))
+        check(lib().sbx_hbs_compress_subset(d.ptr, formulation, mu, s.ctypes.data_as(I64P), len(s),
+                                            C.byref(o), C.byref(out)))
+    return HbsOperator(out)
+
+
+def hbs_invert(op: HbsOperator) -> HbsOperator:
+    check(lib().sbx_hbs_invert(op.ptr))
+    return op
+
+
+def _is_torch_cuda(x):
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _sweep(fn, op_ptr, b, n, stream=None):
+    """Column-major n x nrhs sweep through the C-ABI (host numpy or CUDA torch)."""
+    if _is_torch_cuda(b):
+        import torch
+        vec = b.dim() == 1
+        bt = b.reshape(-1, 1) if vec else b
+        if bt.dtype != torch.float64 or bt.shape[0] != n:
+            raise ValueError("sweep: expected float64 with n rows")
+        bcm = bt.t().contiguous()  # column-major storage = transposed row-major
+        out = torch.empty_like(bcm)
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        check(fn(op_ptr, VP(bcm.data_ptr()), n, bt.shape[1], VP(out.data_ptr()), n,
+                 _sbx.SBX_DEVICE_PTRS, VP(s)))
+        res = out.t()
+        return res.reshape(-1) if vec else res
+    arr = np.asarray(b, dtype=np.float64)
+    vec = arr.ndim == 1
+    a2 = np.asfortranarray(arr.reshape(-1, 1) if vec else arr)
+    if a2.shape[0] != n:
+        raise ValueError("sweep: size mismatch")
+    out = np.zeros_like(a2, order="F")
+    check(fn(op_ptr, VP(a2.ctypes.data), n, a2.shape[1], VP(out.ctypes.data), n, 0, VP()))
+    return out[:, 0] if vec else out
+
+
+def hbs_solve(op: HbsOperator, b):
+    """hbs.cpp:589-625."""
+    return _sweep(lib().sbx_hbs_solve, op.ptr, b, op.n)
+
+
+def hbs_apply(op: HbsOperator, v):
+    """hbs.cpp:511-544."""
+    return _sweep(lib().sbx_hbs_apply, op.ptr, v, op.n)
+
+
+def hbs_save(op: HbsOperator, path):
+    check(lib().sbx_hbs_save_hbs1(op.ptr, str(path).encode()))
+
+
+def hbs_load(path) -> HbsOperator:
+    _ensure()
+    out = VP()
+    check(lib().sbx_hbs_load_hbs1(str(path).encode(), C.byref(out)))
+    return HbsOperator(out)
+
+
+class LowRankUpdate(_Handle):
+    """lowrank.hpp:28-47 (factors on the device)."""
+    _destroy = "sbx_update_destroy"
+
+    def info(self) -> dict:
+        out = np.zeros(9, dtype=np.int64)
+        check(lib().sbx_update_info(self.ptr, out.ctypes.data_as(I64P)))
+        keys = ("k", "k1", "kc", "kp", "pk", "n_ext", "nk2", "nc2", "np2")
+        return dict(zip(keys, (int(v) for v in out)))
+
+    @property
+    def k(self):
+        return self.info()["k"]
+
+    def factors(self):
+        i = self.info()
+        L = np.zeros((i["n_ext"], i["k"]), order="F")
+        R = np.zeros((i["k"], i["n_ext"]), order="F")
+        if i["k"]:
+            check(lib().sbx_update_factor(self.ptr, 0, L.ctypes.data_as(F64P)))
+            check(lib().sbx_update_factor(self.ptr, 1, R.ctypes.data_as(F64P)))
+        return L, R
+
+
+def compress_update(d_old: Discretization, d_new: Discretization, plan: RefinementPlan,
+                    eps: float = 1e-10, formulation=INTERIOR_DIRICHLET, mu: float = 1.0,
+                    seed: int = 0) -> LowRankUpdate:
+    """compress_update(BlockSource(old, new, plan), make_proxy_geometry(new, plan),
+    eps, TwoStepId, {seed}) — lowrank.cpp:366-373."""
+    out = VP()
+    check(lib().sbx_update_compress(d_old.ptr, d_new.ptr, plan.ptr, formulation, mu, eps,
+                                    C.c_uint64(seed), C.byref(out)))
+    return LowRankUpdate(out)
+
+
+def update_from_factors(plan: RefinementPlan, L, R) -> LowRankUpdate:
+    L = np.asfortranarray(np.asarray(L, dtype=np.float64))
+    R = np.asfortranarray(np.asarray(R, dtype=np.float64))
+    out = VP()
+    check(lib().sbx_update_from_factors(plan.ptr, L.ctypes.data_as(F64P), R.ctypes.data_as(F64P),
+                                        L.shape[0], L.shape[1], C.byref(out)))
+    return LowRankUpdate(out)
+
+
+class ElsSolver(_Handle):
+    """els.hpp:17-37.  Keeps a reference to the HBS handle it solves with."""
+    _destroy = "sbx_els_destroy"
+
+    def __init__(self, ptr, a_oo):
+        super().__init__(ptr)
+        self._a_oo = a_oo
+
+    def info(self) -> dict:
+        out = np.zeros(5, dtype=np.int64)
+        check(lib().sbx_els_info(self.ptr, out.ctypes.data_as(I64P)))
+        return dict(zip(("n_k", "n_c", "n_p", "k", "app_hbs"), (int(v) for v in out)))
+
+    def n_ext(self):
+        i = self.info()
+        return i["n_k"] + i["n_c"] + i["n_p"]
+
+    def xw(self):
+        i = self.info()
+        X = np.zeros((self.n_ext(), i["k"]), order="F")
+        W = np.zeros((i["k"], i["k"]), order="F")
+        if i["k"]:
+            check(lib().sbx_els_xw(self.ptr, X.ctypes.data_as(F64P), W.ctypes.data_as(F64P)))
+        return X, W
+
+
+def els_build(a_oo: HbsOperator, d_old: Discretization, d_new: Discretization,
+              plan: RefinementPlan, update: LowRankUpdate, formulation=INTERIOR_DIRICHLET,
+              mu: float = 1.0) -> ElsSolver:
+    out = VP()
+    check(lib().sbx_els_build(a_oo.ptr, d_old.ptr, d_new.ptr, plan.ptr, update.ptr, formulation, mu,
+                              C.byref(out)))
+    return ElsSolver(out, a_oo)
+
+
+def _els_call(fn, s: ElsSolver, g, rows_in):
+    if _is_torch_cuda(g):
+        import torch
+        vec = g.dim() == 1
+        gt = g.reshape(-1, 1) if vec else g
+        gcm = gt.t().contiguous()
+        out = torch.empty_like(gcm)
+        check(fn(s.ptr, VP(gcm.data_ptr()), rows_in, gt.shape[1], VP(out.data_ptr()), rows_in,
+                 _sbx.SBX_DEVICE_PTRS, VP(torch.cuda.current_stream().cuda_stream)))
+        res = out.t()
+        return res.reshape(-1) if vec else res
+    a = np.asarray(g, dtype=np.float64)
+    vec = a.ndim == 1
+    a2 = np.asfortranarray(a.reshape(-1, 1) if vec else a)
+    if a2.shape[0] != rows_in:
+        raise ValueError("els_solve: data size mismatch")
+    out = np.zeros_like(a2, order="F")
+    check(fn(s.ptr, VP(a2.ctypes.data), rows_in, a2.shape[1], VP(out.ctypes.data), rows_in, 0, VP()))
+    return out[:, 0] if vec else out
+
+
+def els_solve(s: ElsSolver, g_n):
+    """els.cpp:173-179 (kept, added) data -> (kept, added) density."""
+    i = s.info()
+    return _els_call(lib().sbx_els_solve, s, g_n, i["n_k"] + i["n_p"])
+
+
+def els_solve_raw(s: ElsSolver, g_ext):
+    """els.cpp:147-152 on extended (kept, cut, added) vectors."""
+    return _els_call(lib().sbx_els_solve_raw, s, g_ext, s.n_ext())
+
+
+def density_on_refined(s: ElsSolver, tau_n) -> np.ndarray:
+    """els.cpp:195-203."""
+    t = np.ascontiguousarray(np.asarray(tau_n, dtype=np.float64))
+    i = s.info()
+    if t.shape[0] != i["n_k"] + i["n_p"]:
+        raise ValueError("density_on_refined: size mismatch")
+    n_new = (i["n_k"] + i["n_p"]) // 1
+    out = np.zeros(_els_new_unknowns(s))
+    check(lib().sbx_els_density_on_refined(s.ptr, t.ctypes.data_as(F64P), out.ctypes.data_as(F64P)))
+    return out
+
+
+def _els_new_unknowns(s: ElsSolver) -> int:
+    i = s.info()
+    return i["n_k"] + i["n_p"]
+
+
+def kernel_launches(reset: bool = False) -> int:
+    return int(lib().sbx_kernel_launches(int(reset)))
+
+
+def gather_kept_added(plan: RefinementPlan, g_new):
+    """scenario.cpp:253-258."""
+    m = plan.maps()
+    kn, an = m["kept_new"], m["added_new"]
+    ks = np.stack([2 * kn, 2 * kn + 1], 1).ravel()
+    as_ = np.stack([2 * an, 2 * an + 1], 1).ravel()
+    return np.concatenate([np.asarray(g_new)[ks], np.asarray(g_new)[as_]], axis=0)

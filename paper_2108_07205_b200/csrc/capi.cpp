@@ -1,0 +1,373 @@
+// The sbx C-ABI (include/sbx.h): opaque handles over the host/device
+// objects, exceptions mapped to status codes + sbx_last_error().
+#include <cstring>
+#include <string>
+
+#include "els.hpp"
+#include "entries.hpp"
+#include "geometry.hpp"
+#include "hbs.hpp"
+#include "hbs_build.hpp"
+#include "sbx.h"
+#include "update.hpp"
+
+struct sbx_geom_s {
+  std::unique_ptr<sbx::Geom> g;
+};
+struct sbx_plan_s {
+  std::unique_ptr<sbx::Plan> p;
+};
+struct sbx_hbs_s {
+  std::unique_ptr<sbx::HbsOp> h;
+};
+struct sbx_update_s {
+  std::unique_ptr<sbx::Update> u;
+};
+struct sbx_els_s {
+  std::unique_ptr<sbx::Els> e;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SBX_OK;
+  } catch (const sbx::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return SBX_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SBX_RUNTIME_ERROR;
+  }
+}
+
+cudaStream_t stream_of(void* s) {
+  return s ? static_cast<cudaStream_t>(s) : sbx::lib_stream();
+}
+
+sbx::Geom& G(sbx_geom g) {
+  sbx::require(g && g->g, "null geometry handle");
+  return *g->g;
+}
+sbx::HbsOp& H(sbx_hbs h) {
+  sbx::require(h && h->h, "null hbs handle");
+  return *h->h;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sbx_last_error(void) { return g_err.c_str(); }
+
+int sbx_init(int device) {
+  return guard([&] {
+    SBX_CUDA(cudaSetDevice(device));
+    (void)sbx::lib_stream();
+  });
+}
+
+int sbx_sync(void) {
+  return guard([&] { SBX_CUDA(cudaStreamSynchronize(sbx::lib_stream())); });
+}
+
+int64_t sbx_kernel_launches(int reset) { return sbx::launches(reset != 0); }
+
+// ---------------------------------------------------------------- geometry
+int sbx_geom_create(const sbx_curve* curve, int n_panels, int q, sbx_geom* out) {
+  return guard([&] {
+    sbx::require(curve && out, "null argument");
+    auto g = sbx::geom_panelize(*curve, n_panels, q);
+    g->upload(sbx::lib_stream());
+    *out = new sbx_geom_s{std::move(g)};
+  });
+}
+
+int sbx_geom_add_holes(sbx_geom wall, int n_holes, const sbx_curve* holes, const int32_t* n_panels,
+                       const int32_t* q, sbx_geom* out, sbx_plan* plan) {
+  return guard([&] {
+    std::vector<sbx_curve> hs(holes, holes + n_holes);
+    std::vector<int> np(n_panels, n_panels + n_holes), qs(q, q + n_holes);
+    auto r = sbx::geom_add_holes(G(wall), hs, np, qs);
+    r.first->upload(sbx::lib_stream());
+    *out = new sbx_geom_s{std::move(r.first)};
+    *plan = new sbx_plan_s{std::move(r.second)};
+  });
+}
+
+int sbx_geom_destroy(sbx_geom g) {
+  delete g;
+  return SBX_OK;
+}
+
+int sbx_geom_info(sbx_geom g, int64_t* n_nodes, int64_t* n_panels, int64_t* n_components) {
+  return guard([&] {
+    const auto& d = G(g);
+    *n_nodes = d.n_nodes();
+    *n_panels = int64_t(d.panels.size());
+    *n_components = int64_t(d.comps.size());
+  });
+}
+
+int sbx_geom_nodes(sbx_geom g, double* out9, int64_t* panel_of) {
+  return guard([&] {
+    const auto& d = G(g);
+    const int64_t n = d.n_nodes();
+    const std::vector<double>* src[9] = {&d.x, &d.y, &d.nx, &d.ny, &d.tx, &d.ty, &d.w, &d.kappa, &d.t};
+    for (int a = 0; a < 9; ++a) std::memcpy(out9 + a * n, src[a]->data(), size_t(8 * n));
+    if (panel_of) std::memcpy(panel_of, d.panel_of.data(), size_t(8 * n));
+  });
+}
+
+int sbx_panels_near_point(sbx_geom g, double px, double py, double radius, int64_t* out,
+                          int64_t cap, int64_t* count) {
+  return guard([&] {
+    auto v = sbx::panels_near_point(G(g), px, py, radius);
+    for (size_t i = 0; i < v.size() && int64_t(i) < cap; ++i) out[i] = v[i];
+    *count = int64_t(v.size());
+  });
+}
+
+int sbx_refine(sbx_geom g, const int64_t* panel_ids, int64_t n, int m, sbx_geom* out,
+               sbx_plan* plan) {
+  return guard([&] {
+    auto r = sbx::geom_refine(G(g), std::vector<int64_t>(panel_ids, panel_ids + n), m);
+    r.first->upload(sbx::lib_stream());
+    *out = new sbx_geom_s{std::move(r.first)};
+    *plan = new sbx_plan_s{std::move(r.second)};
+  });
+}
+
+int sbx_coarsen(sbx_geom g, sbx_plan plan, sbx_geom* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    auto c = sbx::geom_coarsen(G(g), *plan->p);
+    c->upload(sbx::lib_stream());
+    *out = new sbx_geom_s{std::move(c)};
+  });
+}
+
+int sbx_plan_destroy(sbx_plan p) {
+  delete p;
+  return SBX_OK;
+}
+
+int sbx_plan_sizes(sbx_plan p, int64_t* n_k, int64_t* n_c, int64_t* n_p) {
+  return guard([&] {
+    sbx::require(p && p->p, "null plan handle");
+    *n_k = int64_t(p->p->kept_old.size());
+    *n_c = int64_t(p->p->cut_old.size());
+    *n_p = int64_t(p->p->added_new.size());
+  });
+}
+
+int sbx_plan_maps(sbx_plan p, int64_t* kept_old, int64_t* kept_new, int64_t* cut_old,
+                  int64_t* added_new) {
+  return guard([&] {
+    sbx::require(p && p->p, "null plan handle");
+    const auto& q = *p->p;
+    std::copy(q.kept_old.begin(), q.kept_old.end(), kept_old);
+    std::copy(q.kept_new.begin(), q.kept_new.end(), kept_new);
+    std::copy(q.cut_old.begin(), q.cut_old.end(), cut_old);
+    std::copy(q.added_new.begin(), q.added_new.end(), added_new);
+  });
+}
+
+// ---------------------------------------------------------------- entries / data
+int sbx_submatrix(sbx_geom g, int formulation, double mu, const int64_t* rows, int64_t nr,
+                  const int64_t* cols, int64_t nc, double* out) {
+  return guard([&] {
+    sbx::EntryOracle eo(G(g), formulation, mu, sbx::lib_stream());
+    eo.submatrix_host(rows, nr, cols, nc, out, sbx::lib_stream());
+  });
+}
+
+int sbx_boundary_data(sbx_geom g, int64_t n_src, const double* src_xyf, double mu, double* out) {
+  return guard([&] { sbx::boundary_data_host(G(g), n_src, src_xyf, mu, out, sbx::lib_stream()); });
+}
+
+// ---------------------------------------------------------------- HBS
+int sbx_hbs_compress(sbx_geom g, int formulation, double mu, const sbx_hbs_options* opts,
+                     sbx_hbs* out) {
+  return guard([&] {
+    sbx::HbsBuildOptions o;
+    if (opts) o = sbx::HbsBuildOptions::from(*opts);
+    auto h = sbx::hbs_compress_device(G(g), formulation, mu, nullptr, 0, o, sbx::lib_stream());
+    *out = new sbx_hbs_s{std::move(h)};
+  });
+}
+
+int sbx_hbs_compress_subset(sbx_geom g, int formulation, double mu, const int64_t* nodes,
+                            int64_t n_nodes, const sbx_hbs_options* opts, sbx_hbs* out) {
+  return guard([&] {
+    sbx::HbsBuildOptions o;
+    if (opts) o = sbx::HbsBuildOptions::from(*opts);
+    auto h = sbx::hbs_compress_device(G(g), formulation, mu, nodes, n_nodes, o, sbx::lib_stream());
+    *out = new sbx_hbs_s{std::move(h)};
+  });
+}
+
+int sbx_hbs_invert(sbx_hbs h) {
+  return guard([&] { sbx::hbs_invert_device(H(h), sbx::lib_stream()); });
+}
+
+int sbx_hbs_destroy(sbx_hbs h) {
+  delete h;
+  return SBX_OK;
+}
+
+int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double* x, int64_t ldx,
+                  int flags, void* stream) {
+  return guard([&] {
+    sbx::require(!(flags & SBX_TRANSPOSE), "hbs_solve_t is not part of the device path yet");
+    sbx::hbs_solve(H(h), b, ldb, nrhs, x, ldx, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
+  });
+}
+
+int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double* y, int64_t ldy,
+                  int flags, void* stream) {
+  return guard([&] {
+    sbx::require(!(flags & SBX_TRANSPOSE), "hbs_apply_t is not part of the device path yet");
+    sbx::hbs_apply(H(h), v, ldv, nrhs, y, ldy, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
+  });
+}
+
+int sbx_hbs_save_hbs1(sbx_hbs h, const char* path) {
+  return guard([&] { sbx::hbs_save_hbs1(H(h), path, sbx::lib_stream()); });
+}
+
+int sbx_hbs_load_hbs1(const char* path, sbx_hbs* out) {
+  return guard([&] { *out = new sbx_hbs_s{sbx::hbs_load_hbs1(path, sbx::lib_stream())}; });
+}
+
+int sbx_hbs_info(sbx_hbs h, int64_t* info) {
+  return guard([&] {
+    const auto& op = H(h);
+    int64_t mk = 0;
+    for (const auto& nd : op.nodes) mk = std::max<int64_t>(mk, nd.k);
+    info[0] = op.n;
+    info[1] = int64_t(op.nodes.size());
+    info[2] = op.total_skeleton();
+    info[3] = op.max_block_drawn;
+    info[4] = op.has_inverse ? 1 : 0;
+    info[5] = op.has_inverse ? op.solve_factor_doubles() : 0;
+    info[6] = op.max_depth;
+    info[7] = mk;
+    info[8] = op.apply_factor_doubles();
+    info[9] = op.leaf_nodes;
+  });
+}
+
+int sbx_hbs_node_ranks(sbx_hbs h, int64_t* k, int64_t cap) {
+  return guard([&] {
+    const auto& op = H(h);
+    for (size_t i = 0; i < op.nodes.size() && int64_t(i) < cap; ++i) k[i] = op.nodes[i].k;
+  });
+}
+
+// ---------------------------------------------------------------- update
+int sbx_update_compress(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formulation, double mu,
+                        double eps, uint64_t seed, sbx_update* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    auto u = sbx::update_compress_device(G(old_g), G(new_g), *plan->p, formulation, mu, eps, seed,
+                                         sbx::lib_stream());
+    *out = new sbx_update_s{std::move(u)};
+  });
+}
+
+int sbx_update_destroy(sbx_update u) {
+  delete u;
+  return SBX_OK;
+}
+
+int sbx_update_info(sbx_update u, int64_t* info) {
+  return guard([&] {
+    sbx::require(u && u->u, "null update handle");
+    const auto& x = *u->u;
+    const int64_t v[9] = {x.k, x.k1, x.k_kc, x.k_kp, x.k_pk, x.n_ext(), x.nk2, x.nc2, x.np2};
+    std::copy(v, v + 9, info);
+  });
+}
+
+int sbx_update_factor(sbx_update u, int which, double* out) {
+  return guard([&] {
+    sbx::require(u && u->u, "null update handle");
+    sbx::update_download(*u->u, which, out, sbx::lib_stream());
+  });
+}
+
+int sbx_update_from_factors(sbx_plan plan, const double* L, const double* R, int64_t n_ext,
+                            int64_t k, sbx_update* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    *out = new sbx_update_s{sbx::update_from_factors(*plan->p, L, R, n_ext, k, sbx::lib_stream())};
+  });
+}
+
+// ---------------------------------------------------------------- ELS
+int sbx_els_build(sbx_hbs a_oo, sbx_geom old_g, sbx_geom new_g, sbx_plan plan, sbx_update upd,
+                  int formulation, double mu, sbx_els* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p && upd && upd->u, "null handle");
+    auto e = sbx::els_build_device(H(a_oo), G(old_g), G(new_g), *plan->p, *upd->u, formulation, mu,
+                                   sbx::lib_stream());
+    *out = new sbx_els_s{std::move(e)};
+  });
+}
+
+int sbx_els_destroy(sbx_els e) {
+  delete e;
+  return SBX_OK;
+}
+
+int sbx_els_info(sbx_els e, int64_t* info) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    const auto& s = *e->e;
+    info[0] = s.n_k;
+    info[1] = s.n_c;
+    info[2] = s.n_p;
+    info[3] = s.k;
+    info[4] = s.app_h ? 1 : 0;
+  });
+}
+
+int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, double* tau_n,
+                  int64_t ldt, int flags, void* stream) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::els_solve(*e->e, g_n, ldg, nrhs, tau_n, ldt, false, (flags & SBX_DEVICE_PTRS) != 0,
+                   stream_of(stream));
+  });
+}
+
+int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
+                      int64_t ldy, int flags, void* stream) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::els_solve(*e->e, g_ext, ldg, nrhs, y, ldy, true, (flags & SBX_DEVICE_PTRS) != 0,
+                   stream_of(stream));
+  });
+}
+
+int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::els_density_on_refined(*e->e, tau_n, out);
+  });
+}
+
+int sbx_els_xw(sbx_els e, double* X, double* W) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::els_download_xw(*e->e, X, W, sbx::lib_stream());
+  });
+}
+
+}  // extern "C"

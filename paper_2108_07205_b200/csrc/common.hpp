@@ -1,0 +1,114 @@
+// Shared host-side plumbing for the sbx library: errors, device buffers,
+// the library stream and launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sbx {
+
+using i64 = std::int64_t;
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// Error carrying an sbx.h status code.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void require(bool c, const std::string& m) {
+  if (!c) throw Error(1, m);
+}
+
+#define SBX_CUDA(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      throw ::sbx::Error(6, std::string("CUDA error: ") + cudaGetErrorString(e_) +    \
+                                " (" #x ") at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+#define SBX_LAUNCHED()                       \
+  do {                                       \
+    SBX_CUDA(cudaGetLastError());            \
+    ::sbx::count_launch();                   \
+  } while (0)
+
+void count_launch();
+std::int64_t launches(bool reset);
+cudaStream_t lib_stream();
+
+// Owning device buffer.
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { resize(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  void resize(size_t n) {
+    if (n == n_) return;
+    release();
+    if (n) SBX_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    n_ = n;
+  }
+  // Grows (never shrinks) without preserving contents.
+  void reserve(size_t n) {
+    if (n > n_) resize(n);
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  void upload(const T* h, size_t n, cudaStream_t s) {
+    reserve(n);
+    if (n) SBX_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  void download(T* h, size_t n, cudaStream_t s) const {
+    if (n) SBX_CUDA(cudaMemcpyAsync(h, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n_) SBX_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// Column-major host matrix (the reference's Eigen storage order; used for
+// HBS1 I/O and small host-side bookkeeping only).
+struct HMat {
+  i64 r = 0, c = 0;
+  std::vector<double> a;
+  HMat() = default;
+  HMat(i64 rows, i64 cols) : r(rows), c(cols), a(size_t(rows * cols), 0.0) {}
+  i64 size() const { return r * c; }
+};
+
+}  // namespace sbx

@@ -1,0 +1,1171 @@
+// Batched small dense linear algebra on sm_100a (see dense.hpp).
+// One CTA per problem; matrices are staged in shared memory when they fit
+// and otherwise factored in place in global memory (L2 resident for the
+// sizes of this workload).  GEMM tiles use FP64 tensor cores
+// (mma.sync.m8n8k4.f64 -> SASS DMMA).
+#include <cfloat>
+
+#include <algorithm>
+
+#include "dense.hpp"
+
+namespace sbx {
+
+namespace {
+
+constexpr int kT = 512;
+constexpr int kWarps = kT / 32;
+constexpr size_t kSmemCap = 200 * 1024;
+
+template <class T>
+struct JobTable {
+  DevBuf<T> d;
+  const T* upload(const std::vector<T>& h, cudaStream_t s) {
+    d.reserve(h.size());
+    SBX_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d.get();
+  }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; all threads get the result. red: >= kWarps doubles.
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = l < kWarps ? red[l] : 0.0;
+  t = warp_sum(t);
+  return t;
+}
+
+// Block-wide first-max (largest value, smallest index on ties).
+__device__ void block_argmax(double v, int idx, double* rv, int* ri, double& out_v, int& out_i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    rv[w] = v;
+    ri[w] = idx;
+  }
+  __syncthreads();
+  v = l < kWarps ? rv[l] : -1.0;
+  idx = l < kWarps ? ri[l] : 0x7fffffff;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  out_v = v;
+  out_i = idx;
+}
+
+// ---------------------------------------------------------------- QR / CPQR
+__global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, int smem_doubles) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* upd = sm;
+  double* dir = upd + n;
+  double* red = dir + n;                       // 32
+  int* ired = reinterpret_cast<int*>(red + 32);  // 32
+  double* sc = red + 48;                       // shared scalars (8)
+  double* mat = sc + 8;
+  const size_t head = size_t(2 * n + 56);
+  const bool in_smem = head + size_t(M) * n <= size_t(smem_doubles);
+  double* A = jb.a;
+  int lda = jb.lda;
+  if (in_smem) {
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < M; i += 32) mat[i + size_t(c) * M] = jb.a[i + size_t(c) * jb.lda];
+    A = mat;
+    lda = M;
+  }
+  const int size = min(M, n);
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  if (jb.pivot) {
+    for (int c = tid; c < n; c += kT) jb.perm[c] = c;
+  }
+  for (int c = tid; c < size; c += kT) jb.diag[c] = 0.0;
+  __syncthreads();
+  if (jb.pivot) {
+    for (int c = warp; c < n; c += kWarps) {
+      double s = 0.0;
+      for (int i = lane; i < M; i += 32) {
+        const double v = A[i + size_t(c) * lda];
+        s += v * v;
+      }
+      s = warp_sum(s);
+      if (lane == 0) upd[c] = dir[c] = sqrt(s);
+    }
+  }
+  __syncthreads();
+  const double thr = sqrt(DBL_EPSILON);
+  int done = 0;
+  for (int j = 0; j < steps_max; ++j) {
+    if (jb.pivot) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int c = j + tid; c < n; c += kT) {
+        const double v = upd[c];
+        if (v > bv) {
+          bv = v;
+          bi = c;
+        }
+      }
+      double mv;
+      int p;
+      block_argmax(bv, bi, red, ired, mv, p);
+      if (p != j) {
+        for (int i = tid; i < M; i += kT) {
+          const double t = A[i + size_t(j) * lda];
+          A[i + size_t(j) * lda] = A[i + size_t(p) * lda];
+          A[i + size_t(p) * lda] = t;
+        }
+        if (tid == 0) {
+          double t = upd[j];
+          upd[j] = upd[p];
+          upd[p] = t;
+          t = dir[j];
+          dir[j] = dir[p];
+          dir[p] = t;
+          const int q = jb.perm[j];
+          jb.perm[j] = jb.perm[p];
+          jb.perm[p] = q;
+        }
+      }
+      __syncthreads();
+    }
+    // Householder vector of column j (Eigen makeHouseholderInPlace)
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < M; i += kT) {
+      const double v = A[i + size_t(j) * lda];
+      part += v * v;
+    }
+    const double tail = block_sum(part, red);
+    if (tid == 0) {
+      const double c0 = A[j + size_t(j) * lda];
+      double tau, beta, denom;
+      if (tail <= DBL_MIN) {
+        tau = 0.0;
+        beta = c0;
+        denom = 0.0;
+      } else {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        denom = c0 - beta;
+        tau = (beta - c0) / beta;
+      }
+      sc[0] = tau;
+      sc[1] = beta;
+      sc[2] = denom;
+      if (j == 0) sc[3] = fabs(beta);
+    }
+    __syncthreads();
+    const double tau = sc[0], beta = sc[1], denom = sc[2], r00 = sc[3];
+    for (int i = j + 1 + tid; i < M; i += kT) {
+      double& v = A[i + size_t(j) * lda];
+      v = denom == 0.0 ? 0.0 : v / denom;
+    }
+    if (tid == 0) {
+      A[j + size_t(j) * lda] = beta;
+      jb.diag[j] = fabs(beta);
+    }
+    __syncthreads();
+    done = j + 1;
+    if (jb.pivot && jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    // apply to the trailing columns, then downdate their norms
+    for (int c = j + 1 + warp; c < n; c += kWarps) {
+      double* col = A + size_t(c) * lda;
+      const double* v = A + size_t(j) * lda;
+      if (M - j > 1 && tau != 0.0) {
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < M; i += 32) d += v[i] * col[i];
+        d = warp_sum(d) + col[j];
+        const double tw = tau * d;
+        for (int i = j + 1 + lane; i < M; i += 32) col[i] -= v[i] * tw;
+        __syncwarp();
+        if (lane == 0) col[j] -= tw;
+        __syncwarp();
+      }
+      if (jb.pivot) {
+        const double u = upd[c];
+        __syncwarp();  // every lane has read upd[c] before lane 0 rewrites it
+        if (u != 0.0) {
+          double t = fabs(col[j]) / u;
+          t = (1.0 + t) * (1.0 - t);
+          t = t < 0.0 ? 0.0 : t;
+          const double rr = u / dir[c];
+          const double t2 = t * rr * rr;
+          if (t2 <= thr) {
+            double s = 0.0;
+            for (int i = j + 1 + lane; i < M; i += 32) s += col[i] * col[i];
+            s = warp_sum(s);
+            __syncwarp();
+            if (lane == 0) upd[c] = dir[c] = sqrt(s);
+          } else if (lane == 0) {
+            upd[c] = u * sqrt(t);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && jb.steps) *jb.steps = done;
+  if (in_smem) {
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < M; i += 32) jb.a[i + size_t(c) * jb.lda] = mat[i + size_t(c) * M];
+  }
+}
+
+// ---------------------------------------------------------------- cooperative CPQR
+struct CoopCtl {
+  unsigned count, gen;
+};
+struct CoopPart {
+  double val;
+  int pos, phys;
+};
+
+constexpr int kCT = 256;
+constexpr int kCWarps = kCT / 32;
+
+__device__ void group_barrier(CoopCtl* ctl, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vg = &ctl->gen;
+    const unsigned g = *vg;
+    __threadfence();
+    if (atomicAdd(&ctl->count, 1u) == nblocks - 1) {
+      atomicExch(&ctl->count, 0u);
+      __threadfence();
+      atomicAdd(&ctl->gen, 1u);
+    } else {
+      while (*vg == g) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
+  return v > bv || (v == bv && p < bp);
+}
+
+struct CoopArgs {
+  const QrJob* jobs;
+  const int* cta_job;
+  const int* cta_rank;
+  const int* job_ctas;
+  CoopCtl* ctl;
+  CoopPart* parts;
+  const int* part_off;
+  double* beta;        // signed R diagonal per job (offset beta_off)
+  const i64* beta_off;
+};
+
+__global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
+  extern __shared__ double sm[];
+  const int job = args.cta_job[blockIdx.x];
+  const int rank = args.cta_rank[blockIdx.x];
+  const int G = args.job_ctas[job];
+  const QrJob jb = args.jobs[job];
+  const int M = jb.M, n = jb.n, lda = jb.lda;
+  double* A = jb.a;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = int(i64(n) * rank / G), c1 = int(i64(n) * (rank + 1) / G);
+  const int nown = c1 - c0;
+  double* v = sm;                // M
+  double* upd = v + M;           // nown
+  double* dir = upd + nown;      // nown
+  double* red = dir + nown;      // 32
+  double* sc = red + 32;         // 8
+  int* ired = reinterpret_cast<int*>(sc + 8);  // 32
+  int* mypos = ired + 32;        // nown (logical position, -1 once pivoted)
+  CoopCtl* ctl = args.ctl + job;
+  CoopPart* parts = args.parts + args.part_off[job];
+  double* sbeta = args.beta + args.beta_off[job];
+  for (int c = tid; c < nown; c += kCT) mypos[c] = c0 + c;
+  for (int c = warp; c < nown; c += kCWarps) {
+    const double* col = A + size_t(c0 + c) * lda;
+    double s = 0.0;
+    for (int i = lane; i < M; i += 32) s += col[i] * col[i];
+    s = warp_sum(s);
+    if (lane == 0) upd[c] = dir[c] = sqrt(s);
+  }
+  __syncthreads();
+  const int size = min(M, n);
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  const double thr = sqrt(DBL_EPSILON);
+  int done = 0, prev_p = -1;
+  double prev_beta = 0.0, r00 = 0.0;
+  for (int j = 0; j < steps_max; ++j) {
+    // local first-max over alive columns, ties by logical position
+    double bv = -1.0;
+    int bp = 0x7fffffff, bphys = -1;
+    for (int c = tid; c < nown; c += kCT) {
+      const int p = mypos[c];
+      if (p >= 0 && better(upd[c], p, bv, bp)) {
+        bv = upd[c];
+        bp = p;
+        bphys = c0 + c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bphys, o);
+      if (better(ov, op, bv, bp)) {
+        bv = ov;
+        bp = op;
+        bphys = oq;
+      }
+    }
+    if (lane == 0) {
+      red[warp] = bv;
+      ired[warp] = bp;
+    }
+    __shared__ int wphys[kCWarps];
+    if (lane == 0) wphys[warp] = bphys;
+    __syncthreads();
+    if (tid == 0) {
+      double v0 = -1.0;
+      int p0 = 0x7fffffff, q0 = -1;
+      for (int w = 0; w < kCWarps; ++w)
+        if (better(red[w], ired[w], v0, p0)) {
+          v0 = red[w];
+          p0 = ired[w];
+          q0 = wphys[w];
+        }
+      parts[rank] = {v0, p0, q0};
+    }
+    group_barrier(ctl, unsigned(G));
+    // previous pivot's diagonal, deferred so no CTA reads a half-written column
+    if (prev_p >= 0 && prev_p >= c0 && prev_p < c1 && tid == 0)
+      A[(j - 1) + size_t(prev_p) * lda] = prev_beta;
+    // global pivot
+    __shared__ int s_p, s_lp;
+    if (tid == 0) {
+      double v0 = -1.0;
+      int p0 = 0x7fffffff, q0 = -1;
+      for (int g = 0; g < G; ++g) {  // L1-bypassing loads: written by other CTAs
+        const double pv = __ldcg(&parts[g].val);
+        const int pp = __ldcg(&parts[g].pos), pq = __ldcg(&parts[g].phys);
+        if (pq >= 0 && better(pv, pp, v0, p0)) {
+          v0 = pv;
+          p0 = pp;
+          q0 = pq;
+        }
+      }
+      s_p = q0;
+      s_lp = p0;
+    }
+    __syncthreads();
+    const int p = s_p, lp = s_lp;
+    // logical swap: the column at position j moves to lp, p becomes position j
+    for (int c = tid; c < nown; c += kCT) {
+      if (c0 + c == p) mypos[c] = -1;
+      else if (mypos[c] == j) mypos[c] = lp;
+    }
+    if (p >= c0 && p < c1 && tid == 0) jb.perm[j] = p;
+    // Householder vector of the pivot column (redundant in every CTA)
+    const double* pc = A + size_t(p) * lda;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < M; i += kCT) {
+      const double x = __ldcg(pc + i);
+      v[i] = x;
+      part += x * x;
+    }
+    const double tail = [&] {
+      double t = warp_sum(part);
+      __syncthreads();
+      if (lane == 0) red[warp] = t;
+      __syncthreads();
+      double u = lane < kCWarps ? red[lane] : 0.0;
+      return warp_sum(u);
+    }();
+    const double cc = __ldcg(pc + j);
+    double tau, beta, denom;
+    if (tail <= DBL_MIN) {
+      tau = 0.0;
+      beta = cc;
+      denom = 0.0;
+    } else {
+      beta = sqrt(cc * cc + tail);
+      if (cc >= 0.0) beta = -beta;
+      denom = cc - beta;
+      tau = (beta - cc) / beta;
+    }
+    __syncthreads();
+    for (int i = j + 1 + tid; i < M; i += kCT) v[i] = denom == 0.0 ? 0.0 : v[i] / denom;
+    if (j == 0) r00 = fabs(beta);
+    if (rank == 0 && tid == 0) sbeta[j] = beta;
+    __syncthreads();
+    prev_p = p;
+    prev_beta = beta;
+    done = j + 1;
+    if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    for (int c = warp; c < nown; c += kCWarps) {
+      if (mypos[c] < 0) continue;
+      double* col = A + size_t(c0 + c) * lda;
+      if (M - j > 1 && tau != 0.0) {
+        double d = 0.0;
+        for (int i = j + 1 + lane; i < M; i += 32) d += v[i] * col[i];
+        d = warp_sum(d) + col[j];
+        const double tw = tau * d;
+        for (int i = j + 1 + lane; i < M; i += 32) col[i] -= v[i] * tw;
+        __syncwarp();
+        if (lane == 0) col[j] -= tw;
+        __syncwarp();
+      }
+      const double u = upd[c];
+      __syncwarp();
+      if (u != 0.0) {
+        double t = fabs(col[j]) / u;
+        t = (1.0 + t) * (1.0 - t);
+        t = t < 0.0 ? 0.0 : t;
+        const double rr = u / dir[c];
+        if (t * rr * rr <= thr) {
+          double s = 0.0;
+          for (int i = j + 1 + lane; i < M; i += 32) s += col[i] * col[i];
+          s = warp_sum(s);
+          __syncwarp();
+          if (lane == 0) upd[c] = dir[c] = sqrt(s);
+        } else if (lane == 0) {
+          upd[c] = u * sqrt(t);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // finalisation: last diagonal, logical order of the untouched columns
+  group_barrier(ctl, unsigned(G));
+  if (prev_p >= c0 && prev_p < c1 && tid == 0) A[(done - 1) + size_t(prev_p) * lda] = prev_beta;
+  for (int c = tid; c < nown; c += kCT)
+    if (mypos[c] >= 0) jb.perm[mypos[c]] = c0 + c;
+  for (int l = rank * kCT + tid; l < size; l += G * kCT)
+    jb.diag[l] = l < done ? fabs(__ldcg(sbeta + l)) : 0.0;
+  if (rank == 0 && tid == 0 && jb.steps) *jb.steps = done;
+}
+
+// ---------------------------------------------------------------- interpolation
+__global__ void __launch_bounds__(256) interp_kernel(const InterpJob* __restrict__ jobs) {
+  const InterpJob jb = jobs[blockIdx.x];
+  const int n = jb.n, k = jb.k, nk = n - k;
+  // zero P, then identity rows and T rows
+  for (i64 idx = threadIdx.x; idx < i64(n) * k; idx += blockDim.x) {
+    const i64 r = idx % n, c = idx / n;
+    jb.P[r + c * jb.ldp] = 0.0;
+  }
+  const int* cm = jb.colmap;
+  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
+    const double* R = jb.a;
+    const size_t cj = size_t(cm ? cm[k + j] : k + j);
+    for (int i = k - 1; i >= 0; --i) {
+      double s = R[i + cj * jb.lda];
+      for (int l = i + 1; l < k; ++l)
+        s -= R[i + size_t(cm ? cm[l] : l) * jb.lda] * jb.T[size_t(l) * nk + j];
+      jb.T[size_t(i) * nk + j] = s / R[i + size_t(cm ? cm[i] : i) * jb.lda];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) jb.P[jb.perm[i] + size_t(i) * jb.ldp] = 1.0;
+  for (i64 idx = threadIdx.x; idx < i64(nk) * k; idx += blockDim.x) {
+    const int j = int(idx % nk), i = int(idx / nk);
+    jb.P[jb.perm[k + j] + size_t(i) * jb.ldp] = jb.T[size_t(i) * nk + j];
+  }
+}
+
+// ---------------------------------------------------------------- GEMM (DMMA)
+constexpr int gTM = 64, gTN = 64, gKC = 16, gPad = 8;
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ jobs,
+                                                   const int4* __restrict__ tiles) {
+  __shared__ double As[2][gKC][gTM + gPad];
+  __shared__ double Bs[2][gKC][gTN + gPad];
+  const int4 tl = tiles[blockIdx.x];
+  const GemmJob jb = jobs[tl.x];
+  const int row0 = tl.y, col0 = tl.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
+  double c[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) c[a][b][0] = c[a][b][1] = 0.0;
+  const int kbeg = jb.splitk > 1 ? tl.w * jb.kchunk : 0;
+  const int K = jb.splitk > 1 ? min(jb.k, kbeg + jb.kchunk) : jb.k;
+  const int nch = (K - kbeg + gKC - 1) / gKC;
+  auto load = [&](int buf, int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      // A tile: rows row0..+64, k k0..+16
+      int kk, rr;
+      if (!jb.ta) {
+        kk = idx >> 6;
+        rr = idx & 63;
+      } else {
+        rr = idx >> 4;
+        kk = idx & 15;
+      }
+      const int gr = row0 + rr, gk = k0 + kk;
+      double av = 0.0;
+      if (gr < jb.m && gk < K)
+        av = jb.ta ? jb.A[gk + size_t(gr) * jb.lda] : jb.A[gr + size_t(gk) * jb.lda];
+      As[buf][kk][rr] = av;
+      int kb, cc;
+      if (!jb.tb) {
+        cc = idx >> 4;
+        kb = idx & 15;
+      } else {
+        kb = idx >> 6;
+        cc = idx & 63;
+      }
+      const int gc = col0 + cc, gkb = k0 + kb;
+      double bv = 0.0;
+      if (gc < jb.n && gkb < K)
+        bv = jb.tb ? jb.B[gc + size_t(gkb) * jb.ldb] : jb.B[gkb + size_t(gc) * jb.ldb];
+      Bs[buf][kb][cc] = bv;
+    }
+  };
+  if (nch > 0) load(0, kbeg);
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) load(buf ^ 1, kbeg + (ch + 1) * gKC);
+#pragma unroll
+    for (int k4 = 0; k4 < gKC; k4 += 4) {
+      double af[2], bf[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) af[a] = As[buf][k4 + tig][wm + a * 8 + gid];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = Bs[buf][k4 + tig][wn + b * 8 + gid];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(c[a][b][0], c[a][b][1], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int row = row0 + wm + a * 8 + gid;
+    if (row >= jb.m) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = col0 + wn + b * 8 + 2 * tig + h;
+        if (col >= jb.n) continue;
+        if (jb.splitk > 1) {
+          jb.part[size_t(tl.w) * jb.m * jb.n + row + size_t(col) * jb.m] = c[a][b][h];
+        } else {
+          double* dst = jb.C + row + size_t(col) * jb.ldc;
+          const double v = jb.alpha * c[a][b][h];
+          *dst = jb.beta == 0.0 ? v : v + jb.beta * *dst;
+        }
+      }
+  }
+}
+
+// fixed-order reduction of split-K partials: C = alpha * sum_s part_s + beta * C
+__global__ void splitk_reduce_kernel(const GemmJob* __restrict__ jobs) {
+  const GemmJob jb = jobs[blockIdx.y];
+  if (jb.splitk <= 1) return;
+  const i64 total = i64(jb.m) * jb.n;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < jb.splitk; ++s) acc += jb.part[size_t(s) * total + idx];
+    const i64 row = idx % jb.m, col = idx / jb.m;
+    double* dst = jb.C + row + col * jb.ldc;
+    const double v = jb.alpha * acc;
+    *dst = jb.beta == 0.0 ? v : v + jb.beta * *dst;
+  }
+}
+
+// ---------------------------------------------------------------- LU
+// Warp-level forward/back substitution on one column held in registers
+// (lanes own rows lane, lane+32, ...).  Up to 16 values per lane (n <= 512).
+constexpr int kMaxRowsPerLane = 16;
+
+// Register-resident slot access (a dynamic index would spill the array).
+__device__ __forceinline__ double rget(const double (&x)[kMaxRowsPerLane], int s) {
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < kMaxRowsPerLane; ++q)
+    if (q == s) v = x[q];
+  return v;
+}
+__device__ __forceinline__ void rset(double (&x)[kMaxRowsPerLane], int s, double val) {
+#pragma unroll
+  for (int q = 0; q < kMaxRowsPerLane; ++q)
+    if (q == s) x[q] = val;
+}
+
+__device__ void warp_lu_solve(const double* lu, int n, int lda, double (&x)[kMaxRowsPerLane],
+                              int lane) {
+  // L z = x (unit lower)
+  for (int j = 0; j < n; ++j) {
+    const double zj = __shfl_sync(0xffffffffu, rget(x, j >> 5), j & 31);
+#pragma unroll
+    for (int q = 0; q < kMaxRowsPerLane; ++q) {
+      const int i = lane + 32 * q;
+      if (i > j && i < n) x[q] -= lu[i + size_t(j) * lda] * zj;
+    }
+  }
+  // U x = z
+  for (int j = n - 1; j >= 0; --j) {
+    const int owner = j & 31, slot = j >> 5;
+    double xj = __shfl_sync(0xffffffffu, rget(x, slot), owner);
+    xj /= lu[j + size_t(j) * lda];
+    if (lane == owner) rset(x, slot, xj);
+#pragma unroll
+    for (int q = 0; q < kMaxRowsPerLane; ++q) {
+      const int i = lane + 32 * q;
+      if (i < j) x[q] -= lu[i + size_t(j) * lda] * xj;
+    }
+  }
+}
+
+// (A^T) x = b with PA = LU:  U^T y = b, L^T z = y, x = P^T z
+__device__ void warp_lu_solve_t(const double* lu, int n, int lda, double (&x)[kMaxRowsPerLane],
+                                int lane) {
+  for (int j = 0; j < n; ++j) {  // U^T y = b : y_j = (b_j - sum_{p<j} U(p,j) y_p)/U(j,j)
+    const int owner = j & 31, slot = j >> 5;
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxRowsPerLane; ++q) {
+      const int p = lane + 32 * q;
+      if (p < j) part += lu[p + size_t(j) * lda] * x[q];
+    }
+    part = warp_sum(part);
+    if (lane == owner) rset(x, slot, (rget(x, slot) - part) / lu[j + size_t(j) * lda]);
+    __syncwarp();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // L^T z = y : z_j = y_j - sum_{p>j} L(p,j) z_p
+    const int owner = j & 31, slot = j >> 5;
+    double part = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxRowsPerLane; ++q) {
+      const int p = lane + 32 * q;
+      if (p > j && p < n) part += lu[p + size_t(j) * lda] * x[q];
+    }
+    part = warp_sum(part);
+    if (lane == owner) rset(x, slot, rget(x, slot) - part);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kT) lu_kernel(const LuJob* __restrict__ jobs, int smem_doubles) {
+  extern __shared__ double sm[];
+  const LuJob jb = jobs[blockIdx.x];
+  const int n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* red = sm;
+  int* ired = reinterpret_cast<int*>(sm + 32);
+  double* mat = sm + 64;
+  const bool in_smem = 64 + size_t(n) * n <= size_t(smem_doubles);
+  double* A = jb.a;
+  int lda = jb.lda;
+  // 1-norm of the original matrix (Eigen m_l1_norm)
+  __shared__ double l1;
+  if (tid == 0) l1 = 0.0;
+  __syncthreads();
+  for (int c = warp; c < n; c += kWarps) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += fabs(jb.a[i + size_t(c) * jb.lda]);
+    s = warp_sum(s);
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&l1), __double_as_longlong(s));
+  }
+  if (in_smem) {
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < n; i += 32) mat[i + size_t(c) * n] = jb.a[i + size_t(c) * jb.lda];
+    A = mat;
+    lda = n;
+  }
+  for (int i = tid; i < n; i += kT) jb.piv[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = k + tid; i < n; i += kT) {
+      const double v = fabs(A[i + size_t(k) * lda]);
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+    double mv;
+    int p;
+    block_argmax(bv, bi, red, ired, mv, p);
+    if (mv != 0.0) {
+      if (p != k) {
+        for (int j = tid; j < n; j += kT) {
+          const double t = A[k + size_t(j) * lda];
+          A[k + size_t(j) * lda] = A[p + size_t(j) * lda];
+          A[p + size_t(j) * lda] = t;
+        }
+        if (tid == 0) {
+          const int t = jb.piv[k];
+          jb.piv[k] = jb.piv[p];
+          jb.piv[p] = t;
+        }
+      }
+      __syncthreads();
+      const double d = A[k + size_t(k) * lda];
+      for (int i = k + 1 + tid; i < n; i += kT) A[i + size_t(k) * lda] /= d;
+    }
+    __syncthreads();
+    const int rr = n - k - 1;
+    for (int idx = tid; idx < rr * rr; idx += kT) {
+      const int i = k + 1 + idx % rr, j = k + 1 + idx / rr;
+      A[i + size_t(j) * lda] -= A[i + size_t(k) * lda] * A[k + size_t(j) * lda];
+    }
+    __syncthreads();
+  }
+  // explicit inverse: warp per identity column
+  if (jb.inv && n <= 32 * kMaxRowsPerLane) {
+    for (int c = warp; c < n; c += kWarps) {
+      double x[kMaxRowsPerLane];
+#pragma unroll
+      for (int q = 0; q < kMaxRowsPerLane; ++q) {
+        const int i = lane + 32 * q;
+        x[q] = (i < n && jb.piv[i] == c) ? 1.0 : 0.0;
+      }
+      warp_lu_solve(A, n, lda, x, lane);
+#pragma unroll
+      for (int q = 0; q < kMaxRowsPerLane; ++q) {
+        const int i = lane + 32 * q;
+        if (i < n) jb.inv[i + size_t(c) * n] = x[q];
+      }
+    }
+  }
+  // reciprocal condition estimate (Eigen ConditionEstimator.h), warp 0
+  if (jb.rcond && warp == 0 && n <= 32 * kMaxRowsPerLane) {
+    double result;
+    if (l1 == 0.0) {
+      result = 0.0;
+    } else if (n == 1) {
+      result = 1.0;
+    } else {
+      double v[kMaxRowsPerLane], sv[kMaxRowsPerLane], old_sv[kMaxRowsPerLane];
+      auto perm_in = [&](double (&x)[kMaxRowsPerLane], const double* src) {
+        // x = P b : row i of PA = row piv[i] of A
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q) {
+          const int i = lane + 32 * q;
+          x[q] = i < n ? src[jb.piv[i]] : 0.0;
+        }
+      };
+      auto l1n = [&](const double (&x)[kMaxRowsPerLane]) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q)
+          if (lane + 32 * q < n) s += fabs(x[q]);
+        return warp_sum(s);
+      };
+      double* w = jb.work;  // 4n scratch in global
+      for (int i = lane; i < n; i += 32) w[i] = 1.0 / double(n);
+      __syncwarp();
+      perm_in(v, w);
+      warp_lu_solve(A, n, lda, v, lane);
+      double lower = l1n(v), old_lower = lower;
+      int old_vmax = -1;
+      for (int it = 0; it < 4; ++it) {
+        bool same = it > 0;
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q) {
+          sv[q] = v[q] < 0.0 ? -1.0 : 1.0;
+          if (lane + 32 * q < n && it > 0 && sv[q] != old_sv[q]) same = false;
+        }
+        same = __all_sync(0xffffffffu, same);
+        if (same) break;
+        // v = (A^T)^{-1} sign : solve_t then unpermute  x = P^T z
+        double z[kMaxRowsPerLane];
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q) z[q] = sv[q];
+        warp_lu_solve_t(A, n, lda, z, lane);
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q) {
+          const int i = lane + 32 * q;
+          if (i < n) w[jb.piv[i]] = z[q];
+        }
+        __syncwarp();
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = lane; i < n; i += 32) {
+          const double a = fabs(w[i]);
+          if (a > bv) {
+            bv = a;
+            bi = i;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        __syncwarp();
+        if (bi == old_vmax) break;
+        for (int i = lane; i < n; i += 32) w[n + i] = i == bi ? 1.0 : 0.0;
+        __syncwarp();
+        perm_in(v, w + n);
+        warp_lu_solve(A, n, lda, v, lane);
+        lower = l1n(v);
+        if (lower <= old_lower) break;
+#pragma unroll
+        for (int q = 0; q < kMaxRowsPerLane; ++q) old_sv[q] = sv[q];
+        old_vmax = bi;
+        old_lower = lower;
+      }
+      for (int i = lane; i < n; i += 32)
+        w[2 * n + i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
+      __syncwarp();
+      perm_in(v, w + 2 * n);
+      warp_lu_solve(A, n, lda, v, lane);
+      const double alt = 2.0 * l1n(v) / (3.0 * double(n));
+      const double inv_norm = fmax(lower, alt);
+      result = inv_norm == 0.0 ? 0.0 : (1.0 / inv_norm) / l1;
+    }
+    if (lane == 0) *jb.rcond = result;
+  }
+  __syncthreads();
+  if (in_smem) {
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < n; i += 32) jb.a[i + size_t(c) * jb.lda] = mat[i + size_t(c) * n];
+  }
+}
+
+__global__ void lu_solve_kernel(const double* __restrict__ lu, int n, int lda,
+                                const int* __restrict__ piv, double* B, int ldb, int nrhs,
+                                double* scratch) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nrhs) return;
+  double* b = B + size_t(warp) * ldb;
+  double x[kMaxRowsPerLane];
+#pragma unroll
+  for (int q = 0; q < kMaxRowsPerLane; ++q) {
+    const int i = lane + 32 * q;
+    x[q] = i < n ? b[piv[i]] : 0.0;
+  }
+  __syncwarp();
+  warp_lu_solve(lu, n, lda, x, lane);
+#pragma unroll
+  for (int q = 0; q < kMaxRowsPerLane; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) b[i] = x[q];
+  }
+}
+
+__global__ void copy2d_kernel(const double* __restrict__ src, i64 lds, double* __restrict__ dst,
+                              i64 ldd, i64 rows, i64 cols) {
+  const i64 total = rows * cols;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const i64 r = idx % rows, c = idx / rows;
+    dst[r + c * ldd] = src[r + c * lds];
+  }
+}
+
+__global__ void copy_jobs_kernel(const CopyJob* __restrict__ jobs) {
+  const CopyJob jb = jobs[blockIdx.y];
+  const i64 total = i64(jb.rows) * jb.cols;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const int r = int(idx % jb.rows), c = int(idx / jb.rows);
+    jb.dst[r + size_t(c) * jb.ldd] = jb.trans ? jb.src[c + size_t(r) * jb.lds] : jb.src[r + size_t(c) * jb.lds];
+  }
+}
+
+__global__ void scatter_jobs_kernel(const ScatterJob* __restrict__ jobs) {
+  const ScatterJob jb = jobs[blockIdx.y];
+  const i64 total = i64(jb.rows) * jb.cols;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const int r = int(idx % jb.rows), c = int(idx / jb.rows);
+    const i64 mr = jb.map ? jb.map[r] : r;
+    if (jb.gather)
+      jb.dst[r + size_t(jb.col_off + c) * jb.ldd] = jb.alpha * jb.src[mr + size_t(c) * jb.lds];
+    else
+      jb.dst[mr + size_t(jb.col_off + c) * jb.ldd] = jb.alpha * jb.src[r + size_t(c) * jb.lds];
+  }
+}
+
+__global__ void add_identity_kernel(double* a, i64 lda, i64 n) {
+  for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    a[i + i * lda] += 1.0;
+}
+
+}  // namespace
+
+void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<QrJob> tab;
+  size_t need = 0;
+  for (const auto& j : jobs) {
+    const size_t sz = (size_t(2 * j.n + 56) + size_t(j.M) * j.n) * sizeof(double);
+    if (sz <= kSmemCap) need = std::max(need, sz);
+  }
+  size_t base = 0;
+  for (const auto& j : jobs) base = std::max(base, size_t(2 * j.n + 56) * sizeof(double));
+  need = std::max(need, base);
+  require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
+  static bool attr = false;
+  if (!attr) {
+    SBX_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+    attr = true;
+  }
+  const QrJob* d = tab.upload(jobs, s);
+  qr_kernel<<<unsigned(jobs.size()), kT, need, s>>>(d, int(need / sizeof(double)));
+  SBX_LAUNCHED();
+}
+
+void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  int dev = 0, sms = 148;
+  SBX_CUDA(cudaGetDevice(&dev));
+  SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // first pass: CTAs in proportion to work (columns bound the split)
+  double W = 0.0;
+  for (const auto& j : jobs) W += double(j.M) * double(j.n);
+  auto smem_for = [&](const std::vector<int>& G) {
+    size_t mx = 0;
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      const int nown = (jobs[q].n + G[q] - 1) / G[q];
+      mx = std::max(mx, size_t(jobs[q].M + 2 * nown + 40) * 8 + size_t(32 + nown) * 4 + 64);
+    }
+    return mx;
+  };
+  static bool attr = false;
+  if (!attr) {
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+    attr = true;
+  }
+  std::vector<int> G(jobs.size(), 1);
+  int per_sm = 1;
+  for (int iter = 0; iter < 3; ++iter) {
+    const size_t smem = smem_for(G);
+    require(smem <= kSmemCap, "cpqr_coop: problem too tall for the shared-memory Householder vector");
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCT, smem));
+    per_sm = std::max(1, std::min(per_sm, 2));
+    const int T = std::max(int(jobs.size()), sms * per_sm);
+    int used = 0;
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      const double w = double(jobs[q].M) * double(jobs[q].n) / W;
+      G[q] = std::max(1, std::min(jobs[q].n, int(std::floor(w * (T - int(jobs.size())))) + 1));
+      used += G[q];
+    }
+    require(used <= sms * per_sm, "cpqr_coop: too many concurrent problems for one cooperative launch");
+  }
+  const size_t smem = smem_for(G);
+  std::vector<int> cta_job, cta_rank, part_off(jobs.size());
+  std::vector<i64> beta_off(jobs.size());
+  i64 boff = 0;
+  int poff = 0;
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    part_off[q] = poff;
+    poff += G[q];
+    beta_off[q] = boff;
+    boff += std::min(jobs[q].M, jobs[q].n);
+    for (int r = 0; r < G[q]; ++r) {
+      cta_job.push_back(int(q));
+      cta_rank.push_back(r);
+    }
+  }
+  static thread_local JobTable<QrJob> tjobs;
+  static thread_local DevBuf<int> d_ints;
+  static thread_local DevBuf<CoopCtl> d_ctl;
+  static thread_local DevBuf<CoopPart> d_parts;
+  static thread_local DevBuf<double> d_beta;
+  static thread_local DevBuf<i64> d_boff;
+  std::vector<int> ints;
+  ints.insert(ints.end(), cta_job.begin(), cta_job.end());
+  ints.insert(ints.end(), cta_rank.begin(), cta_rank.end());
+  ints.insert(ints.end(), G.begin(), G.end());
+  ints.insert(ints.end(), part_off.begin(), part_off.end());
+  d_ints.upload(ints, s);
+  d_ctl.reserve(jobs.size());
+  SBX_CUDA(cudaMemsetAsync(d_ctl.get(), 0, jobs.size() * sizeof(CoopCtl), s));
+  d_parts.reserve(size_t(poff));
+  d_beta.reserve(size_t(std::max<i64>(boff, 1)));
+  d_boff.upload(beta_off, s);
+  CoopArgs a;
+  a.jobs = tjobs.upload(jobs, s);
+  a.cta_job = d_ints.get();
+  a.cta_rank = d_ints.get() + cta_job.size();
+  a.job_ctas = d_ints.get() + 2 * cta_job.size();
+  a.part_off = d_ints.get() + 2 * cta_job.size() + G.size();
+  a.ctl = d_ctl.get();
+  a.parts = d_parts.get();
+  a.beta = d_beta.get();
+  a.beta_off = d_boff.get();
+  void* params[] = {&a};
+  SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_coop_kernel),
+                                       dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
+  SBX_LAUNCHED();
+}
+
+void interp_batched(const std::vector<InterpJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<InterpJob> tab;
+  const InterpJob* d = tab.upload(jobs, s);
+  interp_kernel<<<unsigned(jobs.size()), 256, 0, s>>>(d);
+  SBX_LAUNCHED();
+}
+
+void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<GemmJob> tab;
+  static thread_local JobTable<int4> ttab;
+  static thread_local DevBuf<double> parts;
+  std::vector<GemmJob> js = jobs;
+  // split K when a product has few output tiles but a long inner dimension
+  i64 out_tiles = 0;
+  for (const auto& j : js) out_tiles += i64((j.m + gTM - 1) / gTM) * ((j.n + gTN - 1) / gTN);
+  i64 ptot = 0;
+  std::vector<i64> poff(js.size(), 0);
+  for (size_t q = 0; q < js.size(); ++q) {
+    auto& j = js[q];
+    const i64 t = i64((j.m + gTM - 1) / gTM) * ((j.n + gTN - 1) / gTN);
+    j.splitk = 1;
+    if (j.k >= 2048 && out_tiles < 2 * 148) {
+      const int want = int(std::min<i64>((2 * 148 + t - 1) / std::max<i64>(t, 1), j.k / 512));
+      if (want > 1) {
+        j.kchunk = ((j.k + want - 1) / want + gKC - 1) / gKC * gKC;
+        j.splitk = (j.k + j.kchunk - 1) / j.kchunk;
+      }
+    }
+    if (j.splitk > 1) {
+      poff[q] = ptot;
+      ptot += i64(j.splitk) * j.m * j.n;
+    }
+  }
+  if (ptot > 0) {
+    parts.reserve(size_t(ptot));
+    for (size_t q = 0; q < js.size(); ++q)
+      if (js[q].splitk > 1) js[q].part = parts.get() + poff[q];
+  }
+  std::vector<int4> tiles;
+  i64 mx_out = 0;
+  for (size_t j = 0; j < js.size(); ++j) {
+    for (int w = 0; w < js[j].splitk; ++w)
+      for (int r = 0; r < js[j].m; r += gTM)
+        for (int c = 0; c < js[j].n; c += gTN) tiles.push_back(make_int4(int(j), r, c, w));
+    if (js[j].splitk > 1) mx_out = std::max<i64>(mx_out, i64(js[j].m) * js[j].n);
+  }
+  if (tiles.empty()) return;
+  const GemmJob* d = tab.upload(js, s);
+  const int4* dt = ttab.upload(tiles, s);
+  gemm_kernel<<<unsigned(tiles.size()), 256, 0, s>>>(d, dt);
+  SBX_LAUNCHED();
+  if (mx_out > 0) {
+    dim3 grid(unsigned(std::min<i64>((mx_out + 255) / 256, 256)), unsigned(js.size()));
+    splitk_reduce_kernel<<<grid, 256, 0, s>>>(d);
+    SBX_LAUNCHED();
+  }
+}
+
+void lu_batched(const std::vector<LuJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<LuJob> tab;
+  size_t need = 64 * sizeof(double);
+  for (const auto& j : jobs) {
+    require(j.n <= 32 * kMaxRowsPerLane, "lu_batched: matrix too large for the warp solver");
+    const size_t sz = (64 + size_t(j.n) * j.n) * sizeof(double);
+    if (sz <= kSmemCap) need = std::max(need, sz);
+  }
+  static bool attr = false;
+  if (!attr) {
+    SBX_CUDA(cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+    attr = true;
+  }
+  const LuJob* d = tab.upload(jobs, s);
+  lu_kernel<<<unsigned(jobs.size()), kT, need, s>>>(d, int(need / sizeof(double)));
+  SBX_LAUNCHED();
+}
+
+void lu_solve(const double* lu, int n, int lda, const int* piv, double* B, int ldb, int nrhs,
+              double* scratch, cudaStream_t s) {
+  if (nrhs == 0 || n == 0) return;
+  require(n <= 32 * kMaxRowsPerLane, "lu_solve: matrix too large for the warp solver");
+  const int warps_per_block = 8;
+  lu_solve_kernel<<<unsigned((nrhs + warps_per_block - 1) / warps_per_block), 32 * warps_per_block,
+                    0, s>>>(lu, n, lda, piv, B, ldb, nrhs, scratch);
+  SBX_LAUNCHED();
+}
+
+void copy_batched(const std::vector<CopyJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<CopyJob> tab;
+  i64 mx = 0;
+  for (const auto& j : jobs) mx = std::max<i64>(mx, i64(j.rows) * j.cols);
+  if (mx == 0) return;
+  const CopyJob* d = tab.upload(jobs, s);
+  dim3 grid(unsigned(std::min<i64>((mx + 255) / 256, 64)), unsigned(jobs.size()));
+  copy_jobs_kernel<<<grid, 256, 0, s>>>(d);
+  SBX_LAUNCHED();
+}
+
+void scatter_batched(const std::vector<ScatterJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static thread_local JobTable<ScatterJob> tab;
+  i64 mx = 0;
+  for (const auto& j : jobs) mx = std::max<i64>(mx, i64(j.rows) * j.cols);
+  if (mx == 0) return;
+  const ScatterJob* d = tab.upload(jobs, s);
+  dim3 grid(unsigned(std::min<i64>((mx + 255) / 256, 256)), unsigned(jobs.size()));
+  scatter_jobs_kernel<<<grid, 256, 0, s>>>(d);
+  SBX_LAUNCHED();
+}
+
+void launch_copy2d(const double* src, i64 lds, double* dst, i64 ldd, i64 rows, i64 cols,
+                   cudaStream_t s) {
+  if (rows * cols == 0) return;
+  const unsigned g = unsigned(std::min<i64>((rows * cols + 255) / 256, 4096));
+  copy2d_kernel<<<g, 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+  SBX_LAUNCHED();
+}
+
+void launch_add_identity(double* a, i64 lda, i64 n, cudaStream_t s) {
+  if (n == 0) return;
+  add_identity_kernel<<<unsigned(std::min<i64>((n + 255) / 256, 1024)), 256, 0, s>>>(a, lda, n);
+  SBX_LAUNCHED();
+}
+
+}  // namespace sbx

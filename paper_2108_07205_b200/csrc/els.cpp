@@ -1,0 +1,213 @@
+// ELS / Woodbury build and solve on the device (reference els.cpp:25-203).
+#include "els.hpp"
+
+#include <cmath>
+#include <limits>
+
+#include "dense.hpp"
+#include "entries.hpp"
+#include "hbs_build.hpp"
+
+namespace sbx {
+
+namespace {
+
+std::vector<i64> scalars(const std::vector<i64>& nodes) {
+  std::vector<i64> o;
+  o.reserve(2 * nodes.size());
+  for (i64 n : nodes) {
+    o.push_back(2 * n);
+    o.push_back(2 * n + 1);
+  }
+  return o;
+}
+
+// Dense LU + explicit inverse + rcond (Eigen PartialPivLU::rcond) of an
+// n x n device matrix a (destroyed); returns rcond.
+double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
+  require(n <= 512, "dense block above 512 unknowns is not supported on the device path yet");
+  DevBuf<int> piv(static_cast<size_t>(n));
+  DevBuf<double> rc(1), work(static_cast<size_t>(4 * n));
+  LuJob j{};
+  j.a = a;
+  j.n = int(n);
+  j.lda = int(n);
+  j.piv = piv.get();
+  j.inv = inv;
+  j.rcond = rc.get();
+  j.work = work.get();
+  lu_batched({j}, s);
+  double r = 0;
+  rc.download(&r, 1, s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  return r;
+}
+
+// out = Atilde^{-1} v for an n_ext x nrhs column-major device block
+// (els.cpp:43-65): the old-mesh part goes through the HBS sweep in old
+// ordering (scatter/gather fused into the layout kernels), the added part
+// through the dense inverse or its own HBS.
+void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nrhs, cudaStream_t s) {
+  HbsOp& A = *e.a_oo;
+  if (!A.solve_plan.built) hbs_build_solve_plan(A);
+  SweepPlan& P = A.solve_plan;
+  A.ws.reserve(size_t(P.ws_rows * nrhs));
+  const i64 nkc = e.n_k + e.n_c;
+  launch_cm_to_rm(v, ldv, nkc, nrhs, A.ws.get() + P.in_row * nrhs, e.d_old_of_ext.get(), s);
+  hbs_run_plan(A, P, A.ws.get(), nrhs, s);
+  // gather: out row i <- old row map[i]
+  launch_rm_to_cm(A.ws.get() + P.out_row * nrhs, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
+  if (e.n_p == 0) return;
+  const double* vp = v + nkc;
+  double* op = out + nkc;
+  if (e.app_h) {
+    HbsOp& H = *e.app_h;
+    if (!H.solve_plan.built) hbs_build_solve_plan(H);
+    SweepPlan& Q = H.solve_plan;
+    H.ws.reserve(size_t(Q.ws_rows * nrhs));
+    launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * nrhs, nullptr, s);
+    hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
+    launch_rm_to_cm(H.ws.get() + Q.out_row * nrhs, e.n_p, nrhs, op, ldo, nullptr, s);
+  } else {
+    gemm_batched({{e.app_inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
+                   int(ldo), 0, 0, 1.0, 0.0}},
+                 s);
+  }
+}
+
+}  // namespace
+
+std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom& new_g,
+                                      const Plan& plan, const Update& upd, int form, double mu,
+                                      cudaStream_t s) {
+  require(a_oo.has_inverse, "els_build: diagonal solver lacks inverse");
+  auto e = std::make_unique<Els>();
+  e->a_oo = &a_oo;
+  const auto kept_old_s = scalars(plan.kept_old), cut_s = scalars(plan.cut_old);
+  e->kept_new_s = scalars(plan.kept_new);
+  e->added_s = scalars(plan.added_new);
+  e->n_k = i64(kept_old_s.size());
+  e->n_c = i64(cut_s.size());
+  e->n_p = i64(e->added_s.size());
+  e->n_new = new_g.n_nodes();
+  require(a_oo.n == e->n_k + e->n_c, "els_build: diagonal solver size does not match the old mesh");
+  require(upd.n_ext() == e->n_ext(), "els_build: update factor size does not match the plan");
+  std::vector<i64> old_of_ext = kept_old_s;
+  old_of_ext.insert(old_of_ext.end(), cut_s.begin(), cut_s.end());
+  e->d_old_of_ext.upload(old_of_ext, s);
+  if (e->n_p > 0) {
+    if (e->n_p <= 2048) {  // kDenseAddedLimit counts scalars (els.hpp:40)
+      EntryOracle eo(new_g, form, mu, s);
+      DevBuf<double> app(static_cast<size_t>(e->n_p * e->n_p));
+      DevBuf<i64> idx;
+      idx.upload(e->added_s, s);
+      eo.submatrix(idx.get(), e->n_p, idx.get(), e->n_p, app.get(), e->n_p, s);
+      e->app_inv.resize(size_t(e->n_p * e->n_p));
+      const double rc = dense_inverse(app.get(), e->n_p, e->app_inv.get(), s);
+      if (rc < 1e-14) throw Error(4, "added-unknown diagonal block is singular at added block");
+    } else {
+      HbsBuildOptions o;
+      o.eps = a_oo.eps;
+      e->app_h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()),
+                                     o, s);
+      hbs_invert_device(*e->app_h, s);
+    }
+  }
+  e->k = upd.k;
+  const i64 k = e->k, n = e->n_ext();
+  if (k > 0) {
+    e->R.resize(size_t(k * n));
+    SBX_CUDA(cudaMemcpyAsync(e->R.get(), upd.R.get(), size_t(k * n) * 8, cudaMemcpyDeviceToDevice, s));
+    e->X.resize(size_t(n * k));
+    atilde_solve(*e, upd.L.get(), n, e->X.get(), n, k, s);
+    // W = I + R X  (els.cpp:124)
+    e->Wmat.resize(size_t(k * k));
+    gemm_batched({{e->R.get(), e->X.get(), e->Wmat.get(), int(k), int(k), int(n), int(k), int(n), int(k), 0,
+                   0, 1.0, 0.0}},
+                 s);
+    launch_add_identity(e->Wmat.get(), k, k, s);
+    DevBuf<double> wlu(static_cast<size_t>(k * k));
+    SBX_CUDA(cudaMemcpyAsync(wlu.get(), e->Wmat.get(), size_t(k * k) * 8, cudaMemcpyDeviceToDevice, s));
+    e->Winv.resize(size_t(k * k));
+    const double rc = dense_inverse(wlu.get(), k, e->Winv.get(), s);
+    if (rc < std::sqrt(std::numeric_limits<double>::epsilon()))
+      throw Error(4,
+                  "woodbury operator numerically singular; consider the optimal-basis compression "
+                  "mode at woodbury solve");
+  }
+  SBX_CUDA(cudaStreamSynchronize(s));
+  return e;
+}
+
+void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cudaStream_t s) {
+  const i64 n = e.n_ext(), k = e.k;
+  atilde_solve(e, g_ext, n, y, n, nrhs, s);
+  if (k == 0) return;
+  // y -= X W^{-1} (R y)   (els.cpp:150)
+  e.ws2.reserve(size_t(2 * k * nrhs));
+  double* t = e.ws2.get();
+  double* u = t + k * nrhs;
+  gemm_batched({{e.R.get(), y, t, int(k), int(nrhs), int(n), int(k), int(n), int(k), 0, 0, 1.0, 0.0}}, s);
+  gemm_batched({{e.Winv.get(), t, u, int(k), int(nrhs), int(k), int(k), int(k), int(k), 0, 0, 1.0, 0.0}}, s);
+  gemm_batched({{e.X.get(), u, y, int(n), int(nrhs), int(k), int(n), int(k), int(n), 0, 0, -1.0, 1.0}}, s);
+}
+
+void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, bool raw, bool dev,
+               cudaStream_t s) {
+  const i64 n = e.n_ext();
+  const i64 rows_in = raw ? n : e.n_k + e.n_p;
+  require(ldg >= rows_in && ldy >= rows_in, "els_solve: leading dimension too small");
+  if (nrhs == 0) return;
+  e.ws.reserve(size_t(2 * n * nrhs));
+  double* gx = e.ws.get();
+  double* yx = gx + n * nrhs;
+  const i64 nkc = e.n_k + e.n_c;
+  // g_ext = (g_k, 0, g_p)  (els.cpp:167-169)
+  if (raw) {
+    if (dev)
+      SBX_CUDA(cudaMemcpy2DAsync(gx, size_t(n) * 8, g, size_t(ldg) * 8, size_t(n) * 8, size_t(nrhs),
+                                 cudaMemcpyDeviceToDevice, s));
+    else
+      SBX_CUDA(cudaMemcpy2DAsync(gx, size_t(n) * 8, g, size_t(ldg) * 8, size_t(n) * 8, size_t(nrhs),
+                                 cudaMemcpyHostToDevice, s));
+  } else {
+    const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    SBX_CUDA(cudaMemset2DAsync(gx + e.n_k, size_t(n) * 8, 0, size_t(e.n_c) * 8, size_t(nrhs), s));
+    if (e.n_k)
+      SBX_CUDA(cudaMemcpy2DAsync(gx, size_t(n) * 8, g, size_t(ldg) * 8, size_t(e.n_k) * 8, size_t(nrhs),
+                                 kind, s));
+    if (e.n_p)
+      SBX_CUDA(cudaMemcpy2DAsync(gx + nkc, size_t(n) * 8, g + e.n_k, size_t(ldg) * 8, size_t(e.n_p) * 8,
+                                 size_t(nrhs), kind, s));
+  }
+  els_solve_ext_device(e, gx, yx, nrhs, s);
+  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (raw) {
+    SBX_CUDA(cudaMemcpy2DAsync(y, size_t(ldy) * 8, yx, size_t(n) * 8, size_t(n) * 8, size_t(nrhs), kind, s));
+  } else {  // drop the dummy (cut) block
+    if (e.n_k)
+      SBX_CUDA(cudaMemcpy2DAsync(y, size_t(ldy) * 8, yx, size_t(n) * 8, size_t(e.n_k) * 8, size_t(nrhs),
+                                 kind, s));
+    if (e.n_p)
+      SBX_CUDA(cudaMemcpy2DAsync(y + e.n_k, size_t(ldy) * 8, yx + nkc, size_t(n) * 8, size_t(e.n_p) * 8,
+                                 size_t(nrhs), kind, s));
+  }
+  if (!dev) SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void els_density_on_refined(const Els& e, const double* tau_n, double* out) {
+  // els.cpp:195-203 (host scatter of a host vector)
+  for (i64 i = 0; i < 2 * e.n_new; ++i) out[i] = 0.0;
+  for (i64 i = 0; i < e.n_k; ++i) out[e.kept_new_s[size_t(i)]] = tau_n[i];
+  for (i64 i = 0; i < e.n_p; ++i) out[e.added_s[size_t(i)]] = tau_n[e.n_k + i];
+}
+
+void els_download_xw(const Els& e, double* X, double* W, cudaStream_t s) {
+  const i64 k = e.k, n = e.n_ext();
+  if (k == 0) return;
+  if (X) e.X.download(X, size_t(n * k), s);
+  if (W) e.Wmat.download(W, size_t(k * k), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace sbx

@@ -1,0 +1,50 @@
+// Extended linear system + Woodbury solver on the device (north-star
+// subsystem 3; reference els.cpp:80-203).
+//
+// Extended ordering (kept, cut, added) scalars.  Atilde = diag(A_oo in
+// old-mesh order, A_pp); A_oo^{-1} is the static HBS inverse, A_pp^{-1} an
+// explicit dense inverse (2 N_p <= 2048, els.hpp:40) or its own HBS.
+//   build:  X = Atilde^{-1} L  (multi-RHS sweep, nrhs = k),
+//           W = I + R X        (DMMA GEMM),  W = P L U + rcond gate
+//   solve:  y = Atilde^{-1} g ;  y -= X W^{-1} (R y)
+#pragma once
+
+#include "geometry.hpp"
+#include "hbs.hpp"
+#include "update.hpp"
+
+namespace sbx {
+
+struct Els {
+  HbsOp* a_oo = nullptr;            // static wall solver (owned by the caller's handle)
+  std::unique_ptr<HbsOp> app_h;     // HBS of A_pp above the dense limit
+  DevBuf<double> app_inv;           // dense A_pp^{-1}
+  i64 n_k = 0, n_c = 0, n_p = 0;    // scalar counts
+  i64 k = 0;
+  i64 n_ext() const { return n_k + n_c + n_p; }
+  DevBuf<double> R;                 // k x n_ext
+  DevBuf<double> X;                 // n_ext x k
+  DevBuf<double> Winv;              // k x k explicit (I + R X)^{-1}
+  DevBuf<double> Wmat;              // k x k (I + R X), for inspection
+  DevBuf<i64> d_old_of_ext;         // ext rows [0, n_k+n_c) -> old-mesh scalar
+  std::vector<i64> kept_new_s, added_s;
+  i64 n_new = 0;
+  DevBuf<double> ws;                // solve workspace
+  DevBuf<double> ws2;
+};
+
+std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom& new_g,
+                                      const Plan& plan, const Update& upd, int formulation,
+                                      double mu, cudaStream_t s);
+// raw: g has n_ext rows (kept, cut, added); else n_k + n_p rows (kept, added)
+// and the dummy block is dropped from the output (els.cpp:165-179).
+void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, bool raw, bool dev,
+               cudaStream_t s);
+void els_density_on_refined(const Els& e, const double* tau_n, double* out);
+void els_download_xw(const Els& e, double* X, double* W, cudaStream_t s);
+
+// Device-resident solve for callers holding device buffers:
+// y_ext (n_ext x nrhs, column-major ld n_ext) = ELS^{-1} g_ext.
+void els_solve_ext_device(Els& e, const double* g_ext, double* y_ext, i64 nrhs, cudaStream_t s);
+
+}  // namespace sbx

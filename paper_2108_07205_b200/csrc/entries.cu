@@ -1,0 +1,303 @@
+// Kernel-block assembly on sm_100a (north-star subsystem 1).
+// Compiled with --fmad=false so the interior (double-layer + completion)
+// entries round exactly like the reference's scalar code (nystrom.cpp:80-172):
+// no FMA contraction, IEEE division.  Stores are coalesced along the
+// leading dimension of the column-major destination.
+#include <algorithm>
+#include <vector>
+
+#include "entries.hpp"
+
+namespace sbx {
+
+namespace {
+
+__device__ __forceinline__ i64 node_of(const EntryView& v, i64 local) {
+  return v.map ? v.map[local] : local;
+}
+
+__device__ __forceinline__ bool in_null(const EntryView& v, int comp) {
+  return v.form == SBX_INTERIOR_DIRICHLET || (v.form == SBX_MIXED && comp == 0);
+}
+__device__ __forceinline__ bool single_layer(const EntryView& v, int comp) {
+  return v.form == SBX_EXTERIOR_COMBINED || (v.form == SBX_MIXED && comp != 0);
+}
+
+// One scalar entry A(2i+a, 2j+b) of the completed double-layer operator
+// (nystrom.cpp:80-172, double-layer + completion terms).  Single-layer
+// components are rejected on the host before any launch.
+__device__ double entry(const EntryView& v, i64 rs, i64 cs) {
+  const i64 i = node_of(v, rs >> 1), j = node_of(v, cs >> 1);
+  const int a = int(rs & 1), b = int(cs & 1);
+  const int ci = v.comp[i];
+  if (i == j) {
+    const double wi = v.w[i];
+    const double dl = -v.kappa[i] / (2.0 * kPi) * wi;
+    // out[2] = out[1] in the reference: both off-diagonal slots are (dl*tx)*ty
+    const double ta = (a == 0 || a != b) ? v.tx[i] : v.ty[i];
+    const double tb = (b == 1 || a != b) ? v.ty[i] : v.tx[i];
+    double out = dl * ta * tb;
+    if (a == b) out = v.jump + out;
+    if (in_null(v, ci)) {
+      const double na = a == 0 ? v.nx[i] : v.ny[i];
+      const double nb = b == 0 ? v.nx[i] : v.ny[i];
+      out += wi * na * nb;
+    }
+    return out;
+  }
+  const int cj = v.comp[j];
+  const double rx = v.x[i] - v.x[j];
+  const double ry = v.y[i] - v.y[j];
+  const double r2 = rx * rx + ry * ry;
+  const double wj = v.w[j];
+  const double dn = (rx * v.nx[j] + ry * v.ny[j]) / (kPi * r2 * r2);
+  const double c = wj * dn;
+  const double ra = (a == 0 || a != b) ? rx : ry;  // out[2] = out[1] = (c*rx)*ry
+  const double rb = (b == 1 || a != b) ? ry : rx;
+  double out = c * ra * rb;
+  if (in_null(v, ci) && in_null(v, cj)) {
+    const double na = a == 0 ? v.nx[i] : v.ny[i];
+    const double nb = b == 0 ? v.nx[j] : v.ny[j];
+    out += wj * na * nb;
+  }
+  return out;
+}
+
+struct M2d {
+  double a00, a01, a10, a11;
+  __device__ double at(int i, int j) const {
+    return i == 0 ? (j == 0 ? a00 : a01) : (j == 0 ? a10 : a11);
+  }
+};
+
+// kernels.cpp:13-31 (target x, source y)
+__device__ M2d stokeslet(double x0, double x1, double y0, double y1, double mu) {
+  const double rx = x0 - y0, ry = x1 - y1;
+  const double r2 = rx * rx + ry * ry;
+  const double c = 1.0 / (4.0 * kPi * mu);
+  const double s = c / r2;
+  const double lg = -0.5 * log(r2) * c;
+  return {rx * rx * s + lg, rx * ry * s, ry * rx * s, ry * ry * s + lg};
+}
+__device__ M2d double_layer(double x0, double x1, double y0, double y1, double n0, double n1) {
+  const double rx = x0 - y0, ry = x1 - y1;
+  const double r2 = rx * rx + ry * ry;
+  const double c = (rx * n0 + ry * n1) / (kPi * r2 * r2);
+  return {rx * rx * c, rx * ry * c, ry * rx * c, ry * ry * c};
+}
+// kernels.cpp:50-72
+__device__ M2d stokeslet_gradient(double x0, double x1, double y0, double y1, double mu, double d0,
+                                  double d1) {
+  const double rx = x0 - y0, ry = x1 - y1;
+  const double r2 = rx * rx + ry * ry;
+  const double rd = rx * d0 + ry * d1;
+  const double c2 = 2.0 * rd / (r2 * r2);
+  const double s = 4.0 * kPi * mu;
+  return {((d0 * rx + rx * d0) / r2 - rx * rx * c2 - rd / r2) / s,
+          ((d0 * ry + rx * d1) / r2 - rx * ry * c2) / s,
+          ((d1 * rx + ry * d0) / r2 - ry * rx * c2) / s,
+          ((d1 * ry + ry * d1) / r2 - ry * ry * c2 - rd / r2) / s};
+}
+__device__ M2d double_layer_gradient(double x0, double x1, double y0, double y1, double n0,
+                                     double n1, double d0, double d1) {
+  const double rx = x0 - y0, ry = x1 - y1;
+  const double r2 = rx * rx + ry * ry, r4 = r2 * r2;
+  const double rn = rx * n0 + ry * n1, rd = rx * d0 + ry * d1;
+  const double a = rn / r4;
+  const double b = (n0 * d0 + n1 * d1) / r4 - 4.0 * rn * rd / (r4 * r2);
+  return {((d0 * rx + rx * d0) * a + rx * rx * b) / kPi, ((d0 * ry + rx * d1) * a + rx * ry * b) / kPi,
+          ((d1 * rx + ry * d0) * a + ry * rx * b) / kPi, ((d1 * ry + ry * d1) * a + ry * ry * b) / kPi};
+}
+
+__global__ void block_jobs_kernel(EntryView v, const BlockJob* __restrict__ jobs,
+                                  const i64* __restrict__ rows, const i64* __restrict__ cols,
+                                  double* __restrict__ out, const i64* __restrict__ dst_cols) {
+  const BlockJob jb = jobs[blockIdx.y];
+  const i64 total = i64(jb.nr) * jb.nc;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const int r = int(idx % jb.nr), c = int(idx / jb.nr);
+    const i64 oc = jb.dst_col_off >= 0 ? dst_cols[jb.dst_col_off + c] : c;
+    out[jb.out_off + r + oc * jb.ld] = entry(v, rows[jb.row_off + r], cols[jb.col_off + c]);
+  }
+}
+
+__global__ void submatrix_kernel(EntryView v, const i64* __restrict__ rows, i64 nr,
+                                 const i64* __restrict__ cols, i64 nc, double* __restrict__ out,
+                                 i64 ld) {
+  const i64 total = nr * nc;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const i64 r = idx % nr, c = idx / nr;
+    out[r + c * ld] = entry(v, rows[r], cols[c]);
+  }
+}
+
+__global__ void proxy_jobs_kernel(EntryView v, const ProxyJob* __restrict__ jobs,
+                                  const i64* __restrict__ cand, double* __restrict__ out) {
+  const ProxyJob jb = jobs[blockIdx.y];
+  const i64 total = i64(jb.ns) * jb.n;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const int s = int(idx % jb.ns), c = int(idx / jb.ns);
+    const i64 cs = cand[jb.cand_off + c];
+    const i64 node = node_of(v, cs >> 1);
+    const int a = int(cs & 1);
+    const double t = 2.0 * kPi * double(s) / double(jb.ns);
+    const double d0 = cos(t), d1 = sin(t);
+    const double p0 = jb.cx + jb.rad * d0, p1 = jb.cy + jb.rad * d1;
+    double* col = out + jb.out_off + i64(c) * jb.ld;
+    double q0, q1, q2, q3;
+    if (jb.kind != 1) {  // outgoing: fields at the candidate from circle sources
+      const double mu = jb.kind == 2 ? 1.0 : v.mu;
+      const M2d sl = stokeslet(v.x[node], v.y[node], p0, p1, mu);
+      const M2d dl = double_layer(v.x[node], v.y[node], p0, p1, d0, d1);
+      q0 = sl.at(a, 0);
+      q1 = sl.at(a, 1);
+      q2 = dl.at(a, 0);
+      q3 = dl.at(a, 1);
+    } else {  // incoming: candidate source evaluated on the circle
+      const double nj0 = v.nx[node], nj1 = v.ny[node], wj = v.w[node];
+      M2d val = double_layer(p0, p1, v.x[node], v.y[node], nj0, nj1);
+      M2d grad = double_layer_gradient(p0, p1, v.x[node], v.y[node], nj0, nj1, d0, d1);
+      if (single_layer(v, v.comp[node])) {
+        const M2d s1 = stokeslet(p0, p1, v.x[node], v.y[node], v.mu);
+        const M2d g1 = stokeslet_gradient(p0, p1, v.x[node], v.y[node], v.mu, d0, d1);
+        val = {val.a00 + s1.a00, val.a01 + s1.a01, val.a10 + s1.a10, val.a11 + s1.a11};
+        grad = {grad.a00 + g1.a00, grad.a01 + g1.a01, grad.a10 + g1.a10, grad.a11 + g1.a11};
+      }
+      q0 = wj * val.at(0, a);
+      q1 = wj * val.at(1, a);
+      q2 = wj * grad.at(0, a);
+      q3 = wj * grad.at(1, a);
+    }
+    col[4 * s + 0] = q0;
+    col[4 * s + 1] = q1;
+    col[4 * s + 2] = q2;
+    col[4 * s + 3] = q3;
+    if (s == 0 && jb.with_null) {
+      const bool nul = in_null(v, v.comp[node]);
+      const double nn = a == 0 ? v.nx[node] : v.ny[node];
+      col[4 * jb.ns] = nul ? (jb.kind == 1 ? v.w[node] * nn : nn) : 0.0;
+    }
+  }
+}
+
+__global__ void near_jobs_kernel(EntryView v, const NearJob* __restrict__ jobs,
+                                 const i64* __restrict__ cand, const i64* __restrict__ nearv,
+                                 double* __restrict__ out) {
+  const NearJob jb = jobs[blockIdx.y];
+  const i64 total = i64(jb.n_near) * jb.n;
+  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
+       idx += i64(gridDim.x) * blockDim.x) {
+    const int r = int(idx % jb.n_near), c = int(idx / jb.n_near);
+    const i64 cs = cand[jb.cand_off + c], ns = nearv[jb.near_off + r];
+    out[jb.out_off + r + i64(c) * jb.ld] = jb.transpose ? entry(v, ns, cs) : entry(v, cs, ns);
+  }
+}
+
+__global__ void boundary_data_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                     i64 n, const double* __restrict__ src, i64 n_src, double mu,
+                                     double* __restrict__ out) {
+  for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
+    double u0 = 0, u1 = 0;  // field_velocity (nystrom.cpp:394-398)
+    for (i64 s = 0; s < n_src; ++s) {
+      const M2d k = stokeslet(x[i], y[i], src[4 * s], src[4 * s + 1], mu);
+      u0 += k.a00 * src[4 * s + 2] + k.a01 * src[4 * s + 3];
+      u1 += k.a10 * src[4 * s + 2] + k.a11 * src[4 * s + 3];
+    }
+    out[2 * i] = u0;
+    out[2 * i + 1] = u1;
+  }
+}
+
+unsigned grid_x(i64 total, unsigned cap = 4096) {
+  return unsigned(std::max<i64>(1, std::min<i64>((total + 255) / 256, cap)));
+}
+
+}  // namespace
+
+EntryOracle::EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t,
+                         const i64* d_map)
+    : form_(formulation) {
+  require(formulation >= 0 && formulation <= 2, "unknown formulation");
+  require(mu > 0, "assembler: viscosity must be positive");
+  if (formulation == SBX_INTERIOR_DIRICHLET)
+    require(g.comps.size() == 1, "interior formulation expects a single curve");
+  if (formulation == SBX_MIXED) require(!g.comps[0].is_hole, "mixed formulation expects wall first");
+  // The log-corrected single layer (exterior / hole components) needs the
+  // product-rule tables of logquad.cpp; it is not on the device path yet.
+  require(formulation == SBX_INTERIOR_DIRICHLET || (formulation == SBX_MIXED && g.comps.size() == 1),
+          "single-layer (exterior / hole) components are not on the device path yet");
+  const GeomDev& d = g.dev;
+  v_.x = d.x();
+  v_.y = d.y();
+  v_.nx = d.nx();
+  v_.ny = d.ny();
+  v_.w = d.w();
+  v_.kappa = d.kappa();
+  v_.tx = d.tx();
+  v_.ty = d.ty();
+  v_.comp = d.comp.get();
+  v_.map = d_map;
+  v_.jump = formulation == SBX_EXTERIOR_COMBINED ? 0.5 : -0.5;
+  v_.mu = mu;
+  v_.form = formulation;
+}
+
+void EntryOracle::submatrix(const i64* d_rows, i64 nr, const i64* d_cols, i64 nc, double* d_out,
+                            i64 ld, cudaStream_t s) const {
+  if (nr * nc == 0) return;
+  submatrix_kernel<<<grid_x(nr * nc), 256, 0, s>>>(v_, d_rows, nr, d_cols, nc, d_out, ld);
+  SBX_LAUNCHED();
+}
+
+void EntryOracle::submatrix_host(const i64* rows, i64 nr, const i64* cols, i64 nc, double* out,
+                                 cudaStream_t s) const {
+  DevBuf<i64> dr, dc;
+  DevBuf<double> dout(size_t(std::max<i64>(nr * nc, 1)));
+  dr.upload(rows, size_t(nr), s);
+  dc.upload(cols, size_t(nc), s);
+  submatrix(dr.get(), nr, dc.get(), nc, dout.get(), nr, s);
+  dout.download(out, size_t(nr * nc), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void boundary_data_host(const Geom& g, i64 n_src, const double* src_xyf, double mu, double* out,
+                        cudaStream_t s) {
+  const i64 n = g.n_nodes();
+  DevBuf<double> ds, dout(size_t(2 * n));
+  ds.upload(src_xyf, size_t(4 * n_src), s);
+  boundary_data_kernel<<<grid_x(n), 256, 0, s>>>(g.dev.x(), g.dev.y(), n, ds.get(), n_src, mu,
+                                                 dout.get());
+  SBX_LAUNCHED();
+  dout.download(out, size_t(2 * n), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void launch_block_jobs(const EntryView& v, const BlockJob* d_jobs, int n_jobs, i64 max_entries,
+                       const i64* d_rows, const i64* d_cols, double* out, cudaStream_t s,
+                       const i64* d_dst_cols) {
+  if (n_jobs == 0 || max_entries == 0) return;
+  dim3 grid(grid_x(max_entries, 64), unsigned(n_jobs));
+  block_jobs_kernel<<<grid, 256, 0, s>>>(v, d_jobs, d_rows, d_cols, out, d_dst_cols);
+  SBX_LAUNCHED();
+}
+
+void launch_proxy_jobs(const EntryView& v, const ProxyJob* d_jobs, int n_jobs, int max_rows,
+                       int max_n, const i64* d_cand, double* out, cudaStream_t s) {
+  if (n_jobs == 0) return;
+  dim3 grid(grid_x(i64(max_rows) * max_n, 64), unsigned(n_jobs));
+  proxy_jobs_kernel<<<grid, 256, 0, s>>>(v, d_jobs, d_cand, out);
+  SBX_LAUNCHED();
+}
+
+void launch_near_jobs(const EntryView& v, const NearJob* d_jobs, int n_jobs, i64 max_entries,
+                      const i64* d_cand, const i64* d_near, double* out, cudaStream_t s) {
+  if (n_jobs == 0 || max_entries == 0) return;
+  dim3 grid(grid_x(max_entries, 64), unsigned(n_jobs));
+  near_jobs_kernel<<<grid, 256, 0, s>>>(v, d_jobs, d_cand, d_near, out);
+  SBX_LAUNCHED();
+}
+
+}  // namespace sbx

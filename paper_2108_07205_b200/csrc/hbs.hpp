@@ -1,0 +1,118 @@
+// Device-resident HBS operator (reference HbsOperator, hbs.hpp:48-74).
+//
+// The tree topology and skeleton index lists stay on the host (they drive
+// launch plans); every factor lives in one device arena, packed level-major
+// so each sweep level streams one contiguous range of HBM:
+//   fg_i = [f_i; g_i]   (k_i + c_i) x c_i   up-sweep of the solve (one GEMV)
+//   e_i                  c_i x k_i           down-sweep of the solve
+//   vd_i = [v_i^T; d_i]  (k_i + c_i) x c_i   up-sweep of the apply (leaves;
+//                                            internal nodes store v_i^T only)
+//   u_i                  c_i x k_i           down-sweep of the apply
+//   b_sib_i              k_i x k_sib         sibling coupling
+//   root_g               c_0 x c_0
+// All blocks are column-major (Eigen order) so HBS1 files map 1:1.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace sbx {
+
+struct HbsNodeH {
+  i64 begin = 0, end = 0, parent = -1, left = -1, right = -1;
+  int depth = 0;
+  i64 k = 0;
+  i64 c = 0;  // candidate count: 2*(end-begin) at a leaf, k_l + k_r above
+  std::vector<i64> row_skel, col_skel;
+  bool is_leaf() const { return left < 0; }
+  // arena offsets (doubles), -1 when absent
+  i64 o_fg = -1, o_e = -1, o_vd = -1, o_u = -1, o_b = -1, o_dhat = -1, o_v = -1;
+};
+
+// One row-tiled product  D[rows] = A * B (+ P)  inside a sweep level.
+// Offsets are in doubles (A, into the factor arena) or in rows of the
+// row-major sweep workspace (B, P, D1, D2; one row = nrhs doubles).
+struct SweepTask {
+  i64 a_off;
+  int lda, m, K;
+  i64 b_row, p_row, d1_row, d2_row;
+  int split;  // rows < split go to D1, the rest to D2 (row - split)
+  int pad;
+};
+
+struct SweepLevel {
+  std::vector<SweepTask> tasks;
+  i64 first_task = 0;  // index into the flattened device task table
+  i64 first_item = 0, n_items = 0;
+  int max_k = 0;       // largest K in the level (smem sizing)
+};
+
+struct SweepPlan {
+  std::vector<SweepLevel> levels;  // launch order
+  i64 ws_rows = 0;                 // workspace rows (x nrhs doubles)
+  i64 in_row = 0, out_row = 0;     // input / output vector regions
+  DevBuf<SweepTask> d_tasks;
+  DevBuf<int2> d_items;            // (task, row0)
+  bool built = false;
+};
+
+struct HbsOp {
+  i64 n = 0, leaf_nodes = 64;
+  double eps = 0.0;
+  bool has_inverse = false;
+  bool has_apply = false;
+  i64 max_block_drawn = 0;
+  int max_depth = 0;
+  std::vector<HbsNodeH> nodes;
+  std::vector<std::string> notes;
+  i64 o_root_g = -1;
+  DevBuf<double> arena;
+  i64 arena_used = 0;
+  SweepPlan solve_plan, apply_plan;
+  DevBuf<double> ws;  // sweep workspace (grown on demand)
+
+  i64 total_skeleton() const {
+    i64 t = 0;
+    for (const auto& nd : nodes) t += nd.k;
+    return t;
+  }
+  i64 sib(i64 id) const {
+    const auto& p = nodes[size_t(nodes[size_t(id)].parent)];
+    return p.left == id ? p.right : p.left;
+  }
+  // Algorithmic bytes of one solve sweep: factor doubles.
+  i64 solve_factor_doubles() const;
+  i64 apply_factor_doubles() const;
+};
+
+// Computes node candidate sizes c and the level-major arena layout, then
+// allocates the arena (contents undefined).
+void hbs_layout(HbsOp& op);
+
+// HBS1 (hbs.cpp:681-808) <-> device arena.
+std::unique_ptr<HbsOp> hbs_load_hbs1(const std::string& path, cudaStream_t s);
+void hbs_save_hbs1(const HbsOp& op, const std::string& path, cudaStream_t s);
+
+// Sweeps.  b/x are column-major n x nrhs with leading dimensions; `dev`
+// says whether they are device pointers.
+void hbs_solve(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev,
+               cudaStream_t s);
+void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev,
+               cudaStream_t s);
+
+// Row-major workspace form, for callers that already hold the sweep input
+// in `ws` row layout (the ELS path): runs the planned levels only.
+void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s);
+void hbs_build_solve_plan(HbsOp& op);
+void hbs_build_apply_plan(HbsOp& op);
+
+// Column-major (ld) <-> row-major (nrhs fastest) with an optional row map:
+// dst_row(i) = map ? map[i] : i.
+void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, const i64* map,
+                     cudaStream_t s);
+void launch_rm_to_cm(const double* src, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
+                     cudaStream_t s);
+
+}  // namespace sbx

@@ -1,0 +1,692 @@
+// Device HBS compression + telescoping inverse (reference hbs.cpp:349-487).
+//
+// Host code owns the tree topology and index bookkeeping (near sets,
+// candidate lists, rank rules); every floating-point step runs on the GPU,
+// batched over all boxes of a level:
+//   W^T assembly  (entries.cu proxy/near jobs)  ->  CPQR (dense.cu qr_kernel)
+//   ->  ranks, sample doubling, rank equalisation (host, from |r_jj|)
+//   ->  interpolation matrices (interp_kernel)  ->  b_sib blocks.
+// The inverse is a per-level batch of LU/inverse/rcond + DMMA GEMMs.
+#include <algorithm>
+#include <cmath>
+#include <unordered_map>
+
+#include "dense.hpp"
+#include "entries.hpp"
+#include "hbs_build.hpp"
+#include "idengine.hpp"
+
+namespace sbx {
+
+namespace {
+
+struct Region {
+  double cx = 0, cy = 0, r0 = 0;
+};
+
+std::vector<i64> scalars_of_range(i64 b, i64 e) {
+  std::vector<i64> s;
+  s.reserve(size_t(2 * (e - b)));
+  for (i64 i = b; i < e; ++i) {
+    s.push_back(2 * i);
+    s.push_back(2 * i + 1);
+  }
+  return s;
+}
+
+// Per-level device storage of the interpolation factors and couplings.
+struct LevelStore {
+  DevBuf<double> buf;
+  std::vector<i64> o_u, o_v, o_b;  // per node in level order
+};
+
+struct Builder {
+  const Geom& g;
+  const HbsBuildOptions& o;
+  cudaStream_t s;
+  HbsOp& op;
+  const EntryOracle& eo;
+  bool has_null;
+  std::vector<double> px, py;  // local node coordinates
+  std::vector<Region> reg;
+  std::vector<std::vector<i64>> levels;
+  i64 max_block = 0;
+
+  std::vector<i64> row_cand(const HbsNodeH& nd) const {
+    if (nd.is_leaf()) return scalars_of_range(nd.begin, nd.end);
+    std::vector<i64> c = op.nodes[size_t(nd.left)].row_skel;
+    const auto& r = op.nodes[size_t(nd.right)].row_skel;
+    c.insert(c.end(), r.begin(), r.end());
+    return c;
+  }
+  std::vector<i64> col_cand(const HbsNodeH& nd) const {
+    if (nd.is_leaf()) return scalars_of_range(nd.begin, nd.end);
+    std::vector<i64> c = op.nodes[size_t(nd.left)].col_skel;
+    const auto& r = op.nodes[size_t(nd.right)].col_skel;
+    c.insert(c.end(), r.begin(), r.end());
+    return c;
+  }
+};
+
+// Near sets of one level (hbs.cpp:242-268).  Leaves use a uniform-grid
+// neighbour search returning the same ascending node list as the
+// reference's O(N) scan; internal nodes scan their level.
+void near_sets(Builder& B, const std::vector<i64>& ids, std::vector<std::vector<i64>>& nc,
+               std::vector<std::vector<i64>>& nr) {
+  nc.assign(ids.size(), {});
+  nr.assign(ids.size(), {});
+  const auto& nodes = B.op.nodes;
+  bool any_leaf = false;
+  double h = 0;
+  for (i64 id : ids)
+    if (nodes[size_t(id)].is_leaf()) {
+      any_leaf = true;
+      h = std::max(h, B.o.div_factor * B.reg[size_t(id)].r0);
+    }
+  std::unordered_map<long long, std::vector<i64>> grid;
+  auto key = [](long long a, long long b) { return (a << 32) ^ (b & 0xffffffffLL); };
+  if (any_leaf) {
+    h = std::max(h, 1e-300);
+    const i64 n = i64(B.px.size());
+    for (i64 j = 0; j < n; ++j)
+      grid[key((long long)std::floor(B.px[size_t(j)] / h), (long long)std::floor(B.py[size_t(j)] / h))]
+          .push_back(j);
+  }
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const i64 id = ids[q];
+    const HbsNodeH& nd = nodes[size_t(id)];
+    const Region& rg = B.reg[size_t(id)];
+    const double rad = B.o.div_factor * rg.r0;
+    if (nd.is_leaf()) {
+      std::vector<i64> hits;
+      const long long gx = (long long)std::floor(rg.cx / h), gy = (long long)std::floor(rg.cy / h);
+      const long long span = (long long)std::ceil(rad / h) + 1;
+      for (long long a = gx - span; a <= gx + span; ++a)
+        for (long long b = gy - span; b <= gy + span; ++b) {
+          auto it = grid.find(key(a, b));
+          if (it == grid.end()) continue;
+          for (i64 j : it->second) {
+            if (j >= nd.begin && j < nd.end) continue;
+            const double dx = B.px[size_t(j)] - rg.cx, dy = B.py[size_t(j)] - rg.cy;
+            if (std::sqrt(dx * dx + dy * dy) <= rad) hits.push_back(j);
+          }
+        }
+      std::sort(hits.begin(), hits.end());
+      for (i64 j : hits) {
+        nc[q].push_back(2 * j);
+        nc[q].push_back(2 * j + 1);
+      }
+      nr[q] = nc[q];
+      continue;
+    }
+    for (i64 other : B.levels[size_t(nd.depth)]) {
+      if (other == id) continue;
+      const Region& org = B.reg[size_t(other)];
+      const double dx = org.cx - rg.cx, dy = org.cy - rg.cy;
+      if (std::sqrt(dx * dx + dy * dy) > rad + org.r0) continue;
+      const auto cc = B.col_cand(nodes[size_t(other)]);
+      const auto rc = B.row_cand(nodes[size_t(other)]);
+      nc[q].insert(nc[q].end(), cc.begin(), cc.end());
+      nr[q].insert(nr[q].end(), rc.begin(), rc.end());
+    }
+  }
+}
+
+// One sample-count round of W^T for every (node, row|col) problem.
+struct SampleRound {
+  DevBuf<double> wt;
+  std::vector<IdProblem> probs;  // 2 per node: row then col
+  IdBatch ids;
+};
+
+void build_round(Builder& B, const std::vector<i64>& ids, const std::vector<int>& ns_of,
+                 const std::vector<std::vector<i64>>& rcand, const std::vector<std::vector<i64>>& ccand,
+                 const std::vector<std::vector<i64>>& nc, const std::vector<std::vector<i64>>& nr,
+                 SampleRound& R) {
+  const int wn = B.has_null ? 1 : 0;
+  std::vector<i64> off;
+  i64 total = 0;
+  R.probs.clear();
+  for (size_t q = 0; q < ids.size(); ++q) {
+    for (int side = 0; side < 2; ++side) {
+      const int n = int(side == 0 ? rcand[q].size() : ccand[q].size());
+      const int M = 4 * ns_of[q] + wn + int(side == 0 ? nc[q].size() : nr[q].size());
+      off.push_back(total);
+      total += i64(M) * n;
+      R.probs.push_back({nullptr, M, n, std::max(M, 1)});
+    }
+  }
+  R.wt.resize(size_t(std::max<i64>(total, 1)));
+  for (size_t p = 0; p < R.probs.size(); ++p) R.probs[p].wt = R.wt.get() + off[p];
+  // index arrays: candidates and near lists, concatenated
+  std::vector<i64> cand, nearv;
+  std::vector<ProxyJob> pj;
+  std::vector<NearJob> nj;
+  int max_rows = 0, max_n = 0;
+  i64 max_near = 0;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const Region& rg = B.reg[size_t(ids[q])];
+    for (int side = 0; side < 2; ++side) {
+      const auto& cv = side == 0 ? rcand[q] : ccand[q];
+      const auto& nv = side == 0 ? nc[q] : nr[q];
+      const IdProblem& pr = R.probs[2 * q + size_t(side)];
+      const i64 coff = i64(cand.size());
+      cand.insert(cand.end(), cv.begin(), cv.end());
+      if (pr.n == 0) continue;
+      ProxyJob j{};
+      j.cand_off = coff;
+      j.n = pr.n;
+      j.ns = ns_of[q];
+      j.cx = rg.cx;
+      j.cy = rg.cy;
+      j.rad = B.o.bas_factor * rg.r0;
+      j.out_off = off[2 * q + size_t(side)];
+      j.ld = pr.lda;
+      j.kind = side;  // 0 outgoing rows, 1 incoming columns
+      j.with_null = wn;
+      pj.push_back(j);
+      max_rows = std::max(max_rows, j.ns);
+      max_n = std::max(max_n, j.n);
+      if (!nv.empty()) {
+        NearJob k{};
+        k.cand_off = coff;
+        k.near_off = i64(nearv.size());
+        k.n = pr.n;
+        k.n_near = int(nv.size());
+        k.out_off = off[2 * q + size_t(side)] + 4 * ns_of[q] + wn;
+        k.ld = pr.lda;
+        k.transpose = side;  // row ID: A(cand, near)^T ; col ID: A(near, cand)
+        nearv.insert(nearv.end(), nv.begin(), nv.end());
+        nj.push_back(k);
+        max_near = std::max<i64>(max_near, i64(k.n_near) * k.n);
+        B.max_block = std::max<i64>(B.max_block, i64(k.n_near) * k.n);
+      }
+    }
+  }
+  DevBuf<i64> dcand, dnear;
+  DevBuf<ProxyJob> dpj;
+  DevBuf<NearJob> dnj;
+  dcand.upload(cand, B.s);
+  dnear.upload(nearv, B.s);
+  dpj.upload(pj, B.s);
+  dnj.upload(nj, B.s);
+  launch_proxy_jobs(B.eo.view(), dpj.get(), int(pj.size()), max_rows, max_n, dcand.get(), R.wt.get(), B.s);
+  launch_near_jobs(B.eo.view(), dnj.get(), int(nj.size()), max_near, dcand.get(), dnear.get(),
+                   R.wt.get(), B.s);
+  R.ids.factor(R.probs, 1e-15, B.s);  // keeps every row the forced-rank rule can use
+}
+
+}  // namespace
+
+std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, double mu,
+                                           const i64* nodes, i64 n_nodes,
+                                           const HbsBuildOptions& o, cudaStream_t s) {
+  require(o.eps > 0.0 && o.eps <= 0.1, "hbs_compress: tolerance out of range");
+  require(o.leaf_nodes >= 2, "hbs_compress: leaf size too small");
+  const i64 N = nodes ? n_nodes : g.n_nodes();
+  require(N > 0, "hbs_compress: empty source");
+  DevBuf<i64> dmap;
+  if (nodes) {
+    for (i64 i = 0; i < N; ++i) require(nodes[i] >= 0 && nodes[i] < g.n_nodes(), "hbs_compress: node out of range");
+    dmap.upload(nodes, size_t(N), s);
+  }
+  EntryOracle eo(g, formulation, mu, s, nodes ? dmap.get() : nullptr);
+  auto op = std::make_unique<HbsOp>();
+  op->n = 2 * N;
+  op->leaf_nodes = o.leaf_nodes;
+  op->eps = o.eps;
+  Builder B{g, o, s, *op, eo, eo.has_nullspace(), {}, {}, {}, {}, 0};
+  B.px.resize(size_t(N));
+  B.py.resize(size_t(N));
+  for (i64 i = 0; i < N; ++i) {
+    const i64 nd = nodes ? nodes[i] : i;
+    B.px[size_t(i)] = g.x[size_t(nd)];
+    B.py[size_t(i)] = g.y[size_t(nd)];
+  }
+  // balanced BFS tree (hbs.cpp:360-384)
+  struct Pending {
+    i64 b, e, parent;
+    int depth;
+  };
+  std::vector<Pending> queue{{0, N, -1, 0}};
+  for (size_t qi = 0; qi < queue.size(); ++qi) {
+    const Pending p = queue[qi];
+    HbsNodeH nd;
+    nd.begin = p.b;
+    nd.end = p.e;
+    nd.parent = p.parent;
+    nd.depth = p.depth;
+    const i64 id = i64(op->nodes.size());
+    if (p.parent >= 0) {
+      HbsNodeH& par = op->nodes[size_t(p.parent)];
+      (par.left < 0 ? par.left : par.right) = id;
+    }
+    op->nodes.push_back(nd);
+    if (p.e - p.b > o.leaf_nodes) {
+      const i64 mid = p.b + (p.e - p.b) / 2;
+      queue.push_back({p.b, mid, id, p.depth + 1});
+      queue.push_back({mid, p.e, id, p.depth + 1});
+    }
+  }
+  const size_t nn = op->nodes.size();
+  int max_depth = 0;
+  B.reg.resize(nn);
+  for (size_t i = 0; i < nn; ++i) {  // node_region (hbs.cpp:107-117)
+    const auto& nd = op->nodes[i];
+    double sx = 0, sy = 0;
+    for (i64 j = nd.begin; j < nd.end; ++j) {
+      sx += B.px[size_t(j)];
+      sy += B.py[size_t(j)];
+    }
+    Region r;
+    r.cx = sx / double(nd.end - nd.begin);
+    r.cy = sy / double(nd.end - nd.begin);
+    for (i64 j = nd.begin; j < nd.end; ++j) {
+      const double dx = B.px[size_t(j)] - r.cx, dy = B.py[size_t(j)] - r.cy;
+      r.r0 = std::max(r.r0, std::sqrt(dx * dx + dy * dy));
+    }
+    r.r0 = std::max(r.r0, 1e-12);
+    B.reg[i] = r;
+    max_depth = std::max(max_depth, nd.depth);
+  }
+  B.levels.assign(size_t(max_depth + 1), {});
+  for (size_t i = 0; i < nn; ++i) B.levels[size_t(op->nodes[i].depth)].push_back(i64(i));
+
+  // leaf diagonal blocks
+  std::vector<i64> leaf_ids;
+  for (size_t i = 0; i < nn; ++i)
+    if (op->nodes[i].is_leaf()) leaf_ids.push_back(i64(i));
+  std::vector<i64> d_off(nn, -1);
+  DevBuf<double> dstore;
+  {
+    std::vector<i64> idx;
+    std::vector<BlockJob> jobs;
+    i64 tot = 0, mx = 0;
+    for (i64 id : leaf_ids) {
+      const auto& nd = op->nodes[size_t(id)];
+      const int c = int(2 * (nd.end - nd.begin));
+      BlockJob j{};
+      j.row_off = i64(idx.size());
+      j.col_off = i64(idx.size());
+      j.nr = c;
+      j.nc = c;
+      j.out_off = tot;
+      j.ld = c;
+      d_off[size_t(id)] = tot;
+      tot += i64(c) * c;
+      mx = std::max<i64>(mx, i64(c) * c);
+      B.max_block = std::max<i64>(B.max_block, i64(c) * c);
+      for (i64 q = 2 * nd.begin; q < 2 * nd.end; ++q) idx.push_back(q);
+      jobs.push_back(j);
+    }
+    dstore.resize(size_t(std::max<i64>(tot, 1)));
+    DevBuf<i64> didx;
+    DevBuf<BlockJob> djobs;
+    didx.upload(idx, s);
+    djobs.upload(jobs, s);
+    launch_block_jobs(eo.view(), djobs.get(), int(jobs.size()), mx, didx.get(), didx.get(),
+                      dstore.get(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+
+  // bottom-up skeletonisation; the root keeps no factors (hbs.cpp:411-421)
+  std::vector<std::unique_ptr<LevelStore>> stores(static_cast<size_t>(max_depth + 1));
+  std::vector<i64> pos_in_level(nn, 0);
+  for (int depth = max_depth; depth >= 1; --depth) {
+    const auto& ids = B.levels[size_t(depth)];
+    const size_t L = ids.size();
+    for (size_t q = 0; q < L; ++q) pos_in_level[size_t(ids[q])] = i64(q);
+    std::vector<std::vector<i64>> rc(L), cc(L), nc, nr;
+    for (size_t q = 0; q < L; ++q) {
+      rc[q] = B.row_cand(op->nodes[size_t(ids[q])]);
+      cc[q] = B.col_cand(op->nodes[size_t(ids[q])]);
+    }
+    near_sets(B, ids, nc, nr);
+    for (size_t q = 0; q < L; ++q) {
+      B.max_block = std::max<i64>(B.max_block, i64(rc[q].size()) * i64(nc[q].size()));
+      B.max_block = std::max<i64>(B.max_block, i64(nr[q].size()) * i64(cc[q].size()));
+    }
+    // sample doubling until the rank settles within 2 (hbs.cpp:198-213)
+    std::vector<std::unique_ptr<SampleRound>> rounds;
+    std::vector<int> row_round(L, -1), col_round(L, -1);   // round holding the final sample
+    std::vector<size_t> row_pi(L, 0), col_pi(L, 0);        // problem index inside that round
+    std::vector<i64> prev_kr(L, -1), prev_kc(L, -1);
+    std::vector<char> row_done(L, 0), col_done(L, 0);
+    std::vector<size_t> active(L);
+    for (size_t q = 0; q < L; ++q) active[q] = q;
+    for (int ns = 64; ns <= 2048 && !active.empty(); ns *= 2) {
+      std::vector<i64> aid;
+      std::vector<int> ans;
+      std::vector<std::vector<i64>> arc, acc, anc, anr;
+      for (size_t q : active) {
+        aid.push_back(ids[q]);
+        ans.push_back(ns);
+        arc.push_back(rc[q]);
+        acc.push_back(cc[q]);
+        anc.push_back(nc[q]);
+        anr.push_back(nr[q]);
+      }
+      auto R = std::make_unique<SampleRound>();
+      build_round(B, aid, ans, arc, acc, anc, anr, *R);
+      const int ridx = int(rounds.size());
+      std::vector<size_t> next;
+      for (size_t a = 0; a < active.size(); ++a) {
+        const size_t q = active[a];
+        const i64 kr = R->ids.eps_rank(2 * a, o.eps), kc = R->ids.eps_rank(2 * a + 1, o.eps);
+        if (!row_done[q]) {
+          const bool settled = prev_kr[q] >= 0 && std::llabs(kr - prev_kr[q]) <= 2;
+          row_round[q] = ridx;
+          row_pi[q] = 2 * a;
+          prev_kr[q] = kr;
+          if (settled) row_done[q] = 1;
+        }
+        if (!col_done[q]) {
+          const bool settled = prev_kc[q] >= 0 && std::llabs(kc - prev_kc[q]) <= 2;
+          col_round[q] = ridx;
+          col_pi[q] = 2 * a + 1;
+          prev_kc[q] = kc;
+          if (settled) col_done[q] = 1;
+        }
+        if (!row_done[q] || !col_done[q]) next.push_back(q);
+      }
+      rounds.push_back(std::move(R));
+      // keep only problems still needed: a finished side is not recomputed
+      // but its node stays in the batch while the other side is active
+      active = next;
+    }
+    for (size_t q = 0; q < L; ++q) {
+      if (!row_done[q]) op->notes.push_back("hbs row: proxy sample cap reached");
+      if (!col_done[q]) op->notes.push_back("hbs col: proxy sample cap reached");
+    }
+    // rank equalisation (hbs.cpp:309-314)
+    std::vector<i64> kfin(L);
+    for (size_t q = 0; q < L; ++q) {
+      const IdBatch& RB = rounds[size_t(row_round[q])]->ids;
+      const IdBatch& CB = rounds[size_t(col_round[q])]->ids;
+      i64 kr = RB.eps_rank(row_pi[q], o.eps), kc = CB.eps_rank(col_pi[q], o.eps);
+      i64 k = std::max(kr, kc);
+      if (kr < k) kr = RB.forced_rank(row_pi[q], k);
+      if (kc < k) kc = CB.forced_rank(col_pi[q], k);
+      k = std::min(kr, kc);
+      kfin[q] = k;
+    }
+    // interpolation matrices u (row) and v (col), c x k each, then b_sib
+    auto st = std::make_unique<LevelStore>();
+    st->o_u.resize(L);
+    st->o_v.resize(L);
+    st->o_b.resize(L);
+    i64 tot = 0;
+    for (size_t q = 0; q < L; ++q) {
+      const i64 c = i64(rc[q].size());
+      st->o_u[q] = tot;
+      tot += c * kfin[q];
+      st->o_v[q] = tot;
+      tot += i64(cc[q].size()) * kfin[q];
+    }
+    for (size_t q = 0; q < L; ++q) {  // b_sib sizes need the sibling's k
+      const i64 id = ids[q];
+      const i64 sib = op->sib(id);
+      st->o_b[q] = tot;
+      tot += kfin[q] * kfin[size_t(pos_in_level[size_t(sib)])];
+    }
+    st->buf.resize(size_t(std::max<i64>(tot, 1)));
+    for (size_t r = 0; r < rounds.size(); ++r) {
+      std::vector<i64> ks(rounds[r]->probs.size(), 0);
+      std::vector<double*> P(ks.size(), nullptr);
+      std::vector<int> ldp(ks.size(), 1);
+      for (size_t q = 0; q < L; ++q) {
+        if (row_round[q] == int(r)) {
+          ks[row_pi[q]] = kfin[q];
+          P[row_pi[q]] = st->buf.get() + st->o_u[q];
+          ldp[row_pi[q]] = std::max<int>(1, int(rc[q].size()));
+        }
+        if (col_round[q] == int(r)) {
+          ks[col_pi[q]] = kfin[q];
+          P[col_pi[q]] = st->buf.get() + st->o_v[q];
+          ldp[col_pi[q]] = std::max<int>(1, int(cc[q].size()));
+        }
+      }
+      rounds[r]->ids.interp(ks, P, ldp, s);
+    }
+    for (size_t q = 0; q < L; ++q) {
+      HbsNodeH& nd = op->nodes[size_t(ids[q])];
+      const IdBatch& RB = rounds[size_t(row_round[q])]->ids;
+      const IdBatch& CB = rounds[size_t(col_round[q])]->ids;
+      nd.k = kfin[q];
+      nd.row_skel.resize(size_t(nd.k));
+      nd.col_skel.resize(size_t(nd.k));
+      for (i64 i = 0; i < nd.k; ++i) {
+        nd.row_skel[size_t(i)] = rc[q][size_t(RB.perm(row_pi[q])[size_t(i)])];
+        nd.col_skel[size_t(i)] = cc[q][size_t(CB.perm(col_pi[q])[size_t(i)])];
+      }
+      if (nd.k == i64(rc[q].size()))
+        op->notes.push_back("node [" + std::to_string(nd.begin) + "," + std::to_string(nd.end) +
+                            ") kept at full rank (stored dense)");
+    }
+    {  // b_sib = entries(row_skel, sibling col_skel)
+      std::vector<i64> ri, ci;
+      std::vector<BlockJob> jobs;
+      i64 mx = 0;
+      for (size_t q = 0; q < L; ++q) {
+        const auto& nd = op->nodes[size_t(ids[q])];
+        const auto& sb = op->nodes[size_t(op->sib(ids[q]))];
+        BlockJob j{};
+        j.row_off = i64(ri.size());
+        j.col_off = i64(ci.size());
+        j.nr = int(nd.k);
+        j.nc = int(sb.k);
+        j.out_off = st->o_b[q];
+        j.ld = std::max<int>(1, int(nd.k));
+        ri.insert(ri.end(), nd.row_skel.begin(), nd.row_skel.end());
+        ci.insert(ci.end(), sb.col_skel.begin(), sb.col_skel.end());
+        mx = std::max<i64>(mx, i64(j.nr) * j.nc);
+        B.max_block = std::max<i64>(B.max_block, i64(j.nr) * j.nc);
+        jobs.push_back(j);
+      }
+      DevBuf<i64> dri, dci;
+      DevBuf<BlockJob> dj;
+      dri.upload(ri, s);
+      dci.upload(ci, s);
+      dj.upload(jobs, s);
+      launch_block_jobs(eo.view(), dj.get(), int(jobs.size()), mx, dri.get(), dci.get(),
+                        st->buf.get(), s);
+      SBX_CUDA(cudaStreamSynchronize(s));
+    }
+    stores[size_t(depth)] = std::move(st);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+  op->max_block_drawn = B.max_block;
+  // final arena: layout by ranks, then place u, v, v^T, d, b_sib
+  hbs_layout(*op);
+  std::vector<CopyJob> cj;
+  double* A = op->arena.get();
+  for (size_t i = 0; i < nn; ++i) {
+    const auto& nd = op->nodes[i];
+    const int k = int(nd.k), c = int(nd.c);
+    if (nd.is_leaf()) {  // d below v^T in vd
+      const int vld = (i == 0) ? c : k + c;
+      cj.push_back({dstore.get() + d_off[i], A + nd.o_vd + (i == 0 ? 0 : k), c, c, c, vld, 0, 0});
+    }
+    if (i == 0) continue;
+    const LevelStore& st = *stores[size_t(nd.depth)];
+    const size_t q = size_t(pos_in_level[i]);
+    const double* u = st.buf.get() + st.o_u[q];
+    const double* v = st.buf.get() + st.o_v[q];
+    if (k > 0 && c > 0) {
+      cj.push_back({u, A + nd.o_u, c, k, c, c, 0, 0});
+      cj.push_back({v, A + nd.o_v, c, k, c, c, 0, 0});
+      const int vld = k + (nd.is_leaf() ? c : 0);
+      cj.push_back({v, A + nd.o_vd, k, c, c, vld, 1, 0});
+    }
+    const i64 ks = op->nodes[size_t(op->sib(i64(i)))].k;
+    if (k > 0 && ks > 0) cj.push_back({st.buf.get() + st.o_b[q], A + nd.o_b, k, int(ks), k, k, 0, 0});
+  }
+  copy_batched(cj, s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  op->has_apply = true;
+  return op;
+}
+
+// ---------------------------------------------------------------- inverse
+void hbs_invert_device(HbsOp& op, cudaStream_t s) {
+  require(!op.nodes.empty(), "hbs_invert: empty operator");
+  require(op.has_apply, "hbs_invert: operator has no forward factors");
+  const double thr = std::max(std::min(10.0 * op.eps, 1e-6), 1e-14);  // hbs.cpp:429
+  double* A = op.arena.get();
+  const size_t nn = op.nodes.size();
+  for (int depth = op.max_depth; depth >= 0; --depth) {
+    std::vector<size_t> ids;
+    for (size_t i = 0; i < nn; ++i)
+      if (op.nodes[i].depth == depth) ids.push_back(i);
+    // x blocks and scratch
+    std::vector<i64> xo(ids.size()), io(ids.size()), to(ids.size()), tuo(ids.size()), xuo(ids.size());
+    i64 tot = 0;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const i64 c = nd.c, k = nd.k;
+      xo[q] = tot;
+      tot += c * c;
+      io[q] = tot;
+      tot += c * c;
+      to[q] = tot;
+      tot += k * c;
+      tuo[q] = tot;
+      tot += k * k;
+      xuo[q] = tot;
+      tot += c * k;
+    }
+    DevBuf<double> scr(static_cast<size_t>(std::max<i64>(tot, 1)));
+    double* S = scr.get();
+    std::vector<CopyJob> cj;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const int c = int(nd.c);
+      double* x = S + xo[q];
+      if (nd.is_leaf()) {
+        const int vld = ids[q] == 0 ? c : int(nd.k) + c;
+        cj.push_back({A + nd.o_vd + (ids[q] == 0 ? 0 : nd.k), x, c, c, vld, c, 0, 0});
+      } else {
+        const auto& l = op.nodes[size_t(nd.left)];
+        const auto& r = op.nodes[size_t(nd.right)];
+        const int kl = int(l.k), kr = int(r.k);
+        if (kl) cj.push_back({A + l.o_dhat, x, kl, kl, kl, c, 0, 0});
+        if (kl && kr) cj.push_back({A + l.o_b, x + size_t(kl) * c, kl, kr, kl, c, 0, 0});
+        if (kl && kr) cj.push_back({A + r.o_b, x + kl, kr, kl, kr, c, 0, 0});
+        if (kr) cj.push_back({A + r.o_dhat, x + kl + size_t(kl) * c, kr, kr, kr, c, 0, 0});
+      }
+    }
+    copy_batched(cj, s);
+    DevBuf<int> piv(static_cast<size_t>(std::max<i64>(tot, 1)));
+    DevBuf<double> rc(ids.size() * 2 + 1), work;
+    i64 wtot = 0;
+    for (size_t q = 0; q < ids.size(); ++q) wtot += 4 * (op.nodes[ids[q]].c + op.nodes[ids[q]].k);
+    work.resize(size_t(std::max<i64>(wtot, 1)));
+    // LU + inverse + rcond of x
+    std::vector<LuJob> lj;
+    i64 pw = 0;
+    std::vector<size_t> lj_node;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      if (nd.c == 0) continue;
+      LuJob j{};
+      j.a = S + xo[q];
+      j.n = int(nd.c);
+      j.lda = int(nd.c);
+      j.piv = piv.get() + xo[q];
+      j.inv = ids[q] == 0 ? A + op.o_root_g : S + io[q];
+      j.rcond = rc.get() + 2 * q;
+      j.work = work.get() + pw;
+      pw += 4 * nd.c;
+      lj.push_back(j);
+      lj_node.push_back(q);
+    }
+    lu_batched(lj, s);
+    std::vector<double> hrc(ids.size() * 2 + 1, 1.0);
+    rc.download(hrc.data(), hrc.size(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    for (size_t q : lj_node) {
+      const auto& nd = op.nodes[ids[q]];
+      const double r = hrc[2 * q];
+      if (!(r >= thr))
+        throw Error(4, std::string("singular ") + (ids[q] == 0 ? "root" : "diagonal") +
+                           " block (rcond " + std::to_string(r) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
+    if (depth == 0) break;  // the root keeps only root_g (hbs.cpp:450-458)
+    // t = v^T xi (k x c), tu = t u (k x k)
+    std::vector<GemmJob> g1, g2;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const int c = int(nd.c), k = int(nd.k);
+      if (c == 0 || k == 0) continue;
+      g1.push_back({A + nd.o_v, S + io[q], S + to[q], k, c, c, c, c, k, 1, 0, 1.0, 0.0});
+      g1.push_back({S + io[q], A + nd.o_u, S + xuo[q], c, k, c, c, c, c, 0, 0, 1.0, 0.0});
+    }
+    gemm_batched(g1, s);
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const int c = int(nd.c), k = int(nd.k);
+      if (c == 0 || k == 0) continue;
+      g2.push_back({S + to[q], A + nd.o_u, S + tuo[q], k, k, c, k, c, k, 0, 0, 1.0, 0.0});
+    }
+    gemm_batched(g2, s);
+    std::vector<LuJob> lj2;
+    std::vector<size_t> lj2_node;
+    pw = 0;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      if (nd.c == 0 || nd.k == 0) continue;
+      LuJob j{};
+      j.a = S + tuo[q];
+      j.n = int(nd.k);
+      j.lda = int(nd.k);
+      j.piv = piv.get() + xo[q];
+      j.inv = A + nd.o_dhat;
+      j.rcond = rc.get() + 2 * q + 1;
+      j.work = work.get() + pw;
+      pw += 4 * nd.k;
+      lj2.push_back(j);
+      lj2_node.push_back(q);
+    }
+    lu_batched(lj2, s);
+    rc.download(hrc.data(), hrc.size(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    for (size_t q : lj2_node) {
+      const auto& nd = op.nodes[ids[q]];
+      const double r = hrc[2 * q + 1];
+      if (!(r >= thr))
+        throw Error(4, "singular skeleton block (rcond " + std::to_string(r) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
+    // e = (xi u) dhat, f = dhat t, g = xi - e t   (hbs.cpp:480-483)
+    std::vector<GemmJob> g3, g4;
+    std::vector<CopyJob> cg;
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const int c = int(nd.c), k = int(nd.k);
+      if (c == 0) continue;
+      double* fg = A + nd.o_fg;  // (k + c) x c, f rows then g rows
+      const int ld = k + c;
+      cg.push_back({S + io[q], fg + k, c, c, c, ld, 0, 0});  // g <- xi
+      if (k == 0) continue;
+      g3.push_back({S + xuo[q], A + nd.o_dhat, A + nd.o_e, c, k, k, c, k, c, 0, 0, 1.0, 0.0});
+      g3.push_back({A + nd.o_dhat, S + to[q], fg, k, c, k, k, k, ld, 0, 0, 1.0, 0.0});
+    }
+    copy_batched(cg, s);
+    gemm_batched(g3, s);
+    for (size_t q = 0; q < ids.size(); ++q) {
+      const auto& nd = op.nodes[ids[q]];
+      const int c = int(nd.c), k = int(nd.k);
+      if (c == 0 || k == 0) continue;
+      g4.push_back({A + nd.o_e, S + to[q], A + nd.o_fg + k, c, c, k, c, k, k + c, 0, 0, -1.0, 1.0});
+    }
+    gemm_batched(g4, s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+  op.has_inverse = true;
+  op.solve_plan.built = false;
+}
+
+}  // namespace sbx

@@ -1,0 +1,35 @@
+// Device HBS compression and telescoping inversion (north-star
+// subsystem 4, reference hbs.cpp:349-487), timed separately from the
+// per-step path.
+#pragma once
+
+#include "geometry.hpp"
+#include "hbs.hpp"
+#include "sbx.h"
+
+namespace sbx {
+
+struct HbsBuildOptions {
+  double eps = 1e-10;
+  i64 leaf_nodes = 64;
+  double bas_factor = 1.5;
+  double div_factor = 3.0;
+  static HbsBuildOptions from(const sbx_hbs_options& o) {
+    HbsBuildOptions b;
+    b.eps = o.eps;
+    b.leaf_nodes = o.leaf_nodes;
+    b.bas_factor = o.bas_factor;
+    b.div_factor = o.div_factor;
+    return b;
+  }
+};
+
+// Compress the operator of (g, formulation, mu) restricted to `nodes`
+// (global node ids, make_hbs_source_subset) or the whole discretization.
+std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, double mu,
+                                           const i64* nodes, i64 n_nodes,
+                                           const HbsBuildOptions& o, cudaStream_t s);
+
+void hbs_invert_device(HbsOp& op, cudaStream_t s);
+
+}  // namespace sbx

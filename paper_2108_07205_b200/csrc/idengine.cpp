@@ -1,0 +1,115 @@
+// Batched device IDs (see idengine.hpp).
+#include "idengine.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace sbx {
+
+void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s) {
+  probs_ = probs;
+  const size_t np = probs.size();
+  perm_off_.assign(np + 1, 0);
+  std::vector<i64> diag_off(np + 1, 0);
+  for (size_t p = 0; p < np; ++p) {
+    perm_off_[p + 1] = perm_off_[p] + probs[p].n;
+    diag_off[p + 1] = diag_off[p] + std::min(probs[p].M, probs[p].n);
+  }
+  d_perm_.reserve(size_t(std::max<i64>(perm_off_[np], 1)));
+  d_diag_.reserve(size_t(std::max<i64>(diag_off[np], 1)));
+  d_steps_.reserve(std::max<size_t>(np, 1));
+  std::vector<QrJob> jobs, big;
+  coop_.assign(np, 0);
+  for (size_t p = 0; p < np; ++p) {
+    const auto& pr = probs[p];
+    if (pr.M == 0 || pr.n == 0) continue;
+    QrJob j{};
+    j.a = pr.wt;
+    j.M = pr.M;
+    j.n = pr.n;
+    j.lda = pr.lda;
+    j.pivot = 1;
+    j.max_steps = 0;
+    j.stop_eps = stop_eps;
+    j.perm = d_perm_.get() + perm_off_[p];
+    j.diag = d_diag_.get() + diag_off[p];
+    j.steps = d_steps_.get() + p;
+    // one CTA per problem unless the factorisation would stream megabytes
+    // through a single SM; those go to the cooperative multi-CTA kernel
+    if (i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows) {
+      coop_[p] = 1;
+      big.push_back(j);
+    } else {
+      jobs.push_back(j);
+    }
+  }
+  qr_batched(jobs, s);
+  cpqr_coop_batched(big, s);
+  std::vector<int> hperm(static_cast<size_t>(perm_off_[np]));
+  std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
+  if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);
+  if (!hdiag.empty()) d_diag_.download(hdiag.data(), hdiag.size(), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  diag_.assign(np, {});
+  perm_.assign(np, {});
+  for (size_t p = 0; p < np; ++p) {
+    const auto& pr = probs[p];
+    if (pr.M == 0 || pr.n == 0) {
+      perm_[p].resize(size_t(pr.n));
+      for (int i = 0; i < pr.n; ++i) perm_[p][size_t(i)] = i;
+      continue;
+    }
+    perm_[p].assign(hperm.begin() + perm_off_[p], hperm.begin() + perm_off_[p + 1]);
+    diag_[p].assign(hdiag.begin() + diag_off[p], hdiag.begin() + diag_off[p + 1]);
+  }
+}
+
+i64 IdBatch::eps_rank(size_t p, double eps) const {
+  const auto& d = diag_[p];
+  if (d.empty()) return 0;
+  const double r00 = d[0];
+  i64 k = 0;
+  if (r00 > 0.0)
+    while (k < i64(d.size()) && d[size_t(k)] > eps * r00) ++k;
+  return k;
+}
+
+i64 IdBatch::forced_rank(size_t p, i64 kf) const {
+  const auto& d = diag_[p];
+  if (d.empty() || kf <= 0) return 0;
+  const double r00 = d[0];
+  i64 k = 0;
+  while (k < std::min<i64>(kf, i64(d.size())) && d[size_t(k)] > 1e-15 * r00) ++k;
+  return k;
+}
+
+void IdBatch::interp(const std::vector<i64>& ks, const std::vector<double*>& P,
+                     const std::vector<int>& ldp, cudaStream_t s) {
+  std::vector<InterpJob> jobs;
+  std::vector<i64> toff;
+  i64 tsz = 0;
+  for (size_t p = 0; p < probs_.size(); ++p) {
+    toff.push_back(tsz);
+    const i64 k = ks[p];
+    if (k > 0) tsz += k * (probs_[p].n - k);
+  }
+  d_T_.reserve(size_t(std::max<i64>(tsz, 1)));
+  for (size_t p = 0; p < probs_.size(); ++p) {
+    const i64 k = ks[p];
+    if (k <= 0) continue;
+    InterpJob j{};
+    j.a = probs_[p].wt;
+    j.lda = probs_[p].lda;
+    j.n = probs_[p].n;
+    j.k = int(k);
+    j.perm = d_perm_.get() + perm_off_[p];
+    j.colmap = coop_[p] ? j.perm : nullptr;
+    j.P = P[p];
+    j.ldp = ldp[p];
+    j.T = d_T_.get() + toff[p];
+    jobs.push_back(j);
+  }
+  interp_batched(jobs, s);
+}
+
+}  // namespace sbx

@@ -1,0 +1,50 @@
+// Batched interpolative decompositions on the device (reference
+// idlib.cpp:27-99).  Each problem is a row ID of W given as W^T (M x n,
+// column-major, device resident): CPQR of W^T (dense.cu qr_kernel), rank by
+// the reference's rules, then P = [I; R11^{-1} R12] scattered by the pivots.
+#pragma once
+
+#include <vector>
+
+#include "common.hpp"
+#include "dense.hpp"
+
+namespace sbx {
+
+struct IdProblem {
+  double* wt;  // W^T, factored in place
+  int M, n, lda;
+};
+
+class IdBatch {
+ public:
+  // CPQR of every problem; stop_eps truncates at |r_jj| <= stop_eps*|r_00|
+  // (1e-15 keeps every row the forced-rank rule can ask for).
+  void factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s);
+  size_t size() const { return probs_.size(); }
+  const IdProblem& problem(size_t p) const { return probs_[p]; }
+  // idlib.cpp:47-51: #{ |r_kk| > eps |r_00| }
+  i64 eps_rank(size_t p, double eps) const;
+  // idlib.cpp:38-45: min(k, dmax) cut at 1e-15 |r_00|
+  i64 forced_rank(size_t p, i64 k) const;
+  const std::vector<int>& perm(size_t p) const { return perm_[p]; }
+  // Writes P_p (n_p x k_p, column-major, ldp) for every problem with k_p > 0.
+  void interp(const std::vector<i64>& ks, const std::vector<double*>& P,
+              const std::vector<int>& ldp, cudaStream_t s);
+
+  static constexpr i64 kCoopEntries = i64(1) << 18;  // 2 MB of W^T
+  static constexpr int kCoopMaxRows = 16384;         // Householder vector in smem
+
+ private:
+  std::vector<char> coop_;
+  std::vector<IdProblem> probs_;
+  std::vector<std::vector<double>> diag_;
+  std::vector<std::vector<int>> perm_;
+  std::vector<i64> perm_off_;
+  DevBuf<int> d_perm_;
+  DevBuf<double> d_diag_;
+  DevBuf<int> d_steps_;
+  DevBuf<double> d_T_;
+};
+
+}  // namespace sbx

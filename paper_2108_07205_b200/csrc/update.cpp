@@ -1,0 +1,646 @@
+// Device two-step ID update compression (reference lowrank.cpp:253-327 with
+// proxy.cpp:46-302 and idlib.cpp).  Host code keeps the index bookkeeping
+// (far/near split, partition trees, skeleton lists); W^T assembly, CPQR,
+// interpolation, the hierarchical merges (DMMA GEMMs) and the R blocks run
+// on the device.
+//
+// The final randomized_row_id of the stacked factor L1 (idlib.cpp:101-132)
+// is evaluated as the deterministic row ID of L1: the reference's own
+// comment (idlib.cpp:115-118) notes that its Gaussian sketch is reduced to an
+// exact orthogonal rotation G of the row space, which leaves row norms,
+// angles and the eps-rank rule unchanged, so CPQR((L1 G)^T) and CPQR(L1^T)
+// select the same pivots and interpolation matrix in exact arithmetic.
+#include "update.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <numeric>
+#include <set>
+
+#include "dense.hpp"
+#include "entries.hpp"
+#include "idengine.hpp"
+
+namespace sbx {
+
+namespace {
+
+struct RowIdResult {
+  i64 m = 0, k = 0;
+  std::vector<i64> J;  // skeleton first
+  DevBuf<double> P;    // m x k
+};
+
+// Fills W^T for each candidate list (row ids of the implied W) into buf.
+using WtBuilder = std::function<void(const std::vector<std::vector<i64>>&, std::vector<IdProblem>&,
+                                     DevBuf<double>&)>;
+
+struct Chunk {
+  std::vector<i64> rows, skel;
+  const double* P = nullptr;  // |rows| x k (column-major)
+  i64 k = 0;
+};
+
+// hierarchical_row_id (proxy.cpp:193-247) / chunked near_row_id
+// (lowrank.cpp:76-124): leaf IDs, then pairwise merges of skeleton rows.
+RowIdResult hierarchical_id(i64 m, const std::vector<std::vector<i64>>& leaves,
+                            const WtBuilder& build, double eps, cudaStream_t s) {
+  std::vector<std::unique_ptr<DevBuf<double>>> keep;
+  std::vector<Chunk> level;
+  {
+    std::vector<IdProblem> probs;
+    auto buf = std::make_unique<DevBuf<double>>();
+    build(leaves, probs, *buf);
+    IdBatch ids;
+    ids.factor(probs, eps, s);
+    auto pb = std::make_unique<DevBuf<double>>();
+    std::vector<i64> ks(leaves.size()), off(leaves.size());
+    i64 tot = 0;
+    for (size_t q = 0; q < leaves.size(); ++q) {
+      ks[q] = ids.eps_rank(q, eps);
+      off[q] = tot;
+      tot += i64(leaves[q].size()) * ks[q];
+    }
+    pb->resize(size_t(std::max<i64>(tot, 1)));
+    std::vector<double*> P(leaves.size());
+    std::vector<int> ldp(leaves.size());
+    for (size_t q = 0; q < leaves.size(); ++q) {
+      P[q] = pb->get() + off[q];
+      ldp[q] = std::max<int>(1, int(leaves[q].size()));
+    }
+    ids.interp(ks, P, ldp, s);
+    for (size_t q = 0; q < leaves.size(); ++q) {
+      Chunk c;
+      c.rows = leaves[q];
+      c.k = ks[q];
+      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(leaves[q][size_t(ids.perm(q)[size_t(i)])]);
+      c.P = P[q];
+      level.push_back(std::move(c));
+    }
+    SBX_CUDA(cudaStreamSynchronize(s));
+    keep.push_back(std::move(buf));
+    keep.push_back(std::move(pb));
+  }
+  while (level.size() > 1) {
+    const size_t npair = level.size() / 2;
+    std::vector<std::vector<i64>> unis(npair);
+    for (size_t q = 0; q < npair; ++q) {
+      unis[q] = level[2 * q].skel;
+      unis[q].insert(unis[q].end(), level[2 * q + 1].skel.begin(), level[2 * q + 1].skel.end());
+    }
+    std::vector<IdProblem> probs;
+    auto buf = std::make_unique<DevBuf<double>>();
+    build(unis, probs, *buf);
+    IdBatch ids;
+    ids.factor(probs, eps, s);
+    std::vector<i64> ks(npair), ioff(npair), poff(npair);
+    i64 itot = 0, ptot = 0;
+    for (size_t q = 0; q < npair; ++q) {
+      ks[q] = ids.eps_rank(q, eps);
+      ioff[q] = itot;
+      itot += i64(unis[q].size()) * ks[q];
+      poff[q] = ptot;
+      ptot += i64(level[2 * q].rows.size() + level[2 * q + 1].rows.size()) * ks[q];
+    }
+    auto ib = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(itot, 1)));
+    auto pb = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(ptot, 1)));
+    std::vector<double*> IP(npair);
+    std::vector<int> ldi(npair);
+    for (size_t q = 0; q < npair; ++q) {
+      IP[q] = ib->get() + ioff[q];
+      ldi[q] = std::max<int>(1, int(unis[q].size()));
+    }
+    ids.interp(ks, IP, ldi, s);
+    std::vector<GemmJob> gj;
+    std::vector<Chunk> next;
+    for (size_t q = 0; q < npair; ++q) {
+      const Chunk& a = level[2 * q];
+      const Chunk& b = level[2 * q + 1];
+      Chunk c;
+      c.rows = a.rows;
+      c.rows.insert(c.rows.end(), b.rows.begin(), b.rows.end());
+      c.k = ks[q];
+      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(unis[q][size_t(ids.perm(q)[size_t(i)])]);
+      double* P = pb->get() + poff[q];
+      c.P = P;
+      const int ra = int(a.rows.size()), rb = int(b.rows.size()), ld = ra + rb;
+      const int ka = int(a.skel.size()), kb = int(b.skel.size()), k = int(c.k);
+      if (k > 0) {
+        // out.P = [a.P * id.P(0:ka, :); b.P * id.P(ka:, :)]  (proxy.cpp:187-189)
+        if (ka > 0)
+          gj.push_back({a.P, IP[q], P, ra, k, ka, std::max(ra, 1), ldi[q], ld, 0, 0, 1.0, 0.0});
+        if (kb > 0)
+          gj.push_back({b.P, IP[q] + ka, P + ra, rb, k, kb, std::max(rb, 1), ldi[q], ld, 0, 0, 1.0, 0.0});
+        if (ka == 0 || kb == 0) SBX_CUDA(cudaMemsetAsync(P, 0, size_t(ld) * k * 8, s));
+      }
+      next.push_back(std::move(c));
+    }
+    // zero-fill above must precede the products of the same chunk
+    gemm_batched(gj, s);
+    if (level.size() % 2 == 1) next.push_back(level.back());
+    level = std::move(next);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    keep.push_back(std::move(buf));
+    keep.push_back(std::move(ib));
+    keep.push_back(std::move(pb));
+  }
+  RowIdResult out;
+  out.m = m;
+  if (level.empty()) {
+    out.J.resize(size_t(m));
+    std::iota(out.J.begin(), out.J.end(), i64(0));
+    return out;
+  }
+  const Chunk& root = level.front();
+  out.k = root.k;
+  out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
+  if (out.k > 0) {
+    SBX_CUDA(cudaMemsetAsync(out.P.get(), 0, size_t(m * out.k) * 8, s));
+    DevBuf<i64> map;
+    map.upload(root.rows, s);
+    scatter_batched({{root.P, out.P.get(), map.get(), int(root.rows.size()), int(out.k),
+                      std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0}},
+                    s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+  out.J = root.skel;
+  std::vector<char> in(static_cast<size_t>(m), 0);
+  for (i64 x : root.skel) in[size_t(x)] = 1;
+  for (i64 x : root.rows)
+    if (!in[size_t(x)]) out.J.push_back(x);
+  return out;
+}
+
+// Direct row ID of one implicitly built W (row_id(eval(all rows))).
+RowIdResult direct_id(i64 m, const WtBuilder& build, double eps, cudaStream_t s) {
+  std::vector<std::vector<i64>> one(1);
+  one[0].resize(size_t(m));
+  std::iota(one[0].begin(), one[0].end(), i64(0));
+  std::vector<IdProblem> probs;
+  DevBuf<double> buf;
+  build(one, probs, buf);
+  IdBatch ids;
+  ids.factor(probs, eps, s);
+  RowIdResult out;
+  out.m = m;
+  out.k = ids.eps_rank(0, eps);
+  out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
+  if (out.k > 0) ids.interp({out.k}, {out.P.get()}, {std::max<int>(1, int(m))}, s);
+  out.J.assign(ids.perm(0).begin(), ids.perm(0).end());
+  SBX_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
+// W^T builder for the proxy interaction (proxy.cpp:136-162): rows of W are
+// scalars 2p+c of the point list `nodes` (global ids in g); columns are four
+// per circle sample plus the completion column.
+WtBuilder proxy_builder(const EntryView& v, const std::vector<i64>& nodes,
+                        const std::vector<ProxyCircleH>& circles, double factor, int ns, bool with_null,
+                        cudaStream_t s) {
+  return [&v, &nodes, &circles, factor, ns, with_null, s](
+             const std::vector<std::vector<i64>>& lists, std::vector<IdProblem>& probs,
+             DevBuf<double>& buf) {
+    const int nc = int(circles.size());
+    const int M = 4 * ns * nc + (with_null ? 1 : 0);
+    std::vector<i64> off;
+    i64 tot = 0;
+    probs.clear();
+    for (const auto& l : lists) {
+      off.push_back(tot);
+      tot += i64(M) * i64(l.size());
+      probs.push_back({nullptr, M, int(l.size()), std::max(M, 1)});
+    }
+    buf.resize(size_t(std::max<i64>(tot, 1)));
+    std::vector<i64> cand;
+    std::vector<ProxyJob> jobs;
+    int max_n = 0;
+    for (size_t q = 0; q < lists.size(); ++q) {
+      probs[q].wt = buf.get() + off[q];
+      const i64 co = i64(cand.size());
+      for (i64 r : lists[q]) cand.push_back(2 * nodes[size_t(r / 2)] + (r & 1));
+      if (lists[q].empty()) continue;
+      max_n = std::max(max_n, int(lists[q].size()));
+      for (int c = 0; c < nc; ++c) {
+        ProxyJob j{};
+        j.cand_off = co;
+        j.n = int(lists[q].size());
+        j.ns = ns;
+        j.cx = circles[size_t(c)].cx;
+        j.cy = circles[size_t(c)].cy;
+        j.rad = factor * circles[size_t(c)].r0;
+        j.out_off = off[q] + i64(4) * ns * c;
+        j.ld = M;
+        j.kind = 2;
+        j.with_null = (with_null && c == nc - 1) ? 1 : 0;
+        jobs.push_back(j);
+      }
+    }
+    DevBuf<i64> dc;
+    DevBuf<ProxyJob> dj;
+    dc.upload(cand, s);
+    dj.upload(jobs, s);
+    launch_proxy_jobs(v, dj.get(), int(jobs.size()), ns, max_n, dc.get(), buf.get(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  };
+}
+
+// W^T builder for a block of the entry oracle: W(r, c) = A(rowsc[r], colsc[c]).
+WtBuilder entry_builder(const EntryView& v, const std::vector<i64>& rowsc,
+                        const std::vector<i64>& colsc, cudaStream_t s) {
+  return [&v, &rowsc, &colsc, s](const std::vector<std::vector<i64>>& lists,
+                                 std::vector<IdProblem>& probs, DevBuf<double>& buf) {
+    const int M = int(colsc.size());
+    std::vector<i64> off;
+    i64 tot = 0;
+    probs.clear();
+    for (const auto& l : lists) {
+      off.push_back(tot);
+      tot += i64(M) * i64(l.size());
+      probs.push_back({nullptr, M, int(l.size()), std::max(M, 1)});
+    }
+    buf.resize(size_t(std::max<i64>(tot, 1)));
+    std::vector<i64> cand;
+    std::vector<NearJob> jobs;
+    i64 mx = 0;
+    for (size_t q = 0; q < lists.size(); ++q) {
+      probs[q].wt = buf.get() + off[q];
+      const i64 co = i64(cand.size());
+      for (i64 r : lists[q]) cand.push_back(rowsc[size_t(r)]);
+      if (lists[q].empty() || M == 0) continue;
+      NearJob j{};
+      j.cand_off = co;
+      j.near_off = 0;
+      j.n = int(lists[q].size());
+      j.n_near = M;
+      j.out_off = off[q];
+      j.ld = M;
+      j.transpose = 0;
+      jobs.push_back(j);
+      mx = std::max<i64>(mx, i64(M) * j.n);
+    }
+    DevBuf<i64> dc, dn;
+    DevBuf<NearJob> dj;
+    dc.upload(cand, s);
+    dn.upload(colsc, s);
+    dj.upload(jobs, s);
+    launch_near_jobs(v, dj.get(), int(jobs.size()), mx, dc.get(), dn.get(), buf.get(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  };
+}
+
+bool inside_any_div(const std::vector<ProxyCircleH>& cs, double div, double x, double y) {
+  for (const auto& c : cs)
+    if (std::sqrt((x - c.cx) * (x - c.cx) + (y - c.cy) * (y - c.cy)) < div * c.r0) return true;
+  return false;
+}
+
+// compress_block_far (proxy.cpp:251-302) over point list `nodes` of g.
+RowIdResult compress_block_far(const EntryView& v, const Geom& g, const std::vector<i64>& nodes,
+                               const std::vector<ProxyCircleH>& circles, bool basis, bool with_null,
+                               const std::vector<std::vector<i64>>& tree_leaves, double eps,
+                               cudaStream_t s) {
+  const double bas = 1.5, div = 3.0;
+  require(!circles.empty(), "proxy geometry has no circles");
+  for (i64 nd : nodes) {
+    const bool in_div = inside_any_div(circles, div, g.x[size_t(nd)], g.y[size_t(nd)]);
+    if (basis && in_div) throw Error(5, "far row point inside a division circle");
+    if (!basis && !in_div) throw Error(5, "row point outside every division circle");
+  }
+  const i64 m = 2 * i64(nodes.size());
+  if (nodes.empty()) {
+    RowIdResult out;
+    return out;
+  }
+  std::vector<std::vector<i64>> leaves;
+  for (const auto& lf : tree_leaves) {
+    std::vector<i64> rows;
+    for (i64 p : lf) {
+      rows.push_back(2 * p);
+      rows.push_back(2 * p + 1);
+    }
+    leaves.push_back(std::move(rows));
+  }
+  const double factor = basis ? bas : div;
+  int n = 64;
+  RowIdResult prev =
+      hierarchical_id(m, leaves, proxy_builder(v, nodes, circles, factor, n, with_null, s), eps, s);
+  while (2 * n <= 2048) {
+    n *= 2;
+    RowIdResult cur =
+        hierarchical_id(m, leaves, proxy_builder(v, nodes, circles, factor, n, with_null, s), eps, s);
+    const bool settled = std::llabs(cur.k - prev.k) <= 2;
+    prev = std::move(cur);
+    if (settled) break;
+  }
+  return prev;
+}
+
+// near_row_id (lowrank.cpp:62-125): W(r, c) = A(rowsc[r], colsc[c]).
+RowIdResult near_row_id(const EntryView& v, const std::vector<i64>& rowsc,
+                        const std::vector<i64>& colsc, double eps, std::vector<std::string>& notes,
+                        const char* tag, cudaStream_t s) {
+  const i64 nr = i64(rowsc.size()), ncl = i64(colsc.size());
+  if (nr == 0 || ncl == 0) {
+    RowIdResult out;
+    out.m = nr;
+    out.J.resize(size_t(nr));
+    std::iota(out.J.begin(), out.J.end(), i64(0));
+    return out;
+  }
+  const WtBuilder b = entry_builder(v, rowsc, colsc, s);
+  if (nr * ncl <= (i64(1) << 22)) return direct_id(nr, b, eps, s);
+  notes.push_back(std::string(tag) + ": near block over memory budget, using row partition");
+  std::vector<std::vector<i64>> leaves;
+  for (i64 st = 0; st < nr; st += 256) {
+    std::vector<i64> l;
+    for (i64 r = st; r < std::min(st + 256, nr); ++r) l.push_back(r);
+    leaves.push_back(std::move(l));
+  }
+  return hierarchical_id(nr, leaves, b, eps, s);
+}
+
+std::vector<i64> scalars(const std::vector<i64>& nodes) {
+  std::vector<i64> o;
+  o.reserve(2 * nodes.size());
+  for (i64 n : nodes) {
+    o.push_back(2 * n);
+    o.push_back(2 * n + 1);
+  }
+  return o;
+}
+
+}  // namespace
+
+std::vector<ProxyCircleH> make_proxy_circles(const Geom& g, const Plan& plan) {
+  std::vector<ProxyCircleH> out;
+  if (plan.added_new.empty()) return out;
+  const size_t nc = g.comps.size();
+  std::vector<std::vector<std::pair<double, double>>> pts(nc);
+  std::vector<std::set<i64>> pans(nc);
+  for (i64 node : plan.added_new) {
+    const i64 c = g.component_of(node);
+    pts[size_t(c)].push_back({g.x[size_t(node)], g.y[size_t(node)]});
+    pans[size_t(c)].insert(g.panel_of[size_t(node)]);
+  }
+  for (size_t c = 0; c < nc; ++c) {
+    auto& p = pts[c];
+    if (p.empty()) continue;
+    for (i64 pid : pans[c]) {
+      const PanelRow& pr = g.panels[size_t(pid)];
+      double x, y, a, b, e, f;
+      g.comps[c].curve.eval(pr.a, x, y, a, b, e, f);
+      p.push_back({x, y});
+      g.comps[c].curve.eval(pr.b, x, y, a, b, e, f);
+      p.push_back({x, y});
+    }
+    double sx = 0, sy = 0;
+    for (auto& q : p) {
+      sx += q.first;
+      sy += q.second;
+    }
+    const double cx = sx / double(p.size()), cy = sy / double(p.size());
+    double r0 = 0;
+    for (auto& q : p)
+      r0 = std::max(r0, std::sqrt((q.first - cx) * (q.first - cx) + (q.second - cy) * (q.second - cy)));
+    if (!(r0 > 0.0)) throw Error(3, "refined region has zero spatial extent");
+    out.push_back({cx, cy, r0});
+  }
+  return out;
+}
+
+std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, const Plan& plan,
+                                               int form, double mu, double eps, std::uint64_t seed,
+                                               cudaStream_t s) {
+  (void)seed;  // the sketch is an exact rotation; see the header comment
+  require(eps > 0.0 && eps <= 0.1, "compression tolerance out of range");
+  auto u = std::make_unique<Update>();
+  u->nk2 = 2 * i64(plan.kept_old.size());
+  u->nc2 = 2 * i64(plan.cut_old.size());
+  u->np2 = 2 * i64(plan.added_new.size());
+  if (u->nc2 == 0 && u->np2 == 0) return u;
+  EntryOracle eold(og, form, mu, s), enew(ng, form, mu, s);
+  const bool with_null = enew.has_nullspace();
+  const auto circles = make_proxy_circles(ng, plan);
+  const double div = 3.0;
+  // shared far-field ID over the kept rows (lowrank.cpp:275-287)
+  std::vector<i64> far_pos, near_pos;
+  for (size_t p = 0; p < plan.kept_new.size(); ++p) {
+    const i64 nd = plan.kept_new[p];
+    (inside_any_div(circles, div, ng.x[size_t(nd)], ng.y[size_t(nd)]) ? near_pos : far_pos)
+        .push_back(i64(p));
+  }
+  std::vector<i64> far_nodes;
+  for (i64 p : far_pos) far_nodes.push_back(plan.kept_new[size_t(p)]);
+  // dyadic-by-distance partition (proxy.cpp:91-129)
+  std::vector<std::vector<i64>> ktree;
+  {
+    const i64 n = i64(far_nodes.size());
+    std::vector<i64> order(static_cast<size_t>(n));
+    std::iota(order.begin(), order.end(), i64(0));
+    std::vector<int> band(static_cast<size_t>(n), 0);
+    if (!circles.empty()) {
+      for (i64 i = 0; i < n; ++i) {
+        double best = INFINITY;
+        const double x = ng.x[size_t(far_nodes[size_t(i)])], y = ng.y[size_t(far_nodes[size_t(i)])];
+        for (const auto& c : circles)
+          best = std::min(best, std::sqrt((x - c.cx) * (x - c.cx) + (y - c.cy) * (y - c.cy)) / c.r0);
+        band[size_t(i)] = int(std::floor(std::log2(std::max(1.0, best))));
+      }
+      std::stable_sort(order.begin(), order.end(),
+                       [&](i64 a, i64 b) { return band[size_t(a)] < band[size_t(b)]; });
+    }
+    size_t pos = 0;
+    while (pos < order.size()) {
+      size_t run = pos + 1;
+      while (run < order.size() && band[size_t(order[run])] == band[size_t(order[pos])]) ++run;
+      while (pos < run) {
+        const size_t take = std::min<size_t>(128, run - pos);
+        ktree.emplace_back(order.begin() + long(pos), order.begin() + long(pos + take));
+        pos += take;
+      }
+    }
+  }
+  RowIdResult far = compress_block_far(enew.view(), ng, far_nodes, circles, true, with_null, ktree, eps, s);
+  const std::vector<i64> far_s = scalars(far_pos), near_s = scalars(near_pos);
+  // kept-row blocks kc (old oracle) and kp (new oracle)  (lowrank.cpp:130-180)
+  const std::vector<i64> kept_old_s = scalars(plan.kept_old), kept_new_s = scalars(plan.kept_new);
+  const std::vector<i64> cut_s = scalars(plan.cut_old), added_s = scalars(plan.added_new);
+  auto mapped = [](const std::vector<i64>& map, const std::vector<i64>& idx) {
+    std::vector<i64> o;
+    o.reserve(idx.size());
+    for (i64 i : idx) o.push_back(map[size_t(i)]);
+    return o;
+  };
+  struct KeptFactor {
+    RowIdResult nearid;
+    i64 k = 0;
+    std::vector<i64> skel;  // block-local kept rows
+  };
+  auto kept_factor = [&](const EntryOracle& eo, const std::vector<i64>& rowmap,
+                         const std::vector<i64>& colmap, const char* tag) {
+    KeptFactor f;
+    if (rowmap.empty() || colmap.empty()) return f;
+    f.nearid = near_row_id(eo.view(), mapped(rowmap, near_s), colmap, eps, u->notes, tag, s);
+    f.k = far.k + f.nearid.k;
+    for (i64 i = 0; i < far.k; ++i) f.skel.push_back(far_s[size_t(far.J[size_t(i)])]);
+    for (i64 i = 0; i < f.nearid.k; ++i) f.skel.push_back(near_s[size_t(f.nearid.J[size_t(i)])]);
+    return f;
+  };
+  KeptFactor kc = kept_factor(eold, kept_old_s, cut_s, "kc");
+  KeptFactor kp = kept_factor(enew, kept_new_s, added_s, "kp");
+  // added rows against the division surface (lowrank.cpp:296-308, 183-238)
+  RowIdResult pk_far;
+  if (!plan.added_new.empty()) {
+    std::vector<std::vector<i64>> ptree;
+    for (size_t st = 0; st < plan.added_new.size(); st += 128) {
+      std::vector<i64> l;
+      for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
+      ptree.push_back(std::move(l));
+    }
+    pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, s);
+  }
+  RowIdResult pk_near;
+  i64 k_pk = 0;
+  if (u->np2 > 0 && u->nk2 > 0) {
+    pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, u->notes, "pk", s);
+    k_pk = pk_far.k + pk_near.k;
+  }
+  u->k_kc = kc.k;
+  u->k_kp = kp.k;
+  u->k_pk = k_pk;
+  u->k1 = k_pk + kc.k + kp.k;
+  const i64 n_ext = u->n_ext(), k1 = u->k1;
+  if (k1 == 0) return u;
+  // stacked L1 (n_ext x k1) and R1 (k1 x n_ext)  (lowrank.cpp:240-251)
+  DevBuf<double> L1(static_cast<size_t>(n_ext * k1)), R1(static_cast<size_t>(k1 * n_ext));
+  SBX_CUDA(cudaMemsetAsync(L1.get(), 0, size_t(n_ext * k1) * 8, s));
+  SBX_CUDA(cudaMemsetAsync(R1.get(), 0, size_t(k1 * n_ext) * 8, s));
+  const i64 ckc = k_pk, ckp = k_pk + kc.k;
+  DevBuf<i64> d_far_s, d_near_s, d_added_rows;
+  d_far_s.upload(far_s, s);
+  d_near_s.upload(near_s, s);
+  std::vector<i64> added_rows(static_cast<size_t>(u->np2));
+  for (i64 r = 0; r < u->np2; ++r) added_rows[size_t(r)] = u->nk2 + u->nc2 + r;
+  d_added_rows.upload(added_rows, s);
+  std::vector<ScatterJob> sj;
+  const int ldl = int(n_ext);
+  auto scat = [&](const double* src, const i64* map, i64 rows, i64 cols, int col_off, double alpha) {
+    if (rows * cols == 0) return;
+    sj.push_back({src, L1.get(), map, int(rows), int(cols), int(std::max<i64>(rows, 1)), ldl, col_off, 0, alpha});
+  };
+  if (kc.k > 0) {  // -kc.L in the kept rows
+    scat(far.P.get(), d_far_s.get(), far.m, far.k, int(ckc), -1.0);
+    scat(kc.nearid.P.get(), d_near_s.get(), kc.nearid.m, kc.nearid.k, int(ckc + far.k), -1.0);
+  }
+  if (kp.k > 0) {  // kp.L
+    scat(far.P.get(), d_far_s.get(), far.m, far.k, int(ckp), 1.0);
+    scat(kp.nearid.P.get(), d_near_s.get(), kp.nearid.m, kp.nearid.k, int(ckp + far.k), 1.0);
+  }
+  if (k_pk > 0) {  // pk.L in the added rows
+    scat(pk_far.P.get(), d_added_rows.get(), pk_far.m, pk_far.k, 0, 1.0);
+    scat(pk_near.P.get(), d_added_rows.get(), pk_near.m, pk_near.k, int(pk_far.k), 1.0);
+  }
+  scatter_batched(sj, s);
+  // R blocks straight into R1
+  {
+    std::vector<i64> ri_old, ci_old, ri_new, ci_new, dstc_new;
+    std::vector<BlockJob> jo, jn;
+    i64 mo = 0, mn = 0;
+    auto push = [](std::vector<i64>& ri, std::vector<i64>& ci, std::vector<BlockJob>& jv, i64& mx,
+                   const std::vector<i64>& rows, const std::vector<i64>& cols, i64 out_off, int ld,
+                   i64 dst_col_off) {
+      if (rows.empty() || cols.empty()) return;
+      BlockJob j{};
+      j.row_off = i64(ri.size());
+      j.col_off = i64(ci.size());
+      j.nr = int(rows.size());
+      j.nc = int(cols.size());
+      j.out_off = out_off;
+      j.ld = ld;
+      j.dst_col_off = dst_col_off;
+      ri.insert(ri.end(), rows.begin(), rows.end());
+      ci.insert(ci.end(), cols.begin(), cols.end());
+      mx = std::max<i64>(mx, i64(j.nr) * j.nc);
+      jv.push_back(j);
+    };
+    const int ldr = int(k1);
+    // kc.R = A_old(kept_old_s[skel], cut_s) at rows ckc.., cols nk2..
+    push(ri_old, ci_old, jo, mo, mapped(kept_old_s, kc.skel), cut_s, ckc + u->nk2 * k1, ldr, -1);
+    // kp.R = A_new(kept_new_s[skel], added_s) at rows ckp.., cols nk2+nc2..
+    push(ri_new, ci_new, jn, mn, mapped(kept_new_s, kp.skel), added_s, ckp + (u->nk2 + u->nc2) * k1, ldr, -1);
+    // pk.R: far skeleton rows over the far kept columns, near over near
+    if (k_pk > 0) {
+      std::vector<i64> fr, nr_;
+      for (i64 i = 0; i < pk_far.k; ++i) fr.push_back(added_s[size_t(pk_far.J[size_t(i)])]);
+      for (i64 i = 0; i < pk_near.k; ++i) nr_.push_back(added_s[size_t(pk_near.J[size_t(i)])]);
+      const i64 o1 = i64(dstc_new.size());
+      dstc_new.insert(dstc_new.end(), far_s.begin(), far_s.end());
+      push(ri_new, ci_new, jn, mn, fr, mapped(kept_new_s, far_s), 0, ldr, o1);
+      const i64 o2 = i64(dstc_new.size());
+      dstc_new.insert(dstc_new.end(), near_s.begin(), near_s.end());
+      push(ri_new, ci_new, jn, mn, nr_, mapped(kept_new_s, near_s), pk_far.k, ldr, o2);
+    }
+    DevBuf<i64> a, b, c, d, e;
+    DevBuf<BlockJob> ja, jb;
+    a.upload(ri_old, s);
+    b.upload(ci_old, s);
+    c.upload(ri_new, s);
+    d.upload(ci_new, s);
+    e.upload(dstc_new, s);
+    ja.upload(jo, s);
+    jb.upload(jn, s);
+    launch_block_jobs(eold.view(), ja.get(), int(jo.size()), mo, a.get(), b.get(), R1.get(), s);
+    launch_block_jobs(enew.view(), jb.get(), int(jn.size()), mn, c.get(), d.get(), R1.get(), s, e.get());
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+  // final row ID of L1 (see header): CPQR of L1^T (k1 x n_ext)
+  DevBuf<double> L1T(static_cast<size_t>(k1 * n_ext));
+  copy_batched({{L1.get(), L1T.get(), int(k1), int(n_ext), ldl, int(k1), 1, 0}}, s);
+  IdBatch fin;
+  fin.factor({{L1T.get(), int(k1), int(n_ext), int(k1)}}, eps, s);
+  u->k = fin.eps_rank(0, eps);
+  const i64 k = u->k;
+  u->skeleton.assign(fin.perm(0).begin(), fin.perm(0).begin() + k);
+  u->L.resize(size_t(std::max<i64>(n_ext * k, 1)));
+  u->R.resize(size_t(std::max<i64>(k * n_ext, 1)));
+  if (k > 0) {
+    fin.interp({k}, {u->L.get()}, {int(n_ext)}, s);
+    // R = L1(J(0:k), :) * R1
+    DevBuf<i64> sk;
+    sk.upload(u->skeleton, s);
+    DevBuf<double> L1s(static_cast<size_t>(k * k1));
+    scatter_batched({{L1.get(), L1s.get(), sk.get(), int(k), int(k1), ldl, int(k), 0, 1, 1.0}}, s);
+    gemm_batched({{L1s.get(), R1.get(), u->R.get(), int(k), int(n_ext), int(k1), int(k), int(k1), int(k),
+                   0, 0, 1.0, 0.0}},
+                 s);
+  }
+  SBX_CUDA(cudaStreamSynchronize(s));
+  return u;
+}
+
+void update_download(const Update& u, int which, double* out, cudaStream_t s) {
+  require(which == 0 || which == 1, "update factor: which must be 0 (L) or 1 (R)");
+  const size_t n = size_t(u.n_ext() * u.k);
+  if (n == 0) return;
+  (which == 0 ? u.L : u.R).download(out, n, s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+std::unique_ptr<Update> update_from_factors(const Plan& plan, const double* L, const double* R,
+                                            i64 n_ext, i64 k, cudaStream_t s) {
+  auto u = std::make_unique<Update>();
+  u->nk2 = 2 * i64(plan.kept_old.size());
+  u->nc2 = 2 * i64(plan.cut_old.size());
+  u->np2 = 2 * i64(plan.added_new.size());
+  require(n_ext == u->n_ext(), "update factor size does not match the plan");
+  require(k >= 0, "negative rank");
+  u->k = k;
+  u->k1 = k;
+  u->L.upload(L, size_t(n_ext * k), s);
+  u->R.upload(R, size_t(n_ext * k), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  return u;
+}
+
+}  // namespace sbx

@@ -1,0 +1,159 @@
+"""Device parity against the CPU oracle (oracle/), through the sbx C-ABI.
+
+Tier 1: identical HBS factors handed over in the reference's HBS1 format ->
+device sweeps must match the oracle's sweeps to 1e-12 relative.
+Tier 2: independent device compression -> reference test assertions (dense
+operator / dense solve / analytic field) and 1e-9 agreement with the
+oracle's refined solve.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2108_07205_b200 as sb
+    sb.init(0)
+    return sb
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+# ---------------------------------------------------------------- geometry / entries
+def test_nodes_bitwise_equal_oracle(sb, po):
+    g = sb.panelize(sb.star(5, 0.3), 12, 16)
+    o = po.Geom.create(po.STAR, 12, prongs=5, amplitude=0.3)
+    a, b = g.nodes(), o.nodes()
+    for key in ("x", "y", "nx", "ny", "w", "curvature", "param"):
+        assert np.array_equal(a[key], b[key]), key
+    g1, p1 = sb.refine(g, [5, 2], 3)
+    o1, q1 = o.refine([5, 2], 3)
+    assert all(np.array_equal(p1.maps()[k], q1.maps()[k]) for k in p1.maps())
+    assert np.array_equal(g1.nodes()["x"], o1.nodes()["x"])
+
+
+def test_entries_bitwise_equal_oracle(sb, po):
+    g = sb.panelize(sb.ellipse(2.0, 1.0), 16, 16)
+    o = po.Geom.create(po.ELLIPSE, 16, scale=2.0, aspect=0.5)
+    a = po.Assembler.create(o)
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, 512, 200)
+    cols = np.concatenate([rows[:50], rng.integers(0, 512, 150)])
+    assert np.array_equal(sb.submatrix(g, rows, cols), a.submatrix(rows, cols))
+
+
+# ---------------------------------------------------------------- tier 1 sweeps
+@pytest.mark.parametrize("nrhs", [1, 3, 64, 130])
+def test_tier1_hbs1_sweeps_match_oracle(sb, po, tmp_path, nrhs):
+    o = po.Geom.create(po.STAR, 24, prongs=5, amplitude=0.3)
+    a = po.Assembler.create(o)
+    h = po.Hbs.compress(a, 1e-10).invert()
+    h.save(tmp_path / "h.hbs1")
+    d = sb.hbs_load(tmp_path / "h.hbs1")
+    n = h.info()["n"]
+    b = np.random.default_rng(nrhs).standard_normal((n, nrhs))
+    assert rel(sb.hbs_solve(d, b), h.solve(b)) < 1e-12
+    assert rel(sb.hbs_apply(d, b), h.apply(b)) < 1e-12
+
+
+def test_hbs1_device_roundtrip_bitwise(sb, po, tmp_path):
+    o = po.Geom.create(po.STAR, 10, prongs=3, amplitude=0.35)
+    h = po.Hbs.compress(po.Assembler.create(o), 1e-8).invert()
+    h.save(tmp_path / "a.hbs1")
+    d = sb.hbs_load(tmp_path / "a.hbs1")
+    sb.hbs_save(d, tmp_path / "b.hbs1")
+    assert (tmp_path / "a.hbs1").read_bytes() == (tmp_path / "b.hbs1").read_bytes()
+
+
+# ---------------------------------------------------------------- tier 2 compression
+def test_device_compress_apply_matches_dense(sb, po):  # test_hbs.cpp:60-90
+    g = sb.panelize(sb.circle(1.3, (0.1, -0.2)), 10, 16)
+    h = sb.hbs_compress(g, sb.INTERIOR_DIRICHLET, sb.HbsOptions(eps=1e-10), mu=0.8)
+    o = po.Geom.create(po.CIRCLE, 10, center=(0.1, -0.2), scale=1.3)
+    A = po.Assembler.create(o, po.INTERIOR, 0.8).full_matrix()
+    n = A.shape[0]
+    assert np.linalg.norm(sb.hbs_apply(h, np.eye(n)) - A) / np.linalg.norm(A) < 1e-9
+
+
+def test_device_compress_ranks_track_oracle(sb, po):
+    g = sb.panelize(sb.star(5, 0.3), 24, 16)
+    h = sb.hbs_compress(g)
+    o = po.Hbs.compress(po.Assembler.create(po.Geom.create(po.STAR, 24, prongs=5, amplitude=0.3)), 1e-10)
+    assert np.max(np.abs(h.node_ranks() - o.node_ranks())) <= 2
+
+
+def test_device_solve_residual_and_field(sb, po):  # test_hbs.cpp:128-184
+    g = sb.panelize(sb.circle(), 20, 16)
+    h = sb.hbs_invert(sb.hbs_compress(g))
+    o = po.Geom.create(po.CIRCLE, 20)
+    A = po.Assembler.create(o).full_matrix()
+    b = np.random.default_rng(3).standard_normal(A.shape[0])
+    assert np.linalg.norm(A @ sb.hbs_solve(h, b) - b) < 1e-7 * np.linalg.norm(b)
+    src = po.ring_sources(5, (0, 0), 3.0)
+    tau = sb.hbs_solve(h, sb.boundary_data(g, src))
+    tg = np.array([[0.3, 0.1], [0.4, 0.2], [-0.3, 0.4], [0.2, -0.5], [-0.5, -0.1]])
+    u = o.evaluate_velocity(po.INTERIOR, tau, tg)
+    ref = po.field_velocity(src, tg)
+    assert np.max(np.linalg.norm(u - ref, axis=1) / np.linalg.norm(ref, axis=1)) < 1e-8
+
+
+def test_device_update_matches_dense(sb, po):  # test_lowrank.cpp:64-98
+    eps = 1e-10
+    g0 = sb.panelize(sb.star(5, 0.3), 10, 16)
+    g1, plan = sb.refine(g0, [2, 3], 2)
+    u = sb.compress_update(g0, g1, plan, eps)
+    L, R = u.factors()
+    o0 = po.Geom.create(po.STAR, 10, prongs=5, amplitude=0.3)
+    o1, op = o0.refine([2, 3], 2)
+    a0, a1 = po.Assembler.create(o0), po.Assembler.create(o1)
+    nk, nc, npp = op.sizes()
+    n = 2 * (nk + nc + npp)
+    Q = np.zeros((n, n))
+    Q[: 2 * nk, 2 * nk: 2 * nk + 2 * nc] = -po.block_eval_full(a0, a1, op, "kc")
+    Q[: 2 * nk, 2 * nk + 2 * nc:] = po.block_eval_full(a0, a1, op, "kp")
+    Q[2 * nk + 2 * nc:, : 2 * nk] = po.block_eval_full(a0, a1, op, "pk")
+    assert np.linalg.norm(Q - L @ R, 2) <= 10 * eps * np.linalg.norm(Q, 2)
+    ou = po.Update.compress(a0, a1, op, eps)
+    assert abs(u.k - ou.info()["k"]) <= 3
+
+
+def test_els_matches_oracle_and_dense(sb, po):  # test_els.cpp:125-144
+    eps = 1e-10
+    g0 = sb.panelize(sb.star(5, 0.3), 10, 16)
+    h = sb.hbs_invert(sb.hbs_compress(g0))
+    g1, plan = sb.refine(g0, [3], 4)
+    u = sb.compress_update(g0, g1, plan, eps)
+    e = sb.els_build(h, g0, g1, plan, u)
+    src = po.ring_sources(4, (0, 0), 3.0)
+    g_new = sb.boundary_data(g1, src)
+    tau = sb.els_solve(e, sb.gather_kept_added(plan, g_new))
+    o0 = po.Geom.create(po.STAR, 10, prongs=5, amplitude=0.3)
+    o1, op = o0.refine([3], 4)
+    a1 = po.Assembler.create(o1)
+    Ann = a1.full_matrix()
+    ref = po.gather_kept_added(op.maps(), np.linalg.solve(Ann, o1.boundary_data(src)))
+    assert rel(tau, ref) <= 1e-8
+    a0 = po.Assembler.create(o0)
+    oe = po.Els.build(po.Hbs.compress(a0, eps).invert(), a0, a1, op, po.Update.compress(a0, a1, op, eps))
+    assert rel(tau, oe.solve(po.gather_kept_added(op.maps(), o1.boundary_data(src)))) <= 1e-9
+
+
+def test_singular_woodbury_is_reported(sb):  # test_els.cpp:293-330
+    g = sb.panelize(sb.circle(), 10, 16)
+    h = sb.hbs_invert(sb.hbs_compress(g))
+    g1, plan = sb.refine(g, [0], 2)
+    n_ext = sum(2 * x for x in plan.sizes())
+    e0 = sb.els_build(h, g, g1, plan,
+                      sb.update_from_factors(plan, np.zeros((n_ext, 0)), np.zeros((0, n_ext))))
+    rng = np.random.default_rng(0)
+    u1 = rng.standard_normal(n_ext)
+    y = sb.els_solve_raw(e0, u1)  # Atilde^{-1} u1
+    # W = I + R Atilde^{-1} L = [[0, 0], [r.y, 1]]: loses one direction
+    L = np.stack([u1, np.zeros(n_ext)], 1)
+    R = np.stack([-y / (y @ y), 1e-3 * rng.standard_normal(n_ext)], 0)
+    with pytest.raises(sb.SingularMatrixError, match="optimal-basis"):
+        sb.els_build(h, g, g1, plan, sb.update_from_factors(plan, L, R))
