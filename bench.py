@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py — refined-wall solves/sec on a B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): star wall
+r(t) = 1 + 0.3 cos 5t, 1024 panels x 16 Gauss nodes (32768 unknowns), static
+HBS inverse precomputed once (timed separately, `t_static_s`).  One step is
+one per-time-step refined-wall solve, exactly the reference's Direct-Local
+branch (scenario.cpp:658-741) without its update cache:
+
+    refine(16 panels, m=16) -> compress_update (two-step ID, eps 1e-10)
+    -> els_build (A_pp HBS, X = Atilde^-1 L, W = I + R X, LU(W))
+    -> els_solve for 64 right-hand sides (8 Stokeslets each).
+
+value  = RHS solves per second over all ranks, device-resident RHS.
+e2e    = the same through the public API with pinned host RHS in and the
+         density back to the host every step.
+Multi-GPU: independent replicas (each rank its own refined wall; the path
+has no exchange step at this size), scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "refined-wall solves/sec (HBS apply + Woodbury, fp64)"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ workload
+def build_problem(cfg, sb):
+    curve = sb.star(cfg.prongs, cfg.amplitude, cfg.a) if cfg.kind == "star" else sb.ellipse(cfg.a, cfg.b)
+    g0 = sb.panelize(curve, cfg.n_panels, cfg.q)
+    t0 = time.perf_counter()
+    h = sb.hbs_invert(sb.hbs_compress(g0, opts=sb.HbsOptions(eps=cfg.eps, leaf_nodes=cfg.leaf)))
+    sb.api.lib().sbx_sync()
+    t_static = time.perf_counter() - t0
+    panels = cfg.refine_panels(g0.nodes())
+    g1, plan = sb.refine(g0, panels, cfg.m)
+    srcs = cfg.sources()
+    G = np.stack([sb.gather_kept_added(plan, sb.boundary_data(g1, s)) for s in srcs], 1)
+    return g0, h, panels, G, t_static
+
+
+def solve_flops_bytes(sb, h, els, nrhs):
+    """Algorithmic work of one els_solve."""
+    info = h.info()
+    e = els.info()
+    n_ext = e["n_k"] + e["n_c"] + e["n_p"]
+    app = els._app_factor_doubles if hasattr(els, "_app_factor_doubles") else 0
+    fd = info["factor_doubles"] + app
+    k = e["k"]
+    flops = 2.0 * nrhs * (fd + 2 * k * n_ext + k * k)
+    bytes_ = 8.0 * (fd + 2 * k * n_ext + k * k) + 16.0 * n_ext * nrhs
+    return flops, bytes_
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2108_07205_b200 as sb
+    from paper_2108_07205_b200.configs import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    torch.cuda.set_device(local_rank)
+    sb.init(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    g0, h, panels, G, t_static = build_problem(cfg, sb)
+    nrhs = G.shape[1]
+    stream = torch.cuda.ExternalStream(sb.api.lib().sbx_stream())
+    G_dev = torch.from_numpy(np.ascontiguousarray(G)).cuda()  # rows x nrhs (C order)
+    G_pin = torch.from_numpy(np.ascontiguousarray(G)).pin_memory()
+    out_pin = torch.empty_like(G_pin).pin_memory()
+
+    state = {}
+
+    def step(e2e):
+        g1, plan = sb.refine(g0, panels, cfg.m)
+        upd = sb.compress_update(g0, g1, plan, cfg.eps, seed=cfg.seed)
+        els = sb.els_build(h, g0, g1, plan, upd)
+        with torch.cuda.stream(stream):
+            if e2e:
+                gd = G_pin.to("cuda", non_blocking=True)
+                tau = sb.els_solve(els, gd)
+                out_pin.copy_(tau, non_blocking=True)
+            else:
+                tau = sb.els_solve(els, G_dev)
+        state["els"], state["upd"], state["tau"] = els, upd, tau
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    sb.kernel_launches(reset=True)
+    with ClockSampler(local_rank) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    launches = sb.kernel_launches(reset=True) // max(1, args.steps) * args.steps
+    ms = e0.elapsed_time(e1)
+    # e2e: host RHS in, density out, every step
+    for _ in range(1):
+        step(True)
+    barrier()
+    f0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(True)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - f0
+    # phase split of one step (device events on the library stream)
+    ph = phase_split(sb, torch, stream, g0, h, panels, cfg, G_dev)
+    times = torch.tensor([ms / 1e3, e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    t_dev, t_e2e = times.tolist()
+    if rank != 0:
+        return None
+    value = world * args.steps * nrhs / t_dev
+    e2e_value = world * args.steps * nrhs / t_e2e
+    roof = roofline_solve(sb, torch, stream, h, state, G_dev)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_dev / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: star r=1+0.3cos5t, 1024x16 nodes (32768 unknowns), "
+                               f"refine 16 panels m=16, 64 RHS, eps 1e-10, leaf 64",
+                   "rhs_per_step": nrhs, "steps_per_s": round(world * args.steps / t_dev, 3),
+                   "t_static_s": round(t_static, 4), "phase_ms": ph,
+                   "k": state["upd"].info()["k"], "l2": "inputs re-streamed each step (> L2 per step)",
+                   "parallelism": f"replicas x{world}", "wall_s": round(wall, 3)},
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
+                "h2d_bytes_per_step": int(G_pin.numel() * 8),
+                "d2h_bytes_per_step": int(out_pin.numel() * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "roofline": roof,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg, G.shape[1], threads=1)
+    return line
+
+
+def phase_split(sb, torch, stream, g0, h, panels, cfg, G_dev):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+        g1, plan = sb.refine(g0, panels, cfg.m)
+        ev[1].record(stream)
+        upd = sb.compress_update(g0, g1, plan, cfg.eps, seed=cfg.seed)
+        ev[2].record(stream)
+        els = sb.els_build(h, g0, g1, plan, upd)
+        ev[3].record(stream)
+        sb.els_solve(els, G_dev)
+        ev[4].record(stream)
+    torch.cuda.synchronize()
+    names = ("refine", "compress_update", "els_build", "els_solve")
+    return {n: round(ev[i].elapsed_time(ev[i + 1]), 3) for i, n in enumerate(names)}
+
+
+def roofline_solve(sb, torch, stream, h, state, G_dev):
+    """Dominant solve kernel family: the HBS inverse sweep with the 64-RHS
+    block (FP64 DMMA).  Achieved = algorithmic flops of one hbs_solve ÷ its
+    CUDA-event time on the library stream, averaged over repeats."""
+    info = h.info()
+    n = info["n"]
+    nrhs = G_dev.shape[1]
+    b = torch.empty((n, nrhs), dtype=torch.float64, device="cuda").uniform_(-1, 1)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            sb.hbs_solve(h, b)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        reps = 10
+        e0.record(stream)
+        for _ in range(reps):
+            sb.hbs_solve(h, b)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * nrhs * info["factor_doubles"]
+    peaks = measured_fp64_peak()
+    achieved = flops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "sweep_dmma_kernel (hbs_solve, nrhs=64, n=32768)",
+            "achieved": round(achieved, 3), "peak": peaks["value"], "unit": "TFLOP/s",
+            "frac": round(achieved / peaks["value"], 4), "peak_source": peaks["source"],
+            "launch_ms": round(ms, 4), "algorithmic_flops": flops, "traffic": None}
+
+
+def measured_fp64_peak():
+    """FP64 DMMA peak measured on this pool (profiles/fp64_peak.json, written
+    by scripts/dmma_peak.cu on a B200); MEASURED_PEAKS.json has no FP64 entry."""
+    p = ROOT / "profiles" / "fp64_peak.json"
+    try:
+        d = json.loads(p.read_text())
+        return {"value": float(d["fp64_dmma_tflops"]), "source": "measured (scripts/dmma_peak.cu)"}
+    except Exception:
+        return {"value": 37.0, "source": "assumed FP64 DMMA peak (no measurement found)"}
+
+
+# ------------------------------------------------------------------ CPU legs
+def _oracle_problem(cfg, po):
+    kind = po.ELLIPSE if cfg.kind == "ellipse" else po.STAR
+    if cfg.kind == "ellipse":
+        o0 = po.Geom.create(kind, cfg.n_panels, scale=cfg.a, aspect=cfg.b / cfg.a)
+    else:
+        o0 = po.Geom.create(kind, cfg.n_panels, prongs=cfg.prongs, amplitude=cfg.amplitude, scale=cfg.a)
+    a0 = po.Assembler.create(o0)
+    return o0, a0
+
+
+def _oracle_step(cfg, po, o0, a0, oh, panels, srcs):
+    o1, op = o0.refine(panels, cfg.m)
+    a1 = po.Assembler.create(o1)
+    ou = po.Update.compress(a0, a1, op, cfg.eps, cfg.seed)
+    oe = po.Els.build(oh, a0, a1, op, ou)
+    OG = np.stack([po.gather_kept_added(op.maps(), o1.boundary_data(s)) for s in srcs], 1)
+    return oe.solve(OG)
+
+
+def cpu_baseline(cfg, nrhs, threads=1, steps=1):
+    """The oracle (C++ restatement of the reference's serial path) on this
+    host's cores: `threads` independent refined-wall steps in parallel."""
+    from oracle import pyoracle as po
+    po.build()
+    o0, a0 = _oracle_problem(cfg, po)
+    t0 = time.perf_counter()
+    oh = po.Hbs.compress(a0, cfg.eps).invert()
+    t_static = time.perf_counter() - t0
+    panels = cfg.refine_panels(o0.nodes())
+    srcs = cfg.sources()
+
+    def work():
+        for _ in range(steps):
+            _oracle_step(cfg, po, o0, a0, oh, panels, srcs)
+
+    t1 = time.perf_counter()
+    ths = [threading.Thread(target=work) for _ in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t1
+    value = threads * steps * nrhs / dt
+    return {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{threads * steps} full refined-wall step(s) of {cfg.name} "
+                      f"({nrhs} RHS each), {dt:.1f} s; static HBS excluded ({t_static:.1f} s)",
+            "seconds": round(dt, 2), "t_static_s": round(t_static, 2)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from paper_2108_07205_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    threads = max(1, os.cpu_count() or 1)
+    base = cpu_baseline(cfg, cfg.nrhs, threads=threads, steps=1)
+    base_per_step = base["seconds"]
+    line = {
+        "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * base_per_step, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} (same as --impl ours)", "rhs_per_step": cfg.nrhs,
+                   "note": "reference C++ needs Eigen3 (absent); its CPU path is timed through "
+                           "the oracle restatement (oracle/), all host threads, one step each"},
+        "impl": "reference",
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def main():
+    args = parse()
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,7 @@ typedef struct {
 const char* sbx_last_error(void);
 int sbx_init(int device);                  /* selects the CUDA device */
 int sbx_sync(void);                        /* waits for the library stream */
+void* sbx_stream(void);                    /* the library stream (cudaStream_t) */
 
 /* ---------------------------------------------------------- geometry
  * panelize (geometry.hpp:103), build_discretization + add_holes
@@ -169,6 +170,12 @@ int sbx_els_xw(sbx_els e, double* X, double* W);
 /* ---------------------------------------------------------- diagnostics
  * Number of sbx kernels launched since the last reset (bench evidence). */
 int64_t sbx_kernel_launches(int reset);
+
+/* Device row ID of a host matrix W (m x n, column-major) — idlib.cpp:73-99
+ * (row_id; forced >= 0 selects row_id_rank).  engine: 0 auto, 1 one CTA per
+ * problem, 2 cooperative multi-CTA.  J: m entries, P: m*min(m,n) doubles. */
+int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
+               int64_t* k, int64_t* J, double* P);
 
 #ifdef __cplusplus
 }

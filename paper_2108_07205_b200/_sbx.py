@@ -64,7 +64,9 @@ _SIGS = [
     ("sbx_last_error", C.c_char_p, []),
     ("sbx_init", C.c_int, [C.c_int]),
     ("sbx_sync", C.c_int, []),
+    ("sbx_stream", C.c_void_p, []),
     ("sbx_kernel_launches", C.c_int64, [C.c_int]),
+    ("sbx_row_id", C.c_int, [F64P, I64, I64, C.c_double, I64, C.c_int, I64P, I64P, F64P]),
     ("sbx_geom_create", C.c_int, [C.POINTER(sbx_curve), C.c_int, C.c_int, C.POINTER(VP)]),
     ("sbx_geom_add_holes", C.c_int,
      [VP, C.c_int, C.POINTER(sbx_curve), C.POINTER(C.c_int32), C.POINTER(C.c_int32),

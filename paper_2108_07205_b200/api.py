@@ -461,6 +461,20 @@ def _els_new_unknowns(s: ElsSolver) -> int:
     return i["n_k"] + i["n_p"]
 
 
+def row_id(w, eps=1e-10, forced=None, engine=0):
+    """Device row ID (idlib.cpp:73-99): returns k, J, P with W ~= P W[J[:k]]."""
+    _ensure()
+    w = np.asfortranarray(np.asarray(w, dtype=np.float64))
+    m, n = w.shape
+    k = C.c_int64()
+    J = np.zeros(m, dtype=np.int64)
+    P = np.zeros(max(1, m * min(m, n)))
+    check(lib().sbx_row_id(w.ctypes.data_as(F64P), m, n, eps, -1 if forced is None else forced,
+                           engine, C.byref(k), J.ctypes.data_as(I64P), P.ctypes.data_as(F64P)))
+    kk = k.value
+    return kk, J, P[: m * kk].reshape((m, kk), order="F")
+
+
 def kernel_launches(reset: bool = False) -> int:
     return int(lib().sbx_kernel_launches(int(reset)))
 

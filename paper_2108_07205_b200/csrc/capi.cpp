@@ -8,6 +8,7 @@
 #include "geometry.hpp"
 #include "hbs.hpp"
 #include "hbs_build.hpp"
+#include "idengine.hpp"
 #include "sbx.h"
 #include "update.hpp"
 
@@ -77,6 +78,47 @@ int sbx_sync(void) {
 }
 
 int64_t sbx_kernel_launches(int reset) { return sbx::launches(reset != 0); }
+
+int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
+               int64_t* k, int64_t* J, double* P) {
+  return guard([&] {
+    sbx::require(m >= 0 && n >= 0, "row_id: negative size");
+    if (forced < 0) sbx::require(eps > 0.0 && eps <= 0.1, "id tolerance must lie in (0, 0.1]");
+    cudaStream_t s = sbx::lib_stream();
+    if (m == 0 || n == 0 || (forced >= 0 && forced == 0)) {
+      *k = 0;
+      for (int64_t i = 0; i < m; ++i) J[i] = i;
+      return;
+    }
+    // W^T (n x m)
+    std::vector<double> wt(size_t(m * n));
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) wt[size_t(j + i * n)] = w[i + j * m];
+    sbx::DevBuf<double> d;
+    d.upload(wt, s);
+    sbx::IdBatch b;
+    b.force_engine = engine;
+    b.factor({{d.get(), int(n), int(m), int(n)}}, forced >= 0 ? 1e-15 : eps, s);
+    const int64_t kk = forced >= 0 ? b.forced_rank(0, forced) : b.eps_rank(0, eps);
+    *k = kk;
+    for (int64_t i = 0; i < m; ++i) J[i] = b.perm(0)[size_t(i)];
+    if (kk > 0) {
+      sbx::DevBuf<double> dp(size_t(m * kk));
+      b.interp({kk}, {dp.get()}, {int(m)}, s);
+      dp.download(P, size_t(m * kk), s);
+    }
+    SBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void* sbx_stream(void) {
+  try {
+    return static_cast<void*>(sbx::lib_stream());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 // ---------------------------------------------------------------- geometry
 int sbx_geom_create(const sbx_curve* curve, int n_panels, int q, sbx_geom* out) {

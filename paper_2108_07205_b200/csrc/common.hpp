@@ -44,6 +44,15 @@ void count_launch();
 std::int64_t launches(bool reset);
 cudaStream_t lib_stream();
 
+// Stream-ordered caching device allocator (the per-step path allocates many
+// short-lived blocks; cudaMalloc/cudaFree would serialise the device).
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+
+// Optional host-side phase timer (SBX_TIMING=1): syncs the stream and prints
+// the elapsed time since the previous mark to stderr.
+void phase_mark(const char* what, cudaStream_t s);
+
 // Owning device buffer.
 template <class T>
 class DevBuf {
@@ -70,7 +79,7 @@ class DevBuf {
   void resize(size_t n) {
     if (n == n_) return;
     release();
-    if (n) SBX_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    if (n) p_ = static_cast<T*>(dev_alloc(n * sizeof(T)));
     n_ = n;
   }
   // Grows (never shrinks) without preserving contents.
@@ -78,7 +87,7 @@ class DevBuf {
     if (n > n_) resize(n);
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) dev_free(p_, n_ * sizeof(T));
     p_ = nullptr;
     n_ = 0;
   }

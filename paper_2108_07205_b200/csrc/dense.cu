@@ -4,6 +4,7 @@
 // sizes of this workload).  GEMM tiles use FP64 tensor cores
 // (mma.sync.m8n8k4.f64 -> SASS DMMA).
 #include <cfloat>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -250,6 +251,9 @@ constexpr int kCT = 256;
 constexpr int kCWarps = kCT / 32;
 
 __device__ void group_barrier(CoopCtl* ctl, unsigned nblocks) {
+  // every thread publishes its own stores at gpu scope before arriving: a
+  // fence by the arriving thread alone does not drain other warps' stores
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* vg = &ctl->gen;
@@ -469,31 +473,35 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
 }
 
 // ---------------------------------------------------------------- interpolation
-__global__ void __launch_bounds__(256) interp_kernel(const InterpJob* __restrict__ jobs) {
-  const InterpJob jb = jobs[blockIdx.x];
+// One work item = (job, first column of a 128-column chunk of R12), or
+// (job, -1) for the k identity rows.  Every row of P is written exactly once,
+// so P needs no zero fill.
+constexpr int kIT = 128;
+
+__global__ void __launch_bounds__(kIT) interp_kernel(const InterpJob* __restrict__ jobs,
+                                                    const int2* __restrict__ items) {
+  const int2 it = items[blockIdx.x];
+  const InterpJob jb = jobs[it.x];
   const int n = jb.n, k = jb.k, nk = n - k;
-  // zero P, then identity rows and T rows
-  for (i64 idx = threadIdx.x; idx < i64(n) * k; idx += blockDim.x) {
-    const i64 r = idx % n, c = idx / n;
-    jb.P[r + c * jb.ldp] = 0.0;
+  if (it.y < 0) {  // P(J_i, :) = e_i
+    for (i64 idx = threadIdx.x; idx < i64(k) * k; idx += kIT) {
+      const int i = int(idx % k), c = int(idx / k);
+      jb.P[jb.perm[i] + size_t(c) * jb.ldp] = i == c ? 1.0 : 0.0;
+    }
+    return;
   }
   const int* cm = jb.colmap;
-  for (int j = threadIdx.x; j < nk; j += blockDim.x) {
-    const double* R = jb.a;
-    const size_t cj = size_t(cm ? cm[k + j] : k + j);
-    for (int i = k - 1; i >= 0; --i) {
-      double s = R[i + cj * jb.lda];
-      for (int l = i + 1; l < k; ++l)
-        s -= R[i + size_t(cm ? cm[l] : l) * jb.lda] * jb.T[size_t(l) * nk + j];
-      jb.T[size_t(i) * nk + j] = s / R[i + size_t(cm ? cm[i] : i) * jb.lda];
-    }
+  const int j = it.y + threadIdx.x;
+  if (j >= nk) return;
+  const double* R = jb.a;
+  const size_t cj = size_t(cm ? cm[k + j] : k + j);
+  for (int i = k - 1; i >= 0; --i) {  // back substitution R11 t = r12 (T row-major [i][j])
+    double s = R[i + cj * jb.lda];
+    for (int l = i + 1; l < k; ++l) s -= R[i + size_t(cm ? cm[l] : l) * jb.lda] * jb.T[size_t(l) * nk + j];
+    jb.T[size_t(i) * nk + j] = s / R[i + size_t(cm ? cm[i] : i) * jb.lda];
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x) jb.P[jb.perm[i] + size_t(i) * jb.ldp] = 1.0;
-  for (i64 idx = threadIdx.x; idx < i64(nk) * k; idx += blockDim.x) {
-    const int j = int(idx % nk), i = int(idx / nk);
-    jb.P[jb.perm[k + j] + size_t(i) * jb.ldp] = jb.T[size_t(i) * nk + j];
-  }
+  double* prow = jb.P + jb.perm[k + j];
+  for (int i = 0; i < k; ++i) prow[size_t(i) * jb.ldp] = jb.T[size_t(i) * nk + j];
 }
 
 // ---------------------------------------------------------------- GEMM (DMMA)
@@ -977,22 +985,31 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     attr = true;
   }
   std::vector<int> G(jobs.size(), 1);
-  int per_sm = 1;
-  for (int iter = 0; iter < 3; ++iter) {
-    const size_t smem = smem_for(G);
-    require(smem <= kSmemCap, "cpqr_coop: problem too tall for the shared-memory Householder vector");
-    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCT, smem));
-    per_sm = std::max(1, std::min(per_sm, 2));
-    const int T = std::max(int(jobs.size()), sms * per_sm);
+  auto split = [&](int T) {
     int used = 0;
     for (size_t q = 0; q < jobs.size(); ++q) {
       const double w = double(jobs[q].M) * double(jobs[q].n) / W;
       G[q] = std::max(1, std::min(jobs[q].n, int(std::floor(w * (T - int(jobs.size())))) + 1));
       used += G[q];
     }
-    require(used <= sms * per_sm, "cpqr_coop: too many concurrent problems for one cooperative launch");
+    return used;
+  };
+  int per_sm = 1;
+  require(int(jobs.size()) <= sms, "cpqr_coop: too many concurrent problems for one cooperative launch");
+  split(sms);
+  for (int iter = 0; iter < 2; ++iter) {
+    const size_t smem = smem_for(G);
+    require(smem <= kSmemCap, "cpqr_coop: problem too tall for the shared-memory Householder vector");
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCT, smem));
+    per_sm = std::max(1, std::min(per_sm, 2));
+    const int used = split(sms * per_sm);
+    if (used > sms * per_sm || smem_for(G) > smem) split(sms);  // stay co-resident
+  }
+  if (const char* cap = std::getenv("SBX_COOP_MAXG")) {  // debugging aid
+    for (auto& g : G) g = std::max(1, std::min(g, std::atoi(cap)));
   }
   const size_t smem = smem_for(G);
+  require(smem <= kSmemCap, "cpqr_coop: problem too tall for the shared-memory Householder vector");
   std::vector<int> cta_job, cta_rank, part_off(jobs.size());
   std::vector<i64> beta_off(jobs.size());
   i64 boff = 0;
@@ -1043,8 +1060,15 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
 void interp_batched(const std::vector<InterpJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
   static thread_local JobTable<InterpJob> tab;
+  static thread_local JobTable<int2> itab;
+  std::vector<int2> items;
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    items.push_back(make_int2(int(q), -1));
+    for (int c = 0; c < jobs[q].n - jobs[q].k; c += kIT) items.push_back(make_int2(int(q), c));
+  }
   const InterpJob* d = tab.upload(jobs, s);
-  interp_kernel<<<unsigned(jobs.size()), 256, 0, s>>>(d);
+  const int2* di = itab.upload(items, s);
+  interp_kernel<<<unsigned(items.size()), kIT, 0, s>>>(d, di);
   SBX_LAUNCHED();
 }
 

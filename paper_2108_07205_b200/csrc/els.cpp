@@ -113,6 +113,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
       hbs_invert_device(*e->app_h, s);
     }
   }
+  phase_mark("els: A_pp", s);
   e->k = upd.k;
   const i64 k = e->k, n = e->n_ext();
   if (k > 0) {
@@ -120,6 +121,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
     SBX_CUDA(cudaMemcpyAsync(e->R.get(), upd.R.get(), size_t(k * n) * 8, cudaMemcpyDeviceToDevice, s));
     e->X.resize(size_t(n * k));
     atilde_solve(*e, upd.L.get(), n, e->X.get(), n, k, s);
+    phase_mark("els: X = Atilde^-1 L", s);
     // W = I + R X  (els.cpp:124)
     e->Wmat.resize(size_t(k * k));
     gemm_batched({{e->R.get(), e->X.get(), e->Wmat.get(), int(k), int(k), int(n), int(k), int(n), int(k), 0,
@@ -136,6 +138,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
                   "mode at woodbury solve");
   }
   SBX_CUDA(cudaStreamSynchronize(s));
+  phase_mark("els: W, LU(W)", s);
   return e;
 }
 

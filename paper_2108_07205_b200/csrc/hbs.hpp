@@ -72,6 +72,7 @@ struct HbsOp {
   i64 arena_used = 0;
   SweepPlan solve_plan, apply_plan;
   DevBuf<double> ws;  // sweep workspace (grown on demand)
+  DevBuf<double> io;  // staging for host-pointer sweeps (grown on demand)
 
   i64 total_skeleton() const {
     i64 t = 0;

@@ -36,7 +36,9 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
     j.steps = d_steps_.get() + p;
     // one CTA per problem unless the factorisation would stream megabytes
     // through a single SM; those go to the cooperative multi-CTA kernel
-    if (i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows) {
+    const bool coop = force_engine == 2 ||
+                      (force_engine == 0 && i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows);
+    if (coop) {
       coop_[p] = 1;
       big.push_back(j);
     } else {

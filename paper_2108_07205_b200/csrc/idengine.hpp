@@ -21,6 +21,8 @@ class IdBatch {
   // CPQR of every problem; stop_eps truncates at |r_jj| <= stop_eps*|r_00|
   // (1e-15 keeps every row the forced-rank rule can ask for).
   void factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s);
+  // engine override for tests: 0 auto, 1 one CTA per problem, 2 cooperative
+  int force_engine = 0;
   size_t size() const { return probs_.size(); }
   const IdProblem& problem(size_t p) const { return probs_[p]; }
   // idlib.cpp:47-51: #{ |r_kk| > eps |r_00| }

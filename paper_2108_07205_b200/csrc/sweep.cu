@@ -410,22 +410,21 @@ void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, d
   if (nrhs == 0) return;
   op.ws.reserve(size_t(plan.ws_rows * nrhs));
   double* ws = op.ws.get();
-  DevBuf<double> hb, hx;
   const double* bd = b;
   double* xd = x;
   if (!dev) {
-    hb.resize(size_t(op.n * nrhs));
-    hx.resize(size_t(op.n * nrhs));
-    SBX_CUDA(cudaMemcpy2DAsync(hb.get(), size_t(op.n) * 8, b, size_t(ldb) * 8, size_t(op.n) * 8,
+    op.io.reserve(size_t(2 * op.n * nrhs));
+    double* hb = op.io.get();
+    SBX_CUDA(cudaMemcpy2DAsync(hb, size_t(op.n) * 8, b, size_t(ldb) * 8, size_t(op.n) * 8,
                                size_t(nrhs), cudaMemcpyHostToDevice, s));
-    bd = hb.get();
-    xd = hx.get();
+    bd = hb;
+    xd = hb + op.n * nrhs;
   }
   launch_cm_to_rm(bd, dev ? ldb : op.n, op.n, nrhs, ws + plan.in_row * nrhs, nullptr, s);
   hbs_run_plan(op, plan, ws, nrhs, s);
   launch_rm_to_cm(ws + plan.out_row * nrhs, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, s);
   if (!dev) {
-    SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, hx.get(), size_t(op.n) * 8, size_t(op.n) * 8,
+    SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, xd, size_t(op.n) * 8, size_t(op.n) * 8,
                                size_t(nrhs), cudaMemcpyDeviceToHost, s));
     SBX_CUDA(cudaStreamSynchronize(s));
   }

@@ -461,7 +461,9 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
       }
     }
   }
+  phase_mark("update: setup", s);
   RowIdResult far = compress_block_far(enew.view(), ng, far_nodes, circles, true, with_null, ktree, eps, s);
+  phase_mark("update: far ID (kept)", s);
   const std::vector<i64> far_s = scalars(far_pos), near_s = scalars(near_pos);
   // kept-row blocks kc (old oracle) and kp (new oracle)  (lowrank.cpp:130-180)
   const std::vector<i64> kept_old_s = scalars(plan.kept_old), kept_new_s = scalars(plan.kept_new);
@@ -488,7 +490,9 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     return f;
   };
   KeptFactor kc = kept_factor(eold, kept_old_s, cut_s, "kc");
+  phase_mark("update: kc near ID", s);
   KeptFactor kp = kept_factor(enew, kept_new_s, added_s, "kp");
+  phase_mark("update: kp near ID", s);
   // added rows against the division surface (lowrank.cpp:296-308, 183-238)
   RowIdResult pk_far;
   if (!plan.added_new.empty()) {
@@ -500,12 +504,14 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     }
     pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, s);
   }
+  phase_mark("update: pk far ID", s);
   RowIdResult pk_near;
   i64 k_pk = 0;
   if (u->np2 > 0 && u->nk2 > 0) {
     pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, u->notes, "pk", s);
     k_pk = pk_far.k + pk_near.k;
   }
+  phase_mark("update: pk near ID", s);
   u->k_kc = kc.k;
   u->k_kp = kp.k;
   u->k_pk = k_pk;
@@ -594,12 +600,14 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     launch_block_jobs(enew.view(), jb.get(), int(jn.size()), mn, c.get(), d.get(), R1.get(), s, e.get());
     SBX_CUDA(cudaStreamSynchronize(s));
   }
+  phase_mark("update: L1/R1 assembly", s);
   // final row ID of L1 (see header): CPQR of L1^T (k1 x n_ext)
   DevBuf<double> L1T(static_cast<size_t>(k1 * n_ext));
   copy_batched({{L1.get(), L1T.get(), int(k1), int(n_ext), ldl, int(k1), 1, 0}}, s);
   IdBatch fin;
   fin.factor({{L1T.get(), int(k1), int(n_ext), int(k1)}}, eps, s);
   u->k = fin.eps_rank(0, eps);
+  phase_mark("update: final ID of L1", s);
   const i64 k = u->k;
   u->skeleton.assign(fin.perm(0).begin(), fin.perm(0).begin() + k);
   u->L.resize(size_t(std::max<i64>(n_ext * k, 1)));
@@ -616,6 +624,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
                  s);
   }
   SBX_CUDA(cudaStreamSynchronize(s));
+  phase_mark("update: L, R", s);
   return u;
 }
 

@@ -1,0 +1,79 @@
+"""Device ID engine (dense.cu qr_kernel / cpqr_coop_kernel + interp) against
+the oracle's restatement of idlib.cpp and the reference's own ID assertions
+(test_idlib.cpp)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sb():
+    import paper_2108_07205_b200 as sb
+    sb.init(0)
+    return sb
+
+
+def spectrum_matrix(m, n, sv, rng):
+    u = np.linalg.qr(rng.standard_normal((m, len(sv))))[0]
+    v = np.linalg.qr(rng.standard_normal((n, len(sv))))[0]
+    return (u * sv) @ v.T
+
+
+def skeleton_identity_exact(k, J, P):
+    return all(P[J[i], j] == (1.0 if i == j else 0.0) for i in range(k) for j in range(k))
+
+
+SHAPES = [(50, 30), (200, 100), (128, 700), (300, 5000), (2500, 300)]
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_row_id_matches_oracle(sb, po, engine, shape):
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=engine)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_row_id_forced_rank(sb, po, engine):  # test_idlib.cpp:203-222
+    rng = np.random.default_rng(31)
+    w = spectrum_matrix(60, 40, 10.0 ** (-0.5 * np.arange(30)), rng)
+    kb, Jb, Pb = sb.row_id(w, 1e-6, engine=engine)
+    kw, Jw, Pw = sb.row_id(w, forced=kb + 5, engine=engine)
+    assert kw == kb + 5 and np.array_equal(Jw[:kb], Jb[:kb])
+    low = w[:, :3] @ rng.uniform(-1, 1, (3, 25))
+    kf, Jf, Pf = sb.row_id(low, forced=10, engine=engine)
+    assert kf <= 4
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_row_id_deterministic(sb, engine):
+    rng = np.random.default_rng(9)
+    w = spectrum_matrix(1200, 512, 10.0 ** (-12 * np.arange(512) / 512), rng)
+    first = sb.row_id(w, 1e-10, engine=engine)
+    for _ in range(4):
+        again = sb.row_id(w, 1e-10, engine=engine)
+        assert again[0] == first[0]
+        assert np.array_equal(again[1], first[1]) and np.array_equal(again[2], first[2])
+
+
+def test_row_id_edge_cases(sb):  # test_idlib.cpp:63-113
+    k, J, P = sb.row_id(np.eye(20), 1e-10)
+    assert k == 20 and skeleton_identity_exact(k, J, P)
+    k, J, P = sb.row_id(np.zeros((8, 5)), 1e-10)
+    assert k == 0
+    rng = np.random.default_rng(7)
+    w = np.outer(rng.standard_normal(50), rng.standard_normal(30))
+    k, J, P = sb.row_id(w, 1e-10)
+    assert k == 1 and skeleton_identity_exact(k, J, P)
+    with pytest.raises(ValueError):
+        sb.row_id(np.eye(4), 0.5)
