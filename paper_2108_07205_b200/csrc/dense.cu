@@ -79,36 +79,82 @@ __device__ void block_argmax(double v, int idx, double* rv, int* ri, double& out
   out_i = idx;
 }
 
+// Applies the Householder reflector (1, v[j+1..M)) with tau to U columns at
+// once (U independent load streams per lane), then the xGEQPF norm
+// downdate of ColPivHouseholderQR for each.  col[u] == nullptr skips a slot.
+template <int U>
+__device__ __forceinline__ void reflect_cols(double* const (&col)[U], const int (&slot)[U],
+                                             const double* v, int j, int M, double tau, bool pivot,
+                                             double* upd, double* dir, double thr, int lane) {
+  if (M - j > 1 && tau != 0.0) {
+    double d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[u] = 0.0;
+    for (int i = j + 1 + lane; i < M; i += 32) {
+      const double vi = v[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col[u]) d[u] += vi * col[u][i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+    double tw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) tw[u] = col[u] ? tau * (d[u] + col[u][j]) : 0.0;
+    for (int i = j + 1 + lane; i < M; i += 32) {
+      const double vi = v[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col[u]) col[u][i] -= vi * tw[u];
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (col[u]) col[u][j] -= tw[u];
+    }
+    __syncwarp();
+  }
+  if (!pivot) return;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!col[u]) continue;
+    const double uu = upd[slot[u]];
+    __syncwarp();  // every lane has read upd before lane 0 rewrites it
+    if (uu == 0.0) continue;
+    double t = fabs(col[u][j]) / uu;
+    t = (1.0 + t) * (1.0 - t);
+    t = t < 0.0 ? 0.0 : t;
+    const double rr = uu / dir[slot[u]];
+    if (t * rr * rr <= thr) {
+      double sacc = 0.0;
+      for (int i = j + 1 + lane; i < M; i += 32) sacc += col[u][i] * col[u][i];
+      sacc = warp_sum(sacc);
+      __syncwarp();
+      if (lane == 0) upd[slot[u]] = dir[slot[u]] = sqrt(sacc);
+    } else if (lane == 0) {
+      upd[slot[u]] = uu * sqrt(t);
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- QR / CPQR
-__global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, int smem_doubles) {
-  extern __shared__ double sm[];
-  const QrJob jb = jobs[blockIdx.x];
-  const int M = jb.M, n = jb.n;
+// Householder QR of A (M x n, ld lda) by one CTA; with `pivot` it is
+// Eigen's ColPivHouseholderQR.  Returns the number of completed steps.
+// Scratch: upd, dir (n each), red (32), ired (32), sc (8).
+__device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps_max,
+                         double stop_eps, int* perm, double* diag, double* upd, double* dir,
+                         double* red, int* ired, double* sc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* upd = sm;
-  double* dir = upd + n;
-  double* red = dir + n;                       // 32
-  int* ired = reinterpret_cast<int*>(red + 32);  // 32
-  double* sc = red + 48;                       // shared scalars (8)
-  double* mat = sc + 8;
-  const size_t head = size_t(2 * n + 56);
-  const bool in_smem = head + size_t(M) * n <= size_t(smem_doubles);
-  double* A = jb.a;
-  int lda = jb.lda;
-  if (in_smem) {
-    for (int c = warp; c < n; c += kWarps)
-      for (int i = lane; i < M; i += 32) mat[i + size_t(c) * M] = jb.a[i + size_t(c) * jb.lda];
-    A = mat;
-    lda = M;
-  }
   const int size = min(M, n);
-  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
-  if (jb.pivot) {
-    for (int c = tid; c < n; c += kT) jb.perm[c] = c;
-  }
-  for (int c = tid; c < size; c += kT) jb.diag[c] = 0.0;
+  if (pivot)
+    for (int c = tid; c < n; c += kT) perm[c] = c;
+  for (int c = tid; c < size; c += kT) diag[c] = 0.0;
   __syncthreads();
-  if (jb.pivot) {
+  if (pivot) {
     for (int c = warp; c < n; c += kWarps) {
       double s = 0.0;
       for (int i = lane; i < M; i += 32) {
@@ -123,7 +169,7 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
   const double thr = sqrt(DBL_EPSILON);
   int done = 0;
   for (int j = 0; j < steps_max; ++j) {
-    if (jb.pivot) {
+    if (pivot) {
       double bv = -1.0;
       int bi = 0x7fffffff;
       for (int c = j + tid; c < n; c += kT) {
@@ -149,9 +195,9 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
           t = dir[j];
           dir[j] = dir[p];
           dir[p] = t;
-          const int q = jb.perm[j];
-          jb.perm[j] = jb.perm[p];
-          jb.perm[p] = q;
+          const int q = perm[j];
+          perm[j] = perm[p];
+          perm[p] = q;
         }
       }
       __syncthreads();
@@ -189,53 +235,150 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
     }
     if (tid == 0) {
       A[j + size_t(j) * lda] = beta;
-      jb.diag[j] = fabs(beta);
+      diag[j] = fabs(beta);
     }
     __syncthreads();
     done = j + 1;
-    if (jb.pivot && jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
-    // apply to the trailing columns, then downdate their norms
-    for (int c = j + 1 + warp; c < n; c += kWarps) {
-      double* col = A + size_t(c) * lda;
-      const double* v = A + size_t(j) * lda;
-      if (M - j > 1 && tau != 0.0) {
-        double d = 0.0;
-        for (int i = j + 1 + lane; i < M; i += 32) d += v[i] * col[i];
-        d = warp_sum(d) + col[j];
-        const double tw = tau * d;
-        for (int i = j + 1 + lane; i < M; i += 32) col[i] -= v[i] * tw;
-        __syncwarp();
-        if (lane == 0) col[j] -= tw;
-        __syncwarp();
+    if (pivot && stop_eps > 0.0 && !(fabs(beta) > stop_eps * r00)) break;
+    // apply to the trailing columns (4 per warp pass), then downdate their norms
+    for (int c = j + 1 + 4 * warp; c < n; c += 4 * kWarps) {
+      double* cols[4];
+      int slot[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cols[u] = c + u < n ? A + size_t(c + u) * lda : nullptr;
+        slot[u] = c + u;
       }
-      if (jb.pivot) {
-        const double u = upd[c];
-        __syncwarp();  // every lane has read upd[c] before lane 0 rewrites it
-        if (u != 0.0) {
-          double t = fabs(col[j]) / u;
-          t = (1.0 + t) * (1.0 - t);
-          t = t < 0.0 ? 0.0 : t;
-          const double rr = u / dir[c];
-          const double t2 = t * rr * rr;
-          if (t2 <= thr) {
-            double s = 0.0;
-            for (int i = j + 1 + lane; i < M; i += 32) s += col[i] * col[i];
-            s = warp_sum(s);
-            __syncwarp();
-            if (lane == 0) upd[c] = dir[c] = sqrt(s);
-          } else if (lane == 0) {
-            upd[c] = u * sqrt(t);
-          }
-        }
-      }
+      reflect_cols<4>(cols, slot, A + size_t(j) * lda, j, M, tau, pivot, upd, dir, thr, lane);
     }
     __syncthreads();
   }
+  return done;
+}
+
+__global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, int smem_doubles) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* upd = sm;
+  double* dir = upd + n;
+  double* red = dir + n;                         // 32
+  int* ired = reinterpret_cast<int*>(red + 32);  // 32
+  double* sc = red + 48;                         // shared scalars (8)
+  double* mat = sc + 8;
+  const size_t head = size_t(2 * n + 56);
+  const bool in_smem = head + size_t(M) * n <= size_t(smem_doubles);
+  double* A = jb.a;
+  int lda = jb.lda;
+  if (in_smem) {
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < M; i += 32) mat[i + size_t(c) * M] = jb.a[i + size_t(c) * jb.lda];
+    A = mat;
+    lda = M;
+  }
+  const int size = min(M, n);
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  const int done = cpqr_core(A, M, n, lda, jb.pivot != 0, steps_max, jb.stop_eps, jb.perm, jb.diag,
+                             upd, dir, red, ired, sc);
   if (tid == 0 && jb.steps) *jb.steps = done;
   if (in_smem) {
+    __syncthreads();
     for (int c = warp; c < n; c += kWarps)
       for (int i = lane; i < M; i += 32) jb.a[i + size_t(c) * jb.lda] = mat[i + size_t(c) * M];
   }
+}
+
+// Tall problems (M > n, n <= 144): a streaming TSQR first reduces W^T to its
+// n x n triangular factor R0 held in shared memory (row blocks of W^T are
+// folded into R0 one Householder column at a time), then the Eigen CPQR runs
+// on R0 in shared memory.  Column norms of R0 equal those of W^T, so the
+// pivot order, |r_jj| and R11^{-1} R12 are those of CPQR(W^T) in exact
+// arithmetic.  R (pivoted) is written to the first n rows of the job matrix.
+__global__ void __launch_bounds__(kT) tsqr_cpqr_kernel(const QrJob* __restrict__ jobs, int bm_max) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* upd = sm;
+  double* dir = upd + n;
+  double* red = dir + n;
+  int* ired = reinterpret_cast<int*>(red + 32);
+  double* sc = red + 48;
+  double* R = sc + 8;                 // n x n, ld n
+  double* B = R + size_t(n) * n;      // bm x n, ld bm_max
+  const int bm = bm_max;
+  for (int idx = tid; idx < n * n; idx += kT) R[idx] = 0.0;
+  __syncthreads();
+  for (int r0 = 0; r0 < M; r0 += bm) {
+    const int rb = min(bm, M - r0);
+    for (int c = warp; c < n; c += kWarps)
+      for (int i = lane; i < rb; i += 32) B[i + c * bm] = jb.a[(r0 + i) + size_t(c) * jb.lda];
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      if (warp == 0) {  // reflector of [R(j,j); B(:,j)]
+        double s = 0.0;
+        for (int i = lane; i < rb; i += 32) s += B[i + j * bm] * B[i + j * bm];
+        s = warp_sum(s);
+        const double c0 = R[j + j * n];
+        double tau = 0.0, beta = c0, denom = 0.0;
+        if (s > DBL_MIN) {
+          beta = sqrt(c0 * c0 + s);
+          if (c0 >= 0.0) beta = -beta;
+          denom = c0 - beta;
+          tau = (beta - c0) / beta;
+        }
+        for (int i = lane; i < rb; i += 32) B[i + j * bm] = denom == 0.0 ? 0.0 : B[i + j * bm] / denom;
+        if (lane == 0) {
+          R[j + j * n] = beta;
+          sc[0] = tau;
+        }
+      }
+      __syncthreads();
+      const double tau = sc[0];
+      if (tau != 0.0) {
+        for (int c = j + 1 + 4 * warp; c < n; c += 4 * kWarps) {
+          double d[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int i = lane; i < rb; i += 32) {
+            const double vi = B[i + j * bm];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + u < n) d[u] += vi * B[i + (c + u) * bm];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+          double tw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tw[u] = c + u < n ? tau * (d[u] + R[j + (c + u) * n]) : 0.0;
+          for (int i = lane; i < rb; i += 32) {
+            const double vi = B[i + j * bm];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + u < n) B[i + (c + u) * bm] -= vi * tw[u];
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (c + u < n) R[j + (c + u) * n] -= tw[u];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // zero the strictly lower part left by the streaming (R0 is upper triangular)
+  for (int idx = tid; idx < n * n; idx += kT)
+    if (idx % n > idx / n) R[idx] = 0.0;
+  __syncthreads();
+  const int steps_max = jb.max_steps > 0 ? min(n, jb.max_steps) : n;
+  const int done = cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
+                             red, ired, sc);
+  if (tid == 0 && jb.steps) *jb.steps = done;
+  __syncthreads();
+  for (int c = warp; c < n; c += kWarps)
+    for (int i = lane; i < n; i += 32) jb.a[i + size_t(c) * jb.lda] = R[i + size_t(c) * n];
 }
 
 // ---------------------------------------------------------------- cooperative CPQR
@@ -361,7 +504,9 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
           p0 = ired[w];
           q0 = wphys[w];
         }
-      parts[rank] = {v0, p0, q0};
+      // double-buffered by step parity: a CTA already in step j+1 must not
+      // overwrite a partial another CTA is still reading for step j
+      parts[(j & 1) * G + rank] = {v0, p0, q0};
     }
     group_barrier(ctl, unsigned(G));
     // previous pivot's diagonal, deferred so no CTA reads a half-written column
@@ -372,9 +517,10 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
     if (tid == 0) {
       double v0 = -1.0;
       int p0 = 0x7fffffff, q0 = -1;
+      const CoopPart* cur = parts + (j & 1) * G;
       for (int g = 0; g < G; ++g) {  // L1-bypassing loads: written by other CTAs
-        const double pv = __ldcg(&parts[g].val);
-        const int pp = __ldcg(&parts[g].pos), pq = __ldcg(&parts[g].phys);
+        const double pv = __ldcg(&cur[g].val);
+        const int pp = __ldcg(&cur[g].pos), pq = __ldcg(&cur[g].phys);
         if (pq >= 0 && better(pv, pp, v0, p0)) {
           v0 = pv;
           p0 = pp;
@@ -429,36 +575,16 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
     prev_beta = beta;
     done = j + 1;
     if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
-    for (int c = warp; c < nown; c += kCWarps) {
-      if (mypos[c] < 0) continue;
-      double* col = A + size_t(c0 + c) * lda;
-      if (M - j > 1 && tau != 0.0) {
-        double d = 0.0;
-        for (int i = j + 1 + lane; i < M; i += 32) d += v[i] * col[i];
-        d = warp_sum(d) + col[j];
-        const double tw = tau * d;
-        for (int i = j + 1 + lane; i < M; i += 32) col[i] -= v[i] * tw;
-        __syncwarp();
-        if (lane == 0) col[j] -= tw;
-        __syncwarp();
+    for (int c = 4 * warp; c < nown; c += 4 * kCWarps) {
+      double* cols[4];
+      int slot[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool live = c + u < nown && mypos[c + u] >= 0;
+        cols[u] = live ? A + size_t(c0 + c + u) * lda : nullptr;
+        slot[u] = c + u;
       }
-      const double u = upd[c];
-      __syncwarp();
-      if (u != 0.0) {
-        double t = fabs(col[j]) / u;
-        t = (1.0 + t) * (1.0 - t);
-        t = t < 0.0 ? 0.0 : t;
-        const double rr = u / dir[c];
-        if (t * rr * rr <= thr) {
-          double s = 0.0;
-          for (int i = j + 1 + lane; i < M; i += 32) s += col[i] * col[i];
-          s = warp_sum(s);
-          __syncwarp();
-          if (lane == 0) upd[c] = dir[c] = sqrt(s);
-        } else if (lane == 0) {
-          upd[c] = u * sqrt(t);
-        }
-      }
+      reflect_cols<4>(cols, slot, v, j, M, tau, true, upd, dir, thr, lane);
     }
     __syncthreads();
   }
@@ -760,115 +886,139 @@ __global__ void __launch_bounds__(kT) lu_kernel(const LuJob* __restrict__ jobs, 
     }
     __syncthreads();
   }
-  // explicit inverse: warp per identity column
-  if (jb.inv && n <= 32 * kMaxRowsPerLane) {
-    for (int c = warp; c < n; c += kWarps) {
-      double x[kMaxRowsPerLane];
-#pragma unroll
-      for (int q = 0; q < kMaxRowsPerLane; ++q) {
-        const int i = lane + 32 * q;
-        x[q] = (i < n && jb.piv[i] == c) ? 1.0 : 0.0;
-      }
-      warp_lu_solve(A, n, lda, x, lane);
-#pragma unroll
-      for (int q = 0; q < kMaxRowsPerLane; ++q) {
-        const int i = lane + 32 * q;
-        if (i < n) jb.inv[i + size_t(c) * n] = x[q];
+  // explicit inverse X = U^{-1} L^{-1} P by blocked triangular solves
+  // (16-row diagonal blocks, rank-16 trailing updates), CTA-wide
+  double* X = jb.inv;
+  const int n2 = n;
+  for (i64 idx = tid; idx < i64(n2) * n2; idx += kT) {
+    const int i = int(idx % n2), c = int(idx / n2);
+    X[idx] = jb.piv[i] == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  constexpr int BS = 16;
+  for (int kb = 0; kb < n; kb += BS) {  // L (unit lower)
+    const int be = min(kb + BS, n);
+    for (int c = tid; c < n; c += kT) {
+      double* xc = X + size_t(c) * n;
+      for (int i = kb + 1; i < be; ++i) {
+        double sacc = xc[i];
+        for (int l = kb; l < i; ++l) sacc -= A[i + size_t(l) * lda] * xc[l];
+        xc[i] = sacc;
       }
     }
+    __syncthreads();
+    const int rows = n - be;
+    for (i64 idx = tid; idx < i64(rows) * n; idx += kT) {
+      const int i = be + int(idx % rows), c = int(idx / rows);
+      double* xc = X + size_t(c) * n;
+      double sacc = xc[i];
+      for (int l = kb; l < be; ++l) sacc -= A[i + size_t(l) * lda] * xc[l];
+      xc[i] = sacc;
+    }
+    __syncthreads();
   }
-  // reciprocal condition estimate (Eigen ConditionEstimator.h), warp 0
-  if (jb.rcond && warp == 0 && n <= 32 * kMaxRowsPerLane) {
+  for (int kb = ((n - 1) / BS) * BS; kb >= 0; kb -= BS) {  // U
+    const int be = min(kb + BS, n);
+    for (int c = tid; c < n; c += kT) {
+      double* xc = X + size_t(c) * n;
+      for (int i = be - 1; i >= kb; --i) {
+        double sacc = xc[i];
+        for (int l = i + 1; l < be; ++l) sacc -= A[i + size_t(l) * lda] * xc[l];
+        xc[i] = sacc / A[i + size_t(i) * lda];
+      }
+    }
+    __syncthreads();
+    for (i64 idx = tid; idx < i64(kb) * n; idx += kT) {
+      const int i = int(idx % kb), c = int(idx / kb);
+      double* xc = X + size_t(c) * n;
+      double sacc = xc[i];
+      for (int l = kb; l < be; ++l) sacc -= A[i + size_t(l) * lda] * xc[l];
+      xc[i] = sacc;
+    }
+    __syncthreads();
+  }
+  // reciprocal condition estimate (Eigen ConditionEstimator.h) with the
+  // explicit inverse standing in for the LU solves
+  if (jb.rcond) {
+    __shared__ int s_flag;
+    double* v = jb.work;          // n
+    double* sg = jb.work + n;     // n
+    double* osg = jb.work + 2 * n;  // n
+    double* tmp = jb.work + 3 * n;  // n
+    auto gemv = [&](const double* x, double* y, bool trans) {  // y = X x or X^T x
+      if (!trans) {
+        for (int i = tid; i < n; i += kT) {
+          double a = 0.0;
+          for (int c = 0; c < n; ++c) a += X[i + size_t(c) * n] * x[c];
+          y[i] = a;
+        }
+      } else {
+        for (int c = warp; c < n; c += kWarps) {
+          double a = 0.0;
+          for (int i = lane; i < n; i += 32) a += X[i + size_t(c) * n] * x[i];
+          a = warp_sum(a);
+          if (lane == 0) y[c] = a;
+        }
+      }
+      __syncthreads();
+    };
+    auto l1sum = [&](const double* x) {
+      double a = 0.0;
+      for (int i = tid; i < n; i += kT) a += fabs(x[i]);
+      return block_sum(a, red);
+    };
     double result;
     if (l1 == 0.0) {
       result = 0.0;
     } else if (n == 1) {
       result = 1.0;
     } else {
-      double v[kMaxRowsPerLane], sv[kMaxRowsPerLane], old_sv[kMaxRowsPerLane];
-      auto perm_in = [&](double (&x)[kMaxRowsPerLane], const double* src) {
-        // x = P b : row i of PA = row piv[i] of A
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q) {
-          const int i = lane + 32 * q;
-          x[q] = i < n ? src[jb.piv[i]] : 0.0;
-        }
-      };
-      auto l1n = [&](const double (&x)[kMaxRowsPerLane]) {
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q)
-          if (lane + 32 * q < n) s += fabs(x[q]);
-        return warp_sum(s);
-      };
-      double* w = jb.work;  // 4n scratch in global
-      for (int i = lane; i < n; i += 32) w[i] = 1.0 / double(n);
-      __syncwarp();
-      perm_in(v, w);
-      warp_lu_solve(A, n, lda, v, lane);
-      double lower = l1n(v), old_lower = lower;
+      for (int i = tid; i < n; i += kT) tmp[i] = 1.0 / double(n);
+      __syncthreads();
+      gemv(tmp, v, false);
+      double lower = l1sum(v), old_lower = lower;
       int old_vmax = -1;
       for (int it = 0; it < 4; ++it) {
-        bool same = it > 0;
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q) {
-          sv[q] = v[q] < 0.0 ? -1.0 : 1.0;
-          if (lane + 32 * q < n && it > 0 && sv[q] != old_sv[q]) same = false;
+        int differs = 0;
+        for (int i = tid; i < n; i += kT) {
+          sg[i] = v[i] < 0.0 ? -1.0 : 1.0;
+          if (it > 0 && sg[i] != osg[i]) differs = 1;
         }
-        same = __all_sync(0xffffffffu, same);
-        if (same) break;
-        // v = (A^T)^{-1} sign : solve_t then unpermute  x = P^T z
-        double z[kMaxRowsPerLane];
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q) z[q] = sv[q];
-        warp_lu_solve_t(A, n, lda, z, lane);
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q) {
-          const int i = lane + 32 * q;
-          if (i < n) w[jb.piv[i]] = z[q];
-        }
-        __syncwarp();
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        if (differs) s_flag = 1;
+        __syncthreads();
+        if (it > 0 && s_flag == 0) break;
+        gemv(sg, tmp, true);
         double bv = -1.0;
         int bi = 0x7fffffff;
-        for (int i = lane; i < n; i += 32) {
-          const double a = fabs(w[i]);
-          if (a > bv) {
-            bv = a;
+        for (int i = tid; i < n; i += kT)
+          if (fabs(tmp[i]) > bv) {
+            bv = fabs(tmp[i]);
             bi = i;
           }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        __syncwarp();
-        if (bi == old_vmax) break;
-        for (int i = lane; i < n; i += 32) w[n + i] = i == bi ? 1.0 : 0.0;
-        __syncwarp();
-        perm_in(v, w + n);
-        warp_lu_solve(A, n, lda, v, lane);
-        lower = l1n(v);
+        double mv;
+        int vmax;
+        block_argmax(bv, bi, red, ired, mv, vmax);
+        if (vmax == old_vmax) break;
+        for (int i = tid; i < n; i += kT) v[i] = X[i + size_t(vmax) * n];
+        __syncthreads();
+        lower = l1sum(v);
         if (lower <= old_lower) break;
-#pragma unroll
-        for (int q = 0; q < kMaxRowsPerLane; ++q) old_sv[q] = sv[q];
-        old_vmax = bi;
+        for (int i = tid; i < n; i += kT) osg[i] = sg[i];
+        __syncthreads();
+        old_vmax = vmax;
         old_lower = lower;
       }
-      for (int i = lane; i < n; i += 32)
-        w[2 * n + i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
-      __syncwarp();
-      perm_in(v, w + 2 * n);
-      warp_lu_solve(A, n, lda, v, lane);
-      const double alt = 2.0 * l1n(v) / (3.0 * double(n));
+      for (int i = tid; i < n; i += kT)
+        tmp[i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
+      __syncthreads();
+      gemv(tmp, v, false);
+      const double alt = 2.0 * l1sum(v) / (3.0 * double(n));
       const double inv_norm = fmax(lower, alt);
       result = inv_norm == 0.0 ? 0.0 : (1.0 / inv_norm) / l1;
     }
-    if (lane == 0) *jb.rcond = result;
+    if (tid == 0) *jb.rcond = result;
   }
   __syncthreads();
   if (in_smem) {
@@ -939,26 +1089,54 @@ __global__ void add_identity_kernel(double* a, i64 lda, i64 n) {
 
 }  // namespace
 
+namespace {
+// Largest TSQR row block that fits next to the n x n factor.
+int tsqr_block_rows(int n) {
+  const size_t head = size_t(2 * n + 56 + n * n) * sizeof(double);
+  if (head >= kSmemCap) return 0;
+  const int bm = int((kSmemCap - head) / (size_t(n) * sizeof(double)));
+  return bm >= 32 ? std::min(bm, 128) : 0;
+}
+}  // namespace
+
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
-  static thread_local JobTable<QrJob> tab;
-  size_t need = 0;
-  for (const auto& j : jobs) {
-    const size_t sz = (size_t(2 * j.n + 56) + size_t(j.M) * j.n) * sizeof(double);
-    if (sz <= kSmemCap) need = std::max(need, sz);
-  }
-  size_t base = 0;
-  for (const auto& j : jobs) base = std::max(base, size_t(2 * j.n + 56) * sizeof(double));
-  need = std::max(need, base);
-  require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
+  static thread_local JobTable<QrJob> tab, ttab;
   static bool attr = false;
   if (!attr) {
     SBX_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
+    SBX_CUDA(cudaFuncSetAttribute(tsqr_cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
     attr = true;
   }
-  const QrJob* d = tab.upload(jobs, s);
-  qr_kernel<<<unsigned(jobs.size()), kT, need, s>>>(d, int(need / sizeof(double)));
+  std::vector<QrJob> plain, tall;
+  for (const auto& j : jobs) {
+    const bool tsqr = j.pivot && j.n <= 144 && j.M > j.n && tsqr_block_rows(j.n) > 0 &&
+                      (size_t(j.M) * j.n + 2 * j.n + 56) * sizeof(double) > kSmemCap;
+    (tsqr ? tall : plain).push_back(j);
+  }
+  if (!tall.empty()) {
+    int nmax = 0;
+    for (const auto& j : tall) nmax = std::max(nmax, j.n);
+    const int bm = tsqr_block_rows(nmax);
+    const size_t smem = size_t(2 * nmax + 56 + nmax * nmax + bm * nmax) * sizeof(double);
+    const QrJob* d = ttab.upload(tall, s);
+    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d, bm);
+    SBX_LAUNCHED();
+  }
+  if (plain.empty()) return;
+  size_t need = 0;
+  for (const auto& j : plain) {
+    const size_t sz = (size_t(2 * j.n + 56) + size_t(j.M) * j.n) * sizeof(double);
+    if (sz <= kSmemCap) need = std::max(need, sz);
+  }
+  size_t base = 0;
+  for (const auto& j : plain) base = std::max(base, size_t(2 * j.n + 56) * sizeof(double));
+  need = std::max(need, base);
+  require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
+  const QrJob* d = tab.upload(plain, s);
+  qr_kernel<<<unsigned(plain.size()), kT, need, s>>>(d, int(need / sizeof(double)));
   SBX_LAUNCHED();
 }
 
@@ -1001,7 +1179,7 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     const size_t smem = smem_for(G);
     require(smem <= kSmemCap, "cpqr_coop: problem too tall for the shared-memory Householder vector");
     SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, kCT, smem));
-    per_sm = std::max(1, std::min(per_sm, 2));
+    per_sm = std::max(1, std::min(per_sm, 4));
     const int used = split(sms * per_sm);
     if (used > sms * per_sm || smem_for(G) > smem) split(sms);  // stay co-resident
   }
@@ -1016,7 +1194,7 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   int poff = 0;
   for (size_t q = 0; q < jobs.size(); ++q) {
     part_off[q] = poff;
-    poff += G[q];
+    poff += 2 * G[q];
     beta_off[q] = boff;
     boff += std::min(jobs[q].M, jobs[q].n);
     for (int r = 0; r < G[q]; ++r) {
@@ -1129,7 +1307,8 @@ void lu_batched(const std::vector<LuJob>& jobs, cudaStream_t s) {
   static thread_local JobTable<LuJob> tab;
   size_t need = 64 * sizeof(double);
   for (const auto& j : jobs) {
-    require(j.n <= 32 * kMaxRowsPerLane, "lu_batched: matrix too large for the warp solver");
+    require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+    require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
     const size_t sz = (64 + size_t(j.n) * j.n) * sizeof(double);
     if (sz <= kSmemCap) need = std::max(need, sz);
   }

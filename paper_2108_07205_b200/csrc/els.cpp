@@ -25,7 +25,7 @@ std::vector<i64> scalars(const std::vector<i64>& nodes) {
 // Dense LU + explicit inverse + rcond (Eigen PartialPivLU::rcond) of an
 // n x n device matrix a (destroyed); returns rcond.
 double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
-  require(n <= 512, "dense block above 512 unknowns is not supported on the device path yet");
+  require(n <= 2048, "dense block above 2048 unknowns (els.hpp:40 limit)");
   DevBuf<int> piv(static_cast<size_t>(n));
   DevBuf<double> rc(1), work(static_cast<size_t>(4 * n));
   LuJob j{};

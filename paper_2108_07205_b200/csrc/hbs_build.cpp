@@ -342,6 +342,7 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
       cc[q] = B.col_cand(op->nodes[size_t(ids[q])]);
     }
     near_sets(B, ids, nc, nr);
+    phase_mark("hbs: near sets", s);
     for (size_t q = 0; q < L; ++q) {
       B.max_block = std::max<i64>(B.max_block, i64(rc[q].size()) * i64(nc[q].size()));
       B.max_block = std::max<i64>(B.max_block, i64(nr[q].size()) * i64(cc[q].size()));
@@ -354,50 +355,58 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
     std::vector<char> row_done(L, 0), col_done(L, 0);
     std::vector<size_t> active(L);
     for (size_t q = 0; q < L; ++q) active[q] = q;
+    // The first two sample counts are always both needed (hbs.cpp:201-206),
+    // so they run as one batch; later doublings only for unsettled boxes.
     for (int ns = 64; ns <= 2048 && !active.empty(); ns *= 2) {
+      const bool pair = ns == 64;
       std::vector<i64> aid;
       std::vector<int> ans;
       std::vector<std::vector<i64>> arc, acc, anc, anr;
-      for (size_t q : active) {
-        aid.push_back(ids[q]);
-        ans.push_back(ns);
-        arc.push_back(rc[q]);
-        acc.push_back(cc[q]);
-        anc.push_back(nc[q]);
-        anr.push_back(nr[q]);
-      }
+      for (int rep = 0; rep < (pair ? 2 : 1); ++rep)
+        for (size_t q : active) {
+          aid.push_back(ids[q]);
+          ans.push_back(ns << rep);
+          arc.push_back(rc[q]);
+          acc.push_back(cc[q]);
+          anc.push_back(nc[q]);
+          anr.push_back(nr[q]);
+        }
       auto R = std::make_unique<SampleRound>();
       build_round(B, aid, ans, arc, acc, anc, anr, *R);
       const int ridx = int(rounds.size());
+      const size_t na = active.size();
       std::vector<size_t> next;
-      for (size_t a = 0; a < active.size(); ++a) {
+      for (size_t a = 0; a < na; ++a) {
         const size_t q = active[a];
-        const i64 kr = R->ids.eps_rank(2 * a, o.eps), kc = R->ids.eps_rank(2 * a + 1, o.eps);
-        if (!row_done[q]) {
-          const bool settled = prev_kr[q] >= 0 && std::llabs(kr - prev_kr[q]) <= 2;
-          row_round[q] = ridx;
-          row_pi[q] = 2 * a;
-          prev_kr[q] = kr;
-          if (settled) row_done[q] = 1;
-        }
-        if (!col_done[q]) {
-          const bool settled = prev_kc[q] >= 0 && std::llabs(kc - prev_kc[q]) <= 2;
-          col_round[q] = ridx;
-          col_pi[q] = 2 * a + 1;
-          prev_kc[q] = kc;
-          if (settled) col_done[q] = 1;
+        for (int rep = 0; rep < (pair ? 2 : 1); ++rep) {
+          const size_t pa = a + size_t(rep) * na;
+          const i64 kr = R->ids.eps_rank(2 * pa, o.eps), kc = R->ids.eps_rank(2 * pa + 1, o.eps);
+          if (!row_done[q]) {
+            const bool settled = prev_kr[q] >= 0 && std::llabs(kr - prev_kr[q]) <= 2;
+            row_round[q] = ridx;
+            row_pi[q] = 2 * pa;
+            prev_kr[q] = kr;
+            if (settled) row_done[q] = 1;
+          }
+          if (!col_done[q]) {
+            const bool settled = prev_kc[q] >= 0 && std::llabs(kc - prev_kc[q]) <= 2;
+            col_round[q] = ridx;
+            col_pi[q] = 2 * pa + 1;
+            prev_kc[q] = kc;
+            if (settled) col_done[q] = 1;
+          }
         }
         if (!row_done[q] || !col_done[q]) next.push_back(q);
       }
       rounds.push_back(std::move(R));
-      // keep only problems still needed: a finished side is not recomputed
-      // but its node stays in the batch while the other side is active
+      if (pair) ns *= 2;  // 64 and 128 done
       active = next;
     }
     for (size_t q = 0; q < L; ++q) {
       if (!row_done[q]) op->notes.push_back("hbs row: proxy sample cap reached");
       if (!col_done[q]) op->notes.push_back("hbs col: proxy sample cap reached");
     }
+    phase_mark("hbs: sample rounds (W^T + CPQR)", s);
     // rank equalisation (hbs.cpp:309-314)
     std::vector<i64> kfin(L);
     for (size_t q = 0; q < L; ++q) {
@@ -493,8 +502,10 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
       SBX_CUDA(cudaStreamSynchronize(s));
     }
     stores[size_t(depth)] = std::move(st);
+    phase_mark("hbs: interp + b_sib", s);
     SBX_CUDA(cudaStreamSynchronize(s));
   }
+  phase_mark("hbs: levels done", s);
   op->max_block_drawn = B.max_block;
   // final arena: layout by ranks, then place u, v, v^T, d, b_sib
   hbs_layout(*op);
@@ -613,6 +624,7 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
                            std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
                            std::to_string(nd.depth));
     }
+    phase_mark("inv: x blocks + LU/inverse", s);
     if (depth == 0) break;  // the root keeps only root_g (hbs.cpp:450-458)
     // t = v^T xi (k x c), tu = t u (k x k)
     std::vector<GemmJob> g1, g2;
@@ -683,8 +695,10 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
       g4.push_back({A + nd.o_e, S + to[q], A + nd.o_fg + k, c, c, k, c, k, k + c, 0, 0, -1.0, 1.0});
     }
     gemm_batched(g4, s);
+    phase_mark("inv: skeleton LU + e,f,g GEMMs", s);
     SBX_CUDA(cudaStreamSynchronize(s));
   }
+  phase_mark("inv: done", s);
   op.has_inverse = true;
   op.solve_plan.built = false;
 }

@@ -44,132 +44,170 @@ struct Chunk {
 
 // hierarchical_row_id (proxy.cpp:193-247) / chunked near_row_id
 // (lowrank.cpp:76-124): leaf IDs, then pairwise merges of skeleton rows.
-RowIdResult hierarchical_id(i64 m, const std::vector<std::vector<i64>>& leaves,
-                            const WtBuilder& build, double eps, cudaStream_t s) {
+// Several independent hierarchies over the same leaves (one W^T builder
+// each, e.g. two proxy sample counts) advance in lockstep so every level
+// is one batched CPQR launch.
+std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vector<i64>>& leaves,
+                                               const std::vector<WtBuilder>& builds, double eps,
+                                               cudaStream_t s) {
+  const size_t H = builds.size();
   std::vector<std::unique_ptr<DevBuf<double>>> keep;
-  std::vector<Chunk> level;
+  std::vector<std::vector<Chunk>> level(H);
+  // leaves
   {
-    std::vector<IdProblem> probs;
-    auto buf = std::make_unique<DevBuf<double>>();
-    build(leaves, probs, *buf);
-    IdBatch ids;
-    ids.factor(probs, eps, s);
-    auto pb = std::make_unique<DevBuf<double>>();
-    std::vector<i64> ks(leaves.size()), off(leaves.size());
-    i64 tot = 0;
-    for (size_t q = 0; q < leaves.size(); ++q) {
-      ks[q] = ids.eps_rank(q, eps);
-      off[q] = tot;
-      tot += i64(leaves[q].size()) * ks[q];
+    std::vector<IdProblem> all;
+    for (size_t h = 0; h < H; ++h) {
+      std::vector<IdProblem> probs;
+      auto buf = std::make_unique<DevBuf<double>>();
+      builds[h](leaves, probs, *buf);
+      all.insert(all.end(), probs.begin(), probs.end());
+      keep.push_back(std::move(buf));
     }
-    pb->resize(size_t(std::max<i64>(tot, 1)));
-    std::vector<double*> P(leaves.size());
-    std::vector<int> ldp(leaves.size());
-    for (size_t q = 0; q < leaves.size(); ++q) {
-      P[q] = pb->get() + off[q];
-      ldp[q] = std::max<int>(1, int(leaves[q].size()));
+    IdBatch ids;
+    ids.factor(all, eps, s);
+    const size_t L = leaves.size();
+    std::vector<i64> ks(all.size()), off(all.size());
+    i64 tot = 0;
+    for (size_t p = 0; p < all.size(); ++p) {
+      ks[p] = ids.eps_rank(p, eps);
+      off[p] = tot;
+      tot += i64(leaves[p % L].size()) * ks[p];
+    }
+    auto pb = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(tot, 1)));
+    std::vector<double*> P(all.size());
+    std::vector<int> ldp(all.size());
+    for (size_t p = 0; p < all.size(); ++p) {
+      P[p] = pb->get() + off[p];
+      ldp[p] = std::max<int>(1, int(leaves[p % L].size()));
     }
     ids.interp(ks, P, ldp, s);
-    for (size_t q = 0; q < leaves.size(); ++q) {
+    for (size_t p = 0; p < all.size(); ++p) {
+      const size_t q = p % L;
       Chunk c;
       c.rows = leaves[q];
-      c.k = ks[q];
-      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(leaves[q][size_t(ids.perm(q)[size_t(i)])]);
-      c.P = P[q];
-      level.push_back(std::move(c));
+      c.k = ks[p];
+      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(leaves[q][size_t(ids.perm(p)[size_t(i)])]);
+      c.P = P[p];
+      level[p / L].push_back(std::move(c));
     }
     SBX_CUDA(cudaStreamSynchronize(s));
-    keep.push_back(std::move(buf));
     keep.push_back(std::move(pb));
   }
-  while (level.size() > 1) {
-    const size_t npair = level.size() / 2;
-    std::vector<std::vector<i64>> unis(npair);
-    for (size_t q = 0; q < npair; ++q) {
-      unis[q] = level[2 * q].skel;
-      unis[q].insert(unis[q].end(), level[2 * q + 1].skel.begin(), level[2 * q + 1].skel.end());
+  for (;;) {
+    bool any = false;
+    for (size_t h = 0; h < H; ++h) any |= level[h].size() > 1;
+    if (!any) break;
+    std::vector<IdProblem> all;
+    std::vector<std::vector<std::vector<i64>>> unis(H);
+    std::vector<size_t> first(H, 0);
+    for (size_t h = 0; h < H; ++h) {
+      first[h] = all.size();
+      const size_t npair = level[h].size() / 2;
+      unis[h].resize(npair);
+      for (size_t q = 0; q < npair; ++q) {
+        unis[h][q] = level[h][2 * q].skel;
+        unis[h][q].insert(unis[h][q].end(), level[h][2 * q + 1].skel.begin(),
+                          level[h][2 * q + 1].skel.end());
+      }
+      if (npair == 0) continue;
+      std::vector<IdProblem> probs;
+      auto buf = std::make_unique<DevBuf<double>>();
+      builds[h](unis[h], probs, *buf);
+      all.insert(all.end(), probs.begin(), probs.end());
+      keep.push_back(std::move(buf));
     }
-    std::vector<IdProblem> probs;
-    auto buf = std::make_unique<DevBuf<double>>();
-    build(unis, probs, *buf);
     IdBatch ids;
-    ids.factor(probs, eps, s);
-    std::vector<i64> ks(npair), ioff(npair), poff(npair);
+    ids.factor(all, eps, s);
+    std::vector<i64> ks(all.size()), ioff(all.size()), poff(all.size());
     i64 itot = 0, ptot = 0;
-    for (size_t q = 0; q < npair; ++q) {
-      ks[q] = ids.eps_rank(q, eps);
-      ioff[q] = itot;
-      itot += i64(unis[q].size()) * ks[q];
-      poff[q] = ptot;
-      ptot += i64(level[2 * q].rows.size() + level[2 * q + 1].rows.size()) * ks[q];
-    }
+    for (size_t h = 0; h < H; ++h)
+      for (size_t q = 0; q < unis[h].size(); ++q) {
+        const size_t p = first[h] + q;
+        ks[p] = ids.eps_rank(p, eps);
+        ioff[p] = itot;
+        itot += i64(unis[h][q].size()) * ks[p];
+        poff[p] = ptot;
+        ptot += i64(level[h][2 * q].rows.size() + level[h][2 * q + 1].rows.size()) * ks[p];
+      }
     auto ib = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(itot, 1)));
     auto pb = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(ptot, 1)));
-    std::vector<double*> IP(npair);
-    std::vector<int> ldi(npair);
-    for (size_t q = 0; q < npair; ++q) {
-      IP[q] = ib->get() + ioff[q];
-      ldi[q] = std::max<int>(1, int(unis[q].size()));
-    }
+    std::vector<double*> IP(all.size());
+    std::vector<int> ldi(all.size());
+    for (size_t h = 0; h < H; ++h)
+      for (size_t q = 0; q < unis[h].size(); ++q) {
+        const size_t p = first[h] + q;
+        IP[p] = ib->get() + ioff[p];
+        ldi[p] = std::max<int>(1, int(unis[h][q].size()));
+      }
     ids.interp(ks, IP, ldi, s);
     std::vector<GemmJob> gj;
-    std::vector<Chunk> next;
-    for (size_t q = 0; q < npair; ++q) {
-      const Chunk& a = level[2 * q];
-      const Chunk& b = level[2 * q + 1];
-      Chunk c;
-      c.rows = a.rows;
-      c.rows.insert(c.rows.end(), b.rows.begin(), b.rows.end());
-      c.k = ks[q];
-      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(unis[q][size_t(ids.perm(q)[size_t(i)])]);
-      double* P = pb->get() + poff[q];
-      c.P = P;
-      const int ra = int(a.rows.size()), rb = int(b.rows.size()), ld = ra + rb;
-      const int ka = int(a.skel.size()), kb = int(b.skel.size()), k = int(c.k);
-      if (k > 0) {
-        // out.P = [a.P * id.P(0:ka, :); b.P * id.P(ka:, :)]  (proxy.cpp:187-189)
-        if (ka > 0)
-          gj.push_back({a.P, IP[q], P, ra, k, ka, std::max(ra, 1), ldi[q], ld, 0, 0, 1.0, 0.0});
-        if (kb > 0)
-          gj.push_back({b.P, IP[q] + ka, P + ra, rb, k, kb, std::max(rb, 1), ldi[q], ld, 0, 0, 1.0, 0.0});
-        if (ka == 0 || kb == 0) SBX_CUDA(cudaMemsetAsync(P, 0, size_t(ld) * k * 8, s));
+    for (size_t h = 0; h < H; ++h) {
+      std::vector<Chunk> next;
+      for (size_t q = 0; q < unis[h].size(); ++q) {
+        const size_t p = first[h] + q;
+        const Chunk& a = level[h][2 * q];
+        const Chunk& b = level[h][2 * q + 1];
+        Chunk c;
+        c.rows = a.rows;
+        c.rows.insert(c.rows.end(), b.rows.begin(), b.rows.end());
+        c.k = ks[p];
+        for (i64 i = 0; i < c.k; ++i) c.skel.push_back(unis[h][q][size_t(ids.perm(p)[size_t(i)])]);
+        double* P = pb->get() + poff[p];
+        c.P = P;
+        const int ra = int(a.rows.size()), rb = int(b.rows.size()), ld = ra + rb;
+        const int ka = int(a.skel.size()), kb = int(b.skel.size()), k = int(c.k);
+        if (k > 0) {
+          // out.P = [a.P * id.P(0:ka, :); b.P * id.P(ka:, :)]  (proxy.cpp:187-189)
+          if (ka == 0 || kb == 0) SBX_CUDA(cudaMemsetAsync(P, 0, size_t(ld) * k * 8, s));
+          if (ka > 0)
+            gj.push_back({a.P, IP[p], P, ra, k, ka, std::max(ra, 1), ldi[p], ld, 0, 0, 1.0, 0.0});
+          if (kb > 0)
+            gj.push_back({b.P, IP[p] + ka, P + ra, rb, k, kb, std::max(rb, 1), ldi[p], ld, 0, 0, 1.0, 0.0});
+        }
+        next.push_back(std::move(c));
       }
-      next.push_back(std::move(c));
+      if (level[h].size() % 2 == 1) next.push_back(level[h].back());
+      if (!unis[h].empty()) level[h] = std::move(next);
     }
-    // zero-fill above must precede the products of the same chunk
     gemm_batched(gj, s);
-    if (level.size() % 2 == 1) next.push_back(level.back());
-    level = std::move(next);
     SBX_CUDA(cudaStreamSynchronize(s));
-    keep.push_back(std::move(buf));
     keep.push_back(std::move(ib));
     keep.push_back(std::move(pb));
   }
-  RowIdResult out;
-  out.m = m;
-  if (level.empty()) {
-    out.J.resize(size_t(m));
-    std::iota(out.J.begin(), out.J.end(), i64(0));
-    return out;
+  std::vector<RowIdResult> outs(H);
+  for (size_t h = 0; h < H; ++h) {
+    RowIdResult& out = outs[h];
+    out.m = m;
+    if (level[h].empty()) {
+      out.J.resize(size_t(m));
+      std::iota(out.J.begin(), out.J.end(), i64(0));
+      continue;
+    }
+    const Chunk& root = level[h].front();
+    out.k = root.k;
+    out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
+    if (out.k > 0) {
+      SBX_CUDA(cudaMemsetAsync(out.P.get(), 0, size_t(m * out.k) * 8, s));
+      DevBuf<i64> map;
+      map.upload(root.rows, s);
+      scatter_batched({{root.P, out.P.get(), map.get(), int(root.rows.size()), int(out.k),
+                        std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0}},
+                      s);
+      SBX_CUDA(cudaStreamSynchronize(s));
+    }
+    out.J = root.skel;
+    std::vector<char> in(size_t(m), 0);
+    for (i64 x : root.skel) in[size_t(x)] = 1;
+    for (i64 x : root.rows)
+      if (!in[size_t(x)]) out.J.push_back(x);
   }
-  const Chunk& root = level.front();
-  out.k = root.k;
-  out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
-  if (out.k > 0) {
-    SBX_CUDA(cudaMemsetAsync(out.P.get(), 0, size_t(m * out.k) * 8, s));
-    DevBuf<i64> map;
-    map.upload(root.rows, s);
-    scatter_batched({{root.P, out.P.get(), map.get(), int(root.rows.size()), int(out.k),
-                      std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0}},
-                    s);
-    SBX_CUDA(cudaStreamSynchronize(s));
-  }
-  out.J = root.skel;
-  std::vector<char> in(static_cast<size_t>(m), 0);
-  for (i64 x : root.skel) in[size_t(x)] = 1;
-  for (i64 x : root.rows)
-    if (!in[size_t(x)]) out.J.push_back(x);
-  return out;
+  return outs;
+}
+
+RowIdResult hierarchical_id(i64 m, const std::vector<std::vector<i64>>& leaves,
+                            const WtBuilder& build, double eps, cudaStream_t s) {
+  auto r = hierarchical_id_multi(m, leaves, {build}, eps, s);
+  return std::move(r[0]);
 }
 
 // Direct row ID of one implicitly built W (row_id(eval(all rows))).
@@ -322,16 +360,18 @@ RowIdResult compress_block_far(const EntryView& v, const Geom& g, const std::vec
     leaves.push_back(std::move(rows));
   }
   const double factor = basis ? bas : div;
-  int n = 64;
-  RowIdResult prev =
-      hierarchical_id(m, leaves, proxy_builder(v, nodes, circles, factor, n, with_null, s), eps, s);
-  while (2 * n <= 2048) {
-    n *= 2;
+  // 64 and 128 samples are always both computed (proxy.cpp:289-300): one batch
+  auto two = hierarchical_id_multi(m, leaves,
+                                   {proxy_builder(v, nodes, circles, factor, 64, with_null, s),
+                                    proxy_builder(v, nodes, circles, factor, 128, with_null, s)},
+                                   eps, s);
+  bool settled = std::llabs(two[1].k - two[0].k) <= 2;
+  RowIdResult prev = std::move(two[1]);
+  for (int n = 256; !settled && n <= 2048; n *= 2) {
     RowIdResult cur =
         hierarchical_id(m, leaves, proxy_builder(v, nodes, circles, factor, n, with_null, s), eps, s);
-    const bool settled = std::llabs(cur.k - prev.k) <= 2;
+    settled = std::llabs(cur.k - prev.k) <= 2;
     prev = std::move(cur);
-    if (settled) break;
   }
   return prev;
 }
