@@ -290,12 +290,45 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
 }
 
 // Tall problems (M > n, n <= 144): a streaming TSQR first reduces W^T to its
-// n x n triangular factor R0 held in shared memory (row blocks of W^T are
-// folded into R0 one Householder column at a time), then the Eigen CPQR runs
-// on R0 in shared memory.  Column norms of R0 equal those of W^T, so the
-// pivot order, |r_jj| and R11^{-1} R12 are those of CPQR(W^T) in exact
-// arithmetic.  R (pivoted) is written to the first n rows of the job matrix.
-__global__ void __launch_bounds__(kT) tsqr_cpqr_kernel(const QrJob* __restrict__ jobs, int bm_max) {
+// n x n triangular factor R0 in shared memory, then the Eigen CPQR runs on
+// R0 in shared memory.  Column norms of R0 equal those of W^T, so the pivot
+// order, |r_jj| and R11^{-1} R12 are those of CPQR(W^T) in exact arithmetic.
+//
+// TSQR: 128-row blocks of W^T live in registers (column c owned by warp
+// c % 16, 4 rows per lane); each Householder step is one barrier — the warp
+// owning column j+1 updates it first and publishes the next reflector
+// (look-ahead) while the other warps finish step j.  R (pivoted) is written
+// to the first n rows of the job matrix.
+constexpr int kTsqrSlots = 9;  // columns per warp: n <= 16 * 9 = 144
+constexpr int kTsqrRpl = 4;    // rows per lane: 128-row blocks
+constexpr int kTsqrBm = 32 * kTsqrRpl;
+
+__device__ __forceinline__ void tsqr_reflector(double (&b)[kTsqrRpl], double* R, int n, int jn,
+                                               double* vbuf, double* tauv, int lane) {
+  double sq = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTsqrRpl; ++r) sq += b[r] * b[r];
+  sq = warp_sum(sq);
+  const double c0 = R[jn + jn * n];
+  double tau = 0.0, beta = c0, denom = 0.0;
+  if (sq > DBL_MIN) {
+    beta = sqrt(c0 * c0 + sq);
+    if (c0 >= 0.0) beta = -beta;
+    denom = c0 - beta;
+    tau = (beta - c0) / beta;
+  }
+#pragma unroll
+  for (int r = 0; r < kTsqrRpl; ++r) {
+    b[r] = denom == 0.0 ? 0.0 : b[r] / denom;
+    vbuf[lane + 32 * r] = b[r];
+  }
+  if (lane == 0) {
+    R[jn + jn * n] = beta;
+    *tauv = tau;
+  }
+}
+
+__global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restrict__ jobs) {
   extern __shared__ double sm[];
   const QrJob jb = jobs[blockIdx.x];
   const int M = jb.M, n = jb.n;
@@ -305,72 +338,51 @@ __global__ void __launch_bounds__(kT) tsqr_cpqr_kernel(const QrJob* __restrict__
   double* red = dir + n;
   int* ired = reinterpret_cast<int*>(red + 32);
   double* sc = red + 48;
-  double* R = sc + 8;                 // n x n, ld n
-  double* B = R + size_t(n) * n;      // bm x n, ld bm_max
-  const int bm = bm_max;
+  double* vb = sc + 8;              // 2 x 128 reflector buffers
+  double* tauv = vb + 2 * kTsqrBm;  // 2 (+pad)
+  double* R = tauv + 8;             // n x n, ld n
   for (int idx = tid; idx < n * n; idx += kT) R[idx] = 0.0;
-  __syncthreads();
-  for (int r0 = 0; r0 < M; r0 += bm) {
-    const int rb = min(bm, M - r0);
-    for (int c = warp; c < n; c += kWarps)
-      for (int i = lane; i < rb; i += 32) B[i + c * bm] = jb.a[(r0 + i) + size_t(c) * jb.lda];
+  double B[kTsqrSlots][kTsqrRpl];
+  for (int r0 = 0; r0 < M; r0 += kTsqrBm) {
+    const int rb = min(kTsqrBm, M - r0);
+#pragma unroll
+    for (int u = 0; u < kTsqrSlots; ++u) {
+      const int c = warp + 16 * u;
+#pragma unroll
+      for (int r = 0; r < kTsqrRpl; ++r) {
+        const int row = lane + 32 * r;
+        B[u][r] = (c < n && row < rb) ? jb.a[(r0 + row) + size_t(c) * jb.lda] : 0.0;
+      }
+    }
+    __syncthreads();  // R from the previous block complete
+    if (warp == 0) tsqr_reflector(B[0], R, n, 0, vb, tauv, lane);
     __syncthreads();
     for (int j = 0; j < n; ++j) {
-      if (warp == 0) {  // reflector of [R(j,j); B(:,j)]
-        double s = 0.0;
-        for (int i = lane; i < rb; i += 32) s += B[i + j * bm] * B[i + j * bm];
-        s = warp_sum(s);
-        const double c0 = R[j + j * n];
-        double tau = 0.0, beta = c0, denom = 0.0;
-        if (s > DBL_MIN) {
-          beta = sqrt(c0 * c0 + s);
-          if (c0 >= 0.0) beta = -beta;
-          denom = c0 - beta;
-          tau = (beta - c0) / beta;
+      const int cur = j & 1;
+      const double tau = tauv[cur];
+      const double* v = vb + cur * kTsqrBm;
+      double vr[kTsqrRpl];
+#pragma unroll
+      for (int r = 0; r < kTsqrRpl; ++r) vr[r] = v[lane + 32 * r];
+#pragma unroll
+      for (int u = 0; u < kTsqrSlots; ++u) {
+        const int c = warp + 16 * u;
+        if (c <= j || c >= n) continue;
+        if (tau != 0.0) {
+          double d = 0.0;
+#pragma unroll
+          for (int r = 0; r < kTsqrRpl; ++r) d += vr[r] * B[u][r];
+          d = warp_sum(d) + R[j + c * n];
+          const double tw = tau * d;
+#pragma unroll
+          for (int r = 0; r < kTsqrRpl; ++r) B[u][r] -= vr[r] * tw;
+          if (lane == 0) R[j + c * n] -= tw;
         }
-        for (int i = lane; i < rb; i += 32) B[i + j * bm] = denom == 0.0 ? 0.0 : B[i + j * bm] / denom;
-        if (lane == 0) {
-          R[j + j * n] = beta;
-          sc[0] = tau;
-        }
-      }
-      __syncthreads();
-      const double tau = sc[0];
-      if (tau != 0.0) {
-        for (int c = j + 1 + 4 * warp; c < n; c += 4 * kWarps) {
-          double d[4] = {0.0, 0.0, 0.0, 0.0};
-          for (int i = lane; i < rb; i += 32) {
-            const double vi = B[i + j * bm];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (c + u < n) d[u] += vi * B[i + (c + u) * bm];
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
-          double tw[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) tw[u] = c + u < n ? tau * (d[u] + R[j + (c + u) * n]) : 0.0;
-          for (int i = lane; i < rb; i += 32) {
-            const double vi = B[i + j * bm];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (c + u < n) B[i + (c + u) * bm] -= vi * tw[u];
-          }
-          if (lane == 0) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (c + u < n) R[j + (c + u) * n] -= tw[u];
-          }
-        }
+        if (c == j + 1) tsqr_reflector(B[u], R, n, c, vb + (cur ^ 1) * kTsqrBm, tauv + (cur ^ 1), lane);
       }
       __syncthreads();
     }
   }
-  // zero the strictly lower part left by the streaming (R0 is upper triangular)
-  for (int idx = tid; idx < n * n; idx += kT)
-    if (idx % n > idx / n) R[idx] = 0.0;
   __syncthreads();
   const int steps_max = jb.max_steps > 0 ? min(n, jb.max_steps) : n;
   const int done = cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
@@ -1091,12 +1103,7 @@ __global__ void add_identity_kernel(double* a, i64 lda, i64 n) {
 
 namespace {
 // Largest TSQR row block that fits next to the n x n factor.
-int tsqr_block_rows(int n) {
-  const size_t head = size_t(2 * n + 56 + n * n) * sizeof(double);
-  if (head >= kSmemCap) return 0;
-  const int bm = int((kSmemCap - head) / (size_t(n) * sizeof(double)));
-  return bm >= 32 ? std::min(bm, 128) : 0;
-}
+size_t tsqr_smem(int n) { return size_t(2 * n + 56 + 2 * kTsqrBm + 8 + n * n) * sizeof(double); }
 }  // namespace
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
@@ -1112,17 +1119,16 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   }
   std::vector<QrJob> plain, tall;
   for (const auto& j : jobs) {
-    const bool tsqr = j.pivot && j.n <= 144 && j.M > j.n && tsqr_block_rows(j.n) > 0 &&
+    const bool tsqr = j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
                       (size_t(j.M) * j.n + 2 * j.n + 56) * sizeof(double) > kSmemCap;
     (tsqr ? tall : plain).push_back(j);
   }
   if (!tall.empty()) {
     int nmax = 0;
     for (const auto& j : tall) nmax = std::max(nmax, j.n);
-    const int bm = tsqr_block_rows(nmax);
-    const size_t smem = size_t(2 * nmax + 56 + nmax * nmax + bm * nmax) * sizeof(double);
+    const size_t smem = tsqr_smem(nmax);
     const QrJob* d = ttab.upload(tall, s);
-    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d, bm);
+    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d);
     SBX_LAUNCHED();
   }
   if (plain.empty()) return;
