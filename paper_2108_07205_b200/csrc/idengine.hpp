@@ -30,6 +30,7 @@ class IdBatch {
   // idlib.cpp:38-45: min(k, dmax) cut at 1e-15 |r_00|
   i64 forced_rank(size_t p, i64 k) const;
   const std::vector<int>& perm(size_t p) const { return perm_[p]; }
+  const std::vector<double>& diag(size_t p) const { return diag_[p]; }
   // Writes P_p (n_p x k_p, column-major, ldp) for every problem with k_p > 0.
   void interp(const std::vector<i64>& ks, const std::vector<double*>& P,
               const std::vector<int>& ldp, cudaStream_t s);

@@ -90,8 +90,8 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
       c.P = P[p];
       level[p / L].push_back(std::move(c));
     }
-    SBX_CUDA(cudaStreamSynchronize(s));
     keep.push_back(std::move(pb));
+    phase_mark("  hier: leaves", s);
   }
   for (;;) {
     bool any = false;
@@ -170,7 +170,7 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
       if (!unis[h].empty()) level[h] = std::move(next);
     }
     gemm_batched(gj, s);
-    SBX_CUDA(cudaStreamSynchronize(s));
+    phase_mark("  hier: merge level", s);
     keep.push_back(std::move(ib));
     keep.push_back(std::move(pb));
   }
@@ -193,7 +193,6 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
       scatter_batched({{root.P, out.P.get(), map.get(), int(root.rows.size()), int(out.k),
                         std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0}},
                       s);
-      SBX_CUDA(cudaStreamSynchronize(s));
     }
     out.J = root.skel;
     std::vector<char> in(size_t(m), 0);
@@ -226,7 +225,6 @@ RowIdResult direct_id(i64 m, const WtBuilder& build, double eps, cudaStream_t s)
   out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
   if (out.k > 0) ids.interp({out.k}, {out.P.get()}, {std::max<int>(1, int(m))}, s);
   out.J.assign(ids.perm(0).begin(), ids.perm(0).end());
-  SBX_CUDA(cudaStreamSynchronize(s));
   return out;
 }
 
@@ -278,8 +276,8 @@ WtBuilder proxy_builder(const EntryView& v, const std::vector<i64>& nodes,
     DevBuf<ProxyJob> dj;
     dc.upload(cand, s);
     dj.upload(jobs, s);
+    // index tables return to the stream-ordered pool: no host sync needed
     launch_proxy_jobs(v, dj.get(), int(jobs.size()), ns, max_n, dc.get(), buf.get(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
   };
 }
 
@@ -323,7 +321,6 @@ WtBuilder entry_builder(const EntryView& v, const std::vector<i64>& rowsc,
     dn.upload(colsc, s);
     dj.upload(jobs, s);
     launch_near_jobs(v, dj.get(), int(jobs.size()), mx, dc.get(), dn.get(), buf.get(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
   };
 }
 
@@ -638,22 +635,130 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     jb.upload(jn, s);
     launch_block_jobs(eold.view(), ja.get(), int(jo.size()), mo, a.get(), b.get(), R1.get(), s);
     launch_block_jobs(enew.view(), jb.get(), int(jn.size()), mn, c.get(), d.get(), R1.get(), s, e.get());
-    SBX_CUDA(cudaStreamSynchronize(s));
   }
   phase_mark("update: L1/R1 assembly", s);
-  // final row ID of L1 (see header): CPQR of L1^T (k1 x n_ext)
-  DevBuf<double> L1T(static_cast<size_t>(k1 * n_ext));
-  copy_batched({{L1.get(), L1T.get(), int(k1), int(n_ext), ldl, int(k1), 1, 0}}, s);
+  // Final row ID of L1 (see header): CPQR of L1^T.  The rows of L1 fall in
+  // three groups with disjoint column supports — far kept rows (shared far
+  // P in the kc and kp columns), near kept rows (near P's), added rows (pk
+  // P's); cut rows are zero.  Columns of L1^T from different groups are
+  // orthogonal, so the greedy CPQR decouples: each group is factored on its
+  // own, the eps-rank uses the global |r_00| = max over groups, and the
+  // global pivot order is the merge of the groups' |r_jj| sequences.
+  struct Group {
+    std::vector<const double*> src;  // interpolation blocks (rows x kcols), stacked as W^T rows
+    std::vector<i64> kcols;
+    i64 rows = 0;
+    const i64* rowmap = nullptr;  // group row -> L1 row
+    std::vector<i64> hrowmap;
+  };
+  Group gf, gn, ga;
+  gf.rows = far.m;
+  gf.hrowmap = far_s;
+  gf.rowmap = d_far_s.get();
+  // far rows of L1 are (-x, x) (kc and kp share the far P): factor x once and
+  // scale its |r_jj| by sqrt(2) (identical Gram matrix up to the factor 2)
+  double far_scale = 1.0;
+  if (far.k > 0 && (kc.k > 0 || kp.k > 0)) {
+    gf.src.push_back(far.P.get());
+    gf.kcols.push_back(far.k);
+    if (kc.k > 0 && kp.k > 0) far_scale = std::sqrt(2.0);
+  }
+  gn.rows = i64(near_s.size());
+  gn.hrowmap = near_s;
+  gn.rowmap = d_near_s.get();
+  if (kc.k > 0 && kc.nearid.k > 0) {
+    gn.src.push_back(kc.nearid.P.get());
+    gn.kcols.push_back(kc.nearid.k);
+  }
+  if (kp.k > 0 && kp.nearid.k > 0) {
+    gn.src.push_back(kp.nearid.P.get());
+    gn.kcols.push_back(kp.nearid.k);
+  }
+  ga.rows = u->np2;
+  ga.hrowmap = added_rows;
+  ga.rowmap = d_added_rows.get();
+  if (k_pk > 0) {
+    if (pk_far.k > 0) {
+      ga.src.push_back(pk_far.P.get());
+      ga.kcols.push_back(pk_far.k);
+    }
+    if (pk_near.k > 0) {
+      ga.src.push_back(pk_near.P.get());
+      ga.kcols.push_back(pk_near.k);
+    }
+  }
+  Group* groups[3] = {&gf, &gn, &ga};
+  std::vector<IdProblem> fprobs(3);
+  std::vector<std::unique_ptr<DevBuf<double>>> gbufs;
+  std::vector<CopyJob> tj;
+  for (int g = 0; g < 3; ++g) {
+    Group& G = *groups[g];
+    i64 M = 0;
+    for (i64 c : G.kcols) M += c;
+    if (G.rows == 0) M = 0;
+    auto buf = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(M * G.rows, 1)));
+    i64 r0 = 0;
+    for (size_t b = 0; b < G.src.size(); ++b) {  // W^T rows r0.. = block^T
+      if (G.rows > 0)
+        tj.push_back({G.src[b], buf->get() + r0, int(G.kcols[b]), int(G.rows), int(G.rows), int(M), 1, 0});
+      r0 += G.kcols[b];
+    }
+    fprobs[size_t(g)] = {buf->get(), int(M), int(G.rows), int(std::max<i64>(M, 1))};
+    gbufs.push_back(std::move(buf));
+  }
+  copy_batched(tj, s);
   IdBatch fin;
-  fin.factor({{L1T.get(), int(k1), int(n_ext), int(k1)}}, eps, s);
-  u->k = fin.eps_rank(0, eps);
+  fin.factor(fprobs, eps * 1e-3, s);  // truncated well below the global threshold
+  const double gscale[3] = {far_scale, 1.0, 1.0};
+  auto rdiag = [&](int g, i64 i) { return gscale[g] * fin.diag(size_t(g))[size_t(i)]; };
+  double r00 = 0.0;
+  for (int g = 0; g < 3; ++g)
+    if (!fin.diag(size_t(g)).empty()) r00 = std::max(r00, rdiag(g, 0));
+  std::vector<i64> kg(3, 0);
+  if (r00 > 0.0)
+    for (int g = 0; g < 3; ++g) {
+      const i64 dn = i64(fin.diag(size_t(g)).size());
+      while (kg[size_t(g)] < dn && rdiag(g, kg[size_t(g)]) > eps * r00) ++kg[size_t(g)];
+    }
+  // global pivot order: merge by |r_jj| (descending; ties keep group order)
+  struct Piv {
+    double r;
+    int g;
+    i64 i;
+  };
+  std::vector<Piv> order;
+  for (int g = 0; g < 3; ++g)
+    for (i64 i = 0; i < kg[size_t(g)]; ++i) order.push_back({rdiag(g, i), g, i});
+  std::stable_sort(order.begin(), order.end(), [](const Piv& a, const Piv& b) { return a.r > b.r; });
+  u->k = i64(order.size());
   phase_mark("update: final ID of L1", s);
   const i64 k = u->k;
-  u->skeleton.assign(fin.perm(0).begin(), fin.perm(0).begin() + k);
+  u->skeleton.clear();
+  for (const Piv& p : order)
+    u->skeleton.push_back(groups[p.g]->hrowmap[size_t(fin.perm(size_t(p.g))[size_t(p.i)])]);
   u->L.resize(size_t(std::max<i64>(n_ext * k, 1)));
   u->R.resize(size_t(std::max<i64>(k * n_ext, 1)));
   if (k > 0) {
-    fin.interp({k}, {u->L.get()}, {int(n_ext)}, s);
+    std::vector<std::unique_ptr<DevBuf<double>>> pg;
+    std::vector<double*> Pp(3, nullptr);
+    std::vector<int> ldp(3, 1);
+    for (int g = 0; g < 3; ++g) {
+      pg.push_back(std::make_unique<DevBuf<double>>(size_t(std::max<i64>(groups[g]->rows * kg[size_t(g)], 1))));
+      Pp[size_t(g)] = pg.back()->get();
+      ldp[size_t(g)] = int(std::max<i64>(groups[g]->rows, 1));
+    }
+    fin.interp(kg, Pp, ldp, s);
+    phase_mark("update: final interp", s);
+    SBX_CUDA(cudaMemsetAsync(u->L.get(), 0, size_t(n_ext * k) * 8, s));
+    std::vector<ScatterJob> lj;
+    for (i64 col = 0; col < k; ++col) {  // L column `col` = group column order[col].i
+      const Piv& p = order[size_t(col)];
+      const Group& G = *groups[p.g];
+      lj.push_back({Pp[size_t(p.g)] + size_t(p.i) * size_t(ldp[size_t(p.g)]), u->L.get(), G.rowmap,
+                    int(G.rows), 1, ldp[size_t(p.g)], int(n_ext), int(col), 0, 1.0});
+    }
+    scatter_batched(lj, s);
+    phase_mark("update: L scatter", s);
     // R = L1(J(0:k), :) * R1
     DevBuf<i64> sk;
     sk.upload(u->skeleton, s);

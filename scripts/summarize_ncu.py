@@ -1,0 +1,86 @@
+"""Summarise ncu artefacts into profiles/ (markdown).
+
+  python scripts/summarize_ncu.py launches <launches.csv> > profiles/x.md
+  python scripts/summarize_ncu.py report <prof.ncu-rep> > profiles/y.md
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hi]
+    data = rows[hi + 1:]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    tot = 0.0
+    for r in data:
+        if len(r) <= vi:
+            continue
+        us = float(r[vi].replace(",", "")) / 1000.0
+        name = r[ki].split("(")[0].replace("sbx::<unnamed>::", "")
+        agg[name][0] += 1
+        agg[name][1] += us
+        tot += us
+    print(f"# ncu launch list summary: `{path}`\n")
+    print("`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole bench.py "
+          "process (setup + warm-up + timed + e2e + roofline steps); cold-cache serialised "
+          "launches, so compare shares, not absolutes.\n")
+    print(f"Total kernel time {tot / 1e3:.2f} ms over {len(data)} launches.\n")
+    print("| kernel | launches | total ms | share | mean us |")
+    print("|---|---:|---:|---:|---:|")
+    for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| {k} | {c} | {t / 1e3:.3f} | {100 * t / tot:.1f}% | {t / c:.1f} |")
+
+
+WANT = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+    "smsp__cycles_active.avg", "l1tex__t_bytes.sum", "lts__t_bytes.sum",
+]
+
+
+def report(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    print(f"# ncu --set full summary: `{path}`\n")
+    for v in rows[2:]:
+        name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        print(f"## {name[:120]}\n")
+        print("| metric | value | unit |")
+        print("|---|---:|---|")
+        for w in WANT:
+            if w in h:
+                i = h.index(w)
+                print(f"| {w} | {v[i]} | {units[i]} |")
+        print()
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src)))
+    try:
+        hh = srows[1]
+        si, sc = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source")
+        data = [r for r in srows[2:] if len(r) > si and r[si].isdigit()]
+        tot = sum(int(r[si]) for r in data) or 1
+        print("### top stall sites (SASS, all samples)\n")
+        print("| share | instruction |")
+        print("|---:|---|")
+        for r in sorted(data, key=lambda r: -int(r[si]))[:12]:
+            print(f"| {100 * int(r[si]) / tot:.1f}% | `{r[sc].strip()[:80]}` |")
+    except Exception as e:  # noqa: BLE001
+        print(f"(source page unavailable: {e})")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
