@@ -143,17 +143,23 @@ __device__ __forceinline__ void reflect_cols(double* const (&col)[U], const int 
 
 // ---------------------------------------------------------------- QR / CPQR
 // Householder QR of A (M x n, ld lda) by one CTA; with `pivot` it is
-// Eigen's ColPivHouseholderQR.  Returns the number of completed steps.
-// Scratch: upd, dir (n each), red (32), ired (32), sc (8).
+// Eigen's ColPivHouseholderQR.  Columns are not moved: the pivot of step j
+// is applied in place and perm[l] records the physical (= original) column
+// at logical position l, so R(i, l) = A(i, perm[l]) (interp uses perm as
+// its column map).  Ties go to the smallest logical position, as Eigen's
+// first-max over the current column order.  Four barriers per step.
+// Scratch: upd, dir (n doubles), pos, lphys (n ints), red (32), ired (32),
+// sc (8).  Returns the number of completed steps.
 __device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps_max,
                          double stop_eps, int* perm, double* diag, double* upd, double* dir,
-                         double* red, int* ired, double* sc) {
+                         int* pos, int* lphys, double* red, int* ired, double* sc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int size = min(M, n);
-  if (pivot)
-    for (int c = tid; c < n; c += kT) perm[c] = c;
+  for (int c = tid; c < n; c += kT) {
+    pos[c] = c;
+    lphys[c] = c;
+  }
   for (int c = tid; c < size; c += kT) diag[c] = 0.0;
-  __syncthreads();
   if (pivot) {
     for (int c = warp; c < n; c += kWarps) {
       double s = 0.0;
@@ -168,91 +174,98 @@ __device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps
   __syncthreads();
   const double thr = sqrt(DBL_EPSILON);
   int done = 0;
+  double r00 = 0.0;
   for (int j = 0; j < steps_max; ++j) {
-    if (pivot) {
+    int p = lphys[j];
+    if (pivot) {  // first max of the updated norms over logical positions >= j
       double bv = -1.0;
-      int bi = 0x7fffffff;
-      for (int c = j + tid; c < n; c += kT) {
-        const double v = upd[c];
-        if (v > bv) {
-          bv = v;
-          bi = c;
+      int bp = 0x7fffffff, bq = -1;
+      for (int c = tid; c < n; c += kT) {
+        const int lc = pos[c];
+        if (lc >= j && (upd[c] > bv || (upd[c] == bv && lc < bp))) {
+          bv = upd[c];
+          bp = lc;
+          bq = c;
         }
       }
-      double mv;
-      int p;
-      block_argmax(bv, bi, red, ired, mv, p);
-      if (p != j) {
-        for (int i = tid; i < M; i += kT) {
-          const double t = A[i + size_t(j) * lda];
-          A[i + size_t(j) * lda] = A[i + size_t(p) * lda];
-          A[i + size_t(p) * lda] = t;
-        }
-        if (tid == 0) {
-          double t = upd[j];
-          upd[j] = upd[p];
-          upd[p] = t;
-          t = dir[j];
-          dir[j] = dir[p];
-          dir[p] = t;
-          const int q = perm[j];
-          perm[j] = perm[p];
-          perm[p] = q;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+        if (ov > bv || (ov == bv && op < bp)) {
+          bv = ov;
+          bp = op;
+          bq = oq;
         }
       }
-      __syncthreads();
+      if (lane == 0) {
+        red[warp] = bv;
+        ired[warp] = bp;
+        ired[kWarps + warp] = bq;
+      }
+      __syncthreads();  // (1)
+      bv = -1.0;
+      bp = 0x7fffffff;
+      for (int w = 0; w < kWarps; ++w)
+        if (red[w] > bv || (red[w] == bv && ired[w] < bp)) {
+          bv = red[w];
+          bp = ired[w];
+          bq = ired[kWarps + w];
+        }
+      p = bq;
     }
-    // Householder vector of column j (Eigen makeHouseholderInPlace)
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < M; i += kT) {
-      const double v = A[i + size_t(j) * lda];
-      part += v * v;
-    }
-    const double tail = block_sum(part, red);
-    if (tid == 0) {
-      const double c0 = A[j + size_t(j) * lda];
-      double tau, beta, denom;
-      if (tail <= DBL_MIN) {
-        tau = 0.0;
-        beta = c0;
-        denom = 0.0;
-      } else {
-        beta = sqrt(c0 * c0 + tail);
+    // Householder vector of the pivot column, one warp (makeHouseholderInPlace)
+    double* pc = A + size_t(p) * lda;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < M; i += 32) s += pc[i] * pc[i];
+      s = warp_sum(s);
+      const double c0 = pc[j];
+      double tau = 0.0, beta = c0, denom = 0.0;
+      if (s > DBL_MIN) {
+        beta = sqrt(c0 * c0 + s);
         if (c0 >= 0.0) beta = -beta;
         denom = c0 - beta;
         tau = (beta - c0) / beta;
       }
-      sc[0] = tau;
-      sc[1] = beta;
-      sc[2] = denom;
-      if (j == 0) sc[3] = fabs(beta);
+      for (int i = j + 1 + lane; i < M; i += 32) pc[i] = denom == 0.0 ? 0.0 : pc[i] / denom;
+      __syncwarp();
+      if (lane == 0) {
+        pc[j] = beta;
+        diag[j] = fabs(beta);
+        sc[0] = tau;
+        sc[1] = beta;
+        if (pivot) {  // logical swap: the column at position j moves to the pivot's slot
+          const int lp = pos[p], q = lphys[j];
+          lphys[lp] = q;
+          pos[q] = lp;
+          lphys[j] = p;
+          pos[p] = j;
+        }
+      }
     }
-    __syncthreads();
-    const double tau = sc[0], beta = sc[1], denom = sc[2], r00 = sc[3];
-    for (int i = j + 1 + tid; i < M; i += kT) {
-      double& v = A[i + size_t(j) * lda];
-      v = denom == 0.0 ? 0.0 : v / denom;
-    }
-    if (tid == 0) {
-      A[j + size_t(j) * lda] = beta;
-      diag[j] = fabs(beta);
-    }
-    __syncthreads();
+    __syncthreads();  // (2)
+    const double tau = sc[0], beta = sc[1];
+    if (j == 0) r00 = fabs(beta);
     done = j + 1;
     if (pivot && stop_eps > 0.0 && !(fabs(beta) > stop_eps * r00)) break;
-    // apply to the trailing columns (4 per warp pass), then downdate their norms
-    for (int c = j + 1 + 4 * warp; c < n; c += 4 * kWarps) {
+    // apply to the alive columns (4 per warp pass), then downdate their norms
+    for (int c = 4 * warp; c < n; c += 4 * kWarps) {
       double* cols[4];
       int slot[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        cols[u] = c + u < n ? A + size_t(c + u) * lda : nullptr;
+        const bool live = c + u < n && pos[c + u] > j;
+        cols[u] = live ? A + size_t(c + u) * lda : nullptr;
         slot[u] = c + u;
       }
-      reflect_cols<4>(cols, slot, A + size_t(j) * lda, j, M, tau, pivot, upd, dir, thr, lane);
+      reflect_cols<4>(cols, slot, pc, j, M, tau, pivot, upd, dir, thr, lane);
     }
-    __syncthreads();
+    __syncthreads();  // (3)
   }
+  for (int l = tid; l < n; l += kT) perm[l] = lphys[l];
+  __syncthreads();
   return done;
 }
 
@@ -263,11 +276,13 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* upd = sm;
   double* dir = upd + n;
-  double* red = dir + n;                         // 32
-  int* ired = reinterpret_cast<int*>(red + 32);  // 32
-  double* sc = red + 48;                         // shared scalars (8)
+  int* pos = reinterpret_cast<int*>(dir + n);
+  int* lphys = pos + n;
+  double* red = dir + 2 * n;                     // 32 (after the two int tables)
+  int* ired = reinterpret_cast<int*>(red + 32);  // 32 (+32)
+  double* sc = red + 64;                         // shared scalars (8)
   double* mat = sc + 8;
-  const size_t head = size_t(2 * n + 56);
+  const size_t head = size_t(3 * n + 72);
   const bool in_smem = head + size_t(M) * n <= size_t(smem_doubles);
   double* A = jb.a;
   int lda = jb.lda;
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
   const int size = min(M, n);
   const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
   const int done = cpqr_core(A, M, n, lda, jb.pivot != 0, steps_max, jb.stop_eps, jb.perm, jb.diag,
-                             upd, dir, red, ired, sc);
+                             upd, dir, pos, lphys, red, ired, sc);
   if (tid == 0 && jb.steps) *jb.steps = done;
   if (in_smem) {
     __syncthreads();
@@ -335,9 +350,11 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* upd = sm;
   double* dir = upd + n;
-  double* red = dir + n;
+  int* pos = reinterpret_cast<int*>(dir + n);
+  int* lphys = pos + n;
+  double* red = dir + 2 * n;
   int* ired = reinterpret_cast<int*>(red + 32);
-  double* sc = red + 48;
+  double* sc = red + 64;
   double* vb = sc + 8;              // 2 x 128 reflector buffers
   double* tauv = vb + 2 * kTsqrBm;  // 2 (+pad)
   double* R = tauv + 8;             // n x n, ld n
@@ -364,21 +381,35 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
       double vr[kTsqrRpl];
 #pragma unroll
       for (int r = 0; r < kTsqrRpl; ++r) vr[r] = v[lane + 32 * r];
+      if (tau != 0.0) {
+        // all owned trailing columns at once: the dot-product reductions of
+        // the slots are interleaved so their shuffles pipeline
+        double d[kTsqrSlots];
 #pragma unroll
-      for (int u = 0; u < kTsqrSlots; ++u) {
-        const int c = warp + 16 * u;
-        if (c <= j || c >= n) continue;
-        if (tau != 0.0) {
-          double d = 0.0;
+        for (int u = 0; u < kTsqrSlots; ++u) {
+          d[u] = 0.0;
 #pragma unroll
-          for (int r = 0; r < kTsqrRpl; ++r) d += vr[r] * B[u][r];
-          d = warp_sum(d) + R[j + c * n];
-          const double tw = tau * d;
+          for (int r = 0; r < kTsqrRpl; ++r) d[u] += vr[r] * B[u][r];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < kTsqrSlots; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+#pragma unroll
+        for (int u = 0; u < kTsqrSlots; ++u) {
+          const int c = warp + 16 * u;
+          if (c <= j || c >= n) continue;
+          const double tw = tau * (d[u] + R[j + c * n]);
 #pragma unroll
           for (int r = 0; r < kTsqrRpl; ++r) B[u][r] -= vr[r] * tw;
           if (lane == 0) R[j + c * n] -= tw;
         }
-        if (c == j + 1) tsqr_reflector(B[u], R, n, c, vb + (cur ^ 1) * kTsqrBm, tauv + (cur ^ 1), lane);
+      }
+      if (j + 1 < n && ((j + 1) & 15) == warp) {  // look-ahead: next reflector
+        const int un = (j + 1) >> 4;
+#pragma unroll
+        for (int u = 0; u < kTsqrSlots; ++u)
+          if (u == un) tsqr_reflector(B[u], R, n, j + 1, vb + (cur ^ 1) * kTsqrBm, tauv + (cur ^ 1), lane);
       }
       __syncthreads();
     }
@@ -386,7 +417,7 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   __syncthreads();
   const int steps_max = jb.max_steps > 0 ? min(n, jb.max_steps) : n;
   const int done = cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
-                             red, ired, sc);
+                             pos, lphys, red, ired, sc);
   if (tid == 0 && jb.steps) *jb.steps = done;
   __syncthreads();
   for (int c = warp; c < n; c += kWarps)
@@ -1103,7 +1134,7 @@ __global__ void add_identity_kernel(double* a, i64 lda, i64 n) {
 
 namespace {
 // Largest TSQR row block that fits next to the n x n factor.
-size_t tsqr_smem(int n) { return size_t(2 * n + 56 + 2 * kTsqrBm + 8 + n * n) * sizeof(double); }
+size_t tsqr_smem(int n) { return size_t(3 * n + 72 + 2 * kTsqrBm + 8 + n * n) * sizeof(double); }
 }  // namespace
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
@@ -1120,7 +1151,7 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   std::vector<QrJob> plain, tall;
   for (const auto& j : jobs) {
     const bool tsqr = j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
-                      (size_t(j.M) * j.n + 2 * j.n + 56) * sizeof(double) > kSmemCap;
+                      (size_t(j.M) * j.n + 3 * j.n + 72) * sizeof(double) > kSmemCap;
     (tsqr ? tall : plain).push_back(j);
   }
   if (!tall.empty()) {
@@ -1134,11 +1165,11 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (plain.empty()) return;
   size_t need = 0;
   for (const auto& j : plain) {
-    const size_t sz = (size_t(2 * j.n + 56) + size_t(j.M) * j.n) * sizeof(double);
+    const size_t sz = (size_t(3 * j.n + 72) + size_t(j.M) * j.n) * sizeof(double);
     if (sz <= kSmemCap) need = std::max(need, sz);
   }
   size_t base = 0;
-  for (const auto& j : plain) base = std::max(base, size_t(2 * j.n + 56) * sizeof(double));
+  for (const auto& j : plain) base = std::max(base, size_t(3 * j.n + 72) * sizeof(double));
   need = std::max(need, base);
   require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
   const QrJob* d = tab.upload(plain, s);

@@ -105,7 +105,7 @@ void IdBatch::interp(const std::vector<i64>& ks, const std::vector<double*>& P,
     j.n = probs_[p].n;
     j.k = int(k);
     j.perm = d_perm_.get() + perm_off_[p];
-    j.colmap = coop_[p] ? j.perm : nullptr;
+    j.colmap = j.perm;  // every engine pivots in place: R(:, l) = A(:, perm[l])
     j.P = P[p];
     j.ldp = ldp[p];
     j.T = d_T_.get() + toff[p];
