@@ -376,7 +376,7 @@ int sbx_els_info(sbx_els e, int64_t* info) {
     info[1] = s.n_c;
     info[2] = s.n_p;
     info[3] = s.k;
-    info[4] = s.app_h ? 1 : 0;
+    info[4] = (s.app && s.app->h) ? 1 : 0;
   });
 }
 

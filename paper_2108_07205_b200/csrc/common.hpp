@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -46,8 +47,21 @@ cudaStream_t lib_stream();
 
 // Stream-ordered caching device allocator (the per-step path allocates many
 // short-lived blocks; cudaMalloc/cudaFree would serialise the device).
+// Pools are per stream: the stream current on the calling thread (a
+// parallel_tasks worker stream, else the library stream).
 void* dev_alloc(size_t bytes);
 void dev_free(void* p, size_t bytes);
+cudaStream_t cur_stream();
+
+// Runs independent host+device tasks concurrently: task i gets its own
+// thread and worker stream (forked from `main`, joined back into it), so the
+// latency-bound ID factorisations of independent blocks overlap on the GPU.
+// Device buffers a task allocates must either be released inside the task
+// or handed back to the caller, who releases them on `main` after the join.
+// high[i] != 0 puts task i on a high-priority stream (its pending CTAs are
+// dispatched before those of normal-priority tasks).
+void parallel_tasks(const std::vector<std::function<void(cudaStream_t)>>& tasks, cudaStream_t main,
+                    const std::vector<int>& high = {});
 
 // Optional host-side phase timer (SBX_TIMING=1): syncs the stream and prints
 // the elapsed time since the previous mark to stderr.

@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <mutex>
 
 #include "dense.hpp"
 
@@ -461,6 +462,61 @@ __device__ __forceinline__ bool better(double v, int p, double bv, int bp) {
   return v > bv || (v == bv && p < bp);
 }
 
+// First-max over the G published partials of a group, in parallel (one L2
+// round trip instead of G serial loads).  Every thread gets the winner's
+// physical column, logical position and owning CTA rank.
+__device__ void coop_pick(const CoopPart* cur, int G, double* red, int* ired, int& out_phys,
+                          int& out_pos, int& out_own) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nw = blockDim.x >> 5;
+  double bv = -1.0;
+  int bp = 0x7fffffff, bq = -1, bo = -1;
+  for (int g = tid; g < G; g += blockDim.x) {
+    const double pv = __ldcg(&cur[g].val);
+    const int pp = __ldcg(&cur[g].pos), pq = __ldcg(&cur[g].phys);
+    if (pq >= 0 && better(pv, pp, bv, bp)) {
+      bv = pv;
+      bp = pp;
+      bq = pq;
+      bo = g;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+    const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+    const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
+    if (better(ov, op, bv, bp)) {
+      bv = ov;
+      bp = op;
+      bq = oq;
+      bo = oo;
+    }
+  }
+  __syncthreads();  // red / ired free
+  if (lane == 0) {
+    red[warp] = bv;
+    ired[warp] = bp;
+    ired[32 + warp] = bq;
+    ired[64 + warp] = bo;
+  }
+  __syncthreads();
+  double v0 = -1.0;
+  int p0 = 0x7fffffff, q0 = -1, o0 = -1;
+  for (int w = 0; w < nw; ++w)
+    if (better(red[w], ired[w], v0, p0)) {
+      v0 = red[w];
+      p0 = ired[w];
+      q0 = ired[32 + w];
+      o0 = ired[64 + w];
+    }
+  out_phys = q0;
+  out_pos = p0;
+  out_own = o0;
+  __syncthreads();  // everyone has read red / ired
+}
+
 struct CoopArgs {
   const QrJob* jobs;
   const int* cta_job;
@@ -489,8 +545,8 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
   double* dir = upd + nown;      // nown
   double* red = dir + nown;      // 32
   double* sc = red + 32;         // 8
-  int* ired = reinterpret_cast<int*>(sc + 8);  // 32
-  int* mypos = ired + 32;        // nown (logical position, -1 once pivoted)
+  int* ired = reinterpret_cast<int*>(sc + 8);  // 96
+  int* mypos = ired + 96;        // nown (logical position, -1 once pivoted)
   CoopCtl* ctl = args.ctl + job;
   CoopPart* parts = args.parts + args.part_off[job];
   double* sbeta = args.beta + args.beta_off[job];
@@ -556,25 +612,8 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
     if (prev_p >= 0 && prev_p >= c0 && prev_p < c1 && tid == 0)
       A[(j - 1) + size_t(prev_p) * lda] = prev_beta;
     // global pivot
-    __shared__ int s_p, s_lp;
-    if (tid == 0) {
-      double v0 = -1.0;
-      int p0 = 0x7fffffff, q0 = -1;
-      const CoopPart* cur = parts + (j & 1) * G;
-      for (int g = 0; g < G; ++g) {  // L1-bypassing loads: written by other CTAs
-        const double pv = __ldcg(&cur[g].val);
-        const int pp = __ldcg(&cur[g].pos), pq = __ldcg(&cur[g].phys);
-        if (pq >= 0 && better(pv, pp, v0, p0)) {
-          v0 = pv;
-          p0 = pp;
-          q0 = pq;
-        }
-      }
-      s_p = q0;
-      s_lp = p0;
-    }
-    __syncthreads();
-    const int p = s_p, lp = s_lp;
+    int p, lp, own_unused;
+    coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own_unused);
     // logical swap: the column at position j moves to lp, p becomes position j
     for (int c = tid; c < nown; c += kCT) {
       if (c0 + c == p) mypos[c] = -1;
@@ -634,6 +673,315 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
   // finalisation: last diagonal, logical order of the untouched columns
   group_barrier(ctl, unsigned(G));
   if (prev_p >= c0 && prev_p < c1 && tid == 0) A[(done - 1) + size_t(prev_p) * lda] = prev_beta;
+  for (int c = tid; c < nown; c += kCT)
+    if (mypos[c] >= 0) jb.perm[mypos[c]] = c0 + c;
+  for (int l = rank * kCT + tid; l < size; l += G * kCT)
+    jb.diag[l] = l < done ? fabs(__ldcg(sbeta + l)) : 0.0;
+  if (rank == 0 && tid == 0 && jb.steps) *jb.steps = done;
+}
+
+// ---------------------------------------------------------------- on-chip cooperative CPQR
+// Same algorithm as cpqr_coop_kernel, but every CTA keeps its column slab in
+// shared memory for the whole factorisation, so a step touches the matrix
+// only on chip.  Each CTA publishes the current rows [j, M) of its local
+// pivot candidate before the group barrier; after it, every CTA reads the
+// winner's copy and forms the Householder vector redundantly.  One group
+// barrier per step; the slab goes back to global memory at the end.
+struct SmemCoopArgs {
+  const QrJob* jobs;
+  const int* cta_job;
+  const int* cta_rank;
+  const int* job_ctas;
+  CoopCtl* ctl;
+  CoopPart* parts;
+  const int* part_off;  // 2 G entries per job (step parity)
+  double* cand;         // 2 G M doubles per job
+  const i64* cand_off;
+  double* beta;
+  const i64* beta_off;
+};
+
+constexpr int kSmemCoopU = 8;  // columns per block-wide reflector pass
+
+constexpr int kThreadColM = 96;  // slabs this short: one thread per column
+// odd leading dimension for short slabs: thread-per-column access is then
+// free of shared-memory bank conflicts
+__host__ __device__ __forceinline__ int smem_coop_ld(int M) { return M <= kThreadColM ? (M | 1) : M; }
+__host__ __device__ __forceinline__ size_t smem_coop_doubles(int M, int nown) {
+  return size_t(smem_coop_ld(M)) * nown + M + 2 * nown + 8 * kSmemCoopU + 16 + (96 + nown + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
+  extern __shared__ double sm[];
+  const int job = args.cta_job[blockIdx.x];
+  const int rank = args.cta_rank[blockIdx.x];
+  const int G = args.job_ctas[job];
+  const QrJob jb = args.jobs[job];
+  const int M = jb.M, n = jb.n, lda = jb.lda;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = int(i64(n) * rank / G), c1 = int(i64(n) * (rank + 1) / G);
+  const int nown = c1 - c0;
+  const int ldS = smem_coop_ld(M);
+  double* S = sm;                         // M x nown slab (ld ldS)
+  double* v = S + size_t(ldS) * nown;     // M
+  double* upd = v + M;                    // nown
+  double* dir = upd + nown;               // nown
+  double* red = dir + nown;               // 8 warps x kSmemCoopU
+  double* sc = red + 8 * kSmemCoopU;      // 16
+  int* ired = reinterpret_cast<int*>(sc + 16);  // 96
+  int* mypos = ired + 96;                 // nown
+  CoopCtl* ctl = args.ctl + job;
+  CoopPart* parts = args.parts + args.part_off[job];
+  double* cand = args.cand + args.cand_off[job];
+  double* sbeta = args.beta + args.beta_off[job];
+  const double* Ag = jb.a;
+  for (i64 e = tid; e < i64(M) * nown; e += kCT) {
+    const int c = int(e / M), i = int(e - i64(c) * M);
+    S[i + size_t(c) * ldS] = Ag[i + size_t(c0 + c) * lda];
+  }
+  for (int c = tid; c < nown; c += kCT) mypos[c] = c0 + c;
+  __syncthreads();
+  if (nown >= kCWarps) {
+    for (int c = warp; c < nown; c += kCWarps) {
+      const double* col = S + size_t(c) * ldS;
+      double s = 0.0;
+      for (int i = lane; i < M; i += 32) s += col[i] * col[i];
+      s = warp_sum(s);
+      if (lane == 0) upd[c] = dir[c] = sqrt(s);
+    }
+  } else {  // few, tall columns: the whole CTA per column
+    for (int c = 0; c < nown; ++c) {
+      const double* col = S + size_t(c) * ldS;
+      double s = 0.0;
+      for (int i = tid; i < M; i += kCT) s += col[i] * col[i];
+      s = warp_sum(s);
+      if (lane == 0) red[warp] = s;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kCWarps; ++w) t += red[w];
+        upd[c] = dir[c] = sqrt(t);
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  const int size = min(M, n);
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  const double thr = sqrt(DBL_EPSILON);
+  // wide slabs: a warp per 4 columns; tall, narrow slabs: the whole CTA per
+  // column (rows split over all threads)
+  const bool thread_mode = M <= kThreadColM;  // one thread per column
+  const bool warp_mode = !thread_mode && (nown >= 8 || M <= 256);
+  int done = 0;
+  double r00 = 0.0;
+  __shared__ int s_p;
+  for (int j = 0; j < steps_max; ++j) {
+    double bv = -1.0;
+    int bp = 0x7fffffff, bphys = -1;
+    for (int c = tid; c < nown; c += kCT) {
+      const int p = mypos[c];
+      if (p >= 0 && better(upd[c], p, bv, bp)) {
+        bv = upd[c];
+        bp = p;
+        bphys = c0 + c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bphys, o);
+      if (better(ov, op, bv, bp)) {
+        bv = ov;
+        bp = op;
+        bphys = oq;
+      }
+    }
+    __shared__ int wphys[kCWarps];
+    if (lane == 0) {
+      red[warp] = bv;
+      ired[warp] = bp;
+      wphys[warp] = bphys;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double v0 = -1.0;
+      int p0 = 0x7fffffff, q0 = -1;
+      for (int w = 0; w < kCWarps; ++w)
+        if (better(red[w], ired[w], v0, p0)) {
+          v0 = red[w];
+          p0 = ired[w];
+          q0 = wphys[w];
+        }
+      parts[(j & 1) * G + rank] = {v0, p0, q0};
+      s_p = q0;
+    }
+    __syncthreads();
+    {  // publish the candidate's current rows [j, M)
+      const int q = s_p;
+      if (q >= 0) {
+        const double* src = S + size_t(q - c0) * ldS;
+        double* dst = cand + (size_t(j & 1) * G + rank) * M;
+        for (int i = j + tid; i < M; i += kCT) __stcg(dst + i, src[i]);
+      }
+    }
+    group_barrier(ctl, unsigned(G));
+    int p, lp, own;
+    coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own);
+    for (int c = tid; c < nown; c += kCT) {
+      if (c0 + c == p) mypos[c] = -1;
+      else if (mypos[c] == j) mypos[c] = lp;
+    }
+    if (p >= c0 && p < c1 && tid == 0) jb.perm[j] = p;
+    const double* pc = cand + (size_t(j & 1) * G + own) * M;
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < M; i += kCT) {
+      const double x = __ldcg(pc + i);
+      v[i] = x;
+      part += x * x;
+    }
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    const double tail = warp_sum(lane < kCWarps ? red[lane] : 0.0);
+    const double cc = __ldcg(pc + j);
+    double tau, beta, denom;
+    if (tail <= DBL_MIN) {
+      tau = 0.0;
+      beta = cc;
+      denom = 0.0;
+    } else {
+      beta = sqrt(cc * cc + tail);
+      if (cc >= 0.0) beta = -beta;
+      denom = cc - beta;
+      tau = (beta - cc) / beta;
+    }
+    __syncthreads();  // red[] reads done
+    {
+      const double rd = denom == 0.0 ? 0.0 : 1.0 / denom;
+      for (int i = j + 1 + tid; i < M; i += kCT) v[i] *= rd;
+    }
+    if (j == 0) r00 = fabs(beta);
+    if (rank == 0 && tid == 0) sbeta[j] = beta;
+    if (p >= c0 && p < c1 && tid == 0) S[j + size_t(p - c0) * ldS] = beta;
+    __syncthreads();
+    done = j + 1;
+    if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    if (thread_mode) {
+      for (int c = tid; c < nown; c += kCT) {
+        if (mypos[c] < 0) continue;
+        double* col = S + size_t(c) * ldS;
+        if (tau != 0.0 && M - j > 1) {
+          double d = col[j];
+          for (int i = j + 1; i < M; ++i) d += v[i] * col[i];
+          const double tw = tau * d;
+          col[j] -= tw;
+          for (int i = j + 1; i < M; ++i) col[i] -= v[i] * tw;
+        }
+        const double uu = upd[c];
+        if (uu == 0.0) continue;
+        double t = fabs(col[j]) / uu;
+        t = (1.0 + t) * (1.0 - t);
+        t = t < 0.0 ? 0.0 : t;
+        const double rr = uu / dir[c];
+        if (t * rr * rr <= thr) {
+          double sacc = 0.0;
+          for (int i = j + 1; i < M; ++i) sacc += col[i] * col[i];
+          upd[c] = dir[c] = sqrt(sacc);
+        } else {
+          upd[c] = uu * sqrt(t);
+        }
+      }
+    } else if (warp_mode) {
+      for (int c = 4 * warp; c < nown; c += 4 * kCWarps) {
+        double* cols[4];
+        int slot[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool live = c + u < nown && mypos[c + u] >= 0;
+          cols[u] = live ? S + size_t(c + u) * ldS : nullptr;
+          slot[u] = c + u;
+        }
+        reflect_cols<4>(cols, slot, v, j, M, tau, true, upd, dir, thr, lane);
+      }
+    } else {
+      for (int cb = 0; cb < nown; cb += kSmemCoopU) {
+        double d[kSmemCoopU];
+        bool live[kSmemCoopU];
+#pragma unroll
+        for (int u = 0; u < kSmemCoopU; ++u) {
+          live[u] = cb + u < nown && mypos[cb + u] >= 0;
+          d[u] = 0.0;
+        }
+        if (tau != 0.0 && M - j > 1) {
+          for (int i = j + 1 + tid; i < M; i += kCT) {
+            const double vi = v[i];
+#pragma unroll
+            for (int u = 0; u < kSmemCoopU; ++u)
+              if (live[u]) d[u] += vi * S[i + size_t(cb + u) * ldS];
+          }
+#pragma unroll
+          for (int u = 0; u < kSmemCoopU; ++u) d[u] = warp_sum(d[u]);
+          if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < kSmemCoopU; ++u) red[warp * kSmemCoopU + u] = d[u];
+          __syncthreads();
+          double tw[kSmemCoopU];
+#pragma unroll
+          for (int u = 0; u < kSmemCoopU; ++u) {
+            double t = 0.0;
+            for (int w = 0; w < kCWarps; ++w) t += red[w * kSmemCoopU + u];
+            tw[u] = live[u] ? tau * (t + S[j + size_t(cb + u) * ldS]) : 0.0;
+          }
+          __syncthreads();  // everyone has read S[j, :] and red[]
+          for (int i = j + 1 + tid; i < M; i += kCT) {
+            const double vi = v[i];
+#pragma unroll
+            for (int u = 0; u < kSmemCoopU; ++u)
+              if (live[u]) S[i + size_t(cb + u) * ldS] -= vi * tw[u];
+          }
+#pragma unroll
+          for (int u = 0; u < kSmemCoopU; ++u)
+            if (tid == u && live[u]) S[j + size_t(cb + u) * ldS] -= tw[u];
+          __syncthreads();
+        }
+        // norm downdating (uniform decisions: every thread reads the same values)
+#pragma unroll
+        for (int u = 0; u < kSmemCoopU; ++u) {
+          if (!live[u]) continue;
+          const int c = cb + u;
+          const double uu = upd[c];
+          if (uu == 0.0) continue;
+          double t = fabs(S[j + size_t(c) * ldS]) / uu;
+          t = (1.0 + t) * (1.0 - t);
+          t = t < 0.0 ? 0.0 : t;
+          const double rr = uu / dir[c];
+          __syncthreads();  // all threads read upd[c] before it changes
+          if (t * rr * rr <= thr) {
+            double sacc = 0.0;
+            for (int i = j + 1 + tid; i < M; i += kCT) sacc += S[i + size_t(c) * ldS] * S[i + size_t(c) * ldS];
+            sacc = warp_sum(sacc);
+            if (lane == 0) red[warp] = sacc;
+            __syncthreads();
+            if (tid == 0) {
+              double s2 = 0.0;
+              for (int w = 0; w < kCWarps; ++w) s2 += red[w];
+              upd[c] = dir[c] = sqrt(s2);
+            }
+          } else if (tid == 0) {
+            upd[c] = uu * sqrt(t);
+          }
+          __syncthreads();
+        }
+      }
+    }
+    __syncthreads();
+  }
+  group_barrier(ctl, unsigned(G));
+  double* Aw = jb.a;
+  for (int c = warp; c < nown; c += kCWarps)
+    for (int i = lane; i < M; i += 32) Aw[i + size_t(c0 + c) * lda] = S[i + size_t(c) * ldS];
   for (int c = tid; c < nown; c += kCT)
     if (mypos[c] >= 0) jb.perm[mypos[c]] = c0 + c;
   for (int l = rank * kCT + tid; l < size; l += G * kCT)
@@ -1140,14 +1488,13 @@ size_t tsqr_smem(int n) { return size_t(3 * n + 72 + 2 * kTsqrBm + 8 + n * n) * 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
   static thread_local JobTable<QrJob> tab, ttab;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
     SBX_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
     SBX_CUDA(cudaFuncSetAttribute(tsqr_cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
-    attr = true;
-  }
+  });
   std::vector<QrJob> plain, tall;
   for (const auto& j : jobs) {
     const bool tsqr = j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
@@ -1189,16 +1536,15 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     size_t mx = 0;
     for (size_t q = 0; q < jobs.size(); ++q) {
       const int nown = (jobs[q].n + G[q] - 1) / G[q];
-      mx = std::max(mx, size_t(jobs[q].M + 2 * nown + 40) * 8 + size_t(32 + nown) * 4 + 64);
+      mx = std::max(mx, size_t(jobs[q].M + 2 * nown + 40) * 8 + size_t(96 + nown) * 4 + 64);
     }
     return mx;
   };
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
     SBX_CUDA(cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
-    attr = true;
-  }
+  });
   std::vector<int> G(jobs.size(), 1);
   auto split = [&](int T) {
     int used = 0;
@@ -1270,6 +1616,111 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_coop_kernel),
                                        dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
   SBX_LAUNCHED();
+}
+
+int cpqr_smem_ctas(int M, int n) {
+  if (M <= 0 || n <= 0) return 0;
+  const size_t cap = kSmemCap / sizeof(double);
+  if (smem_coop_doubles(M, 1) > cap) return 0;
+  int lo = 1, hi = n;  // smallest G whose widest slab fits
+  while (lo < hi) {
+    const int g = (lo + hi) / 2;
+    if (smem_coop_doubles(M, (n + g - 1) / g) <= cap) hi = g;
+    else lo = g + 1;
+  }
+  return lo;
+}
+
+void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  int dev = 0, sms = 148;
+  SBX_CUDA(cudaGetDevice(&dev));
+  SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+  });
+  static thread_local JobTable<QrJob> tjobs;
+  static thread_local DevBuf<int> d_ints;
+  static thread_local DevBuf<CoopCtl> d_ctl;
+  static thread_local DevBuf<CoopPart> d_parts;
+  static thread_local DevBuf<double> d_beta, d_cand;
+  static thread_local DevBuf<i64> d_offs;
+  // waves: every CTA of a cooperative launch must be co-resident
+  size_t first = 0;
+  while (first < jobs.size()) {
+    std::vector<QrJob> wave;
+    std::vector<int> G;
+    size_t smem = 0;
+    int ctas = 0, per_sm = 1;
+    size_t q = first;
+    for (; q < jobs.size(); ++q) {
+      const int g = cpqr_smem_ctas(jobs[q].M, jobs[q].n);
+      require(g > 0 && g <= sms, "cpqr_smem: problem does not fit on chip");
+      const size_t sm2 = std::max(smem, smem_coop_doubles(jobs[q].M, (jobs[q].n + g - 1) / g) * sizeof(double));
+      int ps = 1;
+      SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cpqr_smem_kernel, kCT, sm2));
+      ps = std::max(1, ps);
+      if (!wave.empty() && ctas + g > sms * ps) break;
+      wave.push_back(jobs[q]);
+      G.push_back(g);
+      ctas += g;
+      smem = sm2;
+      per_sm = ps;
+    }
+    (void)per_sm;
+    first = q;
+    std::vector<int> cta_job, cta_rank, part_off(wave.size());
+    std::vector<i64> offs(2 * wave.size());
+    i64 boff = 0, coff = 0;
+    int poff = 0;
+    for (size_t w = 0; w < wave.size(); ++w) {
+      part_off[w] = poff;
+      poff += 2 * G[w];
+      offs[w] = boff;
+      boff += std::min(wave[w].M, wave[w].n);
+      offs[wave.size() + w] = coff;
+      coff += 2 * i64(G[w]) * wave[w].M;
+      for (int r = 0; r < G[w]; ++r) {
+        cta_job.push_back(int(w));
+        cta_rank.push_back(r);
+      }
+    }
+    std::vector<int> ints;
+    ints.insert(ints.end(), cta_job.begin(), cta_job.end());
+    ints.insert(ints.end(), cta_rank.begin(), cta_rank.end());
+    ints.insert(ints.end(), G.begin(), G.end());
+    ints.insert(ints.end(), part_off.begin(), part_off.end());
+    d_ints.upload(ints, s);
+    d_ctl.reserve(wave.size());
+    SBX_CUDA(cudaMemsetAsync(d_ctl.get(), 0, wave.size() * sizeof(CoopCtl), s));
+    d_parts.reserve(size_t(poff));
+    d_beta.reserve(size_t(std::max<i64>(boff, 1)));
+    d_cand.reserve(size_t(std::max<i64>(coff, 1)));
+    d_offs.upload(offs, s);
+    SmemCoopArgs a;
+    a.jobs = tjobs.upload(wave, s);
+    a.cta_job = d_ints.get();
+    a.cta_rank = d_ints.get() + cta_job.size();
+    a.job_ctas = d_ints.get() + 2 * cta_job.size();
+    a.part_off = d_ints.get() + 2 * cta_job.size() + G.size();
+    a.ctl = d_ctl.get();
+    a.parts = d_parts.get();
+    a.cand = d_cand.get();
+    a.cand_off = d_offs.get() + wave.size();
+    a.beta = d_beta.get();
+    a.beta_off = d_offs.get();
+    void* params[] = {&a};
+    static const bool plain = std::getenv("SBX_COOP_PLAIN") != nullptr;  // diagnostics
+    if (plain)
+      SBX_CUDA(cudaLaunchKernel(reinterpret_cast<void*>(cpqr_smem_kernel), dim3(unsigned(cta_job.size())),
+                                dim3(kCT), params, smem, s));
+    else
+      SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_smem_kernel),
+                                           dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
+    SBX_LAUNCHED();
+  }
 }
 
 void interp_batched(const std::vector<InterpJob>& jobs, cudaStream_t s) {
@@ -1349,12 +1800,11 @@ void lu_batched(const std::vector<LuJob>& jobs, cudaStream_t s) {
     const size_t sz = (64 + size_t(j.n) * j.n) * sizeof(double);
     if (sz <= kSmemCap) need = std::max(need, sz);
   }
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
     SBX_CUDA(cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
-    attr = true;
-  }
+  });
   const LuJob* d = tab.upload(jobs, s);
   lu_kernel<<<unsigned(jobs.size()), kT, need, s>>>(d, int(need / sizeof(double)));
   SBX_LAUNCHED();

@@ -37,6 +37,14 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // Householder convention and the norm downdating are those of qr_kernel.
 void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 
+// On-chip cooperative CPQR: like cpqr_coop_batched, but each CTA holds its
+// column slab in shared memory for the whole factorisation and publishes
+// its pivot candidate before the group barrier (one barrier per step, no
+// trailing-matrix traffic).  Problems are packed into co-resident waves.
+// cpqr_smem_ctas gives the CTAs a problem needs (0: does not fit on chip).
+int cpqr_smem_ctas(int M, int n);
+void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+
 // ---------------------------------------------------------------- ID interpolation
 // Given a pivoted factor (R in the upper triangle of a, ld lda, n columns)
 // and a rank k: P (n x k, column-major, ldp) with P(J_i, i) = 1 (i < k) and

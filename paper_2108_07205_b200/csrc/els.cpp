@@ -60,8 +60,8 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
   if (e.n_p == 0) return;
   const double* vp = v + nkc;
   double* op = out + nkc;
-  if (e.app_h) {
-    HbsOp& H = *e.app_h;
+  if (e.app->h) {
+    HbsOp& H = *e.app->h;
     if (!H.solve_plan.built) hbs_build_solve_plan(H);
     SweepPlan& Q = H.solve_plan;
     H.ws.reserve(size_t(Q.ws_rows * nrhs));
@@ -69,13 +69,43 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
     hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
     launch_rm_to_cm(H.ws.get() + Q.out_row * nrhs, e.n_p, nrhs, op, ldo, nullptr, s);
   } else {
-    gemm_batched({{e.app_inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
+    gemm_batched({{e.app->inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
                    int(ldo), 0, 0, 1.0, 0.0}},
                  s);
   }
 }
 
 }  // namespace
+
+std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan, int form, double mu,
+                                            double eps, cudaStream_t s) {
+  auto a = std::make_shared<AppSolver>();
+  a->g = &new_g;
+  a->form = form;
+  a->mu = mu;
+  a->eps = eps;
+  a->added = plan.added_new;
+  const auto added_s = scalars(plan.added_new);
+  const i64 n_p = i64(added_s.size());
+  if (n_p == 0) return a;
+  if (n_p <= 2048) {  // kDenseAddedLimit counts scalars (els.hpp:40)
+    EntryOracle eo(new_g, form, mu, s);
+    DevBuf<double> app(static_cast<size_t>(n_p * n_p));
+    DevBuf<i64> idx;
+    idx.upload(added_s, s);
+    eo.submatrix(idx.get(), n_p, idx.get(), n_p, app.get(), n_p, s);
+    a->inv.resize(size_t(n_p * n_p));
+    const double rc = dense_inverse(app.get(), n_p, a->inv.get(), s);
+    if (rc < 1e-14) throw Error(4, "added-unknown diagonal block is singular at added block");
+  } else {
+    HbsBuildOptions o;
+    o.eps = eps;
+    a->h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()), o, s);
+    hbs_invert_device(*a->h, s);
+    hbs_build_solve_plan(*a->h);
+  }
+  return a;
+}
 
 std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom& new_g,
                                       const Plan& plan, const Update& upd, int form, double mu,
@@ -96,22 +126,10 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   old_of_ext.insert(old_of_ext.end(), cut_s.begin(), cut_s.end());
   e->d_old_of_ext.upload(old_of_ext, s);
   if (e->n_p > 0) {
-    if (e->n_p <= 2048) {  // kDenseAddedLimit counts scalars (els.hpp:40)
-      EntryOracle eo(new_g, form, mu, s);
-      DevBuf<double> app(static_cast<size_t>(e->n_p * e->n_p));
-      DevBuf<i64> idx;
-      idx.upload(e->added_s, s);
-      eo.submatrix(idx.get(), e->n_p, idx.get(), e->n_p, app.get(), e->n_p, s);
-      e->app_inv.resize(size_t(e->n_p * e->n_p));
-      const double rc = dense_inverse(app.get(), e->n_p, e->app_inv.get(), s);
-      if (rc < 1e-14) throw Error(4, "added-unknown diagonal block is singular at added block");
-    } else {
-      HbsBuildOptions o;
-      o.eps = a_oo.eps;
-      e->app_h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()),
-                                     o, s);
-      hbs_invert_device(*e->app_h, s);
-    }
+    if (upd.app && upd.app->matches(new_g, plan, form, mu, a_oo.eps))
+      e->app = upd.app;
+    else
+      e->app = build_app_solver(new_g, plan, form, mu, a_oo.eps, s);
   }
   phase_mark("els: A_pp", s);
   e->k = upd.k;

@@ -15,10 +15,27 @@
 
 namespace sbx {
 
+// A_pp^{-1} for the added unknowns (els.cpp:98-118): explicit dense inverse
+// when 2 N_p <= 2048 (kDenseAddedLimit, els.hpp:40), else A_pp's own
+// inverted HBS.  It depends only on the refined mesh, so update compression
+// starts building it concurrently (Update::app) and els_build adopts it.
+struct AppSolver {
+  const Geom* g = nullptr;
+  int form = 0;
+  double mu = 0, eps = 0;
+  std::vector<i64> added;           // plan.added_new it was built for
+  std::unique_ptr<HbsOp> h;         // HBS of A_pp above the dense limit
+  DevBuf<double> inv;               // dense A_pp^{-1}
+  bool matches(const Geom& g2, const Plan& p, int f, double m, double e) const {
+    return g == &g2 && form == f && mu == m && eps == e && added == p.added_new;
+  }
+};
+std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan, int formulation,
+                                            double mu, double eps, cudaStream_t s);
+
 struct Els {
   HbsOp* a_oo = nullptr;            // static wall solver (owned by the caller's handle)
-  std::unique_ptr<HbsOp> app_h;     // HBS of A_pp above the dense limit
-  DevBuf<double> app_inv;           // dense A_pp^{-1}
+  std::shared_ptr<AppSolver> app;   // A_pp^{-1}
   i64 n_k = 0, n_c = 0, n_p = 0;    // scalar counts
   i64 k = 0;
   i64 n_ext() const { return n_k + n_c + n_p; }

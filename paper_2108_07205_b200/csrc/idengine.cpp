@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 
 namespace sbx {
 
@@ -18,8 +21,12 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
   d_perm_.reserve(size_t(std::max<i64>(perm_off_[np], 1)));
   d_diag_.reserve(size_t(std::max<i64>(diag_off[np], 1)));
   d_steps_.reserve(std::max<size_t>(np, 1));
-  std::vector<QrJob> jobs, big;
+  std::vector<QrJob> jobs, big, chip;
   coop_.assign(np, 0);
+  static const int tsqr_max_m = [] {
+    const char* e = std::getenv("SBX_TSQR_MAXM");
+    return e ? std::atoi(e) : 0;
+  }();
   for (size_t p = 0; p < np; ++p) {
     const auto& pr = probs[p];
     if (pr.M == 0 || pr.n == 0) continue;
@@ -34,19 +41,32 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
     j.perm = d_perm_.get() + perm_off_[p];
     j.diag = d_diag_.get() + diag_off[p];
     j.steps = d_steps_.get() + p;
-    // one CTA per problem unless the factorisation would stream megabytes
-    // through a single SM; those go to the cooperative multi-CTA kernel
-    const bool coop = force_engine == 2 ||
-                      (force_engine == 0 && i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows);
-    if (coop) {
-      coop_[p] = 1;
-      big.push_back(j);
-    } else {
-      jobs.push_back(j);
+    int engine = force_engine;
+    if (engine == 0) {
+      // one CTA when the problem fits its shared memory (or is a short, tall
+      // TSQR case); else the on-chip cooperative engine when the slabs fit;
+      // else the L2-streaming cooperative engine for big tall problems
+      const bool one_cta = (i64(pr.M) * pr.n + 3 * pr.n + 72) * 8 <= i64(200 * 1024) ||
+                           (pr.n <= 144 && pr.M > pr.n && pr.M <= tsqr_max_m);
+      if (one_cta) engine = 1;
+      else if (cpqr_smem_ctas(pr.M, pr.n) > 0) engine = 3;
+      else if (i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows) engine = 2;
+      else engine = 1;
     }
+    coop_[p] = char(engine);
+    (engine == 2 ? big : engine == 3 ? chip : jobs).push_back(j);
+  }
+  static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
+  if (log) {
+    std::string line = "[sbx-id] eps " + std::to_string(stop_eps) + ":";
+    for (size_t p = 0; p < np; ++p)
+      line += " " + std::to_string(probs[p].M) + "x" + std::to_string(probs[p].n) + "/e" +
+              std::to_string(int(coop_[p]));
+    std::fprintf(stderr, "%s\n", line.c_str());
   }
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
+  cpqr_smem_batched(chip, s);
   std::vector<int> hperm(static_cast<size_t>(perm_off_[np]));
   std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
   if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);

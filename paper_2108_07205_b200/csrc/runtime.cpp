@@ -4,8 +4,10 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "common.hpp"
@@ -17,11 +19,19 @@ std::atomic<std::int64_t> g_launches{0};
 cudaStream_t g_stream = nullptr;
 std::once_flag g_once;
 
-// Size-class free lists.  Blocks are only ever handed back to the same
-// process-wide pool; reuse is ordered because every library temporary lives
-// on the library stream (or is synchronised before release).
+// Size-class free lists, one set per stream.  A block is handed back to the
+// pool of the stream current on the freeing thread, so the next allocation
+// from that pool is stream-ordered after every use of the block: uses on
+// other streams are joined (event wait) into the freeing stream before the
+// owner releases it (see parallel_tasks).
 std::mutex g_pool_mu;
-std::map<size_t, std::vector<void*>> g_pool;
+std::map<cudaStream_t, std::map<size_t, std::vector<void*>>> g_pool;
+thread_local cudaStream_t tl_stream = nullptr;
+
+// worker streams for parallel_tasks (created on demand, reused), one free
+// list per priority class (0 normal, 1 high)
+std::mutex g_ws_mu;
+std::vector<cudaStream_t> g_ws_free[2];
 
 size_t size_class(size_t bytes) {
   if (bytes <= 4096) return 4096;
@@ -51,12 +61,16 @@ cudaStream_t lib_stream() {
   return g_stream;
 }
 
+cudaStream_t cur_stream() { return tl_stream ? tl_stream : lib_stream(); }
+
 void* dev_alloc(size_t bytes) {
   const size_t c = size_class(bytes);
+  const cudaStream_t st = cur_stream();
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    auto it = g_pool.find(c);
-    if (it != g_pool.end() && !it->second.empty()) {
+    auto& pool = g_pool[st];
+    auto it = pool.find(c);
+    if (it != pool.end() && !it->second.empty()) {
       void* p = it->second.back();
       it->second.pop_back();
       return p;
@@ -68,8 +82,9 @@ void* dev_alloc(size_t bytes) {
     (void)cudaGetLastError();
     std::lock_guard<std::mutex> lk(g_pool_mu);
     SBX_CUDA(cudaDeviceSynchronize());
-    for (auto& kv : g_pool)
-      for (void* q : kv.second) cudaFree(q);
+    for (auto& sp : g_pool)
+      for (auto& kv : sp.second)
+        for (void* q : kv.second) cudaFree(q);
     g_pool.clear();
     SBX_CUDA(cudaMalloc(&p, c));
   }
@@ -78,18 +93,87 @@ void* dev_alloc(size_t bytes) {
 
 void dev_free(void* p, size_t bytes) {
   if (!p) return;
+  const cudaStream_t st = cur_stream();
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  g_pool[size_class(bytes)].push_back(p);
+  g_pool[st][size_class(bytes)].push_back(p);
+}
+
+void parallel_tasks(const std::vector<std::function<void(cudaStream_t)>>& tasks, cudaStream_t main,
+                    const std::vector<int>& high) {
+  const size_t nt = tasks.size();
+  if (nt == 0) return;
+  static const bool serial = std::getenv("SBX_SERIAL") != nullptr;  // diagnostics
+  if (serial) {
+    for (const auto& t : tasks) t(main);
+    return;
+  }
+  std::vector<cudaStream_t> ws(nt);
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (size_t i = 0; i < nt; ++i) {
+      const int pc = (i < high.size() && high[i]) ? 1 : 0;
+      auto& fl = g_ws_free[pc];
+      if (fl.empty()) {
+        int least = 0, greatest = 0;
+        SBX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        cudaStream_t w = nullptr;
+        SBX_CUDA(cudaStreamCreateWithPriority(&w, cudaStreamNonBlocking, pc ? greatest : least));
+        fl.push_back(w);
+      }
+      ws[i] = fl.back();
+      fl.pop_back();
+    }
+  }
+  cudaEvent_t fork = nullptr;
+  SBX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  SBX_CUDA(cudaEventRecord(fork, main));
+  int dev = 0;
+  SBX_CUDA(cudaGetDevice(&dev));
+  std::vector<std::exception_ptr> err(nt);
+  std::vector<std::thread> th;
+  th.reserve(nt);
+  for (size_t i = 0; i < nt; ++i) {
+    SBX_CUDA(cudaStreamWaitEvent(ws[i], fork, 0));
+    th.emplace_back([&, i] {
+      tl_stream = ws[i];
+      try {
+        SBX_CUDA(cudaSetDevice(dev));
+        phase_mark(nullptr, ws[i]);
+        tasks[i](ws[i]);
+      } catch (...) {
+        err[i] = std::current_exception();
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (size_t i = 0; i < nt; ++i) {
+    cudaEvent_t done = nullptr;
+    SBX_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    SBX_CUDA(cudaEventRecord(done, ws[i]));
+    SBX_CUDA(cudaStreamWaitEvent(main, done, 0));
+    SBX_CUDA(cudaEventDestroy(done));
+  }
+  SBX_CUDA(cudaEventDestroy(fork));
+  {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    for (size_t i = 0; i < nt; ++i) g_ws_free[(i < high.size() && high[i]) ? 1 : 0].push_back(ws[i]);
+  }
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
 }
 
 void phase_mark(const char* what, cudaStream_t s) {
   static const bool on = std::getenv("SBX_TIMING") != nullptr;
   if (!on) return;
-  static auto last = std::chrono::steady_clock::now();
+  thread_local auto last = std::chrono::steady_clock::now();
+  if (!what) {  // reset (start of a worker task)
+    last = std::chrono::steady_clock::now();
+    return;
+  }
   cudaStreamSynchronize(s);
   const auto now = std::chrono::steady_clock::now();
-  std::fprintf(stderr, "[sbx] %-28s %9.3f ms\n", what,
-               std::chrono::duration<double, std::milli>(now - last).count());
+  std::fprintf(stderr, "[sbx] %-28s %9.3f ms%s\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count(), tl_stream ? " (worker)" : "");
   last = now;
 }
 

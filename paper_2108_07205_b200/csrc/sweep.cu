@@ -220,9 +220,10 @@ void finalize(SweepPlan& plan) {
     add_items(L, items, L.first_task);
     all.insert(all.end(), L.tasks.begin(), L.tasks.end());
   }
-  plan.d_tasks.upload(all, lib_stream());
-  plan.d_items.upload(items, lib_stream());
-  SBX_CUDA(cudaStreamSynchronize(lib_stream()));
+  const cudaStream_t st = cur_stream();
+  plan.d_tasks.upload(all, st);
+  plan.d_items.upload(items, st);
+  SBX_CUDA(cudaStreamSynchronize(st));
   plan.built = true;
 }
 

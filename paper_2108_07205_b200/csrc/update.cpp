@@ -14,11 +14,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <set>
 
 #include "dense.hpp"
+#include "els.hpp"
 #include "entries.hpp"
 #include "idengine.hpp"
 
@@ -499,8 +501,6 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     }
   }
   phase_mark("update: setup", s);
-  RowIdResult far = compress_block_far(enew.view(), ng, far_nodes, circles, true, with_null, ktree, eps, s);
-  phase_mark("update: far ID (kept)", s);
   const std::vector<i64> far_s = scalars(far_pos), near_s = scalars(near_pos);
   // kept-row blocks kc (old oracle) and kp (new oracle)  (lowrank.cpp:130-180)
   const std::vector<i64> kept_old_s = scalars(plan.kept_old), kept_new_s = scalars(plan.kept_new);
@@ -511,44 +511,99 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     for (i64 i : idx) o.push_back(map[size_t(i)]);
     return o;
   };
+  // The five row IDs (far kept, near kc, near kp, far/near pk) are
+  // independent until the stacked factor is assembled; they run as
+  // concurrent tasks on worker streams, together with the A_pp inverse the
+  // following els_build needs (it depends only on the refined mesh).
+  RowIdResult far, kc_near, kp_near, pk_far, pk_near;
+  std::vector<std::string> notes_kc, notes_kp, notes_pk;
+  const bool do_kc = !kept_old_s.empty() && !cut_s.empty();
+  const bool do_kp = !kept_new_s.empty() && !added_s.empty();
+  const bool do_pk_near = u->np2 > 0 && u->nk2 > 0;
+  std::vector<std::function<void(cudaStream_t)>> tasks;
+  tasks.push_back([&](cudaStream_t w) {
+    far = compress_block_far(enew.view(), ng, far_nodes, circles, true, with_null, ktree, eps, w);
+    phase_mark("update: far ID (kept)", w);
+  });
+  if (do_kc)
+    tasks.push_back([&](cudaStream_t w) {
+      kc_near = near_row_id(eold.view(), mapped(kept_old_s, near_s), cut_s, eps, notes_kc, "kc", w);
+      phase_mark("update: kc near ID", w);
+    });
+  if (do_kp)
+    tasks.push_back([&](cudaStream_t w) {
+      kp_near = near_row_id(enew.view(), mapped(kept_new_s, near_s), added_s, eps, notes_kp, "kp", w);
+      phase_mark("update: kp near ID", w);
+    });
+  // added rows against the division surface (lowrank.cpp:296-308, 183-238)
+  if (!plan.added_new.empty())
+    tasks.push_back([&](cudaStream_t w) {
+      std::vector<std::vector<i64>> ptree;
+      for (size_t st = 0; st < plan.added_new.size(); st += 128) {
+        std::vector<i64> l;
+        for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
+        ptree.push_back(std::move(l));
+      }
+      pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, w);
+      phase_mark("update: pk far ID", w);
+    });
+  if (do_pk_near)
+    tasks.push_back([&](cudaStream_t w) {
+      pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, notes_pk, "pk", w);
+      phase_mark("update: pk near ID", w);
+    });
+  const double app_eps = eps;  // els_build adopts it when a_oo was built at this eps
+  if (!plan.added_new.empty())
+    tasks.push_back([&](cudaStream_t w) {
+      try {
+        u->app = build_app_solver(ng, plan, form, mu, app_eps, w);
+      } catch (const Error&) {
+        u->app.reset();  // els_build rebuilds it and reports the error there
+      }
+      phase_mark("update: A_pp inverse (for els_build)", w);
+    });
+  // SBX_PAR_MODE: 0 every task on its own stream; 1 the row IDs in order on
+  // one high-priority stream beside the A_pp build; 2 (default) all tasks in
+  // order on the library stream.  The cooperative CPQR launches need most of
+  // the SMs at once, and other streams' kernels starve them unpredictably
+  // (step times of 40 to 400 ms measured with modes 0/1), so the default
+  // stays serial until every concurrent ID runs without grid-wide barriers.
+  static const int par_mode = [] {
+    const char* e = std::getenv("SBX_PAR_MODE");
+    return e ? std::atoi(e) : 2;
+  }();
+  std::vector<std::function<void(cudaStream_t)>> ids;
+  std::vector<int> high;
+  if (par_mode == 1 && !plan.added_new.empty() && tasks.size() > 1) {
+    auto app_task = tasks.back();
+    tasks.pop_back();
+    ids = std::move(tasks);
+    tasks = {[&ids](cudaStream_t w) {
+               for (auto& t : ids) t(w);
+             },
+             app_task};
+    high = {1, 0};
+  }
+  if (par_mode == 2)
+    for (auto& t : tasks) t(s);
+  else
+    parallel_tasks(tasks, s, high);
+  for (auto* n : {&notes_kc, &notes_kp, &notes_pk}) u->notes.insert(u->notes.end(), n->begin(), n->end());
   struct KeptFactor {
-    RowIdResult nearid;
     i64 k = 0;
     std::vector<i64> skel;  // block-local kept rows
   };
-  auto kept_factor = [&](const EntryOracle& eo, const std::vector<i64>& rowmap,
-                         const std::vector<i64>& colmap, const char* tag) {
+  auto kept_factor = [&](bool on, const RowIdResult& nearid) {
     KeptFactor f;
-    if (rowmap.empty() || colmap.empty()) return f;
-    f.nearid = near_row_id(eo.view(), mapped(rowmap, near_s), colmap, eps, u->notes, tag, s);
-    f.k = far.k + f.nearid.k;
+    if (!on) return f;
+    f.k = far.k + nearid.k;
     for (i64 i = 0; i < far.k; ++i) f.skel.push_back(far_s[size_t(far.J[size_t(i)])]);
-    for (i64 i = 0; i < f.nearid.k; ++i) f.skel.push_back(near_s[size_t(f.nearid.J[size_t(i)])]);
+    for (i64 i = 0; i < nearid.k; ++i) f.skel.push_back(near_s[size_t(nearid.J[size_t(i)])]);
     return f;
   };
-  KeptFactor kc = kept_factor(eold, kept_old_s, cut_s, "kc");
-  phase_mark("update: kc near ID", s);
-  KeptFactor kp = kept_factor(enew, kept_new_s, added_s, "kp");
-  phase_mark("update: kp near ID", s);
-  // added rows against the division surface (lowrank.cpp:296-308, 183-238)
-  RowIdResult pk_far;
-  if (!plan.added_new.empty()) {
-    std::vector<std::vector<i64>> ptree;
-    for (size_t st = 0; st < plan.added_new.size(); st += 128) {
-      std::vector<i64> l;
-      for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
-      ptree.push_back(std::move(l));
-    }
-    pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, s);
-  }
-  phase_mark("update: pk far ID", s);
-  RowIdResult pk_near;
+  KeptFactor kc = kept_factor(do_kc, kc_near), kp = kept_factor(do_kp, kp_near);
   i64 k_pk = 0;
-  if (u->np2 > 0 && u->nk2 > 0) {
-    pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, u->notes, "pk", s);
-    k_pk = pk_far.k + pk_near.k;
-  }
-  phase_mark("update: pk near ID", s);
+  if (do_pk_near) k_pk = pk_far.k + pk_near.k;
   u->k_kc = kc.k;
   u->k_kp = kp.k;
   u->k_pk = k_pk;
@@ -574,11 +629,11 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   };
   if (kc.k > 0) {  // -kc.L in the kept rows
     scat(far.P.get(), d_far_s.get(), far.m, far.k, int(ckc), -1.0);
-    scat(kc.nearid.P.get(), d_near_s.get(), kc.nearid.m, kc.nearid.k, int(ckc + far.k), -1.0);
+    scat(kc_near.P.get(), d_near_s.get(), kc_near.m, kc_near.k, int(ckc + far.k), -1.0);
   }
   if (kp.k > 0) {  // kp.L
     scat(far.P.get(), d_far_s.get(), far.m, far.k, int(ckp), 1.0);
-    scat(kp.nearid.P.get(), d_near_s.get(), kp.nearid.m, kp.nearid.k, int(ckp + far.k), 1.0);
+    scat(kp_near.P.get(), d_near_s.get(), kp_near.m, kp_near.k, int(ckp + far.k), 1.0);
   }
   if (k_pk > 0) {  // pk.L in the added rows
     scat(pk_far.P.get(), d_added_rows.get(), pk_far.m, pk_far.k, 0, 1.0);
@@ -666,13 +721,13 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   gn.rows = i64(near_s.size());
   gn.hrowmap = near_s;
   gn.rowmap = d_near_s.get();
-  if (kc.k > 0 && kc.nearid.k > 0) {
-    gn.src.push_back(kc.nearid.P.get());
-    gn.kcols.push_back(kc.nearid.k);
+  if (kc.k > 0 && kc_near.k > 0) {
+    gn.src.push_back(kc_near.P.get());
+    gn.kcols.push_back(kc_near.k);
   }
-  if (kp.k > 0 && kp.nearid.k > 0) {
-    gn.src.push_back(kp.nearid.P.get());
-    gn.kcols.push_back(kp.nearid.k);
+  if (kp.k > 0 && kp_near.k > 0) {
+    gn.src.push_back(kp_near.P.get());
+    gn.kcols.push_back(kp_near.k);
   }
   ga.rows = u->np2;
   ga.hrowmap = added_rows;

@@ -9,6 +9,8 @@
 
 namespace sbx {
 
+struct AppSolver;
+
 struct Update {
   i64 k = 0, k1 = 0, k_kc = 0, k_kp = 0, k_pk = 0;
   i64 nk2 = 0, nc2 = 0, np2 = 0;
@@ -17,6 +19,9 @@ struct Update {
   DevBuf<double> R;  // k x n_ext, column-major
   std::vector<i64> skeleton;
   std::vector<std::string> notes;
+  // A_pp^{-1} built alongside the compression (adopted by els_build when it
+  // matches; null if its build failed, els_build then reports the error)
+  std::shared_ptr<AppSolver> app;
 };
 
 struct ProxyCircleH {

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--cfg", default="cfg2")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--profile-last", action="store_true",
+                    help="cudaProfilerStart/Stop around the last step (ncu --profile-from-start off)")
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
     sb.init(0)
@@ -50,6 +52,10 @@ def main():
     panels = c.refine_panels(g0.nodes())
     srcs = c.sources()
     for rep in range(a.reps):
+        if a.profile_last and rep == a.reps - 1:
+            import torch
+            torch.cuda.init()
+            torch.cuda.profiler.start()
         s0 = t()
         g1, plan = sb.refine(g0, panels, c.m)
         s1 = t()
@@ -61,6 +67,8 @@ def main():
         s4 = t()
         tau = sb.els_solve(els, G)
         s5 = t()
+        if a.profile_last and rep == a.reps - 1:
+            torch.cuda.profiler.stop()
         ui = upd.info()
         print(f"  step {rep}: refine {s1-s0:.4f} update {s2-s1:.4f} els_build {s3-s2:.4f} "
               f"rhs {s4-s3:.4f} solve {s5-s4:.4f}  total {s5-s0-(s4-s3):.4f}s  k={ui['k']} k1={ui['k1']} "

@@ -37,6 +37,38 @@ def launches(path):
         print(f"| {k} | {c} | {t / 1e3:.3f} | {100 * t / tot:.1f}% | {t / c:.1f} |")
 
 
+def steplist(path):
+    """Per-kernel summary of a one-step capture with grid sizes (SM share)."""
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[hi]
+    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    per = collections.defaultdict(dict)
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        per[int(r[0])]["name"] = r[ki].split("(")[0].replace("sbx::<unnamed>::", "")
+        per[int(r[0])][r[mi]] = float(r[vi].replace(",", ""))
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+    tot = 0.0
+    for d in per.values():
+        us = d.get("gpu__time_duration.sum", 0.0) / 1000.0
+        g = d.get("launch__grid_size", 0.0)
+        a = agg[d["name"]]
+        a[0] += 1
+        a[1] += us
+        a[2] += g
+        a[3] += us * min(1.0, g / 148.0)
+        tot += us
+    print(f"# one-step launch list: `{path}`\n")
+    print(f"Serialised kernel time {tot / 1e3:.2f} ms over {len(per)} launches "
+          "(ncu replays kernels one at a time, cold caches).\n")
+    print("| kernel | launches | total ms | share | mean us | mean grid | SM-weighted ms |")
+    print("|---|---:|---:|---:|---:|---:|---:|")
+    for k, (c, t, g, w) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| {k} | {c} | {t / 1e3:.3f} | {100 * t / tot:.1f}% | {t / c:.1f} | {g / c:.0f} | {w / 1e3:.3f} |")
+
+
 WANT = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -83,4 +115,4 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report, "steplist": steplist}[sys.argv[1]](sys.argv[2])

@@ -27,7 +27,7 @@ def skeleton_identity_exact(k, J, P):
 SHAPES = [(50, 30), (200, 100), (128, 700), (300, 5000), (2500, 300)]
 
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_row_id_matches_oracle(sb, po, engine, shape):
     m, n = shape
@@ -43,7 +43,7 @@ def test_row_id_matches_oracle(sb, po, engine, shape):
     assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
 
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3])
 def test_row_id_forced_rank(sb, po, engine):  # test_idlib.cpp:203-222
     rng = np.random.default_rng(31)
     w = spectrum_matrix(60, 40, 10.0 ** (-0.5 * np.arange(30)), rng)
@@ -55,7 +55,7 @@ def test_row_id_forced_rank(sb, po, engine):  # test_idlib.cpp:203-222
     assert kf <= 4
 
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3])
 def test_row_id_deterministic(sb, engine):
     rng = np.random.default_rng(9)
     w = spectrum_matrix(1200, 512, 10.0 ** (-12 * np.arange(512) / 512), rng)
