@@ -97,21 +97,20 @@ def report(path):
                 i = h.index(w)
                 print(f"| {w} | {v[i]} | {units[i]} |")
         print()
-    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
-    srows = list(csv.reader(io.StringIO(src)))
-    try:
-        hh = srows[1]
-        si, sc = hh.index("Warp Stall Sampling (All Samples)"), hh.index("Source")
-        data = [r for r in srows[2:] if len(r) > si and r[si].isdigit()]
-        tot = sum(int(r[si]) for r in data) or 1
-        print("### top stall sites (SASS, all samples)\n")
-        print("| share | instruction |")
-        print("|---:|---|")
-        for r in sorted(data, key=lambda r: -int(r[si]))[:12]:
-            print(f"| {100 * int(r[si]) / tot:.1f}% | `{r[sc].strip()[:80]}` |")
-    except Exception as e:  # noqa: BLE001
-        print(f"(source page unavailable: {e})")
+    lines, fname = [], "?"
+    for r in csv.reader(io.StringIO(out)):
+        if r and r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+        if len(r) > 4 and r[0].isdigit() and r[4].isdigit():
+            lines.append((int(r[4]), fname, int(r[0]), r[1].strip()))
+    tot = sum(x[0] for x in lines) or 1
+    print("### top source lines by warp-stall samples\n")
+    print("| share | line | source |")
+    print("|---:|---|---|")
+    for smp, f, ln, src_ in sorted(lines, reverse=True)[:15]:
+        print(f"| {100 * smp / tot:.1f}% | {f}:{ln} | `{src_[:90]}` |")
 
 
 if __name__ == "__main__":
