@@ -266,7 +266,7 @@ def roofline_solve(sb, torch, stream, h, state, G_dev):
     flops = 2.0 * nrhs * info["factor_doubles"]
     peaks = measured_fp64_peak()
     achieved = flops / (ms * 1e-3) / 1e12
-    return {"bound": "tensor", "kernel": "sweep_dmma_kernel (hbs_solve, nrhs=64, n=32768)",
+    return {"bound": "tensor", "kernel": "sweep_flow_kernel<DMMA> (one-launch dataflow hbs_solve, nrhs=64, n=32768)",
             "achieved": round(achieved, 3), "peak": peaks["value"], "unit": "TFLOP/s",
             "frac": round(achieved / peaks["value"], 4), "peak_source": peaks["source"],
             "launch_ms": round(ms, 4), "algorithmic_flops": flops, "traffic": None}

@@ -51,12 +51,13 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
   HbsOp& A = *e.a_oo;
   if (!A.solve_plan.built) hbs_build_solve_plan(A);
   SweepPlan& P = A.solve_plan;
-  A.ws.reserve(size_t(P.ws_rows * nrhs));
+  const i64 ldw = sweep_ld(nrhs);
+  A.ws.reserve(size_t(P.ws_rows * ldw));
   const i64 nkc = e.n_k + e.n_c;
-  launch_cm_to_rm(v, ldv, nkc, nrhs, A.ws.get() + P.in_row * nrhs, e.d_old_of_ext.get(), s);
+  launch_cm_to_rm(v, ldv, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
   hbs_run_plan(A, P, A.ws.get(), nrhs, s);
   // gather: out row i <- old row map[i]
-  launch_rm_to_cm(A.ws.get() + P.out_row * nrhs, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
+  launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
   if (e.n_p == 0) return;
   const double* vp = v + nkc;
   double* op = out + nkc;
@@ -64,10 +65,10 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
     HbsOp& H = *e.app->h;
     if (!H.solve_plan.built) hbs_build_solve_plan(H);
     SweepPlan& Q = H.solve_plan;
-    H.ws.reserve(size_t(Q.ws_rows * nrhs));
-    launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * nrhs, nullptr, s);
+    H.ws.reserve(size_t(Q.ws_rows * ldw));
+    launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
     hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
-    launch_rm_to_cm(H.ws.get() + Q.out_row * nrhs, e.n_p, nrhs, op, ldo, nullptr, s);
+    launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, op, ldo, nullptr, s);
   } else {
     gemm_batched({{e.app->inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
                    int(ldo), 0, 0, 1.0, 0.0}},

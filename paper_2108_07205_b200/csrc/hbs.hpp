@@ -39,13 +39,23 @@ struct SweepTask {
   int lda, m, K;
   i64 b_row, p_row, d1_row, d2_row;
   int split;  // rows < split go to D1, the rest to D2 (row - split)
-  int pad;
+  int ndep;   // tasks whose outputs this task reads (dataflow sweep)
+  int dep[4];
+};
+
+// One work item of the dataflow sweep: rows [row0, row0 + tile) x column
+// tile ct of task `task`, over the K range [kb, ke).  Items of a split-K
+// tile (nsplit > 1) write partial tiles at `poff` (+ ks * tile size); the
+// last one to finish (tile counter cidx) sums them in split order.
+struct FlowItem {
+  int task, row0, ct, ks;
+  int nsplit, cidx, kb, ke;
+  long long poff;
 };
 
 struct SweepLevel {
   std::vector<SweepTask> tasks;
   i64 first_task = 0;  // index into the flattened device task table
-  i64 first_item = 0, n_items = 0;
   int max_k = 0;       // largest K in the level (smem sizing)
 };
 
@@ -53,8 +63,19 @@ struct SweepPlan {
   std::vector<SweepLevel> levels;  // launch order
   i64 ws_rows = 0;                 // workspace rows (x nrhs doubles)
   i64 in_row = 0, out_row = 0;     // input / output vector regions
+  int n_tasks = 0;
   DevBuf<SweepTask> d_tasks;
-  DevBuf<int2> d_items;            // (task, row0)
+  // work items (task, row0, col tile) for the current (tile, column-tile
+  // count) key, per-level ranges, and the per-(task, col tile) completion
+  // counters + item ticket of the dataflow sweep
+  int flow_key = -1;
+  std::vector<int2> level_items;
+  DevBuf<FlowItem> d_flow_items;
+  i64 partial_elems = 0;           // split-K partial tiles (doubles)
+  int n_tile_cnt = 0;
+  DevBuf<double> d_partials;
+  i64 n_flow_items = 0;
+  DevBuf<int> d_counters;
   bool built = false;
 };
 
@@ -109,11 +130,15 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
 void hbs_build_solve_plan(HbsOp& op);
 void hbs_build_apply_plan(HbsOp& op);
 
-// Column-major (ld) <-> row-major (nrhs fastest) with an optional row map:
-// dst_row(i) = map ? map[i] : i.
-void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, const i64* map,
+// Row stride (doubles) of the row-major sweep workspace for nrhs columns:
+// even above one column so 64-column B tiles move as 16-byte cp.async.cg.
+inline i64 sweep_ld(i64 nrhs) { return nrhs > 1 ? (nrhs + 1) & ~i64(1) : 1; }
+
+// Column-major (ld) <-> row-major (nrhs fastest, row stride ldw) with an
+// optional row map: dst_row(i) = map ? map[i] : i.
+void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, i64 ldw, const i64* map,
                      cudaStream_t s);
-void launch_rm_to_cm(const double* src, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
+void launch_rm_to_cm(const double* src, i64 ldw, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
                      cudaStream_t s);
 
 }  // namespace sbx

@@ -1,8 +1,10 @@
 // HBS inverse / forward apply sweeps on sm_100a (reference hbs.cpp:511-625).
 //
-// Every level of the up- and down-sweep is one launch of a batched,
-// variable-size product D = A*B (+P) over all boxes of that level, row-tiled
-// so large boxes spread over several CTAs:
+// The whole up- and down-sweep is ONE persistent dataflow launch
+// (sweep_flow_kernel): every box product D = A*B (+P) is cut into row-tile
+// work items taken in tree order, each waiting only for the items that
+// produce its inputs, so tree levels overlap instead of meeting at kernel
+// boundaries (SBX_SWEEP_LEVELS=1 restores one launch per level):
 //   * nrhs == 1 : HBM-bound GEMV (sweep_gemv_kernel).  Factors are read once,
 //     coalesced along columns, with 8 independent loads in flight per thread;
 //     the input vector segment is staged in shared memory.
@@ -11,6 +13,9 @@
 // The leaf products g*b and d*v that only depend on the input are folded
 // into the first (leaf) up-level, so the down-sweep streams e / u only.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 
 #include "hbs.hpp"
 
@@ -21,31 +26,63 @@ namespace {
 constexpr int kTM = 64;       // rows per work item
 constexpr int kThreads = 256;
 
-// ---------------------------------------------------------------- nrhs == 1
-__global__ void __launch_bounds__(kThreads)
-    sweep_gemv_kernel(const double* __restrict__ fac, double* __restrict__ ws,
-                      const SweepTask* __restrict__ tasks, const int2* __restrict__ items) {
-  extern __shared__ double sm[];
-  const int2 it = items[blockIdx.x];
-  const SweepTask t = tasks[it.x];
+// ---------------------------------------------------------------- item bodies
+// One work item = rows [row0, row0 + kTM) (x one 64-column tile for nrhs > 1)
+// of one task's product D = A B (+ P).  Inputs produced inside the same
+// launch are read with L2 loads (__ldcg): the producer published them with
+// a fence before bumping its completion counter.
+
+// nrhs == 1: HBM-bound GEMV over 64-row items, 4 K-slices per item, 8
+// independent loads in flight per thread.  The first batch of the item's
+// factor block is loaded BEFORE the dependency wait, so on the critical
+// path of the sweep the producers' output and the factor stream overlap.
+constexpr int kGR = 64;                // rows per GEMV item
+constexpr int kGS = kThreads / kGR;    // K slices
+constexpr int kGV = 8;                 // columns per load batch
+
+struct GemvRegs {
+  double av[kGV];
+  int j0, j1;
+};
+
+__device__ __forceinline__ void gemv_prefetch(const double* __restrict__ fac, const SweepTask& t,
+                                              int row0, int kb, int ke, GemvRegs& g) {
+  const int r = threadIdx.x % kGR, slice = threadIdx.x / kGR;
+  const int row = row0 + r;
+  const int per = (ke - kb + kGS - 1) / kGS;
+  g.j0 = kb + slice * per;
+  g.j1 = min(ke, g.j0 + per);
+  const double* a = fac + t.a_off + row;
+#pragma unroll
+  for (int q = 0; q < kGV; ++q) {
+    const int j = g.j0 + q;
+    g.av[q] = (row < t.m && j < g.j1) ? __ldg(a + size_t(j) * t.lda) : 0.0;
+  }
+}
+
+// partial != null: write the item's partial row sums there instead of the
+// final rows (split-K).
+__device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, double* __restrict__ ws,
+                                            const SweepTask& t, int row0, int kb, int ke, const GemvRegs& g,
+                                            double* sm, double* partial) {
   const int K = t.K;
-  double* xs = sm;                   // K doubles
-  double* red = sm + ((K + 1) & ~1); // kThreads partial sums
-  for (int j = threadIdx.x; j < K; j += kThreads) xs[j] = ws[t.b_row + j];
+  double* xs = sm;                    // K doubles
+  double* red = sm + ((K + 1) & ~1);  // kThreads partial sums
+  for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(ws + t.b_row + j);
   __syncthreads();
-  const int r = threadIdx.x % kTM;
-  const int slice = threadIdx.x / kTM;
-  constexpr int kSlices = kThreads / kTM;
-  const int row = it.y + r;
-  double acc = 0.0;
+  const int r = threadIdx.x % kGR, slice = threadIdx.x / kGR;
+  const int row = row0 + r;
+  double acc = 0.0, acc1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < kGV; q += 2) {
+    const int j = g.j0 + q;
+    if (j < g.j1) acc = fma(g.av[q], xs[j], acc);
+    if (j + 1 < g.j1) acc1 = fma(g.av[q + 1], xs[j + 1], acc1);
+  }
   if (row < t.m) {
     const double* a = fac + t.a_off + row;
-    const int per = (K + kSlices - 1) / kSlices;
-    const int j0 = slice * per;
-    const int j1 = min(K, j0 + per);
-    int j = j0;
-    double acc1 = 0.0;
-    for (; j + 8 <= j1; j += 8) {
+    int j = g.j0 + kGV;
+    for (; j + 8 <= g.j1; j += 8) {
       double v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) v[q] = __ldg(a + size_t(j + q) * t.lda);
@@ -55,26 +92,39 @@ __global__ void __launch_bounds__(kThreads)
         acc1 = fma(v[q + 1], xs[j + q + 1], acc1);
       }
     }
-    for (; j < j1; ++j) acc = fma(__ldg(a + size_t(j) * t.lda), xs[j], acc);
-    acc += acc1;
+    for (; j < g.j1; ++j) acc = fma(__ldg(a + size_t(j) * t.lda), xs[j], acc);
   }
-  red[threadIdx.x] = acc;
+  red[threadIdx.x] = acc + acc1;
   __syncthreads();
   if (slice == 0 && row < t.m) {
     double s = red[r];
 #pragma unroll
-    for (int q = 1; q < kSlices; ++q) s += red[r + q * kTM];
-    if (t.p_row >= 0) s += ws[t.p_row + row];
+    for (int q = 1; q < kGS; ++q) s += red[r + q * kGR];
+    if (partial) {
+      partial[r] = s;
+      return;
+    }
+    if (t.p_row >= 0) s += __ldcg(ws + t.p_row + row);
     const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
     ws[dst] = s;
   }
 }
 
-// ---------------------------------------------------------------- nrhs >= 2
-// C tile 64 x 64, 8 warps, warp tile 16 x 32 = 2 x 4 m8n8 blocks.
+// nrhs >= 2: C tile 64 x 64 on FP64 tensor cores (mma.sync.m8n8k4.f64 ->
+// SASS DMMA), 8 warps with 16 x 32 warp tiles.  K moves through a 4-stage
+// cp.async pipeline: A (read-only factors, 8-byte .ca copies: factor
+// columns need not be 16-byte aligned) and B (workspace rows produced by
+// other CTAs of the launch: 16-byte .cg copies that bypass L1, whose lines
+// could hold stale neighbours of a just-published row).
 constexpr int kTN = 64;
 constexpr int kKC = 16;
-constexpr int kPad = 8;  // row stride 72 doubles = 16 banks mod 32: 2 wavefronts
+constexpr int kStages = 4;
+constexpr int kPad = 8;  // row stride 72 doubles
+
+struct DmmaSmem {
+  double As[kStages][kKC][kTM + kPad];
+  double Bs[kStages][kKC][kTN + kPad];
+};
 
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -82,101 +132,285 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kThreads)
-    sweep_dmma_kernel(const double* __restrict__ fac, double* __restrict__ ws,
-                      const SweepTask* __restrict__ tasks, const int2* __restrict__ items,
-                      int nrhs) {
-  __shared__ double As[2][kKC][kTM + kPad];
-  __shared__ double Bs[2][kKC][kTN + kPad];
-  const int2 it = items[blockIdx.x];
-  const SweepTask t = tasks[it.x];
-  const int col0 = blockIdx.y * kTN;
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int sz = pred ? 8 : 0;  // zero-fill when out of range
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16_cg(double* dst, const double* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma_issue_a(const double* __restrict__ fac, const SweepTask& t, int row0,
+                                             int stage, int k0, int ke, DmmaSmem& S) {
+  const double* A = fac + t.a_off;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // 0..1023
+    const int kk = idx >> 6, rr = idx & 63;
+    const int grow = row0 + rr, gk = k0 + kk;
+    const bool pa = grow < t.m && gk < ke;
+    cp_async8(&S.As[stage][kk][rr], pa ? A + grow + size_t(gk) * t.lda : A, pa);
+  }
+}
+
+__device__ __forceinline__ void dmma_issue_b(const double* __restrict__ ws, const SweepTask& t, int col0,
+                                             int nrhs, int ldw, int stage, int k0, int ke, DmmaSmem& S) {
+  const double* B = ws + t.b_row * ldw;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // 0..511: 16 rows x 32 pairs
+    const int kk = idx >> 5, pr = (idx & 31) * 2;
+    const int gk = k0 + kk, gcol = col0 + pr;
+    int bytes = 0;
+    if (gk < ke) bytes = gcol + 1 < nrhs ? 16 : (gcol < nrhs ? 8 : 0);
+    cp_async16_cg(&S.Bs[stage][kk][pr], bytes ? B + size_t(gk) * ldw + gcol : B, bytes);
+  }
+}
+
+// Issues the A parts of the first kStages-1 chunks (call before waiting on
+// the producers of B); they join the first commit group.
+__device__ __forceinline__ void dmma_prefetch(const double* __restrict__ fac, const SweepTask& t, int row0,
+                                              int kb, int ke, DmmaSmem& S) {
+  const int nchunks = (ke - kb + kKC - 1) / kKC;
+#pragma unroll
+  for (int c = 0; c < kStages - 1; ++c)
+    if (c < nchunks) dmma_issue_a(fac, t, row0, c, kb + c * kKC, ke, S);
+}
+
+// partial != null: write the raw 64 x 64 tile there (row-major) instead of
+// the final rows (split-K).
+__device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double* __restrict__ ws,
+                                          const SweepTask& t, int row0, int col0, int nrhs, int ldw,
+                                          int kb, int ke, DmmaSmem& S, double* partial) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wm = (warp & 3) * 16;  // warp row offset in tile
-  const int wn = (warp >> 2) * 32; // warp col offset
+  const int wm = (warp & 3) * 16;
+  const int wn = (warp >> 2) * 32;
   double c[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) c[a][b][0] = c[a][b][1] = 0.0;
-
-  const double* A = fac + t.a_off;
-  const double* B = ws + t.b_row * nrhs;
-  const int K = t.K;
-  const int nchunks = (K + kKC - 1) / kKC;
-
-  // loaders: A chunk 16 x 64 (4 per thread), B chunk 16 x 64 (4 per thread)
-  auto load = [&](int buf, int k0) {
+  const int nchunks = (ke - kb + kKC - 1) / kKC;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = threadIdx.x + q * kThreads;  // 0..1023
-      const int kk = idx >> 6, rr = idx & 63;
-      const int grow = it.y + rr, gk = k0 + kk;
-      As[buf][kk][rr] = (grow < t.m && gk < K) ? __ldg(A + grow + size_t(gk) * t.lda) : 0.0;
-      const int gcol = col0 + rr;
-      Bs[buf][kk][rr] = (gk < K && gcol < nrhs) ? B[size_t(gk) * nrhs + gcol] : 0.0;
-    }
-  };
-
-  if (nchunks > 0) load(0, 0);
-  __syncthreads();
+  for (int ch = 0; ch < kStages - 1; ++ch) {  // B of the prologue chunks (A already issued)
+    if (ch < nchunks) dmma_issue_b(ws, t, col0, nrhs, ldw, ch, kb + ch * kKC, ke, S);
+    cp_async_commit();
+  }
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < nchunks) load(buf ^ 1, (ch + 1) * kKC);
+    const int st = ch % kStages;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // chunk ch visible; stage (ch-1) % kStages is free
+    const int nx = ch + kStages - 1;
+    if (nx < nchunks) {
+      dmma_issue_a(fac, t, row0, nx % kStages, kb + nx * kKC, ke, S);
+      dmma_issue_b(ws, t, col0, nrhs, ldw, nx % kStages, kb + nx * kKC, ke, S);
+    }
+    cp_async_commit();
 #pragma unroll
     for (int k4 = 0; k4 < kKC; k4 += 4) {
       double af[2], bf[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = As[buf][k4 + tig][wm + a * 8 + gid];
+      for (int a = 0; a < 2; ++a) af[a] = S.As[st][k4 + tig][wm + a * 8 + gid];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = Bs[buf][k4 + tig][wn + b * 8 + gid];
+      for (int b = 0; b < 4; ++b) bf[b] = S.Bs[st][k4 + tig][wn + b * 8 + gid];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma_m8n8k4(c[a][b][0], c[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
-  // epilogue: rows wm + a*8 + gid, cols wn + b*8 + 2*tig + {0,1}
+  cp_async_wait<0>();
+  __syncthreads();  // smem free for the next item
+  if (partial) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int r = wm + a * 8 + gid, cc = wn + b * 8 + 2 * tig;
+        partial[r * kTN + cc] = c[a][b][0];
+        partial[r * kTN + cc + 1] = c[a][b][1];
+      }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
-    const int row = it.y + wm + a * 8 + gid;
+    const int row = row0 + wm + a * 8 + gid;
     if (row >= t.m) continue;
     const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = col0 + wn + b * 8 + 2 * tig + h;
-        if (col >= nrhs) continue;
-        double v = c[a][b][h];
-        if (t.p_row >= 0) v += ws[(t.p_row + row) * nrhs + col];
-        ws[dst * nrhs + col] = v;
+    for (int b = 0; b < 4; ++b) {
+      const int col = col0 + wn + b * 8 + 2 * tig;
+      double v0 = c[a][b][0], v1 = c[a][b][1];
+      if (t.p_row >= 0) {
+        if (col < nrhs) v0 += __ldcg(ws + (t.p_row + row) * ldw + col);
+        if (col + 1 < nrhs) v1 += __ldcg(ws + (t.p_row + row) * ldw + col + 1);
       }
+      if (col < nrhs) ws[dst * ldw + col] = v0;
+      if (col + 1 < nrhs) ws[dst * ldw + col + 1] = v1;
+    }
   }
+}
+
+// ---------------------------------------------------------------- dataflow sweep
+// The whole up/down sweep is ONE persistent launch.  CTAs take work items
+// in plan order from a ticket counter; an item first waits until every item
+// of the tasks it reads from (same column tile) has completed, then computes
+// and publishes (fence + counter bump).  Items are taken in dependency order
+// and a CTA only waits after taking a ticket, so every awaited item is held
+// by a running CTA: no deadlock, and levels overlap instead of meeting at
+// kernel boundaries.
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool kDmma>
+__global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
+    sweep_flow_kernel(const double* __restrict__ fac, double* __restrict__ ws,
+                      const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
+                      int n_items, int* __restrict__ counters, int ncol, int nrhs, int ldw,
+                      double* __restrict__ partials, int* __restrict__ tile_cnt,
+                      unsigned long long* __restrict__ trace) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int s_next, s_last;
+  constexpr int tile = kDmma ? kTM : kGR;
+  constexpr int tile_elems = kDmma ? kTM * kTN : kGR;
+  int* ticket = counters;  // counters[0]; per-(task, col tile) counts follow
+  if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1);
+  for (;;) {
+    __syncthreads();
+    const int idx = s_next;
+    __syncthreads();  // everyone has read s_next
+    if (idx >= n_items) break;
+    int nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(ticket, 1);  // next ticket, consumed at the end
+    unsigned long long t0 = 0, t1 = 0;
+    if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const FlowItem it = items[idx];
+    const SweepTask t = tasks[it.task];
+    GemvRegs g;
+    if constexpr (kDmma)
+      dmma_prefetch(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem*>(dsm));
+    else
+      gemv_prefetch(fac, t, it.row0, it.kb, it.ke, g);
+    if (threadIdx.x < t.ndep) {
+      const int d = tasks[it.task].dep[threadIdx.x];
+      const int need = (tasks[d].m + tile - 1) / tile;
+      const int* p = counters + 1 + d * ncol + it.ct;
+      while (ld_acquire(p) < need) __nanosleep(32);
+    }
+    __syncthreads();
+    if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    double* part = it.nsplit > 1 ? partials + it.poff + i64(it.ks) * tile_elems : nullptr;
+    if constexpr (kDmma)
+      dmma_item(fac, ws, t, it.row0, it.ct * kTN, nrhs, ldw, it.kb, it.ke,
+                *reinterpret_cast<DmmaSmem*>(dsm), part);
+    else
+      gemv_finish(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
+    __threadfence();
+    __syncthreads();
+    bool done = true;
+    if (it.nsplit > 1) {  // last split of the tile reduces the partials in split order
+      if (threadIdx.x == 0) s_last = atomicAdd(tile_cnt + it.cidx, 1) == it.nsplit - 1;
+      __syncthreads();
+      done = s_last != 0;
+      if (done) {
+        __threadfence();
+        const double* pb = partials + it.poff;
+        if constexpr (kDmma) {
+          for (int e = threadIdx.x; e < kTM * kTN; e += kThreads) {
+            const int r = e / kTN, cc = e % kTN;
+            const int row = it.row0 + r, col = it.ct * kTN + cc;
+            if (row >= t.m || col >= nrhs) continue;
+            double v = 0.0;
+            for (int q = 0; q < it.nsplit; ++q) v += __ldcg(pb + i64(q) * tile_elems + e);
+            if (t.p_row >= 0) v += __ldcg(ws + (t.p_row + row) * ldw + col);
+            const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
+            ws[dst * ldw + col] = v;
+          }
+        } else {
+          for (int r = threadIdx.x; r < kGR; r += kThreads) {
+            const int row = it.row0 + r;
+            if (row >= t.m) continue;
+            double v = 0.0;
+            for (int q = 0; q < it.nsplit; ++q) v += __ldcg(pb + i64(q) * tile_elems + r);
+            if (t.p_row >= 0) v += __ldcg(ws + t.p_row + row);
+            const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
+            ws[dst] = v;
+          }
+        }
+        __threadfence();
+        __syncthreads();
+      }
+    }
+    if (threadIdx.x == 0) {
+      if (done) atomicAdd(counters + 1 + it.task * ncol + it.ct, 1);
+      s_next = nxt;
+      if (trace) {
+        unsigned long long t2;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+        trace[4 * idx] = t0;
+        trace[4 * idx + 1] = t1;
+        trace[4 * idx + 2] = t2;
+        trace[4 * idx + 3] = blockIdx.x;
+      }
+    }
+  }
+}
+
+// Per-level launches (diagnostic path, SBX_SWEEP_LEVELS=1).
+__global__ void __launch_bounds__(kThreads)
+    sweep_gemv_kernel(const double* __restrict__ fac, double* __restrict__ ws,
+                      const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items) {
+  extern __shared__ __align__(16) double dsm[];
+  const FlowItem f = items[blockIdx.x];
+  const int4 it = make_int4(f.task, f.row0, f.ct, 0);
+  const SweepTask t = tasks[it.x];
+  GemvRegs g;
+  gemv_prefetch(fac, t, it.y, 0, t.K, g);
+  gemv_finish(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    sweep_dmma_kernel(const double* __restrict__ fac, double* __restrict__ ws,
+                      const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
+                      int nrhs, int ldw) {
+  extern __shared__ __align__(16) double dsm[];
+  const FlowItem f = items[blockIdx.x];
+  const int4 it = make_int4(f.task, f.row0, f.ct, 0);
+  const SweepTask t = tasks[it.x];
+  DmmaSmem& S = *reinterpret_cast<DmmaSmem*>(dsm);
+  dmma_prefetch(fac, t, it.y, 0, t.K, S);
+  dmma_item(fac, ws, t, it.y, it.z * kTN, nrhs, ldw, 0, t.K, S, nullptr);
 }
 
 // ---------------------------------------------------------------- layout moves
 __global__ void cm_to_rm_kernel(const double* __restrict__ src, i64 ld, i64 n, i64 nrhs,
-                                double* __restrict__ dst, const i64* __restrict__ map) {
+                                double* __restrict__ dst, i64 ldw, const i64* __restrict__ map) {
   const i64 total = n * nrhs;
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
     const i64 i = idx % n, c = idx / n;  // coalesced read along columns
     const i64 r = map ? map[i] : i;
-    dst[r * nrhs + c] = src[i + c * ld];
+    dst[r * ldw + c] = src[i + c * ld];
   }
 }
 
-__global__ void rm_to_cm_kernel(const double* __restrict__ src, i64 n, i64 nrhs,
+__global__ void rm_to_cm_kernel(const double* __restrict__ src, i64 ldw, i64 n, i64 nrhs,
                                 double* __restrict__ dst, i64 ld, const i64* __restrict__ map) {
   const i64 total = n * nrhs;
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
     const i64 i = idx % n, c = idx / n;
     const i64 r = map ? map[i] : i;
-    dst[i + c * ld] = src[r * nrhs + c];
+    dst[i + c * ld] = src[r * ldw + c];
   }
 }
 
@@ -186,43 +420,108 @@ int grid_for(i64 total) {
 
 }  // namespace
 
-void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, const i64* map,
+void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, i64 ldw, const i64* map,
                      cudaStream_t s) {
   if (n * nrhs == 0) return;
-  cm_to_rm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, ld, n, nrhs, dst, map);
+  cm_to_rm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, ld, n, nrhs, dst, ldw, map);
   SBX_LAUNCHED();
 }
 
-void launch_rm_to_cm(const double* src, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
+void launch_rm_to_cm(const double* src, i64 ldw, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
                      cudaStream_t s) {
   if (n * nrhs == 0) return;
-  rm_to_cm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, n, nrhs, dst, ld, map);
+  rm_to_cm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, ldw, n, nrhs, dst, ld, map);
   SBX_LAUNCHED();
 }
 
 namespace {
 
-void add_items(SweepLevel& L, std::vector<int2>& items, i64 task_base) {
-  L.first_item = i64(items.size());
-  for (size_t t = 0; t < L.tasks.size(); ++t) {
-    const auto& tk = L.tasks[t];
-    L.max_k = std::max(L.max_k, tk.K);
-    for (int r0 = 0; r0 < tk.m; r0 += kTM) items.push_back(make_int2(int(task_base + i64(t)), r0));
+// Work items in level order; per level: column tile, then task, then row
+// tile, then K split.  Levels with too few tiles to fill the GPU split K so
+// the short upper levels of the tree (the sweep's critical path) spread
+// over more CTAs.  Returns per-level [first, count).
+std::vector<FlowItem> make_items(SweepPlan& plan, int tile, int ncol, int tile_elems, int target,
+                                 std::vector<int2>* ranges, i64* partial_elems, int* n_tile_cnt) {
+  std::vector<FlowItem> fi;
+  i64 poff = 0;
+  int cidx = 0;
+  for (auto& L : plan.levels) {
+    const i64 first = i64(fi.size());
+    i64 base = 0;
+    for (const auto& tk : L.tasks) base += (tk.m + tile - 1) / tile;
+    base *= ncol;
+    const int lsplit = target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base)) : 1;
+    for (int ct = 0; ct < ncol; ++ct)
+      for (size_t t = 0; t < L.tasks.size(); ++t) {
+        const auto& tk = L.tasks[t];
+        const int ns = std::max(1, std::min(lsplit, tk.K / 32));
+        // split boundaries on multiples of 16 (the DMMA K chunk)
+        const int per = ((tk.K + ns - 1) / ns + 15) / 16 * 16;
+        const int nsplit = std::max(1, (tk.K + per - 1) / std::max(per, 1));
+        for (int r0 = 0; r0 < tk.m; r0 += tile) {
+          for (int ks = 0; ks < nsplit; ++ks) {
+            FlowItem f{};
+            f.task = int(L.first_task + i64(t));
+            f.row0 = r0;
+            f.ct = ct;
+            f.ks = ks;
+            f.nsplit = nsplit;
+            f.kb = ks * per;
+            f.ke = std::min(tk.K, (ks + 1) * per);
+            f.cidx = nsplit > 1 ? cidx : -1;
+            f.poff = nsplit > 1 ? poff : 0;
+            fi.push_back(f);
+          }
+          if (nsplit > 1) {
+            ++cidx;
+            poff += i64(nsplit) * tile_elems;
+          }
+        }
+      }
+    if (ranges) ranges->push_back(make_int2(int(first), int(i64(fi.size()) - first)));
   }
-  L.n_items = i64(items.size()) - L.first_item;
+  *partial_elems = poff;
+  *n_tile_cnt = cidx;
+  return fi;
 }
 
+// Dependencies of the dataflow sweep: every workspace row is written by
+// exactly one task per sweep; a task depends on the writers of the rows it
+// reads (its B rows and its P rows).  Rows written before the launch (the
+// input region) have no writer.
 void finalize(SweepPlan& plan) {
   std::vector<SweepTask> all;
-  std::vector<int2> items;
   for (auto& L : plan.levels) {
     L.first_task = i64(all.size());
-    add_items(L, items, L.first_task);
+    for (const auto& tk : L.tasks) L.max_k = std::max(L.max_k, tk.K);
     all.insert(all.end(), L.tasks.begin(), L.tasks.end());
   }
+  std::vector<int> writer(size_t(plan.ws_rows), -1);
+  for (size_t ti = 0; ti < all.size(); ++ti) {
+    auto& t = all[ti];
+    t.ndep = 0;
+    auto add_reads = [&](i64 r0, i64 nr) {
+      for (i64 r = r0; r < r0 + nr; ++r) {
+        const int w = writer[size_t(r)];
+        if (w < 0) continue;
+        bool seen = false;
+        for (int q = 0; q < t.ndep; ++q) seen |= t.dep[q] == w;
+        if (seen) continue;
+        require(t.ndep < 4, "sweep plan: task reads from more than four producers");
+        t.dep[t.ndep++] = w;
+      }
+    };
+    add_reads(t.b_row, t.K);
+    if (t.p_row >= 0) add_reads(t.p_row, t.m);
+    for (int r = 0; r < t.m; ++r) {
+      const i64 dst = r < t.split ? t.d1_row + r : t.d2_row + (r - t.split);
+      writer[size_t(dst)] = int(ti);
+    }
+  }
+  plan.n_tasks = int(all.size());
+  plan.flow_key = -1;
   const cudaStream_t st = cur_stream();
   plan.d_tasks.upload(all, st);
-  plan.d_items.upload(items, st);
   SBX_CUDA(cudaStreamSynchronize(st));
   plan.built = true;
 }
@@ -238,7 +537,8 @@ SweepTask mk(i64 a_off, i64 lda, i64 m, i64 K, i64 b_row, i64 p_row, i64 d1, i64
   t.d1_row = d1;
   t.d2_row = d2;
   t.split = int(split);
-  t.pad = 0;
+  t.ndep = 0;
+  for (int& d : t.dep) d = -1;
   return t;
 }
 
@@ -388,18 +688,103 @@ void hbs_build_apply_plan(HbsOp& op) {
 
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
   const double* fac = op.arena.get();
-  for (auto& L : plan.levels) {
-    if (L.n_items == 0) continue;
-    const SweepTask* tasks = plan.d_tasks.get();
-    const int2* items = plan.d_items.get() + L.first_item;
-    if (nrhs == 1) {
-      const size_t smem = size_t(((L.max_k + 1) & ~1) + kThreads) * sizeof(double);
-      sweep_gemv_kernel<<<unsigned(L.n_items), kThreads, smem, s>>>(fac, ws, tasks, items);
-    } else {
-      dim3 grid(unsigned(L.n_items), unsigned((nrhs + kTN - 1) / kTN));
-      sweep_dmma_kernel<<<grid, kThreads, 0, s>>>(fac, ws, tasks, items, int(nrhs));
+  const bool dmma = nrhs > 1;
+  static const bool per_level = std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
+  int max_k = 0;
+  for (auto& L : plan.levels) max_k = std::max(max_k, L.max_k);
+  const size_t gemv_smem = size_t(((max_k + 1) & ~1) + kThreads) * sizeof(double);
+  const size_t smem = dmma ? sizeof(DmmaSmem) : gemv_smem;
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(sweep_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(DmmaSmem))));
+    SBX_CUDA(cudaFuncSetAttribute(sweep_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(DmmaSmem))));
+  });
+  const int ncol = dmma ? int((nrhs + kTN - 1) / kTN) : 1;
+  const int tile = dmma ? kTM : kGR;
+  int dev = 0, sms = 148, per_sm = 1;
+  SBX_CUDA(cudaGetDevice(&dev));
+  SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (dmma)
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<true>, kThreads, smem));
+  else
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<false>, kThreads, smem));
+  per_sm = std::max(per_sm, 1);
+  static const int split_env = [] {
+    // split-K of the short upper levels: measured slower on cfg2/cfg3 (the
+    // partial-tile round trip costs more than the shorter K loop saves), so
+    // it is off unless SBX_SWEEP_SPLIT=1
+    const char* e = std::getenv("SBX_SWEEP_SPLIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int target = (per_level || split_env == 0) ? 0 : sms * per_sm;
+  const int key = (ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0);
+  if (plan.flow_key != key) {
+    plan.level_items.clear();
+    const std::vector<FlowItem> fi =
+        make_items(plan, tile, ncol, dmma ? kTM * kTN : kGR, target, &plan.level_items, &plan.partial_elems,
+                   &plan.n_tile_cnt);
+    plan.d_flow_items.upload(fi, s);
+    plan.n_flow_items = i64(fi.size());
+    plan.flow_key = key;
+  }
+  if (per_level) {
+    for (const int2 rg : plan.level_items) {
+      if (rg.y == 0) continue;
+      const FlowItem* items = plan.d_flow_items.get() + rg.x;
+      if (!dmma)
+        sweep_gemv_kernel<<<unsigned(rg.y), kThreads, gemv_smem, s>>>(fac, ws, plan.d_tasks.get(), items);
+      else
+        sweep_dmma_kernel<<<unsigned(rg.y), kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), items, int(nrhs),
+                                                                  int(sweep_ld(nrhs)));
+      SBX_LAUNCHED();
     }
-    SBX_LAUNCHED();
+    return;
+  }
+  if (plan.n_flow_items == 0) return;
+  const size_t ncount = size_t(1 + plan.n_tasks * ncol + plan.n_tile_cnt);
+  plan.d_counters.reserve(ncount);
+  plan.d_partials.reserve(size_t(std::max<i64>(plan.partial_elems, 1)));
+  SBX_CUDA(cudaMemsetAsync(plan.d_counters.get(), 0, ncount * sizeof(int), s));
+  int* tile_cnt = plan.d_counters.get() + 1 + plan.n_tasks * ncol;
+  const int grid = int(std::min<i64>(plan.n_flow_items, i64(sms) * per_sm));
+  static const char* trace_path = std::getenv("SBX_SWEEP_TRACE");  // diagnostics: per-item timeline
+  DevBuf<unsigned long long> trace;
+  if (trace_path) trace.resize(size_t(4 * plan.n_flow_items));
+  if (dmma)
+    sweep_flow_kernel<true><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
+                                                         int(plan.n_flow_items), plan.d_counters.get(), ncol,
+                                                         int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
+                                                         tile_cnt, trace.get());
+  else
+    sweep_flow_kernel<false><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
+                                                          plan.d_flow_items.get(), int(plan.n_flow_items),
+                                                          plan.d_counters.get(), ncol, int(nrhs), 1,
+                                                          plan.d_partials.get(), tile_cnt, trace.get());
+  SBX_LAUNCHED();
+  if (trace_path) {
+    std::vector<unsigned long long> h(size_t(4 * plan.n_flow_items));
+    std::vector<FlowItem> fi(size_t(plan.n_flow_items));
+    trace.download(h.data(), h.size(), s);
+    plan.d_flow_items.download(fi.data(), fi.size(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    std::vector<int> level_of(size_t(plan.n_tasks), 0);
+    for (size_t l = 0; l < plan.levels.size(); ++l)
+      for (size_t t = 0; t < plan.levels[l].tasks.size(); ++t)
+        level_of[size_t(plan.levels[l].first_task) + t] = int(l);
+    if (FILE* f = std::fopen(trace_path, "a")) {
+      std::fprintf(f, "# nrhs %lld items %lld grid %d\n", (long long)nrhs, (long long)plan.n_flow_items, grid);
+      for (i64 i = 0; i < plan.n_flow_items; ++i) {
+        const auto& it = fi[size_t(i)];
+        const auto& tk = plan.levels[size_t(level_of[size_t(it.task)])];
+        (void)tk;
+        std::fprintf(f, "%lld %d %d %d %d %d %llu %llu %llu %llu\n", (long long)i, level_of[size_t(it.task)],
+                     it.task, it.nsplit, it.ke - it.kb, it.row0, h[size_t(4 * i)], h[size_t(4 * i + 1)],
+                     h[size_t(4 * i + 2)], h[size_t(4 * i + 3)]);
+      }
+      std::fclose(f);
+    }
   }
 }
 
@@ -409,7 +794,8 @@ void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, d
   require(nrhs >= 0, "sweep: negative nrhs");
   require(ldb >= op.n && ldx >= op.n, "sweep: leading dimension smaller than n");
   if (nrhs == 0) return;
-  op.ws.reserve(size_t(plan.ws_rows * nrhs));
+  const i64 ldw = sweep_ld(nrhs);
+  op.ws.reserve(size_t(plan.ws_rows * ldw));
   double* ws = op.ws.get();
   const double* bd = b;
   double* xd = x;
@@ -421,9 +807,9 @@ void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, d
     bd = hb;
     xd = hb + op.n * nrhs;
   }
-  launch_cm_to_rm(bd, dev ? ldb : op.n, op.n, nrhs, ws + plan.in_row * nrhs, nullptr, s);
+  launch_cm_to_rm(bd, dev ? ldb : op.n, op.n, nrhs, ws + plan.in_row * ldw, ldw, nullptr, s);
   hbs_run_plan(op, plan, ws, nrhs, s);
-  launch_rm_to_cm(ws + plan.out_row * nrhs, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, s);
+  launch_rm_to_cm(ws + plan.out_row * ldw, ldw, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, s);
   if (!dev) {
     SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, xd, size_t(op.n) * 8, size_t(op.n) * 8,
                                size_t(nrhs), cudaMemcpyDeviceToHost, s));
