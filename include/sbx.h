@@ -126,6 +126,23 @@ int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double*
                   int64_t ldx, int flags, void* stream);
 int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double* y,
                   int64_t ldy, int flags, void* stream);
+/* Subtree-partitioned solve across G = 2^g ranks (one
+ * process per GPU, the caller owns the collective).  Rank p owns the
+ * subtree rooted at the p-th BFS node of depth g: old-mesh scalar rows
+ * [row0, row1).  kmax = largest subtree-root skeleton rank (rows of one
+ * exchanged hat block).  Sequence per solve:
+ *   sbx_hbs_solve_shard_up(b_local -> hat_out)          local up-sweep
+ *   all-gather of the G hat blocks (kmax x nrhs, row-major) in rank order
+ *   sbx_hbs_solve_shard_down(hats -> x_local)           top g levels
+ *                                                       (redundant) + local
+ *                                                       down-sweep
+ * Replaces hbs_solve (hbs.cpp:589-625) split at depth g; the reference is
+ * single-process, so there is no reference signature to mirror. */
+int sbx_hbs_shard_info(sbx_hbs h, int G, int p, int64_t* row0, int64_t* row1, int64_t* kmax);
+int sbx_hbs_solve_shard_up(sbx_hbs h, int G, int p, const double* b_local, int64_t ldb,
+                           int64_t nrhs, double* hat_out, int flags, void* stream);
+int sbx_hbs_solve_shard_down(sbx_hbs h, int G, int p, const double* hats, int64_t nrhs,
+                             double* x_local, int64_t ldx, int flags, void* stream);
 int sbx_hbs_save_hbs1(sbx_hbs h, const char* path);
 int sbx_hbs_load_hbs1(const char* path, sbx_hbs* out);
 /* info[0..9]: n, nodes, total_skeleton, max_block_drawn, has_inverse,

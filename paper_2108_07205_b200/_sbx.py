@@ -89,6 +89,9 @@ _SIGS = [
     ("sbx_hbs_destroy", C.c_int, [VP]),
     ("sbx_hbs_solve", C.c_int, [VP, VP, I64, I64, VP, I64, C.c_int, VP]),
     ("sbx_hbs_apply", C.c_int, [VP, VP, I64, I64, VP, I64, C.c_int, VP]),
+    ("sbx_hbs_shard_info", C.c_int, [VP, C.c_int, C.c_int, I64P, I64P, I64P]),
+    ("sbx_hbs_solve_shard_up", C.c_int, [VP, C.c_int, C.c_int, VP, I64, I64, VP, C.c_int, VP]),
+    ("sbx_hbs_solve_shard_down", C.c_int, [VP, C.c_int, C.c_int, VP, I64, VP, I64, C.c_int, VP]),
     ("sbx_hbs_save_hbs1", C.c_int, [VP, C.c_char_p]),
     ("sbx_hbs_load_hbs1", C.c_int, [C.c_char_p, C.POINTER(VP)]),
     ("sbx_hbs_info", C.c_int, [VP, I64P]),

@@ -287,6 +287,17 @@ def _is_torch_cuda(x):
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: a null handle means "library stream" in sbx.h
+
+
+def torch_stream_handle():
+    """The caller's current torch stream as an sbx.h stream argument (the
+    legacy default stream is passed as cudaStreamLegacy, not as null)."""
+    import torch
+    s = torch.cuda.current_stream().cuda_stream
+    return s if s else CUDA_STREAM_LEGACY
+
+
 def _sweep(fn, op_ptr, b, n, stream=None):
     """Column-major n x nrhs sweep through the C-ABI (host numpy or CUDA torch)."""
     if _is_torch_cuda(b):
@@ -297,7 +308,7 @@ def _sweep(fn, op_ptr, b, n, stream=None):
             raise ValueError("sweep: expected float64 with n rows")
         bcm = bt.t().contiguous()  # column-major storage = transposed row-major
         out = torch.empty_like(bcm)
-        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        s = stream if stream is not None else torch_stream_handle()
         check(fn(op_ptr, VP(bcm.data_ptr()), n, bt.shape[1], VP(out.data_ptr()), n,
                  _sbx.SBX_DEVICE_PTRS, VP(s)))
         res = out.t()
@@ -420,7 +431,7 @@ def _els_call(fn, s: ElsSolver, g, rows_in):
         gcm = gt.t().contiguous()
         out = torch.empty_like(gcm)
         check(fn(s.ptr, VP(gcm.data_ptr()), rows_in, gt.shape[1], VP(out.data_ptr()), rows_in,
-                 _sbx.SBX_DEVICE_PTRS, VP(torch.cuda.current_stream().cuda_stream)))
+                 _sbx.SBX_DEVICE_PTRS, VP(torch_stream_handle())))
         res = out.t()
         return res.reshape(-1) if vec else res
     a = np.asarray(g, dtype=np.float64)

@@ -266,6 +266,7 @@ int sbx_hbs_destroy(sbx_hbs h) {
 int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double* x, int64_t ldx,
                   int flags, void* stream) {
   return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
     sbx::require(!(flags & SBX_TRANSPOSE), "hbs_solve_t is not part of the device path yet");
     sbx::hbs_solve(H(h), b, ldb, nrhs, x, ldx, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
   });
@@ -274,8 +275,36 @@ int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double*
 int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double* y, int64_t ldy,
                   int flags, void* stream) {
   return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
     sbx::require(!(flags & SBX_TRANSPOSE), "hbs_apply_t is not part of the device path yet");
     sbx::hbs_apply(H(h), v, ldv, nrhs, y, ldy, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
+  });
+}
+
+int sbx_hbs_shard_info(sbx_hbs h, int G, int p, int64_t* row0, int64_t* row1, int64_t* kmax) {
+  return guard([&] {
+    const sbx::ShardPlans& S = sbx::hbs_shard(H(h), G, p);
+    *row0 = S.row0;
+    *row1 = S.row1;
+    *kmax = S.kmax;
+  });
+}
+
+int sbx_hbs_solve_shard_up(sbx_hbs h, int G, int p, const double* b_local, int64_t ldb, int64_t nrhs,
+                           double* hat_out, int flags, void* stream) {
+  return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
+    sbx::hbs_solve_shard_up(H(h), G, p, b_local, ldb, nrhs, hat_out, (flags & SBX_DEVICE_PTRS) != 0,
+                            stream_of(stream));
+  });
+}
+
+int sbx_hbs_solve_shard_down(sbx_hbs h, int G, int p, const double* hats, int64_t nrhs, double* x_local,
+                             int64_t ldx, int flags, void* stream) {
+  return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
+    sbx::hbs_solve_shard_down(H(h), G, p, hats, nrhs, x_local, ldx, (flags & SBX_DEVICE_PTRS) != 0,
+                              stream_of(stream));
   });
 }
 
@@ -383,6 +412,7 @@ int sbx_els_info(sbx_els e, int64_t* info) {
 int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, double* tau_n,
                   int64_t ldt, int flags, void* stream) {
   return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
     sbx::require(e && e->e, "null els handle");
     sbx::els_solve(*e->e, g_n, ldg, nrhs, tau_n, ldt, false, (flags & SBX_DEVICE_PTRS) != 0,
                    stream_of(stream));
@@ -392,6 +422,7 @@ int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, doubl
 int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
                       int64_t ldy, int flags, void* stream) {
   return guard([&] {
+    sbx::StreamScope scope(stream_of(stream));
     sbx::require(e && e->e, "null els handle");
     sbx::els_solve(*e->e, g_ext, ldg, nrhs, y, ldy, true, (flags & SBX_DEVICE_PTRS) != 0,
                    stream_of(stream));

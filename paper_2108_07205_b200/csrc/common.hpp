@@ -52,6 +52,20 @@ cudaStream_t lib_stream();
 void* dev_alloc(size_t bytes);
 void dev_free(void* p, size_t bytes);
 cudaStream_t cur_stream();
+// Makes `s` the calling thread's current stream (allocation pool and plan
+// uploads follow it) for the scope's lifetime: C-ABI calls that take a
+// caller stream run entirely on it.
+cudaStream_t set_cur_stream(cudaStream_t s);
+class StreamScope {
+ public:
+  explicit StreamScope(cudaStream_t s) : prev_(set_cur_stream(s)) {}
+  ~StreamScope() { set_cur_stream(prev_); }
+  StreamScope(const StreamScope&) = delete;
+  StreamScope& operator=(const StreamScope&) = delete;
+
+ private:
+  cudaStream_t prev_;
+};
 
 // Runs independent host+device tasks concurrently: task i gets its own
 // thread and worker stream (forked from `main`, joined back into it), so the

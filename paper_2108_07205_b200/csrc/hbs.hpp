@@ -79,6 +79,8 @@ struct SweepPlan {
   bool built = false;
 };
 
+struct ShardPlans;
+
 struct HbsOp {
   i64 n = 0, leaf_nodes = 64;
   double eps = 0.0;
@@ -92,6 +94,7 @@ struct HbsOp {
   DevBuf<double> arena;
   i64 arena_used = 0;
   SweepPlan solve_plan, apply_plan;
+  std::unique_ptr<struct ShardPlans> shard;  // subtree-partitioned solve (multi-GPU)
   DevBuf<double> ws;  // sweep workspace (grown on demand)
   DevBuf<double> io;  // staging for host-pointer sweeps (grown on demand)
 
@@ -129,6 +132,24 @@ void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s);
 void hbs_build_solve_plan(HbsOp& op);
 void hbs_build_apply_plan(HbsOp& op);
+
+// Subtree-partitioned solve: rank p of G = 2^g owns the
+// subtree rooted at the p-th BFS node of depth g, i.e. old-mesh scalar rows
+// [row0, row1).  shard_up runs the local up-sweep and packs the subtree
+// root's hat (k_p x nrhs, zero-padded to kmax rows, row-major) into hat_out;
+// after the caller all-gathers the G hats, shard_down runs the top g levels
+// redundantly and the local down-sweep into x_local.
+struct ShardPlans {
+  int G = 0, p = -1, g = 0;
+  i64 row0 = 0, row1 = 0, kmax = 0;
+  std::vector<i64> roots;  // BFS ids of the G subtree roots
+  SweepPlan up, top, down;
+};
+ShardPlans& hbs_shard(HbsOp& op, int G, int p);
+void hbs_solve_shard_up(HbsOp& op, int G, int p, const double* b_local, i64 ldb, i64 nrhs, double* hat_out,
+                        bool dev, cudaStream_t s);
+void hbs_solve_shard_down(HbsOp& op, int G, int p, const double* hats, i64 nrhs, double* x_local, i64 ldx,
+                          bool dev, cudaStream_t s);
 
 // Row stride (doubles) of the row-major sweep workspace for nrhs columns:
 // even above one column so 64-column B tiles move as 16-byte cp.async.cg.

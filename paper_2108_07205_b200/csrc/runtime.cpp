@@ -63,6 +63,12 @@ cudaStream_t lib_stream() {
 
 cudaStream_t cur_stream() { return tl_stream ? tl_stream : lib_stream(); }
 
+cudaStream_t set_cur_stream(cudaStream_t s) {
+  const cudaStream_t prev = tl_stream;
+  tl_stream = s;
+  return prev;
+}
+
 void* dev_alloc(size_t bytes) {
   const size_t c = size_class(bytes);
   const cudaStream_t st = cur_stream();

@@ -544,36 +544,56 @@ SweepTask mk(i64 a_off, i64 lda, i64 m, i64 K, i64 b_row, i64 p_row, i64 d1, i64
 
 }  // namespace
 
-void hbs_build_solve_plan(HbsOp& op) {
-  require(op.has_inverse, "hbs_solve: inverse not built");
-  SweepPlan& P = op.solve_plan;
-  P.levels.clear();
+namespace {
+// Workspace rows of the solve: IN, OUT, HAT (k_i), PP (c_i), INC (k_i).
+struct SolveLayout {
+  std::vector<i64> hat, pp, inc;
+  i64 in_row = 0, out_row = 0, ws_rows = 0;
+};
+
+SolveLayout solve_layout(const HbsOp& op) {
   const size_t nn = op.nodes.size();
-  // workspace rows: IN, OUT, HAT (k_i), PP (c_i), INC (k_i); node order
-  std::vector<i64> hat(nn, 0), pp(nn, 0), inc(nn, 0);
+  SolveLayout Y;
+  Y.hat.assign(nn, 0);
+  Y.pp.assign(nn, 0);
+  Y.inc.assign(nn, 0);
   i64 row = 0;
-  P.in_row = row;
+  Y.in_row = row;
   row += op.n;
-  P.out_row = row;
+  Y.out_row = row;
   row += op.n;
   for (size_t i = 1; i < nn; ++i) {
-    hat[i] = row;
+    Y.hat[i] = row;
     row += op.nodes[i].k;
   }
   for (size_t i = 1; i < nn; ++i) {
-    pp[i] = row;
+    Y.pp[i] = row;
     row += op.nodes[i].c;
   }
   for (size_t i = 1; i < nn; ++i) {
-    inc[i] = row;
+    Y.inc[i] = row;
     row += op.nodes[i].k;
   }
-  P.ws_rows = row;
+  Y.ws_rows = row;
+  return Y;
+}
+
+// Solve tasks: up-sweep of the nodes in up_sel (deepest level first), the
+// root product when `root`, down-sweep of the nodes in down_sel.
+void build_solve_tasks(const HbsOp& op, const SolveLayout& Y, const std::vector<char>& up_sel, bool root,
+                       const std::vector<char>& down_sel, SweepPlan& P) {
+  P.levels.clear();
+  P.in_row = Y.in_row;
+  P.out_row = Y.out_row;
+  P.ws_rows = Y.ws_rows;
+  const size_t nn = op.nodes.size();
   if (nn == 1) {  // single leaf: x = root_g b (hbs.cpp:592)
-    SweepLevel L;
-    const i64 c = op.nodes[0].c;
-    L.tasks.push_back(mk(op.o_root_g, c, c, c, P.in_row, -1, P.out_row, 0, c));
-    P.levels.push_back(std::move(L));
+    if (root) {
+      SweepLevel L;
+      const i64 c = op.nodes[0].c;
+      L.tasks.push_back(mk(op.o_root_g, c, c, c, Y.in_row, -1, Y.out_row, 0, c));
+      P.levels.push_back(std::move(L));
+    }
     finalize(P);
     return;
   }
@@ -581,29 +601,150 @@ void hbs_build_solve_plan(HbsOp& op) {
     SweepLevel L;
     for (size_t i = 1; i < nn; ++i) {
       const auto& nd = op.nodes[i];
-      if (nd.depth != d) continue;
-      const i64 b = nd.is_leaf() ? P.in_row + 2 * nd.begin : hat[size_t(nd.left)];
-      L.tasks.push_back(mk(nd.o_fg, nd.k + nd.c, nd.k + nd.c, nd.c, b, -1, hat[i], pp[i], nd.k));
+      if (nd.depth != d || !up_sel[i]) continue;
+      const i64 b = nd.is_leaf() ? Y.in_row + 2 * nd.begin : Y.hat[size_t(nd.left)];
+      L.tasks.push_back(mk(nd.o_fg, nd.k + nd.c, nd.k + nd.c, nd.c, b, -1, Y.hat[i], Y.pp[i], nd.k));
     }
     if (!L.tasks.empty()) P.levels.push_back(std::move(L));
   }
-  for (int d = 0; d <= op.max_depth; ++d) {  // down
+  if (root) {
     SweepLevel L;
-    for (size_t i = 0; i < nn; ++i) {
+    const auto& nd = op.nodes[0];
+    L.tasks.push_back(mk(op.o_root_g, nd.c, nd.c, nd.c, Y.hat[size_t(nd.left)], -1, Y.inc[size_t(nd.left)], 0,
+                         nd.c));
+    P.levels.push_back(std::move(L));
+  }
+  for (int d = 1; d <= op.max_depth; ++d) {  // down
+    SweepLevel L;
+    for (size_t i = 1; i < nn; ++i) {
       const auto& nd = op.nodes[i];
-      if (nd.depth != d) continue;
-      if (i == 0) {
-        const i64 c = nd.c;
-        L.tasks.push_back(mk(op.o_root_g, c, c, c, hat[size_t(nd.left)], -1, inc[size_t(nd.left)], 0, c));
-      } else if (!nd.is_leaf()) {
-        L.tasks.push_back(mk(nd.o_e, nd.c, nd.c, nd.k, inc[i], pp[i], inc[size_t(nd.left)], 0, nd.c));
-      } else {
-        L.tasks.push_back(mk(nd.o_e, nd.c, nd.c, nd.k, inc[i], pp[i], P.out_row + 2 * nd.begin, 0, nd.c));
-      }
+      if (nd.depth != d || !down_sel[i]) continue;
+      const i64 dst = nd.is_leaf() ? Y.out_row + 2 * nd.begin : Y.inc[size_t(nd.left)];
+      L.tasks.push_back(mk(nd.o_e, nd.c, nd.c, nd.k, Y.inc[i], Y.pp[i], dst, 0, nd.c));
     }
     if (!L.tasks.empty()) P.levels.push_back(std::move(L));
   }
   finalize(P);
+}
+}  // namespace
+
+void hbs_build_solve_plan(HbsOp& op) {
+  require(op.has_inverse, "hbs_solve: inverse not built");
+  const SolveLayout Y = solve_layout(op);
+  const std::vector<char> all(op.nodes.size(), 1);
+  build_solve_tasks(op, Y, all, true, all, op.solve_plan);
+}
+
+ShardPlans& hbs_shard(HbsOp& op, int G, int p) {
+  require(op.has_inverse, "hbs_solve: inverse not built");
+  require(G >= 1 && (G & (G - 1)) == 0, "shard: rank count must be a power of two");
+  require(p >= 0 && p < G, "shard: rank out of range");
+  if (op.shard && op.shard->G == G && op.shard->p == p) return *op.shard;
+  // the previous plans' tables may still be read by kernels in flight on
+  // another stream: drain before they return to the pool
+  if (op.shard) SBX_CUDA(cudaDeviceSynchronize());
+  auto S = std::make_unique<ShardPlans>();
+  S->G = G;
+  S->p = p;
+  int g = 0;
+  while ((1 << g) < G) ++g;
+  S->g = g;
+  const size_t nn = op.nodes.size();
+  // subtree roots: BFS nodes of depth g, in order; every leaf must lie at depth >= g
+  for (size_t i = 0; i < nn; ++i) {
+    if (op.nodes[i].depth == g) S->roots.push_back(i64(i));
+    if (op.nodes[i].is_leaf())
+      require(op.nodes[i].depth >= g, "shard: tree has a leaf above the partition depth");
+  }
+  require(i64(S->roots.size()) == G, "shard: tree has fewer subtrees than ranks at that depth");
+  std::vector<i64> owner(nn, -1);  // subtree index of every node at depth >= g
+  for (size_t q = 0; q < S->roots.size(); ++q) owner[size_t(S->roots[q])] = i64(q);
+  for (size_t i = 0; i < nn; ++i)  // BFS order: parents come first
+    if (op.nodes[i].depth > g) owner[i] = owner[size_t(op.nodes[i].parent)];
+  const auto& sr = op.nodes[size_t(S->roots[size_t(p)])];
+  S->row0 = 2 * sr.begin;
+  S->row1 = 2 * sr.end;
+  for (i64 r : S->roots) S->kmax = std::max(S->kmax, op.nodes[size_t(r)].k);
+  const SolveLayout Y = solve_layout(op);
+  std::vector<char> mine(nn, 0), above(nn, 0), none(nn, 0);
+  for (size_t i = 1; i < nn; ++i) {
+    mine[i] = owner[i] == p;
+    above[i] = op.nodes[i].depth >= 1 && op.nodes[i].depth < g;
+  }
+  if (g == 0) {  // one rank: the subtree is the whole tree, the root product is "top"
+    build_solve_tasks(op, Y, mine, false, none, S->up);
+    build_solve_tasks(op, Y, none, true, none, S->top);
+    build_solve_tasks(op, Y, none, false, mine, S->down);
+  } else {
+    build_solve_tasks(op, Y, mine, false, none, S->up);
+    build_solve_tasks(op, Y, above, true, above, S->top);
+    build_solve_tasks(op, Y, none, false, mine, S->down);
+  }
+  op.shard = std::move(S);
+  return *op.shard;
+}
+
+void hbs_solve_shard_up(HbsOp& op, int G, int p, const double* b_local, i64 ldb, i64 nrhs, double* hat_out,
+                        bool dev, cudaStream_t s) {
+  ShardPlans& S = hbs_shard(op, G, p);
+  const i64 rows = S.row1 - S.row0;
+  require(nrhs >= 1 && ldb >= rows, "shard_up: bad sizes");
+  const i64 ldw = sweep_ld(nrhs);
+  op.ws.reserve(size_t(S.up.ws_rows * ldw));
+  double* ws = op.ws.get();
+  const double* bd = b_local;
+  if (!dev) {
+    op.io.reserve(size_t(rows * nrhs));
+    SBX_CUDA(cudaMemcpy2DAsync(op.io.get(), size_t(rows) * 8, b_local, size_t(ldb) * 8, size_t(rows) * 8,
+                               size_t(nrhs), cudaMemcpyHostToDevice, s));
+    bd = op.io.get();
+  }
+  launch_cm_to_rm(bd, dev ? ldb : rows, rows, nrhs, ws + (S.up.in_row + S.row0) * ldw, ldw, nullptr, s);
+  hbs_run_plan(op, S.up, ws, nrhs, s);
+  // pack hat of the subtree root: k rows (x nrhs, row-major), zero-padded to kmax
+  const auto& sr = op.nodes[size_t(S.roots[size_t(p)])];
+  const i64 hat_row = solve_layout(op).hat[size_t(S.roots[size_t(p)])];
+  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (S.kmax > 0) {
+    if (dev) SBX_CUDA(cudaMemsetAsync(hat_out, 0, size_t(S.kmax * nrhs) * 8, s));
+    else std::memset(hat_out, 0, size_t(S.kmax * nrhs) * 8);
+    if (sr.k > 0 && S.g > 0)
+      SBX_CUDA(cudaMemcpy2DAsync(hat_out, size_t(nrhs) * 8, ws + hat_row * ldw, size_t(ldw) * 8,
+                                 size_t(nrhs) * 8, size_t(sr.k), kind, s));
+  }
+  if (!dev) SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+void hbs_solve_shard_down(HbsOp& op, int G, int p, const double* hats, i64 nrhs, double* x_local, i64 ldx,
+                          bool dev, cudaStream_t s) {
+  ShardPlans& S = hbs_shard(op, G, p);
+  const i64 rows = S.row1 - S.row0;
+  require(nrhs >= 1 && ldx >= rows, "shard_down: bad sizes");
+  const i64 ldw = sweep_ld(nrhs);
+  require(op.ws.size() >= size_t(S.up.ws_rows * ldw), "shard_down: call shard_up first");
+  double* ws = op.ws.get();
+  const SolveLayout Y = solve_layout(op);
+  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if (S.g > 0)
+    for (int q = 0; q < G; ++q) {  // the other ranks' subtree-root hats
+      if (q == p) continue;
+      const i64 r = S.roots[size_t(q)];
+      const i64 k = op.nodes[size_t(r)].k;
+      if (k > 0)
+        SBX_CUDA(cudaMemcpy2DAsync(ws + Y.hat[size_t(r)] * ldw, size_t(ldw) * 8, hats + i64(q) * S.kmax * nrhs,
+                                   size_t(nrhs) * 8, size_t(nrhs) * 8, size_t(k), kind, s));
+    }
+  hbs_run_plan(op, S.top, ws, nrhs, s);
+  hbs_run_plan(op, S.down, ws, nrhs, s);
+  if (dev) {
+    launch_rm_to_cm(ws + (S.down.out_row + S.row0) * ldw, ldw, rows, nrhs, x_local, ldx, nullptr, s);
+  } else {
+    op.io.reserve(size_t(rows * nrhs));
+    launch_rm_to_cm(ws + (S.down.out_row + S.row0) * ldw, ldw, rows, nrhs, op.io.get(), rows, nullptr, s);
+    SBX_CUDA(cudaMemcpy2DAsync(x_local, size_t(ldx) * 8, op.io.get(), size_t(rows) * 8, size_t(rows) * 8,
+                               size_t(nrhs), cudaMemcpyDeviceToHost, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
 }
 
 void hbs_build_apply_plan(HbsOp& op) {
