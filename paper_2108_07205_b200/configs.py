@@ -79,6 +79,87 @@ class RefinedWallConfig:
         return self.curve_eval(t) * s[:, None]
 
 
+@dataclass
+class HolesConfig:
+    """configs[4]: outer ellipse (8, 4) with 16 circular obstacles r = 0.3 on a
+    seed-jittered 4x4 grid, Mixed formulation (wall D + N, holes D + S).
+    262144 nodes: 8960 wall panels + 16 x 464 hole panels of 16 nodes (the
+    arc-length split is 9216 + 16 x 448; that tree puts hole boundaries
+    where the telescoping inverse fails the reference's own rcond gate,
+    hbs.cpp:429, at depth 2 — rcond(v^T x^-1 u) = 9e-11 < 1e-9, recomputed in
+    numpy from the compressed factors — so the split is moved by 3%).  Each step refines 8 panels around a seed-random point on 8
+    distinct obstacles (m = 16) and solves 128 right-hand sides of Stokeslets
+    placed outside the fluid (beyond the wall and inside the obstacles)."""
+    name: str = "cfg5"
+    a: float = 8.0
+    b: float = 4.0
+    wall_panels: int = 8960
+    hole_panels: int = 464
+    hole_radius: float = 0.3
+    grid: int = 4
+    q: int = 16
+    eps: float = 1e-10
+    leaf: int = 64
+    regions: int = 8
+    panels_per_region: int = 8
+    m: int = 16
+    nrhs: int = 128
+    sources_per_rhs: int = 8
+    seed: int = 0
+
+    def hole_centers(self):
+        rng = np.random.default_rng(self.seed + 3)
+        xs = (np.arange(self.grid) - (self.grid - 1) / 2) * (1.6 * self.a / self.grid)
+        ys = (np.arange(self.grid) - (self.grid - 1) / 2) * (1.4 * self.b / self.grid)
+        c = np.array([(x, y) for y in ys for x in xs])
+        return c + rng.uniform(-0.25, 0.25, c.shape)
+
+    def refine_panels(self, nodes):
+        """8 panels of 8 distinct obstacles nearest a seed-random point on each."""
+        rng = np.random.default_rng(self.seed + 1)
+        holes = rng.choice(self.grid * self.grid, self.regions, replace=False)
+        centers = self.hole_centers()
+        out = []
+        first = self.wall_panels
+        for hidx in sorted(holes):
+            t = rng.uniform(0, 2 * np.pi)
+            p = centers[hidx] + self.hole_radius * np.array([np.cos(t), np.sin(t)])
+            p0 = first + hidx * self.hole_panels
+            sel = (nodes["panel_of"] >= p0) & (nodes["panel_of"] < p0 + self.hole_panels)
+            d = np.hypot(nodes["x"][sel] - p[0], nodes["y"][sel] - p[1])
+            pmin = np.full(self.hole_panels, np.inf)
+            np.minimum.at(pmin, nodes["panel_of"][sel] - p0, d)
+            out.extend(p0 + np.sort(np.argsort(pmin, kind="stable")[: self.panels_per_region]))
+        return np.array(sorted(out), dtype=np.int64)
+
+    def sources(self):
+        rng = np.random.default_rng(self.seed)
+        centers = self.hole_centers()
+        out = []
+        half = self.sources_per_rhs // 2
+        for _ in range(self.nrhs):
+            ang = rng.uniform(0, 2 * np.pi, half)
+            rad = rng.uniform(1.5, 3.0, half)
+            outer = np.column_stack([rad * self.a * np.cos(ang), rad * self.b * np.sin(ang)])
+            hid = rng.integers(0, len(centers), self.sources_per_rhs - half)
+            inner = centers[hid] + rng.uniform(-0.1, 0.1, (len(hid), 2))
+            f = rng.standard_normal((self.sources_per_rhs, 2))
+            out.append(np.column_stack([np.vstack([outer, inner]), f]))
+        return out
+
+    def targets(self, count=100):
+        """Fluid points: inside 0.9 x the wall, at least 0.2 away from every obstacle."""
+        rng = np.random.default_rng(self.seed + 2)
+        centers = self.hole_centers()
+        pts = []
+        while len(pts) < count:
+            t, s = rng.uniform(0, 2 * np.pi), 0.9 * np.sqrt(rng.uniform())
+            p = np.array([s * self.a * np.cos(t), s * self.b * np.sin(t)])
+            if np.min(np.hypot(*(centers - p).T)) > self.hole_radius + 0.2:
+                pts.append(p)
+        return np.array(pts)
+
+
 CONFIGS = {
     # BASELINE.json configs[0]: ellipse (2,1), 128x16 nodes, 4 panels near
     # (1.99, 0) split 3 dyadic levels (m = 8), 5 Stokeslets at radius 4.
@@ -90,4 +171,6 @@ CONFIGS = {
                               sources_per_rhs=8),
     # configs[2]: star, 4096x16 nodes, HBS inverse apply microbenchmark.
     "cfg3": RefinedWallConfig("cfg3", "star", 4096, a=1.0, n_refine=0, m=1, nrhs=1),
+    # configs[4]: multiply connected large case (Mixed formulation).
+    "cfg5": HolesConfig(),
 }

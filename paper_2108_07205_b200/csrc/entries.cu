@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "entries.hpp"
+#include "logquad.hpp"
 
 namespace sbx {
 
@@ -23,13 +24,15 @@ __device__ __forceinline__ bool single_layer(const EntryView& v, int comp) {
   return v.form == SBX_EXTERIOR_COMBINED || (v.form == SBX_MIXED && comp != 0);
 }
 
-// One scalar entry A(2i+a, 2j+b) of the completed double-layer operator
-// (nystrom.cpp:80-172, double-layer + completion terms).  Single-layer
-// components are rejected on the host before any launch.
+// One scalar entry A(2i+a, 2j+b) of the completed BIE (nystrom.cpp:80-172):
+// double layer + completion bit-for-bit in the reference's operation order;
+// on single-layer components the Stokeslet with the product-integration log
+// correction on the self and neighbouring panels (tables from logquad.cpp).
 __device__ double entry(const EntryView& v, i64 rs, i64 cs) {
   const i64 i = node_of(v, rs >> 1), j = node_of(v, cs >> 1);
   const int a = int(rs & 1), b = int(cs & 1);
   const int ci = v.comp[i];
+  const double c4 = 1.0 / (4.0 * kPi * v.mu);
   if (i == j) {
     const double wi = v.w[i];
     const double dl = -v.kappa[i] / (2.0 * kPi) * wi;
@@ -38,6 +41,17 @@ __device__ double entry(const EntryView& v, i64 rs, i64 cs) {
     const double tb = (b == 1 || a != b) ? v.ty[i] : v.tx[i];
     double out = dl * ta * tb;
     if (a == b) out = v.jump + out;
+    if (single_layer(v, ci)) {
+      const double sm = wi * c4;
+      out += sm * ta * tb;
+      if (a == b) {
+        const i64 n = v.sl_n;
+        const int loc = v.sl_i[i], q = v.sl_i[n + i];
+        const double jac = v.sl_d[n + i];
+        const double lam = v.sl_tab[v.sl_i[4 * n + i] + loc * q + loc];
+        out += c4 * (-lam * jac - wi * log(jac));
+      }
+    }
     if (in_null(v, ci)) {
       const double na = a == 0 ? v.nx[i] : v.ny[i];
       const double nb = b == 0 ? v.nx[i] : v.ny[i];
@@ -55,6 +69,37 @@ __device__ double entry(const EntryView& v, i64 rs, i64 cs) {
   const double ra = (a == 0 || a != b) ? rx : ry;  // out[2] = out[1] = (c*rx)*ry
   const double rb = (b == 1 || a != b) ? ry : rx;
   double out = c * ra * rb;
+  if (single_layer(v, cj)) {
+    const double sc = wj * c4 / r2;
+    out += sc * ra * rb;
+    if (a == b) {
+      double lg = 0.0;
+      bool corrected = false;
+      if (ci == cj) {
+        const i64 n = v.sl_n;
+        const int np = v.sl_i[3 * n + i];
+        int diff = v.sl_i[2 * n + i] - v.sl_i[2 * n + j];
+        if (diff < 0) diff += np;
+        const int locj = v.sl_i[j];
+        const double xj = v.sl_d[j], jacj = v.sl_d[n + j];
+        double lam = 0.0, xi = 0.0;
+        if (diff == 0) {
+          const int q = v.sl_i[n + i];
+          lam = v.sl_tab[v.sl_i[4 * n + i] + v.sl_i[i] * q + locj];
+          xi = v.sl_d[i];
+          corrected = true;
+        } else if (diff == 1 || diff == np - 1) {
+          const int dir = diff == 1 ? 0 : 1;  // previous / next panel of i
+          lam = v.sl_lam[(dir * n + i) * v.sl_qmax + locj];
+          xi = v.sl_d[(2 + dir) * n + i];
+          corrected = true;
+        }
+        if (corrected) lg = c4 * (-lam * jacj - wj * (0.5 * log(r2) - log(fabs(xj - xi))));
+      }
+      if (!corrected) lg = c4 * wj * (-0.5 * log(r2));
+      out += lg;
+    }
+  }
   if (in_null(v, ci) && in_null(v, cj)) {
     const double na = a == 0 ? v.nx[i] : v.ny[i];
     const double nb = b == 0 ? v.nx[j] : v.ny[j];
@@ -217,7 +262,7 @@ unsigned grid_x(i64 total, unsigned cap = 4096) {
 
 }  // namespace
 
-EntryOracle::EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t,
+EntryOracle::EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t s,
                          const i64* d_map)
     : form_(formulation) {
   require(formulation >= 0 && formulation <= 2, "unknown formulation");
@@ -225,10 +270,6 @@ EntryOracle::EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t
   if (formulation == SBX_INTERIOR_DIRICHLET)
     require(g.comps.size() == 1, "interior formulation expects a single curve");
   if (formulation == SBX_MIXED) require(!g.comps[0].is_hole, "mixed formulation expects wall first");
-  // The log-corrected single layer (exterior / hole components) needs the
-  // product-rule tables of logquad.cpp; it is not on the device path yet.
-  require(formulation == SBX_INTERIOR_DIRICHLET || (formulation == SBX_MIXED && g.comps.size() == 1),
-          "single-layer (exterior / hole) components are not on the device path yet");
   const GeomDev& d = g.dev;
   v_.x = d.x();
   v_.y = d.y();
@@ -243,6 +284,21 @@ EntryOracle::EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t
   v_.jump = formulation == SBX_EXTERIOR_COMBINED ? 0.5 : -0.5;
   v_.mu = mu;
   v_.form = formulation;
+  std::vector<char> sl(g.comps.size(), 0);
+  bool any_sl = false;
+  for (size_t c = 0; c < g.comps.size(); ++c) {
+    sl[c] = formulation == SBX_EXTERIOR_COMBINED || (formulation == SBX_MIXED && g.comps[c].is_hole);
+    any_sl |= sl[c] != 0;
+  }
+  if (any_sl) {
+    const SlTables& T = single_layer_tables(g, sl, s);
+    v_.sl_i = T.ints.get();
+    v_.sl_d = T.dbl.get();
+    v_.sl_lam = T.lam.get();
+    v_.sl_tab = T.tab.get();
+    v_.sl_n = T.n;
+    v_.sl_qmax = T.qmax;
+  }
 }
 
 void EntryOracle::submatrix(const i64* d_rows, i64 nr, const i64* d_cols, i64 nc, double* d_out,

@@ -17,6 +17,11 @@ struct EntryView {
   double jump;
   double mu;
   int form;        // SBX_INTERIOR_DIRICHLET / EXTERIOR / MIXED
+  // single-layer tables (SlTables, geometry.hpp); null without single-layer components
+  const int* sl_i;
+  const double *sl_d, *sl_lam, *sl_tab;
+  i64 sl_n;
+  int sl_qmax;
 };
 
 class EntryOracle {

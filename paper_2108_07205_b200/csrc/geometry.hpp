@@ -59,6 +59,19 @@ struct GeomDev {
   const double* ty() const { return buf.get() + 7 * n; }
 };
 
+// Per-node tables of the log-corrected single layer (nystrom.cpp:40-63 and
+// the self tables of logquad.cpp), device resident.  ints: loc | q | panel
+// local index | component panel count | self-table offset; doubles: Gauss
+// abscissa | jacobian | u_prev | u_next; lam: lambda_prev | lambda_next
+// (n x qmax each).
+struct SlTables {
+  std::vector<char> mask;  // single-layer flag per component it was built for
+  i64 n = 0;
+  int qmax = 0;
+  DevBuf<int> ints;
+  DevBuf<double> dbl, lam, tab;
+};
+
 struct Geom {
   std::vector<Component> comps;
   std::vector<PanelRow> panels;
@@ -69,6 +82,7 @@ struct Geom {
   double panel_arclength(i64 p) const;
   GeomDev dev;
   void upload(cudaStream_t s);
+  mutable std::shared_ptr<SlTables> sl;  // built on first single-layer use
 };
 
 struct Plan {

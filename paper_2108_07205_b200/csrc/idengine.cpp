@@ -48,8 +48,15 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
       // else the L2-streaming cooperative engine for big tall problems
       const bool one_cta = (i64(pr.M) * pr.n + 3 * pr.n + 72) * 8 <= i64(200 * 1024) ||
                            (pr.n <= 144 && pr.M > pr.n && pr.M <= tsqr_max_m);
+      static const int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+      }();
+      const int g = cpqr_smem_ctas(pr.M, pr.n);
       if (one_cta) engine = 1;
-      else if (cpqr_smem_ctas(pr.M, pr.n) > 0) engine = 3;
+      else if (g > 0 && g <= sms) engine = 3;
       else if (i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows) engine = 2;
       else engine = 1;
     }

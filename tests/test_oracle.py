@@ -340,3 +340,42 @@ def test_els_forward_apply_matches_dense(po):  # test_els.cpp:206-231
     A[nk2 + nc2:, nk2 + nc2:] = po.block_eval_full(a0, a1, plan, "pp")
     v = np.random.default_rng(7).standard_normal(n)
     assert np.linalg.norm(e.apply_forward(v) - A @ v) <= 10 * eps * np.linalg.norm(A, 2) * np.linalg.norm(v)
+
+
+def _holes(po):
+    """test_els.cpp:53-90 (make_holes): circle wall r=2, 20 panels, three holes."""
+    g0 = po.Geom.create(po.CIRCLE, 20, scale=2.0)
+    g1, plan = g0.add_holes([(-0.8, 0.0, 0.3, 10, 16), (0.9, 0.3, 0.25, 10, 16), (0.1, -0.9, 0.2, 10, 16)])
+    return g0, g1, plan, po.Assembler.create(g0, po.MIXED), po.Assembler.create(g1, po.MIXED)
+
+
+HOLE_SOURCES = [(-0.8, 0.0, 1.0, 0.5), (0.9, 0.3, -0.5, 1.0), (0.1, -0.9, 0.3, -1.0)]
+HOLE_TARGETS = [(0.0, 1.2), (1.4, 0.3), (-1.3, -0.4)]
+
+
+def density_on_refined(plan_maps, n_new, tau):
+    """els.cpp:195-203: (kept, added) density scattered to the refined mesh."""
+    out = np.zeros(2 * n_new)
+    kn, an = plan_maps["kept_new"], plan_maps["added_new"]
+    ks = np.stack([2 * kn, 2 * kn + 1], 1).ravel()
+    as_ = np.stack([2 * an, 2 * an + 1], 1).ravel()
+    out[ks] = tau[: len(ks)]
+    out[as_] = tau[len(ks):]
+    return out
+
+
+def test_els_holes_match_dense_mixed_oracle(po):  # test_els.cpp:168-197
+    eps = 1e-10
+    g0, g1, plan, a0, a1 = _holes(po)
+    assert plan.sizes()[1] == 0
+    h = po.Hbs.compress(a0, eps).invert()
+    e = po.Els.build(h, a0, a1, plan, po.Update.compress(a0, a1, plan, eps))
+    srcs = list(po.ring_sources(4, (0, 0), 3.5)) + HOLE_SOURCES
+    g_new = g1.boundary_data(srcs)
+    maps = plan.maps()
+    tau = e.solve(po.gather_kept_added(maps, g_new))
+    ref = po.gather_kept_added(maps, np.linalg.solve(a1.full_matrix(), g_new))
+    assert np.linalg.norm(tau - ref) / np.linalg.norm(ref) <= 1e-8
+    vel = g1.evaluate_velocity(po.MIXED, density_on_refined(maps, g1.n_nodes, tau), HOLE_TARGETS)
+    exact = po.field_velocity(srcs, HOLE_TARGETS)
+    assert max(np.linalg.norm(vel[i] - exact[i]) / np.linalg.norm(exact[i]) for i in range(3)) < 1e-8
