@@ -527,6 +527,8 @@ struct CoopArgs {
   const int* part_off;
   double* beta;        // signed R diagonal per job (offset beta_off)
   const i64* beta_off;
+  double* vglob;       // per-CTA Householder vectors in global memory (null: in smem)
+  i64 vstride;
 };
 
 __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
@@ -540,8 +542,10 @@ __global__ void __launch_bounds__(kCT) cpqr_coop_kernel(CoopArgs args) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int c0 = int(i64(n) * rank / G), c1 = int(i64(n) * (rank + 1) / G);
   const int nown = c1 - c0;
-  double* v = sm;                // M
-  double* upd = v + M;           // nown
+  // Householder vector: shared memory, or this CTA's global (L2) slot for
+  // functionals too many for it
+  double* v = args.vglob ? args.vglob + size_t(blockIdx.x) * args.vstride : sm;  // M
+  double* upd = args.vglob ? sm : v + M;  // nown
   double* dir = upd + nown;      // nown
   double* red = dir + nown;      // 32
   double* sc = red + 32;         // 8
@@ -1210,6 +1214,94 @@ __device__ void warp_lu_solve_t(const double* lu, int n, int lda, double (&x)[kM
   }
 }
 
+// Reciprocal 1-norm condition estimate (Eigen ConditionEstimator.h,
+// Hager/Higham) of a matrix with 1-norm l1 from its explicit inverse X
+// (n x n, ld n), CTA-wide.  work: 4n doubles; red/ired: block scratch.
+__device__ double rcond_from_inverse(const double* X, int n, double l1, double* work, double* red, int* ired) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {
+    __shared__ int s_flag;
+    double* v = work;          // n
+    double* sg = work + n;     // n
+    double* osg = work + 2 * n;  // n
+    double* tmp = work + 3 * n;  // n
+    auto gemv = [&](const double* x, double* y, bool trans) {  // y = X x or X^T x
+      if (!trans) {
+        for (int i = tid; i < n; i += kT) {
+          double a = 0.0;
+          for (int c = 0; c < n; ++c) a += X[i + size_t(c) * n] * x[c];
+          y[i] = a;
+        }
+      } else {
+        for (int c = warp; c < n; c += kWarps) {
+          double a = 0.0;
+          for (int i = lane; i < n; i += 32) a += X[i + size_t(c) * n] * x[i];
+          a = warp_sum(a);
+          if (lane == 0) y[c] = a;
+        }
+      }
+      __syncthreads();
+    };
+    auto l1sum = [&](const double* x) {
+      double a = 0.0;
+      for (int i = tid; i < n; i += kT) a += fabs(x[i]);
+      return block_sum(a, red);
+    };
+    double result;
+    if (l1 == 0.0) {
+      result = 0.0;
+    } else if (n == 1) {
+      result = 1.0;
+    } else {
+      for (int i = tid; i < n; i += kT) tmp[i] = 1.0 / double(n);
+      __syncthreads();
+      gemv(tmp, v, false);
+      double lower = l1sum(v), old_lower = lower;
+      int old_vmax = -1;
+      for (int it = 0; it < 4; ++it) {
+        int differs = 0;
+        for (int i = tid; i < n; i += kT) {
+          sg[i] = v[i] < 0.0 ? -1.0 : 1.0;
+          if (it > 0 && sg[i] != osg[i]) differs = 1;
+        }
+        if (tid == 0) s_flag = 0;
+        __syncthreads();
+        if (differs) s_flag = 1;
+        __syncthreads();
+        if (it > 0 && s_flag == 0) break;
+        gemv(sg, tmp, true);
+        double bv = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = tid; i < n; i += kT)
+          if (fabs(tmp[i]) > bv) {
+            bv = fabs(tmp[i]);
+            bi = i;
+          }
+        double mv;
+        int vmax;
+        block_argmax(bv, bi, red, ired, mv, vmax);
+        if (vmax == old_vmax) break;
+        for (int i = tid; i < n; i += kT) v[i] = X[i + size_t(vmax) * n];
+        __syncthreads();
+        lower = l1sum(v);
+        if (lower <= old_lower) break;
+        for (int i = tid; i < n; i += kT) osg[i] = sg[i];
+        __syncthreads();
+        old_vmax = vmax;
+        old_lower = lower;
+      }
+      for (int i = tid; i < n; i += kT)
+        tmp[i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
+      __syncthreads();
+      gemv(tmp, v, false);
+      const double alt = 2.0 * l1sum(v) / (3.0 * double(n));
+      const double inv_norm = fmax(lower, alt);
+      result = inv_norm == 0.0 ? 0.0 : (1.0 / inv_norm) / l1;
+    }
+    return result;
+  }
+}
+
 __global__ void __launch_bounds__(kT) lu_kernel(const LuJob* __restrict__ jobs, int smem_doubles) {
   extern __shared__ double sm[];
   const LuJob jb = jobs[blockIdx.x];
@@ -1331,90 +1423,178 @@ __global__ void __launch_bounds__(kT) lu_kernel(const LuJob* __restrict__ jobs, 
   // reciprocal condition estimate (Eigen ConditionEstimator.h) with the
   // explicit inverse standing in for the LU solves
   if (jb.rcond) {
-    __shared__ int s_flag;
-    double* v = jb.work;          // n
-    double* sg = jb.work + n;     // n
-    double* osg = jb.work + 2 * n;  // n
-    double* tmp = jb.work + 3 * n;  // n
-    auto gemv = [&](const double* x, double* y, bool trans) {  // y = X x or X^T x
-      if (!trans) {
-        for (int i = tid; i < n; i += kT) {
-          double a = 0.0;
-          for (int c = 0; c < n; ++c) a += X[i + size_t(c) * n] * x[c];
-          y[i] = a;
-        }
-      } else {
-        for (int c = warp; c < n; c += kWarps) {
-          double a = 0.0;
-          for (int i = lane; i < n; i += 32) a += X[i + size_t(c) * n] * x[i];
-          a = warp_sum(a);
-          if (lane == 0) y[c] = a;
-        }
-      }
-      __syncthreads();
-    };
-    auto l1sum = [&](const double* x) {
-      double a = 0.0;
-      for (int i = tid; i < n; i += kT) a += fabs(x[i]);
-      return block_sum(a, red);
-    };
-    double result;
-    if (l1 == 0.0) {
-      result = 0.0;
-    } else if (n == 1) {
-      result = 1.0;
-    } else {
-      for (int i = tid; i < n; i += kT) tmp[i] = 1.0 / double(n);
-      __syncthreads();
-      gemv(tmp, v, false);
-      double lower = l1sum(v), old_lower = lower;
-      int old_vmax = -1;
-      for (int it = 0; it < 4; ++it) {
-        int differs = 0;
-        for (int i = tid; i < n; i += kT) {
-          sg[i] = v[i] < 0.0 ? -1.0 : 1.0;
-          if (it > 0 && sg[i] != osg[i]) differs = 1;
-        }
-        if (tid == 0) s_flag = 0;
-        __syncthreads();
-        if (differs) s_flag = 1;
-        __syncthreads();
-        if (it > 0 && s_flag == 0) break;
-        gemv(sg, tmp, true);
-        double bv = -1.0;
-        int bi = 0x7fffffff;
-        for (int i = tid; i < n; i += kT)
-          if (fabs(tmp[i]) > bv) {
-            bv = fabs(tmp[i]);
-            bi = i;
-          }
-        double mv;
-        int vmax;
-        block_argmax(bv, bi, red, ired, mv, vmax);
-        if (vmax == old_vmax) break;
-        for (int i = tid; i < n; i += kT) v[i] = X[i + size_t(vmax) * n];
-        __syncthreads();
-        lower = l1sum(v);
-        if (lower <= old_lower) break;
-        for (int i = tid; i < n; i += kT) osg[i] = sg[i];
-        __syncthreads();
-        old_vmax = vmax;
-        old_lower = lower;
-      }
-      for (int i = tid; i < n; i += kT)
-        tmp[i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
-      __syncthreads();
-      gemv(tmp, v, false);
-      const double alt = 2.0 * l1sum(v) / (3.0 * double(n));
-      const double inv_norm = fmax(lower, alt);
-      result = inv_norm == 0.0 ? 0.0 : (1.0 / inv_norm) / l1;
-    }
-    if (tid == 0) *jb.rcond = result;
+    const double r = rcond_from_inverse(X, n, l1, jb.work, red, ired);
+    if (tid == 0) *jb.rcond = r;
   }
   __syncthreads();
   if (in_smem) {
     for (int c = warp; c < n; c += kWarps)
       for (int i = lane; i < n; i += 32) jb.a[i + size_t(c) * jb.lda] = mat[i + size_t(c) * n];
+  }
+}
+
+
+// ---------------------------------------------------------------- blocked LU (large n)
+// Right-looking partial-pivot LU in panels of kLuNb columns: panel
+// factorisation by one CTA (smem when it fits, else L2), row swaps, unit
+// lower TRSM for the U12 block row and the A22 update as a DMMA GEMM; the
+// explicit inverse by blocked forward/backward substitution (diagonal-block
+// kernels + DMMA GEMM updates).  Same pivots (first max) and rounding model
+// as lu_kernel up to summation order; used for the large dense blocks
+// (A_pp up to 2048, Woodbury W, upper HBS levels).
+constexpr int kLuNb = 32;
+constexpr int kLuBlockedMin = 384;
+
+__global__ void l1norm_kernel(const double* __restrict__ A, int n, int lda, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= n) return;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += fabs(A[i + size_t(c) * lda]);
+  s = warp_sum(s);
+  if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(s));
+}
+
+__global__ void __launch_bounds__(kT) panel_lu_kernel(double* A, int n, int lda, int j0, int nb, int* ipiv,
+                                                      int smem_doubles) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x;
+  double* red = sm;
+  int* ired = reinterpret_cast<int*>(sm + 32);
+  double* P = sm + 64;
+  const int m = n - j0;
+  const bool in_smem = 64 + size_t(m) * nb <= size_t(smem_doubles);
+  double* Pn = in_smem ? P : A + j0 + size_t(j0) * lda;
+  const int ld = in_smem ? m : lda;
+  if (in_smem) {
+    for (int e = tid; e < m * nb; e += kT) {
+      const int i = e % m, c = e / m;
+      P[e] = A[j0 + i + size_t(j0 + c) * lda];
+    }
+    __syncthreads();
+  }
+  for (int c = 0; c < nb; ++c) {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = c + tid; i < m; i += kT) {
+      const double v = fabs(Pn[i + size_t(c) * ld]);
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+    double mv;
+    int p;
+    block_argmax(bv, bi, red, ired, mv, p);
+    if (mv == 0.0) p = c;  // exactly singular column: no swap, no scaling
+    if (tid == 0) ipiv[j0 + c] = j0 + p;
+    if (p != c)
+      for (int q = tid; q < nb; q += kT) {
+        const double t = Pn[c + size_t(q) * ld];
+        Pn[c + size_t(q) * ld] = Pn[p + size_t(q) * ld];
+        Pn[p + size_t(q) * ld] = t;
+      }
+    __syncthreads();
+    if (mv != 0.0) {
+      const double d = Pn[c + size_t(c) * ld];
+      for (int i = c + 1 + tid; i < m; i += kT) Pn[i + size_t(c) * ld] /= d;
+    }
+    __syncthreads();
+    const int rr = m - c - 1, cc = nb - c - 1;
+    for (int e = tid; e < rr * cc; e += kT) {
+      const int i = c + 1 + e % rr, q = c + 1 + e / rr;
+      Pn[i + size_t(q) * ld] -= Pn[i + size_t(c) * ld] * Pn[c + size_t(q) * ld];
+    }
+    __syncthreads();
+  }
+  if (in_smem)
+    for (int e = tid; e < m * nb; e += kT) {
+      const int i = e % m, c = e / m;
+      A[j0 + i + size_t(j0 + c) * lda] = P[e];
+    }
+}
+
+// The panel's row interchanges applied to the columns outside it.
+__global__ void lu_swap_kernel(double* A, int n, int lda, int j0, int nb, const int* __restrict__ ipiv) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= n || (col >= j0 && col < j0 + nb)) return;
+  double* a = A + size_t(col) * lda;
+  for (int c = 0; c < nb; ++c) {
+    const int p = ipiv[j0 + c], r = j0 + c;
+    if (p != r) {
+      const double t = a[r];
+      a[r] = a[p];
+      a[p] = t;
+    }
+  }
+}
+
+// B(r0:r0+nb, cols) <- T^{-1} B(r0:r0+nb, cols), T = the nb x nb diagonal
+// block of L (unit lower, lower=1) or U (upper, lower=0) at (r0, r0) of A.
+__global__ void lu_diag_trsm_kernel(const double* __restrict__ A, int lda, int r0, int nb, double* B, int ldb,
+                                    int c0, int ncols, int lower) {
+  __shared__ double T[kLuNb * kLuNb];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    T[e] = A[r0 + i + size_t(r0 + j) * lda];
+  }
+  __syncthreads();
+  const int col = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= c0 + ncols) return;
+  double* b = B + size_t(col) * ldb + r0;
+  double x[kLuNb];
+#pragma unroll
+  for (int i = 0; i < kLuNb; ++i) x[i] = i < nb ? b[i] : 0.0;
+  if (lower) {
+#pragma unroll
+    for (int i = 0; i < kLuNb; ++i) {
+      if (i >= nb) break;
+      double acc = x[i];
+#pragma unroll
+      for (int l = 0; l < kLuNb; ++l)
+        if (l < i) acc -= T[i + l * nb] * x[l];
+      x[i] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int i = kLuNb - 1; i >= 0; --i) {
+      if (i >= nb) continue;
+      double acc = x[i];
+#pragma unroll
+      for (int l = 0; l < kLuNb; ++l)
+        if (l > i && l < nb) acc -= T[i + l * nb] * x[l];
+      x[i] = acc / T[i + i * nb];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kLuNb; ++i)
+    if (i < nb) b[i] = x[i];
+}
+
+__global__ void perm_identity_kernel(double* X, int n, const int* __restrict__ perm) {
+  const i64 total = i64(n) * n;
+  for (i64 e = blockIdx.x * i64(blockDim.x) + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const int i = int(e % n), c = int(e / n);
+    X[e] = perm[i] == c ? 1.0 : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kT) rcond_kernel(const double* __restrict__ X, int n, const double* l1,
+                                                   double* work, double* out) {
+  __shared__ double red[32];
+  __shared__ int ired[64];
+  const double r = rcond_from_inverse(X, n, *l1, work, red, ired);
+  if (threadIdx.x == 0) *out = r;
+}
+
+__global__ void ipiv_to_perm_kernel(const int* __restrict__ ipiv, int n, int* perm) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int i = 0; i < n; ++i) perm[i] = i;
+  for (int i = 0; i < n; ++i) {
+    const int p = ipiv[i];
+    const int t = perm[i];
+    perm[i] = perm[p];
+    perm[p] = t;
   }
 }
 
@@ -1532,11 +1712,14 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   // first pass: CTAs in proportion to work (columns bound the split)
   double W = 0.0;
   for (const auto& j : jobs) W += double(j.M) * double(j.n);
+  int maxM = 0;
+  for (const auto& j : jobs) maxM = std::max(maxM, j.M);
+  const bool vglob = size_t(maxM) * 8 > kSmemCap / 2;  // tall: Householder vector in L2
   auto smem_for = [&](const std::vector<int>& G) {
     size_t mx = 0;
     for (size_t q = 0; q < jobs.size(); ++q) {
       const int nown = (jobs[q].n + G[q] - 1) / G[q];
-      mx = std::max(mx, size_t(jobs[q].M + 2 * nown + 40) * 8 + size_t(96 + nown) * 4 + 64);
+      mx = std::max(mx, size_t((vglob ? 0 : jobs[q].M) + 2 * nown + 40) * 8 + size_t(96 + nown) * 4 + 64);
     }
     return mx;
   };
@@ -1612,6 +1795,14 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   a.parts = d_parts.get();
   a.beta = d_beta.get();
   a.beta_off = d_boff.get();
+  static thread_local DevBuf<double> d_v;
+  a.vglob = nullptr;
+  a.vstride = 0;
+  if (vglob) {
+    a.vstride = (i64(maxM) + 31) / 32 * 32;
+    d_v.reserve(size_t(a.vstride) * cta_job.size());
+    a.vglob = d_v.get();
+  }
   void* params[] = {&a};
   SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_coop_kernel),
                                        dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
@@ -1790,7 +1981,86 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
   }
 }
 
-void lu_batched(const std::vector<LuJob>& jobs, cudaStream_t s) {
+
+namespace {
+void lu_blocked(const LuJob& j, cudaStream_t s) {
+  const int n = j.n, lda = j.lda;
+  static thread_local DevBuf<int> d_ipiv;
+  static thread_local DevBuf<double> d_l1;
+  d_ipiv.reserve(size_t(n));
+  d_l1.reserve(1);
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(panel_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+  });
+  if (j.rcond) {
+    SBX_CUDA(cudaMemsetAsync(d_l1.get(), 0, sizeof(double), s));
+    l1norm_kernel<<<unsigned((n + 7) / 8), 256, 0, s>>>(j.a, n, lda, d_l1.get());
+    SBX_LAUNCHED();
+  }
+  for (int j0 = 0; j0 < n; j0 += kLuNb) {
+    const int nb = std::min(kLuNb, n - j0);
+    const size_t need = std::min(kSmemCap, (64 + size_t(n - j0) * nb) * sizeof(double));
+    panel_lu_kernel<<<1, kT, need, s>>>(j.a, n, lda, j0, nb, d_ipiv.get(), int(need / sizeof(double)));
+    SBX_LAUNCHED();
+    lu_swap_kernel<<<unsigned((n + 127) / 128), 128, 0, s>>>(j.a, n, lda, j0, nb, d_ipiv.get());
+    SBX_LAUNCHED();
+    const int rest = n - j0 - nb;
+    if (rest > 0) {
+      lu_diag_trsm_kernel<<<unsigned((rest + 127) / 128), 128, 0, s>>>(j.a, lda, j0, nb, j.a, lda, j0 + nb,
+                                                                      rest, 1);
+      SBX_LAUNCHED();
+      gemm_batched({{j.a + (j0 + nb) + size_t(j0) * lda, j.a + j0 + size_t(j0 + nb) * lda,
+                     j.a + (j0 + nb) + size_t(j0 + nb) * lda, rest, rest, nb, lda, lda, lda, 0, 0, -1.0, 1.0}},
+                   s);
+    }
+  }
+  ipiv_to_perm_kernel<<<1, 1, 0, s>>>(d_ipiv.get(), n, j.piv);
+  SBX_LAUNCHED();
+  // X = U^{-1} L^{-1} P
+  double* X = j.inv;
+  perm_identity_kernel<<<unsigned(std::min<i64>((i64(n) * n + 255) / 256, 148 * 16)), 256, 0, s>>>(X, n, j.piv);
+  SBX_LAUNCHED();
+  const unsigned cg = unsigned((n + 127) / 128);
+  for (int r0 = 0; r0 < n; r0 += kLuNb) {
+    const int nb = std::min(kLuNb, n - r0);
+    lu_diag_trsm_kernel<<<cg, 128, 0, s>>>(j.a, lda, r0, nb, X, n, 0, n, 1);
+    SBX_LAUNCHED();
+    const int below = n - r0 - nb;
+    if (below > 0)
+      gemm_batched({{j.a + (r0 + nb) + size_t(r0) * lda, X + r0, X + r0 + nb, below, n, nb, lda, n, n, 0, 0,
+                     -1.0, 1.0}},
+                   s);
+  }
+  for (int r0 = ((n - 1) / kLuNb) * kLuNb; r0 >= 0; r0 -= kLuNb) {
+    const int nb = std::min(kLuNb, n - r0);
+    lu_diag_trsm_kernel<<<cg, 128, 0, s>>>(j.a, lda, r0, nb, X, n, 0, n, 0);
+    SBX_LAUNCHED();
+    if (r0 > 0)
+      gemm_batched({{j.a + size_t(r0) * lda, X + r0, X, r0, n, nb, lda, n, n, 0, 0, -1.0, 1.0}}, s);
+  }
+  if (j.rcond) {
+    rcond_kernel<<<1, kT, 0, s>>>(X, n, d_l1.get(), j.work, j.rcond);
+    SBX_LAUNCHED();
+  }
+}
+}  // namespace
+
+void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
+  if (all.empty()) return;
+  // large blocks (few per batch) go through the blocked multi-kernel path
+  std::vector<LuJob> jobs, big;
+  for (const auto& j : all) (j.n >= kLuBlockedMin ? big : jobs).push_back(j);
+  if (big.size() > 16) {
+    jobs = all;
+    big.clear();
+  }
+  for (const auto& j : big) {
+    require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+    require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
+    lu_blocked(j, s);
+  }
   if (jobs.empty()) return;
   static thread_local JobTable<LuJob> tab;
   size_t need = 64 * sizeof(double);

@@ -57,7 +57,7 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
       const int g = cpqr_smem_ctas(pr.M, pr.n);
       if (one_cta) engine = 1;
       else if (g > 0 && g <= sms) engine = 3;
-      else if (i64(pr.M) * pr.n >= kCoopEntries && pr.M <= kCoopMaxRows) engine = 2;
+      else if (i64(pr.M) * pr.n >= kCoopEntries) engine = 2;
       else engine = 1;
     }
     coop_[p] = char(engine);

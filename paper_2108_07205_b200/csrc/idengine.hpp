@@ -37,7 +37,6 @@ class IdBatch {
               const std::vector<int>& ldp, cudaStream_t s);
 
   static constexpr i64 kCoopEntries = i64(1) << 18;  // 2 MB of W^T
-  static constexpr int kCoopMaxRows = 16384;         // Householder vector in smem
 
  private:
   std::vector<char> coop_;

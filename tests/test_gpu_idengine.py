@@ -77,3 +77,17 @@ def test_row_id_edge_cases(sb):  # test_idlib.cpp:63-113
     assert k == 1 and skeleton_identity_exact(k, J, P)
     with pytest.raises(ValueError):
         sb.row_id(np.eye(4), 0.5)
+
+
+@pytest.mark.parametrize("engine", [0, 2])
+def test_row_id_very_tall_functionals(sb, po, engine):
+    # W^T with 20000 functionals: the Householder vector no longer fits shared
+    # memory, the cooperative engine keeps it in L2
+    rng = np.random.default_rng(11)
+    w = spectrum_matrix(180, 20000, 10.0 ** (-14 * np.arange(180) / 180), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=engine)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)

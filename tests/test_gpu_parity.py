@@ -157,3 +157,30 @@ def test_singular_woodbury_is_reported(sb):  # test_els.cpp:293-330
     R = np.stack([-y / (y @ y), 1e-3 * rng.standard_normal(n_ext)], 0)
     with pytest.raises(sb.SingularMatrixError, match="optimal-basis"):
         sb.els_build(h, g, g1, plan, sb.update_from_factors(plan, L, R))
+
+
+def test_cfg1_els_matches_dense_and_field(sb, po):
+    """BASELINE configs[0] at full size: ellipse (2, 1), 128 x 16 nodes, the 4
+    panels nearest (1.99, 0) split m = 8 (A_pp is 1024 x 1024: blocked dense
+    LU), 5 Stokeslets at radius 4; against the dense LU of A_nn (4992
+    unknowns) and the analytic field at interior targets."""
+    from paper_2108_07205_b200.configs import CONFIGS
+    c = CONFIGS["cfg1"]
+    g0 = sb.panelize(sb.ellipse(c.a, c.b), c.n_panels, c.q)
+    panels = c.refine_panels(g0.nodes())
+    assert list(panels) == [0, 1, 126, 127]
+    h = sb.hbs_invert(sb.hbs_compress(g0, opts=sb.HbsOptions(eps=c.eps)))
+    g1, plan = sb.refine(g0, panels, c.m)
+    u = sb.compress_update(g0, g1, plan, c.eps)
+    e = sb.els_build(h, g0, g1, plan, u)
+    src = c.sources()[0]
+    tau = sb.els_solve(e, sb.gather_kept_added(plan, sb.boundary_data(g1, src)))
+    o0 = po.Geom.create(po.ELLIPSE, c.n_panels, scale=c.a, aspect=c.b / c.a)
+    o1, op = o0.refine(panels, c.m)
+    A = po.Assembler.create(o1).full_matrix()
+    ref = po.gather_kept_added(op.maps(), np.linalg.solve(A, o1.boundary_data(src)))
+    assert rel(tau, ref) <= 1e-8
+    tg = c.interior_targets()[:20]
+    vel = o1.evaluate_velocity(po.INTERIOR, sb.density_on_refined(e, tau), tg)
+    ex = po.field_velocity(src, tg)
+    assert np.max(np.linalg.norm(vel - ex, axis=1) / np.linalg.norm(ex, axis=1)) < 1e-8
