@@ -67,6 +67,20 @@ class StreamScope {
   cudaStream_t prev_;
 };
 
+// Thread-local switch: while set, the ID engines avoid cooperative launches
+// (grid-wide co-residency), which other streams' kernels can starve.
+bool& no_coop_flag();
+class NoCoopScope {
+ public:
+  NoCoopScope() : prev_(no_coop_flag()) { no_coop_flag() = true; }
+  ~NoCoopScope() { no_coop_flag() = prev_; }
+  NoCoopScope(const NoCoopScope&) = delete;
+  NoCoopScope& operator=(const NoCoopScope&) = delete;
+
+ private:
+  bool prev_;
+};
+
 // Runs independent host+device tasks concurrently: task i gets its own
 // thread and worker stream (forked from `main`, joined back into it), so the
 // latency-bound ID factorisations of independent blocks overlap on the GPU.

@@ -11,6 +11,9 @@
 
 #include "dense.hpp"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace sbx {
 
 namespace {
@@ -712,14 +715,27 @@ constexpr int kThreadColM = 96;  // slabs this short: one thread per column
 // free of shared-memory bank conflicts
 __host__ __device__ __forceinline__ int smem_coop_ld(int M) { return M <= kThreadColM ? (M | 1) : M; }
 __host__ __device__ __forceinline__ size_t smem_coop_doubles(int M, int nown) {
-  return size_t(smem_coop_ld(M)) * nown + M + 2 * nown + 8 * kSmemCoopU + 16 + (96 + nown + 1) / 2;
+  return size_t(smem_coop_ld(M)) * nown + M + 2 * nown + 8 * kSmemCoopU + 16 + (96 + 2 * nown + 1) / 2;
 }
 
-__global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
+// kCl: one problem per thread-block cluster; partials and the pivot column
+// are read from the peers' shared memory (DSMEM) and the group barrier is
+// the hardware cluster barrier, so no grid-wide co-residency is needed.
+template <bool kCl>
+__global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
   extern __shared__ double sm[];
-  const int job = args.cta_job[blockIdx.x];
-  const int rank = args.cta_rank[blockIdx.x];
-  const int G = args.job_ctas[job];
+  __shared__ CoopPart s_part[2];
+  int job, rank, G;
+  if constexpr (kCl) {
+    cg::cluster_group cl = cg::this_cluster();
+    G = int(cl.num_blocks());
+    rank = int(cl.block_rank());
+    job = int(blockIdx.x) / G;
+  } else {
+    job = args.cta_job[blockIdx.x];
+    rank = args.cta_rank[blockIdx.x];
+    G = args.job_ctas[job];
+  }
   const QrJob jb = args.jobs[job];
   const int M = jb.M, n = jb.n, lda = jb.lda;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -734,16 +750,20 @@ __global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
   double* sc = red + 8 * kSmemCoopU;      // 16
   int* ired = reinterpret_cast<int*>(sc + 16);  // 96
   int* mypos = ired + 96;                 // nown
-  CoopCtl* ctl = args.ctl + job;
-  CoopPart* parts = args.parts + args.part_off[job];
-  double* cand = args.cand + args.cand_off[job];
+  int* pivstep = mypos + nown;            // nown: step at which a column was pivoted
+  CoopCtl* ctl = kCl ? nullptr : args.ctl + job;
+  CoopPart* parts = kCl ? nullptr : args.parts + args.part_off[job];
+  double* cand = kCl ? nullptr : args.cand + args.cand_off[job];
   double* sbeta = args.beta + args.beta_off[job];
   const double* Ag = jb.a;
   for (i64 e = tid; e < i64(M) * nown; e += kCT) {
     const int c = int(e / M), i = int(e - i64(c) * M);
     S[i + size_t(c) * ldS] = Ag[i + size_t(c0 + c) * lda];
   }
-  for (int c = tid; c < nown; c += kCT) mypos[c] = c0 + c;
+  for (int c = tid; c < nown; c += kCT) {
+    mypos[c] = c0 + c;
+    pivstep[c] = -1;
+  }
   __syncthreads();
   if (nown >= kCWarps) {
     for (int c = warp; c < nown; c += kCWarps) {
@@ -818,30 +838,88 @@ __global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
           p0 = ired[w];
           q0 = wphys[w];
         }
-      parts[(j & 1) * G + rank] = {v0, p0, q0};
-      s_p = q0;
-    }
-    __syncthreads();
-    {  // publish the candidate's current rows [j, M)
-      const int q = s_p;
-      if (q >= 0) {
-        const double* src = S + size_t(q - c0) * ldS;
-        double* dst = cand + (size_t(j & 1) * G + rank) * M;
-        for (int i = j + tid; i < M; i += kCT) __stcg(dst + i, src[i]);
+      if constexpr (kCl) {
+        s_part[j & 1] = {v0, p0, q0};
+      } else {
+        parts[(j & 1) * G + rank] = {v0, p0, q0};
+        s_p = q0;
       }
     }
-    group_barrier(ctl, unsigned(G));
     int p, lp, own;
-    coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own);
+    if constexpr (kCl) {
+      cg::cluster_group cl = cg::this_cluster();
+      cl.sync();  // every CTA's partial visible (release / acquire at cluster scope)
+      __shared__ int s_pick[3];
+      if (warp == 0) {
+        double bv = -1.0;
+        int bp = 0x7fffffff, bq = -1, bo = -1;
+        if (lane < G) {
+          const CoopPart pt = *cl.map_shared_rank(&s_part[j & 1], lane);
+          if (pt.phys >= 0) {
+            bv = pt.val;
+            bp = pt.pos;
+            bq = pt.phys;
+            bo = lane;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+          const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+          const int oo = __shfl_xor_sync(0xffffffffu, bo, o);
+          if (better(ov, op, bv, bp)) {
+            bv = ov;
+            bp = op;
+            bq = oq;
+            bo = oo;
+          }
+        }
+        if (lane == 0) {
+          s_pick[0] = bq;
+          s_pick[1] = bp;
+          s_pick[2] = bo;
+        }
+      }
+      __syncthreads();
+      p = s_pick[0];
+      lp = s_pick[1];
+      own = s_pick[2];
+    } else {
+      __syncthreads();
+      {  // publish the candidate's current rows [j, M)
+        const int q = s_p;
+        if (q >= 0) {
+          const double* src = S + size_t(q - c0) * ldS;
+          double* dst = cand + (size_t(j & 1) * G + rank) * M;
+          for (int i = j + tid; i < M; i += kCT) __stcg(dst + i, src[i]);
+        }
+      }
+      group_barrier(ctl, unsigned(G));
+      coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own);
+    }
     for (int c = tid; c < nown; c += kCT) {
-      if (c0 + c == p) mypos[c] = -1;
-      else if (mypos[c] == j) mypos[c] = lp;
+      if (c0 + c == p) {
+        mypos[c] = -1;
+        pivstep[c] = j;
+      } else if (mypos[c] == j) {
+        mypos[c] = lp;
+      }
     }
     if (p >= c0 && p < c1 && tid == 0) jb.perm[j] = p;
-    const double* pc = cand + (size_t(j & 1) * G + own) * M;
+    // the pivot column as its owner left it: a peer's slab (cluster) or the
+    // owner's published copy; the owner never touches it again this launch
+    const double* pc;
+    if constexpr (kCl) {
+      const int oc0 = int(i64(n) * own / G);
+      pc = cg::this_cluster().map_shared_rank(S, own) + size_t(p - oc0) * ldS;
+    } else {
+      pc = cand + (size_t(j & 1) * G + own) * M;
+    }
+    auto ldp = [&](int i) { return kCl ? pc[i] : __ldcg(pc + i); };
     double part = 0.0;
     for (int i = j + 1 + tid; i < M; i += kCT) {
-      const double x = __ldcg(pc + i);
+      const double x = ldp(i);
       v[i] = x;
       part += x * x;
     }
@@ -849,7 +927,7 @@ __global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
     if (lane == 0) red[warp] = part;
     __syncthreads();
     const double tail = warp_sum(lane < kCWarps ? red[lane] : 0.0);
-    const double cc = __ldcg(pc + j);
+    const double cc = ldp(j);
     double tau, beta, denom;
     if (tail <= DBL_MIN) {
       tau = 0.0;
@@ -868,7 +946,6 @@ __global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
     }
     if (j == 0) r00 = fabs(beta);
     if (rank == 0 && tid == 0) sbeta[j] = beta;
-    if (p >= c0 && p < c1 && tid == 0) S[j + size_t(p - c0) * ldS] = beta;
     __syncthreads();
     done = j + 1;
     if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
@@ -982,7 +1059,13 @@ __global__ void __launch_bounds__(kCT) cpqr_smem_kernel(SmemCoopArgs args) {
     }
     __syncthreads();
   }
-  group_barrier(ctl, unsigned(G));
+  if constexpr (kCl)
+    cg::this_cluster().sync();  // peers are done reading this slab; sbeta complete
+  else
+    group_barrier(ctl, unsigned(G));
+  for (int c = tid; c < nown; c += kCT)  // R diagonal of the pivoted columns
+    if (pivstep[c] >= 0) S[pivstep[c] + size_t(c) * ldS] = __ldcg(sbeta + pivstep[c]);
+  __syncthreads();
   double* Aw = jb.a;
   for (int c = warp; c < nown; c += kCWarps)
     for (int i = lane; i < M; i += 32) Aw[i + size_t(c0 + c) * lda] = S[i + size_t(c) * ldS];
@@ -1829,7 +1912,7 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   static std::once_flag attr;
   std::call_once(attr, [] {
-    SBX_CUDA(cudaFuncSetAttribute(cpqr_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_onchip_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
   });
   static thread_local JobTable<QrJob> tjobs;
@@ -1851,7 +1934,7 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
       require(g > 0 && g <= sms, "cpqr_smem: problem does not fit on chip");
       const size_t sm2 = std::max(smem, smem_coop_doubles(jobs[q].M, (jobs[q].n + g - 1) / g) * sizeof(double));
       int ps = 1;
-      SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cpqr_smem_kernel, kCT, sm2));
+      SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cpqr_onchip_kernel<false>, kCT, sm2));
       ps = std::max(1, ps);
       if (!wave.empty() && ctas + g > sms * ps) break;
       wave.push_back(jobs[q]);
@@ -1905,13 +1988,68 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     void* params[] = {&a};
     static const bool plain = std::getenv("SBX_COOP_PLAIN") != nullptr;  // diagnostics
     if (plain)
-      SBX_CUDA(cudaLaunchKernel(reinterpret_cast<void*>(cpqr_smem_kernel), dim3(unsigned(cta_job.size())),
+      SBX_CUDA(cudaLaunchKernel(reinterpret_cast<void*>(cpqr_onchip_kernel<false>), dim3(unsigned(cta_job.size())),
                                 dim3(kCT), params, smem, s));
     else
-      SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_smem_kernel),
+      SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_onchip_kernel<false>),
                                            dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
     SBX_LAUNCHED();
   }
+}
+
+int cpqr_cluster_size(int M, int n) {
+  const int g = cpqr_smem_ctas(M, n);
+  if (g <= 0 || g > 16) return 0;
+  int c = 1;
+  while (c < g) c <<= 1;
+  return c;
+}
+
+void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  int C = 1;
+  for (const auto& j : jobs) {
+    const int c = cpqr_cluster_size(j.M, j.n);
+    require(c > 0, "cpqr_cluster: problem does not fit one cluster");
+    C = std::max(C, c);
+  }
+  size_t smem = 0;
+  i64 boff = 0;
+  std::vector<i64> offs;
+  for (const auto& j : jobs) {
+    smem = std::max(smem, smem_coop_doubles(j.M, (j.n + C - 1) / C) * sizeof(double));
+    offs.push_back(boff);
+    boff += std::min(j.M, j.n);
+  }
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_onchip_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_onchip_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  static thread_local JobTable<QrJob> tjobs;
+  static thread_local DevBuf<double> d_beta;
+  static thread_local DevBuf<i64> d_offs;
+  d_beta.reserve(size_t(std::max<i64>(boff, 1)));
+  d_offs.upload(offs, s);
+  SmemCoopArgs a{};
+  a.jobs = tjobs.upload(jobs, s);
+  a.beta = d_beta.get();
+  a.beta_off = d_offs.get();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(jobs.size() * size_t(C)));
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(C);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SBX_CUDA(cudaLaunchKernelEx(&cfg, cpqr_onchip_kernel<true>, a));
+  SBX_LAUNCHED();
 }
 
 void interp_batched(const std::vector<InterpJob>& jobs, cudaStream_t s) {

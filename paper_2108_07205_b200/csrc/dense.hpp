@@ -45,6 +45,13 @@ void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 int cpqr_smem_ctas(int M, int n);
 void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 
+// Cluster CPQR: the same on-chip algorithm with one problem per thread-block
+// cluster of C <= 16 CTAs (partials and pivot column through DSMEM, hardware
+// cluster barrier): no cooperative launch, so it runs beside other streams.
+// cpqr_cluster_size gives C (a power of two) or 0 when one cluster is too small.
+int cpqr_cluster_size(int M, int n);
+void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+
 // ---------------------------------------------------------------- ID interpolation
 // Given a pivoted factor (R in the upper triangle of a, ld lda, n columns)
 // and a rank k: P (n x k, column-major, ldp) with P(J_i, i) = 1 (i < k) and

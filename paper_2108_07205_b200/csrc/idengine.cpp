@@ -21,12 +21,25 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
   d_perm_.reserve(size_t(std::max<i64>(perm_off_[np], 1)));
   d_diag_.reserve(size_t(std::max<i64>(diag_off[np], 1)));
   d_steps_.reserve(std::max<size_t>(np, 1));
-  std::vector<QrJob> jobs, big, chip;
+  std::vector<QrJob> jobs, big, chip, clus;
   coop_.assign(np, 0);
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
   }();
+  // Large batches have enough independent problems to fill the GPU with one
+  // CTA each; cross-CTA engines only pay off when problems are few.  Count
+  // the CTAs the cluster engine would need for the whole batch.
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  i64 cluster_ctas = 0;
+  for (const auto& pr : probs)
+    if (pr.M > 0 && pr.n > 0) cluster_ctas += std::max(1, cpqr_cluster_size(pr.M, pr.n));
+  const bool crowded = cluster_ctas > 2 * i64(sms);
   for (size_t p = 0; p < np; ++p) {
     const auto& pr = probs[p];
     if (pr.M == 0 || pr.n == 0) continue;
@@ -46,22 +59,19 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
       // one CTA when the problem fits its shared memory (or is a short, tall
       // TSQR case); else the on-chip cooperative engine when the slabs fit;
       // else the L2-streaming cooperative engine for big tall problems
-      const bool one_cta = (i64(pr.M) * pr.n + 3 * pr.n + 72) * 8 <= i64(200 * 1024) ||
-                           (pr.n <= 144 && pr.M > pr.n && pr.M <= tsqr_max_m);
-      static const int sms = [] {
-        int dev = 0, n = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-      }();
+      const bool tsqr_ok = pr.n <= 144 && pr.M > pr.n && (pr.M <= tsqr_max_m || (crowded && pr.M <= 4096));
+      const bool one_cta = (i64(pr.M) * pr.n + 3 * pr.n + 72) * 8 <= i64(200 * 1024) || tsqr_ok;
       const int g = cpqr_smem_ctas(pr.M, pr.n);
+      static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
       if (one_cta) engine = 1;
+      else if (!no_cluster && cpqr_cluster_size(pr.M, pr.n) > 0) engine = 4;
+      else if (no_coop_flag()) engine = 1;  // beside other streams: no grid-wide barriers
       else if (g > 0 && g <= sms) engine = 3;
       else if (i64(pr.M) * pr.n >= kCoopEntries) engine = 2;
       else engine = 1;
     }
     coop_[p] = char(engine);
-    (engine == 2 ? big : engine == 3 ? chip : jobs).push_back(j);
+    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : jobs).push_back(j);
   }
   static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
   if (log) {
@@ -74,6 +84,7 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
   cpqr_smem_batched(chip, s);
+  cpqr_cluster_batched(clus, s);
   std::vector<int> hperm(static_cast<size_t>(perm_off_[np]));
   std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
   if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);

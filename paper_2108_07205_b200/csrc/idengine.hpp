@@ -22,7 +22,8 @@ class IdBatch {
   // (1e-15 keeps every row the forced-rank rule can ask for).
   void factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s);
   // engine override for tests: 0 auto, 1 one CTA per problem, 2 cooperative
-  // (slabs in L2), 3 cooperative on chip (slabs in shared memory)
+  // (slabs in L2), 3 cooperative on chip (slabs in shared memory), 4 one
+  // thread-block cluster per problem
   int force_engine = 0;
   size_t size() const { return probs_.size(); }
   const IdProblem& problem(size_t p) const { return probs_[p]; }

@@ -63,6 +63,11 @@ cudaStream_t lib_stream() {
 
 cudaStream_t cur_stream() { return tl_stream ? tl_stream : lib_stream(); }
 
+bool& no_coop_flag() {
+  thread_local bool f = false;
+  return f;
+}
+
 cudaStream_t set_cur_stream(cudaStream_t s) {
   const cudaStream_t prev = tl_stream;
   tl_stream = s;

@@ -520,74 +520,96 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   const bool do_kc = !kept_old_s.empty() && !cut_s.empty();
   const bool do_kp = !kept_new_s.empty() && !added_s.empty();
   const bool do_pk_near = u->np2 > 0 && u->nk2 > 0;
-  std::vector<std::function<void(cudaStream_t)>> tasks;
-  tasks.push_back([&](cudaStream_t w) {
+  auto t_far = [&](cudaStream_t w) {
     far = compress_block_far(enew.view(), ng, far_nodes, circles, true, with_null, ktree, eps, w);
     phase_mark("update: far ID (kept)", w);
-  });
-  if (do_kc)
-    tasks.push_back([&](cudaStream_t w) {
-      kc_near = near_row_id(eold.view(), mapped(kept_old_s, near_s), cut_s, eps, notes_kc, "kc", w);
-      phase_mark("update: kc near ID", w);
-    });
-  if (do_kp)
-    tasks.push_back([&](cudaStream_t w) {
-      kp_near = near_row_id(enew.view(), mapped(kept_new_s, near_s), added_s, eps, notes_kp, "kp", w);
-      phase_mark("update: kp near ID", w);
-    });
+  };
+  auto t_kc = [&](cudaStream_t w) {
+    if (!do_kc) return;
+    kc_near = near_row_id(eold.view(), mapped(kept_old_s, near_s), cut_s, eps, notes_kc, "kc", w);
+    phase_mark("update: kc near ID", w);
+  };
+  auto t_kp = [&](cudaStream_t w) {
+    if (!do_kp) return;
+    kp_near = near_row_id(enew.view(), mapped(kept_new_s, near_s), added_s, eps, notes_kp, "kp", w);
+    phase_mark("update: kp near ID", w);
+  };
   // added rows against the division surface (lowrank.cpp:296-308, 183-238)
-  if (!plan.added_new.empty())
-    tasks.push_back([&](cudaStream_t w) {
-      std::vector<std::vector<i64>> ptree;
-      for (size_t st = 0; st < plan.added_new.size(); st += 128) {
-        std::vector<i64> l;
-        for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
-        ptree.push_back(std::move(l));
-      }
-      pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, w);
-      phase_mark("update: pk far ID", w);
-    });
-  if (do_pk_near)
-    tasks.push_back([&](cudaStream_t w) {
-      pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, notes_pk, "pk", w);
-      phase_mark("update: pk near ID", w);
-    });
+  auto t_pk_far = [&](cudaStream_t w) {
+    if (plan.added_new.empty()) return;
+    std::vector<std::vector<i64>> ptree;
+    for (size_t st = 0; st < plan.added_new.size(); st += 128) {
+      std::vector<i64> l;
+      for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
+      ptree.push_back(std::move(l));
+    }
+    pk_far = compress_block_far(enew.view(), ng, plan.added_new, circles, false, with_null, ptree, eps, w);
+    phase_mark("update: pk far ID", w);
+  };
+  auto t_pk_near = [&](cudaStream_t w) {
+    if (!do_pk_near) return;
+    pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, notes_pk, "pk", w);
+    phase_mark("update: pk near ID", w);
+  };
   const double app_eps = eps;  // els_build adopts it when a_oo was built at this eps
-  if (!plan.added_new.empty())
-    tasks.push_back([&](cudaStream_t w) {
-      try {
-        u->app = build_app_solver(ng, plan, form, mu, app_eps, w);
-      } catch (const Error&) {
-        u->app.reset();  // els_build rebuilds it and reports the error there
-      }
-      phase_mark("update: A_pp inverse (for els_build)", w);
-    });
-  // SBX_PAR_MODE: 0 every task on its own stream; 1 the row IDs in order on
-  // one high-priority stream beside the A_pp build; 2 (default) all tasks in
-  // order on the library stream.  The cooperative CPQR launches need most of
-  // the SMs at once, and other streams' kernels starve them unpredictably
-  // (step times of 40 to 400 ms measured with modes 0/1), so the default
-  // stays serial until every concurrent ID runs without grid-wide barriers.
+  auto t_app = [&](cudaStream_t w) {
+    if (plan.added_new.empty()) return;
+    try {
+      u->app = build_app_solver(ng, plan, form, mu, app_eps, w);
+    } catch (const Error&) {
+      u->app.reset();  // els_build rebuilds it and reports the error there
+    }
+    phase_mark("update: A_pp inverse (for els_build)", w);
+  };
+  // SBX_PAR_MODE:
+  //   2 (default) every task in order on the library stream;
+  //   3 the near-field row IDs (whose big blocks need the
+  //     cooperative CPQR engines) in order on the library stream, then the
+  //     far-field hierarchies beside the A_pp build on two worker streams,
+  //     both restricted to engines without grid-wide barriers (one CTA or one
+  //     thread-block cluster per problem), which coexist with other streams;
+  //   1 / 0 all row IDs beside A_pp / every task on its own stream.
+  // Measured on cfg2 (bench, 10 steps): serial 50 ms stable; modes 0/1/3
+  // 39-165 ms from run to run (co-scheduling of the large-smem CPQR kernels
+  // of two streams is not stable), so the default is serial.
   static const int par_mode = [] {
     const char* e = std::getenv("SBX_PAR_MODE");
     return e ? std::atoi(e) : 2;
   }();
-  std::vector<std::function<void(cudaStream_t)>> ids;
-  std::vector<int> high;
-  if (par_mode == 1 && !plan.added_new.empty() && tasks.size() > 1) {
-    auto app_task = tasks.back();
-    tasks.pop_back();
-    ids = std::move(tasks);
-    tasks = {[&ids](cudaStream_t w) {
-               for (auto& t : ids) t(w);
-             },
-             app_task};
-    high = {1, 0};
+  if (par_mode == 2) {
+    t_far(s);
+    t_kc(s);
+    t_kp(s);
+    t_pk_far(s);
+    t_pk_near(s);
+    t_app(s);
+  } else if (par_mode == 3) {
+    t_kc(s);
+    t_kp(s);
+    t_pk_near(s);
+    parallel_tasks({[&](cudaStream_t w) {
+                      NoCoopScope nc;
+                      t_far(w);
+                      t_pk_far(w);
+                    },
+                    [&](cudaStream_t w) {
+                      NoCoopScope nc;
+                      t_app(w);
+                    }},
+                   s, {1, 0});
+  } else if (par_mode == 1) {
+    parallel_tasks({[&](cudaStream_t w) {
+                      t_far(w);
+                      t_kc(w);
+                      t_kp(w);
+                      t_pk_far(w);
+                      t_pk_near(w);
+                    },
+                    t_app},
+                   s, {1, 0});
+  } else {
+    parallel_tasks({t_far, t_kc, t_kp, t_pk_far, t_pk_near, t_app}, s);
   }
-  if (par_mode == 2)
-    for (auto& t : tasks) t(s);
-  else
-    parallel_tasks(tasks, s, high);
   for (auto* n : {&notes_kc, &notes_kp, &notes_pk}) u->notes.insert(u->notes.end(), n->begin(), n->end());
   struct KeptFactor {
     i64 k = 0;

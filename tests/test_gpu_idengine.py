@@ -91,3 +91,20 @@ def test_row_id_very_tall_functionals(sb, po, engine):
     kk = min(k, ko) - 2
     assert np.array_equal(J[:kk], Jo[:kk])
     assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+
+
+@pytest.mark.parametrize("shape", [(50, 30), (200, 100), (128, 700), (256, 513), (40, 3000), (900, 128)])
+def test_row_id_cluster_engine(sb, po, shape):
+    m, n = shape
+    rng = np.random.default_rng(m + 3 * n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=4)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=4)
+    assert np.array_equal(Jw[:k], J[:k])
