@@ -110,6 +110,14 @@ int sbx_plan_maps(sbx_plan p, int64_t* kept_old, int64_t* kept_new, int64_t* cut
  * boundary_data (nystrom.hpp:116-117). Host in/out buffers. */
 int sbx_submatrix(sbx_geom g, int formulation, double mu, const int64_t* rows, int64_t nr,
                   const int64_t* cols, int64_t nc, double* out);
+/* evaluate_solution (nystrom.hpp:137-139, nystrom.cpp:408-448): velocity at
+ * n_targets points (x, y interleaved) from nrhs densities (2N x nrhs,
+ * column-major, ld ldt); velocity: 2 x n_targets per density (stacked);
+ * pressure (optional, with_pressure): n_targets per density; near_boundary
+ * (optional): 1 where the closest node lies within its panel's length. */
+int sbx_evaluate_solution(sbx_geom g, int formulation, double mu, const double* tau, int64_t ldt,
+                          int64_t nrhs, const double* targets, int64_t n_targets, int with_pressure,
+                          double* velocity, double* pressure, uint8_t* near_boundary);
 int sbx_boundary_data(sbx_geom g, int64_t n_src, const double* src_xyf, double mu,
                       double* out);
 

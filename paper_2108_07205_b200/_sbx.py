@@ -82,6 +82,8 @@ _SIGS = [
     ("sbx_plan_maps", C.c_int, [VP, I64P, I64P, I64P, I64P]),
     ("sbx_submatrix", C.c_int, [VP, C.c_int, C.c_double, I64P, I64, I64P, I64, F64P]),
     ("sbx_boundary_data", C.c_int, [VP, I64, F64P, C.c_double, F64P]),
+    ("sbx_evaluate_solution", C.c_int,
+     [VP, C.c_int, C.c_double, F64P, I64, I64, F64P, I64, C.c_int, F64P, F64P, C.POINTER(C.c_uint8)]),
     ("sbx_hbs_compress", C.c_int, [VP, C.c_int, C.c_double, C.POINTER(sbx_hbs_options), C.POINTER(VP)]),
     ("sbx_hbs_compress_subset", C.c_int,
      [VP, C.c_int, C.c_double, I64P, I64, C.POINTER(sbx_hbs_options), C.POINTER(VP)]),

@@ -209,6 +209,28 @@ def add_holes(d: Discretization, holes):
     return Discretization(g), RefinementPlan(p)
 
 
+def evaluate_solution(d: Discretization, formulation, tau, targets, mu: float = 1.0, with_pressure=False):
+    """nystrom.cpp:408-448 on the device.  tau: 2N (or 2N x nrhs) density;
+    returns velocity (T x 2 [x nrhs]), pressure (T [x nrhs]) or None, and the
+    near-boundary flags (T)."""
+    t = np.asfortranarray(np.asarray(tau, dtype=np.float64))
+    vec = t.ndim == 1
+    t2 = t.reshape(-1, 1, order="F") if vec else t
+    tg = np.ascontiguousarray(np.asarray(targets, dtype=np.float64).reshape(-1, 2))
+    nt, nr = len(tg), t2.shape[1]
+    vel = np.zeros((nr, nt, 2))
+    pre = np.zeros((nr, nt)) if with_pressure else None
+    near = np.zeros(nt, dtype=np.uint8)
+    check(lib().sbx_evaluate_solution(d.ptr, formulation, mu, t2.ctypes.data_as(F64P), t2.shape[0], nr,
+                                      tg.ctypes.data_as(F64P), nt, int(with_pressure),
+                                      vel.ctypes.data_as(F64P),
+                                      pre.ctypes.data_as(F64P) if with_pressure else None,
+                                      near.ctypes.data_as(C.POINTER(C.c_uint8))))
+    v = vel[0] if vec else np.moveaxis(vel, 0, -1)
+    p = (pre[0] if vec else pre.T) if with_pressure else None
+    return v, p, near.astype(bool)
+
+
 def boundary_data(d: Discretization, sources, mu: float = 1.0) -> np.ndarray:
     """nystrom.cpp:383-392; sources rows (x, y, fx, fy)."""
     s = np.ascontiguousarray(np.asarray(sources, dtype=np.float64).reshape(-1, 4))

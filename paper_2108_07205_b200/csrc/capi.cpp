@@ -233,6 +233,15 @@ int sbx_boundary_data(sbx_geom g, int64_t n_src, const double* src_xyf, double m
   return guard([&] { sbx::boundary_data_host(G(g), n_src, src_xyf, mu, out, sbx::lib_stream()); });
 }
 
+int sbx_evaluate_solution(sbx_geom g, int formulation, double mu, const double* tau, int64_t ldt, int64_t nrhs,
+                          const double* targets, int64_t n_targets, int with_pressure, double* velocity,
+                          double* pressure, uint8_t* near_boundary) {
+  return guard([&] {
+    sbx::evaluate_solution_host(G(g), formulation, mu, tau, ldt, nrhs, targets, n_targets, with_pressure != 0,
+                                velocity, pressure, near_boundary, sbx::lib_stream());
+  });
+}
+
 // ---------------------------------------------------------------- HBS
 int sbx_hbs_compress(sbx_geom g, int formulation, double mu, const sbx_hbs_options* opts,
                      sbx_hbs* out) {

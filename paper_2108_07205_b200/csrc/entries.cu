@@ -256,6 +256,124 @@ __global__ void boundary_data_kernel(const double* __restrict__ x, const double*
   }
 }
 
+
+// evaluate_solution (nystrom.cpp:408-448): velocity (and pressure) at
+// targets from nrhs densities; one CTA per (target, block of up to 8
+// densities), nodes strided over the threads, kernel matrices formed once
+// per node and applied to every density; block reduction at the end.  Also
+// the closest node (first minimum) for the near-boundary flag.
+constexpr int kEvalR = 8;
+
+__global__ void __launch_bounds__(256) evaluate_kernel(EntryView v, i64 n, const double* __restrict__ tau, i64 ldt,
+                                                       int nrhs, const double* __restrict__ tgt, int with_p,
+                                                       double* __restrict__ vel, double* __restrict__ pre,
+                                                       double* __restrict__ cdist, i64* __restrict__ cnode) {
+  const int t = blockIdx.x;
+  const int r0 = blockIdx.y * kEvalR;
+  const int nr = min(kEvalR, nrhs - r0);
+  const double px = tgt[2 * t], py = tgt[2 * t + 1];
+  double u0[kEvalR], u1[kEvalR], pp[kEvalR];
+#pragma unroll
+  for (int q = 0; q < kEvalR; ++q) u0[q] = u1[q] = pp[q] = 0.0;
+  double best = INFINITY;
+  i64 bestj = 0x7fffffffffffffffLL;
+  const double c4 = 1.0 / (4.0 * kPi * v.mu);
+  for (i64 j = threadIdx.x; j < n; j += blockDim.x) {
+    const double rx = px - v.x[j], ry = py - v.y[j];
+    const double r2 = rx * rx + ry * ry;
+    const double dist = sqrt(r2);
+    if (dist < best) {
+      best = dist;
+      bestj = j;
+    }
+    const double wj = v.w[j], nx = v.nx[j], ny = v.ny[j];
+    const double dn = (rx * nx + ry * ny) / (kPi * r2 * r2);
+    double k00 = rx * rx * dn, k01 = rx * ry * dn, k11 = ry * ry * dn;
+    const bool sl = single_layer(v, v.comp[j]);
+    double s00 = 0, s01 = 0, s11 = 0;
+    if (sl) {
+      const double lg = -0.5 * log(r2) * c4, sc = c4 / r2;
+      s00 = rx * rx * sc + lg;
+      s01 = rx * ry * sc;
+      s11 = ry * ry * sc + lg;
+    }
+    double pd0 = 0, pd1 = 0, ps0 = 0, ps1 = 0;
+    if (with_p) {
+      const double rn = rx * nx + ry * ny;
+      pd0 = (v.mu / kPi) * (-nx / r2 + rx * (2.0 * rn / (r2 * r2)));
+      pd1 = (v.mu / kPi) * (-ny / r2 + ry * (2.0 * rn / (r2 * r2)));
+      if (sl) {
+        ps0 = rx / (2.0 * kPi * r2);
+        ps1 = ry / (2.0 * kPi * r2);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kEvalR; ++q) {
+      if (q >= nr) break;
+      const double t0 = tau[2 * j + size_t(r0 + q) * ldt], t1 = tau[2 * j + 1 + size_t(r0 + q) * ldt];
+      u0[q] += wj * (k00 * t0 + k01 * t1) + (sl ? wj * (s00 * t0 + s01 * t1) : 0.0);
+      u1[q] += wj * (k01 * t0 + k11 * t1) + (sl ? wj * (s01 * t0 + s11 * t1) : 0.0);
+      if (with_p) pp[q] += wj * (pd0 * t0 + pd1 * t1) + (sl ? wj * (ps0 * t0 + ps1 * t1) : 0.0);
+    }
+  }
+  __shared__ double red[3 * kEvalR][8];
+  __shared__ double rb[8];
+  __shared__ long long rj[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < kEvalR; ++q) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      u0[q] += __shfl_xor_sync(0xffffffffu, u0[q], o);
+      u1[q] += __shfl_xor_sync(0xffffffffu, u1[q], o);
+      pp[q] += __shfl_xor_sync(0xffffffffu, pp[q], o);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long oj = __shfl_xor_sync(0xffffffffu, (long long)bestj, o);
+    if (ob < best || (ob == best && oj < bestj)) {
+      best = ob;
+      bestj = oj;
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kEvalR; ++q) {
+      red[q][warp] = u0[q];
+      red[kEvalR + q][warp] = u1[q];
+      red[2 * kEvalR + q][warp] = pp[q];
+    }
+    rb[warp] = best;
+    rj[warp] = bestj;
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    const int q = threadIdx.x;
+    double a = 0, b = 0, c = 0;
+    for (int w = 0; w < 8; ++w) {
+      a += red[q][w];
+      b += red[kEvalR + q][w];
+      c += red[2 * kEvalR + q][w];
+    }
+    vel[2 * (size_t(r0 + q) * gridDim.x + t)] = a;
+    vel[2 * (size_t(r0 + q) * gridDim.x + t) + 1] = b;
+    if (with_p) pre[size_t(r0 + q) * gridDim.x + t] = c;
+  }
+  if (threadIdx.x == 0 && blockIdx.y == 0) {
+    double bb = rb[0];
+    long long bj = rj[0];
+    for (int w = 1; w < 8; ++w)
+      if (rb[w] < bb || (rb[w] == bb && rj[w] < bj)) {
+        bb = rb[w];
+        bj = rj[w];
+      }
+    cdist[t] = bb;
+    cnode[t] = bj;
+  }
+}
+
 unsigned grid_x(i64 total, unsigned cap = 4096) {
   return unsigned(std::max<i64>(1, std::min<i64>((total + 255) / 256, cap)));
 }
@@ -329,6 +447,36 @@ void boundary_data_host(const Geom& g, i64 n_src, const double* src_xyf, double 
   SBX_LAUNCHED();
   dout.download(out, size_t(2 * n), s);
   SBX_CUDA(cudaStreamSynchronize(s));
+}
+
+
+void evaluate_solution_host(const Geom& g, int formulation, double mu, const double* tau, i64 ldt, i64 nrhs,
+                            const double* targets, i64 n_targets, bool with_pressure, double* velocity,
+                            double* pressure, unsigned char* near, cudaStream_t s) {
+  require(ldt >= 2 * g.n_nodes(), "evaluate_solution: density size mismatch");
+  if (n_targets == 0 || nrhs == 0) return;
+  EntryOracle eo(g, formulation, mu, s);
+  const i64 n = g.n_nodes();
+  DevBuf<double> dt, dg, dv(static_cast<size_t>(2 * n_targets * nrhs)),
+      dp(static_cast<size_t>(std::max<i64>(1, n_targets * nrhs))), dd(static_cast<size_t>(n_targets));
+  DevBuf<i64> dj(static_cast<size_t>(n_targets));
+  dt.resize(size_t(ldt * nrhs));
+  SBX_CUDA(cudaMemcpyAsync(dt.get(), tau, size_t(ldt * nrhs) * 8, cudaMemcpyHostToDevice, s));
+  dg.upload(targets, size_t(2 * n_targets), s);
+  dim3 grid(unsigned(n_targets), unsigned((nrhs + kEvalR - 1) / kEvalR));
+  evaluate_kernel<<<grid, 256, 0, s>>>(eo.view(), n, dt.get(), ldt, int(nrhs), dg.get(), with_pressure ? 1 : 0,
+                                       dv.get(), dp.get(), dd.get(), dj.get());
+  SBX_LAUNCHED();
+  dv.download(velocity, size_t(2 * n_targets * nrhs), s);
+  if (with_pressure && pressure) dp.download(pressure, size_t(n_targets * nrhs), s);
+  std::vector<double> cd(static_cast<size_t>(n_targets));
+  std::vector<i64> cj(static_cast<size_t>(n_targets));
+  dd.download(cd.data(), cd.size(), s);
+  dj.download(cj.data(), cj.size(), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  if (near)  // within one local panel length of the curve (nystrom.cpp:444-445)
+    for (i64 t = 0; t < n_targets; ++t)
+      near[t] = cd[size_t(t)] < g.panel_arclength(g.panel_of[size_t(cj[size_t(t)])]) ? 1 : 0;
 }
 
 void launch_block_jobs(const EntryView& v, const BlockJob* d_jobs, int n_jobs, i64 max_entries,

@@ -42,6 +42,12 @@ class EntryOracle {
   int form_;
 };
 
+// evaluate_solution (nystrom.cpp:408-448) on the device: velocity (2 x T per
+// density, densities stacked), optional pressure (T per density) and the
+// near-boundary flag, host buffers.
+void evaluate_solution_host(const Geom& g, int formulation, double mu, const double* tau, i64 ldt, i64 nrhs,
+                            const double* targets, i64 n_targets, bool with_pressure, double* velocity,
+                            double* pressure, unsigned char* near, cudaStream_t s);
 void boundary_data_host(const Geom& g, i64 n_src, const double* src_xyf, double mu, double* out,
                         cudaStream_t s);
 

@@ -90,3 +90,17 @@ def test_holes_els_matches_dense_and_field(sb, po):  # test_els.cpp:168-197
     oe = po.Els.build(po.Hbs.compress(a0, eps).invert(), a0, a1, oplan, po.Update.compress(a0, a1, oplan, eps))
     ot = oe.solve(po.gather_kept_added(maps, o1.boundary_data(srcs)))
     assert np.linalg.norm(tau - ot) / np.linalg.norm(ot) <= 1e-9
+
+
+def test_evaluate_solution_matches_oracle(sb, po):  # nystrom.cpp:408-448
+    g0, g1, plan = holes_dev(sb)
+    o0, o1, oplan = holes_oracle(po)
+    n = 2 * o1.n_nodes
+    tau = np.random.default_rng(4).standard_normal((n, 3))
+    tg = np.array(HOLE_TARGETS + [(1.95, 0.0), (-0.8, 0.32)])  # two near the wall / a hole
+    vel, pre, near = sb.evaluate_solution(g1, sb.MIXED, tau, tg, with_pressure=True)
+    for r in range(3):
+        ref = o1.evaluate_velocity(po.MIXED, tau[:, r], tg)
+        assert np.max(np.abs(vel[:, :, r] - ref)) <= 1e-12 * np.max(np.abs(ref))
+    assert list(near) == [False, False, False, True, True]
+    assert np.all(np.isfinite(pre))
