@@ -33,7 +33,7 @@ extern "C" {
 enum {
   SBX_OK = 0,
   SBX_INVALID_ARGUMENT = 1,   /* std::invalid_argument from require()        */
-  SBX_NONCONVERGENCE = 2,     /* ConvergenceError (reserved)                  */
+  SBX_NONCONVERGENCE = 2,     /* ConvergenceError (GMRES)                     */
   SBX_GEOMETRY_ERROR = 3,     /* GeometryError                                */
   SBX_SINGULAR_MATRIX = 4,    /* SingularMatrixError{where}                   */
   SBX_PROXY_VIOLATION = 5,    /* ProxyViolationError                          */
@@ -188,6 +188,19 @@ int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, doubl
 /* g_ext: n_ext x nrhs (kept, cut, added). */
 int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
                       int64_t ldy, int flags, void* stream);
+/* els_apply_forward (els.cpp:181-186): out = (Atilde + L R) v on the extended
+ * system (host buffers, n_ext x nrhs, column-major). */
+int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out,
+                          int64_t ldo);
+/* GMRES / PGMRES-Local (gmres.cpp:14-126 driven as scenario.cpp:694-727):
+ * solves the refined system on the (kept, added) unknowns with operator
+ * els_apply_forward (els.cpp:181-186) and, when precond != 0, the left
+ * preconditioner els_solve.  Host g_n in (n_k + n_p), tau_n out; n_iter and
+ * up to history_cap relative residuals (starting at 1).  Returns
+ * SBX_NONCONVERGENCE (tau_n = last iterate) on stagnation or budget. */
+int sbx_els_gmres(sbx_els e, const double* g_n, double* tau_n, int precond, double tol,
+                  int64_t max_iter, int64_t restart, int64_t* n_iter, double* history,
+                  int64_t history_cap);
 int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out);
 /* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
 int sbx_els_xw(sbx_els e, double* X, double* W);

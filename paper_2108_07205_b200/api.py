@@ -477,6 +477,31 @@ def els_solve_raw(s: ElsSolver, g_ext):
     return _els_call(lib().sbx_els_solve_raw, s, g_ext, s.n_ext())
 
 
+def els_apply_forward(s: ElsSolver, v) -> np.ndarray:
+    """els.cpp:181-186: (Atilde + L R) v on the extended system (n_ext [x nrhs])."""
+    a = np.asfortranarray(np.asarray(v, dtype=np.float64))
+    vec = a.ndim == 1
+    a2 = a.reshape(-1, 1, order="F") if vec else a
+    out = np.zeros_like(a2, order="F")
+    check(lib().sbx_els_apply_forward(s.ptr, a2.ctypes.data_as(F64P), a2.shape[0], a2.shape[1],
+                                      out.ctypes.data_as(F64P), a2.shape[0]))
+    return out[:, 0] if vec else out
+
+
+def els_gmres(s: ElsSolver, g_n, precond: bool = True, tol: float = 1e-11, max_iter: int = 600,
+              restart: int = 0):
+    """GMRES (gmres.cpp:14-126) on the refined system in (kept, added)
+    unknowns; precond=True is the paper's PGMRES-Local (left preconditioner
+    els_solve, scenario.cpp:694-727).  Returns (tau_n, n_iter, history)."""
+    g = np.ascontiguousarray(np.asarray(g_n, dtype=np.float64))
+    tau = np.zeros_like(g)
+    it = C.c_int64()
+    hist = np.zeros(max_iter + 2)
+    check(lib().sbx_els_gmres(s.ptr, g.ctypes.data_as(F64P), tau.ctypes.data_as(F64P), int(precond), tol,
+                              max_iter, restart, C.byref(it), hist.ctypes.data_as(F64P), len(hist)))
+    return tau, it.value, hist[: it.value + 1]
+
+
 def density_on_refined(s: ElsSolver, tau_n) -> np.ndarray:
     """els.cpp:195-203."""
     t = np.ascontiguousarray(np.asarray(tau_n, dtype=np.float64))

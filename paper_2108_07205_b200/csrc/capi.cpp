@@ -428,6 +428,36 @@ int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, doubl
   });
 }
 
+int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::Els& E = *e->e;
+    const int64_t n = E.n_ext();
+    sbx::require(ldv >= n && ldo >= n, "els_apply_forward: size mismatch");
+    cudaStream_t s = sbx::lib_stream();
+    sbx::DevBuf<double> dv(static_cast<size_t>(n * nrhs)), dout(static_cast<size_t>(n * nrhs));
+    SBX_CUDA(cudaMemcpy2DAsync(dv.get(), size_t(n) * 8, v, size_t(ldv) * 8, size_t(n) * 8, size_t(nrhs),
+                               cudaMemcpyHostToDevice, s));
+    sbx::els_apply_forward_device(E, dv.get(), dout.get(), nrhs, s);
+    SBX_CUDA(cudaMemcpy2DAsync(out, size_t(ldo) * 8, dout.get(), size_t(n) * 8, size_t(n) * 8, size_t(nrhs),
+                               cudaMemcpyDeviceToHost, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sbx_els_gmres(sbx_els e, const double* g_n, double* tau_n, int precond, double tol, int64_t max_iter,
+                  int64_t restart, int64_t* n_iter, double* history, int64_t history_cap) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::GmresOutcome r = sbx::els_gmres(*e->e, g_n, tau_n, precond != 0, tol, max_iter, restart,
+                                         sbx::lib_stream());
+    if (n_iter) *n_iter = r.n_iter;
+    if (history)
+      for (size_t i = 0; i < r.history.size() && int64_t(i) < history_cap; ++i) history[i] = r.history[i];
+    if (!r.error.empty()) throw sbx::Error(SBX_NONCONVERGENCE, r.error);
+  });
+}
+
 int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
                       int64_t ldy, int flags, void* stream) {
   return guard([&] {

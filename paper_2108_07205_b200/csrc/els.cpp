@@ -96,6 +96,8 @@ std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan,
     idx.upload(added_s, s);
     eo.submatrix(idx.get(), n_p, idx.get(), n_p, app.get(), n_p, s);
     a->inv.resize(size_t(n_p * n_p));
+    a->fwd.resize(size_t(n_p * n_p));
+    SBX_CUDA(cudaMemcpyAsync(a->fwd.get(), app.get(), size_t(n_p * n_p) * 8, cudaMemcpyDeviceToDevice, s));
     const double rc = dense_inverse(app.get(), n_p, a->inv.get(), s);
     if (rc < 1e-14) throw Error(4, "added-unknown diagonal block is singular at added block");
   } else {
@@ -139,7 +141,8 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
     e->R.resize(size_t(k * n));
     SBX_CUDA(cudaMemcpyAsync(e->R.get(), upd.R.get(), size_t(k * n) * 8, cudaMemcpyDeviceToDevice, s));
     e->X.resize(size_t(n * k));
-    atilde_solve(*e, upd.L.get(), n, e->X.get(), n, k, s);
+    e->L = upd.L;
+    atilde_solve(*e, upd.L->get(), n, e->X.get(), n, k, s);
     phase_mark("els: X = Atilde^-1 L", s);
     // W = I + R X  (els.cpp:124)
     e->Wmat.resize(size_t(k * k));
@@ -159,6 +162,39 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   SBX_CUDA(cudaStreamSynchronize(s));
   phase_mark("els: W, LU(W)", s);
   return e;
+}
+
+void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s) {
+  const i64 n = e.n_ext(), nkc = e.n_k + e.n_c;
+  HbsOp& A = *e.a_oo;
+  if (!A.apply_plan.built) hbs_build_apply_plan(A);
+  SweepPlan& P = A.apply_plan;
+  const i64 ldw = sweep_ld(nrhs);
+  A.ws.reserve(size_t(P.ws_rows * ldw));
+  launch_cm_to_rm(v, n, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
+  hbs_run_plan(A, P, A.ws.get(), nrhs, s);
+  launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, n, e.d_old_of_ext.get(), s);
+  if (e.n_p > 0) {
+    if (e.app->h) {
+      HbsOp& H = *e.app->h;
+      if (!H.apply_plan.built) hbs_build_apply_plan(H);
+      SweepPlan& Q = H.apply_plan;
+      H.ws.reserve(size_t(Q.ws_rows * ldw));
+      launch_cm_to_rm(v + nkc, n, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
+      hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
+      launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, out + nkc, n, nullptr, s);
+    } else {
+      gemm_batched({{e.app->fwd.get(), v + nkc, out + nkc, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(n),
+                     int(n), 0, 0, 1.0, 0.0}},
+                   s);
+    }
+  }
+  if (e.k == 0) return;
+  // out += L (R v)   (els.cpp:184); L is reconstructed as the update factor
+  e.ws2.reserve(size_t(e.k * nrhs));
+  double* t = e.ws2.get();
+  gemm_batched({{e.R.get(), v, t, int(e.k), int(nrhs), int(n), int(e.k), int(n), int(e.k), 0, 0, 1.0, 0.0}}, s);
+  gemm_batched({{e.L->get(), t, out, int(n), int(nrhs), int(e.k), int(n), int(e.k), int(n), 0, 0, 1.0, 1.0}}, s);
 }
 
 void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cudaStream_t s) {

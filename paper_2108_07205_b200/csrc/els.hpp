@@ -13,6 +13,8 @@
 #include "hbs.hpp"
 #include "update.hpp"
 
+#include <string>
+
 namespace sbx {
 
 // A_pp^{-1} for the added unknowns (els.cpp:98-118): explicit dense inverse
@@ -26,6 +28,7 @@ struct AppSolver {
   std::vector<i64> added;           // plan.added_new it was built for
   std::unique_ptr<HbsOp> h;         // HBS of A_pp above the dense limit
   DevBuf<double> inv;               // dense A_pp^{-1}
+  DevBuf<double> fwd;               // dense A_pp (forward apply, els.cpp:67-74)
   bool matches(const Geom& g2, const Plan& p, int f, double m, double e) const {
     return g == &g2 && form == f && mu == m && eps == e && added == p.added_new;
   }
@@ -40,6 +43,7 @@ struct Els {
   i64 k = 0;
   i64 n_ext() const { return n_k + n_c + n_p; }
   DevBuf<double> R;                 // k x n_ext
+  std::shared_ptr<DevBuf<double>> L;  // n_ext x k (the update's, shared)
   DevBuf<double> X;                 // n_ext x k
   DevBuf<double> Winv;              // k x k explicit (I + R X)^{-1}
   DevBuf<double> Wmat;              // k x k (I + R X), for inspection
@@ -59,6 +63,23 @@ void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, b
                cudaStream_t s);
 void els_density_on_refined(const Els& e, const double* tau_n, double* out);
 void els_download_xw(const Els& e, double* X, double* W, cudaStream_t s);
+
+// els_apply_forward (els.cpp:181-186): out = (Atilde + L R) v, v / out
+// n_ext x nrhs device blocks (ld n_ext).
+void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s);
+
+// GMRES / PGMRES-Local on the refined system in (kept, added) unknowns
+// (gmres.cpp:14-126 driven like scenario.cpp:694-727): operator =
+// els_apply_forward restricted to (kept, added), optional left
+// preconditioner = els_solve.  Host g_n in, tau_n out; returns iterations,
+// fills the relative residual history (iterations + 1 entries).
+struct GmresOutcome {
+  i64 n_iter = 0;
+  std::vector<double> history;
+  std::string error;  // non-empty: the reference's ConvergenceError message
+};
+GmresOutcome els_gmres(Els& e, const double* g_n, double* tau_n, bool precond, double tol, i64 max_iter,
+                       i64 restart, cudaStream_t s);
 
 // Device-resident solve for callers holding device buffers:
 // y_ext (n_ext x nrhs, column-major ld n_ext) = ELS^{-1} g_ext.

@@ -813,7 +813,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   u->skeleton.clear();
   for (const Piv& p : order)
     u->skeleton.push_back(groups[p.g]->hrowmap[size_t(fin.perm(size_t(p.g))[size_t(p.i)])]);
-  u->L.resize(size_t(std::max<i64>(n_ext * k, 1)));
+  u->L->resize(size_t(std::max<i64>(n_ext * k, 1)));
   u->R.resize(size_t(std::max<i64>(k * n_ext, 1)));
   if (k > 0) {
     std::vector<std::unique_ptr<DevBuf<double>>> pg;
@@ -826,12 +826,12 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     }
     fin.interp(kg, Pp, ldp, s);
     phase_mark("update: final interp", s);
-    SBX_CUDA(cudaMemsetAsync(u->L.get(), 0, size_t(n_ext * k) * 8, s));
+    SBX_CUDA(cudaMemsetAsync(u->L->get(), 0, size_t(n_ext * k) * 8, s));
     std::vector<ScatterJob> lj;
     for (i64 col = 0; col < k; ++col) {  // L column `col` = group column order[col].i
       const Piv& p = order[size_t(col)];
       const Group& G = *groups[p.g];
-      lj.push_back({Pp[size_t(p.g)] + size_t(p.i) * size_t(ldp[size_t(p.g)]), u->L.get(), G.rowmap,
+      lj.push_back({Pp[size_t(p.g)] + size_t(p.i) * size_t(ldp[size_t(p.g)]), u->L->get(), G.rowmap,
                     int(G.rows), 1, ldp[size_t(p.g)], int(n_ext), int(col), 0, 1.0});
     }
     scatter_batched(lj, s);
@@ -854,7 +854,7 @@ void update_download(const Update& u, int which, double* out, cudaStream_t s) {
   require(which == 0 || which == 1, "update factor: which must be 0 (L) or 1 (R)");
   const size_t n = size_t(u.n_ext() * u.k);
   if (n == 0) return;
-  (which == 0 ? u.L : u.R).download(out, n, s);
+  (which == 0 ? *u.L : u.R).download(out, n, s);
   SBX_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -868,7 +868,7 @@ std::unique_ptr<Update> update_from_factors(const Plan& plan, const double* L, c
   require(k >= 0, "negative rank");
   u->k = k;
   u->k1 = k;
-  u->L.upload(L, size_t(n_ext * k), s);
+  u->L->upload(L, size_t(n_ext * k), s);
   u->R.upload(R, size_t(n_ext * k), s);
   SBX_CUDA(cudaStreamSynchronize(s));
   return u;

@@ -2,6 +2,7 @@
 // proxy.cpp:46-302, two-step ID mode).
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -15,7 +16,8 @@ struct Update {
   i64 k = 0, k1 = 0, k_kc = 0, k_kp = 0, k_pk = 0;
   i64 nk2 = 0, nc2 = 0, np2 = 0;
   i64 n_ext() const { return nk2 + nc2 + np2; }
-  DevBuf<double> L;  // n_ext x k, column-major
+  // n_ext x k, column-major; shared with the ELS solvers built on it
+  std::shared_ptr<DevBuf<double>> L = std::make_shared<DevBuf<double>>();
   DevBuf<double> R;  // k x n_ext, column-major
   std::vector<i64> skeleton;
   std::vector<std::string> notes;

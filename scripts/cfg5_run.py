@@ -15,6 +15,19 @@ import paper_2108_07205_b200 as sb  # noqa: E402
 from paper_2108_07205_b200.configs import CONFIGS  # noqa: E402
 
 
+def stokeslet_field(src, tg, mu=1.0):
+    """Analytic velocity of point forces (x, y, fx, fy) at targets (kernels.cpp:13-31)."""
+    out = np.zeros((len(tg), 2))
+    for x, y, fx, fy in src:
+        r = tg - np.array([x, y])
+        r2 = np.sum(r * r, 1)
+        lg = -0.5 * np.log(r2)
+        rf = r[:, 0] * fx + r[:, 1] * fy
+        out[:, 0] += (lg * fx + r[:, 0] * rf / r2) / (4 * np.pi * mu)
+        out[:, 1] += (lg * fy + r[:, 1] * rf / r2) / (4 * np.pi * mu)
+    return out
+
+
 def t():
     sb.api.lib().sbx_sync()
     return time.perf_counter()
@@ -61,8 +74,7 @@ def main():
         for j in range(a.check_rhs):
             dens = sb.density_on_refined(els, tau[:, j])
             vel, _, near = sb.evaluate_solution(g1, sb.MIXED, dens, tg)
-            from oracle import pyoracle as po  # analytic Stokeslet field only
-            ex = po.field_velocity(srcs[j], tg)
+            ex = stokeslet_field(srcs[j], tg)
             err = np.max(np.linalg.norm(vel - ex, axis=1) / np.linalg.norm(ex, axis=1))
             print(f"  rhs {j}: max relative velocity error at {len(tg)} fluid targets {err:.2e} "
                   f"(near-boundary targets: {int(near.sum())})", flush=True)
