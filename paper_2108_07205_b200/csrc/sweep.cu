@@ -116,14 +116,16 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
 // columns need not be 16-byte aligned) and B (workspace rows produced by
 // other CTAs of the launch: 16-byte .cg copies that bypass L1, whose lines
 // could hold stale neighbours of a just-published row).
-constexpr int kTN = 64;
 constexpr int kKC = 16;
 constexpr int kStages = 4;
 constexpr int kPad = 8;  // row stride 72 doubles
 
+// TN: columns per tile (64, or 32 to halve the work per item on the
+// latency-bound upper levels of the tree)
+template <int TN>
 struct DmmaSmem {
   double As[kStages][kKC][kTM + kPad];
-  double Bs[kStages][kKC][kTN + kPad];
+  double Bs[kStages][kKC][TN + kPad];
 };
 
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
@@ -145,8 +147,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+template <int TN>
 __device__ __forceinline__ void dmma_issue_a(const double* __restrict__ fac, const SweepTask& t, int row0,
-                                             int stage, int k0, int ke, DmmaSmem& S) {
+                                             int stage, int k0, int ke, DmmaSmem<TN>& S) {
   const double* A = fac + t.a_off;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -158,13 +161,15 @@ __device__ __forceinline__ void dmma_issue_a(const double* __restrict__ fac, con
   }
 }
 
+template <int TN>
 __device__ __forceinline__ void dmma_issue_b(const double* __restrict__ ws, const SweepTask& t, int col0,
-                                             int nrhs, int ldw, int stage, int k0, int ke, DmmaSmem& S) {
+                                             int nrhs, int ldw, int stage, int k0, int ke, DmmaSmem<TN>& S) {
   const double* B = ws + t.b_row * ldw;
+  constexpr int kPairs = TN / 2;  // 16-byte pairs per B row
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int idx = threadIdx.x + q * kThreads;  // 0..511: 16 rows x 32 pairs
-    const int kk = idx >> 5, pr = (idx & 31) * 2;
+  for (int q = 0; q < TN / 32; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // 16 rows x kPairs pairs
+    const int kk = idx / kPairs, pr = (idx % kPairs) * 2;
     const int gk = k0 + kk, gcol = col0 + pr;
     int bytes = 0;
     if (gk < ke) bytes = gcol + 1 < nrhs ? 16 : (gcol < nrhs ? 8 : 0);
@@ -174,8 +179,9 @@ __device__ __forceinline__ void dmma_issue_b(const double* __restrict__ ws, cons
 
 // Issues the A parts of the first kStages-1 chunks (call before waiting on
 // the producers of B); they join the first commit group.
+template <int TN>
 __device__ __forceinline__ void dmma_prefetch(const double* __restrict__ fac, const SweepTask& t, int row0,
-                                              int kb, int ke, DmmaSmem& S) {
+                                              int kb, int ke, DmmaSmem<TN>& S) {
   const int nchunks = (ke - kb + kKC - 1) / kKC;
 #pragma unroll
   for (int c = 0; c < kStages - 1; ++c)
@@ -184,19 +190,33 @@ __device__ __forceinline__ void dmma_prefetch(const double* __restrict__ fac, co
 
 // partial != null: write the raw 64 x 64 tile there (row-major) instead of
 // the final rows (split-K).
+template <int TN>
 __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double* __restrict__ ws,
                                           const SweepTask& t, int row0, int col0, int nrhs, int ldw,
-                                          int kb, int ke, DmmaSmem& S, double* partial) {
+                                          int kb, int ke, DmmaSmem<TN>& S, double* partial) {
+  constexpr int NB = TN / 16;  // 8-column blocks per warp (warps: 4 row x 2 column groups)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wm = (warp & 3) * 16;
-  const int wn = (warp >> 2) * 32;
-  double c[2][4][2];
+  const int wn = (warp >> 2) * (TN / 2);
+  double c[2][NB][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) c[a][b][0] = c[a][b][1] = 0.0;
+    for (int b = 0; b < NB; ++b) c[a][b][0] = c[a][b][1] = 0.0;
   const int nchunks = (ke - kb + kKC - 1) / kKC;
+  // the P block (produced long before, by the up-sweep) is loaded now so its
+  // latency hides behind the K loop
+  double pv[2][NB][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int row = row0 + wm + a * 8 + gid, col = col0 + wn + b * 8 + 2 * tig;
+      const bool ok = !partial && t.p_row >= 0 && row < t.m;
+      pv[a][b][0] = ok && col < nrhs ? __ldcg(ws + (t.p_row + row) * ldw + col) : 0.0;
+      pv[a][b][1] = ok && col + 1 < nrhs ? __ldcg(ws + (t.p_row + row) * ldw + col + 1) : 0.0;
+    }
 #pragma unroll
   for (int ch = 0; ch < kStages - 1; ++ch) {  // B of the prologue chunks (A already issued)
     if (ch < nchunks) dmma_issue_b(ws, t, col0, nrhs, ldw, ch, kb + ch * kKC, ke, S);
@@ -214,15 +234,15 @@ __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double
     cp_async_commit();
 #pragma unroll
     for (int k4 = 0; k4 < kKC; k4 += 4) {
-      double af[2], bf[4];
+      double af[2], bf[NB];
 #pragma unroll
       for (int a = 0; a < 2; ++a) af[a] = S.As[st][k4 + tig][wm + a * 8 + gid];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = S.Bs[st][k4 + tig][wn + b * 8 + gid];
+      for (int b = 0; b < NB; ++b) bf[b] = S.Bs[st][k4 + tig][wn + b * 8 + gid];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma_m8n8k4(c[a][b][0], c[a][b][1], af[a], bf[b]);
+        for (int b = 0; b < NB; ++b) dmma_m8n8k4(c[a][b][0], c[a][b][1], af[a], bf[b]);
     }
   }
   cp_async_wait<0>();
@@ -231,10 +251,10 @@ __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < NB; ++b) {
         const int r = wm + a * 8 + gid, cc = wn + b * 8 + 2 * tig;
-        partial[r * kTN + cc] = c[a][b][0];
-        partial[r * kTN + cc + 1] = c[a][b][1];
+        partial[r * TN + cc] = c[a][b][0];
+        partial[r * TN + cc + 1] = c[a][b][1];
       }
     return;
   }
@@ -244,12 +264,12 @@ __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double
     if (row >= t.m) continue;
     const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const int col = col0 + wn + b * 8 + 2 * tig;
       double v0 = c[a][b][0], v1 = c[a][b][1];
       if (t.p_row >= 0) {
-        if (col < nrhs) v0 += __ldcg(ws + (t.p_row + row) * ldw + col);
-        if (col + 1 < nrhs) v1 += __ldcg(ws + (t.p_row + row) * ldw + col + 1);
+        v0 += pv[a][b][0];
+        v1 += pv[a][b][1];
       }
       if (col < nrhs) ws[dst * ldw + col] = v0;
       if (col + 1 < nrhs) ws[dst * ldw + col + 1] = v1;
@@ -271,7 +291,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-template <bool kDmma>
+template <bool kDmma, int TN>
 __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     sweep_flow_kernel(const double* __restrict__ fac, double* __restrict__ ws,
                       const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
@@ -281,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_next, s_last;
   constexpr int tile = kDmma ? kTM : kGR;
-  constexpr int tile_elems = kDmma ? kTM * kTN : kGR;
+  constexpr int tile_elems = kDmma ? kTM * TN : kGR;
   int* ticket = counters;  // counters[0]; per-(task, col tile) counts follow
   if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1);
   for (;;) {
@@ -297,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     const SweepTask t = tasks[it.task];
     GemvRegs g;
     if constexpr (kDmma)
-      dmma_prefetch(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem*>(dsm));
+      dmma_prefetch<TN>(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem<TN>*>(dsm));
     else
       gemv_prefetch(fac, t, it.row0, it.kb, it.ke, g);
     if (threadIdx.x < t.ndep) {
@@ -310,24 +330,26 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     double* part = it.nsplit > 1 ? partials + it.poff + i64(it.ks) * tile_elems : nullptr;
     if constexpr (kDmma)
-      dmma_item(fac, ws, t, it.row0, it.ct * kTN, nrhs, ldw, it.kb, it.ke,
-                *reinterpret_cast<DmmaSmem*>(dsm), part);
+      dmma_item<TN>(fac, ws, t, it.row0, it.ct * TN, nrhs, ldw, it.kb, it.ke,
+                    *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
     else
       gemv_finish(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // the item's stores happen-before thread 0's release below
     bool done = true;
     if (it.nsplit > 1) {  // last split of the tile reduces the partials in split order
-      if (threadIdx.x == 0) s_last = atomicAdd(tile_cnt + it.cidx, 1) == it.nsplit - 1;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(tile_cnt + it.cidx, 1) == it.nsplit - 1;
+      }
       __syncthreads();
       done = s_last != 0;
       if (done) {
         __threadfence();
         const double* pb = partials + it.poff;
         if constexpr (kDmma) {
-          for (int e = threadIdx.x; e < kTM * kTN; e += kThreads) {
-            const int r = e / kTN, cc = e % kTN;
-            const int row = it.row0 + r, col = it.ct * kTN + cc;
+          for (int e = threadIdx.x; e < kTM * TN; e += kThreads) {
+            const int r = e / TN, cc = e % TN;
+            const int row = it.row0 + r, col = it.ct * TN + cc;
             if (row >= t.m || col >= nrhs) continue;
             double v = 0.0;
             for (int q = 0; q < it.nsplit; ++q) v += __ldcg(pb + i64(q) * tile_elems + e);
@@ -346,12 +368,14 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
             ws[dst] = v;
           }
         }
-        __threadfence();
         __syncthreads();
       }
     }
     if (threadIdx.x == 0) {
-      if (done) atomicAdd(counters + 1 + it.task * ncol + it.ct, 1);
+      if (done) {
+        __threadfence();  // cumulative: covers every thread's stores ordered by the barrier
+        atomicAdd(counters + 1 + it.task * ncol + it.ct, 1);
+      }
       s_next = nxt;
       if (trace) {
         unsigned long long t2;
@@ -378,6 +402,7 @@ __global__ void __launch_bounds__(kThreads)
   gemv_finish(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr);
 }
 
+template <int TN>
 __global__ void __launch_bounds__(kThreads)
     sweep_dmma_kernel(const double* __restrict__ fac, double* __restrict__ ws,
                       const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
@@ -386,9 +411,9 @@ __global__ void __launch_bounds__(kThreads)
   const FlowItem f = items[blockIdx.x];
   const int4 it = make_int4(f.task, f.row0, f.ct, 0);
   const SweepTask t = tasks[it.x];
-  DmmaSmem& S = *reinterpret_cast<DmmaSmem*>(dsm);
-  dmma_prefetch(fac, t, it.y, 0, t.K, S);
-  dmma_item(fac, ws, t, it.y, it.z * kTN, nrhs, ldw, 0, t.K, S, nullptr);
+  DmmaSmem<TN>& S = *reinterpret_cast<DmmaSmem<TN>*>(dsm);
+  dmma_prefetch<TN>(fac, t, it.y, 0, t.K, S);
+  dmma_item<TN>(fac, ws, t, it.y, it.z * TN, nrhs, ldw, 0, t.K, S, nullptr);
 }
 
 // ---------------------------------------------------------------- layout moves
@@ -827,30 +852,32 @@ void hbs_build_apply_plan(HbsOp& op) {
   finalize(P);
 }
 
-void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
+namespace {
+template <int TN>
+void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
   const double* fac = op.arena.get();
   const bool dmma = nrhs > 1;
   static const bool per_level = std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
   int max_k = 0;
   for (auto& L : plan.levels) max_k = std::max(max_k, L.max_k);
   const size_t gemv_smem = size_t(((max_k + 1) & ~1) + kThreads) * sizeof(double);
-  const size_t smem = dmma ? sizeof(DmmaSmem) : gemv_smem;
+  const size_t smem = dmma ? sizeof(DmmaSmem<TN>) : gemv_smem;
   static std::once_flag attr;
   std::call_once(attr, [] {
-    SBX_CUDA(cudaFuncSetAttribute(sweep_flow_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(sizeof(DmmaSmem))));
-    SBX_CUDA(cudaFuncSetAttribute(sweep_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(sizeof(DmmaSmem))));
+    SBX_CUDA(cudaFuncSetAttribute(sweep_flow_kernel<true, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(DmmaSmem<TN>))));
+    SBX_CUDA(cudaFuncSetAttribute(sweep_dmma_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(DmmaSmem<TN>))));
   });
-  const int ncol = dmma ? int((nrhs + kTN - 1) / kTN) : 1;
+  const int ncol = dmma ? int((nrhs + TN - 1) / TN) : 1;
   const int tile = dmma ? kTM : kGR;
   int dev = 0, sms = 148, per_sm = 1;
   SBX_CUDA(cudaGetDevice(&dev));
   SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (dmma)
-    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<true>, kThreads, smem));
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<true, TN>, kThreads, smem));
   else
-    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<false>, kThreads, smem));
+    SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_flow_kernel<false, TN>, kThreads, smem));
   per_sm = std::max(per_sm, 1);
   static const int split_env = [] {
     // split-K of the short upper levels: measured slower on cfg2/cfg3 (the
@@ -859,12 +886,16 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
     const char* e = std::getenv("SBX_SWEEP_SPLIT");
     return e ? std::atoi(e) : 0;
   }();
-  const int target = (per_level || split_env == 0) ? 0 : sms * per_sm;
-  const int key = (ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0);
+  static const int split_target = [] {
+    const char* e = std::getenv("SBX_SWEEP_SPLIT_TARGET");
+    return e ? std::atoi(e) : 64;
+  }();
+  const int target = (per_level || split_env == 0) ? 0 : split_target;
+  const int key = ((ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0)) * 128 + TN;
   if (plan.flow_key != key) {
     plan.level_items.clear();
     const std::vector<FlowItem> fi =
-        make_items(plan, tile, ncol, dmma ? kTM * kTN : kGR, target, &plan.level_items, &plan.partial_elems,
+        make_items(plan, tile, ncol, dmma ? kTM * TN : kGR, target, &plan.level_items, &plan.partial_elems,
                    &plan.n_tile_cnt);
     plan.d_flow_items.upload(fi, s);
     plan.n_flow_items = i64(fi.size());
@@ -877,8 +908,8 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
       if (!dmma)
         sweep_gemv_kernel<<<unsigned(rg.y), kThreads, gemv_smem, s>>>(fac, ws, plan.d_tasks.get(), items);
       else
-        sweep_dmma_kernel<<<unsigned(rg.y), kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), items, int(nrhs),
-                                                                  int(sweep_ld(nrhs)));
+        sweep_dmma_kernel<TN><<<unsigned(rg.y), kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), items,
+                                                                      int(nrhs), int(sweep_ld(nrhs)));
       SBX_LAUNCHED();
     }
     return;
@@ -894,15 +925,15 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
   DevBuf<unsigned long long> trace;
   if (trace_path) trace.resize(size_t(4 * plan.n_flow_items));
   if (dmma)
-    sweep_flow_kernel<true><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
-                                                         int(plan.n_flow_items), plan.d_counters.get(), ncol,
-                                                         int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
-                                                         tile_cnt, trace.get());
+    sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
+                                                             int(plan.n_flow_items), plan.d_counters.get(), ncol,
+                                                             int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
+                                                             tile_cnt, trace.get());
   else
-    sweep_flow_kernel<false><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
-                                                          plan.d_flow_items.get(), int(plan.n_flow_items),
-                                                          plan.d_counters.get(), ncol, int(nrhs), 1,
-                                                          plan.d_partials.get(), tile_cnt, trace.get());
+    sweep_flow_kernel<false, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
+                                                              plan.d_flow_items.get(), int(plan.n_flow_items),
+                                                              plan.d_counters.get(), ncol, int(nrhs), 1,
+                                                              plan.d_partials.get(), tile_cnt, trace.get());
   SBX_LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(size_t(4 * plan.n_flow_items));
@@ -927,6 +958,22 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
       std::fclose(f);
     }
   }
+}
+
+}  // namespace
+
+void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
+  // column tile: 32 when the block is narrow enough that the tree depth
+  // (not the tensor throughput) bounds the sweep (SBX_SWEEP_TN overrides)
+  static const int tn_env = [] {
+    const char* e = std::getenv("SBX_SWEEP_TN");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int tn = tn_env == 32 || tn_env == 64 ? tn_env : (nrhs <= 192 ? 32 : 64);
+  if (tn == 32)
+    run_flow<32>(op, plan, ws, nrhs, s);
+  else
+    run_flow<64>(op, plan, ws, nrhs, s);
 }
 
 namespace {
