@@ -64,8 +64,8 @@ typedef struct {
   double center_x, center_y, scale;
   int32_t flip_normal, n_prongs;
   double amplitude, aspect;
-  int32_t n_cos, n_sin;          /* fourier coefficient counts (<= 16 each) */
-  double cos_coef[16], sin_coef[16];
+  int32_t n_cos, n_sin;          /* fourier coefficient counts (<= 64 each) */
+  double cos_coef[64], sin_coef[64];
 } sbx_curve;
 
 /* HbsOptions (hbs.hpp:39-46). n_proxy is accepted and, as in the reference

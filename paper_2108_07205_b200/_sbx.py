@@ -42,8 +42,8 @@ class sbx_curve(C.Structure):
         ("aspect", C.c_double),
         ("n_cos", C.c_int32),
         ("n_sin", C.c_int32),
-        ("cos_coef", C.c_double * 16),
-        ("sin_coef", C.c_double * 16),
+        ("cos_coef", C.c_double * 64),
+        ("sin_coef", C.c_double * 64),
     ]
 
 

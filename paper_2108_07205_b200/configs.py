@@ -160,6 +160,78 @@ class HolesConfig:
         return np.array(pts)
 
 
+@dataclass
+class ChannelConfig:
+    """configs[3]: transient sequence on a wavy channel closed into a smooth
+    curve.  The reference has no general parametric curve,
+    so the channel y = +/-(1 + 0.2 sin(2 pi x / 4)), x in [0, 8], with round
+    end caps is represented as a radial Fourier curve about (4, 0) (the
+    reference's CurveKind::Fourier, geometry.cpp:49-63): 64 sigma-smoothed
+    modes of the polar radius of that shape.  2048 panels x 16 nodes.  A disk
+    of radius 0.1 (a proximity trigger only, never discretized, as in
+    scenario.cpp:773-788) approaches the right end cap along y = 0 (where the
+    equal-parameter panels of the radial curve are longest, ~0.015), the gap
+    shrinking geometrically from 0.5 to 0.005 over 200 steps; each step
+    refines the base panels within 5 gaps of the disk so panel length is at
+    most the gap (m = ceil(max length / gap)) and solves one Stokeslet RHS."""
+    name: str = "cfg4"
+    n_panels: int = 2048
+    q: int = 16
+    modes: int = 64
+    eps: float = 1e-10
+    leaf: int = 64
+    steps: int = 200
+    gap0: float = 0.5
+    gap1: float = 0.005
+    disk_radius: float = 0.1
+    seed: int = 0
+
+    def shape_inside(self, x, y):
+        h = 1.0 + 0.2 * np.sin(2 * np.pi * x / 4.0)
+        if 0.0 <= x <= 8.0:
+            return abs(y) < h
+        if x < 0.0:
+            return x * x + y * y < 1.0
+        return (x - 8.0) ** 2 + y * y < 1.0
+
+    def fourier(self):
+        """(scale, cos_coef, sin_coef) of the radial curve about (4, 0)."""
+        m = 2048
+        th = 2 * np.pi * np.arange(m) / m
+        r = np.empty(m)
+        for i, t in enumerate(th):
+            c, s_ = np.cos(t), np.sin(t)
+            lo = 0.0
+            while self.shape_inside(4 + (lo + 0.002) * c, (lo + 0.002) * s_):
+                lo += 0.002
+            hi = lo + 0.002
+            for _ in range(50):
+                mid = 0.5 * (lo + hi)
+                if self.shape_inside(4 + mid * c, mid * s_):
+                    lo = mid
+                else:
+                    hi = mid
+            r[i] = 0.5 * (lo + hi)
+        F = np.fft.rfft(r) / m
+        a0 = F[0].real
+        k = np.arange(1, self.modes + 1)
+        sig = np.sinc(k / (self.modes + 1))  # Lanczos sigma factors against Gibbs ringing
+        return a0, list(2 * F[1:self.modes + 1].real * sig / a0), list(-2 * F[1:self.modes + 1].imag * sig / a0)
+
+    def gaps(self):
+        return self.gap0 * (self.gap1 / self.gap0) ** (np.arange(self.steps) / (self.steps - 1))
+
+    def sources(self):
+        rng = np.random.default_rng(self.seed)
+        xs = np.linspace(1.0, 7.0, 4)
+        pts = np.array([(x, y) for x in xs for y in (-2.6, 2.6)])
+        return np.column_stack([pts, rng.standard_normal((len(pts), 2))])
+
+    def targets(self):
+        xs = np.linspace(1.5, 6.5, 6)
+        return np.array([(x, y) for x in xs for y in (-0.3, 0.0, 0.3)])
+
+
 CONFIGS = {
     # BASELINE.json configs[0]: ellipse (2,1), 128x16 nodes, 4 panels near
     # (1.99, 0) split 3 dyadic levels (m = 8), 5 Stokeslets at radius 4.
@@ -171,6 +243,8 @@ CONFIGS = {
                               sources_per_rhs=8),
     # configs[2]: star, 4096x16 nodes, HBS inverse apply microbenchmark.
     "cfg3": RefinedWallConfig("cfg3", "star", 4096, a=1.0, n_refine=0, m=1, nrhs=1),
+    # configs[3]: 200-step transient on the wavy channel.
+    "cfg4": ChannelConfig(),
     # configs[4]: multiply connected large case (Mixed formulation).
     "cfg5": HolesConfig(),
 }

@@ -63,7 +63,7 @@ void check_curve(const sbx_curve& p) {  // geometry.cpp:11-34
   }
   if (p.kind == SBX_ELLIPSE && p.aspect <= 0) throw Error(3, "ellipse aspect must be positive");
   if (p.kind < 0 || p.kind > 3) throw Error(1, "unknown curve kind");
-  if (p.n_cos < 0 || p.n_cos > 16 || p.n_sin < 0 || p.n_sin > 16)
+  if (p.n_cos < 0 || p.n_cos > 64 || p.n_sin < 0 || p.n_sin > 64)
     throw Error(1, "fourier coefficient count out of range");
 }
 
@@ -187,7 +187,10 @@ bool inside(const CurveDef& cv, double qx, double qy, int samples = 512) {  // g
   return crossings % 2 == 1;
 }
 
-void append_nodes(Geom& g, i64 ci) {  // geometry.cpp:149-179
+// skip (optional, per panel of the component): leave the node arrays of
+// those panels zero for the caller to fill (refine copies kept nodes bit for
+// bit, so evaluating the curve there is wasted work).
+void append_nodes(Geom& g, i64 ci, const std::vector<char>* skip = nullptr) {  // geometry.cpp:149-179
   Component& comp = g.comps[size_t(ci)];
   const GaussTable& gt = gauss_table(comp.q);
   const int q = comp.q;
@@ -197,6 +200,11 @@ void append_nodes(Geom& g, i64 ci) {  // geometry.cpp:149-179
     const i64 pid = i64(g.panels.size());
     g.panels.push_back({ci, i64(pl), pd.a, pd.b, pd.level, g.n_nodes(), q});
     const double half = 0.5 * (pd.b - pd.a);
+    if (skip && (*skip)[pl]) {
+      for (auto* v : {&g.x, &g.y, &g.nx, &g.ny, &g.tx, &g.ty, &g.w, &g.kappa, &g.t}) v->resize(v->size() + size_t(q));
+      g.panel_of.insert(g.panel_of.end(), size_t(q), pid);
+      continue;
+    }
     for (int j = 0; j < q; ++j) {
       const double t = pd.a + half * (gt.x[size_t(j)] + 1.0);
       double px, py, dx, dy, ddx, ddy;
@@ -323,6 +331,7 @@ std::pair<std::unique_ptr<Geom>, std::unique_ptr<Plan>> geom_refine(const Geom& 
     plan->old_panels.push_back(comp.panels);
     plan->old_q.push_back(comp.q);
     std::vector<PanelDef> mesh;
+    std::vector<char> kept;  // new panels that are unrefined copies
     for (size_t pl = 0; pl < comp.panels.size(); ++pl) {
       const PanelDef& p = comp.panels[pl];
       if (refined[size_t(comp.panel_offset + i64(pl))]) {
@@ -330,15 +339,17 @@ std::pair<std::unique_ptr<Geom>, std::unique_ptr<Plan>> geom_refine(const Geom& 
         for (int j = 1; j <= m; ++j) {
           const double next = (j == m) ? p.b : p.a + (p.b - p.a) * j / m;
           mesh.push_back({prev, next, p.level + 1});
+          kept.push_back(0);
           prev = next;
         }
       } else {
         mesh.push_back(p);
+        kept.push_back(1);
       }
     }
     ng->comps.push_back({comp.curve, std::move(mesh), comp.q, ng->n_nodes(), i64(ng->panels.size()),
                          comp.is_hole});
-    append_nodes(*ng, i64(ci));
+    append_nodes(*ng, i64(ci), &kept);
   }
   i64 new_panel = 0;
   for (i64 op = 0; op < np; ++op) {
