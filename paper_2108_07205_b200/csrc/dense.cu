@@ -219,12 +219,14 @@ __device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps
         }
       p = bq;
     }
-    // Householder vector of the pivot column, one warp (makeHouseholderInPlace)
+    // Householder vector of the pivot column (makeHouseholderInPlace): the
+    // tail norm is a CTA-wide reduction, beta / tau are formed redundantly
+    // by every thread, the scaling is spread over the CTA
     double* pc = A + size_t(p) * lda;
-    if (warp == 0) {
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < M; i += 32) s += pc[i] * pc[i];
-      s = warp_sum(s);
+    {
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < M; i += kT) part += pc[i] * pc[i];
+      const double s = block_sum(part, red);
       const double c0 = pc[j];
       double tau = 0.0, beta = c0, denom = 0.0;
       if (s > DBL_MIN) {
@@ -233,9 +235,9 @@ __device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps
         denom = c0 - beta;
         tau = (beta - c0) / beta;
       }
-      for (int i = j + 1 + lane; i < M; i += 32) pc[i] = denom == 0.0 ? 0.0 : pc[i] / denom;
-      __syncwarp();
-      if (lane == 0) {
+      __syncthreads();  // every thread has read pc[j] and red
+      for (int i = j + 1 + tid; i < M; i += kT) pc[i] = denom == 0.0 ? 0.0 : pc[i] / denom;
+      if (tid == 0) {
         pc[j] = beta;
         diag[j] = fabs(beta);
         sc[0] = tau;
@@ -273,7 +275,219 @@ __device__ int cpqr_core(double* A, int M, int n, int lda, bool pivot, int steps
   return done;
 }
 
-__global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, int smem_doubles) {
+// Blocked column-pivoted QR (LAPACK dgeqp3/dlaqps organisation) with the
+// pivot rule, Householder convention and norm downdating of cpqr_core.
+// Within a block of kCpqrNb steps the trailing matrix is not touched: the
+// pivot column gets the block's pending reflectors (A - V F^T), F gains one
+// column per step (tau * (A^T v - F (V^T v))), and only the current row of
+// the trailing matrix is updated (for the norm downdates).  One read of the
+// trailing matrix per step instead of two reads and a write; the block ends
+// early when a norm needs recomputation (LAPACK lsticc) and closes with one
+// rank-jb update.  Same pivots as the unblocked loop in exact arithmetic.
+constexpr int kCpqrNb = 8;
+
+__host__ __device__ constexpr int cpqr_blocked_head(int n) { return 3 * n + 72 + kCpqrNb * n + 3 * kCpqrNb + (n + 1) / 2 + 2; }
+
+__device__ int cpqr_core_blocked(double* A, int M, int n, int lda, int steps_max, double stop_eps, int* perm,
+                                 double* diag, double* upd, double* dir, int* pos, int* lphys, double* red,
+                                 int* ired, double* sc, double* F, double* aux, double* vrow, int* bp,
+                                 int* rec) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int size = min(M, n);
+  __shared__ int s_anyrec;
+  for (int c = tid; c < n; c += kT) {
+    pos[c] = c;
+    lphys[c] = c;
+    rec[c] = 0;
+  }
+  for (int c = tid; c < size; c += kT) diag[c] = 0.0;
+  for (int c = warp; c < n; c += kWarps) {
+    double s = 0.0;
+    for (int i = lane; i < M; i += 32) {
+      const double v = A[i + size_t(c) * lda];
+      s += v * v;
+    }
+    s = warp_sum(s);
+    if (lane == 0) upd[c] = dir[c] = sqrt(s);
+  }
+  if (tid == 0) s_anyrec = 0;
+  __syncthreads();
+  const double thr = sqrt(DBL_EPSILON);
+  int done = 0, j = 0;
+  double r00 = 0.0;
+  bool stop = false;
+  while (j < steps_max && !stop) {
+    int nbk = 0;  // steps taken in this block
+    for (; nbk < kCpqrNb && j < steps_max; ++nbk, ++j) {
+      // (1) first max of the partial norms over logical positions >= j
+      double bv = -1.0;
+      int bpos = 0x7fffffff, bq = -1;
+      for (int c = tid; c < n; c += kT) {
+        const int lc = pos[c];
+        if (lc >= j && (upd[c] > bv || (upd[c] == bv && lc < bpos))) {
+          bv = upd[c];
+          bpos = lc;
+          bq = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+        const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+        if (ov > bv || (ov == bv && op < bpos)) {
+          bv = ov;
+          bpos = op;
+          bq = oq;
+        }
+      }
+      if (lane == 0) {
+        red[warp] = bv;
+        ired[warp] = bpos;
+        ired[kWarps + warp] = bq;
+      }
+      __syncthreads();
+      bv = -1.0;
+      bpos = 0x7fffffff;
+      for (int w = 0; w < kWarps; ++w)
+        if (red[w] > bv || (red[w] == bv && ired[w] < bpos)) {
+          bv = red[w];
+          bpos = ired[w];
+          bq = ired[kWarps + w];
+        }
+      const int p = bq;
+      double* pc = A + size_t(p) * lda;
+      // (3) pending reflectors of the block on the pivot column, rows >= j
+      for (int i = j + tid; i < M; i += kT) {
+        double acc = pc[i];
+        for (int b = 0; b < nbk; ++b) acc -= A[i + size_t(bp[b]) * lda] * F[size_t(p) * kCpqrNb + b];
+        pc[i] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {  // (2) logical swap: the column at position j moves to the pivot's slot
+        const int lp = pos[p], q = lphys[j];
+        lphys[lp] = q;
+        pos[q] = lp;
+        lphys[j] = p;
+        pos[p] = j;
+        bp[nbk] = p;
+      }
+      // (4) Householder vector (makeHouseholderInPlace)
+      double part = 0.0;
+      for (int i = j + 1 + tid; i < M; i += kT) part += pc[i] * pc[i];
+      const double tail = block_sum(part, red);
+      const double c0 = pc[j];
+      double tau = 0.0, beta = c0, denom = 0.0;
+      if (tail > DBL_MIN) {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        denom = c0 - beta;
+        tau = (beta - c0) / beta;
+      }
+      for (int i = j + 1 + tid; i < M; i += kT) pc[i] = denom == 0.0 ? 0.0 : pc[i] / denom;
+      if (j == 0) r00 = fabs(beta);
+      if (tid == 0) {
+        diag[j] = fabs(beta);
+        pc[j] = beta;
+      }
+      done = j + 1;
+      __syncthreads();
+      if (!(fabs(beta) > stop_eps * r00) && stop_eps > 0.0) {
+        stop = true;
+        ++j;
+        break;
+      }
+      // (5) aux_b = V_b^T v over rows >= j, then F(:, nbk) for the live columns
+      if (warp < nbk) {
+        const double* vb = A + size_t(bp[warp]) * lda;
+        double a = lane == 0 ? vb[j] : 0.0;  // v_j = 1
+        for (int i = j + 1 + lane; i < M; i += 32) a += vb[i] * pc[i];
+        a = warp_sum(a);
+        if (lane == 0) aux[warp] = a;
+      }
+      if (tid < nbk) vrow[tid] = A[j + size_t(bp[tid]) * lda];
+      __syncthreads();
+      for (int c = warp; c < n; c += kWarps) {
+        if (pos[c] <= j) continue;
+        const double* col = A + size_t(c) * lda;
+        double a = lane == 0 ? col[j] : 0.0;
+        for (int i = j + 1 + lane; i < M; i += 32) a += col[i] * pc[i];
+        a = warp_sum(a);
+        if (lane == 0) {
+          double corr = 0.0;
+          for (int b = 0; b < nbk; ++b) corr += F[size_t(c) * kCpqrNb + b] * aux[b];
+          F[size_t(c) * kCpqrNb + nbk] = tau * (a - corr);
+        }
+      }
+      __syncthreads();
+      // (6) current row of the live columns, (7) norm downdating
+      for (int c = tid; c < n; c += kT) {
+        if (pos[c] <= j) continue;
+        double a = A[j + size_t(c) * lda];
+        for (int b = 0; b < nbk; ++b) a -= vrow[b] * F[size_t(c) * kCpqrNb + b];
+        a -= F[size_t(c) * kCpqrNb + nbk];  // v_j = 1
+        A[j + size_t(c) * lda] = a;
+        const double uu = upd[c];
+        if (uu == 0.0) continue;
+        double t = fabs(a) / uu;
+        t = (1.0 + t) * (1.0 - t);
+        t = t < 0.0 ? 0.0 : t;
+        const double rr = uu / dir[c];
+        if (t * rr * rr <= thr) {
+          rec[c] = 1;
+          s_anyrec = 1;
+        } else {
+          upd[c] = uu * sqrt(t);
+        }
+      }
+      __syncthreads();
+      if (s_anyrec) {  // a norm must be recomputed from the updated column: close the block
+        ++nbk;
+        ++j;
+        break;
+      }
+    }
+    if (stop) break;
+    // rank-nbk update of the live columns below the block's last row
+    const int r0 = j;
+    for (int c = warp; c < n; c += kWarps) {
+      if (pos[c] < r0) continue;
+      double* col = A + size_t(c) * lda;
+      double f[kCpqrNb];
+#pragma unroll
+      for (int b = 0; b < kCpqrNb; ++b) f[b] = b < nbk ? F[size_t(c) * kCpqrNb + b] : 0.0;
+      for (int i = r0 + lane; i < M; i += 32) {
+        double acc = col[i];
+#pragma unroll
+        for (int b = 0; b < kCpqrNb; ++b)
+          if (b < nbk) acc -= A[i + size_t(bp[b]) * lda] * f[b];
+        col[i] = acc;
+      }
+    }
+    __syncthreads();
+    if (s_anyrec) {
+      for (int c = warp; c < n; c += kWarps) {
+        if (!rec[c]) continue;
+        const double* col = A + size_t(c) * lda;
+        double s2 = 0.0;
+        for (int i = r0 + lane; i < M; i += 32) s2 += col[i] * col[i];
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          upd[c] = dir[c] = sqrt(s2);
+          rec[c] = 0;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_anyrec = 0;
+      __syncthreads();
+    }
+  }
+  for (int l = tid; l < n; l += kT) perm[l] = lphys[l];
+  __syncthreads();
+  return done;
+}
+
+__global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, int smem_doubles, int blocked) {
   extern __shared__ double sm[];
   const QrJob jb = jobs[blockIdx.x];
   const int M = jb.M, n = jb.n;
@@ -285,8 +499,13 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
   double* red = dir + 2 * n;                     // 32 (after the two int tables)
   int* ired = reinterpret_cast<int*>(red + 32);  // 32 (+32)
   double* sc = red + 64;                         // shared scalars (8)
-  double* mat = sc + 8;
-  const size_t head = size_t(3 * n + 72);
+  double* F = sc + 8;                            // blocked CPQR: n x kCpqrNb
+  double* aux = F + size_t(kCpqrNb) * n;
+  double* vrow = aux + kCpqrNb;
+  int* bp = reinterpret_cast<int*>(vrow + kCpqrNb);
+  int* rec = bp + kCpqrNb;
+  const size_t head = blocked ? size_t(cpqr_blocked_head(n)) : size_t(3 * n + 72);
+  double* mat = sm + head;
   const bool in_smem = head + size_t(M) * n <= size_t(smem_doubles);
   double* A = jb.a;
   int lda = jb.lda;
@@ -298,8 +517,12 @@ __global__ void __launch_bounds__(kT) qr_kernel(const QrJob* __restrict__ jobs, 
   }
   const int size = min(M, n);
   const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
-  const int done = cpqr_core(A, M, n, lda, jb.pivot != 0, steps_max, jb.stop_eps, jb.perm, jb.diag,
-                             upd, dir, pos, lphys, red, ired, sc);
+  const int done =
+      (blocked && jb.pivot)
+          ? cpqr_core_blocked(A, M, n, lda, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir, pos, lphys, red,
+                              ired, sc, F, aux, vrow, bp, rec)
+          : cpqr_core(A, M, n, lda, jb.pivot != 0, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir, pos,
+                      lphys, red, ired, sc);
   if (tid == 0 && jb.steps) *jb.steps = done;
   if (in_smem) {
     __syncthreads();
@@ -347,7 +570,7 @@ __device__ __forceinline__ void tsqr_reflector(double (&b)[kTsqrRpl], double* R,
   }
 }
 
-__global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restrict__ jobs, int blocked) {
   extern __shared__ double sm[];
   const QrJob jb = jobs[blockIdx.x];
   const int M = jb.M, n = jb.n;
@@ -359,7 +582,12 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   double* red = dir + 2 * n;
   int* ired = reinterpret_cast<int*>(red + 32);
   double* sc = red + 64;
-  double* vb = sc + 8;              // 2 x 128 reflector buffers
+  double* F = sc + 8;               // blocked CPQR: n x kCpqrNb
+  double* aux = F + size_t(kCpqrNb) * n;
+  double* vrow = aux + kCpqrNb;
+  int* bp = reinterpret_cast<int*>(vrow + kCpqrNb);
+  int* rec = bp + kCpqrNb;
+  double* vb = sm + cpqr_blocked_head(n);  // 2 x 128 reflector buffers
   double* tauv = vb + 2 * kTsqrBm;  // 2 (+pad)
   double* R = tauv + 8;             // n x n, ld n
   for (int idx = tid; idx < n * n; idx += kT) R[idx] = 0.0;
@@ -420,8 +648,10 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   }
   __syncthreads();
   const int steps_max = jb.max_steps > 0 ? min(n, jb.max_steps) : n;
-  const int done = cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
-                             pos, lphys, red, ired, sc);
+  const int done = blocked ? cpqr_core_blocked(R, n, n, n, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
+                                               pos, lphys, red, ired, sc, F, aux, vrow, bp, rec)
+                           : cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
+                                       pos, lphys, red, ired, sc);
   if (tid == 0 && jb.steps) *jb.steps = done;
   __syncthreads();
   for (int c = warp; c < n; c += kWarps)
@@ -1745,8 +1975,20 @@ __global__ void add_identity_kernel(double* a, i64 lda, i64 n) {
 
 namespace {
 // Largest TSQR row block that fits next to the n x n factor.
-size_t tsqr_smem(int n) { return size_t(3 * n + 72 + 2 * kTsqrBm + 8 + n * n) * sizeof(double); }
+size_t tsqr_smem(int n) { return size_t(cpqr_blocked_head(n) + 2 * kTsqrBm + 8 + n * n) * sizeof(double); }
 }  // namespace
+
+size_t qr_smem_need(int M, int n, bool blocked) {
+  return (size_t(blocked ? cpqr_blocked_head(n) : 3 * n + 72) + size_t(M) * n) * sizeof(double);
+}
+
+int cpqr_blocked_enabled() {
+  // the blocked loop reads the trailing matrix once per step instead of
+  // three times, but one-CTA CPQR is bound by per-step latency, not shared
+  // memory traffic: measured no faster, so it is opt-in (SBX_CPQR_BLOCKED=1)
+  static const int on = std::getenv("SBX_CPQR_BLOCKED") ? 1 : 0;
+  return on;
+}
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
@@ -1761,7 +2003,7 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   std::vector<QrJob> plain, tall;
   for (const auto& j : jobs) {
     const bool tsqr = j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
-                      (size_t(j.M) * j.n + 3 * j.n + 72) * sizeof(double) > kSmemCap;
+                      qr_smem_need(j.M, j.n, true) > kSmemCap;
     (tsqr ? tall : plain).push_back(j);
   }
   if (!tall.empty()) {
@@ -1769,21 +2011,27 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     for (const auto& j : tall) nmax = std::max(nmax, j.n);
     const size_t smem = tsqr_smem(nmax);
     const QrJob* d = ttab.upload(tall, s);
-    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d);
+    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d, cpqr_blocked_enabled());
     SBX_LAUNCHED();
   }
   if (plain.empty()) return;
+  // the blocked loop's F table (kCpqrNb doubles per column) must fit next
+  // to the norm tables; very wide problems keep the unblocked loop
+  int blk = cpqr_blocked_enabled();
+  for (const auto& j : plain)
+    if (size_t(cpqr_blocked_head(j.n)) * sizeof(double) > kSmemCap) blk = 0;
   size_t need = 0;
   for (const auto& j : plain) {
-    const size_t sz = (size_t(3 * j.n + 72) + size_t(j.M) * j.n) * sizeof(double);
+    const size_t sz = qr_smem_need(j.M, j.n, blk != 0);
     if (sz <= kSmemCap) need = std::max(need, sz);
   }
   size_t base = 0;
-  for (const auto& j : plain) base = std::max(base, size_t(3 * j.n + 72) * sizeof(double));
+  for (const auto& j : plain)
+    base = std::max(base, size_t(blk ? cpqr_blocked_head(j.n) : 3 * j.n + 72) * sizeof(double));
   need = std::max(need, base);
   require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
   const QrJob* d = tab.upload(plain, s);
-  qr_kernel<<<unsigned(plain.size()), kT, need, s>>>(d, int(need / sizeof(double)));
+  qr_kernel<<<unsigned(plain.size()), kT, need, s>>>(d, int(need / sizeof(double)), blk);
   SBX_LAUNCHED();
 }
 

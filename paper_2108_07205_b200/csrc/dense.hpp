@@ -28,6 +28,10 @@ struct QrJob {
   int* steps;     // number of completed steps
 };
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Shared memory qr_batched needs to keep one problem on chip (bytes), and
+// whether the blocked (LAPACK dlaqps-style) CPQR loop is in use.
+size_t qr_smem_need(int M, int n, bool blocked = true);
+int cpqr_blocked_enabled();
 
 // Cooperative CPQR for problems too large for one CTA: the CTAs of a group
 // own disjoint column slabs of A (kept in global memory / L2), recompute the

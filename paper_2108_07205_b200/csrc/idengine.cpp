@@ -60,7 +60,7 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
       // TSQR case); else the on-chip cooperative engine when the slabs fit;
       // else the L2-streaming cooperative engine for big tall problems
       const bool tsqr_ok = pr.n <= 144 && pr.M > pr.n && (pr.M <= tsqr_max_m || (crowded && pr.M <= 4096));
-      const bool one_cta = (i64(pr.M) * pr.n + 3 * pr.n + 72) * 8 <= i64(200 * 1024) || tsqr_ok;
+      const bool one_cta = qr_smem_need(pr.M, pr.n) <= size_t(200 * 1024) || tsqr_ok;
       const int g = cpqr_smem_ctas(pr.M, pr.n);
       static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
       if (one_cta) engine = 1;
