@@ -51,6 +51,7 @@ struct FlowItem {
   int task, row0, ct, ks;
   int nsplit, cidx, kb, ke;
   long long poff;
+  int tile, pad;  // rows of this item
 };
 
 struct SweepLevel {
@@ -71,6 +72,7 @@ struct SweepPlan {
   int flow_key = -1;
   std::vector<int2> level_items;
   DevBuf<FlowItem> d_flow_items;
+  DevBuf<int> d_needs;             // items per task and column tile (dependency counts)
   i64 partial_elems = 0;           // split-K partial tiles (doubles)
   int n_tile_cnt = 0;
   DevBuf<double> d_partials;

@@ -36,18 +36,30 @@ constexpr int kThreads = 256;
 // independent loads in flight per thread.  The first batch of the item's
 // factor block is loaded BEFORE the dependency wait, so on the critical
 // path of the sweep the producers' output and the factor stream overlap.
-constexpr int kGR = 64;                // rows per GEMV item
-constexpr int kGS = kThreads / kGR;    // K slices
-constexpr int kGV = 8;                 // columns per load batch
+constexpr int kGR = 64;                // rows per GEMV item (throughput levels)
+constexpr int kGRs = 16;               // rows per GEMV item on latency-bound levels
 
+// Rows-per-item GR: 64 rows x 4 K-slices streams the big levels with 8
+// loads in flight per thread; 16 rows x 16 K-slices on the short upper
+// levels holds a whole K <= 256 item in registers before the dependency
+// wait, so the critical path only pays the input-vector fetch.
+// One register set serves both shapes (only kGV of the 16 slots are used by
+// the 64-row shape), so the kernel holds a single copy.
+template <int GR>
+struct GemvShape {
+  static constexpr int kGS = kThreads / GR;      // K slices
+  static constexpr int kGV = GR == 64 ? 8 : 16;  // columns prefetched per thread
+};
 struct GemvRegs {
-  double av[kGV];
+  double av[16];
   int j0, j1;
 };
 
+template <int GR>
 __device__ __forceinline__ void gemv_prefetch(const double* __restrict__ fac, const SweepTask& t,
                                               int row0, int kb, int ke, GemvRegs& g) {
-  const int r = threadIdx.x % kGR, slice = threadIdx.x / kGR;
+  constexpr int kGS = GemvShape<GR>::kGS, kGV = GemvShape<GR>::kGV;
+  const int r = threadIdx.x % GR, slice = threadIdx.x / GR;
   const int row = row0 + r;
   const int per = (ke - kb + kGS - 1) / kGS;
   g.j0 = kb + slice * per;
@@ -62,15 +74,17 @@ __device__ __forceinline__ void gemv_prefetch(const double* __restrict__ fac, co
 
 // partial != null: write the item's partial row sums there instead of the
 // final rows (split-K).
+template <int GR>
 __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, double* __restrict__ ws,
                                             const SweepTask& t, int row0, int kb, int ke, const GemvRegs& g,
                                             double* sm, double* partial) {
+  constexpr int kGS = GemvShape<GR>::kGS, kGV = GemvShape<GR>::kGV;
   const int K = t.K;
   double* xs = sm;                    // K doubles
   double* red = sm + ((K + 1) & ~1);  // kThreads partial sums
   for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(ws + t.b_row + j);
   __syncthreads();
-  const int r = threadIdx.x % kGR, slice = threadIdx.x / kGR;
+  const int r = threadIdx.x % GR, slice = threadIdx.x / GR;
   const int row = row0 + r;
   double acc = 0.0, acc1 = 0.0;
 #pragma unroll
@@ -99,7 +113,7 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
   if (slice == 0 && row < t.m) {
     double s = red[r];
 #pragma unroll
-    for (int q = 1; q < kGS; ++q) s += red[r + q * kGR];
+    for (int q = 1; q < kGS; ++q) s += red[r + q * GR];
     if (partial) {
       partial[r] = s;
       return;
@@ -297,10 +311,9 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
                       const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
                       int n_items, int* __restrict__ counters, int ncol, int nrhs, int ldw,
                       double* __restrict__ partials, int* __restrict__ tile_cnt,
-                      unsigned long long* __restrict__ trace) {
+                      unsigned long long* __restrict__ trace, const int* __restrict__ needs) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_next, s_last;
-  constexpr int tile = kDmma ? kTM : kGR;
   constexpr int tile_elems = kDmma ? kTM * TN : kGR;
   int* ticket = counters;  // counters[0]; per-(task, col tile) counts follow
   if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1);
@@ -316,13 +329,16 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     const FlowItem it = items[idx];
     const SweepTask t = tasks[it.task];
     GemvRegs g;
+    const bool small = !kDmma && it.tile == kGRs;
     if constexpr (kDmma)
       dmma_prefetch<TN>(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem<TN>*>(dsm));
+    else if (small)
+      gemv_prefetch<kGRs>(fac, t, it.row0, it.kb, it.ke, g);
     else
-      gemv_prefetch(fac, t, it.row0, it.kb, it.ke, g);
+      gemv_prefetch<kGR>(fac, t, it.row0, it.kb, it.ke, g);
     if (threadIdx.x < t.ndep) {
       const int d = tasks[it.task].dep[threadIdx.x];
-      const int need = (tasks[d].m + tile - 1) / tile;
+      const int need = needs[d];
       const int* p = counters + 1 + d * ncol + it.ct;
       while (ld_acquire(p) < need) __nanosleep(32);
     }
@@ -332,8 +348,10 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     if constexpr (kDmma)
       dmma_item<TN>(fac, ws, t, it.row0, it.ct * TN, nrhs, ldw, it.kb, it.ke,
                     *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
+    else if (small)
+      gemv_finish<kGRs>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
     else
-      gemv_finish(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
+      gemv_finish<kGR>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
     __syncthreads();  // the item's stores happen-before thread 0's release below
     bool done = true;
     if (it.nsplit > 1) {  // last split of the tile reduces the partials in split order
@@ -398,8 +416,8 @@ __global__ void __launch_bounds__(kThreads)
   const int4 it = make_int4(f.task, f.row0, f.ct, 0);
   const SweepTask t = tasks[it.x];
   GemvRegs g;
-  gemv_prefetch(fac, t, it.y, 0, t.K, g);
-  gemv_finish(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr);
+  gemv_prefetch<kGR>(fac, t, it.y, 0, t.K, g);
+  gemv_finish<kGR>(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr);
 }
 
 template <int TN>
@@ -465,17 +483,23 @@ namespace {
 // tile, then K split.  Levels with too few tiles to fill the GPU split K so
 // the short upper levels of the tree (the sweep's critical path) spread
 // over more CTAs.  Returns per-level [first, count).
-std::vector<FlowItem> make_items(SweepPlan& plan, int tile, int ncol, int tile_elems, int target,
-                                 std::vector<int2>* ranges, i64* partial_elems, int* n_tile_cnt) {
+std::vector<FlowItem> make_items(SweepPlan& plan, int tile0, int ncol, int tile_elems, int target,
+                                 std::vector<int2>* ranges, i64* partial_elems, int* n_tile_cnt,
+                                 std::vector<int>* needs, int small_tile, i64 small_below) {
   std::vector<FlowItem> fi;
+  needs->assign(size_t(plan.n_tasks), 0);
   i64 poff = 0;
   int cidx = 0;
   for (auto& L : plan.levels) {
     const i64 first = i64(fi.size());
     i64 base = 0;
-    for (const auto& tk : L.tasks) base += (tk.m + tile - 1) / tile;
+    for (const auto& tk : L.tasks) base += (tk.m + tile0 - 1) / tile0;
     base *= ncol;
-    const int lsplit = target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base)) : 1;
+    // short levels (the tree's critical path) take smaller row tiles
+    const int tile = (small_tile > 0 && base < small_below) ? small_tile : tile0;
+    const int lsplit_ok = tile == tile0;
+    const int lsplit =
+        lsplit_ok && target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base)) : 1;
     for (int ct = 0; ct < ncol; ++ct)
       for (size_t t = 0; t < L.tasks.size(); ++t) {
         const auto& tk = L.tasks[t];
@@ -483,6 +507,7 @@ std::vector<FlowItem> make_items(SweepPlan& plan, int tile, int ncol, int tile_e
         // split boundaries on multiples of 16 (the DMMA K chunk)
         const int per = ((tk.K + ns - 1) / ns + 15) / 16 * 16;
         const int nsplit = std::max(1, (tk.K + per - 1) / std::max(per, 1));
+        (*needs)[size_t(L.first_task + i64(t))] = (tk.m + tile - 1) / tile;
         for (int r0 = 0; r0 < tk.m; r0 += tile) {
           for (int ks = 0; ks < nsplit; ++ks) {
             FlowItem f{};
@@ -495,6 +520,7 @@ std::vector<FlowItem> make_items(SweepPlan& plan, int tile, int ncol, int tile_e
             f.ke = std::min(tk.K, (ks + 1) * per);
             f.cidx = nsplit > 1 ? cidx : -1;
             f.poff = nsplit > 1 ? poff : 0;
+            f.tile = tile;
             fi.push_back(f);
           }
           if (nsplit > 1) {
@@ -894,10 +920,12 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
   const int key = ((ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0)) * 128 + TN;
   if (plan.flow_key != key) {
     plan.level_items.clear();
+    std::vector<int> needs;
     const std::vector<FlowItem> fi =
         make_items(plan, tile, ncol, dmma ? kTM * TN : kGR, target, &plan.level_items, &plan.partial_elems,
-                   &plan.n_tile_cnt);
+                   &plan.n_tile_cnt, &needs, (dmma || per_level) ? 0 : kGRs, 600);
     plan.d_flow_items.upload(fi, s);
+    plan.d_needs.upload(needs, s);
     plan.n_flow_items = i64(fi.size());
     plan.flow_key = key;
   }
@@ -928,12 +956,13 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
     sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
                                                              int(plan.n_flow_items), plan.d_counters.get(), ncol,
                                                              int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
-                                                             tile_cnt, trace.get());
+                                                             tile_cnt, trace.get(), plan.d_needs.get());
   else
     sweep_flow_kernel<false, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
                                                               plan.d_flow_items.get(), int(plan.n_flow_items),
                                                               plan.d_counters.get(), ncol, int(nrhs), 1,
-                                                              plan.d_partials.get(), tile_cnt, trace.get());
+                                                              plan.d_partials.get(), tile_cnt, trace.get(),
+                                                              plan.d_needs.get());
   SBX_LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(size_t(4 * plan.n_flow_items));
