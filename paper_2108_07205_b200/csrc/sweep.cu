@@ -161,14 +161,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int TN>
+template <int TN, int TM = kTM>
 __device__ __forceinline__ void dmma_issue_a(const double* __restrict__ fac, const SweepTask& t, int row0,
                                              int stage, int k0, int ke, DmmaSmem<TN>& S) {
   const double* A = fac + t.a_off;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int idx = threadIdx.x + q * kThreads;  // 0..1023
-    const int kk = idx >> 6, rr = idx & 63;
+  for (int q = 0; q < TM / 16; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // TM x 16
+    const int kk = idx / TM, rr = idx % TM;
     const int grow = row0 + rr, gk = k0 + kk;
     const bool pa = grow < t.m && gk < ke;
     cp_async8(&S.As[stage][kk][rr], pa ? A + grow + size_t(gk) * t.lda : A, pa);
@@ -193,26 +193,28 @@ __device__ __forceinline__ void dmma_issue_b(const double* __restrict__ ws, cons
 
 // Issues the A parts of the first kStages-1 chunks (call before waiting on
 // the producers of B); they join the first commit group.
-template <int TN>
+template <int TN, int TM = kTM>
 __device__ __forceinline__ void dmma_prefetch(const double* __restrict__ fac, const SweepTask& t, int row0,
                                               int kb, int ke, DmmaSmem<TN>& S) {
   const int nchunks = (ke - kb + kKC - 1) / kKC;
 #pragma unroll
   for (int c = 0; c < kStages - 1; ++c)
-    if (c < nchunks) dmma_issue_a(fac, t, row0, c, kb + c * kKC, ke, S);
+    if (c < nchunks) dmma_issue_a<TN, TM>(fac, t, row0, c, kb + c * kKC, ke, S);
 }
 
 // partial != null: write the raw 64 x 64 tile there (row-major) instead of
 // the final rows (split-K).
-template <int TN>
+template <int TN, int TM = kTM>
 __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double* __restrict__ ws,
                                           const SweepTask& t, int row0, int col0, int nrhs, int ldw,
                                           int kb, int ke, DmmaSmem<TN>& S, double* partial) {
-  constexpr int NB = TN / 16;  // 8-column blocks per warp (warps: 4 row x 2 column groups)
+  constexpr int RG = TM / 16;      // warp row groups (16 rows each)
+  constexpr int CG = 8 / RG;       // warp column groups
+  constexpr int NB = TN / CG / 8;  // 8-column blocks per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int wm = (warp & 3) * 16;
-  const int wn = (warp >> 2) * (TN / 2);
+  const int wm = (warp % RG) * 16;
+  const int wn = (warp / RG) * (TN / CG);
   double c[2][NB][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -242,7 +244,7 @@ __device__ __forceinline__ void dmma_item(const double* __restrict__ fac, double
     __syncthreads();  // chunk ch visible; stage (ch-1) % kStages is free
     const int nx = ch + kStages - 1;
     if (nx < nchunks) {
-      dmma_issue_a(fac, t, row0, nx % kStages, kb + nx * kKC, ke, S);
+      dmma_issue_a<TN, TM>(fac, t, row0, nx % kStages, kb + nx * kKC, ke, S);
       dmma_issue_b(ws, t, col0, nrhs, ldw, nx % kStages, kb + nx * kKC, ke, S);
     }
     cp_async_commit();
@@ -329,10 +331,13 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     const FlowItem it = items[idx];
     const SweepTask t = tasks[it.task];
     GemvRegs g;
-    const bool small = !kDmma && it.tile == kGRs;
-    if constexpr (kDmma)
-      dmma_prefetch<TN>(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem<TN>*>(dsm));
-    else if (small)
+    const bool small = it.tile != (kDmma ? kTM : kGR);
+    if constexpr (kDmma) {
+      if (small)
+        dmma_prefetch<TN, 32>(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem<TN>*>(dsm));
+      else
+        dmma_prefetch<TN>(fac, t, it.row0, it.kb, it.ke, *reinterpret_cast<DmmaSmem<TN>*>(dsm));
+    } else if (small)
       gemv_prefetch<kGRs>(fac, t, it.row0, it.kb, it.ke, g);
     else
       gemv_prefetch<kGR>(fac, t, it.row0, it.kb, it.ke, g);
@@ -345,9 +350,14 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     __syncthreads();
     if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     double* part = it.nsplit > 1 ? partials + it.poff + i64(it.ks) * tile_elems : nullptr;
-    if constexpr (kDmma)
-      dmma_item<TN>(fac, ws, t, it.row0, it.ct * TN, nrhs, ldw, it.kb, it.ke,
-                    *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
+    if constexpr (kDmma) {
+      if (small)
+        dmma_item<TN, 32>(fac, ws, t, it.row0, it.ct * TN, nrhs, ldw, it.kb, it.ke,
+                          *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
+      else
+        dmma_item<TN>(fac, ws, t, it.row0, it.ct * TN, nrhs, ldw, it.kb, it.ke,
+                      *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
+    }
     else if (small)
       gemv_finish<kGRs>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
     else
@@ -917,13 +927,22 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
     return e ? std::atoi(e) : 64;
   }();
   const int target = (per_level || split_env == 0) ? 0 : split_target;
+  static const int dmma_small = [] {  // 32-row DMMA tiles on short levels (SBX_SWEEP_DMMA_SMALL=0 disables)
+    const char* e = std::getenv("SBX_SWEEP_DMMA_SMALL");
+    return (e && std::atoi(e) == 0) ? 0 : 32;
+  }();
+  static const int small_below_dmma = [] {
+    const char* e = std::getenv("SBX_SWEEP_DMMA_SMALL_BELOW");
+    return e ? std::atoi(e) : 300;
+  }();
   const int key = ((ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0)) * 128 + TN;
   if (plan.flow_key != key) {
     plan.level_items.clear();
     std::vector<int> needs;
     const std::vector<FlowItem> fi =
         make_items(plan, tile, ncol, dmma ? kTM * TN : kGR, target, &plan.level_items, &plan.partial_elems,
-                   &plan.n_tile_cnt, &needs, (dmma || per_level) ? 0 : kGRs, 600);
+                   &plan.n_tile_cnt, &needs, per_level ? 0 : (dmma ? dmma_small : kGRs),
+                   dmma ? small_below_dmma : 600);
     plan.d_flow_items.upload(fi, s);
     plan.d_needs.upload(needs, s);
     plan.n_flow_items = i64(fi.size());
