@@ -1,5 +1,6 @@
 // ELS / Woodbury build and solve on the device (reference els.cpp:25-203).
 #include "els.hpp"
+#include "idengine.hpp"
 
 #include <cmath>
 #include <limits>
@@ -104,6 +105,7 @@ std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan,
     HbsBuildOptions o;
     o.eps = eps;
     a->h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()), o, s);
+    id_rendezvous_leave();  // no factorisations below (joint CPQR launches, update.cpp)
     hbs_invert_device(*a->h, s);
     hbs_build_solve_plan(*a->h);
   }

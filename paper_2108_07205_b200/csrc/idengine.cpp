@@ -6,8 +6,118 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <condition_variable>
+#include <mutex>
 
 namespace sbx {
+
+namespace {
+thread_local IdRendezvous* tl_rv = nullptr;
+
+int sm_count() {
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
+}  // namespace
+
+// Engine routing and launches for one batch of CPQR jobs (engine: 0 auto).
+void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
+  std::vector<QrJob> jobs, big, chip, clus;
+  static const int tsqr_max_m = [] {
+    const char* e = std::getenv("SBX_TSQR_MAXM");
+    return e ? std::atoi(e) : 0;
+  }();
+  // Large batches have enough independent problems to fill the GPU with one
+  // CTA each; cross-CTA engines only pay off when problems are few.  Count
+  // the CTAs the cluster engine would need for the whole batch.
+  const int sms = sm_count();
+  i64 cluster_ctas = 0;
+  for (const auto& j : all) cluster_ctas += std::max(1, cpqr_cluster_size(j.M, j.n));
+  const bool crowded = cluster_ctas > 2 * i64(sms);
+  static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
+  std::string line;
+  for (const auto& j : all) {
+    int engine = force_engine;
+    if (engine == 0) {
+      // one CTA when the problem fits its shared memory (or is a short, tall
+      // TSQR case); else a thread-block cluster, else the on-chip cooperative
+      // engine when the slabs fit the GPU, else the L2-streaming cooperative
+      // engine for big problems
+      const bool tsqr_ok = j.n <= 144 && j.M > j.n && (j.M <= tsqr_max_m || (crowded && j.M <= 4096));
+      const bool one_cta = qr_smem_need(j.M, j.n) <= size_t(200 * 1024) || tsqr_ok;
+      const int g = cpqr_smem_ctas(j.M, j.n);
+      static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
+      if (one_cta) engine = 1;
+      else if (!no_cluster && cpqr_cluster_size(j.M, j.n) > 0) engine = 4;
+      else if (no_coop_flag()) engine = 1;  // beside other streams: no grid-wide barriers
+      else if (g > 0 && g <= sms) engine = 3;
+      else if (i64(j.M) * j.n >= IdBatch::kCoopEntries) engine = 2;
+      else engine = 1;
+    }
+    if (log) line += " " + std::to_string(j.M) + "x" + std::to_string(j.n) + "/e" + std::to_string(engine);
+    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : jobs).push_back(j);
+  }
+  if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
+  qr_batched(jobs, s);
+  cpqr_coop_batched(big, s);
+  cpqr_smem_batched(chip, s);
+  cpqr_cluster_batched(clus, s);
+}
+
+// ---------------------------------------------------------------- rendezvous
+IdRendezvous::IdRendezvous(int participants) : active_(participants) {}
+
+void IdRendezvous::flush_locked(cudaStream_t s) {
+  std::vector<QrJob> merged;
+  for (auto* v : pending_) merged.insert(merged.end(), v->begin(), v->end());
+  launch_id_jobs(merged, 0, s);
+  pending_.clear();
+  waiting_ = 0;
+  ++generation_;
+  cv_.notify_all();
+}
+
+void IdRendezvous::submit(std::vector<QrJob>& jobs, cudaStream_t s) {
+  std::unique_lock<std::mutex> lk(mu_);
+  pending_.push_back(&jobs);
+  ++waiting_;
+  last_stream_ = s;
+  if (waiting_ >= active_) {
+    flush_locked(s);
+    return;
+  }
+  const unsigned long long gen = generation_;
+  cv_.wait(lk, [&] { return generation_ != gen; });
+}
+
+void IdRendezvous::leave() {
+  std::lock_guard<std::mutex> lk(mu_);
+  --active_;
+  if (waiting_ > 0 && waiting_ >= active_) flush_locked(last_stream_);
+}
+
+IdRendezvousScope::IdRendezvousScope(IdRendezvous* rv) : rv_(rv), prev_(tl_rv) { tl_rv = rv; }
+IdRendezvousScope::~IdRendezvousScope() { leave(); }
+void IdRendezvousScope::leave() {
+  if (rv_) {
+    rv_->leave();
+    rv_ = nullptr;
+    tl_rv = prev_;
+  }
+}
+
+void id_rendezvous_leave() {
+  if (tl_rv) {
+    IdRendezvous* rv = tl_rv;
+    tl_rv = nullptr;
+    rv->leave();
+  }
+}
 
 void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s) {
   probs_ = probs;
@@ -21,25 +131,7 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
   d_perm_.reserve(size_t(std::max<i64>(perm_off_[np], 1)));
   d_diag_.reserve(size_t(std::max<i64>(diag_off[np], 1)));
   d_steps_.reserve(std::max<size_t>(np, 1));
-  std::vector<QrJob> jobs, big, chip, clus;
-  coop_.assign(np, 0);
-  static const int tsqr_max_m = [] {
-    const char* e = std::getenv("SBX_TSQR_MAXM");
-    return e ? std::atoi(e) : 0;
-  }();
-  // Large batches have enough independent problems to fill the GPU with one
-  // CTA each; cross-CTA engines only pay off when problems are few.  Count
-  // the CTAs the cluster engine would need for the whole batch.
-  static const int sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  i64 cluster_ctas = 0;
-  for (const auto& pr : probs)
-    if (pr.M > 0 && pr.n > 0) cluster_ctas += std::max(1, cpqr_cluster_size(pr.M, pr.n));
-  const bool crowded = cluster_ctas > 2 * i64(sms);
+  std::vector<QrJob> jobs;
   for (size_t p = 0; p < np; ++p) {
     const auto& pr = probs[p];
     if (pr.M == 0 || pr.n == 0) continue;
@@ -54,37 +146,12 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
     j.perm = d_perm_.get() + perm_off_[p];
     j.diag = d_diag_.get() + diag_off[p];
     j.steps = d_steps_.get() + p;
-    int engine = force_engine;
-    if (engine == 0) {
-      // one CTA when the problem fits its shared memory (or is a short, tall
-      // TSQR case); else the on-chip cooperative engine when the slabs fit;
-      // else the L2-streaming cooperative engine for big tall problems
-      const bool tsqr_ok = pr.n <= 144 && pr.M > pr.n && (pr.M <= tsqr_max_m || (crowded && pr.M <= 4096));
-      const bool one_cta = qr_smem_need(pr.M, pr.n) <= size_t(200 * 1024) || tsqr_ok;
-      const int g = cpqr_smem_ctas(pr.M, pr.n);
-      static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
-      if (one_cta) engine = 1;
-      else if (!no_cluster && cpqr_cluster_size(pr.M, pr.n) > 0) engine = 4;
-      else if (no_coop_flag()) engine = 1;  // beside other streams: no grid-wide barriers
-      else if (g > 0 && g <= sms) engine = 3;
-      else if (i64(pr.M) * pr.n >= kCoopEntries) engine = 2;
-      else engine = 1;
-    }
-    coop_[p] = char(engine);
-    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : jobs).push_back(j);
+    jobs.push_back(j);
   }
-  static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
-  if (log) {
-    std::string line = "[sbx-id] eps " + std::to_string(stop_eps) + ":";
-    for (size_t p = 0; p < np; ++p)
-      line += " " + std::to_string(probs[p].M) + "x" + std::to_string(probs[p].n) + "/e" +
-              std::to_string(int(coop_[p]));
-    std::fprintf(stderr, "%s\n", line.c_str());
-  }
-  qr_batched(jobs, s);
-  cpqr_coop_batched(big, s);
-  cpqr_smem_batched(chip, s);
-  cpqr_cluster_batched(clus, s);
+  if (tl_rv && force_engine == 0)
+    tl_rv->submit(jobs, s);  // one joint launch with the other participants' batches
+  else
+    launch_id_jobs(jobs, force_engine, s);
   std::vector<int> hperm(static_cast<size_t>(perm_off_[np]));
   std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
   if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);

@@ -4,6 +4,8 @@
 // the reference's rules, then P = [I; R11^{-1} R12] scattered by the pivots.
 #pragma once
 
+#include <condition_variable>
+#include <mutex>
 #include <vector>
 
 #include "common.hpp"
@@ -40,7 +42,6 @@ class IdBatch {
   static constexpr i64 kCoopEntries = i64(1) << 18;  // 2 MB of W^T
 
  private:
-  std::vector<char> coop_;
   std::vector<IdProblem> probs_;
   std::vector<std::vector<double>> diag_;
   std::vector<std::vector<int>> perm_;
@@ -50,5 +51,49 @@ class IdBatch {
   DevBuf<int> d_steps_;
   DevBuf<double> d_T_;
 };
+
+// Engine routing + launches of one batch of CPQR jobs (force_engine 0: auto).
+void launch_id_jobs(const std::vector<QrJob>& jobs, int force_engine, cudaStream_t s);
+
+// Joint CPQR launches across independent algorithms running in separate host
+// threads on ONE stream: every IdBatch::factor of a participating thread
+// waits until each still-active participant has submitted its batch, then a
+// single launch factors all of them (the update's row-ID hierarchies and the
+// A_pp HBS build advance level by level together instead of one after the
+// other).  A participant that has no more factorisations must leave().
+class IdRendezvous {
+ public:
+  explicit IdRendezvous(int participants);
+  void submit(std::vector<QrJob>& jobs, cudaStream_t s);
+  void leave();
+
+ private:
+  void flush_locked(cudaStream_t s);
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int active_ = 0, waiting_ = 0;
+  unsigned long long generation_ = 0;
+  std::vector<std::vector<QrJob>*> pending_;
+  cudaStream_t last_stream_ = nullptr;
+};
+
+// Installs a rendezvous for the calling thread's IdBatch::factor calls;
+// leaves it (at the latest) on destruction.
+class IdRendezvousScope {
+ public:
+  explicit IdRendezvousScope(IdRendezvous* rv);
+  ~IdRendezvousScope();
+  void leave();
+  IdRendezvousScope(const IdRendezvousScope&) = delete;
+  IdRendezvousScope& operator=(const IdRendezvousScope&) = delete;
+
+ private:
+  IdRendezvous* rv_;
+  IdRendezvous* prev_;
+};
+
+// Leaves the calling thread's rendezvous, if any (a producer whose remaining
+// work has no factorisations).
+void id_rendezvous_leave();
 
 }  // namespace sbx

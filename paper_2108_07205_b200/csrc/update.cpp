@@ -18,6 +18,8 @@
 #include <functional>
 #include <numeric>
 #include <set>
+#include <thread>
+#include <memory>
 
 #include "dense.hpp"
 #include "els.hpp"
@@ -44,53 +46,62 @@ struct Chunk {
   i64 k = 0;
 };
 
+// One hierarchy of row IDs: m rows cut into leaves, W^T built by `build`.
+struct HierSpec {
+  i64 m = 0;
+  std::vector<std::vector<i64>> leaves;
+  WtBuilder build;
+};
+
 // hierarchical_row_id (proxy.cpp:193-247) / chunked near_row_id
 // (lowrank.cpp:76-124): leaf IDs, then pairwise merges of skeleton rows.
-// Several independent hierarchies over the same leaves (one W^T builder
-// each, e.g. two proxy sample counts) advance in lockstep so every level
-// is one batched CPQR launch.
-std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vector<i64>>& leaves,
-                                               const std::vector<WtBuilder>& builds, double eps,
+// Independent hierarchies (the far-field IDs at two proxy sample counts,
+// the near-field blocks, ...) advance in lockstep: every tree level of all
+// of them is one batched CPQR, so the step pays max(depth) dependent levels
+// instead of the sum.
+std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& specs, double eps,
                                                cudaStream_t s) {
-  const size_t H = builds.size();
+  const size_t H = specs.size();
   std::vector<std::unique_ptr<DevBuf<double>>> keep;
   std::vector<std::vector<Chunk>> level(H);
   // leaves
   {
     std::vector<IdProblem> all;
+    std::vector<std::pair<size_t, size_t>> who;  // problem -> (hierarchy, leaf)
     for (size_t h = 0; h < H; ++h) {
+      if (specs[h].leaves.empty()) continue;
       std::vector<IdProblem> probs;
       auto buf = std::make_unique<DevBuf<double>>();
-      builds[h](leaves, probs, *buf);
+      specs[h].build(specs[h].leaves, probs, *buf);
+      for (size_t q = 0; q < probs.size(); ++q) who.push_back({h, q});
       all.insert(all.end(), probs.begin(), probs.end());
       keep.push_back(std::move(buf));
     }
     IdBatch ids;
     ids.factor(all, eps, s);
-    const size_t L = leaves.size();
     std::vector<i64> ks(all.size()), off(all.size());
     i64 tot = 0;
     for (size_t p = 0; p < all.size(); ++p) {
       ks[p] = ids.eps_rank(p, eps);
       off[p] = tot;
-      tot += i64(leaves[p % L].size()) * ks[p];
+      tot += i64(specs[who[p].first].leaves[who[p].second].size()) * ks[p];
     }
     auto pb = std::make_unique<DevBuf<double>>(size_t(std::max<i64>(tot, 1)));
     std::vector<double*> P(all.size());
     std::vector<int> ldp(all.size());
     for (size_t p = 0; p < all.size(); ++p) {
       P[p] = pb->get() + off[p];
-      ldp[p] = std::max<int>(1, int(leaves[p % L].size()));
+      ldp[p] = std::max<int>(1, int(specs[who[p].first].leaves[who[p].second].size()));
     }
     ids.interp(ks, P, ldp, s);
     for (size_t p = 0; p < all.size(); ++p) {
-      const size_t q = p % L;
+      const auto& lf = specs[who[p].first].leaves[who[p].second];
       Chunk c;
-      c.rows = leaves[q];
+      c.rows = lf;
       c.k = ks[p];
-      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(leaves[q][size_t(ids.perm(p)[size_t(i)])]);
+      for (i64 i = 0; i < c.k; ++i) c.skel.push_back(lf[size_t(ids.perm(p)[size_t(i)])]);
       c.P = P[p];
-      level[p / L].push_back(std::move(c));
+      level[who[p].first].push_back(std::move(c));
     }
     keep.push_back(std::move(pb));
     phase_mark("  hier: leaves", s);
@@ -114,7 +125,7 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
       if (npair == 0) continue;
       std::vector<IdProblem> probs;
       auto buf = std::make_unique<DevBuf<double>>();
-      builds[h](unis[h], probs, *buf);
+      specs[h].build(unis[h], probs, *buf);
       all.insert(all.end(), probs.begin(), probs.end());
       keep.push_back(std::move(buf));
     }
@@ -179,6 +190,7 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
   std::vector<RowIdResult> outs(H);
   for (size_t h = 0; h < H; ++h) {
     RowIdResult& out = outs[h];
+    const i64 m = specs[h].m;
     out.m = m;
     if (level[h].empty()) {
       out.J.resize(size_t(m));
@@ -207,7 +219,7 @@ std::vector<RowIdResult> hierarchical_id_multi(i64 m, const std::vector<std::vec
 
 RowIdResult hierarchical_id(i64 m, const std::vector<std::vector<i64>>& leaves,
                             const WtBuilder& build, double eps, cudaStream_t s) {
-  auto r = hierarchical_id_multi(m, leaves, {build}, eps, s);
+  auto r = hierarchical_id_multi({HierSpec{m, leaves, build}}, eps, s);
   return std::move(r[0]);
 }
 
@@ -360,9 +372,8 @@ RowIdResult compress_block_far(const EntryView& v, const Geom& g, const std::vec
   }
   const double factor = basis ? bas : div;
   // 64 and 128 samples are always both computed (proxy.cpp:289-300): one batch
-  auto two = hierarchical_id_multi(m, leaves,
-                                   {proxy_builder(v, nodes, circles, factor, 64, with_null, s),
-                                    proxy_builder(v, nodes, circles, factor, 128, with_null, s)},
+  auto two = hierarchical_id_multi({HierSpec{m, leaves, proxy_builder(v, nodes, circles, factor, 64, with_null, s)},
+                                    HierSpec{m, leaves, proxy_builder(v, nodes, circles, factor, 128, with_null, s)}},
                                    eps, s);
   bool settled = std::llabs(two[1].k - two[0].k) <= 2;
   RowIdResult prev = std::move(two[1]);
@@ -397,6 +408,74 @@ RowIdResult near_row_id(const EntryView& v, const std::vector<i64>& rowsc,
     leaves.push_back(std::move(l));
   }
   return hierarchical_id(nr, leaves, b, eps, s);
+}
+
+// compress_block_far split for the lockstep driver: validation and the two
+// first hierarchies (64 and 128 samples), then the doubling loop on the
+// results (proxy.cpp:251-302).
+struct FarPrep {
+  bool basis = true;
+  double factor = 1.5;
+  i64 m = 0;
+  std::vector<std::vector<i64>> leaves;
+};
+FarPrep far_prepare(const Geom& g, const std::vector<i64>& nodes, const std::vector<ProxyCircleH>& circles,
+                    bool basis, const std::vector<std::vector<i64>>& tree_leaves) {
+  const double div = 3.0;
+  require(!circles.empty(), "proxy geometry has no circles");
+  for (i64 nd : nodes) {
+    const bool in_div = inside_any_div(circles, div, g.x[size_t(nd)], g.y[size_t(nd)]);
+    if (basis && in_div) throw Error(5, "far row point inside a division circle");
+    if (!basis && !in_div) throw Error(5, "row point outside every division circle");
+  }
+  FarPrep f;
+  f.basis = basis;
+  f.factor = basis ? 1.5 : div;
+  f.m = 2 * i64(nodes.size());
+  if (nodes.empty()) return f;
+  for (const auto& lf : tree_leaves) {
+    std::vector<i64> rows;
+    for (i64 p : lf) {
+      rows.push_back(2 * p);
+      rows.push_back(2 * p + 1);
+    }
+    f.leaves.push_back(std::move(rows));
+  }
+  return f;
+}
+
+RowIdResult far_settle(const EntryView& v, const std::vector<i64>& nodes, const std::vector<ProxyCircleH>& circles,
+                       bool with_null, const FarPrep& f, RowIdResult r64, RowIdResult r128, double eps,
+                       cudaStream_t s) {
+  if (f.leaves.empty()) return RowIdResult{};
+  bool settled = std::llabs(r128.k - r64.k) <= 2;
+  RowIdResult prev = std::move(r128);
+  for (int n = 256; !settled && n <= 2048; n *= 2) {
+    RowIdResult cur =
+        hierarchical_id(f.m, f.leaves, proxy_builder(v, nodes, circles, f.factor, n, with_null, s), eps, s);
+    settled = std::llabs(cur.k - prev.k) <= 2;
+    prev = std::move(cur);
+  }
+  return prev;
+}
+
+// near_row_id as a hierarchy spec: one leaf (direct ID) up to 2^22 entries,
+// else 256-row chunks (lowrank.cpp:62-125).
+HierSpec near_spec(const EntryView& v, const std::vector<i64>& rowsc, const std::vector<i64>& colsc,
+                   std::vector<std::string>& notes, const char* tag, cudaStream_t s) {
+  HierSpec h;
+  const i64 nr = i64(rowsc.size()), ncl = i64(colsc.size());
+  h.m = nr;
+  if (nr == 0 || ncl == 0) return h;
+  h.build = entry_builder(v, rowsc, colsc, s);
+  const i64 chunk = nr * ncl <= (i64(1) << 22) ? nr : 256;
+  if (chunk < nr) notes.push_back(std::string(tag) + ": near block over memory budget, using row partition");
+  for (i64 st = 0; st < nr; st += chunk) {
+    std::vector<i64> l;
+    for (i64 r = st; r < std::min(st + chunk, nr); ++r) l.push_back(r);
+    h.leaves.push_back(std::move(l));
+  }
+  return h;
 }
 
 std::vector<i64> scalars(const std::vector<i64>& nodes) {
@@ -576,13 +655,70 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     const char* e = std::getenv("SBX_PAR_MODE");
     return e ? std::atoi(e) : 2;
   }();
-  if (par_mode == 2) {
-    t_far(s);
-    t_kc(s);
-    t_kp(s);
-    t_pk_far(s);
-    t_pk_near(s);
-    t_app(s);
+  if (par_mode == 2 || par_mode == 4) {
+    // mode 4: the A_pp HBS build runs in a second host thread on the SAME
+    // stream; its factorisations and the update's share joint CPQR launches
+    // through a rendezvous until one side has no more of them
+    std::unique_ptr<IdRendezvous> rv;
+    std::thread app_thread;
+    std::exception_ptr app_err;
+    if (par_mode == 4 && !plan.added_new.empty()) {
+      rv = std::make_unique<IdRendezvous>(2);
+      int dev = 0;
+      SBX_CUDA(cudaGetDevice(&dev));
+      app_thread = std::thread([&, dev] {
+        try {
+          SBX_CUDA(cudaSetDevice(dev));
+          StreamScope ss(s);
+          IdRendezvousScope rs(rv.get());
+          phase_mark(nullptr, s);
+          t_app(s);
+        } catch (...) {
+          app_err = std::current_exception();
+        }
+      });
+    }
+    IdRendezvousScope main_rs(rv.get());
+    // every row-ID hierarchy of the update advances in lockstep (one batched
+    // CPQR per tree level across all of them)
+    std::vector<std::vector<i64>> ptree;
+    for (size_t st = 0; st < plan.added_new.size(); st += 128) {
+      std::vector<i64> l;
+      for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
+      ptree.push_back(std::move(l));
+    }
+    const FarPrep fk = far_prepare(ng, far_nodes, circles, true, ktree);
+    FarPrep fp;
+    if (!plan.added_new.empty()) fp = far_prepare(ng, plan.added_new, circles, false, ptree);
+    const std::vector<i64> kc_rows = do_kc ? mapped(kept_old_s, near_s) : std::vector<i64>{};
+    const std::vector<i64> kp_rows = do_kp ? mapped(kept_new_s, near_s) : std::vector<i64>{};
+    const std::vector<i64> pk_cols = do_pk_near ? mapped(kept_new_s, near_s) : std::vector<i64>{};
+    std::vector<HierSpec> specs;
+    specs.push_back({fk.m, fk.leaves, proxy_builder(enew.view(), far_nodes, circles, fk.factor, 64, with_null, s)});
+    specs.push_back({fk.m, fk.leaves, proxy_builder(enew.view(), far_nodes, circles, fk.factor, 128, with_null, s)});
+    specs.push_back({fp.m, fp.leaves,
+                     proxy_builder(enew.view(), plan.added_new, circles, fp.factor, 64, with_null, s)});
+    specs.push_back({fp.m, fp.leaves,
+                     proxy_builder(enew.view(), plan.added_new, circles, fp.factor, 128, with_null, s)});
+    specs.push_back(near_spec(eold.view(), kc_rows, cut_s, notes_kc, "kc", s));
+    specs.push_back(near_spec(enew.view(), kp_rows, added_s, notes_kp, "kp", s));
+    specs.push_back(near_spec(enew.view(), added_s, pk_cols, notes_pk, "pk", s));
+    auto res = hierarchical_id_multi(specs, eps, s);
+    phase_mark("update: lockstep row IDs", s);
+    far = far_settle(enew.view(), far_nodes, circles, with_null, fk, std::move(res[0]), std::move(res[1]), eps, s);
+    if (!plan.added_new.empty())
+      pk_far = far_settle(enew.view(), plan.added_new, circles, with_null, fp, std::move(res[2]), std::move(res[3]),
+                          eps, s);
+    kc_near = std::move(res[4]);
+    kp_near = std::move(res[5]);
+    pk_near = std::move(res[6]);
+    main_rs.leave();
+    if (app_thread.joinable()) {
+      app_thread.join();
+      if (app_err) std::rethrow_exception(app_err);
+    } else {
+      t_app(s);
+    }
   } else if (par_mode == 3) {
     t_kc(s);
     t_kp(s);
