@@ -212,7 +212,9 @@ int64_t sbx_kernel_launches(int reset);
 /* Device row ID of a host matrix W (m x n, column-major) — idlib.cpp:73-99
  * (row_id; forced >= 0 selects row_id_rank).  engine: 0 auto, 1 one CTA per
  * problem, 2 cooperative multi-CTA (slabs in L2), 3 cooperative on chip
- * (slabs in shared memory).  J: m entries, P: m*min(m,n) doubles. */
+ * (slabs in shared memory), 4 one thread-block cluster per problem (slabs in
+ * shared memory), 5 one cluster per problem with the slab in registers.
+ * J: m entries, P: m*min(m,n) doubles. */
 int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
                int64_t* k, int64_t* J, double* P);
 

@@ -122,27 +122,48 @@ __device__ __forceinline__ void reflect_cols(double* const (&col)[U], const int 
     __syncwarp();
   }
   if (!pivot) return;
+  // lane u downdates slot u (same arithmetic as one column at a time); the
+  // rare recomputations from the remaining rows take the whole warp
+  const double* mc = nullptr;
+  int ms = 0;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    if (!col[u]) continue;
-    const double uu = upd[slot[u]];
-    __syncwarp();  // every lane has read upd before lane 0 rewrites it
-    if (uu == 0.0) continue;
-    double t = fabs(col[u][j]) / uu;
-    t = (1.0 + t) * (1.0 - t);
-    t = t < 0.0 ? 0.0 : t;
-    const double rr = uu / dir[slot[u]];
-    if (t * rr * rr <= thr) {
-      double sacc = 0.0;
-      for (int i = j + 1 + lane; i < M; i += 32) sacc += col[u][i] * col[u][i];
-      sacc = warp_sum(sacc);
-      __syncwarp();
-      if (lane == 0) upd[slot[u]] = dir[slot[u]] = sqrt(sacc);
-    } else if (lane == 0) {
-      upd[slot[u]] = uu * sqrt(t);
+  for (int u = 0; u < U; ++u)
+    if (lane == u) {
+      mc = col[u];
+      ms = slot[u];
     }
-    __syncwarp();
+  bool rec = false;
+  if (lane < U && mc) {
+    const double uu = upd[ms];
+    if (uu != 0.0) {
+      double t = fabs(mc[j]) / uu;
+      t = (1.0 + t) * (1.0 - t);
+      t = t < 0.0 ? 0.0 : t;
+      const double rr = uu / dir[ms];
+      if (t * rr * rr <= thr)
+        rec = true;
+      else
+        upd[ms] = uu * sqrt(t);
+    }
   }
+  unsigned todo = __ballot_sync(0xffffffffu, rec);
+  while (todo) {
+    const int u = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const double* cu = nullptr;
+    int su = 0;
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+      if (q == u) {
+        cu = col[q];
+        su = slot[q];
+      }
+    double sacc = 0.0;
+    for (int i = j + 1 + lane; i < M; i += 32) sacc += cu[i] * cu[i];
+    sacc = warp_sum(sacc);
+    if (lane == 0) upd[su] = dir[su] = sqrt(sacc);
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------- QR / CPQR
@@ -939,20 +960,33 @@ struct SmemCoopArgs {
 };
 
 constexpr int kSmemCoopU = 8;  // columns per block-wide reflector pass
+constexpr int kOT = 512;        // threads of the on-chip / cluster CPQR CTA
+constexpr int kOWarps = kOT / 32;
 
 constexpr int kThreadColM = 96;  // slabs this short: one thread per column
 // odd leading dimension for short slabs: thread-per-column access is then
 // free of shared-memory bank conflicts
 __host__ __device__ __forceinline__ int smem_coop_ld(int M) { return M <= kThreadColM ? (M | 1) : M; }
 __host__ __device__ __forceinline__ size_t smem_coop_doubles(int M, int nown) {
-  return size_t(smem_coop_ld(M)) * nown + M + 2 * nown + 8 * kSmemCoopU + 16 + (96 + 2 * nown + 1) / 2;
+  return size_t(smem_coop_ld(M)) * nown + M + 2 * nown + kOWarps * kSmemCoopU + 16 + (96 + 2 * nown + 1) / 2;
 }
 
 // kCl: one problem per thread-block cluster; partials and the pivot column
 // are read from the peers' shared memory (DSMEM) and the group barrier is
 // the hardware cluster barrier, so no grid-wide co-residency is needed.
+#ifdef SBX_CPQR_PROF
+__device__ long long g_cpqr_prof[64 * 8];
+#define CPQR_T(ph)                                                              \
+  do {                                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64) g_cpqr_prof[j * 8 + (ph)] = clock64(); \
+  } while (0)
+#else
+#define CPQR_T(ph) \
+  do {             \
+  } while (0)
+#endif
 template <bool kCl>
-__global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
+__global__ void __launch_bounds__(kOT) cpqr_onchip_kernel(SmemCoopArgs args) {
   extern __shared__ double sm[];
   __shared__ CoopPart s_part[2];
   int job, rank, G;
@@ -976,7 +1010,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
   double* v = S + size_t(ldS) * nown;     // M
   double* upd = v + M;                    // nown
   double* dir = upd + nown;               // nown
-  double* red = dir + nown;               // 8 warps x kSmemCoopU
+  double* red = dir + nown;               // kOWarps x kSmemCoopU
   double* sc = red + 8 * kSmemCoopU;      // 16
   int* ired = reinterpret_cast<int*>(sc + 16);  // 96
   int* mypos = ired + 96;                 // nown
@@ -986,17 +1020,27 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
   double* cand = kCl ? nullptr : args.cand + args.cand_off[job];
   double* sbeta = args.beta + args.beta_off[job];
   const double* Ag = jb.a;
-  for (i64 e = tid; e < i64(M) * nown; e += kCT) {
-    const int c = int(e / M), i = int(e - i64(c) * M);
-    S[i + size_t(c) * ldS] = Ag[i + size_t(c0 + c) * lda];
+  for (int c = warp; c < nown; c += kOWarps) {  // coalesced column loads, 4 in flight per lane
+    const double* src = Ag + size_t(c0 + c) * lda;
+    double* dst = S + size_t(c) * ldS;
+    int i = lane;
+    for (; i + 96 < M; i += 128) {
+      const double x0 = __ldg(src + i), x1 = __ldg(src + i + 32), x2 = __ldg(src + i + 64),
+                   x3 = __ldg(src + i + 96);
+      dst[i] = x0;
+      dst[i + 32] = x1;
+      dst[i + 64] = x2;
+      dst[i + 96] = x3;
+    }
+    for (; i < M; i += 32) dst[i] = __ldg(src + i);
   }
-  for (int c = tid; c < nown; c += kCT) {
+  for (int c = tid; c < nown; c += kOT) {
     mypos[c] = c0 + c;
     pivstep[c] = -1;
   }
   __syncthreads();
-  if (nown >= kCWarps) {
-    for (int c = warp; c < nown; c += kCWarps) {
+  if (nown >= kOWarps) {
+    for (int c = warp; c < nown; c += kOWarps) {
       const double* col = S + size_t(c) * ldS;
       double s = 0.0;
       for (int i = lane; i < M; i += 32) s += col[i] * col[i];
@@ -1007,13 +1051,13 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     for (int c = 0; c < nown; ++c) {
       const double* col = S + size_t(c) * ldS;
       double s = 0.0;
-      for (int i = tid; i < M; i += kCT) s += col[i] * col[i];
+      for (int i = tid; i < M; i += kOT) s += col[i] * col[i];
       s = warp_sum(s);
       if (lane == 0) red[warp] = s;
       __syncthreads();
       if (tid == 0) {
         double t = 0.0;
-        for (int w = 0; w < kCWarps; ++w) t += red[w];
+        for (int w = 0; w < kOWarps; ++w) t += red[w];
         upd[c] = dir[c] = sqrt(t);
       }
       __syncthreads();
@@ -1031,9 +1075,10 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
   double r00 = 0.0;
   __shared__ int s_p;
   for (int j = 0; j < steps_max; ++j) {
+    CPQR_T(0);
     double bv = -1.0;
     int bp = 0x7fffffff, bphys = -1;
-    for (int c = tid; c < nown; c += kCT) {
+    for (int c = tid; c < nown; c += kOT) {
       const int p = mypos[c];
       if (p >= 0 && better(upd[c], p, bv, bp)) {
         bv = upd[c];
@@ -1052,7 +1097,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
         bphys = oq;
       }
     }
-    __shared__ int wphys[kCWarps];
+    __shared__ int wphys[kOWarps];
     if (lane == 0) {
       red[warp] = bv;
       ired[warp] = bp;
@@ -1062,7 +1107,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     if (tid == 0) {
       double v0 = -1.0;
       int p0 = 0x7fffffff, q0 = -1;
-      for (int w = 0; w < kCWarps; ++w)
+      for (int w = 0; w < kOWarps; ++w)
         if (better(red[w], ired[w], v0, p0)) {
           v0 = red[w];
           p0 = ired[w];
@@ -1078,6 +1123,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     int p, lp, own;
     if constexpr (kCl) {
       cg::cluster_group cl = cg::this_cluster();
+      CPQR_T(1);
       cl.sync();  // every CTA's partial visible (release / acquire at cluster scope)
       __shared__ int s_pick[3];
       if (warp == 0) {
@@ -1111,6 +1157,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
           s_pick[2] = bo;
         }
       }
+      CPQR_T(2);
       __syncthreads();
       p = s_pick[0];
       lp = s_pick[1];
@@ -1122,13 +1169,13 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
         if (q >= 0) {
           const double* src = S + size_t(q - c0) * ldS;
           double* dst = cand + (size_t(j & 1) * G + rank) * M;
-          for (int i = j + tid; i < M; i += kCT) __stcg(dst + i, src[i]);
+          for (int i = j + tid; i < M; i += kOT) __stcg(dst + i, src[i]);
         }
       }
       group_barrier(ctl, unsigned(G));
       coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own);
     }
-    for (int c = tid; c < nown; c += kCT) {
+    for (int c = tid; c < nown; c += kOT) {
       if (c0 + c == p) {
         mypos[c] = -1;
         pivstep[c] = j;
@@ -1148,7 +1195,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     }
     auto ldp = [&](int i) { return kCl ? pc[i] : __ldcg(pc + i); };
     double part = 0.0;
-    for (int i = j + 1 + tid; i < M; i += kCT) {
+    for (int i = j + 1 + tid; i < M; i += kOT) {
       const double x = ldp(i);
       v[i] = x;
       part += x * x;
@@ -1156,7 +1203,8 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     part = warp_sum(part);
     if (lane == 0) red[warp] = part;
     __syncthreads();
-    const double tail = warp_sum(lane < kCWarps ? red[lane] : 0.0);
+    CPQR_T(3);
+    const double tail = warp_sum(lane < kOWarps ? red[lane] : 0.0);
     const double cc = ldp(j);
     double tau, beta, denom;
     if (tail <= DBL_MIN) {
@@ -1172,15 +1220,16 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
     __syncthreads();  // red[] reads done
     {
       const double rd = denom == 0.0 ? 0.0 : 1.0 / denom;
-      for (int i = j + 1 + tid; i < M; i += kCT) v[i] *= rd;
+      for (int i = j + 1 + tid; i < M; i += kOT) v[i] *= rd;
     }
     if (j == 0) r00 = fabs(beta);
     if (rank == 0 && tid == 0) sbeta[j] = beta;
     __syncthreads();
     done = j + 1;
+    CPQR_T(4);
     if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
     if (thread_mode) {
-      for (int c = tid; c < nown; c += kCT) {
+      for (int c = tid; c < nown; c += kOT) {
         if (mypos[c] < 0) continue;
         double* col = S + size_t(c) * ldS;
         if (tau != 0.0 && M - j > 1) {
@@ -1205,7 +1254,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
         }
       }
     } else if (warp_mode) {
-      for (int c = 4 * warp; c < nown; c += 4 * kCWarps) {
+      for (int c = 4 * warp; c < nown; c += 4 * kOWarps) {
         double* cols[4];
         int slot[4];
 #pragma unroll
@@ -1226,7 +1275,7 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
           d[u] = 0.0;
         }
         if (tau != 0.0 && M - j > 1) {
-          for (int i = j + 1 + tid; i < M; i += kCT) {
+          for (int i = j + 1 + tid; i < M; i += kOT) {
             const double vi = v[i];
 #pragma unroll
             for (int u = 0; u < kSmemCoopU; ++u)
@@ -1242,11 +1291,11 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
 #pragma unroll
           for (int u = 0; u < kSmemCoopU; ++u) {
             double t = 0.0;
-            for (int w = 0; w < kCWarps; ++w) t += red[w * kSmemCoopU + u];
+            for (int w = 0; w < kOWarps; ++w) t += red[w * kSmemCoopU + u];
             tw[u] = live[u] ? tau * (t + S[j + size_t(cb + u) * ldS]) : 0.0;
           }
           __syncthreads();  // everyone has read S[j, :] and red[]
-          for (int i = j + 1 + tid; i < M; i += kCT) {
+          for (int i = j + 1 + tid; i < M; i += kOT) {
             const double vi = v[i];
 #pragma unroll
             for (int u = 0; u < kSmemCoopU; ++u)
@@ -1271,13 +1320,13 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
           __syncthreads();  // all threads read upd[c] before it changes
           if (t * rr * rr <= thr) {
             double sacc = 0.0;
-            for (int i = j + 1 + tid; i < M; i += kCT) sacc += S[i + size_t(c) * ldS] * S[i + size_t(c) * ldS];
+            for (int i = j + 1 + tid; i < M; i += kOT) sacc += S[i + size_t(c) * ldS] * S[i + size_t(c) * ldS];
             sacc = warp_sum(sacc);
             if (lane == 0) red[warp] = sacc;
             __syncthreads();
             if (tid == 0) {
               double s2 = 0.0;
-              for (int w = 0; w < kCWarps; ++w) s2 += red[w];
+              for (int w = 0; w < kOWarps; ++w) s2 += red[w];
               upd[c] = dir[c] = sqrt(s2);
             }
           } else if (tid == 0) {
@@ -1288,22 +1337,272 @@ __global__ void __launch_bounds__(kCT) cpqr_onchip_kernel(SmemCoopArgs args) {
       }
     }
     __syncthreads();
+    CPQR_T(5);
   }
   if constexpr (kCl)
     cg::this_cluster().sync();  // peers are done reading this slab; sbeta complete
   else
     group_barrier(ctl, unsigned(G));
-  for (int c = tid; c < nown; c += kCT)  // R diagonal of the pivoted columns
+  for (int c = tid; c < nown; c += kOT)  // R diagonal of the pivoted columns
     if (pivstep[c] >= 0) S[pivstep[c] + size_t(c) * ldS] = __ldcg(sbeta + pivstep[c]);
   __syncthreads();
   double* Aw = jb.a;
-  for (int c = warp; c < nown; c += kCWarps)
+  for (int c = warp; c < nown; c += kOWarps)
     for (int i = lane; i < M; i += 32) Aw[i + size_t(c0 + c) * lda] = S[i + size_t(c) * ldS];
-  for (int c = tid; c < nown; c += kCT)
+  for (int c = tid; c < nown; c += kOT)
     if (mypos[c] >= 0) jb.perm[mypos[c]] = c0 + c;
-  for (int l = rank * kCT + tid; l < size; l += G * kCT)
+  for (int l = rank * kOT + tid; l < size; l += G * kOT)
     jb.diag[l] = l < done ? fabs(__ldcg(sbeta + l)) : 0.0;
   if (rank == 0 && tid == 0 && jb.steps) *jb.steps = done;
+}
+
+// ---------------------------------------------------------------- register-resident cluster CPQR
+// One problem per thread-block cluster of G CTAs (columns split across CTAs
+// like cpqr_onchip_kernel<true>), but the slab lives in REGISTERS: warp w of
+// a CTA owns CPW whole columns, lane l rows l + 32 r (r < RPL).  Per step:
+//  (1) every warp picks its best live column (first max of the downdated
+//      norms) and builds that column's Householder vector speculatively
+//      (warp reductions only);
+//  (2) one CTA barrier; every warp reduces the 16 warp candidates, the
+//      winning warp publishes its vector in shared memory and pushes the
+//      CTA candidate (norm, position, beta, tau) into every peer's smem;
+//  (3) one cluster barrier; every warp reduces the G candidates locally,
+//      copies the winner's vector from the owner CTA (DSMEM) and applies the
+//      reflector + the xGEQPF norm downdate to its columns in registers.
+// Two barriers and one DSMEM round trip per step.  Same pivot rule, stop
+// rule and R layout (columns never move, perm names them) as the other
+// engines; results agree to rounding (the Householder norms are summed per
+// warp instead of across the CTA).
+struct RegPart {
+  double val, beta, tau;
+  int pos, phys;
+};
+
+// First max of (val, pos) over the first W lanes (W a power of two <= 32);
+// returns the winning lane, every lane gets it.
+template <int W>
+__device__ __forceinline__ int lane_argmax(double val, int pos) {
+  int id = threadIdx.x & 31;
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+    const int op = __shfl_xor_sync(0xffffffffu, pos, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, id, o);
+    if (better(ov, op, val, pos)) {
+      val = ov;
+      pos = op;
+      id = oi;
+    }
+  }
+  return __shfl_sync(0xffffffffu, id, 0);
+}
+
+template <int RPL, int CPW>
+__global__ void __launch_bounds__(kOT, 1) cpqr_reg_kernel(const QrJob* __restrict__ jobs) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = int(cl.num_blocks()), rank = int(cl.block_rank());
+  const QrJob jb = jobs[int(blockIdx.x) / G];
+  const int M = jb.M, n = jb.n, lda = jb.lda;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = int(i64(n) * rank / G), c1 = int(i64(n) * (rank + 1) / G);
+  constexpr int MR = 32 * RPL;
+  extern __shared__ double rsm[];
+  double* pubv = rsm;            // 2 x MR: this CTA's candidate vector (step parity), v_j = 1
+  double* vloc = rsm + 2 * MR;   // MR: the winning vector, local copy
+  double* betas = vloc + MR;     // min(M, n)
+  __shared__ RegPart wpart[kOWarps];
+  __shared__ RegPart cpart[2][16];
+  double a[CPW][RPL];
+  double upd[CPW], dir[CPW];
+  int pos[CPW], pst[CPW];
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int c = c0 + warp * CPW + u;
+    const bool live = c < c1;
+    const double* src = jb.a + size_t(live ? c : 0) * lda;
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      a[u][r] = (live && i < M) ? src[i] : 0.0;
+      sq += a[u][r] * a[u][r];
+    }
+    sq = warp_sum(sq);
+    upd[u] = dir[u] = sqrt(sq);
+    pos[u] = live ? c : -1;
+    pst[u] = -1;
+  }
+  const int size = min(M, n);
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  const double thr = sqrt(DBL_EPSILON);
+  int done = 0;
+  double r00 = 0.0;
+  for (int j = 0; j < steps_max; ++j) {
+    const int par = j & 1, rj = j >> 5, lj = j & 31;
+    CPQR_T(0);
+    // (1) warp candidate + its Householder vector
+    int wu = -1;
+    double wv = -1.0;
+    int wp = 0x7fffffff;
+#pragma unroll
+    for (int u = 0; u < CPW; ++u)
+      if (pos[u] >= 0 && better(upd[u], pos[u], wv, wp)) {
+        wv = upd[u];
+        wp = pos[u];
+        wu = u;
+      }
+    double beta = 0.0, tau = 0.0, rd = 0.0;
+    if (wu >= 0) {
+      double part = 0.0, ccl = 0.0;
+#pragma unroll
+      for (int u = 0; u < CPW; ++u)
+        if (u == wu) {  // warp-uniform
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i > j) part += a[u][r] * a[u][r];
+            if (r == rj) ccl = a[u][r];
+          }
+        }
+      const double tail = warp_sum(part);
+      const double cc = __shfl_sync(0xffffffffu, ccl, lj);
+      double denom;
+      if (tail <= DBL_MIN) {
+        tau = 0.0;
+        beta = cc;
+        denom = 0.0;
+      } else {
+        beta = sqrt(cc * cc + tail);
+        if (cc >= 0.0) beta = -beta;
+        denom = cc - beta;
+        tau = (beta - cc) / beta;
+      }
+      rd = denom == 0.0 ? 0.0 : 1.0 / denom;
+    }
+    CPQR_T(1);
+    if (lane == 0)
+      wpart[warp] = {wu >= 0 ? wv : -1.0, beta, tau, wu >= 0 ? wp : 0x7fffffff, wu >= 0 ? c0 + warp * CPW + wu : -1};
+    __syncthreads();
+    // (2) CTA candidate; its warp publishes the vector and the candidate
+    {
+      const bool in = lane < kOWarps;
+      const int bid = lane_argmax<kOWarps>(in ? wpart[lane].val : -1.0, in ? wpart[lane].pos : 0x7fffffff);
+      if (warp == bid) {
+#pragma unroll
+        for (int u = 0; u < CPW; ++u)
+          if (u == wu) {
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+              const int i = lane + 32 * r;
+              pubv[par * MR + i] = i > j ? a[u][r] * rd : (i == j ? 1.0 : 0.0);
+            }
+          }
+        if (lane < G) *cl.map_shared_rank(&cpart[par][rank], lane) = wpart[bid];
+      }
+    }
+    CPQR_T(2);
+    cl.sync();
+    CPQR_T(3);
+    // (3) cluster winner
+    const int own = lane_argmax<16>(lane < G ? cpart[par][lane].val : -1.0,
+                                    lane < G ? cpart[par][lane].pos : 0x7fffffff);
+    const RegPart w = cpart[par][own];
+    const int p = w.phys, lp = w.pos;
+    beta = w.beta;
+    tau = w.tau;
+    if (tid == 0) {
+      betas[j] = beta;
+      if (p >= c0 && p < c1) jb.perm[j] = p;
+    }
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      if (c0 + warp * CPW + u == p) {
+        pos[u] = -1;
+        pst[u] = j;
+      } else if (pos[u] == j) {
+        pos[u] = lp;
+      }
+    }
+    if (j == 0) r00 = fabs(beta);
+    done = j + 1;
+    if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    CPQR_T(4);
+    {
+      const double* rv = cl.map_shared_rank(pubv + par * MR, own);
+      for (int i = tid; i < MR; i += kOT) vloc[i] = rv[i];
+    }
+    __syncthreads();
+    CPQR_T(5);
+    double d[CPW];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) d[u] = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const double vi = vloc[lane + 32 * r];
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) d[u] += vi * a[u][r];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+    double rowj[CPW];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      rowj[u] = 0.0;
+      if (pos[u] < 0) continue;  // warp-uniform
+      const double tw = tau * d[u];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        a[u][r] -= vloc[lane + 32 * r] * tw;
+        if (r == rj) rowj[u] = a[u][r];
+      }
+    }
+    // xGEQPF downdate, all columns at once (no branches between the
+    // divisions); the rare recomputations afterwards
+    bool rec[CPW];
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const double colj = __shfl_sync(0xffffffffu, rowj[u], lj);
+      const double uu = upd[u];
+      double t = fabs(colj) / uu;
+      t = (1.0 + t) * (1.0 - t);
+      t = t < 0.0 ? 0.0 : t;
+      const double rr = uu / dir[u];
+      const bool live = pos[u] >= 0 && uu != 0.0;
+      rec[u] = live && t * rr * rr <= thr;
+      if (live && !rec[u]) upd[u] = uu * sqrt(t);
+    }
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      if (!rec[u]) continue;  // warp-uniform
+      double sq = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i > j) sq += a[u][r] * a[u][r];
+      }
+      upd[u] = dir[u] = sqrt(warp_sum(sq));
+    }
+    CPQR_T(6);
+  }
+  cl.sync();  // peers are done reading this CTA's shared memory
+#pragma unroll
+  for (int u = 0; u < CPW; ++u) {
+    const int c = c0 + warp * CPW + u;
+    if (c >= c1) continue;
+    double* dst = jb.a + size_t(c) * lda;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < M) dst[i] = i == pst[u] ? betas[i] : a[u][r];
+    }
+    if (pos[u] >= 0 && lane == 0) jb.perm[pos[u]] = c;
+  }
+  if (rank == 0) {
+    for (int l = tid; l < size; l += kOT) jb.diag[l] = l < done ? fabs(betas[l]) : 0.0;
+    if (tid == 0 && jb.steps) *jb.steps = done;
+  }
 }
 
 // ---------------------------------------------------------------- interpolation
@@ -1336,6 +1635,71 @@ __global__ void __launch_bounds__(kIT) interp_kernel(const InterpJob* __restrict
   }
   double* prow = jb.P + jb.perm[k + j];
   for (int i = 0; i < k; ++i) prow[size_t(i) * jb.ldp] = jb.T[size_t(i) * nk + j];
+}
+
+// Warp per column of R12 (k <= 32 * RPL): lane l holds rows l, l + 32, ...
+// of the right-hand side in registers; column-oriented back substitution
+// (x_i broadcast by shuffle, then an axpy with column i of R11), so the
+// dependent chain per step is one shuffle + one division instead of a
+// k-long dot product per row.  Eight columns per CTA.
+constexpr int kIWarps = 8;
+
+template <int RPL>
+__global__ void __launch_bounds__(kIWarps * 32) interp_warp_kernel(const InterpJob* __restrict__ jobs,
+                                                                   const int2* __restrict__ items) {
+  const int2 it = items[blockIdx.x];
+  const InterpJob jb = jobs[it.x];
+  const int n = jb.n, k = jb.k, nk = n - k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (it.y < 0) {  // P(J_i, :) = e_i
+    for (i64 idx = threadIdx.x; idx < i64(k) * k; idx += kIWarps * 32) {
+      const int i = int(idx % k), c = int(idx / k);
+      jb.P[jb.perm[i] + size_t(c) * jb.ldp] = i == c ? 1.0 : 0.0;
+    }
+    return;
+  }
+  const int j = it.y + warp;
+  if (j >= nk) return;
+  const int* cm = jb.colmap;
+  const double* R = jb.a;
+  const size_t lda = size_t(jb.lda);
+  const double* rj = R + size_t(cm ? cm[k + j] : k + j) * lda;
+  double b[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int l = lane + 32 * r;
+    b[r] = l < k ? rj[l] : 0.0;
+  }
+  double* prow = jb.P + jb.perm[k + j];
+  auto col_of = [&](int i) { return R + size_t(cm ? cm[i] : i) * lda; };
+#pragma unroll
+  for (int rb = RPL - 1; rb >= 0; --rb) {
+    if (32 * rb >= k) continue;
+    const int top = min(31, k - 1 - 32 * rb);
+    // column i of R11 is fetched one step ahead of its use
+    const double* ri = col_of(32 * rb + top);
+    double d = ri[32 * rb + top], rv[RPL];
+#pragma unroll
+    for (int r = 0; r <= rb; ++r) rv[r] = lane + 32 * r < k ? ri[lane + 32 * r] : 0.0;
+    for (int ii = top; ii >= 0; --ii) {
+      const int i = 32 * rb + ii;
+      double dn = 1.0, vn[RPL];
+      if (ii > 0) {
+        const double* rn = col_of(i - 1);
+        dn = rn[i - 1];
+#pragma unroll
+        for (int r = 0; r <= rb; ++r) vn[r] = lane + 32 * r < k ? rn[lane + 32 * r] : 0.0;
+      }
+      const double x = __shfl_sync(0xffffffffu, b[rb], ii) / d;
+      if (lane == 0) prow[size_t(i) * jb.ldp] = x;
+#pragma unroll
+      for (int r = 0; r <= rb; ++r)
+        if (r < rb || lane < ii) b[r] -= rv[r] * x;
+      d = dn;
+#pragma unroll
+      for (int r = 0; r <= rb; ++r) rv[r] = vn[r];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- GEMM (DMMA)
@@ -1747,6 +2111,157 @@ __global__ void __launch_bounds__(kT) lu_kernel(const LuJob* __restrict__ jobs, 
 }
 
 
+// ---------------------------------------------------------------- Gauss-Jordan inverse (n <= 128)
+// Explicit inverse by in-place Gauss-Jordan with partial (row) pivoting and
+// the matrix held in REGISTERS: lane l of warp w owns rows l + 32a (a < RA)
+// and columns w + 16b (b < CB).  Rows are never moved: row i used as the
+// pivot of step k gives inv[k, piv[m]] = M[i, m] at the end.  The pivot of
+// step k is the first largest |M[i, k]| over the rows not yet used, which in
+// exact arithmetic is the pivot PartialPivLU takes (the unused rows carry
+// LU's Schur complement); results agree with lu_kernel to rounding.
+// Per step: the owner warp of column k picks the pivot and publishes the
+// column; the owners of the pivot row publish it scaled; everyone updates its
+// register tile (two CTA barriers per step).
+template <int RA, int CB>
+__global__ void __launch_bounds__(kT) gj_inverse_kernel(const LuJob* __restrict__ jobs) {
+  static_assert(kT == 512, "16 warps x 32 lanes");
+  extern __shared__ double sm[];
+  const LuJob jb = jobs[blockIdx.x];
+  const int n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* X = sm;                            // n x n (final inverse, for rcond)
+  double* colb = X + size_t(n) * n;          // 2 x 128: pivot column, double buffered
+  double* rowb = colb + 256;                 // 2 x 128: scaled pivot row
+  double* red = rowb + 256;                  // 64
+  int* ired = reinterpret_cast<int*>(red + 64);  // 64
+  int* pivrow = ired + 64;                   // 128: row used at step k
+  int* rowstep = pivrow + 128;               // 128: step at which row i pivoted
+  __shared__ int s_p;
+  __shared__ double s_l1;
+  __shared__ int s_sing;
+  if (tid == 0) {
+    s_l1 = 0.0;
+    s_sing = 0;
+  }
+  double M[RA][CB];
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int i = lane + 32 * a, j = warp + 16 * b;
+      M[a][b] = (i < n && j < n) ? jb.a[i + size_t(j) * jb.lda] : 0.0;
+    }
+  __syncthreads();
+  // 1-norm of A (max column sum)
+#pragma unroll
+  for (int b = 0; b < CB; ++b) {
+    double cs = 0.0;
+#pragma unroll
+    for (int a = 0; a < RA; ++a) cs += fabs(M[a][b]);
+    cs = warp_sum(cs);
+    if (lane == 0 && warp + 16 * b < n)
+      atomicMax(reinterpret_cast<unsigned long long*>(&s_l1), __double_as_longlong(cs));
+  }
+  unsigned used = 0;  // bit a: row lane + 32 a already pivoted
+  for (int k = 0; k < n; ++k) {
+    double* col = colb + 128 * (k & 1);
+    double* row = rowb + 128 * (k & 1);
+    const int wk = k & 15, bk = k >> 4;
+    if (warp == wk) {  // pivot search + publish column k
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int b = 0; b < CB; ++b)
+        if (b == bk) {
+#pragma unroll
+          for (int a = 0; a < RA; ++a) {
+            const int i = lane + 32 * a;
+            if (i < n) {
+              col[i] = M[a][b];
+              const double v = fabs(M[a][b]);
+              if (!((used >> a) & 1u) && v > bv) {
+                bv = v;
+                bi = i;
+              }
+            }
+          }
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        pivrow[k] = bi;
+        rowstep[bi] = k;
+        if (!(bv > 0.0)) s_sing = 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const int ap = p >> 5, lp = p & 31;
+    const double piv = col[p];
+    const double rinv = piv != 0.0 ? 1.0 / piv : 0.0;
+    if (lane == lp) {  // owners of row p publish it scaled (column k: 1/piv)
+#pragma unroll
+      for (int a = 0; a < RA; ++a)
+        if (a == ap) {
+          used |= 1u << a;
+#pragma unroll
+          for (int b = 0; b < CB; ++b) {
+            const int j = warp + 16 * b;
+            if (j < n) {
+              const double u = j == k ? rinv : M[a][b] * rinv;
+              row[j] = u;
+              M[a][b] = u;
+            }
+          }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < RA; ++a) {
+      const int i = lane + 32 * a;
+      if (i >= n || i == p) continue;
+      const double f = col[i];
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int j = warp + 16 * b;
+        if (j == k)
+          M[a][b] = -f * rinv;
+        else
+          M[a][b] -= f * row[j];
+      }
+    }
+  }
+  // unscramble: inv[k, pivrow[m]] = M[pivrow[k], m]
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      const int i = lane + 32 * a, m = warp + 16 * b;
+      if (i < n && m < n) {
+        const size_t o = size_t(rowstep[i]) + size_t(pivrow[m]) * n;
+        X[o] = M[a][b];
+        jb.inv[o] = M[a][b];
+      }
+    }
+  for (int q = tid; q < n; q += kT) jb.piv[q] = pivrow[q];
+  __syncthreads();
+  if (jb.rcond) {
+    const double r = s_sing ? 0.0 : rcond_from_inverse(X, n, s_l1, jb.work, red, ired);
+    if (tid == 0) *jb.rcond = r;
+  }
+}
+
+constexpr int kGjMax = 128;
+size_t gj_smem(int n) { return (size_t(n) * n + 256 + 256 + 64 + 32 + 128) * sizeof(double); }
+
 // ---------------------------------------------------------------- blocked LU (large n)
 // Right-looking partial-pivot LU in panels of kLuNb columns: panel
 // factorisation by one CTA (smem when it fits, else L2), row swaps, unit
@@ -2001,8 +2516,9 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
                                   int(kSmemCap)));
   });
   std::vector<QrJob> plain, tall;
+  static const bool no_tsqr = std::getenv("SBX_NO_TSQR") != nullptr;  // diagnostics
   for (const auto& j : jobs) {
-    const bool tsqr = j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
+    const bool tsqr = !no_tsqr && j.pivot && j.n <= 16 * kTsqrSlots && j.M > j.n && tsqr_smem(j.n) <= kSmemCap &&
                       qr_smem_need(j.M, j.n, true) > kSmemCap;
     (tsqr ? tall : plain).push_back(j);
   }
@@ -2182,7 +2698,7 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
       require(g > 0 && g <= sms, "cpqr_smem: problem does not fit on chip");
       const size_t sm2 = std::max(smem, smem_coop_doubles(jobs[q].M, (jobs[q].n + g - 1) / g) * sizeof(double));
       int ps = 1;
-      SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cpqr_onchip_kernel<false>, kCT, sm2));
+      SBX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, cpqr_onchip_kernel<false>, kOT, sm2));
       ps = std::max(1, ps);
       if (!wave.empty() && ctas + g > sms * ps) break;
       wave.push_back(jobs[q]);
@@ -2237,10 +2753,10 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     static const bool plain = std::getenv("SBX_COOP_PLAIN") != nullptr;  // diagnostics
     if (plain)
       SBX_CUDA(cudaLaunchKernel(reinterpret_cast<void*>(cpqr_onchip_kernel<false>), dim3(unsigned(cta_job.size())),
-                                dim3(kCT), params, smem, s));
+                                dim3(kOT), params, smem, s));
     else
       SBX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cpqr_onchip_kernel<false>),
-                                           dim3(unsigned(cta_job.size())), dim3(kCT), params, smem, s));
+                                           dim3(unsigned(cta_job.size())), dim3(kOT), params, smem, s));
     SBX_LAUNCHED();
   }
 }
@@ -2253,19 +2769,43 @@ int cpqr_cluster_size(int M, int n) {
   return c;
 }
 
-void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
-  if (jobs.empty()) return;
-  int C = 1;
-  for (const auto& j : jobs) {
-    const int c = cpqr_cluster_size(j.M, j.n);
-    require(c > 0, "cpqr_cluster: problem does not fit one cluster");
-    C = std::max(C, c);
+#ifdef SBX_CPQR_PROF
+void cpqr_prof_dump() {
+  long long h[64 * 8];
+  SBX_CUDA(cudaMemcpyFromSymbol(h, g_cpqr_prof, sizeof(h)));
+  for (int j = 0; j < 64; ++j) {
+    if (h[j * 8 + 5] == 0) break;
+    std::fprintf(stderr, "step %2d:", j);
+    int last = 5;
+    while (last < 7 && h[j * 8 + last + 1]) ++last;
+    for (int q = 1; q <= last; ++q) std::fprintf(stderr, " %6lld", h[j * 8 + q] - h[j * 8 + q - 1]);
+    std::fprintf(stderr, "  | next %lld\n", j < 63 && h[j * 8 + 8] ? h[j * 8 + 8] - h[j * 8 + last] : 0LL);
   }
-  size_t smem = 0;
+}
+#endif
+
+void cpqr_cluster_batched(const std::vector<QrJob>& all, cudaStream_t s) {
+  if (all.empty()) return;
+  // one launch per cluster size: a batch mixing sizes would otherwise give
+  // every problem the largest cluster (and the fewest co-resident clusters)
+  std::vector<QrJob> jobs;
+  std::vector<int> csz;
+  {
+    std::vector<std::pair<int, size_t>> order;
+    for (size_t q = 0; q < all.size(); ++q) {
+      const int c = cpqr_cluster_size(all[q].M, all[q].n);
+      require(c > 0, "cpqr_cluster: problem does not fit one cluster");
+      order.push_back({c, q});
+    }
+    std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (const auto& o : order) {
+      jobs.push_back(all[o.second]);
+      csz.push_back(o.first);
+    }
+  }
   i64 boff = 0;
   std::vector<i64> offs;
   for (const auto& j : jobs) {
-    smem = std::max(smem, smem_coop_doubles(j.M, (j.n + C - 1) / C) * sizeof(double));
     offs.push_back(boff);
     boff += std::min(j.M, j.n);
   }
@@ -2280,36 +2820,158 @@ void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   static thread_local DevBuf<i64> d_offs;
   d_beta.reserve(size_t(std::max<i64>(boff, 1)));
   d_offs.upload(offs, s);
-  SmemCoopArgs a{};
-  a.jobs = tjobs.upload(jobs, s);
-  a.beta = d_beta.get();
-  a.beta_off = d_offs.get();
+  const QrJob* dj = tjobs.upload(jobs, s);
+  for (size_t g0 = 0; g0 < jobs.size();) {
+    const int C = csz[g0];
+    size_t g1 = g0;
+    size_t smem = 0;
+    while (g1 < jobs.size() && csz[g1] == C) {
+      smem = std::max(smem, smem_coop_doubles(jobs[g1].M, (jobs[g1].n + C - 1) / C) * sizeof(double));
+      ++g1;
+    }
+    SmemCoopArgs a{};
+    a.jobs = dj + g0;
+    a.beta = d_beta.get();
+    a.beta_off = d_offs.get() + g0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((g1 - g0) * size_t(C)));
+    cfg.blockDim = dim3(kOT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(C);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SBX_CUDA(cudaLaunchKernelEx(&cfg, cpqr_onchip_kernel<true>, a));
+    SBX_LAUNCHED();
+    g0 = g1;
+  }
+}
+
+namespace {
+struct RegCfg {
+  int rpl, cpw;
+};
+constexpr RegCfg kRegCfgs[] = {{9, 4}, {17, 2}, {20, 2}, {27, 1}, {34, 1}};
+constexpr int kRegCfgN = int(sizeof(kRegCfgs) / sizeof(kRegCfgs[0]));
+
+template <int RPL, int CPW>
+void launch_reg(const QrJob* d, int np, int G, int size_max, cudaStream_t s) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_reg_kernel<RPL, CPW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_reg_kernel<RPL, CPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int((3 * 32 * 34 + 2048) * sizeof(double))));
+  });
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(jobs.size() * size_t(C)));
-  cfg.blockDim = dim3(kCT);
-  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(unsigned(np * G));
+  cfg.blockDim = dim3(kOT);
+  cfg.dynamicSmemBytes = (size_t(3 * 32 * RPL) + size_t(size_max)) * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = unsigned(C);
+  at[0].val.clusterDim.x = unsigned(G);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  SBX_CUDA(cudaLaunchKernelEx(&cfg, cpqr_onchip_kernel<true>, a));
+  SBX_CUDA(cudaLaunchKernelEx(&cfg, cpqr_reg_kernel<RPL, CPW>, d));
   SBX_LAUNCHED();
 }
+}  // namespace
 
-void interp_batched(const std::vector<InterpJob>& jobs, cudaStream_t s) {
-  if (jobs.empty()) return;
-  static thread_local JobTable<InterpJob> tab;
-  static thread_local JobTable<int2> itab;
-  std::vector<int2> items;
-  for (size_t q = 0; q < jobs.size(); ++q) {
-    items.push_back(make_int2(int(q), -1));
-    for (int c = 0; c < jobs[q].n - jobs[q].k; c += kIT) items.push_back(make_int2(int(q), c));
+int cpqr_reg_config(int M, int n, int* G) {
+  if (M <= 0 || n <= 0) return -1;
+  for (int c = 0; c < kRegCfgN; ++c) {
+    if (32 * kRegCfgs[c].rpl < M) continue;
+    const int g = (n + 16 * kRegCfgs[c].cpw - 1) / (16 * kRegCfgs[c].cpw);
+    if (g > 16 || std::min(M, n) > 2048) return -1;
+    if (G) *G = g;
+    return c;
   }
-  const InterpJob* d = tab.upload(jobs, s);
+  return -1;
+}
+
+void cpqr_reg_batched(const std::vector<QrJob>& all, cudaStream_t s) {
+  if (all.empty()) return;
+  // one launch per (register layout, cluster size)
+  std::vector<std::pair<int, size_t>> order;
+  for (size_t q = 0; q < all.size(); ++q) {
+    int G = 0;
+    const int c = cpqr_reg_config(all[q].M, all[q].n, &G);
+    require(c >= 0, "cpqr_reg: problem does not fit the register engine");
+    order.push_back({c * 64 + G, q});
+  }
+  std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<QrJob> jobs;
+  for (const auto& o : order) jobs.push_back(all[o.second]);
+  static thread_local JobTable<QrJob> tjobs;
+  const QrJob* dj = tjobs.upload(jobs, s);
+  for (size_t g0 = 0; g0 < jobs.size();) {
+    const int key = order[g0].first;
+    size_t g1 = g0;
+    int size_max = 1;
+    while (g1 < jobs.size() && order[g1].first == key) {
+      size_max = std::max(size_max, std::min(jobs[g1].M, jobs[g1].n));
+      ++g1;
+    }
+    const int c = key / 64, G = key % 64, np = int(g1 - g0);
+    switch (c) {
+      case 0: launch_reg<9, 4>(dj + g0, np, G, size_max, s); break;
+      case 1: launch_reg<17, 2>(dj + g0, np, G, size_max, s); break;
+      case 2: launch_reg<20, 2>(dj + g0, np, G, size_max, s); break;
+      case 3: launch_reg<27, 1>(dj + g0, np, G, size_max, s); break;
+      default: launch_reg<34, 1>(dj + g0, np, G, size_max, s); break;
+    }
+    g0 = g1;
+  }
+}
+
+void interp_batched(const std::vector<InterpJob>& all, cudaStream_t s) {
+  if (all.empty()) return;
+  static thread_local JobTable<InterpJob> tab, wtab[3];
+  static thread_local JobTable<int2> itab, witab[3];
+  // register-resident warp kernel by rank class; very high ranks keep the
+  // thread-per-column kernel
+  std::vector<InterpJob> cls[3], rest;
+  for (const auto& j : all) {
+    if (j.k <= 64)
+      cls[0].push_back(j);
+    else if (j.k <= 128)
+      cls[1].push_back(j);
+    else if (j.k <= 256)
+      cls[2].push_back(j);
+    else
+      rest.push_back(j);
+  }
+  for (int c = 0; c < 3; ++c) {
+    if (cls[c].empty()) continue;
+    std::vector<int2> items;
+    for (size_t q = 0; q < cls[c].size(); ++q) {
+      items.push_back(make_int2(int(q), -1));
+      for (int col = 0; col < cls[c][q].n - cls[c][q].k; col += kIWarps) items.push_back(make_int2(int(q), col));
+    }
+    const InterpJob* d = wtab[c].upload(cls[c], s);
+    const int2* di = witab[c].upload(items, s);
+    const unsigned g = unsigned(items.size());
+    if (c == 0)
+      interp_warp_kernel<2><<<g, kIWarps * 32, 0, s>>>(d, di);
+    else if (c == 1)
+      interp_warp_kernel<4><<<g, kIWarps * 32, 0, s>>>(d, di);
+    else
+      interp_warp_kernel<8><<<g, kIWarps * 32, 0, s>>>(d, di);
+    SBX_LAUNCHED();
+  }
+  if (rest.empty()) return;
+  std::vector<int2> items;
+  for (size_t q = 0; q < rest.size(); ++q) {
+    items.push_back(make_int2(int(q), -1));
+    for (int c = 0; c < rest[q].n - rest[q].k; c += kIT) items.push_back(make_int2(int(q), c));
+  }
+  const InterpJob* d = tab.upload(rest, s);
   const int2* di = itab.upload(items, s);
   interp_kernel<<<unsigned(items.size()), kIT, 0, s>>>(d, di);
   SBX_LAUNCHED();
@@ -2435,6 +3097,12 @@ void lu_blocked(const LuJob& j, cudaStream_t s) {
 
 void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
   if (all.empty()) return;
+  static const bool log = std::getenv("SBX_LU_LOG") != nullptr;  // diagnostics
+  if (log) {
+    std::string line;
+    for (const auto& j : all) line += " " + std::to_string(j.n);
+    std::fprintf(stderr, "[sbx-lu]%s\n", line.c_str());
+  }
   // large blocks (few per batch) go through the blocked multi-kernel path
   std::vector<LuJob> jobs, big;
   for (const auto& j : all) (j.n >= kLuBlockedMin ? big : jobs).push_back(j);
@@ -2448,6 +3116,42 @@ void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
     lu_blocked(j, s);
   }
   if (jobs.empty()) return;
+  static const bool no_gj = std::getenv("SBX_NO_GJ") != nullptr;  // diagnostics
+  if (!no_gj) {
+    std::vector<LuJob> gj[3], rest;
+    for (const auto& j : jobs) (j.n <= 32 ? gj[0] : j.n <= 64 ? gj[1] : j.n <= kGjMax ? gj[2] : rest).push_back(j);
+    static thread_local JobTable<LuJob> gtab[3];
+    static std::once_flag gattr;
+    std::call_once(gattr, [] {
+      SBX_CUDA(cudaFuncSetAttribute(gj_inverse_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(gj_smem(kGjMax))));
+      SBX_CUDA(cudaFuncSetAttribute(gj_inverse_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(gj_smem(kGjMax))));
+      SBX_CUDA(cudaFuncSetAttribute(gj_inverse_kernel<4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(gj_smem(kGjMax))));
+    });
+    for (int c = 0; c < 3; ++c) {
+      if (gj[c].empty()) continue;
+      int nmax = 1;
+      for (const auto& j : gj[c]) {
+        require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+        require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
+        nmax = std::max(nmax, j.n);
+      }
+      const LuJob* d = gtab[c].upload(gj[c], s);
+      const unsigned g = unsigned(gj[c].size());
+      const size_t sm = gj_smem(nmax);
+      if (c == 0)
+        gj_inverse_kernel<1, 2><<<g, kT, sm, s>>>(d);
+      else if (c == 1)
+        gj_inverse_kernel<2, 4><<<g, kT, sm, s>>>(d);
+      else
+        gj_inverse_kernel<4, 8><<<g, kT, sm, s>>>(d);
+      SBX_LAUNCHED();
+    }
+    jobs = rest;
+    if (jobs.empty()) return;
+  }
   static thread_local JobTable<LuJob> tab;
   size_t need = 64 * sizeof(double);
   for (const auto& j : jobs) {

@@ -55,6 +55,10 @@ void cpqr_smem_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // cpqr_cluster_size gives C (a power of two) or 0 when one cluster is too small.
 int cpqr_cluster_size(int M, int n);
 void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Register-resident cluster CPQR (one problem per cluster of G <= 16 CTAs,
+// M <= 1088): returns the layout index (G set) or -1 when it does not apply.
+int cpqr_reg_config(int M, int n, int* G);
+void cpqr_reg_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 
 // ---------------------------------------------------------------- ID interpolation
 // Given a pivoted factor (R in the upper triangle of a, ld lda, n columns)

@@ -26,47 +26,90 @@ int sm_count() {
 }  // namespace
 
 // Engine routing and launches for one batch of CPQR jobs (engine: 0 auto).
+namespace {
+// SBX_ID_DUMP=<dir>: every batch (shapes, stop rule and W^T) as
+// <dir>/batch_NNNN.bin for offline engine comparisons (scripts/id_bench.cu).
+void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
+  static const char* dir = std::getenv("SBX_ID_DUMP");
+  if (!dir || all.empty()) return;
+  static int seq = 0;
+  char path[512];
+  std::snprintf(path, sizeof(path), "%s/batch_%04d.bin", dir, seq++);
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return;
+  const long long np = static_cast<long long>(all.size());
+  std::fwrite(&np, sizeof(np), 1, f);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  for (const auto& j : all) {
+    const long long hdr[4] = {j.M, j.n, j.max_steps, 0};
+    std::fwrite(hdr, sizeof(hdr), 1, f);
+    std::fwrite(&j.stop_eps, sizeof(double), 1, f);
+    std::vector<double> h(size_t(j.M) * j.n);
+    SBX_CUDA(cudaMemcpy2D(h.data(), size_t(j.M) * sizeof(double), j.a, size_t(j.lda) * sizeof(double),
+                          size_t(j.M) * sizeof(double), size_t(j.n), cudaMemcpyDeviceToHost));
+    std::fwrite(h.data(), sizeof(double), h.size(), f);
+  }
+  std::fclose(f);
+}
+}  // namespace
+
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
-  std::vector<QrJob> jobs, big, chip, clus;
+  dump_batch(all, s);
+  std::vector<QrJob> jobs, big, chip, clus, reg;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
   }();
-  // Large batches have enough independent problems to fill the GPU with one
-  // CTA each; cross-CTA engines only pay off when problems are few.  Count
-  // the CTAs the cluster engine would need for the whole batch.
+  // Routing (measured per batch on the per-step problem mix, see
+  // scripts/id_bench.cu --replay): while the whole batch fits the chip in
+  // about two waves, the on-chip cooperative engine (exact CTA counts, one
+  // grid barrier per step) wins; crowded batches are throughput bound, where
+  // streaming TSQR (one CTA per tall problem, R0 on chip) and the
+  // register-resident cluster engine win.
   const int sms = sm_count();
-  i64 cluster_ctas = 0;
-  for (const auto& j : all) cluster_ctas += std::max(1, cpqr_cluster_size(j.M, j.n));
-  const bool crowded = cluster_ctas > 2 * i64(sms);
+  i64 chip_ctas = 0;
+  for (const auto& j : all) {
+    const int g = cpqr_smem_ctas(j.M, j.n);
+    chip_ctas += g > 0 ? g : sms;
+  }
+  const bool crowded = chip_ctas > 2 * i64(sms);
+  // streaming TSQR is slow per problem (all n Householder steps before the
+  // pivoted ones) and only pays off by sheer numbers of tall problems
+  i64 n_tall = 0;
+  for (const auto& j : all) n_tall += (j.n <= 144 && j.M > j.n && j.M <= 4096) ? 1 : 0;
+  const bool tsqr_crowd = crowded && n_tall >= sms / 2;
   static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
+  static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
+  static const bool no_reg = std::getenv("SBX_NO_REG") != nullptr;          // diagnostics
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
     if (engine == 0) {
-      // one CTA when the problem fits its shared memory (or is a short, tall
-      // TSQR case); else a thread-block cluster, else the on-chip cooperative
-      // engine when the slabs fit the GPU, else the L2-streaming cooperative
-      // engine for big problems
-      const bool tsqr_ok = j.n <= 144 && j.M > j.n && (j.M <= tsqr_max_m || (crowded && j.M <= 4096));
-      const bool one_cta = qr_smem_need(j.M, j.n) <= size_t(200 * 1024) || tsqr_ok;
       const int g = cpqr_smem_ctas(j.M, j.n);
-      static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
-      if (one_cta) engine = 1;
-      else if (!no_cluster && cpqr_cluster_size(j.M, j.n) > 0) engine = 4;
-      else if (no_coop_flag()) engine = 1;  // beside other streams: no grid-wide barriers
-      else if (g > 0 && g <= sms) engine = 3;
-      else if (i64(j.M) * j.n >= IdBatch::kCoopEntries) engine = 2;
+      const bool chip_ok = !no_coop_flag() && g > 0 && g <= sms;
+      const bool tsqr_ok = j.n <= 144 && j.M > j.n && (j.M <= tsqr_max_m || (tsqr_crowd && j.M <= 4096));
+      const bool one_cta = qr_smem_need(j.M, j.n) <= size_t(200 * 1024);
+      int rg = 0;
+      const int rc = no_reg ? -1 : cpqr_reg_config(j.M, j.n, &rg);
+      const int cs = cpqr_cluster_size(j.M, j.n);
+      if (!crowded && chip_ok) engine = 3;
+      else if (tsqr_ok) engine = 1;
+      else if (rc >= 0 && !(rc >= 3 && cs > 0 && cs < rg)) engine = 5;
+      else if (one_cta) engine = 1;
+      else if (!no_cluster && cs > 0) engine = 4;
+      else if (chip_ok) engine = 3;
+      else if (!no_coop_flag() && i64(j.M) * j.n >= IdBatch::kCoopEntries) engine = 2;
       else engine = 1;
     }
     if (log) line += " " + std::to_string(j.M) + "x" + std::to_string(j.n) + "/e" + std::to_string(engine);
-    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : jobs).push_back(j);
+    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : engine == 5 ? reg : jobs).push_back(j);
   }
   if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
   cpqr_smem_batched(chip, s);
   cpqr_cluster_batched(clus, s);
+  cpqr_reg_batched(reg, s);
 }
 
 // ---------------------------------------------------------------- rendezvous

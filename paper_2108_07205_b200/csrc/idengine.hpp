@@ -25,7 +25,7 @@ class IdBatch {
   void factor(const std::vector<IdProblem>& probs, double stop_eps, cudaStream_t s);
   // engine override for tests: 0 auto, 1 one CTA per problem, 2 cooperative
   // (slabs in L2), 3 cooperative on chip (slabs in shared memory), 4 one
-  // thread-block cluster per problem
+  // thread-block cluster per problem, 5 register-resident cluster
   int force_engine = 0;
   size_t size() const { return probs_.size(); }
   const IdProblem& problem(size_t p) const { return probs_[p]; }
