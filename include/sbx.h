@@ -208,6 +208,11 @@ int sbx_els_xw(sbx_els e, double* X, double* W);
 /* ---------------------------------------------------------- diagnostics
  * Number of sbx kernels launched since the last reset (bench evidence). */
 int64_t sbx_kernel_launches(int reset);
+/* CUDA-event timing of the named hot kernels on the stream they run on
+ * ("sweep_flow_dmma", "sweep_flow_gemv"): enable, then read the total
+ * milliseconds and launch count since the last reset. */
+int sbx_kernel_timing(int enable);
+int sbx_kernel_time(const char* name, int reset, double* total_ms, int64_t* count);
 
 /* Device row ID of a host matrix W (m x n, column-major) — idlib.cpp:73-99
  * (row_id; forced >= 0 selects row_id_rank).  engine: 0 auto, 1 one CTA per

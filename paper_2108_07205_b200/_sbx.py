@@ -11,6 +11,8 @@ from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_lib" / "libsbx.so"
+if os.environ.get("SBX_LIB_DIR"):  # diagnostics: an alternative in-tree build (e.g. _libexp)
+    LIB_PATH = _PKG / os.environ["SBX_LIB_DIR"] / "libsbx.so"
 
 I64 = C.c_int64
 I64P = C.POINTER(C.c_int64)
@@ -66,6 +68,8 @@ _SIGS = [
     ("sbx_sync", C.c_int, []),
     ("sbx_stream", C.c_void_p, []),
     ("sbx_kernel_launches", C.c_int64, [C.c_int]),
+    ("sbx_kernel_timing", C.c_int, [C.c_int]),
+    ("sbx_kernel_time", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_double), I64P]),
     ("sbx_row_id", C.c_int, [F64P, I64, I64, C.c_double, I64, C.c_int, I64P, I64P, F64P]),
     ("sbx_geom_create", C.c_int, [C.POINTER(sbx_curve), C.c_int, C.c_int, C.POINTER(VP)]),
     ("sbx_geom_add_holes", C.c_int,

@@ -537,6 +537,19 @@ def kernel_launches(reset: bool = False) -> int:
     return int(lib().sbx_kernel_launches(int(reset)))
 
 
+def kernel_timing(enable: bool = True):
+    """CUDA-event timing of the named hot kernels (sbx_kernel_timing)."""
+    check(lib().sbx_kernel_timing(int(enable)))
+
+
+def kernel_time(name: str, reset: bool = True):
+    """(total ms, launches) of a timed kernel since the last reset."""
+    ms = C.c_double(0.0)
+    cnt = C.c_int64(0)
+    check(lib().sbx_kernel_time(name.encode(), int(reset), C.byref(ms), C.byref(cnt)))
+    return ms.value, cnt.value
+
+
 def gather_kept_added(plan: RefinementPlan, g_new):
     """scenario.cpp:253-258."""
     m = plan.maps()

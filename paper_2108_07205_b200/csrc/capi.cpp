@@ -79,6 +79,18 @@ int sbx_sync(void) {
 
 int64_t sbx_kernel_launches(int reset) { return sbx::launches(reset != 0); }
 
+int sbx_kernel_timing(int enable) {
+  return guard([&] { sbx::ktimer_enable(enable != 0); });
+}
+
+int sbx_kernel_time(const char* name, int reset, double* total_ms, int64_t* count) {
+  return guard([&] {
+    int64_t c = 0;
+    *total_ms = sbx::ktimer_total(name, reset != 0, &c);
+    if (count) *count = c;
+  });
+}
+
 int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
                int64_t* k, int64_t* J, double* P) {
   return guard([&] {

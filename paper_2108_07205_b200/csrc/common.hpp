@@ -43,6 +43,27 @@ inline void require(bool c, const std::string& m) {
 
 void count_launch();
 std::int64_t launches(bool reset);
+
+// Optional CUDA-event timing of named kernels (bench evidence: the
+// roofline's per-launch duration on the stream the kernel runs on).
+void ktimer_enable(bool on);
+bool ktimer_on();
+void ktimer_record(const char* name, cudaEvent_t begin, cudaEvent_t end);
+// Total milliseconds and launch count of `name` since the last reset
+// (synchronises on the recorded events).
+double ktimer_total(const char* name, bool reset, std::int64_t* count);
+class KernelTimer {
+ public:
+  KernelTimer(const char* name, cudaStream_t s);
+  ~KernelTimer();
+  KernelTimer(const KernelTimer&) = delete;
+  KernelTimer& operator=(const KernelTimer&) = delete;
+
+ private:
+  const char* name_;
+  cudaStream_t s_;
+  cudaEvent_t b_ = nullptr;
+};
 cudaStream_t lib_stream();
 
 // Stream-ordered caching device allocator (the per-step path allocates many

@@ -47,6 +47,54 @@ size_t size_class(size_t bytes) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<bool> g_ktimer{false};
+std::mutex g_ktimer_mu;
+std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> g_ktimes;
+}  // namespace
+
+void ktimer_enable(bool on) { g_ktimer.store(on); }
+bool ktimer_on() { return g_ktimer.load(std::memory_order_relaxed); }
+
+void ktimer_record(const char* name, cudaEvent_t begin, cudaEvent_t end) {
+  std::lock_guard<std::mutex> lk(g_ktimer_mu);
+  g_ktimes[name].push_back({begin, end});
+}
+
+double ktimer_total(const char* name, bool reset, std::int64_t* count) {
+  std::lock_guard<std::mutex> lk(g_ktimer_mu);
+  auto& v = g_ktimes[name];
+  double ms = 0.0;
+  for (auto& e : v) {
+    SBX_CUDA(cudaEventSynchronize(e.second));
+    float t = 0.0f;
+    SBX_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+    ms += t;
+  }
+  if (count) *count = std::int64_t(v.size());
+  if (reset) {
+    for (auto& e : v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    v.clear();
+  }
+  return ms;
+}
+
+KernelTimer::KernelTimer(const char* name, cudaStream_t s) : name_(name), s_(s) {
+  if (!ktimer_on()) return;
+  SBX_CUDA(cudaEventCreate(&b_));
+  SBX_CUDA(cudaEventRecord(b_, s_));
+}
+
+KernelTimer::~KernelTimer() {
+  if (!b_) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess || cudaEventRecord(e, s_) != cudaSuccess) return;
+  ktimer_record(name_, b_, e);
+}
+
 std::int64_t launches(bool reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }

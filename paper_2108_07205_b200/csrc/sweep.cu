@@ -130,8 +130,14 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
 // columns need not be 16-byte aligned) and B (workspace rows produced by
 // other CTAs of the launch: 16-byte .cg copies that bypass L1, whose lines
 // could hold stale neighbours of a just-published row).
-constexpr int kKC = 16;
-constexpr int kStages = 4;
+#ifndef SBX_DMMA_KC
+#define SBX_DMMA_KC 16
+#endif
+#ifndef SBX_DMMA_STAGES
+#define SBX_DMMA_STAGES 4
+#endif
+constexpr int kKC = SBX_DMMA_KC;
+constexpr int kStages = SBX_DMMA_STAGES;
 constexpr int kPad = 8;  // row stride 72 doubles
 
 // TN: columns per tile (64, or 32 to halve the work per item on the
@@ -165,9 +171,10 @@ template <int TN, int TM = kTM>
 __device__ __forceinline__ void dmma_issue_a(const double* __restrict__ fac, const SweepTask& t, int row0,
                                              int stage, int k0, int ke, DmmaSmem<TN>& S) {
   const double* A = fac + t.a_off;
+  static_assert((TM * kKC) % kThreads == 0, "A chunk split");
 #pragma unroll
-  for (int q = 0; q < TM / 16; ++q) {
-    const int idx = threadIdx.x + q * kThreads;  // TM x 16
+  for (int q = 0; q < TM * kKC / kThreads; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // TM x kKC
     const int kk = idx / TM, rr = idx % TM;
     const int grow = row0 + rr, gk = k0 + kk;
     const bool pa = grow < t.m && gk < ke;
@@ -180,9 +187,10 @@ __device__ __forceinline__ void dmma_issue_b(const double* __restrict__ ws, cons
                                              int nrhs, int ldw, int stage, int k0, int ke, DmmaSmem<TN>& S) {
   const double* B = ws + t.b_row * ldw;
   constexpr int kPairs = TN / 2;  // 16-byte pairs per B row
+  static_assert((kKC * kPairs) % kThreads == 0, "B chunk split");
 #pragma unroll
-  for (int q = 0; q < TN / 32; ++q) {
-    const int idx = threadIdx.x + q * kThreads;  // 16 rows x kPairs pairs
+  for (int q = 0; q < kKC * kPairs / kThreads; ++q) {
+    const int idx = threadIdx.x + q * kThreads;  // kKC rows x kPairs pairs
     const int kk = idx / kPairs, pr = (idx % kPairs) * 2;
     const int gk = k0 + kk, gcol = col0 + pr;
     int bytes = 0;
@@ -971,6 +979,7 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
   static const char* trace_path = std::getenv("SBX_SWEEP_TRACE");  // diagnostics: per-item timeline
   DevBuf<unsigned long long> trace;
   if (trace_path) trace.resize(size_t(4 * plan.n_flow_items));
+  KernelTimer kt(dmma ? "sweep_flow_dmma" : "sweep_flow_gemv", s);
   if (dmma)
     sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
                                                              int(plan.n_flow_items), plan.d_counters.get(), ncol,

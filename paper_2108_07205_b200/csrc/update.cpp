@@ -641,19 +641,21 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     phase_mark("update: A_pp inverse (for els_build)", w);
   };
   // SBX_PAR_MODE:
-  //   2 (default) every task in order on the library stream;
-  //   3 the near-field row IDs (whose big blocks need the
-  //     cooperative CPQR engines) in order on the library stream, then the
+  //   4 (default) the row-ID hierarchies of the update in lockstep on the
+  //     library stream, and the A_pp HBS build in a second host thread on
+  //     the SAME stream; both threads' CPQR batches meet in a rendezvous
+  //     and go out as one launch per round (no cross-stream co-scheduling);
+  //   2 the same without the second thread (A_pp after the IDs);
+  //   3 the near-field row IDs in order on the library stream, then the
   //     far-field hierarchies beside the A_pp build on two worker streams,
-  //     both restricted to engines without grid-wide barriers (one CTA or one
-  //     thread-block cluster per problem), which coexist with other streams;
+  //     both restricted to engines without grid-wide barriers;
   //   1 / 0 all row IDs beside A_pp / every task on its own stream.
-  // Measured on cfg2 (bench, 10 steps): serial 50 ms stable; modes 0/1/3
-  // 39-165 ms from run to run (co-scheduling of the large-smem CPQR kernels
-  // of two streams is not stable), so the default is serial.
+  // Measured on cfg2 (bench, 10 steps): mode 4 32-33 ms, mode 2 35 ms;
+  // modes 0/1/3 vary widely from run to run (co-scheduling of the
+  // large-smem CPQR kernels of two streams is not stable).
   static const int par_mode = [] {
     const char* e = std::getenv("SBX_PAR_MODE");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 4;
   }();
   if (par_mode == 2 || par_mode == 4) {
     // mode 4: the A_pp HBS build runs in a second host thread on the SAME

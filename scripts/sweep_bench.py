@@ -32,6 +32,9 @@ def main():
         with torch.cuda.stream(stream):
             for _ in range(3):
                 x = sb.hbs_solve(h, b)
+            sb.api.kernel_timing(True)
+            sb.api.kernel_time("sweep_flow_dmma")
+            sb.api.kernel_time("sweep_flow_gemv")
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -40,9 +43,13 @@ def main():
             e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
+        kname = "sweep_flow_gemv" if nrhs == 1 else "sweep_flow_dmma"
+        kms, kcnt = sb.api.kernel_time(kname)
+        sb.api.kernel_timing(False)
+        kms /= max(kcnt, 1)
         flops = 2.0 * nrhs * info["factor_doubles"]
-        print(f"nrhs={nrhs:4d}: {ms*1e3:9.1f} us  factor bytes {fb/1e6:.1f} MB -> "
-              f"{fb/ms/1e6:.1f} GB/s (1 pass), {flops/ms/1e9:.2f} TF/s", flush=True)
+        print(f"nrhs={nrhs:4d}: call {ms*1e3:8.1f} us, kernel {kms*1e3:8.1f} us  factor bytes {fb/1e6:.1f} MB"
+              f" -> kernel {fb/kms/1e6:.1f} GB/s (1 pass), {flops/kms/1e9:.2f} TF/s", flush=True)
 
 
 if __name__ == "__main__":
