@@ -54,6 +54,14 @@ struct FlowItem {
   int tile, pad;  // rows of this item
 };
 
+// Everything one dataflow item needs, denormalised so a CTA can prefetch the
+// descriptor of its next item with one asynchronous copy (144 bytes).
+struct alignas(16) ItemDesc {
+  FlowItem it;
+  SweepTask t;
+  int need[4];  // completed items awaited per producer task (same column tile)
+};
+
 struct SweepLevel {
   std::vector<SweepTask> tasks;
   i64 first_task = 0;  // index into the flattened device task table
@@ -72,6 +80,8 @@ struct SweepPlan {
   int flow_key = -1;
   std::vector<int2> level_items;
   DevBuf<FlowItem> d_flow_items;
+  DevBuf<ItemDesc> d_descs;        // per flow item (dataflow kernel)
+  std::vector<SweepTask> h_tasks;  // host copy of the flattened task table
   DevBuf<int> d_needs;             // items per task and column tile (dependency counts)
   i64 partial_elems = 0;           // split-K partial tiles (doubles)
   int n_tile_cnt = 0;

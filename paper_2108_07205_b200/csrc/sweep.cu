@@ -19,6 +19,8 @@
 
 #include "hbs.hpp"
 
+#include <type_traits>
+
 namespace sbx {
 
 namespace {
@@ -321,23 +323,41 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
                       const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
                       int n_items, int* __restrict__ counters, int ncol, int nrhs, int ldw,
                       double* __restrict__ partials, int* __restrict__ tile_cnt,
-                      unsigned long long* __restrict__ trace, const int* __restrict__ needs) {
+                      unsigned long long* __restrict__ trace, const ItemDesc* __restrict__ descs) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ int s_next, s_last;
+  __shared__ int s_last;
+  __shared__ __align__(16) ItemDesc sdesc[2];
   constexpr int tile_elems = kDmma ? kTM * TN : kGR;
-  int* ticket = counters;  // counters[0]; per-(task, col tile) counts follow
-  if (threadIdx.x == 0) s_next = atomicAdd(ticket, 1);
-  for (;;) {
+  constexpr int kDescChunks = int(sizeof(ItemDesc) / 16);
+  static_assert(sizeof(ItemDesc) % 16 == 0, "descriptor copies are 16-byte chunks");
+  // Static round-robin schedule: CTA b takes items b, b + G, ...  Items are
+  // in dependency order, a CTA waits only on items that precede its own and
+  // every CTA is resident, so the lowest unfinished item always has its
+  // producers done and its CTA working on it (no deadlock).  The descriptor
+  // of the next item is fetched asynchronously while the current one
+  // computes (no ticket atomics, no dependent descriptor loads).
+  const int G = int(gridDim.x);
+  if (threadIdx.x < kDescChunks && int(blockIdx.x) < n_items)
+    cp_async16_cg(reinterpret_cast<double*>(&sdesc[0]) + 2 * threadIdx.x,
+                  reinterpret_cast<const double*>(descs + blockIdx.x) + 2 * threadIdx.x, 16);
+  cp_async_commit();
+  for (int r = 0, idx = int(blockIdx.x);; ++r, idx += G) {
+    cp_async_wait<0>();
     __syncthreads();
-    const int idx = s_next;
-    __syncthreads();  // everyone has read s_next
     if (idx >= n_items) break;
-    int nxt = 0;
-    if (threadIdx.x == 0) nxt = atomicAdd(ticket, 1);  // next ticket, consumed at the end
+    if (threadIdx.x < kDescChunks && idx + G < n_items)
+      cp_async16_cg(reinterpret_cast<double*>(&sdesc[(r + 1) & 1]) + 2 * threadIdx.x,
+                    reinterpret_cast<const double*>(descs + idx + G) + 2 * threadIdx.x, 16);
+    cp_async_commit();
     unsigned long long t0 = 0, t1 = 0;
     if (trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    const FlowItem it = items[idx];
-    const SweepTask t = tasks[it.task];
+    const ItemDesc& D = sdesc[r & 1];
+    // DMMA items keep the descriptor in registers (their K loop reads it per
+    // chunk); GEMV items read it from shared memory on use
+    using ItT = std::conditional_t<kDmma, const FlowItem, const FlowItem&>;
+    using TaskT = std::conditional_t<kDmma, const SweepTask, const SweepTask&>;
+    ItT it = D.it;
+    TaskT t = D.t;
     GemvRegs g;
     const bool small = it.tile != (kDmma ? kTM : kGR);
     if constexpr (kDmma) {
@@ -350,8 +370,8 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
     else
       gemv_prefetch<kGR>(fac, t, it.row0, it.kb, it.ke, g);
     if (threadIdx.x < t.ndep) {
-      const int d = tasks[it.task].dep[threadIdx.x];
-      const int need = needs[d];
+      const int d = t.dep[threadIdx.x];
+      const int need = D.need[threadIdx.x];
       const int* p = counters + 1 + d * ncol + it.ct;
       while (ld_acquire(p) < need) __nanosleep(32);
     }
@@ -412,7 +432,6 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
         __threadfence();  // cumulative: covers every thread's stores ordered by the barrier
         atomicAdd(counters + 1 + it.task * ncol + it.ct, 1);
       }
-      s_next = nxt;
       if (trace) {
         unsigned long long t2;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
@@ -591,6 +610,7 @@ void finalize(SweepPlan& plan) {
   plan.flow_key = -1;
   const cudaStream_t st = cur_stream();
   plan.d_tasks.upload(all, st);
+  plan.h_tasks = all;
   SBX_CUDA(cudaStreamSynchronize(st));
   plan.built = true;
 }
@@ -953,6 +973,14 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
                    dmma ? small_below_dmma : 600);
     plan.d_flow_items.upload(fi, s);
     plan.d_needs.upload(needs, s);
+    std::vector<ItemDesc> descs(fi.size());
+    for (size_t q = 0; q < fi.size(); ++q) {
+      ItemDesc& D = descs[q];
+      D.it = fi[q];
+      D.t = plan.h_tasks[size_t(fi[q].task)];
+      for (int d = 0; d < 4; ++d) D.need[d] = d < D.t.ndep ? needs[size_t(D.t.dep[d])] : 0;
+    }
+    plan.d_descs.upload(descs, s);
     plan.n_flow_items = i64(fi.size());
     plan.flow_key = key;
   }
@@ -984,13 +1012,13 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
     sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
                                                              int(plan.n_flow_items), plan.d_counters.get(), ncol,
                                                              int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
-                                                             tile_cnt, trace.get(), plan.d_needs.get());
+                                                             tile_cnt, trace.get(), plan.d_descs.get());
   else
     sweep_flow_kernel<false, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
                                                               plan.d_flow_items.get(), int(plan.n_flow_items),
                                                               plan.d_counters.get(), ncol, int(nrhs), 1,
                                                               plan.d_partials.get(), tile_cnt, trace.get(),
-                                                              plan.d_needs.get());
+                                                              plan.d_descs.get());
   SBX_LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(size_t(4 * plan.n_flow_items));
