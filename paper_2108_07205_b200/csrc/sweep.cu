@@ -84,10 +84,13 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
   const int K = t.K;
   double* xs = sm;                    // K doubles
   double* red = sm + ((K + 1) & ~1);  // kThreads partial sums
-  for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(ws + t.b_row + j);
-  __syncthreads();
   const int r = threadIdx.x % GR, slice = threadIdx.x / GR;
   const int row = row0 + r;
+  // the P row is fetched together with the input vector (one round trip on
+  // the critical path instead of two)
+  const double pv = (slice == 0 && row < t.m && t.p_row >= 0 && !partial) ? __ldcg(ws + t.p_row + row) : 0.0;
+  for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(ws + t.b_row + j);
+  __syncthreads();
   double acc = 0.0, acc1 = 0.0;
 #pragma unroll
   for (int q = 0; q < kGV; q += 2) {
@@ -120,7 +123,7 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
       partial[r] = s;
       return;
     }
-    if (t.p_row >= 0) s += __ldcg(ws + t.p_row + row);
+    if (t.p_row >= 0) s += pv;
     const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
     ws[dst] = s;
   }
