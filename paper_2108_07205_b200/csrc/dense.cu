@@ -1605,6 +1605,272 @@ __global__ void __launch_bounds__(kOT, 1) cpqr_reg_kernel(const QrJob* __restric
   }
 }
 
+// ---------------------------------------------------------------- streaming one-CTA CPQR
+// One CTA (16 warps) per problem; the first ns columns of W^T live in shared
+// memory, the rest are updated in place in global memory (L2 resident for
+// these sizes), so any M <= 32 RPL fits one SM and a crowded batch needs one
+// SM per problem instead of a cluster.  Warp w owns columns w, w + 16, ...;
+// a column is processed in registers (lane l: rows l + 32 r, only rows >= j
+// touched at step j).  Per step: warp-local candidate (after its downdate),
+// one CTA barrier, the owner warp of the winner builds the Householder
+// vector (v_j = 1 stored explicitly), a second barrier, then every warp
+// reflects its live columns (read, dot, update, write back, downdate).
+// Pivot rule, stop rule and R layout as the other engines; results agree to
+// rounding.
+struct StreamCand {
+  double val;
+  int pos, col;
+};
+
+template <int RPL>
+__device__ __forceinline__ double reg_row(const double (&x)[RPL], int r) {
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < RPL; ++q)
+    if (q == r) v = x[q];
+  return v;
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(kOT, 1) cpqr_stream_kernel(const QrJob* __restrict__ jobs, int ns_cap) {
+  extern __shared__ double ssm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n, lda = jb.lda;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int MR = 32 * RPL;
+  const int size = min(M, n);
+  double* v = ssm;                        // MR: Householder vector of the step (v_j = 1)
+  double* upd = v + MR;                   // n
+  double* dir = upd + n;                  // n
+  double* betas = dir + n;                // size
+  int* pos = reinterpret_cast<int*>(betas + size);  // n
+  int* pst = pos + n;                               // n
+  double* S = betas + size + (n + 1);     // ns x M resident slab (ld M)
+  const int ns = min(n, ns_cap);
+  __shared__ StreamCand wbest[kOWarps];
+  __shared__ double s_beta, s_tau;
+  auto colp = [&](int c) -> double* { return c < ns ? S + size_t(c) * M : jb.a + size_t(c) * lda; };
+  // load the resident slab, column norms, positions
+  for (int c = warp; c < n; c += kOWarps) {
+    double* dst = colp(c);
+    const double* src = jb.a + size_t(c) * lda;
+    double sq = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < M) {
+        const double x = src[i];
+        if (c < ns) dst[i] = x;
+        sq += x * x;
+      }
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) {
+      upd[c] = dir[c] = sqrt(sq);
+      pos[c] = c;
+      pst[c] = -1;
+    }
+  }
+  for (int i = tid; i < MR; i += kOT) v[i] = 0.0;
+  __syncthreads();
+  // warp candidates of step 0
+  auto warp_candidate = [&]() {
+    double bv = -1.0;
+    int bp = 0x7fffffff, bc = -1;
+    for (int c = warp + kOWarps * lane; c < n; c += kOWarps * 32) {
+      const int pc = pos[c];
+      if (pc >= 0 && better(upd[c], pc, bv, bp)) {
+        bv = upd[c];
+        bp = pc;
+        bc = c;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (better(ov, op, bv, bp)) {
+        bv = ov;
+        bp = op;
+        bc = oc;
+      }
+    }
+    if (lane == 0) wbest[warp] = {bc >= 0 ? bv : -1.0, bc >= 0 ? bp : 0x7fffffff, bc};
+  };
+  warp_candidate();
+  const int steps_max = jb.max_steps > 0 ? min(size, jb.max_steps) : size;
+  const double thr = sqrt(DBL_EPSILON);
+  int done = 0;
+  double r00 = 0.0;
+  for (int j = 0; j < steps_max; ++j) {
+    const int rj = j >> 5, lj = j & 31;
+    __syncthreads();  // candidates published; previous reflections written
+    // CTA winner (every warp computes it)
+    StreamCand w = lane < kOWarps ? wbest[lane] : StreamCand{-1.0, 0x7fffffff, -1};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, w.val, o);
+      const int op = __shfl_xor_sync(0xffffffffu, w.pos, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, w.col, o);
+      if (better(ov, op, w.val, w.pos)) w = {ov, op, oc};
+    }
+    const int p = w.col, lp = w.pos;
+    if (warp == (p & (kOWarps - 1))) {  // owner builds the Householder vector
+      const double* pc = colp(p);
+      double a[RPL];
+      double part = 0.0, ccl = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        a[r] = (i >= j && i < M) ? pc[i] : 0.0;
+        if (i > j) part += a[r] * a[r];
+        if (r == rj) ccl = a[r];
+      }
+      const double tail = warp_sum(part);
+      const double cc = __shfl_sync(0xffffffffu, ccl, lj);
+      double beta, tau, denom;
+      if (tail <= DBL_MIN) {
+        tau = 0.0;
+        beta = cc;
+        denom = 0.0;
+      } else {
+        beta = sqrt(cc * cc + tail);
+        if (cc >= 0.0) beta = -beta;
+        denom = cc - beta;
+        tau = (beta - cc) / beta;
+      }
+      const double rd = denom == 0.0 ? 0.0 : 1.0 / denom;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= j - 1 && i < MR) v[i] = i > j ? a[r] * rd : (i == j ? 1.0 : 0.0);
+      }
+      if (lane == 0) {
+        s_beta = beta;
+        s_tau = tau;
+        betas[j] = beta;
+        jb.perm[j] = p;
+      }
+    }
+    // positions (each warp its own columns; the winner's owner marks it)
+    for (int c = warp + kOWarps * lane; c < n; c += kOWarps * 32) {
+      if (c == p) {
+        pos[c] = -1;
+        pst[c] = j;
+      } else if (pos[c] == j) {
+        pos[c] = lp;
+      }
+    }
+    __syncthreads();  // v, beta, tau, positions visible
+    const double beta = s_beta, tau = s_tau;
+    if (j == 0) r00 = fabs(beta);
+    done = j + 1;
+    if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    const bool refl = tau != 0.0 && M - j > 1;
+    // CPI columns per pass share the loads of v and the row masks; row
+    // blocks below j are skipped (warp-uniform), v is zero there anyway
+    constexpr int CPI = RPL <= 20 ? 2 : 1;
+    for (int cb = warp; cb < n; cb += CPI * kOWarps) {
+      int cc[CPI];
+      bool live[CPI], any = false;
+      double* colv[CPI];
+#pragma unroll
+      for (int u = 0; u < CPI; ++u) {
+        cc[u] = cb + u * kOWarps;
+        live[u] = cc[u] < n && pos[cc[u]] >= 0;
+        any |= live[u];
+        colv[u] = live[u] ? colp(cc[u]) : nullptr;
+      }
+      if (!any) continue;  // warp-uniform
+      double a[CPI][RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int i = lane + 32 * r;
+        const bool ok = r >= rj && i >= j && i < M;
+#pragma unroll
+        for (int u = 0; u < CPI; ++u) a[u][r] = (ok && live[u]) ? colv[u][i] : 0.0;
+      }
+      double rowj[CPI];
+#pragma unroll
+      for (int u = 0; u < CPI; ++u) rowj[u] = 0.0;
+      if (refl) {
+        double d[CPI];
+#pragma unroll
+        for (int u = 0; u < CPI; ++u) d[u] = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          if (r < rj) continue;
+          const double vi = v[lane + 32 * r];
+#pragma unroll
+          for (int u = 0; u < CPI; ++u) d[u] += vi * a[u][r];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < CPI; ++u) d[u] += __shfl_xor_sync(0xffffffffu, d[u], o);
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          if (r < rj) continue;
+          const int i = lane + 32 * r;
+          const double vi = v[i];
+          const bool st = i >= j && i < M;
+#pragma unroll
+          for (int u = 0; u < CPI; ++u) {
+            a[u][r] -= vi * (tau * d[u]);
+            if (st && live[u]) colv[u][i] = a[u][r];
+            if (r == rj) rowj[u] = a[u][r];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < CPI; ++u) rowj[u] = reg_row(a[u], rj);
+      }
+#pragma unroll
+      for (int u = 0; u < CPI; ++u) {
+        if (!live[u]) continue;
+        const int c = cc[u];
+        const double colj = __shfl_sync(0xffffffffu, rowj[u], lj);
+        const double uu = upd[c];
+        if (uu == 0.0) continue;
+        double t = fabs(colj) / uu;
+        t = (1.0 + t) * (1.0 - t);
+        t = t < 0.0 ? 0.0 : t;
+        const double rr = uu / dir[c];
+        if (t * rr * rr <= thr) {
+          double sq = 0.0;
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const int i = lane + 32 * r;
+            if (i > j) sq += a[u][r] * a[u][r];
+          }
+          sq = sqrt(warp_sum(sq));
+          if (lane == 0) upd[c] = dir[c] = sq;
+        } else if (lane == 0) {
+          upd[c] = uu * sqrt(t);
+        }
+      }
+    }
+    __syncwarp();
+    warp_candidate();
+  }
+  __syncthreads();
+  // write back: resident columns, and the R diagonal of the pivoted ones
+  for (int c = warp; c < n; c += kOWarps) {
+    double* dst = jb.a + size_t(c) * lda;
+    const int ps = pst[c];
+    if (c < ns) {
+      const double* src = S + size_t(c) * M;
+      for (int i = lane; i < M; i += 32) dst[i] = i == ps ? betas[i] : src[i];
+    } else if (ps >= 0 && lane == 0) {
+      dst[ps] = betas[ps];
+    }
+    if (lane == 0 && pos[c] >= 0) jb.perm[pos[c]] = c;
+  }
+  for (int l = tid; l < size; l += kOT) jb.diag[l] = l < done ? fabs(betas[l]) : 0.0;
+  if (tid == 0 && jb.steps) *jb.steps = done;
+}
+
 // ---------------------------------------------------------------- interpolation
 // One work item = (job, first column of a 128-column chunk of R12), or
 // (job, -1) for the k identity rows.  Every row of P is written exactly once,
@@ -2882,6 +3148,69 @@ void launch_reg(const QrJob* d, int np, int G, int size_max, cudaStream_t s) {
   SBX_LAUNCHED();
 }
 }  // namespace
+
+namespace {
+constexpr int kStreamRpl[] = {9, 17, 20, 27, 34};
+size_t stream_fixed_doubles(int M, int n, int rpl) {
+  return size_t(32 * rpl) + 3 * size_t(n) + size_t(std::min(M, n)) + size_t(n) + 1;
+}
+template <int RPL>
+void launch_stream(const QrJob* d, int np, int ns_cap, size_t smem, cudaStream_t s) {
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(cpqr_stream_kernel<RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kSmemCap)));
+  });
+  cpqr_stream_kernel<RPL><<<unsigned(np), kOT, smem, s>>>(d, ns_cap);
+  SBX_LAUNCHED();
+}
+}  // namespace
+
+bool cpqr_stream_ok(int M, int n) {
+  if (M <= 0 || n <= 0 || M > 32 * 34) return false;
+  int rpl = 0;
+  for (int r : kStreamRpl)
+    if (32 * r >= M) {
+      rpl = r;
+      break;
+    }
+  return stream_fixed_doubles(M, n, rpl) * sizeof(double) + size_t(M) * sizeof(double) <= kSmemCap;
+}
+
+void cpqr_stream_batched(const std::vector<QrJob>& all, cudaStream_t s) {
+  if (all.empty()) return;
+  // one launch per register layout; the resident slab takes what the
+  // fixed tables leave of the shared memory
+  std::vector<QrJob> cls[5];
+  for (const auto& j : all) {
+    require(cpqr_stream_ok(j.M, j.n), "cpqr_stream: problem does not fit the streaming engine");
+    int c = 0;
+    while (32 * kStreamRpl[c] < j.M) ++c;
+    cls[c].push_back(j);
+  }
+  static thread_local JobTable<QrJob> tj[5];
+  for (int c = 0; c < 5; ++c) {
+    if (cls[c].empty()) continue;
+    size_t fixed = 0;
+    int Mmax = 1;
+    for (const auto& j : cls[c]) {
+      fixed = std::max(fixed, stream_fixed_doubles(j.M, j.n, kStreamRpl[c]));
+      Mmax = std::max(Mmax, j.M);
+    }
+    const size_t cap = kSmemCap / sizeof(double);
+    const int ns_cap = int((cap - fixed) / size_t(Mmax));
+    const size_t smem = kSmemCap;
+    const QrJob* d = tj[c].upload(cls[c], s);
+    const int np = int(cls[c].size());
+    switch (c) {
+      case 0: launch_stream<9>(d, np, ns_cap, smem, s); break;
+      case 1: launch_stream<17>(d, np, ns_cap, smem, s); break;
+      case 2: launch_stream<20>(d, np, ns_cap, smem, s); break;
+      case 3: launch_stream<27>(d, np, ns_cap, smem, s); break;
+      default: launch_stream<34>(d, np, ns_cap, smem, s); break;
+    }
+  }
+}
 
 int cpqr_reg_config(int M, int n, int* G) {
   if (M <= 0 || n <= 0) return -1;

@@ -59,6 +59,10 @@ void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // M <= 1088): returns the layout index (G set) or -1 when it does not apply.
 int cpqr_reg_config(int M, int n, int* G);
 void cpqr_reg_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Streaming one-CTA CPQR (M <= 1088): columns beyond the shared-memory slab
+// are updated in place in global memory (L2).
+bool cpqr_stream_ok(int M, int n);
+void cpqr_stream_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 
 // ---------------------------------------------------------------- ID interpolation
 // Given a pivoted factor (R in the upper triangle of a, ld lda, n columns)

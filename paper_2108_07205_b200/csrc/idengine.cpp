@@ -55,7 +55,7 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
-  std::vector<QrJob> jobs, big, chip, clus, reg;
+  std::vector<QrJob> jobs, big, chip, clus, reg, strm;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
@@ -102,7 +102,8 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
       else engine = 1;
     }
     if (log) line += " " + std::to_string(j.M) + "x" + std::to_string(j.n) + "/e" + std::to_string(engine);
-    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : engine == 5 ? reg : jobs).push_back(j);
+    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : engine == 5 ? reg : engine == 6 ? strm : jobs)
+        .push_back(j);
   }
   if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
   qr_batched(jobs, s);
@@ -110,6 +111,7 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   cpqr_smem_batched(chip, s);
   cpqr_cluster_batched(clus, s);
   cpqr_reg_batched(reg, s);
+  cpqr_stream_batched(strm, s);
 }
 
 // ---------------------------------------------------------------- rendezvous

@@ -129,3 +129,24 @@ def test_row_id_register_engine(sb, po, shape):
     if k + 3 <= r:
         kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=5)
         assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
+
+
+@pytest.mark.parametrize("shape", [(50, 30), (200, 100), (128, 700), (256, 513), (900, 128), (256, 257),
+                                   (256, 1088), (4, 9), (2000, 300)])
+def test_row_id_streaming_engine(sb, po, shape):
+    """Streaming one-CTA CPQR (engine 6; slab partly in shared memory, the
+    rest updated in place in L2): oracle pivots and forced-rank extension."""
+    m, n = shape
+    rng = np.random.default_rng(m + 7 * n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=6)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    if k + 3 <= r:
+        kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=6)
+        assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
