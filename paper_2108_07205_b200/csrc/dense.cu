@@ -2525,6 +2525,107 @@ __global__ void __launch_bounds__(kT) gj_inverse_kernel(const LuJob* __restrict_
   }
 }
 
+// Gauss-Jordan for 128 < n <= 160 with the matrix in shared memory (the
+// register tile would not fit): same pivoting and unscrambling as above; per
+// step one warp picks the pivot, the pivot row and column are staged, every
+// thread updates its elements.
+__global__ void __launch_bounds__(kT) gj_inverse_smem_kernel(const LuJob* __restrict__ jobs) {
+  extern __shared__ double sm[];
+  const LuJob jb = jobs[blockIdx.x];
+  const int n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* A = sm;                     // n x n, ld n
+  double* col = A + size_t(n) * n;    // n
+  double* row = col + n;              // n
+  double* red = row + n;              // 64
+  int* ired = reinterpret_cast<int*>(red + 64);  // 64
+  int* pivrow = ired + 64;            // n
+  int* rowstep = pivrow + n;          // n
+  int* used = rowstep + n;            // n
+  __shared__ int s_p, s_sing;
+  __shared__ double s_l1;
+  // element ownership: row ti of columns tj, tj + cpp, ...
+  const int R = (n + 31) / 32 * 32, cpp = kT / R;
+  const int ti = tid % R, tj = tid / R;
+  if (tid == 0) {
+    s_sing = 0;
+    s_l1 = 0.0;
+  }
+  for (int c = warp; c < n; c += kWarps) {
+    double cs = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double x = jb.a[i + size_t(c) * jb.lda];
+      A[i + size_t(c) * n] = x;
+      cs += fabs(x);
+    }
+    cs = warp_sum(cs);
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_l1), __double_as_longlong(cs));
+  }
+  for (int i = tid; i < n; i += kT) used[i] = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      double bv = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = lane; i < n; i += 32) {
+        const double v = fabs(A[i + size_t(k) * n]);
+        if (!used[i] && v > bv) {
+          bv = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        pivrow[k] = bi;
+        rowstep[bi] = k;
+        used[bi] = 1;
+        if (!(bv > 0.0)) s_sing = 1;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double piv = A[p + size_t(k) * n];
+    const double rinv = piv != 0.0 ? 1.0 / piv : 0.0;
+    for (int j = tid; j < n; j += kT) {
+      const double u = j == k ? rinv : A[p + size_t(j) * n] * rinv;
+      row[j] = u;
+      A[p + size_t(j) * n] = u;
+      col[j] = A[j + size_t(k) * n];
+    }
+    __syncthreads();
+    if (ti < n && tj < cpp && ti != p) {
+      const double f = col[ti];
+      for (int j = tj; j < n; j += cpp) {
+        double* a = A + ti + size_t(j) * n;
+        *a = j == k ? -f * rinv : *a - f * row[j];
+      }
+    }
+    __syncthreads();
+  }
+  if (ti < n && tj < cpp) {
+    const size_t o = size_t(rowstep[ti]);
+    for (int m = tj; m < n; m += cpp) jb.inv[o + size_t(pivrow[m]) * n] = A[ti + size_t(m) * n];
+  }
+  for (int q = tid; q < n; q += kT) jb.piv[q] = pivrow[q];
+  __syncthreads();
+  if (jb.rcond) {
+    const double r = s_sing ? 0.0 : rcond_from_inverse(jb.inv, n, s_l1, jb.work, red, ired);
+    if (tid == 0) *jb.rcond = r;
+  }
+}
+
+constexpr int kGjSmemMax = 160;
+size_t gj_smem_bytes(int n) { return (size_t(n) * n + 2 * size_t(n) + 64 + 32 + 2 * size_t(n)) * sizeof(double); }
+
 constexpr int kGjMax = 128;
 size_t gj_smem(int n) { return (size_t(n) * n + 256 + 256 + 64 + 32 + 128) * sizeof(double); }
 
@@ -3478,7 +3579,27 @@ void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
         gj_inverse_kernel<4, 8><<<g, kT, sm, s>>>(d);
       SBX_LAUNCHED();
     }
-    jobs = rest;
+    // 128 < n <= 160: shared-memory Gauss-Jordan
+    std::vector<LuJob> mid, rest2;
+    for (const auto& j : rest) (j.n <= kGjSmemMax ? mid : rest2).push_back(j);
+    if (!mid.empty()) {
+      int nmax = 1;
+      for (const auto& j : mid) {
+        require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+        require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
+        nmax = std::max(nmax, j.n);
+      }
+      static std::once_flag mattr;
+      std::call_once(mattr, [] {
+        SBX_CUDA(cudaFuncSetAttribute(gj_inverse_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(gj_smem_bytes(kGjSmemMax))));
+      });
+      static thread_local JobTable<LuJob> mtab;
+      const LuJob* d = mtab.upload(mid, s);
+      gj_inverse_smem_kernel<<<unsigned(mid.size()), kT, gj_smem_bytes(nmax), s>>>(d);
+      SBX_LAUNCHED();
+    }
+    jobs = rest2;
     if (jobs.empty()) return;
   }
   static thread_local JobTable<LuJob> tab;
