@@ -277,7 +277,17 @@ def roofline_solve(sb, torch, stream, h, state, G_dev):
             "achieved": round(achieved, 3), "peak": peaks["value"], "unit": "TFLOP/s",
             "frac": round(achieved / peaks["value"], 4), "peak_source": peaks["source"],
             "launch_ms": round(ms, 4), "call_ms": round(call_ms, 4), "algorithmic_flops": flops,
-            "traffic": None}
+            "traffic": measured_traffic("sweep_dmma")}
+
+
+def measured_traffic(kernel):
+    """DRAM bytes (read + write) per launch of the roofline kernel from the
+    committed ncu --set full capture (profiles/r01_traffic.json), else None."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        return d[kernel]["traffic_bytes"]
+    except Exception:
+        return None
 
 
 def measured_fp64_peak():

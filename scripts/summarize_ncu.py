@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 
-def launches(path):
+def launches(path, what="the whole bench.py process (setup + warm-up + timed + e2e + roofline steps)"):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hi]
@@ -27,9 +27,8 @@ def launches(path):
         agg[name][1] += us
         tot += us
     print(f"# ncu launch list summary: `{path}`\n")
-    print("`ncu --metrics gpu__time_duration.sum --clock-control none` over the whole bench.py "
-          "process (setup + warm-up + timed + e2e + roofline steps); cold-cache serialised "
-          "launches, so compare shares, not absolutes.\n")
+    print(f"`ncu --metrics gpu__time_duration.sum --clock-control none` over {what}; cold-cache "
+          "serialised launches, so compare shares, not absolutes.\n")
     print(f"Total kernel time {tot / 1e3:.2f} ms over {len(data)} launches.\n")
     print("| kernel | launches | total ms | share | mean us |")
     print("|---|---:|---:|---:|---:|")
@@ -114,4 +113,4 @@ def report(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "report": report, "steplist": steplist}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "report": report, "steplist": steplist}[sys.argv[1]](*sys.argv[2:])
