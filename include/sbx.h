@@ -185,13 +185,17 @@ int sbx_els_info(sbx_els e, int64_t* info);
 /* g_n: (n_k + n_p) x nrhs (kept, added); tau_n same shape. */
 int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, double* tau_n,
                   int64_t ldt, int flags, void* stream);
-/* g_ext: n_ext x nrhs (kept, cut, added). */
+/* g_ext: n_ext x nrhs (kept, cut, added).  flags & SBX_TRANSPOSE:
+ * els_solve_raw_t (els.cpp:154-163), y = ELS^{-T} g_ext. */
 int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs, double* y,
                       int64_t ldy, int flags, void* stream);
 /* els_apply_forward (els.cpp:181-186): out = (Atilde + L R) v on the extended
  * system (host buffers, n_ext x nrhs, column-major). */
 int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out,
                           int64_t ldo);
+/* els_apply_forward_t (els.cpp:188-193): out = (Atilde + L R)^T v. */
+int sbx_els_apply_forward_t(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out,
+                            int64_t ldo);
 /* GMRES / PGMRES-Local (gmres.cpp:14-126 driven as scenario.cpp:694-727):
  * solves the refined system on the (kept, added) unknowns with operator
  * els_apply_forward (els.cpp:181-186) and, when precond != 0, the left

@@ -115,6 +115,7 @@ _SIGS = [
     ("sbx_els_solve_raw", C.c_int, [VP, VP, I64, I64, VP, I64, C.c_int, VP]),
     ("sbx_els_density_on_refined", C.c_int, [VP, F64P, F64P]),
     ("sbx_els_apply_forward", C.c_int, [VP, F64P, I64, I64, F64P, I64]),
+    ("sbx_els_apply_forward_t", C.c_int, [VP, F64P, I64, I64, F64P, I64]),
     ("sbx_els_gmres", C.c_int, [VP, F64P, F64P, C.c_int, C.c_double, I64, I64, I64P, F64P, I64]),
     ("sbx_els_xw", C.c_int, [VP, F64P, F64P]),
 ]

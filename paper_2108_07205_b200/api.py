@@ -320,7 +320,7 @@ def torch_stream_handle():
     return s if s else CUDA_STREAM_LEGACY
 
 
-def _sweep(fn, op_ptr, b, n, stream=None):
+def _sweep(fn, op_ptr, b, n, stream=None, flags=0):
     """Column-major n x nrhs sweep through the C-ABI (host numpy or CUDA torch)."""
     if _is_torch_cuda(b):
         import torch
@@ -332,7 +332,7 @@ def _sweep(fn, op_ptr, b, n, stream=None):
         out = torch.empty_like(bcm)
         s = stream if stream is not None else torch_stream_handle()
         check(fn(op_ptr, VP(bcm.data_ptr()), n, bt.shape[1], VP(out.data_ptr()), n,
-                 _sbx.SBX_DEVICE_PTRS, VP(s)))
+                 _sbx.SBX_DEVICE_PTRS | flags, VP(s)))
         res = out.t()
         return res.reshape(-1) if vec else res
     arr = np.asarray(b, dtype=np.float64)
@@ -341,18 +341,18 @@ def _sweep(fn, op_ptr, b, n, stream=None):
     if a2.shape[0] != n:
         raise ValueError("sweep: size mismatch")
     out = np.zeros_like(a2, order="F")
-    check(fn(op_ptr, VP(a2.ctypes.data), n, a2.shape[1], VP(out.ctypes.data), n, 0, VP()))
+    check(fn(op_ptr, VP(a2.ctypes.data), n, a2.shape[1], VP(out.ctypes.data), n, flags, VP()))
     return out[:, 0] if vec else out
 
 
-def hbs_solve(op: HbsOperator, b):
-    """hbs.cpp:589-625."""
-    return _sweep(lib().sbx_hbs_solve, op.ptr, b, op.n)
+def hbs_solve(op: HbsOperator, b, transpose: bool = False):
+    """hbs.cpp:589-625; transpose: hbs_solve_t (hbs.cpp:627-664)."""
+    return _sweep(lib().sbx_hbs_solve, op.ptr, b, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0)
 
 
-def hbs_apply(op: HbsOperator, v):
-    """hbs.cpp:511-544."""
-    return _sweep(lib().sbx_hbs_apply, op.ptr, v, op.n)
+def hbs_apply(op: HbsOperator, v, transpose: bool = False):
+    """hbs.cpp:511-544; transpose: hbs_apply_t (hbs.cpp:546-587)."""
+    return _sweep(lib().sbx_hbs_apply, op.ptr, v, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0)
 
 
 def hbs_save(op: HbsOperator, path):
@@ -445,7 +445,7 @@ def els_build(a_oo: HbsOperator, d_old: Discretization, d_new: Discretization,
     return ElsSolver(out, a_oo)
 
 
-def _els_call(fn, s: ElsSolver, g, rows_in):
+def _els_call(fn, s: ElsSolver, g, rows_in, flags=0):
     if _is_torch_cuda(g):
         import torch
         vec = g.dim() == 1
@@ -453,7 +453,7 @@ def _els_call(fn, s: ElsSolver, g, rows_in):
         gcm = gt.t().contiguous()
         out = torch.empty_like(gcm)
         check(fn(s.ptr, VP(gcm.data_ptr()), rows_in, gt.shape[1], VP(out.data_ptr()), rows_in,
-                 _sbx.SBX_DEVICE_PTRS, VP(torch_stream_handle())))
+                 _sbx.SBX_DEVICE_PTRS | flags, VP(torch_stream_handle())))
         res = out.t()
         return res.reshape(-1) if vec else res
     a = np.asarray(g, dtype=np.float64)
@@ -462,7 +462,7 @@ def _els_call(fn, s: ElsSolver, g, rows_in):
     if a2.shape[0] != rows_in:
         raise ValueError("els_solve: data size mismatch")
     out = np.zeros_like(a2, order="F")
-    check(fn(s.ptr, VP(a2.ctypes.data), rows_in, a2.shape[1], VP(out.ctypes.data), rows_in, 0, VP()))
+    check(fn(s.ptr, VP(a2.ctypes.data), rows_in, a2.shape[1], VP(out.ctypes.data), rows_in, flags, VP()))
     return out[:, 0] if vec else out
 
 
@@ -472,19 +472,21 @@ def els_solve(s: ElsSolver, g_n):
     return _els_call(lib().sbx_els_solve, s, g_n, i["n_k"] + i["n_p"])
 
 
-def els_solve_raw(s: ElsSolver, g_ext):
-    """els.cpp:147-152 on extended (kept, cut, added) vectors."""
-    return _els_call(lib().sbx_els_solve_raw, s, g_ext, s.n_ext())
+def els_solve_raw(s: ElsSolver, g_ext, transpose: bool = False):
+    """els.cpp:147-152 on extended (kept, cut, added) vectors; transpose:
+    els_solve_raw_t (els.cpp:154-163)."""
+    return _els_call(lib().sbx_els_solve_raw, s, g_ext, s.n_ext(), _sbx.SBX_TRANSPOSE if transpose else 0)
 
 
-def els_apply_forward(s: ElsSolver, v) -> np.ndarray:
-    """els.cpp:181-186: (Atilde + L R) v on the extended system (n_ext [x nrhs])."""
+def els_apply_forward(s: ElsSolver, v, transpose: bool = False) -> np.ndarray:
+    """els.cpp:181-186: (Atilde + L R) v on the extended system (n_ext [x nrhs]);
+    transpose: els_apply_forward_t (els.cpp:188-193)."""
     a = np.asfortranarray(np.asarray(v, dtype=np.float64))
     vec = a.ndim == 1
     a2 = a.reshape(-1, 1, order="F") if vec else a
     out = np.zeros_like(a2, order="F")
-    check(lib().sbx_els_apply_forward(s.ptr, a2.ctypes.data_as(F64P), a2.shape[0], a2.shape[1],
-                                      out.ctypes.data_as(F64P), a2.shape[0]))
+    fn = lib().sbx_els_apply_forward_t if transpose else lib().sbx_els_apply_forward
+    check(fn(s.ptr, a2.ctypes.data_as(F64P), a2.shape[0], a2.shape[1], out.ctypes.data_as(F64P), a2.shape[0]))
     return out[:, 0] if vec else out
 
 

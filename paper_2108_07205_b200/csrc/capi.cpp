@@ -288,8 +288,11 @@ int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double*
                   int flags, void* stream) {
   return guard([&] {
     sbx::StreamScope scope(stream_of(stream));
-    sbx::require(!(flags & SBX_TRANSPOSE), "hbs_solve_t is not part of the device path yet");
-    sbx::hbs_solve(H(h), b, ldb, nrhs, x, ldx, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
+    const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    if (flags & SBX_TRANSPOSE)
+      sbx::hbs_solve_t(H(h), b, ldb, nrhs, x, ldx, dev, stream_of(stream));
+    else
+      sbx::hbs_solve(H(h), b, ldb, nrhs, x, ldx, dev, stream_of(stream));
   });
 }
 
@@ -297,8 +300,11 @@ int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double*
                   int flags, void* stream) {
   return guard([&] {
     sbx::StreamScope scope(stream_of(stream));
-    sbx::require(!(flags & SBX_TRANSPOSE), "hbs_apply_t is not part of the device path yet");
-    sbx::hbs_apply(H(h), v, ldv, nrhs, y, ldy, (flags & SBX_DEVICE_PTRS) != 0, stream_of(stream));
+    const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    if (flags & SBX_TRANSPOSE)
+      sbx::hbs_apply_t(H(h), v, ldv, nrhs, y, ldy, dev, stream_of(stream));
+    else
+      sbx::hbs_apply(H(h), v, ldv, nrhs, y, ldy, dev, stream_of(stream));
   });
 }
 
@@ -440,7 +446,9 @@ int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, doubl
   });
 }
 
-int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo) {
+namespace {
+int els_apply_forward_host(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo,
+                           bool tr) {
   return guard([&] {
     sbx::require(e && e->e, "null els handle");
     sbx::Els& E = *e->e;
@@ -450,11 +458,20 @@ int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs,
     sbx::DevBuf<double> dv(static_cast<size_t>(n * nrhs)), dout(static_cast<size_t>(n * nrhs));
     SBX_CUDA(cudaMemcpy2DAsync(dv.get(), size_t(n) * 8, v, size_t(ldv) * 8, size_t(n) * 8, size_t(nrhs),
                                cudaMemcpyHostToDevice, s));
-    sbx::els_apply_forward_device(E, dv.get(), dout.get(), nrhs, s);
+    sbx::els_apply_forward_device(E, dv.get(), dout.get(), nrhs, s, tr);
     SBX_CUDA(cudaMemcpy2DAsync(out, size_t(ldo) * 8, dout.get(), size_t(n) * 8, size_t(n) * 8, size_t(nrhs),
                                cudaMemcpyDeviceToHost, s));
     SBX_CUDA(cudaStreamSynchronize(s));
   });
+}
+}  // namespace
+
+int sbx_els_apply_forward(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo) {
+  return els_apply_forward_host(e, v, ldv, nrhs, out, ldo, false);
+}
+
+int sbx_els_apply_forward_t(sbx_els e, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo) {
+  return els_apply_forward_host(e, v, ldv, nrhs, out, ldo, true);
 }
 
 int sbx_els_gmres(sbx_els e, const double* g_n, double* tau_n, int precond, double tol, int64_t max_iter,
@@ -476,7 +493,7 @@ int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs,
     sbx::StreamScope scope(stream_of(stream));
     sbx::require(e && e->e, "null els handle");
     sbx::els_solve(*e->e, g_ext, ldg, nrhs, y, ldy, true, (flags & SBX_DEVICE_PTRS) != 0,
-                   stream_of(stream));
+                   stream_of(stream), (flags & SBX_TRANSPOSE) != 0);
   });
 }
 

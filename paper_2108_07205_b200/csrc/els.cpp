@@ -48,15 +48,17 @@ double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
 // (els.cpp:43-65): the old-mesh part goes through the HBS sweep in old
 // ordering (scatter/gather fused into the layout kernels), the added part
 // through the dense inverse or its own HBS.
-void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nrhs, cudaStream_t s) {
+void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nrhs, cudaStream_t s,
+                  bool tr = false) {
   HbsOp& A = *e.a_oo;
   if (!A.solve_plan.built) hbs_build_solve_plan(A);
+  if (tr) hbs_ensure_transpose(A, true, false, s);
   SweepPlan& P = A.solve_plan;
   const i64 ldw = sweep_ld(nrhs);
   A.ws.reserve(size_t(P.ws_rows * ldw));
   const i64 nkc = e.n_k + e.n_c;
   launch_cm_to_rm(v, ldv, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
-  hbs_run_plan(A, P, A.ws.get(), nrhs, s);
+  hbs_run_plan(A, P, A.ws.get(), nrhs, s, tr ? A.arena_t.get() : nullptr);
   // gather: out row i <- old row map[i]
   launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
   if (e.n_p == 0) return;
@@ -65,14 +67,15 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
   if (e.app->h) {
     HbsOp& H = *e.app->h;
     if (!H.solve_plan.built) hbs_build_solve_plan(H);
+    if (tr) hbs_ensure_transpose(H, true, false, s);
     SweepPlan& Q = H.solve_plan;
     H.ws.reserve(size_t(Q.ws_rows * ldw));
     launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
-    hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
+    hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
     launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, op, ldo, nullptr, s);
-  } else {
+  } else {  // explicit inverse of A_pp (els.cpp:47: app_lu.solve / app_lu.transpose().solve)
     gemm_batched({{e.app->inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
-                   int(ldo), 0, 0, 1.0, 0.0}},
+                   int(ldo), tr ? 1 : 0, 0, 1.0, 0.0}},
                  s);
   }
 }
@@ -166,37 +169,45 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   return e;
 }
 
-void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s) {
+void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s, bool tr) {
   const i64 n = e.n_ext(), nkc = e.n_k + e.n_c;
   HbsOp& A = *e.a_oo;
   if (!A.apply_plan.built) hbs_build_apply_plan(A);
+  if (tr) hbs_ensure_transpose(A, false, true, s);
   SweepPlan& P = A.apply_plan;
   const i64 ldw = sweep_ld(nrhs);
   A.ws.reserve(size_t(P.ws_rows * ldw));
   launch_cm_to_rm(v, n, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
-  hbs_run_plan(A, P, A.ws.get(), nrhs, s);
+  hbs_run_plan(A, P, A.ws.get(), nrhs, s, tr ? A.arena_t.get() : nullptr);
   launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, n, e.d_old_of_ext.get(), s);
   if (e.n_p > 0) {
     if (e.app->h) {
       HbsOp& H = *e.app->h;
       if (!H.apply_plan.built) hbs_build_apply_plan(H);
+      if (tr) hbs_ensure_transpose(H, false, true, s);
       SweepPlan& Q = H.apply_plan;
       H.ws.reserve(size_t(Q.ws_rows * ldw));
       launch_cm_to_rm(v + nkc, n, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
-      hbs_run_plan(H, Q, H.ws.get(), nrhs, s);
+      hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
       launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, out + nkc, n, nullptr, s);
     } else {
       gemm_batched({{e.app->fwd.get(), v + nkc, out + nkc, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(n),
-                     int(n), 0, 0, 1.0, 0.0}},
+                     int(n), tr ? 1 : 0, 0, 1.0, 0.0}},
                    s);
     }
   }
   if (e.k == 0) return;
-  // out += L (R v)   (els.cpp:184); L is reconstructed as the update factor
   e.ws2.reserve(size_t(e.k * nrhs));
   double* t = e.ws2.get();
-  gemm_batched({{e.R.get(), v, t, int(e.k), int(nrhs), int(n), int(e.k), int(n), int(e.k), 0, 0, 1.0, 0.0}}, s);
-  gemm_batched({{e.L->get(), t, out, int(n), int(nrhs), int(e.k), int(n), int(e.k), int(n), 0, 0, 1.0, 1.0}}, s);
+  if (!tr) {
+    // out += L (R v)   (els.cpp:184); L is reconstructed as the update factor
+    gemm_batched({{e.R.get(), v, t, int(e.k), int(nrhs), int(n), int(e.k), int(n), int(e.k), 0, 0, 1.0, 0.0}}, s);
+    gemm_batched({{e.L->get(), t, out, int(n), int(nrhs), int(e.k), int(n), int(e.k), int(n), 0, 0, 1.0, 1.0}}, s);
+  } else {
+    // out += R^T (L^T v)   (els.cpp:191)
+    gemm_batched({{e.L->get(), v, t, int(e.k), int(nrhs), int(n), int(n), int(n), int(e.k), 1, 0, 1.0, 0.0}}, s);
+    gemm_batched({{e.R.get(), t, out, int(n), int(nrhs), int(e.k), int(e.k), int(e.k), int(n), 1, 0, 1.0, 1.0}}, s);
+  }
 }
 
 void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cudaStream_t s) {
@@ -212,8 +223,27 @@ void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cuda
   gemm_batched({{e.X.get(), u, y, int(n), int(nrhs), int(k), int(n), int(k), int(n), 0, 0, -1.0, 1.0}}, s);
 }
 
+void els_solve_ext_t_device(Els& e, const double* g_ext, double* y, i64 nrhs, cudaStream_t s) {
+  const i64 n = e.n_ext(), k = e.k;
+  if (k == 0) {
+    atilde_solve(e, g_ext, n, y, n, nrhs, s, true);
+    return;
+  }
+  // z = g - R^T W^{-T} (X^T g);  y = Atilde^{-T} z   (els.cpp:157-162)
+  e.ws2.reserve(size_t(2 * k * nrhs));
+  double* t = e.ws2.get();
+  double* u = t + k * nrhs;
+  DevBuf<double> z(static_cast<size_t>(n * nrhs));
+  SBX_CUDA(cudaMemcpyAsync(z.get(), g_ext, size_t(n * nrhs) * 8, cudaMemcpyDeviceToDevice, s));
+  gemm_batched({{e.X.get(), g_ext, t, int(k), int(nrhs), int(n), int(n), int(n), int(k), 1, 0, 1.0, 0.0}}, s);
+  gemm_batched({{e.Winv.get(), t, u, int(k), int(nrhs), int(k), int(k), int(k), int(k), 1, 0, 1.0, 0.0}}, s);
+  gemm_batched({{e.R.get(), u, z.get(), int(n), int(nrhs), int(k), int(k), int(k), int(n), 1, 0, -1.0, 1.0}}, s);
+  atilde_solve(e, z.get(), n, y, n, nrhs, s, true);
+}
+
 void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, bool raw, bool dev,
-               cudaStream_t s) {
+               cudaStream_t s, bool tr) {
+  require(raw || !tr, "els_solve: the transpose solve is defined on the extended system (els_solve_raw_t)");
   const i64 n = e.n_ext();
   const i64 rows_in = raw ? n : e.n_k + e.n_p;
   require(ldg >= rows_in && ldy >= rows_in, "els_solve: leading dimension too small");
@@ -240,7 +270,10 @@ void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, b
       SBX_CUDA(cudaMemcpy2DAsync(gx + nkc, size_t(n) * 8, g + e.n_k, size_t(ldg) * 8, size_t(e.n_p) * 8,
                                  size_t(nrhs), kind, s));
   }
-  els_solve_ext_device(e, gx, yx, nrhs, s);
+  if (tr)
+    els_solve_ext_t_device(e, gx, yx, nrhs, s);
+  else
+    els_solve_ext_device(e, gx, yx, nrhs, s);
   const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (raw) {
     SBX_CUDA(cudaMemcpy2DAsync(y, size_t(ldy) * 8, yx, size_t(n) * 8, size_t(n) * 8, size_t(nrhs), kind, s));

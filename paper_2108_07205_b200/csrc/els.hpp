@@ -59,14 +59,17 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
                                       double mu, cudaStream_t s);
 // raw: g has n_ext rows (kept, cut, added); else n_k + n_p rows (kept, added)
 // and the dummy block is dropped from the output (els.cpp:165-179).
+// transpose (raw only): els_solve_raw_t (els.cpp:154-163).
 void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, bool raw, bool dev,
-               cudaStream_t s);
+               cudaStream_t s, bool transpose = false);
 void els_density_on_refined(const Els& e, const double* tau_n, double* out);
 void els_download_xw(const Els& e, double* X, double* W, cudaStream_t s);
 
 // els_apply_forward (els.cpp:181-186): out = (Atilde + L R) v, v / out
 // n_ext x nrhs device blocks (ld n_ext).
-void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s);
+// transpose: els_apply_forward_t (els.cpp:188-193), out = (Atilde + L R)^T v.
+void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s,
+                              bool transpose = false);
 
 // GMRES / PGMRES-Local on the refined system in (kept, added) unknowns
 // (gmres.cpp:14-126 driven like scenario.cpp:694-727): operator =
@@ -84,5 +87,7 @@ GmresOutcome els_gmres(Els& e, const double* g_n, double* tau_n, bool precond, d
 // Device-resident solve for callers holding device buffers:
 // y_ext (n_ext x nrhs, column-major ld n_ext) = ELS^{-1} g_ext.
 void els_solve_ext_device(Els& e, const double* g_ext, double* y_ext, i64 nrhs, cudaStream_t s);
+// y_ext = ELS^{-T} g_ext (els.cpp:154-163).
+void els_solve_ext_t_device(Els& e, const double* g_ext, double* y_ext, i64 nrhs, cudaStream_t s);
 
 }  // namespace sbx

@@ -106,6 +106,12 @@ struct HbsOp {
   DevBuf<double> arena;
   i64 arena_used = 0;
   SweepPlan solve_plan, apply_plan;
+  // Transposed factors in the SAME layout (hbs_solve_t / hbs_apply_t run the
+  // unchanged plans over this arena): fg <- [e^T; g^T], e <- f^T,
+  // root_g <- root_g^T; vd <- [u^T; d^T], u <- v, b_l <- b_r^T.  Built on
+  // first use.
+  DevBuf<double> arena_t;
+  bool t_solve = false, t_apply = false;
   std::unique_ptr<struct ShardPlans> shard;  // subtree-partitioned solve (multi-GPU)
   DevBuf<double> ws;  // sweep workspace (grown on demand)
   DevBuf<double> io;  // staging for host-pointer sweeps (grown on demand)
@@ -141,7 +147,13 @@ void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy
 
 // Row-major workspace form, for callers that already hold the sweep input
 // in `ws` row layout (the ELS path): runs the planned levels only.
-void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s);
+void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s,
+                  const double* fac = nullptr);
+// hbs.cpp:627-664 / :546-587: transposed solve and apply.
+void hbs_solve_t(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev, cudaStream_t s);
+void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev, cudaStream_t s);
+// Builds the transposed arena parts (solve and/or apply) if missing.
+void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s);
 void hbs_build_solve_plan(HbsOp& op);
 void hbs_build_apply_plan(HbsOp& op);
 

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "dense.hpp"
 #include "hbs.hpp"
 
 #include <type_traits>
@@ -921,8 +922,7 @@ void hbs_build_apply_plan(HbsOp& op) {
 
 namespace {
 template <int TN>
-void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
-  const double* fac = op.arena.get();
+void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
   const bool dmma = nrhs > 1;
   static const bool per_level = std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
   int max_k = 0;
@@ -1050,7 +1050,8 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) 
 
 }  // namespace
 
-void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s) {
+void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
+  if (!fac) fac = op.arena.get();
   // column tile: 32 when the block is narrow enough that the tree depth
   // (not the tensor throughput) bounds the sweep (SBX_SWEEP_TN overrides)
   static const int tn_env = [] {
@@ -1059,14 +1060,14 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
   }();
   const int tn = tn_env == 32 || tn_env == 64 ? tn_env : (nrhs <= 192 ? 32 : 64);
   if (tn == 32)
-    run_flow<32>(op, plan, ws, nrhs, s);
+    run_flow<32>(op, plan, ws, nrhs, s, fac);
   else
-    run_flow<64>(op, plan, ws, nrhs, s);
+    run_flow<64>(op, plan, ws, nrhs, s, fac);
 }
 
 namespace {
 void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx,
-               bool dev, cudaStream_t s) {
+               bool dev, cudaStream_t s, const double* fac = nullptr) {
   require(nrhs >= 0, "sweep: negative nrhs");
   require(ldb >= op.n && ldx >= op.n, "sweep: leading dimension smaller than n");
   if (nrhs == 0) return;
@@ -1084,7 +1085,7 @@ void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, d
     xd = hb + op.n * nrhs;
   }
   launch_cm_to_rm(bd, dev ? ldb : op.n, op.n, nrhs, ws + plan.in_row * ldw, ldw, nullptr, s);
-  hbs_run_plan(op, plan, ws, nrhs, s);
+  hbs_run_plan(op, plan, ws, nrhs, s, fac);
   launch_rm_to_cm(ws + plan.out_row * ldw, ldw, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, s);
   if (!dev) {
     SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, xd, size_t(op.n) * 8, size_t(op.n) * 8,
@@ -1104,6 +1105,71 @@ void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy
                cudaStream_t s) {
   if (!op.apply_plan.built) hbs_build_apply_plan(op);
   run_sweep(op, op.apply_plan, v, ldv, nrhs, y, ldy, dev, s);
+}
+
+void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s) {
+  solve = solve && !op.t_solve;
+  apply = apply && !op.t_apply;
+  if (!solve && !apply) return;
+  if (!op.arena_t.get() || op.arena_t.size() < op.arena.size()) {
+    require(!op.t_solve && !op.t_apply, "transposed arena: layout changed after build");
+    op.arena_t.resize(op.arena.size());
+  }
+  const double* A = op.arena.get();
+  double* T = op.arena_t.get();
+  std::vector<CopyJob> jobs;
+  auto tr = [&](i64 src, int lds, i64 dst, int ldd, int rows, int cols, int trans) {
+    if (rows > 0 && cols > 0) jobs.push_back({A + src, T + dst, rows, cols, lds, ldd, trans, 0});
+  };
+  const size_t nn = op.nodes.size();
+  if (solve) {
+    require(op.has_inverse, "hbs_solve_t: inverse not built");
+    const i64 c0 = op.nodes[0].c;
+    tr(op.o_root_g, int(c0), op.o_root_g, int(c0), int(c0), int(c0), 1);
+    for (size_t i = 1; i < nn; ++i) {
+      const auto& nd = op.nodes[i];
+      const int k = int(nd.k), c = int(nd.c), ld = k + c;
+      tr(nd.o_e, c, nd.o_fg, ld, k, c, 1);                  // [e^T; .]
+      tr(nd.o_fg + k, ld, nd.o_fg + k, ld, c, c, 1);        // [.; g^T]
+      tr(nd.o_fg, ld, nd.o_e, c, c, k, 1);                  // f^T
+    }
+  }
+  if (apply) {
+    require(op.has_apply, "hbs_apply_t: operator has no forward factors");
+    if (nn == 1) {
+      const int c = int(op.nodes[0].c);
+      tr(op.nodes[0].o_vd, c, op.nodes[0].o_vd, c, c, c, 1);  // d^T
+    }
+    for (size_t i = 1; i < nn; ++i) {
+      const auto& nd = op.nodes[i];
+      const int k = int(nd.k), c = int(nd.c);
+      const int ld = k + (nd.is_leaf() ? c : 0);
+      tr(nd.o_u, c, nd.o_vd, ld, k, c, 1);                                    // [u^T; .]
+      if (nd.is_leaf()) tr(nd.o_vd + k, ld, nd.o_vd + k, ld, c, c, 1);        // [.; d^T]
+      tr(nd.o_v, c, nd.o_u, c, c, k, 0);                                      // u <- v
+      const auto& sb = op.nodes[size_t(op.sib(i64(i)))];
+      tr(sb.o_b, int(sb.k), nd.o_b, k, k, int(sb.k), 1);                      // b_i <- b_sib^T
+    }
+  }
+  for (size_t q = 0; q < jobs.size(); q += 60000)  // grid.y limit of the copy kernel
+    copy_batched(std::vector<CopyJob>(jobs.begin() + q, jobs.begin() + std::min(jobs.size(), q + 60000)), s);
+  SBX_CUDA(cudaStreamSynchronize(s));  // job tables and the arena are shared state
+  if (solve) op.t_solve = true;
+  if (apply) op.t_apply = true;
+}
+
+void hbs_solve_t(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev,
+                 cudaStream_t s) {
+  if (!op.solve_plan.built) hbs_build_solve_plan(op);
+  hbs_ensure_transpose(op, true, false, s);
+  run_sweep(op, op.solve_plan, b, ldb, nrhs, x, ldx, dev, s, op.arena_t.get());
+}
+
+void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev,
+                 cudaStream_t s) {
+  if (!op.apply_plan.built) hbs_build_apply_plan(op);
+  hbs_ensure_transpose(op, false, true, s);
+  run_sweep(op, op.apply_plan, v, ldv, nrhs, y, ldy, dev, s, op.arena_t.get());
 }
 
 }  // namespace sbx
