@@ -206,6 +206,13 @@ int sbx_els_gmres(sbx_els e, const double* g_n, double* tau_n, int precond, doub
                   int64_t max_iter, int64_t restart, int64_t* n_iter, double* history,
                   int64_t history_cap);
 int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out);
+/* conditioning_report (els.cpp:225-270), estimator route: out[7] = kappa_w,
+ * kappa_l, kappa_r, kappa_ext, kappa_tilde, bound, bound_holds (0/1).
+ * kappa_w / kappa_l / kappa_r are exact (singular values of W and of the R
+ * factors of L and R^T); kappa_ext / kappa_tilde by `iters` rounds of seeded
+ * power iteration on the device operators and their solves (linop.cpp:17-43;
+ * the reference uses 80). */
+int sbx_els_conditioning(sbx_els e, int iters, double* out);
 /* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
 int sbx_els_xw(sbx_els e, double* X, double* W);
 

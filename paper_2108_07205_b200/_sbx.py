@@ -116,6 +116,7 @@ _SIGS = [
     ("sbx_els_density_on_refined", C.c_int, [VP, F64P, F64P]),
     ("sbx_els_apply_forward", C.c_int, [VP, F64P, I64, I64, F64P, I64]),
     ("sbx_els_apply_forward_t", C.c_int, [VP, F64P, I64, I64, F64P, I64]),
+    ("sbx_els_conditioning", C.c_int, [VP, C.c_int, F64P]),
     ("sbx_els_gmres", C.c_int, [VP, F64P, F64P, C.c_int, C.c_double, I64, I64, I64P, F64P, I64]),
     ("sbx_els_xw", C.c_int, [VP, F64P, F64P]),
 ]

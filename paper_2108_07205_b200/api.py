@@ -490,6 +490,18 @@ def els_apply_forward(s: ElsSolver, v, transpose: bool = False) -> np.ndarray:
     return out[:, 0] if vec else out
 
 
+def els_conditioning(s: ElsSolver, iters: int = 80) -> dict:
+    """conditioning_report (els.cpp:225-270), estimator route: exact kappa_w,
+    kappa_l, kappa_r; kappa_ext, kappa_tilde by seeded power iteration on the
+    device operators and solves (linop.cpp:17-43)."""
+    out = np.zeros(7)
+    check(lib().sbx_els_conditioning(s.ptr, int(iters), out.ctypes.data_as(F64P)))
+    keys = ("kappa_w", "kappa_l", "kappa_r", "kappa_ext", "kappa_tilde", "bound")
+    r = {k: float(v) for k, v in zip(keys, out[:6])}
+    r["bound_holds"] = bool(out[6] != 0.0)
+    return r
+
+
 def els_gmres(s: ElsSolver, g_n, precond: bool = True, tol: float = 1e-11, max_iter: int = 600,
               restart: int = 0):
     """GMRES (gmres.cpp:14-126) on the refined system in (kept, added)

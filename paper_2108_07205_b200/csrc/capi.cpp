@@ -497,6 +497,21 @@ int sbx_els_solve_raw(sbx_els e, const double* g_ext, int64_t ldg, int64_t nrhs,
   });
 }
 
+int sbx_els_conditioning(sbx_els e, int iters, double* out) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::require(iters >= 1, "conditioning: iteration count must be positive");
+    const sbx::CondReport r = sbx::els_conditioning(*e->e, iters, sbx::lib_stream());
+    out[0] = r.kappa_w;
+    out[1] = r.kappa_l;
+    out[2] = r.kappa_r;
+    out[3] = r.kappa_ext;
+    out[4] = r.kappa_tilde;
+    out[5] = r.bound;
+    out[6] = r.bound_holds ? 1.0 : 0.0;
+  });
+}
+
 int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out) {
   return guard([&] {
     sbx::require(e && e->e, "null els handle");

@@ -169,7 +169,8 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   return e;
 }
 
-void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s, bool tr) {
+void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s, bool tr,
+                              bool with_update) {
   const i64 n = e.n_ext(), nkc = e.n_k + e.n_c;
   HbsOp& A = *e.a_oo;
   if (!A.apply_plan.built) hbs_build_apply_plan(A);
@@ -196,7 +197,7 @@ void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cu
                    s);
     }
   }
-  if (e.k == 0) return;
+  if (e.k == 0 || !with_update) return;
   e.ws2.reserve(size_t(e.k * nrhs));
   double* t = e.ws2.get();
   if (!tr) {
@@ -221,6 +222,10 @@ void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cuda
   gemm_batched({{e.R.get(), y, t, int(k), int(nrhs), int(n), int(k), int(n), int(k), 0, 0, 1.0, 0.0}}, s);
   gemm_batched({{e.Winv.get(), t, u, int(k), int(nrhs), int(k), int(k), int(k), int(k), 0, 0, 1.0, 0.0}}, s);
   gemm_batched({{e.X.get(), u, y, int(n), int(nrhs), int(k), int(n), int(k), int(n), 0, 0, -1.0, 1.0}}, s);
+}
+
+void els_atilde_solve(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s, bool tr) {
+  atilde_solve(e, v, e.n_ext(), out, e.n_ext(), nrhs, s, tr);
 }
 
 void els_solve_ext_t_device(Els& e, const double* g_ext, double* y, i64 nrhs, cudaStream_t s) {

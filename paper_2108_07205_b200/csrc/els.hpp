@@ -68,8 +68,25 @@ void els_download_xw(const Els& e, double* X, double* W, cudaStream_t s);
 // els_apply_forward (els.cpp:181-186): out = (Atilde + L R) v, v / out
 // n_ext x nrhs device blocks (ld n_ext).
 // transpose: els_apply_forward_t (els.cpp:188-193), out = (Atilde + L R)^T v.
+// with_update = false: the block-diagonal part Atilde alone (els.cpp:67-74).
 void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s,
-                              bool transpose = false);
+                              bool transpose = false, bool with_update = true);
+// Atilde^{-1} v or Atilde^{-T} v on extended blocks (els.cpp:58-65).
+void els_atilde_solve(Els& e, const double* v, double* out, i64 nrhs, cudaStream_t s, bool transpose);
+
+// conditioning_report (els.cpp:225-270) on the estimator route: kappa_w,
+// kappa_l, kappa_r from the singular values of W and of the R factors of
+// device QRs of L and R^T (one-sided Jacobi on the k x k factors, host);
+// kappa_ext and kappa_tilde by seeded power iteration on the device
+// operators and their solves (linop.cpp:17-43, mt19937_64 Gaussian starts).
+struct CondReport {
+  double kappa_w = 1.0, kappa_l = 1.0, kappa_r = 1.0, kappa_ext = 1.0, kappa_tilde = 1.0, bound = 1.0;
+  bool bound_holds = true;
+};
+CondReport els_conditioning(Els& e, int iters, cudaStream_t s);
+// Singular values (descending) of a column-major m x n host matrix, m >= n
+// (one-sided Jacobi).
+std::vector<double> jacobi_singular_values(std::vector<double> a, i64 m, i64 n);
 
 // GMRES / PGMRES-Local on the refined system in (kept, added) unknowns
 // (gmres.cpp:14-126 driven like scenario.cpp:694-727): operator =

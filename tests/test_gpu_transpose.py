@@ -87,3 +87,60 @@ def test_els_transposes_are_adjoints(sb, m):  # els.cpp:154-163, :188-193
     # compression tolerance, like the forward round trip)
     r = sb.els_apply_forward(e, sty, transpose=True)
     assert np.linalg.norm(r - y) < 1e-6 * np.linalg.norm(y)
+
+
+def test_transposed_sweeps_match_oracle_bitwise_factors(sb, po, tmp_path):
+    """Tier 1: the oracle's factors loaded through HBS1; the device
+    transposed sweeps against the oracle's hbs_solve_t / hbs_apply_t."""
+    o = po.Geom.create(po.STAR, 12, prongs=3, amplitude=0.35)
+    h = po.Hbs.compress(po.Assembler.create(o), 1e-10).invert()
+    h.save(tmp_path / "t.hbs1")
+    d = sb.hbs_load(tmp_path / "t.hbs1")
+    b = rng_mat(d.n, 3, 6)
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)
+    assert rel(sb.hbs_solve(d, b, transpose=True), h.solve_t(b)) < 1e-12
+    assert rel(sb.hbs_apply(d, b, transpose=True), h.apply_t(b)) < 1e-12
+
+
+def scalars(nodes):
+    return np.stack([2 * np.asarray(nodes), 2 * np.asarray(nodes) + 1], 1).reshape(-1)
+
+
+def test_conditioning_report(sb, po):  # test_els.cpp:268-291
+    eps = 1e-10
+    g0 = sb.panelize(sb.star(5, 0.3), 10, 16)
+    h = sb.hbs_invert(sb.hbs_compress(g0))
+    g1, plan = sb.refine(g0, [3], 4)
+    u = sb.compress_update(g0, g1, plan, eps)
+    e = sb.els_build(h, g0, g1, plan, u)
+    rep = sb.els_conditioning(e)
+    assert rep["kappa_w"] >= 1.0 and rep["bound_holds"] and rep["kappa_w"] <= rep["bound"]
+    assert rep["kappa_ext"] > 1.0 and rep["kappa_tilde"] > 1.0
+    # dense numbers (numpy SVD) of the same operators
+    o0 = po.Geom.create(po.STAR, 10, prongs=5, amplitude=0.3)
+    o1, op = o0.refine([3], 4)
+    a0, a1 = po.Assembler.create(o0), po.Assembler.create(o1)
+    m = op.maps()
+    oc = np.concatenate([scalars(m["kept_old"]), scalars(m["cut_old"])])
+    ad = scalars(m["added_new"])
+    n = len(oc) + len(ad)
+    At = np.zeros((n, n))
+    At[: len(oc), : len(oc)] = a0.submatrix(oc, oc)
+    At[len(oc):, len(oc):] = a1.submatrix(ad, ad)
+    L, R = u.factors()
+    cond = lambda a: (lambda s: s[0] / s[-1])(np.linalg.svd(a, compute_uv=False))
+    k = L.shape[1]
+
+    def factor_close(got, f):  # factor_cond (els.cpp:216-222); numerically singular factors only agree on "huge"
+        s = np.linalg.svd(f, compute_uv=False)
+        ref = s[0] / s[k - 1]
+        return (got > 1e12 and ref > 1e12) if ref > 1e12 else abs(got / ref - 1) < 1e-6
+
+    assert factor_close(rep["kappa_l"], L)
+    assert factor_close(rep["kappa_r"], R)
+    X, W = e.xw()
+    assert abs(rep["kappa_w"] / cond(W) - 1) < 1e-6
+    # the estimator route lands near the dense numbers (the reference's 0.3x .. 3x)
+    ke, kt = cond(At + L @ R), cond(At)
+    assert 0.3 * ke <= rep["kappa_ext"] <= 3.0 * ke
+    assert 0.3 * kt <= rep["kappa_tilde"] <= 3.0 * kt
