@@ -2402,7 +2402,7 @@ __global__ void __launch_bounds__(kT) gj_inverse_kernel(const LuJob* __restrict_
   int* ired = reinterpret_cast<int*>(red + 64);  // 64
   int* pivrow = ired + 64;                   // 128: row used at step k
   int* rowstep = pivrow + 128;               // 128: step at which row i pivoted
-  __shared__ int s_p;
+  __shared__ int sp[2];
   __shared__ double s_l1;
   __shared__ int s_sing;
   if (tid == 0) {
@@ -2429,81 +2429,80 @@ __global__ void __launch_bounds__(kT) gj_inverse_kernel(const LuJob* __restrict_
       atomicMax(reinterpret_cast<unsigned long long*>(&s_l1), __double_as_longlong(cs));
   }
   unsigned used = 0;  // bit a: row lane + 32 a already pivoted
-  for (int k = 0; k < n; ++k) {
+  // Pivot search of column k by its owner warp (values in registers), which
+  // publishes the column for the other warps: the step's only barrier.
+  auto search = [&](int k) {
     double* col = colb + 128 * (k & 1);
-    double* row = rowb + 128 * (k & 1);
-    const int wk = k & 15, bk = k >> 4;
-    if (warp == wk) {  // pivot search + publish column k
-      double bv = -1.0;
-      int bi = 0x7fffffff;
+    const int bk = k >> 4;
+    double bv = -1.0;
+    int bi = 0x7fffffff;
 #pragma unroll
-      for (int b = 0; b < CB; ++b)
-        if (b == bk) {
+    for (int b = 0; b < CB; ++b)
+      if (b == bk) {
 #pragma unroll
-          for (int a = 0; a < RA; ++a) {
-            const int i = lane + 32 * a;
-            if (i < n) {
-              col[i] = M[a][b];
-              const double v = fabs(M[a][b]);
-              if (!((used >> a) & 1u) && v > bv) {
-                bv = v;
-                bi = i;
-              }
+        for (int a = 0; a < RA; ++a) {
+          const int i = lane + 32 * a;
+          if (i < n) {
+            col[i] = M[a][b];
+            const double v = fabs(M[a][b]);
+            if (!((used >> a) & 1u) && v > bv) {
+              bv = v;
+              bi = i;
             }
           }
         }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
       }
-      if (lane == 0) {
-        s_p = bi;
-        pivrow[k] = bi;
-        rowstep[bi] = k;
-        if (!(bv > 0.0)) s_sing = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
       }
     }
-    __syncthreads();
-    const int p = s_p;
+    if (lane == 0) {
+      sp[k & 1] = bi;
+      pivrow[k] = bi;
+      rowstep[bi] = k;
+      if (!(bv > 0.0)) s_sing = 1;
+    }
+  };
+  if (warp == 0) search(0);
+  for (int k = 0; k < n; ++k) {
+    __syncthreads();  // column k and its pivot published
+    const double* col = colb + 128 * (k & 1);
+    const int p = sp[k & 1];
     const int ap = p >> 5, lp = p & 31;
     const double piv = col[p];
     const double rinv = piv != 0.0 ? 1.0 / piv : 0.0;
-    if (lane == lp) {  // owners of row p publish it scaled (column k: 1/piv)
+    // the pivot row of this warp's columns lives in lane lp: broadcast it
+    double pr[CB];
+#pragma unroll
+    for (int b = 0; b < CB; ++b) {
+      double x = 0.0;
 #pragma unroll
       for (int a = 0; a < RA; ++a)
-        if (a == ap) {
-          used |= 1u << a;
-#pragma unroll
-          for (int b = 0; b < CB; ++b) {
-            const int j = warp + 16 * b;
-            if (j < n) {
-              const double u = j == k ? rinv : M[a][b] * rinv;
-              row[j] = u;
-              M[a][b] = u;
-            }
-          }
-        }
+        if (a == ap) x = M[a][b];
+      pr[b] = __shfl_sync(0xffffffffu, x, lp) * rinv;
     }
-    __syncthreads();
+    const bool own_k = warp == (k & 15);
+    const int bk = k >> 4;
 #pragma unroll
     for (int a = 0; a < RA; ++a) {
       const int i = lane + 32 * a;
-      if (i >= n || i == p) continue;
+      if (i >= n) continue;
+      if (i == p) {  // the pivot row becomes the scaled row (column k: 1/piv)
+        used |= 1u << a;
+#pragma unroll
+        for (int b = 0; b < CB; ++b) M[a][b] = (own_k && b == bk) ? rinv : pr[b];
+        continue;
+      }
       const double f = col[i];
 #pragma unroll
-      for (int b = 0; b < CB; ++b) {
-        const int j = warp + 16 * b;
-        if (j == k)
-          M[a][b] = -f * rinv;
-        else
-          M[a][b] -= f * row[j];
-      }
+      for (int b = 0; b < CB; ++b) M[a][b] = (own_k && b == bk) ? -f * rinv : M[a][b] - f * pr[b];
     }
+    if (k + 1 < n && warp == ((k + 1) & 15)) search(k + 1);
   }
   // unscramble: inv[k, pivrow[m]] = M[pivrow[k], m]
 #pragma unroll
