@@ -611,9 +611,10 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   double* vb = sm + cpqr_blocked_head(n);  // 2 x 128 reflector buffers
   double* tauv = vb + 2 * kTsqrBm;  // 2 (+pad)
   double* R = tauv + 8;             // n x n, ld n
-  for (int idx = tid; idx < n * n; idx += kT) R[idx] = 0.0;
+  for (int idx = tid; idx < n * n; idx += kT)
+    R[idx] = (blocked & 4) ? jb.a[(idx % n) + size_t(idx / n) * jb.lda] : 0.0;
   double B[kTsqrSlots][kTsqrRpl];
-  for (int r0 = 0; r0 < M; r0 += kTsqrBm) {
+  for (int r0 = 0; r0 < ((blocked & 4) ? 0 : M); r0 += kTsqrBm) {
     const int rb = min(kTsqrBm, M - r0);
 #pragma unroll
     for (int u = 0; u < kTsqrSlots; ++u) {
@@ -668,7 +669,8 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
     }
   }
   __syncthreads();
-  const int steps_max = jb.max_steps > 0 ? min(n, jb.max_steps) : n;
+  const int steps_max = (blocked & 8) ? 0 : jb.max_steps > 0 ? min(n, jb.max_steps) : n;
+  blocked &= 1;
   const int done = blocked ? cpqr_core_blocked(R, n, n, n, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
                                                pos, lphys, red, ired, sc, F, aux, vrow, bp, rec)
                            : cpqr_core(R, n, n, n, true, steps_max, jb.stop_eps, jb.perm, jb.diag, upd, dir,
@@ -677,6 +679,365 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
   __syncthreads();
   for (int c = warp; c < n; c += kWarps)
     for (int i = lane; i < n; i += 32) jb.a[i + size_t(c) * jb.lda] = R[i + size_t(c) * n];
+}
+
+// Tall problems with n <= 128, quad layout: 256 threads; quad g (threads
+// 4g..4g+3) owns columns g and g + 64 and, of each, the rows q + 4 i
+// (q = thread & 3, i < 32) of the current 128-row block in registers.  A
+// column's dot product with the Householder vector reduces over its quad
+// (two shuffle levels instead of a warp's five), and the vector reaches the
+// quads through shared memory in the owners' row order (row q + 4 i at
+// v[q * kQPad + i]; one 16-byte broadcast load serves both columns).
+//   TSQR: per 128-row block, n Householder steps on [R; B] with one barrier
+//   each; the quad owning column j + 1 applies step j to it first and
+//   publishes reflector j + 1 (look-ahead) while the others finish step j.
+//   CPQR of R0 (n x n, loaded into the same registers): Eigen's
+//   ColPivHouseholderQR pivot rule and xGEQPF norm downdating (as cpqr_core),
+//   two barriers per step (pivot partials; reflector).
+// Output contract as tsqr_cpqr_kernel: R0's CPQR factor in the first n rows
+// of the job matrix, columns in place (perm[l] = physical column at l).
+constexpr int kQT = 256;               // threads
+constexpr int kQWarps = kQT / 32;
+constexpr int kQRows = 32;             // rows per thread and column
+constexpr int kQBm = 4 * kQRows;       // rows per block; also the largest n
+constexpr int kQHalf = kQT / 4;        // column offset of a quad's second column
+constexpr int kQPad = kQRows + 2;      // padded quarter stride of v
+
+// quad-local shuffles: the callers branch per column pair (quad-uniformly)
+__device__ __forceinline__ unsigned quad_mask() { return 0xFu << (threadIdx.x & 28); }
+
+__device__ __forceinline__ double quad_sum(double v) {
+  const unsigned m = quad_mask();
+  v += __shfl_xor_sync(m, v, 1);
+  v += __shfl_xor_sync(m, v, 2);
+  return v;
+}
+
+// register b[i] of the quad thread holding row `row` (quad-uniform result)
+__device__ __forceinline__ double quad_row(const double (&b)[kQRows], int row) {
+  double x = 0.0;
+  const int ir = row >> 2;
+#pragma unroll
+  for (int i = 0; i < kQRows; ++i)
+    if (i == ir) x = b[i];
+  return __shfl_sync(quad_mask(), x, (threadIdx.x & 28) | (row & 3));
+}
+
+// shared-memory 16-byte load the compiler may not cache in registers across
+// the two passes of a reflector application (it would hold v next to b)
+__device__ __forceinline__ double2 lds_v2(const double* p) {
+  double2 r;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return r;
+}
+
+// Applies the reflector (v, tau) to the live columns of a quad: A0 / A1 say
+// which of its two columns take part; extra0 / extra1 are added to the dot
+// products (the R-row entry in TSQR, 0 in the CPQR phase).  Returns tau * w.
+template <bool A0, bool A1>
+__device__ __forceinline__ void quad_apply(double (&b)[2][kQRows], const double* v, double tau, double extra0,
+                                           double extra1, double& tw0, double& tw1) {
+  double d0[4] = {0.0, 0.0, 0.0, 0.0}, d1[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < kQRows; i += 2) {
+    const double2 vv = lds_v2(v + i);
+    if (A0) {
+      d0[i & 3] = fma(vv.x, b[0][i], d0[i & 3]);
+      d0[(i & 3) + 1] = fma(vv.y, b[0][i + 1], d0[(i & 3) + 1]);
+    }
+    if (A1) {
+      d1[i & 3] = fma(vv.x, b[1][i], d1[i & 3]);
+      d1[(i & 3) + 1] = fma(vv.y, b[1][i + 1], d1[(i & 3) + 1]);
+    }
+  }
+  tw0 = A0 ? tau * (quad_sum((d0[0] + d0[1]) + (d0[2] + d0[3])) + extra0) : 0.0;
+  tw1 = A1 ? tau * (quad_sum((d1[0] + d1[1]) + (d1[2] + d1[3])) + extra1) : 0.0;
+#pragma unroll
+  for (int i = 0; i < kQRows; i += 2) {
+    const double2 vv = lds_v2(v + i);
+    if (A0) {
+      b[0][i] = fma(-vv.x, tw0, b[0][i]);
+      b[0][i + 1] = fma(-vv.y, tw0, b[0][i + 1]);
+    }
+    if (A1) {
+      b[1][i] = fma(-vv.x, tw1, b[1][i]);
+      b[1][i + 1] = fma(-vv.y, tw1, b[1][i + 1]);
+    }
+  }
+}
+
+__device__ __forceinline__ void quad_apply_any(bool a0, bool a1, double (&b)[2][kQRows], const double* v, double tau,
+                                               double e0, double e1, double& tw0, double& tw1) {
+  tw0 = tw1 = 0.0;
+  if (a0 && a1)
+    quad_apply<true, true>(b, v, tau, e0, e1, tw0, tw1);
+  else if (a1)
+    quad_apply<false, true>(b, v, tau, e0, e1, tw0, tw1);
+  else if (a0)
+    quad_apply<true, false>(b, v, tau, e0, e1, tw0, tw1);
+}
+
+// TSQR reflector of one owned column (rows of the block) against R(jn, jn).
+__device__ __forceinline__ void quad_tsqr_reflector(double (&b)[kQRows], double* R, int ldr, int jn, double* v,
+                                                    double* tau_out, int q) {
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < kQRows; ++i) s4[i & 3] = fma(b[i], b[i], s4[i & 3]);
+  const double sq = quad_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+  const double c0 = R[jn * ldr + jn];
+  double tau = 0.0, beta = c0, inv = 0.0;
+  if (sq > DBL_MIN) {  // Q is discarded: reciprocals instead of divisions
+    beta = sqrt(c0 * c0 + sq);
+    if (c0 >= 0.0) beta = -beta;
+    inv = 1.0 / (c0 - beta);
+    tau = (beta - c0) * (1.0 / beta);
+  }
+  double* vw = v + q * kQPad;
+#pragma unroll
+  for (int i = 0; i < kQRows; i += 2) {
+    b[i] *= inv;
+    b[i + 1] *= inv;
+    *reinterpret_cast<double2*>(vw + i) = make_double2(b[i], b[i + 1]);
+  }
+  if (q == 0) {
+    R[jn * ldr + jn] = beta;
+    *tau_out = tau;
+  }
+}
+
+// CPQR reflector of the pivot column over rows >= j (Eigen
+// makeHouseholderInPlace); v gets (0 above j, 1 at j, essential below).
+__device__ __forceinline__ void quad_cpqr_reflector(double (&b)[kQRows], int j, double* v, double* sc, int q) {
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < kQRows; ++i)
+    if (q + 4 * i > j) s4[i & 3] = fma(b[i], b[i], s4[i & 3]);
+  const double s = quad_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+  const double c0 = quad_row(b, j);
+  double tau = 0.0, beta = c0, inv = 0.0;
+  if (s > DBL_MIN) {
+    beta = sqrt(c0 * c0 + s);
+    if (c0 >= 0.0) beta = -beta;
+    inv = 1.0 / (c0 - beta);
+    tau = (beta - c0) / beta;
+  }
+  double* vw = v + q * kQPad;
+#pragma unroll
+  for (int i = 0; i < kQRows; i += 2) {
+    double e[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = q + 4 * (i + h);
+      if (row > j) {
+        b[i + h] *= inv;
+        e[h] = b[i + h];
+      } else if (row == j) {
+        b[i + h] = beta;
+        e[h] = 1.0;
+      } else {
+        e[h] = 0.0;
+      }
+    }
+    *reinterpret_cast<double2*>(vw + i) = make_double2(e[0], e[1]);
+  }
+  if (q == 0) {
+    sc[0] = tau;
+    sc[1] = beta;
+  }
+}
+
+// xGEQPF downdate of one live column's norms after step j (quad-uniform).
+__device__ __forceinline__ void quad_downdate(const double (&b)[kQRows], int j, int q, double& upd, double& dirn,
+                                              double thr) {
+  if (upd == 0.0) return;
+  double t = fabs(quad_row(b, j)) / upd;
+  t = (1.0 + t) * (1.0 - t);
+  t = t < 0.0 ? 0.0 : t;
+  const double rr = upd / dirn;
+  if (t * rr * rr <= thr) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kQRows; ++i)
+      if (q + 4 * i > j) s = fma(b[i], b[i], s);
+    upd = dirn = sqrt(quad_sum(s));
+  } else {
+    upd *= sqrt(t);
+  }
+}
+
+size_t tsqr_quad_smem(int n) {
+  return size_t(n) * size_t(n + 1) * sizeof(double) + size_t(2 * 4 * kQPad + 16 + 2 * kQWarps) * sizeof(double) +
+         size_t(2 * kQWarps) * sizeof(int);
+}
+
+__global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restrict__ jobs, int phases) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n, ldr = n + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = tid >> 2, q = tid & 3;
+  const int c0 = g, c1 = g + kQHalf;         // owned columns
+  const bool h0 = c0 < n, h1 = c1 < n;
+  double* R = sm;                                  // n x n, row-major, ld n + 1
+  double* vq = R + n * ldr;                        // 2 x (4 x kQPad) reflector buffers
+  double* taus = vq + 2 * 4 * kQPad;               // 2 (+pad)
+  double* sc = taus + 8;                           // tau, beta
+  double* red = sc + 8;                            // kQWarps pivot partials
+  int* ired = reinterpret_cast<int*>(red + 2 * kQWarps);
+  for (int idx = tid; idx < n * ldr; idx += kQT) R[idx] = 0.0;
+  double b[2][kQRows];
+  // ---------------- TSQR: R0 of W^T
+  for (int r0 = 0; r0 < ((phases & 4) ? 0 : M); r0 += kQBm) {
+    const int rb = min(kQBm, M - r0);
+    const double* s0 = jb.a + r0 + size_t(h0 ? c0 : 0) * jb.lda;
+    const double* s1 = jb.a + r0 + size_t(h1 ? c1 : 0) * jb.lda;
+#pragma unroll
+    for (int i = 0; i < kQRows; ++i) {
+      const int row = q + 4 * i;
+      b[0][i] = (h0 && row < rb) ? __ldg(s0 + row) : 0.0;
+      b[1][i] = (h1 && row < rb) ? __ldg(s1 + row) : 0.0;
+    }
+    __syncthreads();  // R of the previous block complete, buffers free
+    if (g == 0) quad_tsqr_reflector(b[0], R, ldr, 0, vq, taus, q);
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      const int cur = j & 1;
+      const bool a0 = h0 && c0 > j, a1 = h1 && c1 > j;
+      if (a0 || a1) {
+        const double tau = taus[cur];
+        if (tau != 0.0) {
+          const double e0 = a0 ? R[j * ldr + c0] : 0.0, e1 = a1 ? R[j * ldr + c1] : 0.0;
+          double tw0, tw1;
+          quad_apply_any(a0, a1, b, vq + cur * (4 * kQPad) + q * kQPad, tau, e0, e1, tw0, tw1);
+          if (q == 0) {
+            if (a0) R[j * ldr + c0] = e0 - tw0;
+            if (a1) R[j * ldr + c1] = e1 - tw1;
+          }
+        }
+        const int jn = j + 1;
+        if (jn < n && (jn & (kQHalf - 1)) == g) {  // look-ahead: next reflector
+          if (jn < kQHalf)
+            quad_tsqr_reflector(b[0], R, ldr, jn, vq + (cur ^ 1) * (4 * kQPad), taus + (cur ^ 1), q);
+          else
+            quad_tsqr_reflector(b[1], R, ldr, jn, vq + (cur ^ 1) * (4 * kQPad), taus + (cur ^ 1), q);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ---------------- CPQR of R0 (Eigen ColPivHouseholderQR semantics)
+  if (phases & 4) {  // diagnostics: CPQR of the top n x n block alone
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += kQT) R[(idx % n) * ldr + idx / n] = jb.a[(idx % n) + size_t(idx / n) * jb.lda];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < kQRows; ++i) {
+    const int row = q + 4 * i;
+    b[0][i] = (h0 && row < n) ? R[row * ldr + c0] : 0.0;
+    b[1][i] = (h1 && row < n) ? R[row * ldr + c1] : 0.0;
+  }
+  for (int l = tid; l < n; l += kQT) jb.diag[l] = 0.0;
+  double upd0, dir0, upd1, dir1;
+  {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < kQRows; ++i) {
+      s0 = fma(b[0][i], b[0][i], s0);
+      s1 = fma(b[1][i], b[1][i], s1);
+    }
+    upd0 = dir0 = sqrt(quad_sum(s0));
+    upd1 = dir1 = sqrt(quad_sum(s1));
+  }
+  const double thr = sqrt(DBL_EPSILON);
+  int pos0 = c0, pos1 = c1;
+  int done = 0;
+  double r00 = 0.0;
+  const int steps_max = (phases & 8) ? 0 : jb.max_steps > 0 ? min(n, jb.max_steps) : n;
+  for (int j = 0; j < steps_max; ++j) {
+    // (1) first max of the updated norms over logical positions >= j
+    double bv = -1.0;
+    int bp = 0x7fffffff, bq = -1;
+    if (h0 && pos0 >= j) {
+      bv = upd0;
+      bp = pos0;
+      bq = c0;
+    }
+    if (h1 && pos1 >= j && (upd1 > bv || (upd1 == bv && pos1 < bp))) {
+      bv = upd1;
+      bp = pos1;
+      bq = c1;
+    }
+#pragma unroll
+    for (int o = 16; o >= 4; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+      if (ov > bv || (ov == bv && op < bp)) {
+        bv = ov;
+        bp = op;
+        bq = oq;
+      }
+    }
+    if (lane == 0) {
+      red[warp] = bv;
+      ired[warp] = bp;
+      ired[kQWarps + warp] = bq;
+    }
+    __syncthreads();  // (A)
+    bv = -1.0;
+    bp = 0x7fffffff;
+#pragma unroll
+    for (int w = 0; w < kQWarps; ++w) {
+      const double rv = red[w];
+      const int rp = ired[w];
+      if (rv > bv || (rv == bv && rp < bp)) {
+        bv = rv;
+        bp = rp;
+        bq = ired[kQWarps + w];
+      }
+    }
+    const int p = bq, lp = bp;
+    double* v = vq + (j & 1) * (4 * kQPad);
+    // (2) Householder vector of the pivot column over rows >= j
+    if (p == c0)
+      quad_cpqr_reflector(b[0], j, v, sc, q);
+    else if (p == c1)
+      quad_cpqr_reflector(b[1], j, v, sc, q);
+    // logical swap: the column at position j moves to the pivot's slot
+    if (h0) pos0 = (c0 == p) ? j : (pos0 == j ? lp : pos0);
+    if (h1) pos1 = (c1 == p) ? j : (pos1 == j ? lp : pos1);
+    __syncthreads();  // (B)
+    const double tau = sc[0], beta = sc[1];
+    if (j == 0) r00 = fabs(beta);
+    if (tid == 0) jb.diag[j] = fabs(beta);
+    done = j + 1;
+    if (jb.stop_eps > 0.0 && !(fabs(beta) > jb.stop_eps * r00)) break;
+    // (3) the live columns: apply, then downdate their norms
+    const bool a0 = h0 && pos0 > j, a1 = h1 && pos1 > j;
+    if (a0 || a1) {
+      if (tau != 0.0) {
+        double tw0, tw1;
+        quad_apply_any(a0, a1, b, v + q * kQPad, tau, 0.0, 0.0, tw0, tw1);
+      }
+      if (a0) quad_downdate(b[0], j, q, upd0, dir0, thr);
+      if (a1) quad_downdate(b[1], j, q, upd1, dir1, thr);
+    }
+  }
+  if (tid == 0 && jb.steps) *jb.steps = done;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int cu = u ? c1 : c0;
+    if (cu >= n) continue;
+    if (q == 0) jb.perm[u ? pos1 : pos0] = cu;
+#pragma unroll
+    for (int i = 0; i < kQRows; ++i) {
+      const int row = q + 4 * i;
+      if (row < n) jb.a[row + size_t(cu) * jb.lda] = b[u][i];
+    }
+  }
 }
 
 // ---------------------------------------------------------------- cooperative CPQR
@@ -2873,13 +3234,15 @@ int cpqr_blocked_enabled() {
 
 void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
-  static thread_local JobTable<QrJob> tab, ttab;
+  static thread_local JobTable<QrJob> tab, ttab, qtab;
   static std::once_flag attr;
   std::call_once(attr, [] {
     SBX_CUDA(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
     SBX_CUDA(cudaFuncSetAttribute(tsqr_cpqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(kSmemCap)));
+    SBX_CUDA(cudaFuncSetAttribute(tsqr_quad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(tsqr_quad_smem(kQBm))));
   });
   std::vector<QrJob> plain, tall;
   static const bool no_tsqr = std::getenv("SBX_NO_TSQR") != nullptr;  // diagnostics
@@ -2888,12 +3251,26 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
                       qr_smem_need(j.M, j.n, true) > kSmemCap;
     (tsqr ? tall : plain).push_back(j);
   }
-  if (!tall.empty()) {
+  static const int phases = [] {  // diagnostics: bit 2 skips the TSQR, bit 3 the CPQR of R0
+    const char* e = std::getenv("SBX_TSQR_PHASES");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const bool old_tsqr = std::getenv("SBX_TSQR_WARP") != nullptr;  // diagnostics: warp-layout kernel
+  std::vector<QrJob> quad, wide;
+  for (const auto& j : tall) (!old_tsqr && j.n <= kQBm ? quad : wide).push_back(j);
+  if (!quad.empty()) {
     int nmax = 0;
-    for (const auto& j : tall) nmax = std::max(nmax, j.n);
+    for (const auto& j : quad) nmax = std::max(nmax, j.n);
+    const QrJob* d = qtab.upload(quad, s);
+    tsqr_quad_kernel<<<unsigned(quad.size()), kQT, tsqr_quad_smem(nmax), s>>>(d, phases);
+    SBX_LAUNCHED();
+  }
+  if (!wide.empty()) {
+    int nmax = 0;
+    for (const auto& j : wide) nmax = std::max(nmax, j.n);
     const size_t smem = tsqr_smem(nmax);
-    const QrJob* d = ttab.upload(tall, s);
-    tsqr_cpqr_kernel<<<unsigned(tall.size()), kT, smem, s>>>(d, cpqr_blocked_enabled());
+    const QrJob* d = ttab.upload(wide, s);
+    tsqr_cpqr_kernel<<<unsigned(wide.size()), kT, smem, s>>>(d, cpqr_blocked_enabled() | phases);
     SBX_LAUNCHED();
   }
   if (plain.empty()) return;

@@ -150,3 +150,26 @@ def test_row_id_streaming_engine(sb, po, shape):
     if k + 3 <= r:
         kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=6)
         assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
+
+
+TALL = [(128, 700), (114, 855), (20, 1088), (64, 3000), (127, 511), (3, 9000), (96, 400), (1, 30000)]
+
+
+@pytest.mark.parametrize("shape", TALL)
+def test_row_id_tall_quad_tsqr(sb, po, shape):
+    """Tall W^T (functionals >> candidates, n <= 128) on engine 1: the
+    quad-layout TSQR + register CPQR of R0 (dense.cu tsqr_quad_kernel)
+    reproduces the oracle's pivots, rank and interpolation error."""
+    m, n = shape
+    rng = np.random.default_rng(m * 11 + n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=1)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    kf, Jf, Pf = sb.row_id(w, forced=min(k + 3, m), engine=1)
+    assert np.array_equal(Jf[:kk], Jo[:kk])
