@@ -153,8 +153,10 @@ int sbx_hbs_solve_shard_down(sbx_hbs h, int G, int p, const double* hats, int64_
                              double* x_local, int64_t ldx, int flags, void* stream);
 int sbx_hbs_save_hbs1(sbx_hbs h, const char* path);
 int sbx_hbs_load_hbs1(const char* path, sbx_hbs* out);
-/* info[0..9]: n, nodes, total_skeleton, max_block_drawn, has_inverse,
- * solve_factor_doubles, max_depth, max_k, apply_factor_doubles, leaf_nodes */
+/* info[0..11]: n, nodes, total_skeleton, max_block_drawn, has_inverse,
+ * solve_factor_doubles, max_depth, max_k, apply_factor_doubles, leaf_nodes,
+ * top_depth, top_size (the solve's collapsed top: depth and K of the dense
+ * map, 0 when every level runs; set once a solve plan exists) */
 int sbx_hbs_info(sbx_hbs h, int64_t* info);
 int sbx_hbs_node_ranks(sbx_hbs h, int64_t* k, int64_t cap);
 

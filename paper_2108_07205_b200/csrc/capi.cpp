@@ -358,6 +358,8 @@ int sbx_hbs_info(sbx_hbs h, int64_t* info) {
     info[7] = mk;
     info[8] = op.apply_factor_doubles();
     info[9] = op.leaf_nodes;
+    info[10] = op.top_L;
+    info[11] = op.top_K;
   });
 }
 

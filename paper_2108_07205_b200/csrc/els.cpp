@@ -61,6 +61,7 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
   hbs_run_plan(A, P, A.ws.get(), nrhs, s, tr ? A.arena_t.get() : nullptr);
   // gather: out row i <- old row map[i]
   launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
+  phase_mark("els:   a_oo sweep", s);
   if (e.n_p == 0) return;
   const double* vp = v + nkc;
   double* op = out + nkc;
@@ -73,6 +74,7 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
     launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
     hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
     launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, op, ldo, nullptr, s);
+    phase_mark("els:   A_pp sweep", s);
   } else {  // explicit inverse of A_pp (els.cpp:47: app_lu.solve / app_lu.transpose().solve)
     gemm_batched({{e.app->inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
                    int(ldo), tr ? 1 : 0, 0, 1.0, 0.0}},
@@ -155,6 +157,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
                    0, 1.0, 0.0}},
                  s);
     launch_add_identity(e->Wmat.get(), k, k, s);
+    phase_mark("els:   W = I + R X", s);
     DevBuf<double> wlu(static_cast<size_t>(k * k));
     SBX_CUDA(cudaMemcpyAsync(wlu.get(), e->Wmat.get(), size_t(k * k) * 8, cudaMemcpyDeviceToDevice, s));
     e->Winv.resize(size_t(k * k));

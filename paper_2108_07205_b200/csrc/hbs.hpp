@@ -13,6 +13,8 @@
 // All blocks are column-major (Eigen order) so HBS1 files map 1:1.
 #pragma once
 
+#include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -34,13 +36,17 @@ struct HbsNodeH {
 // One row-tiled product  D[rows] = A * B (+ P)  inside a sweep level.
 // Offsets are in doubles (A, into the factor arena) or in rows of the
 // row-major sweep workspace (B, P, D1, D2; one row = nrhs doubles).
+// Producers one sweep task may wait on (the collapsed top of the tree reads
+// the hats of up to 2^5 boxes).
+constexpr int kMaxDep = 32;
+
 struct SweepTask {
   i64 a_off;
   int lda, m, K;
   i64 b_row, p_row, d1_row, d2_row;
   int split;  // rows < split go to D1, the rest to D2 (row - split)
   int ndep;   // tasks whose outputs this task reads (dataflow sweep)
-  int dep[4];
+  int dep[kMaxDep];
 };
 
 // One work item of the dataflow sweep: rows [row0, row0 + tile) x column
@@ -55,17 +61,18 @@ struct FlowItem {
 };
 
 // Everything one dataflow item needs, denormalised so a CTA can prefetch the
-// descriptor of its next item with one asynchronous copy (144 bytes).
+// descriptor of its next item with one asynchronous copy.
 struct alignas(16) ItemDesc {
   FlowItem it;
   SweepTask t;
-  int need[4];  // completed items awaited per producer task (same column tile)
+  int need[kMaxDep];  // completed items awaited per producer task (same column tile)
 };
 
 struct SweepLevel {
   std::vector<SweepTask> tasks;
   i64 first_task = 0;  // index into the flattened device task table
   int max_k = 0;       // largest K in the level (smem sizing)
+  int ksplit = 0;      // > 0: split K of this level's full row tiles this many ways
 };
 
 struct SweepPlan {
@@ -74,21 +81,25 @@ struct SweepPlan {
   i64 in_row = 0, out_row = 0;     // input / output vector regions
   int n_tasks = 0;
   DevBuf<SweepTask> d_tasks;
-  // work items (task, row0, col tile) for the current (tile, column-tile
-  // count) key, per-level ranges, and the per-(task, col tile) completion
-  // counters + item ticket of the dataflow sweep
-  int flow_key = -1;
+  std::vector<SweepTask> h_tasks;  // host copy of the flattened task table
+  // work items (task, row0, col tile), per-level ranges, and the per-(task,
+  // col tile) completion counters of the dataflow sweep, one set per
+  // (tile, column-tile count) key: a step alternates block widths (the
+  // Woodbury build's u columns, the solve's RHS) without rebuilding them
+  std::map<int, std::unique_ptr<struct FlowCache>> flows;
+  bool built = false;
+};
+
+struct FlowCache {
   std::vector<int2> level_items;
   DevBuf<FlowItem> d_flow_items;
-  DevBuf<ItemDesc> d_descs;        // per flow item (dataflow kernel)
-  std::vector<SweepTask> h_tasks;  // host copy of the flattened task table
-  DevBuf<int> d_needs;             // items per task and column tile (dependency counts)
-  i64 partial_elems = 0;           // split-K partial tiles (doubles)
+  DevBuf<ItemDesc> d_descs;  // per flow item (dataflow kernel)
+  DevBuf<int> d_needs;       // items per task and column tile (dependency counts)
+  i64 partial_elems = 0;     // split-K partial tiles (doubles)
   int n_tile_cnt = 0;
   DevBuf<double> d_partials;
   i64 n_flow_items = 0;
   DevBuf<int> d_counters;
-  bool built = false;
 };
 
 struct ShardPlans;
@@ -103,6 +114,12 @@ struct HbsOp {
   std::vector<HbsNodeH> nodes;
   std::vector<std::string> notes;
   i64 o_root_g = -1;
+  // Collapsed top of the tree (sweep.cu hbs_build_top): the solve's levels
+  // above depth top_L fold into one dense K x K map (at o_top in the arena)
+  // from the stacked up-sweep hats of the depth-top_L boxes to their
+  // down-sweep inputs; top_L == 0 runs every level.
+  int top_L = 0;
+  i64 o_top = -1, top_K = 0, top_cap = 0;
   DevBuf<double> arena;
   i64 arena_used = 0;
   SweepPlan solve_plan, apply_plan;

@@ -545,6 +545,15 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
   const double thr = std::max(std::min(10.0 * op.eps, 1e-6), 1e-14);  // hbs.cpp:429
   double* A = op.arena.get();
   const size_t nn = op.nodes.size();
+  // rcond gates (hbs.cpp:429) are checked once at the end: the levels run
+  // back to back on the stream without host round trips; a failing block
+  // is reported as the deepest (first factored) offending one
+  struct Gate {
+    std::vector<size_t> ids;
+    DevBuf<double> rc;
+    int depth;
+  };
+  std::vector<std::unique_ptr<Gate>> gates;
   for (int depth = op.max_depth; depth >= 0; --depth) {
     std::vector<size_t> ids;
     for (size_t i = 0; i < nn; ++i)
@@ -588,7 +597,14 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
     }
     copy_batched(cj, s);
     DevBuf<int> piv(static_cast<size_t>(std::max<i64>(tot, 1)));
-    DevBuf<double> rc(ids.size() * 2 + 1), work;
+    gates.push_back(std::make_unique<Gate>());
+    Gate& gt = *gates.back();
+    gt.ids = ids;
+    gt.depth = depth;
+    gt.rc.resize(ids.size() * 2 + 1);
+    DevBuf<double>& rc = gt.rc;
+    SBX_CUDA(cudaMemsetAsync(rc.get(), 0x7f, rc.size() * sizeof(double), s));  // unset gates pass
+    DevBuf<double> work;
     i64 wtot = 0;
     for (size_t q = 0; q < ids.size(); ++q) wtot += 4 * (op.nodes[ids[q]].c + op.nodes[ids[q]].k);
     work.resize(size_t(std::max<i64>(wtot, 1)));
@@ -612,18 +628,6 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
       lj_node.push_back(q);
     }
     lu_batched(lj, s);
-    std::vector<double> hrc(ids.size() * 2 + 1, 1.0);
-    rc.download(hrc.data(), hrc.size(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
-    for (size_t q : lj_node) {
-      const auto& nd = op.nodes[ids[q]];
-      const double r = hrc[2 * q];
-      if (!(r >= thr))
-        throw Error(4, std::string("singular ") + (ids[q] == 0 ? "root" : "diagonal") +
-                           " block (rcond " + std::to_string(r) + ") at tree node [" +
-                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
-                           std::to_string(nd.depth));
-    }
     phase_mark("inv: x blocks + LU/inverse", s);
     if (depth == 0) break;  // the root keeps only root_g (hbs.cpp:450-458)
     // t = v^T xi (k x c), tu = t u (k x k)
@@ -662,16 +666,6 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
       lj2_node.push_back(q);
     }
     lu_batched(lj2, s);
-    rc.download(hrc.data(), hrc.size(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
-    for (size_t q : lj2_node) {
-      const auto& nd = op.nodes[ids[q]];
-      const double r = hrc[2 * q + 1];
-      if (!(r >= thr))
-        throw Error(4, "singular skeleton block (rcond " + std::to_string(r) + ") at tree node [" +
-                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
-                           std::to_string(nd.depth));
-    }
     // e = (xi u) dhat, f = dhat t, g = xi - e t   (hbs.cpp:480-483)
     std::vector<GemmJob> g3, g4;
     std::vector<CopyJob> cg;
@@ -696,7 +690,27 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
     }
     gemm_batched(g4, s);
     phase_mark("inv: skeleton LU + e,f,g GEMMs", s);
+  }
+  for (const auto& gp : gates) {  // deepest level first, x block before skeleton block
+    const Gate& gt = *gp;
+    std::vector<double> hrc(gt.rc.size());
+    gt.rc.download(hrc.data(), hrc.size(), s);
     SBX_CUDA(cudaStreamSynchronize(s));
+    for (size_t q = 0; q < gt.ids.size(); ++q) {
+      const auto& nd = op.nodes[gt.ids[q]];
+      if (nd.c > 0 && !(hrc[2 * q] >= thr))
+        throw Error(4, std::string("singular ") + (gt.ids[q] == 0 ? "root" : "diagonal") +
+                           " block (rcond " + std::to_string(hrc[2 * q]) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
+    for (size_t q = 0; q < gt.ids.size(); ++q) {
+      const auto& nd = op.nodes[gt.ids[q]];
+      if (gt.ids[q] != 0 && nd.c > 0 && nd.k > 0 && !(hrc[2 * q + 1] >= thr))
+        throw Error(4, "singular skeleton block (rcond " + std::to_string(hrc[2 * q + 1]) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
   }
   phase_mark("inv: done", s);
   op.has_inverse = true;

@@ -81,6 +81,9 @@ void hbs_layout(HbsOp& op) {
   op.o_root_g = place(op.nodes[0].c * op.nodes[0].c);
   op.arena_used = off;
   op.arena.resize(size_t(std::max<i64>(off, 32)));
+  op.top_L = 0;
+  op.o_top = -1;
+  op.top_K = op.top_cap = 0;
   op.solve_plan.built = false;
   op.apply_plan.built = false;
 }

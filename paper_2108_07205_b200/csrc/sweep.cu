@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
       gemv_prefetch<kGRs>(fac, t, it.row0, it.kb, it.ke, g);
     else
       gemv_prefetch<kGR>(fac, t, it.row0, it.kb, it.ke, g);
-    if (threadIdx.x < t.ndep) {
-      const int d = t.dep[threadIdx.x];
+    if (threadIdx.x < D.t.ndep) {  // from the shared descriptor (dynamic index)
+      const int d = D.t.dep[threadIdx.x];
       const int need = D.need[threadIdx.x];
       const int* p = counters + 1 + d * ncol + it.ct;
       while (ld_acquire(p) < need) __nanosleep(32);
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
         __threadfence();
         const double* pb = partials + it.poff;
         if constexpr (kDmma) {
-          for (int e = threadIdx.x; e < kTM * TN; e += kThreads) {
+          for (int e = threadIdx.x; e < it.tile * TN; e += kThreads) {
             const int r = e / TN, cc = e % TN;
             const int row = it.row0 + r, col = it.ct * TN + cc;
             if (row >= t.m || col >= nrhs) continue;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
             ws[dst * ldw + col] = v;
           }
         } else {
-          for (int r = threadIdx.x; r < kGR; r += kThreads) {
+          for (int r = threadIdx.x; r < it.tile; r += kThreads) {
             const int row = it.row0 + r;
             if (row >= t.m) continue;
             double v = 0.0;
@@ -526,7 +526,7 @@ namespace {
 // over more CTAs.  Returns per-level [first, count).
 std::vector<FlowItem> make_items(SweepPlan& plan, int tile0, int ncol, int tile_elems, int target,
                                  std::vector<int2>* ranges, i64* partial_elems, int* n_tile_cnt,
-                                 std::vector<int>* needs, int small_tile, i64 small_below) {
+                                 std::vector<int>* needs, int small_tile, i64 small_below, int kcap) {
   std::vector<FlowItem> fi;
   needs->assign(size_t(plan.n_tasks), 0);
   i64 poff = 0;
@@ -536,15 +536,20 @@ std::vector<FlowItem> make_items(SweepPlan& plan, int tile0, int ncol, int tile_
     i64 base = 0;
     for (const auto& tk : L.tasks) base += (tk.m + tile0 - 1) / tile0;
     base *= ncol;
-    // short levels (the tree's critical path) take smaller row tiles
-    const int tile = (small_tile > 0 && base < small_below) ? small_tile : tile0;
+    // short levels (the tree's critical path) take smaller row tiles; a
+    // level with a forced K split (the collapsed top) is cut into K chunks
+    // of at most kcap (a GEMV item then holds its whole block in registers
+    // before the dependency wait)
+    const int tile = L.ksplit > 0 ? (kcap > 128 && small_tile > 0 ? small_tile : tile0)
+                     : (small_tile > 0 && base < small_below) ? small_tile : tile0;
     const int lsplit_ok = tile == tile0;
-    const int lsplit =
-        lsplit_ok && target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base)) : 1;
+    const int lsplit = L.ksplit > 0 ? int((L.max_k + kcap - 1) / kcap)
+                       : lsplit_ok && target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base))
+                                                               : 1;
     for (int ct = 0; ct < ncol; ++ct)
       for (size_t t = 0; t < L.tasks.size(); ++t) {
         const auto& tk = L.tasks[t];
-        const int ns = std::max(1, std::min(lsplit, tk.K / 32));
+        const int ns = L.ksplit > 0 ? lsplit : std::max(1, std::min(lsplit, tk.K / 32));
         // split boundaries on multiples of 16 (the DMMA K chunk)
         const int per = ((tk.K + ns - 1) / ns + 15) / 16 * 16;
         const int nsplit = std::max(1, (tk.K + per - 1) / std::max(per, 1));
@@ -599,7 +604,7 @@ void finalize(SweepPlan& plan) {
         bool seen = false;
         for (int q = 0; q < t.ndep; ++q) seen |= t.dep[q] == w;
         if (seen) continue;
-        require(t.ndep < 4, "sweep plan: task reads from more than four producers");
+        require(t.ndep < kMaxDep, "sweep plan: task reads from too many producers");
         t.dep[t.ndep++] = w;
       }
     };
@@ -611,7 +616,7 @@ void finalize(SweepPlan& plan) {
     }
   }
   plan.n_tasks = int(all.size());
-  plan.flow_key = -1;
+  plan.flows.clear();
   const cudaStream_t st = cur_stream();
   plan.d_tasks.upload(all, st);
   plan.h_tasks = all;
@@ -674,7 +679,7 @@ SolveLayout solve_layout(const HbsOp& op) {
 // Solve tasks: up-sweep of the nodes in up_sel (deepest level first), the
 // root product when `root`, down-sweep of the nodes in down_sel.
 void build_solve_tasks(const HbsOp& op, const SolveLayout& Y, const std::vector<char>& up_sel, bool root,
-                       const std::vector<char>& down_sel, SweepPlan& P) {
+                       const std::vector<char>& down_sel, SweepPlan& P, int top = 0) {
   P.levels.clear();
   P.in_row = Y.in_row;
   P.out_row = Y.out_row;
@@ -690,7 +695,7 @@ void build_solve_tasks(const HbsOp& op, const SolveLayout& Y, const std::vector<
     finalize(P);
     return;
   }
-  for (int d = op.max_depth; d >= 1; --d) {  // up
+  for (int d = op.max_depth; d >= std::max(top, 1); --d) {  // up
     SweepLevel L;
     for (size_t i = 1; i < nn; ++i) {
       const auto& nd = op.nodes[i];
@@ -700,14 +705,22 @@ void build_solve_tasks(const HbsOp& op, const SolveLayout& Y, const std::vector<
     }
     if (!L.tasks.empty()) P.levels.push_back(std::move(L));
   }
-  if (root) {
+  if (root && top > 0) {  // collapsed top: inc(depth-top boxes) = T * hat(depth-top boxes)
+    size_t first = 0;
+    while (op.nodes[first].depth != top) ++first;
+    SweepLevel L;
+    const i64 K = op.top_K;
+    L.tasks.push_back(mk(op.o_top, K, K, K, Y.hat[first], -1, Y.inc[first], 0, K));
+    L.ksplit = int(std::min<i64>(8, std::max<i64>(1, (K + 127) / 128)));
+    P.levels.push_back(std::move(L));
+  } else if (root) {
     SweepLevel L;
     const auto& nd = op.nodes[0];
     L.tasks.push_back(mk(op.o_root_g, nd.c, nd.c, nd.c, Y.hat[size_t(nd.left)], -1, Y.inc[size_t(nd.left)], 0,
                          nd.c));
     P.levels.push_back(std::move(L));
   }
-  for (int d = 1; d <= op.max_depth; ++d) {  // down
+  for (int d = std::max(top, 1); d <= op.max_depth; ++d) {  // down
     SweepLevel L;
     for (size_t i = 1; i < nn; ++i) {
       const auto& nd = op.nodes[i];
@@ -721,11 +734,111 @@ void build_solve_tasks(const HbsOp& op, const SolveLayout& Y, const std::vector<
 }
 }  // namespace
 
+namespace {
+// Depth at which the solve's top collapses (0: none).  Every box above it
+// must be internal, the depth-L boxes feed one task (2^L <= kMaxDep
+// producers) and the dense map stays small next to the factors.
+int choose_top(const HbsOp& op) {
+  static const int env = [] {
+    const char* e = std::getenv("SBX_SWEEP_TOP");  // depth, 0 disables
+    return e ? std::atoi(e) : -1;
+  }();
+  static const i64 kmax = [] {
+    const char* e = std::getenv("SBX_SWEEP_TOP_KMAX");
+    return e ? std::atoll(e) : 1280;
+  }();
+  if (op.nodes.size() < 3 || env == 0) return 0;
+  int min_leaf = 1 << 30;
+  for (const auto& nd : op.nodes)
+    if (nd.is_leaf()) min_leaf = std::min(min_leaf, nd.depth);
+  if (env < 0 && op.max_depth < 7) return 0;  // shallow trees: few levels to save
+  int best = 0;
+  for (int L = 2; L < min_leaf && (1 << L) <= kMaxDep; ++L) {
+    i64 K = 0;
+    for (const auto& nd : op.nodes)
+      if (nd.depth == L) K += nd.k;
+    if (env > 0) {
+      if (L == env) best = L;
+      continue;
+    }
+    if (K <= kmax) best = L;
+  }
+  return best;
+}
+
+// T_L by the recursion over the top levels (d = 1 .. L-1):
+//   M_1 = root_g,  M_{d+1} = blockdiag(e_p) M_d blockdiag(f_p) + blockdiag(g_p)
+// over the depth-d boxes p in BFS order (their children are the depth-(d+1)
+// boxes, in order), which is the map the up-sweep, root product and
+// down-sweep of those levels apply to the stacked depth-(d+1) hats.  The
+// transposed solve sees M^T (same recursion over the transposed factors).
+void hbs_build_top(HbsOp& op, int L, cudaStream_t s) {
+  std::vector<std::vector<size_t>> lev(size_t(L + 1));
+  for (size_t i = 0; i < op.nodes.size(); ++i)
+    if (op.nodes[i].depth <= L) lev[size_t(op.nodes[i].depth)].push_back(i);
+  auto ksum = [&](int d) {
+    i64 K = 0;
+    for (size_t i : lev[size_t(d)]) K += op.nodes[i].k;
+    return K;
+  };
+  const double* A = op.arena.get();
+  i64 Kd = op.nodes[0].c;
+  DevBuf<double> M(static_cast<size_t>(Kd * Kd));
+  SBX_CUDA(cudaMemcpyAsync(M.get(), A + op.o_root_g, size_t(Kd * Kd) * 8, cudaMemcpyDeviceToDevice, s));
+  for (int d = 1; d < L; ++d) {
+    const i64 Kn = ksum(d + 1);
+    DevBuf<double> Z(static_cast<size_t>(Kd * Kn)), Mn(static_cast<size_t>(Kn * Kn));
+    SBX_CUDA(cudaMemsetAsync(Mn.get(), 0, size_t(Kn * Kn) * 8, s));
+    std::vector<GemmJob> zj, ej;
+    std::vector<CopyJob> gj;
+    i64 ko = 0, co = 0;
+    for (size_t i : lev[size_t(d)]) {
+      const auto& p = op.nodes[i];
+      const int k = int(p.k), c = int(p.c);
+      if (k > 0) {
+        zj.push_back({M.get() + ko * Kd, A + p.o_fg, Z.get() + co * Kd, int(Kd), c, k, int(Kd), k + c, int(Kd), 0, 0,
+                      1.0, 0.0});
+        ej.push_back({A + p.o_e, Z.get() + ko, Mn.get() + co, c, int(Kn), k, c, int(Kd), int(Kn), 0, 0, 1.0, 1.0});
+      }
+      gj.push_back({A + p.o_fg + k, Mn.get() + co + co * Kn, c, c, k + c, int(Kn), 0, 0});
+      ko += k;
+      co += c;
+    }
+    require(ko == Kd && co == Kn, "sweep top: level sizes inconsistent");
+    copy_batched(gj, s);
+    if (!zj.empty()) {
+      SBX_CUDA(cudaMemsetAsync(Z.get(), 0, size_t(Kd * Kn) * 8, s));
+      gemm_batched(zj, s);
+      gemm_batched(ej, s);
+    }
+    SBX_CUDA(cudaStreamSynchronize(s));  // job tables are reused by the next level
+    M = std::move(Mn);
+    Kd = Kn;
+  }
+  if (op.o_top < 0 || op.top_cap < Kd * Kd) {  // grow the arena by the map
+    const i64 off = (op.arena_used + 31) / 32 * 32;
+    DevBuf<double> grown(static_cast<size_t>(off + Kd * Kd));
+    SBX_CUDA(cudaMemcpyAsync(grown.get(), op.arena.get(), size_t(op.arena_used) * 8, cudaMemcpyDeviceToDevice, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
+    op.arena = std::move(grown);
+    op.o_top = off;
+    op.top_cap = Kd * Kd;
+    op.t_solve = op.t_apply = false;  // the transposed arena is rebuilt on next use
+  }
+  SBX_CUDA(cudaMemcpyAsync(op.arena.get() + op.o_top, M.get(), size_t(Kd * Kd) * 8, cudaMemcpyDeviceToDevice, s));
+  SBX_CUDA(cudaStreamSynchronize(s));
+  op.top_L = L;
+  op.top_K = Kd;
+}
+}  // namespace
+
 void hbs_build_solve_plan(HbsOp& op) {
   require(op.has_inverse, "hbs_solve: inverse not built");
   const SolveLayout Y = solve_layout(op);
   const std::vector<char> all(op.nodes.size(), 1);
-  build_solve_tasks(op, Y, all, true, all, op.solve_plan);
+  const int L = choose_top(op);
+  if (L > 0) hbs_build_top(op, L, cur_stream());
+  build_solve_tasks(op, Y, all, true, all, op.solve_plan, L);
 }
 
 ShardPlans& hbs_shard(HbsOp& op, int G, int p) {
@@ -966,31 +1079,37 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     const char* e = std::getenv("SBX_SWEEP_DMMA_SMALL_BELOW");
     return e ? std::atoi(e) : 300;
   }();
+  static const int small_below_gemv = [] {
+    const char* e = std::getenv("SBX_SWEEP_GEMV_SMALL_BELOW");
+    return e ? std::atoi(e) : 300;
+  }();
   const int key = ((ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0)) * 128 + TN;
-  if (plan.flow_key != key) {
-    plan.level_items.clear();
+  auto& slot = plan.flows[key];
+  const bool fresh = !slot;
+  if (fresh) slot = std::make_unique<FlowCache>();
+  FlowCache& F = *slot;
+  if (fresh) {
     std::vector<int> needs;
     const std::vector<FlowItem> fi =
-        make_items(plan, tile, ncol, dmma ? kTM * TN : kGR, target, &plan.level_items, &plan.partial_elems,
-                   &plan.n_tile_cnt, &needs, per_level ? 0 : (dmma ? dmma_small : kGRs),
-                   dmma ? small_below_dmma : 600);
-    plan.d_flow_items.upload(fi, s);
-    plan.d_needs.upload(needs, s);
+        make_items(plan, tile, ncol, dmma ? kTM * TN : kGR, target, &F.level_items, &F.partial_elems,
+                   &F.n_tile_cnt, &needs, per_level ? 0 : (dmma ? dmma_small : kGRs),
+                   dmma ? small_below_dmma : small_below_gemv, dmma ? 128 : kGRs * GemvShape<kGRs>::kGV);
+    F.d_flow_items.upload(fi, s);
+    F.d_needs.upload(needs, s);
     std::vector<ItemDesc> descs(fi.size());
     for (size_t q = 0; q < fi.size(); ++q) {
       ItemDesc& D = descs[q];
       D.it = fi[q];
       D.t = plan.h_tasks[size_t(fi[q].task)];
-      for (int d = 0; d < 4; ++d) D.need[d] = d < D.t.ndep ? needs[size_t(D.t.dep[d])] : 0;
+      for (int d = 0; d < kMaxDep; ++d) D.need[d] = d < D.t.ndep ? needs[size_t(D.t.dep[d])] : 0;
     }
-    plan.d_descs.upload(descs, s);
-    plan.n_flow_items = i64(fi.size());
-    plan.flow_key = key;
+    F.d_descs.upload(descs, s);
+    F.n_flow_items = i64(fi.size());
   }
   if (per_level) {
-    for (const int2 rg : plan.level_items) {
+    for (const int2 rg : F.level_items) {
       if (rg.y == 0) continue;
-      const FlowItem* items = plan.d_flow_items.get() + rg.x;
+      const FlowItem* items = F.d_flow_items.get() + rg.x;
       if (!dmma)
         sweep_gemv_kernel<<<unsigned(rg.y), kThreads, gemv_smem, s>>>(fac, ws, plan.d_tasks.get(), items);
       else
@@ -1000,42 +1119,42 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     }
     return;
   }
-  if (plan.n_flow_items == 0) return;
-  const size_t ncount = size_t(1 + plan.n_tasks * ncol + plan.n_tile_cnt);
-  plan.d_counters.reserve(ncount);
-  plan.d_partials.reserve(size_t(std::max<i64>(plan.partial_elems, 1)));
-  SBX_CUDA(cudaMemsetAsync(plan.d_counters.get(), 0, ncount * sizeof(int), s));
-  int* tile_cnt = plan.d_counters.get() + 1 + plan.n_tasks * ncol;
-  const int grid = int(std::min<i64>(plan.n_flow_items, i64(sms) * per_sm));
+  if (F.n_flow_items == 0) return;
+  const size_t ncount = size_t(1 + plan.n_tasks * ncol + F.n_tile_cnt);
+  F.d_counters.reserve(ncount);
+  F.d_partials.reserve(size_t(std::max<i64>(F.partial_elems, 1)));
+  SBX_CUDA(cudaMemsetAsync(F.d_counters.get(), 0, ncount * sizeof(int), s));
+  int* tile_cnt = F.d_counters.get() + 1 + plan.n_tasks * ncol;
+  const int grid = int(std::min<i64>(F.n_flow_items, i64(sms) * per_sm));
   static const char* trace_path = std::getenv("SBX_SWEEP_TRACE");  // diagnostics: per-item timeline
   DevBuf<unsigned long long> trace;
-  if (trace_path) trace.resize(size_t(4 * plan.n_flow_items));
+  if (trace_path) trace.resize(size_t(4 * F.n_flow_items));
   KernelTimer kt(dmma ? "sweep_flow_dmma" : "sweep_flow_gemv", s);
   if (dmma)
-    sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), plan.d_flow_items.get(),
-                                                             int(plan.n_flow_items), plan.d_counters.get(), ncol,
-                                                             int(nrhs), int(sweep_ld(nrhs)), plan.d_partials.get(),
-                                                             tile_cnt, trace.get(), plan.d_descs.get());
+    sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), F.d_flow_items.get(),
+                                                             int(F.n_flow_items), F.d_counters.get(), ncol,
+                                                             int(nrhs), int(sweep_ld(nrhs)), F.d_partials.get(),
+                                                             tile_cnt, trace.get(), F.d_descs.get());
   else
     sweep_flow_kernel<false, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
-                                                              plan.d_flow_items.get(), int(plan.n_flow_items),
-                                                              plan.d_counters.get(), ncol, int(nrhs), 1,
-                                                              plan.d_partials.get(), tile_cnt, trace.get(),
-                                                              plan.d_descs.get());
+                                                              F.d_flow_items.get(), int(F.n_flow_items),
+                                                              F.d_counters.get(), ncol, int(nrhs), 1,
+                                                              F.d_partials.get(), tile_cnt, trace.get(),
+                                                              F.d_descs.get());
   SBX_LAUNCHED();
   if (trace_path) {
-    std::vector<unsigned long long> h(size_t(4 * plan.n_flow_items));
-    std::vector<FlowItem> fi(size_t(plan.n_flow_items));
+    std::vector<unsigned long long> h(size_t(4 * F.n_flow_items));
+    std::vector<FlowItem> fi(size_t(F.n_flow_items));
     trace.download(h.data(), h.size(), s);
-    plan.d_flow_items.download(fi.data(), fi.size(), s);
+    F.d_flow_items.download(fi.data(), fi.size(), s);
     SBX_CUDA(cudaStreamSynchronize(s));
     std::vector<int> level_of(size_t(plan.n_tasks), 0);
     for (size_t l = 0; l < plan.levels.size(); ++l)
       for (size_t t = 0; t < plan.levels[l].tasks.size(); ++t)
         level_of[size_t(plan.levels[l].first_task) + t] = int(l);
     if (FILE* f = std::fopen(trace_path, "a")) {
-      std::fprintf(f, "# nrhs %lld items %lld grid %d\n", (long long)nrhs, (long long)plan.n_flow_items, grid);
-      for (i64 i = 0; i < plan.n_flow_items; ++i) {
+      std::fprintf(f, "# nrhs %lld items %lld grid %d\n", (long long)nrhs, (long long)F.n_flow_items, grid);
+      for (i64 i = 0; i < F.n_flow_items; ++i) {
         const auto& it = fi[size_t(i)];
         const auto& tk = plan.levels[size_t(level_of[size_t(it.task)])];
         (void)tk;
@@ -1126,6 +1245,7 @@ void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s) {
     require(op.has_inverse, "hbs_solve_t: inverse not built");
     const i64 c0 = op.nodes[0].c;
     tr(op.o_root_g, int(c0), op.o_root_g, int(c0), int(c0), int(c0), 1);
+    if (op.top_L > 0) tr(op.o_top, int(op.top_K), op.o_top, int(op.top_K), int(op.top_K), int(op.top_K), 1);
     for (size_t i = 1; i < nn; ++i) {
       const auto& nd = op.nodes[i];
       const int k = int(nd.k), c = int(nd.c), ld = k + c;

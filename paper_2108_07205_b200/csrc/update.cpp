@@ -721,6 +721,18 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     } else {
       t_app(s);
     }
+  } else if (par_mode == 5) {
+    // the A_pp build (the step's critical path) on a high-priority worker
+    // stream, every row ID of the update on a normal-priority one
+    parallel_tasks({[&](cudaStream_t w) {
+                      t_far(w);
+                      t_kc(w);
+                      t_kp(w);
+                      t_pk_far(w);
+                      t_pk_near(w);
+                    },
+                    t_app},
+                   s, {0, 1});
   } else if (par_mode == 3) {
     t_kc(s);
     t_kp(s);
@@ -771,9 +783,12 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   const i64 n_ext = u->n_ext(), k1 = u->k1;
   if (k1 == 0) return u;
   // stacked L1 (n_ext x k1) and R1 (k1 x n_ext)  (lowrank.cpp:240-251)
+  phase_mark("update:   settle", s);
   DevBuf<double> L1(static_cast<size_t>(n_ext * k1)), R1(static_cast<size_t>(k1 * n_ext));
+  phase_mark("update:   L1/R1 alloc", s);
   SBX_CUDA(cudaMemsetAsync(L1.get(), 0, size_t(n_ext * k1) * 8, s));
   SBX_CUDA(cudaMemsetAsync(R1.get(), 0, size_t(k1 * n_ext) * 8, s));
+  phase_mark("update:   L1/R1 memset", s);
   const i64 ckc = k_pk, ckp = k_pk + kc.k;
   DevBuf<i64> d_far_s, d_near_s, d_added_rows;
   d_far_s.upload(far_s, s);
@@ -800,6 +815,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     scat(pk_near.P.get(), d_added_rows.get(), pk_near.m, pk_near.k, int(pk_far.k), 1.0);
   }
   scatter_batched(sj, s);
+  phase_mark("update:   L1 scatter", s);
   // R blocks straight into R1
   {
     std::vector<i64> ri_old, ci_old, ri_new, ci_new, dstc_new;
@@ -848,6 +864,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     e.upload(dstc_new, s);
     ja.upload(jo, s);
     jb.upload(jn, s);
+    phase_mark("update:   R1 index upload", s);
     launch_block_jobs(eold.view(), ja.get(), int(jo.size()), mo, a.get(), b.get(), R1.get(), s);
     launch_block_jobs(enew.view(), jb.get(), int(jn.size()), mn, c.get(), d.get(), R1.get(), s, e.get());
   }

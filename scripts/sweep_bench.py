@@ -50,6 +50,8 @@ def main():
         flops = 2.0 * nrhs * info["factor_doubles"]
         print(f"nrhs={nrhs:4d}: call {ms*1e3:8.1f} us, kernel {kms*1e3:8.1f} us  factor bytes {fb/1e6:.1f} MB"
               f" -> kernel {fb/kms/1e6:.1f} GB/s (1 pass), {flops/kms/1e9:.2f} TF/s", flush=True)
+    i2 = h.info()
+    print(f"collapsed top: depth {i2['top_L']}, K {i2['top_K']} ({i2['top_K'] ** 2 * 8 / 1e6:.1f} MB)")
 
 
 if __name__ == "__main__":

@@ -6,6 +6,8 @@ Tier 2: independent device compression -> reference test assertions (dense
 operator / dense solve / analytic field) and 1e-9 agreement with the
 oracle's refined solve.
 """
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -184,3 +186,29 @@ def test_cfg1_els_matches_dense_and_field(sb, po):
     vel = o1.evaluate_velocity(po.INTERIOR, sb.density_on_refined(e, tau), tg)
     ex = po.field_velocity(src, tg)
     assert np.max(np.linalg.norm(vel - ex, axis=1) / np.linalg.norm(ex, axis=1)) < 1e-8
+
+
+@pytest.mark.parametrize("top", [2, 3, 4])
+def test_collapsed_top_matches_oracle(po, tmp_path, top):
+    """Solve with the top of the tree collapsed into one dense map
+    (sweep.cu hbs_build_top, SBX_SWEEP_TOP=depth) against the oracle's
+    level-by-level sweep on the same HBS1 factors, plain and transposed."""
+    import os
+    import subprocess
+    import sys
+    o = po.Geom.create(po.STAR, 80, prongs=5, amplitude=0.3)  # 1280 nodes: leaves at depth 5
+    a = po.Assembler.create(o)
+    h = po.Hbs.compress(a, 1e-10).invert()
+    h.save(tmp_path / "h.hbs1")
+    n = h.info()["n"]
+    b = np.random.default_rng(5).standard_normal((n, 130))
+    np.save(tmp_path / "b.npy", b)
+    np.save(tmp_path / "x.npy", h.solve(b))
+    np.save(tmp_path / "xt.npy", h.solve_t(b))
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, SBX_SWEEP_TOP=str(top), PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, str(Path(__file__).parent / "top_sweep_case.py"), str(tmp_path / "h.hbs1"),
+                        str(tmp_path / "b.npy"), str(tmp_path / "x.npy"), str(tmp_path / "xt.npy")],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"top {top}" in r.stdout, r.stdout
