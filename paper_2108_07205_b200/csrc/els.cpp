@@ -1,5 +1,7 @@
 // ELS / Woodbury build and solve on the device (reference els.cpp:25-203).
 #include "els.hpp"
+
+#include <cstdlib>
 #include "idengine.hpp"
 
 #include <cmath>
@@ -109,9 +111,15 @@ std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan,
   } else {
     HbsBuildOptions o;
     o.eps = eps;
-    a->h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()), o, s);
-    id_rendezvous_leave();  // no factorisations below (joint CPQR launches, update.cpp)
-    hbs_invert_device(*a->h, s);
+    static const bool unfused = std::getenv("SBX_APP_UNFUSED") != nullptr;  // diagnostics
+    if (unfused) {
+      a->h = hbs_compress_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()), o, s);
+      id_rendezvous_leave();  // no factorisations below (joint CPQR launches, update.cpp)
+      hbs_invert_device(*a->h, s);
+    } else {  // the inverse of each level overlaps the compression of the next
+      a->h = hbs_compress_invert_device(new_g, form, mu, plan.added_new.data(), i64(plan.added_new.size()), o, s);
+      id_rendezvous_leave();
+    }
     hbs_build_solve_plan(*a->h);
   }
   return a;

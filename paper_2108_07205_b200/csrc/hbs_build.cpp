@@ -8,7 +8,11 @@
 //   ->  interpolation matrices (interp_kernel)  ->  b_sib blocks.
 // The inverse is a per-level batch of LU/inverse/rcond + DMMA GEMMs.
 #include <algorithm>
+#include <climits>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <unordered_map>
 
 #include "dense.hpp"
@@ -218,9 +222,243 @@ void build_round(Builder& B, const std::vector<i64>& ids, const std::vector<int>
 
 }  // namespace
 
-std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, double mu,
-                                           const i64* nodes, i64 n_nodes,
-                                           const HbsBuildOptions& o, cudaStream_t s) {
+// ---------------------------------------------------------------- inverse
+namespace {
+// Where one node's inputs and outputs of the telescoping inverse live: the
+// arena (hbs_invert_device) or the per-level staging of the fused build.
+struct InvSrc {
+  const double* d = nullptr;  // leaf diagonal block (c x c, ld ldd)
+  int ldd = 0;
+  const double* u = nullptr;  // c x k, ld c
+  const double* v = nullptr;  // c x k, ld c
+  const double* b = nullptr;  // b_sib: k x k_sib, ld k
+  double* dhat = nullptr;     // k x k
+  double* e = nullptr;        // c x k, ld c
+  double* fg = nullptr;       // (k + c) x c, ld k + c
+};
+
+// rcond gates (hbs.cpp:429) of one level, checked after the last level:
+// the levels run back to back on the stream without host round trips; a
+// failing block is reported as the first one in factorisation order
+struct Gate {
+  std::vector<size_t> ids;
+  DevBuf<double> rc;
+  int depth = 0;
+};
+
+void check_gates(const HbsOp& op, std::vector<std::unique_ptr<Gate>>& gates, double thr, cudaStream_t s) {
+  for (const auto& gp : gates) {
+    const Gate& gt = *gp;
+    std::vector<double> hrc(gt.rc.size());
+    gt.rc.download(hrc.data(), hrc.size(), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    for (size_t q = 0; q < gt.ids.size(); ++q) {
+      const auto& nd = op.nodes[gt.ids[q]];
+      if (nd.c > 0 && !(hrc[2 * q] >= thr))
+        throw Error(4, std::string("singular ") + (gt.ids[q] == 0 ? "root" : "diagonal") +
+                           " block (rcond " + std::to_string(hrc[2 * q]) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
+    for (size_t q = 0; q < gt.ids.size(); ++q) {
+      const auto& nd = op.nodes[gt.ids[q]];
+      if (gt.ids[q] != 0 && nd.c > 0 && nd.k > 0 && !(hrc[2 * q + 1] >= thr))
+        throw Error(4, "singular skeleton block (rcond " + std::to_string(hrc[2 * q + 1]) + ") at tree node [" +
+                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
+                           std::to_string(nd.depth));
+    }
+  }
+}
+
+// One level of the telescoping inverse (hbs.cpp:427-487) for the nodes
+// `ids` (all of one depth), batched: x blocks, LU/inverse/rcond of x,
+// t = v^T xi, xu = xi u, tu = t u, dhat = tu^{-1}, e = xu dhat, f = dhat t,
+// g = xi - e t.  The root (id 0) only gets root_g = x^{-1}.
+void invert_level(const HbsOp& op, const std::vector<size_t>& ids, const std::vector<InvSrc>& P, double* root_g,
+                  std::vector<std::unique_ptr<Gate>>& gates, cudaStream_t s) {
+  // x blocks and scratch
+  std::vector<i64> xo(ids.size()), io(ids.size()), to(ids.size()), tuo(ids.size()), xuo(ids.size());
+  i64 tot = 0;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const i64 c = nd.c, k = nd.k;
+    xo[q] = tot;
+    tot += c * c;
+    io[q] = tot;
+    tot += c * c;
+    to[q] = tot;
+    tot += k * c;
+    tuo[q] = tot;
+    tot += k * k;
+    xuo[q] = tot;
+    tot += c * k;
+  }
+  DevBuf<double> scr(static_cast<size_t>(std::max<i64>(tot, 1)));
+  double* S = scr.get();
+  std::vector<CopyJob> cj;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const int c = int(nd.c);
+    double* x = S + xo[q];
+    if (nd.is_leaf()) {
+      cj.push_back({P[ids[q]].d, x, c, c, P[ids[q]].ldd, c, 0, 0});
+    } else {
+      const InvSrc& l = P[size_t(nd.left)];
+      const InvSrc& r = P[size_t(nd.right)];
+      const int kl = int(op.nodes[size_t(nd.left)].k), kr = int(op.nodes[size_t(nd.right)].k);
+      if (kl) cj.push_back({l.dhat, x, kl, kl, kl, c, 0, 0});
+      if (kl && kr) cj.push_back({l.b, x + size_t(kl) * c, kl, kr, kl, c, 0, 0});
+      if (kl && kr) cj.push_back({r.b, x + kl, kr, kl, kr, c, 0, 0});
+      if (kr) cj.push_back({r.dhat, x + kl + size_t(kl) * c, kr, kr, kr, c, 0, 0});
+    }
+  }
+  copy_batched(cj, s);
+  DevBuf<int> piv(static_cast<size_t>(std::max<i64>(tot, 1)));
+  gates.push_back(std::make_unique<Gate>());
+  Gate& gt = *gates.back();
+  gt.ids = ids;
+  gt.depth = ids.empty() ? 0 : op.nodes[ids[0]].depth;
+  gt.rc.resize(ids.size() * 2 + 1);
+  DevBuf<double>& rc = gt.rc;
+  SBX_CUDA(cudaMemsetAsync(rc.get(), 0x7f, rc.size() * sizeof(double), s));  // unset gates pass
+  DevBuf<double> work;
+  i64 wtot = 0;
+  for (size_t q = 0; q < ids.size(); ++q) wtot += 4 * (op.nodes[ids[q]].c + op.nodes[ids[q]].k);
+  work.resize(size_t(std::max<i64>(wtot, 1)));
+  // LU + inverse + rcond of x
+  std::vector<LuJob> lj;
+  i64 pw = 0;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    if (nd.c == 0) continue;
+    LuJob j{};
+    j.a = S + xo[q];
+    j.n = int(nd.c);
+    j.lda = int(nd.c);
+    j.piv = piv.get() + xo[q];
+    j.inv = ids[q] == 0 ? root_g : S + io[q];
+    j.rcond = rc.get() + 2 * q;
+    j.work = work.get() + pw;
+    pw += 4 * nd.c;
+    lj.push_back(j);
+  }
+  lu_batched(lj, s);
+  phase_mark("inv: x blocks + LU/inverse", s);
+  if (ids.size() == 1 && ids[0] == 0) return;  // the root keeps only root_g (hbs.cpp:450-458)
+  // t = v^T xi (k x c), tu = t u (k x k)
+  std::vector<GemmJob> g1, g2;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const InvSrc& p = P[ids[q]];
+    const int c = int(nd.c), k = int(nd.k);
+    if (c == 0 || k == 0) continue;
+    g1.push_back({p.v, S + io[q], S + to[q], k, c, c, c, c, k, 1, 0, 1.0, 0.0});
+    g1.push_back({S + io[q], p.u, S + xuo[q], c, k, c, c, c, c, 0, 0, 1.0, 0.0});
+  }
+  gemm_batched(g1, s);
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const int c = int(nd.c), k = int(nd.k);
+    if (c == 0 || k == 0) continue;
+    g2.push_back({S + to[q], P[ids[q]].u, S + tuo[q], k, k, c, k, c, k, 0, 0, 1.0, 0.0});
+  }
+  gemm_batched(g2, s);
+  std::vector<LuJob> lj2;
+  pw = 0;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    if (nd.c == 0 || nd.k == 0) continue;
+    LuJob j{};
+    j.a = S + tuo[q];
+    j.n = int(nd.k);
+    j.lda = int(nd.k);
+    j.piv = piv.get() + xo[q];
+    j.inv = P[ids[q]].dhat;
+    j.rcond = rc.get() + 2 * q + 1;
+    j.work = work.get() + pw;
+    pw += 4 * nd.k;
+    lj2.push_back(j);
+  }
+  lu_batched(lj2, s);
+  // e = (xi u) dhat, f = dhat t, g = xi - e t   (hbs.cpp:480-483)
+  std::vector<GemmJob> g3, g4;
+  std::vector<CopyJob> cg;
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const InvSrc& p = P[ids[q]];
+    const int c = int(nd.c), k = int(nd.k);
+    if (c == 0) continue;
+    const int ld = k + c;
+    cg.push_back({S + io[q], p.fg + k, c, c, c, ld, 0, 0});  // g <- xi
+    if (k == 0) continue;
+    g3.push_back({S + xuo[q], p.dhat, p.e, c, k, k, c, k, c, 0, 0, 1.0, 0.0});
+    g3.push_back({p.dhat, S + to[q], p.fg, k, c, k, k, k, ld, 0, 0, 1.0, 0.0});
+  }
+  copy_batched(cg, s);
+  gemm_batched(g3, s);
+  for (size_t q = 0; q < ids.size(); ++q) {
+    const auto& nd = op.nodes[ids[q]];
+    const InvSrc& p = P[ids[q]];
+    const int c = int(nd.c), k = int(nd.k);
+    if (c == 0 || k == 0) continue;
+    g4.push_back({p.e, S + to[q], p.fg + k, c, c, k, c, k, k + c, 0, 0, -1.0, 1.0});
+  }
+  gemm_batched(g4, s);
+  phase_mark("inv: skeleton LU + e,f,g GEMMs", s);
+}
+}  // namespace
+
+namespace {
+// The fused build (with_inverse): a second host thread runs invert_level for
+// depth d on its own stream as soon as the compression of depth d (u, v,
+// b_sib) is complete, while the compression moves on to depth d - 1; the
+// inverse factors go to per-level staging and join the arena at the end.
+struct FusedInverse {
+  std::mutex mu;
+  std::condition_variable cv;
+  int ready = INT_MAX;  // lowest depth whose factors are complete
+  bool abort = false;
+  std::vector<InvSrc> P;
+  std::vector<DevBuf<double>> stage;  // per depth: dhat | e | fg of its nodes
+  DevBuf<double> rootg;
+  std::vector<std::unique_ptr<Gate>> gates;
+  std::exception_ptr err;
+  std::thread th;
+  cudaEvent_t done = nullptr;
+  void publish(int depth) {
+    std::lock_guard<std::mutex> lk(mu);
+    ready = depth;
+    cv.notify_all();
+  }
+  bool wait_for(int depth) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return abort || ready <= depth; });
+    return !abort;
+  }
+  ~FusedInverse() {
+    if (th.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+        cv.notify_all();
+      }
+      th.join();
+    }
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+cudaStream_t inverse_stream() {
+  static const cudaStream_t w = [] {
+    cudaStream_t x = nullptr;
+    SBX_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    return x;
+  }();
+  return w;
+}
+
+std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, const i64* nodes, i64 n_nodes,
+                                     const HbsBuildOptions& o, cudaStream_t s, bool with_inverse) {
   require(o.eps > 0.0 && o.eps <= 0.1, "hbs_compress: tolerance out of range");
   require(o.leaf_nodes >= 2, "hbs_compress: leaf size too small");
   const i64 N = nodes ? n_nodes : g.n_nodes();
@@ -329,6 +567,40 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
     SBX_CUDA(cudaStreamSynchronize(s));
   }
 
+  std::unique_ptr<FusedInverse> fz;
+  if (with_inverse) {
+    fz = std::make_unique<FusedInverse>();
+    fz->P.resize(nn);
+    fz->stage.resize(size_t(max_depth + 1));
+    for (i64 id : leaf_ids) {
+      fz->P[size_t(id)].d = dstore.get() + d_off[size_t(id)];
+      fz->P[size_t(id)].ldd = int(2 * (op->nodes[size_t(id)].end - op->nodes[size_t(id)].begin));
+    }
+    SBX_CUDA(cudaEventCreateWithFlags(&fz->done, cudaEventDisableTiming));
+    int dev = 0;
+    SBX_CUDA(cudaGetDevice(&dev));
+    FusedInverse* F = fz.get();
+    const HbsOp* opp = op.get();
+    const std::vector<std::vector<i64>>* levels = &B.levels;
+    F->th = std::thread([F, opp, levels, dev, max_depth] {
+      const cudaStream_t w = inverse_stream();
+      try {
+        SBX_CUDA(cudaSetDevice(dev));
+        StreamScope ss(w);
+        phase_mark(nullptr, w);
+        for (int d = max_depth; d >= 0; --d) {
+          if (!F->wait_for(d)) break;
+          std::vector<size_t> ids;
+          for (i64 id : (*levels)[size_t(d)]) ids.push_back(size_t(id));
+          invert_level(*opp, ids, F->P, d == 0 ? F->rootg.get() : nullptr, F->gates, w);
+        }
+      } catch (...) {
+        F->err = std::current_exception();
+      }
+      cudaEventRecord(F->done, w);
+      cudaStreamSynchronize(w);  // thread-local job tables die with the thread
+    });
+  }
   // bottom-up skeletonisation; the root keeps no factors (hbs.cpp:411-421)
   std::vector<std::unique_ptr<LevelStore>> stores(static_cast<size_t>(max_depth + 1));
   std::vector<i64> pos_in_level(nn, 0);
@@ -501,12 +773,48 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
                         st->buf.get(), s);
       SBX_CUDA(cudaStreamSynchronize(s));
     }
+    if (fz) {  // this level's inverse inputs are complete: hand it to the inversion thread
+      const LevelStore& S = *st;
+      i64 tot2 = 0;
+      for (size_t q = 0; q < L; ++q) {
+        HbsNodeH& nd = op->nodes[size_t(ids[q])];
+        nd.c = i64(rc[q].size());
+        tot2 += nd.k * nd.k + 2 * nd.c * nd.k + nd.c * nd.c;
+      }
+      DevBuf<double>& sb = fz->stage[size_t(depth)];
+      sb.resize(size_t(std::max<i64>(tot2, 1)));
+      i64 off = 0;
+      for (size_t q = 0; q < L; ++q) {
+        const HbsNodeH& nd = op->nodes[size_t(ids[q])];
+        InvSrc& p = fz->P[size_t(ids[q])];
+        p.u = S.buf.get() + S.o_u[q];
+        p.v = S.buf.get() + S.o_v[q];
+        p.b = S.buf.get() + S.o_b[q];
+        p.dhat = sb.get() + off;
+        off += nd.k * nd.k;
+        p.e = sb.get() + off;
+        off += nd.c * nd.k;
+        p.fg = sb.get() + off;
+        off += (nd.k + nd.c) * nd.c;
+      }
+    }
     stores[size_t(depth)] = std::move(st);
     phase_mark("hbs: interp + b_sib", s);
     SBX_CUDA(cudaStreamSynchronize(s));
+    if (fz) fz->publish(depth);
+  }
+  if (fz) {  // the root: c_0 = k_l + k_r (or the whole single leaf)
+    HbsNodeH& r0 = op->nodes[0];
+    r0.c = r0.is_leaf() ? 2 * (r0.end - r0.begin) : op->nodes[size_t(r0.left)].k + op->nodes[size_t(r0.right)].k;
+    fz->rootg.resize(size_t(std::max<i64>(r0.c * r0.c, 1)));
+    fz->publish(0);
   }
   phase_mark("hbs: levels done", s);
   op->max_block_drawn = B.max_block;
+  if (fz) {  // the layout below rewrites node fields the inversion thread reads
+    fz->th.join();
+    if (fz->err) std::rethrow_exception(fz->err);
+  }
   // final arena: layout by ranks, then place u, v, v^T, d, b_sib
   hbs_layout(*op);
   std::vector<CopyJob> cj;
@@ -535,183 +843,72 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
   copy_batched(cj, s);
   SBX_CUDA(cudaStreamSynchronize(s));
   op->has_apply = true;
+  if (fz) {
+    SBX_CUDA(cudaStreamWaitEvent(s, fz->done, 0));
+    std::vector<CopyJob> ij;
+    double* A2 = op->arena.get();
+    for (size_t i = 1; i < nn; ++i) {
+      const auto& nd = op->nodes[i];
+      const InvSrc& p = fz->P[i];
+      const int k = int(nd.k), c = int(nd.c);
+      if (k > 0) ij.push_back({p.dhat, A2 + nd.o_dhat, k, k, k, k, 0, 0});
+      if (k > 0 && c > 0) ij.push_back({p.e, A2 + nd.o_e, c, k, c, c, 0, 0});
+      if (c > 0) ij.push_back({p.fg, A2 + nd.o_fg, k + c, c, k + c, k + c, 0, 0});
+    }
+    const int c0 = int(op->nodes[0].c);
+    if (c0 > 0) ij.push_back({fz->rootg.get(), A2 + op->o_root_g, c0, c0, c0, c0, 0, 0});
+    copy_batched(ij, s);
+    const double thr = std::max(std::min(10.0 * op->eps, 1e-6), 1e-14);  // hbs.cpp:429
+    check_gates(*op, fz->gates, thr, s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    phase_mark("hbs: fused inverse joined", s);
+    op->has_inverse = true;
+    op->solve_plan.built = false;
+  }
   return op;
 }
+}  // namespace
 
-// ---------------------------------------------------------------- inverse
+std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, double mu, const i64* nodes,
+                                           i64 n_nodes, const HbsBuildOptions& o, cudaStream_t s) {
+  return compress_impl(g, formulation, mu, nodes, n_nodes, o, s, false);
+}
+
+std::unique_ptr<HbsOp> hbs_compress_invert_device(const Geom& g, int formulation, double mu, const i64* nodes,
+                                                  i64 n_nodes, const HbsBuildOptions& o, cudaStream_t s) {
+  return compress_impl(g, formulation, mu, nodes, n_nodes, o, s, true);
+}
+
 void hbs_invert_device(HbsOp& op, cudaStream_t s) {
   require(!op.nodes.empty(), "hbs_invert: empty operator");
   require(op.has_apply, "hbs_invert: operator has no forward factors");
   const double thr = std::max(std::min(10.0 * op.eps, 1e-6), 1e-14);  // hbs.cpp:429
   double* A = op.arena.get();
   const size_t nn = op.nodes.size();
-  // rcond gates (hbs.cpp:429) are checked once at the end: the levels run
-  // back to back on the stream without host round trips; a failing block
-  // is reported as the deepest (first factored) offending one
-  struct Gate {
-    std::vector<size_t> ids;
-    DevBuf<double> rc;
-    int depth;
-  };
+  std::vector<InvSrc> P(nn);
+  for (size_t i = 0; i < nn; ++i) {
+    const auto& nd = op.nodes[i];
+    InvSrc& p = P[i];
+    if (nd.is_leaf()) {
+      p.d = A + nd.o_vd + (i == 0 ? 0 : nd.k);
+      p.ldd = int(i == 0 ? nd.c : nd.k + nd.c);
+    }
+    if (i == 0) continue;
+    p.u = A + nd.o_u;
+    p.v = A + nd.o_v;
+    p.b = A + nd.o_b;
+    p.dhat = A + nd.o_dhat;
+    p.e = A + nd.o_e;
+    p.fg = A + nd.o_fg;
+  }
   std::vector<std::unique_ptr<Gate>> gates;
   for (int depth = op.max_depth; depth >= 0; --depth) {
     std::vector<size_t> ids;
     for (size_t i = 0; i < nn; ++i)
       if (op.nodes[i].depth == depth) ids.push_back(i);
-    // x blocks and scratch
-    std::vector<i64> xo(ids.size()), io(ids.size()), to(ids.size()), tuo(ids.size()), xuo(ids.size());
-    i64 tot = 0;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const i64 c = nd.c, k = nd.k;
-      xo[q] = tot;
-      tot += c * c;
-      io[q] = tot;
-      tot += c * c;
-      to[q] = tot;
-      tot += k * c;
-      tuo[q] = tot;
-      tot += k * k;
-      xuo[q] = tot;
-      tot += c * k;
-    }
-    DevBuf<double> scr(static_cast<size_t>(std::max<i64>(tot, 1)));
-    double* S = scr.get();
-    std::vector<CopyJob> cj;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const int c = int(nd.c);
-      double* x = S + xo[q];
-      if (nd.is_leaf()) {
-        const int vld = ids[q] == 0 ? c : int(nd.k) + c;
-        cj.push_back({A + nd.o_vd + (ids[q] == 0 ? 0 : nd.k), x, c, c, vld, c, 0, 0});
-      } else {
-        const auto& l = op.nodes[size_t(nd.left)];
-        const auto& r = op.nodes[size_t(nd.right)];
-        const int kl = int(l.k), kr = int(r.k);
-        if (kl) cj.push_back({A + l.o_dhat, x, kl, kl, kl, c, 0, 0});
-        if (kl && kr) cj.push_back({A + l.o_b, x + size_t(kl) * c, kl, kr, kl, c, 0, 0});
-        if (kl && kr) cj.push_back({A + r.o_b, x + kl, kr, kl, kr, c, 0, 0});
-        if (kr) cj.push_back({A + r.o_dhat, x + kl + size_t(kl) * c, kr, kr, kr, c, 0, 0});
-      }
-    }
-    copy_batched(cj, s);
-    DevBuf<int> piv(static_cast<size_t>(std::max<i64>(tot, 1)));
-    gates.push_back(std::make_unique<Gate>());
-    Gate& gt = *gates.back();
-    gt.ids = ids;
-    gt.depth = depth;
-    gt.rc.resize(ids.size() * 2 + 1);
-    DevBuf<double>& rc = gt.rc;
-    SBX_CUDA(cudaMemsetAsync(rc.get(), 0x7f, rc.size() * sizeof(double), s));  // unset gates pass
-    DevBuf<double> work;
-    i64 wtot = 0;
-    for (size_t q = 0; q < ids.size(); ++q) wtot += 4 * (op.nodes[ids[q]].c + op.nodes[ids[q]].k);
-    work.resize(size_t(std::max<i64>(wtot, 1)));
-    // LU + inverse + rcond of x
-    std::vector<LuJob> lj;
-    i64 pw = 0;
-    std::vector<size_t> lj_node;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      if (nd.c == 0) continue;
-      LuJob j{};
-      j.a = S + xo[q];
-      j.n = int(nd.c);
-      j.lda = int(nd.c);
-      j.piv = piv.get() + xo[q];
-      j.inv = ids[q] == 0 ? A + op.o_root_g : S + io[q];
-      j.rcond = rc.get() + 2 * q;
-      j.work = work.get() + pw;
-      pw += 4 * nd.c;
-      lj.push_back(j);
-      lj_node.push_back(q);
-    }
-    lu_batched(lj, s);
-    phase_mark("inv: x blocks + LU/inverse", s);
-    if (depth == 0) break;  // the root keeps only root_g (hbs.cpp:450-458)
-    // t = v^T xi (k x c), tu = t u (k x k)
-    std::vector<GemmJob> g1, g2;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const int c = int(nd.c), k = int(nd.k);
-      if (c == 0 || k == 0) continue;
-      g1.push_back({A + nd.o_v, S + io[q], S + to[q], k, c, c, c, c, k, 1, 0, 1.0, 0.0});
-      g1.push_back({S + io[q], A + nd.o_u, S + xuo[q], c, k, c, c, c, c, 0, 0, 1.0, 0.0});
-    }
-    gemm_batched(g1, s);
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const int c = int(nd.c), k = int(nd.k);
-      if (c == 0 || k == 0) continue;
-      g2.push_back({S + to[q], A + nd.o_u, S + tuo[q], k, k, c, k, c, k, 0, 0, 1.0, 0.0});
-    }
-    gemm_batched(g2, s);
-    std::vector<LuJob> lj2;
-    std::vector<size_t> lj2_node;
-    pw = 0;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      if (nd.c == 0 || nd.k == 0) continue;
-      LuJob j{};
-      j.a = S + tuo[q];
-      j.n = int(nd.k);
-      j.lda = int(nd.k);
-      j.piv = piv.get() + xo[q];
-      j.inv = A + nd.o_dhat;
-      j.rcond = rc.get() + 2 * q + 1;
-      j.work = work.get() + pw;
-      pw += 4 * nd.k;
-      lj2.push_back(j);
-      lj2_node.push_back(q);
-    }
-    lu_batched(lj2, s);
-    // e = (xi u) dhat, f = dhat t, g = xi - e t   (hbs.cpp:480-483)
-    std::vector<GemmJob> g3, g4;
-    std::vector<CopyJob> cg;
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const int c = int(nd.c), k = int(nd.k);
-      if (c == 0) continue;
-      double* fg = A + nd.o_fg;  // (k + c) x c, f rows then g rows
-      const int ld = k + c;
-      cg.push_back({S + io[q], fg + k, c, c, c, ld, 0, 0});  // g <- xi
-      if (k == 0) continue;
-      g3.push_back({S + xuo[q], A + nd.o_dhat, A + nd.o_e, c, k, k, c, k, c, 0, 0, 1.0, 0.0});
-      g3.push_back({A + nd.o_dhat, S + to[q], fg, k, c, k, k, k, ld, 0, 0, 1.0, 0.0});
-    }
-    copy_batched(cg, s);
-    gemm_batched(g3, s);
-    for (size_t q = 0; q < ids.size(); ++q) {
-      const auto& nd = op.nodes[ids[q]];
-      const int c = int(nd.c), k = int(nd.k);
-      if (c == 0 || k == 0) continue;
-      g4.push_back({A + nd.o_e, S + to[q], A + nd.o_fg + k, c, c, k, c, k, k + c, 0, 0, -1.0, 1.0});
-    }
-    gemm_batched(g4, s);
-    phase_mark("inv: skeleton LU + e,f,g GEMMs", s);
+    invert_level(op, ids, P, A + op.o_root_g, gates, s);
   }
-  for (const auto& gp : gates) {  // deepest level first, x block before skeleton block
-    const Gate& gt = *gp;
-    std::vector<double> hrc(gt.rc.size());
-    gt.rc.download(hrc.data(), hrc.size(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
-    for (size_t q = 0; q < gt.ids.size(); ++q) {
-      const auto& nd = op.nodes[gt.ids[q]];
-      if (nd.c > 0 && !(hrc[2 * q] >= thr))
-        throw Error(4, std::string("singular ") + (gt.ids[q] == 0 ? "root" : "diagonal") +
-                           " block (rcond " + std::to_string(hrc[2 * q]) + ") at tree node [" +
-                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
-                           std::to_string(nd.depth));
-    }
-    for (size_t q = 0; q < gt.ids.size(); ++q) {
-      const auto& nd = op.nodes[gt.ids[q]];
-      if (gt.ids[q] != 0 && nd.c > 0 && nd.k > 0 && !(hrc[2 * q + 1] >= thr))
-        throw Error(4, "singular skeleton block (rcond " + std::to_string(hrc[2 * q + 1]) + ") at tree node [" +
-                           std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
-                           std::to_string(nd.depth));
-    }
-  }
+  check_gates(op, gates, thr, s);
   phase_mark("inv: done", s);
   op.has_inverse = true;
   op.solve_plan.built = false;

@@ -32,4 +32,10 @@ std::unique_ptr<HbsOp> hbs_compress_device(const Geom& g, int formulation, doubl
 
 void hbs_invert_device(HbsOp& op, cudaStream_t s);
 
+// Compression and inverse in one pass: the telescoping inverse of depth d
+// runs on a second stream while depth d - 1 is compressed (same kernels and
+// results as hbs_compress_device + hbs_invert_device).
+std::unique_ptr<HbsOp> hbs_compress_invert_device(const Geom& g, int formulation, double mu, const i64* nodes,
+                                                  i64 n_nodes, const HbsBuildOptions& o, cudaStream_t s);
+
 }  // namespace sbx

@@ -51,7 +51,7 @@ constexpr int kGRs = 16;               // rows per GEMV item on latency-bound le
 template <int GR>
 struct GemvShape {
   static constexpr int kGS = kThreads / GR;      // K slices
-  static constexpr int kGV = GR == 64 ? 8 : 16;  // columns prefetched per thread
+  static constexpr int kGV = 16;                 // columns prefetched per thread
 };
 struct GemvRegs {
   double av[16];
@@ -102,6 +102,16 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
   if (row < t.m) {
     const double* a = fac + t.a_off + row;
     int j = g.j0 + kGV;
+    for (; j + 16 <= g.j1; j += 16) {  // 16 loads in flight per thread
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __ldg(a + size_t(j + q) * t.lda);
+#pragma unroll
+      for (int q = 0; q < 16; q += 2) {
+        acc = fma(v[q], xs[j + q], acc);
+        acc1 = fma(v[q + 1], xs[j + q + 1], acc1);
+      }
+    }
     for (; j + 8 <= g.j1; j += 8) {
       double v[8];
 #pragma unroll

@@ -212,3 +212,24 @@ def test_collapsed_top_matches_oracle(po, tmp_path, top):
                        env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"top {top}" in r.stdout, r.stdout
+
+
+def test_fused_app_build_bitwise(po, tmp_path):
+    """The added block's HBS built with each level's inverse overlapping the
+    next level's compression (hbs_compress_invert_device) gives the same
+    refined solve, bit for bit, as compress-then-invert."""
+    import os
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    out = {}
+    for mode in ("fused", "unfused"):
+        env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        if mode == "unfused":
+            env["SBX_APP_UNFUSED"] = "1"
+        r = subprocess.run([sys.executable, str(Path(__file__).parent / "app_case.py"), str(tmp_path / f"{mode}.npy")],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        out[mode] = np.load(tmp_path / f"{mode}.npy")
+    assert np.array_equal(out["fused"], out["unfused"])
+    assert np.all(np.isfinite(out["fused"]))
