@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-apply-bench", action="store_true",
+                    help="skip the cfg3 HBS-apply microbenchmark and the Woodbury-build roofline")
     return ap.parse_args()
 
 
@@ -119,8 +121,7 @@ def solve_flops_bytes(sb, h, els, nrhs):
     info = h.info()
     e = els.info()
     n_ext = e["n_k"] + e["n_c"] + e["n_p"]
-    app = els._app_factor_doubles if hasattr(els, "_app_factor_doubles") else 0
-    fd = info["factor_doubles"] + app
+    fd = info["factor_doubles"] + e["app_solve_doubles"]
     k = e["k"]
     flops = 2.0 * nrhs * (fd + 2 * k * n_ext + k * k)
     bytes_ = 8.0 * (fd + 2 * k * n_ext + k * k) + 16.0 * n_ext * nrhs
@@ -221,9 +222,106 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "roofline": roof,
     }
+    if not args.no_apply_bench and world == 1:
+        line["woodbury_build"] = roofline_woodbury(sb, torch, stream, g0, h, panels, cfg)
+        line["apply_microbench"] = apply_microbench(sb, torch, stream)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, G.shape[1], threads=1)
     return line
+
+
+def _kernel_ms(sb, torch, stream, name, fn, reps=10):
+    """(mean launch ms of kernel `name` from CUDA events around each launch on
+    its stream, mean call ms) over `reps` calls of fn after 3 warm-up calls."""
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            fn()
+        sb.api.kernel_timing(True)
+        sb.api.kernel_time(name)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    kms, kcnt = sb.api.kernel_time(name)
+    sb.api.kernel_timing(False)
+    return kms / max(kcnt, 1), e0.elapsed_time(e1) / reps
+
+
+def apply_microbench(sb, torch, stream):
+    """BASELINE.json configs[2]: HBS inverse apply (hbs_solve) of the
+    4096-panel star (131072 unknowns) on device-resident uniform(-1, 1)
+    blocks of 1, 32 and 256 RHS.  1 RHS is HBM-bound (achieved = factor bytes
+    + 16 n bytes per launch over the sweep kernel's launch time, against the
+    measured copy bandwidth); 32 / 256 RHS are FP64-tensor-bound."""
+    from paper_2108_07205_b200.configs import CONFIGS
+    c = CONFIGS["cfg3"]
+    g = sb.panelize(sb.star(c.prongs, c.amplitude, c.a), c.n_panels, c.q)
+    t0 = time.perf_counter()
+    h = sb.hbs_invert(sb.hbs_compress(g, opts=sb.HbsOptions(eps=c.eps, leaf_nodes=c.leaf)))
+    sb.api.lib().sbx_sync()
+    t_static = time.perf_counter() - t0
+    info = h.info()
+    n, fd = info["n"], info["factor_doubles"]
+    sb.hbs_solve(h, np.zeros((n, 1)))  # builds the solve plan (and its collapsed top)
+    info = h.info()
+    hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6553.6
+    fp64 = measured_fp64_peak()["value"]
+    out = {"workload": "cfg3: star r=1+0.3cos5t, 4096x16 nodes (131072 unknowns), leaf 64, eps 1e-10",
+           "t_static_s": round(t_static, 3), "factor_MB": round(8e-6 * fd, 1),
+           "collapsed_top": {"depth": info["top_L"], "K": info["top_K"]}}
+    for nrhs in (1, 32, 256):
+        b = torch.empty((n, nrhs), dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        kname = "sweep_flow_gemv" if nrhs == 1 else "sweep_flow_dmma"
+        ms, call_ms = _kernel_ms(sb, torch, stream, kname, lambda: sb.hbs_solve(h, b))
+        if nrhs == 1:
+            byts = 8.0 * fd + 16.0 * n
+            ach = byts / (ms * 1e-3) / 1e9
+            out["rhs1"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                           "frac": round(ach / hbm, 4), "launch_ms": round(ms, 4), "call_ms": round(call_ms, 4),
+                           "algorithmic_bytes": byts, "traffic": measured_traffic("sweep_gemv")}
+        else:
+            fl = 2.0 * nrhs * fd
+            ach = fl / (ms * 1e-3) / 1e12
+            out[f"rhs{nrhs}"] = {"bound": "tensor", "achieved": round(ach, 3), "peak": fp64, "unit": "TFLOP/s",
+                                 "frac": round(ach / fp64, 4), "launch_ms": round(ms, 4),
+                                 "call_ms": round(call_ms, 4), "algorithmic_flops": fl}
+    return out
+
+
+def roofline_woodbury(sb, torch, stream, g0, h, panels, cfg):
+    """North-star subsystem (3): the Woodbury factor build (els_build:
+    X = Atilde^-1 L over the u update columns through both HBS inverses,
+    W = I + R X, inverse of W), CUDA events around els_build on the library
+    stream (the A_pp HBS it reuses was built inside compress_update).
+    Algorithmic flops: 2 u (a_oo + A_pp solve factor doubles) + 2 u^2 n_ext
+    + 2 u^3 (explicit W^-1); achieved against the measured FP64 DMMA peak."""
+    g1, plan = sb.refine(g0, panels, cfg.m)
+    upd = sb.compress_update(g0, g1, plan, cfg.eps, seed=cfg.seed)
+    ts = []
+    for rep in range(6):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            els = sb.els_build(h, g0, g1, plan, upd)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if rep:
+            ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    e = els.info()
+    u = e["k"]
+    n_ext = e["n_k"] + e["n_c"] + e["n_p"]
+    fd = h.info()["factor_doubles"] + e["app_solve_doubles"]
+    fl = 2.0 * u * fd + 2.0 * u * u * n_ext + 2.0 * u ** 3
+    fp64 = measured_fp64_peak()["value"]
+    ach = fl / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(ach, 3), "peak": fp64, "unit": "TFLOP/s",
+            "frac": round(ach / fp64, 4), "ms": round(ms, 4), "u": u, "n_ext": n_ext,
+            "algorithmic_flops": fl}
 
 
 def phase_split(sb, torch, stream, g0, h, panels, cfg, G_dev):

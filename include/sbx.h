@@ -182,7 +182,8 @@ int sbx_update_from_factors(sbx_plan plan, const double* L, const double* R, int
 int sbx_els_build(sbx_hbs a_oo, sbx_geom old_g, sbx_geom new_g, sbx_plan plan,
                   sbx_update upd, int formulation, double mu, sbx_els* out);
 int sbx_els_destroy(sbx_els e);
-/* info: n_k, n_c, n_p (scalars), k, app_is_hbs */
+/* info[0..5]: n_k, n_c, n_p (scalars), k, app_is_hbs, app_solve_doubles (factor
+ * doubles one A_pp solve streams: its HBS factors, or n_p^2 for the dense inverse) */
 int sbx_els_info(sbx_els e, int64_t* info);
 /* g_n: (n_k + n_p) x nrhs (kept, added); tau_n same shape. */
 int sbx_els_solve(sbx_els e, const double* g_n, int64_t ldg, int64_t nrhs, double* tau_n,

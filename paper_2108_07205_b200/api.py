@@ -420,9 +420,9 @@ class ElsSolver(_Handle):
         self._a_oo = a_oo
 
     def info(self) -> dict:
-        out = np.zeros(5, dtype=np.int64)
+        out = np.zeros(6, dtype=np.int64)
         check(lib().sbx_els_info(self.ptr, out.ctypes.data_as(I64P)))
-        return dict(zip(("n_k", "n_c", "n_p", "k", "app_hbs"), (int(v) for v in out)))
+        return dict(zip(("n_k", "n_c", "n_p", "k", "app_hbs", "app_solve_doubles"), (int(v) for v in out)))
 
     def n_ext(self):
         i = self.info()

@@ -435,6 +435,8 @@ int sbx_els_info(sbx_els e, int64_t* info) {
     info[2] = s.n_p;
     info[3] = s.k;
     info[4] = (s.app && s.app->h) ? 1 : 0;
+    // algorithmic doubles of one A_pp solve: its HBS factors or the dense inverse
+    info[5] = (s.app && s.app->h) ? s.app->h->solve_factor_doubles() : s.n_p * s.n_p;
   });
 }
 

@@ -2338,10 +2338,31 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// 8-byte asynchronous global -> shared copy; src_bytes 0 zero-fills
+__device__ __forceinline__ void gcp_async8(double* dst, const double* src, bool pred) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void gcp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void gcp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+constexpr int gStages = 4;
+struct GemmSmem {
+  double As[gStages][gKC][gTM + gPad];
+  double Bs[gStages][gKC][gTN + gPad];
+};
+
+// 64 x 64 output tile per CTA on FP64 tensor cores (mma.sync.m8n8k4 ->
+// DMMA), 8 warps of 16 x 32; K moves through a gStages-deep cp.async
+// pipeline (8-byte copies: operands may be transposed and unaligned), so
+// the global loads of chunk ch + 3 are in flight while chunk ch computes.
 __global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ jobs,
                                                    const int4* __restrict__ tiles) {
-  __shared__ double As[2][gKC][gTM + gPad];
-  __shared__ double Bs[2][gKC][gTN + gPad];
+  extern __shared__ __align__(16) double gsm[];
+  GemmSmem& S = *reinterpret_cast<GemmSmem*>(gsm);
   const int4 tl = tiles[blockIdx.x];
   const GemmJob jb = jobs[tl.x];
   const int row0 = tl.y, col0 = tl.z;
@@ -2356,11 +2377,10 @@ __global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ j
   const int kbeg = jb.splitk > 1 ? tl.w * jb.kchunk : 0;
   const int K = jb.splitk > 1 ? min(jb.k, kbeg + jb.kchunk) : jb.k;
   const int nch = (K - kbeg + gKC - 1) / gKC;
-  auto load = [&](int buf, int k0) {
+  auto issue = [&](int st, int k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int idx = threadIdx.x + q * 256;
-      // A tile: rows row0..+64, k k0..+16
       int kk, rr;
       if (!jb.ta) {
         kk = idx >> 6;
@@ -2370,10 +2390,10 @@ __global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ j
         kk = idx & 15;
       }
       const int gr = row0 + rr, gk = k0 + kk;
-      double av = 0.0;
-      if (gr < jb.m && gk < K)
-        av = jb.ta ? jb.A[gk + size_t(gr) * jb.lda] : jb.A[gr + size_t(gk) * jb.lda];
-      As[buf][kk][rr] = av;
+      const bool pa = gr < jb.m && gk < K;
+      gcp_async8(&S.As[st][kk][rr], pa ? (jb.ta ? jb.A + gk + size_t(gr) * jb.lda : jb.A + gr + size_t(gk) * jb.lda)
+                                       : jb.A,
+                 pa);
       int kb, cc;
       if (!jb.tb) {
         cc = idx >> 4;
@@ -2383,31 +2403,37 @@ __global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ j
         cc = idx & 63;
       }
       const int gc = col0 + cc, gkb = k0 + kb;
-      double bv = 0.0;
-      if (gc < jb.n && gkb < K)
-        bv = jb.tb ? jb.B[gc + size_t(gkb) * jb.ldb] : jb.B[gkb + size_t(gc) * jb.ldb];
-      Bs[buf][kb][cc] = bv;
+      const bool pb = gc < jb.n && gkb < K;
+      gcp_async8(&S.Bs[st][kb][cc],
+                 pb ? (jb.tb ? jb.B + gc + size_t(gkb) * jb.ldb : jb.B + gkb + size_t(gc) * jb.ldb) : jb.B, pb);
     }
   };
-  if (nch > 0) load(0, kbeg);
-  __syncthreads();
+#pragma unroll
+  for (int st = 0; st < gStages - 1; ++st) {
+    if (st < nch) issue(st, kbeg + st * gKC);
+    gcp_commit();
+  }
   for (int ch = 0; ch < nch; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < nch) load(buf ^ 1, kbeg + (ch + 1) * gKC);
+    const int st = ch % gStages;
+    gcp_wait<gStages - 2>();
+    __syncthreads();  // chunk ch visible to all; stage (ch - 1) % gStages free
+    const int nx = ch + gStages - 1;
+    if (nx < nch) issue(nx % gStages, kbeg + nx * gKC);
+    gcp_commit();
 #pragma unroll
     for (int k4 = 0; k4 < gKC; k4 += 4) {
       double af[2], bf[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) af[a] = As[buf][k4 + tig][wm + a * 8 + gid];
+      for (int a = 0; a < 2; ++a) af[a] = S.As[st][k4 + tig][wm + a * 8 + gid];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bf[b] = Bs[buf][k4 + tig][wn + b * 8 + gid];
+      for (int b = 0; b < 4; ++b) bf[b] = S.Bs[st][k4 + tig][wn + b * 8 + gid];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma(c[a][b][0], c[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
   }
+  gcp_wait<0>();
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
     const int row = row0 + wm + a * 8 + gid;
@@ -3826,7 +3852,11 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
   if (tiles.empty()) return;
   const GemmJob* d = tab.upload(js, s);
   const int4* dt = ttab.upload(tiles, s);
-  gemm_kernel<<<unsigned(tiles.size()), 256, 0, s>>>(d, dt);
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(GemmSmem))));
+  });
+  gemm_kernel<<<unsigned(tiles.size()), 256, sizeof(GemmSmem), s>>>(d, dt);
   SBX_LAUNCHED();
   if (mx_out > 0) {
     dim3 grid(unsigned(std::min<i64>((mx_out + 255) / 256, 256)), unsigned(js.size()));
