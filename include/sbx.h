@@ -57,6 +57,7 @@ typedef struct sbx_plan_s* sbx_plan;     /* RefinementPlan           */
 typedef struct sbx_hbs_s* sbx_hbs;       /* HbsOperator (device)     */
 typedef struct sbx_update_s* sbx_update; /* LowRankUpdate (device)   */
 typedef struct sbx_els_s* sbx_els;       /* ElsSolver (device)       */
+typedef struct sbx_app_s* sbx_app;       /* A_pp inverse (device)    */
 
 /* CurveParams (geometry.hpp:14-26). */
 typedef struct {
@@ -182,6 +183,17 @@ int sbx_update_from_factors(sbx_plan plan, const double* L, const double* R, int
 int sbx_els_build(sbx_hbs a_oo, sbx_geom old_g, sbx_geom new_g, sbx_plan plan,
                   sbx_update upd, int formulation, double mu, sbx_els* out);
 int sbx_els_destroy(sbx_els e);
+/* The added-unknown diagonal block's inverse alone (els.cpp:111-118: dense
+ * LU for 2 N_p <= 2048 scalars, else its own HBS), for callers that split the
+ * extended system across ranks (parallel.ShardedWoodbury: the block lives on
+ * one rank).  new_g must outlive the handle.  info: n_p (scalars), is_hbs.
+ * sbx_app_solve: out = A_pp^{-1} v (flags & SBX_TRANSPOSE: A_pp^{-T} v),
+ * n_p x nrhs column-major; flags & SBX_DEVICE_PTRS for device buffers. */
+int sbx_app_build(sbx_geom new_g, sbx_plan plan, int formulation, double mu, double eps, sbx_app* out);
+int sbx_app_destroy(sbx_app a);
+int sbx_app_info(sbx_app a, int64_t* info);
+int sbx_app_solve(sbx_app a, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo, int flags,
+                  void* stream);
 /* info[0..5]: n_k, n_c, n_p (scalars), k, app_is_hbs, app_solve_doubles (factor
  * doubles one A_pp solve streams: its HBS factors, or n_p^2 for the dense inverse) */
 int sbx_els_info(sbx_els e, int64_t* info);

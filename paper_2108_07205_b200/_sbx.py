@@ -119,6 +119,10 @@ _SIGS = [
     ("sbx_els_conditioning", C.c_int, [VP, C.c_int, F64P]),
     ("sbx_els_gmres", C.c_int, [VP, F64P, F64P, C.c_int, C.c_double, I64, I64, I64P, F64P, I64]),
     ("sbx_els_xw", C.c_int, [VP, F64P, F64P]),
+    ("sbx_app_build", C.c_int, [VP, VP, C.c_int, C.c_double, C.c_double, C.POINTER(VP)]),
+    ("sbx_app_destroy", C.c_int, [VP]),
+    ("sbx_app_info", C.c_int, [VP, I64P]),
+    ("sbx_app_solve", C.c_int, [VP, VP, I64, I64, VP, I64, C.c_int, VP]),
 ]
 
 EXPORTS = [s[0] for s in _SIGS]

@@ -446,6 +446,33 @@ def els_build(a_oo: HbsOperator, d_old: Discretization, d_new: Discretization,
     return ElsSolver(out, a_oo)
 
 
+class AppBlockSolver(_Handle):
+    """The added-unknown diagonal block's inverse alone (els.cpp:111-118:
+    dense LU up to 2048 scalars, else its own HBS); keeps the refined mesh
+    it was built on alive."""
+    _destroy = "sbx_app_destroy"
+
+    def __init__(self, ptr, d_new):
+        super().__init__(ptr)
+        self._d_new = d_new
+
+    def info(self) -> dict:
+        out = np.zeros(2, dtype=np.int64)
+        check(lib().sbx_app_info(self.ptr, out.ctypes.data_as(I64P)))
+        return {"n_p": int(out[0]), "hbs": int(out[1])}
+
+    def solve(self, v, transpose: bool = False):
+        return _sweep(lib().sbx_app_solve, self.ptr, v, self.info()["n_p"],
+                      flags=_sbx.SBX_TRANSPOSE if transpose else 0)
+
+
+def app_build(d_new: Discretization, plan: RefinementPlan, eps: float = 1e-10,
+              formulation=INTERIOR_DIRICHLET, mu: float = 1.0) -> AppBlockSolver:
+    out = VP()
+    check(lib().sbx_app_build(d_new.ptr, plan.ptr, formulation, mu, eps, C.byref(out)))
+    return AppBlockSolver(out, d_new)
+
+
 def _els_call(fn, s: ElsSolver, g, rows_in, flags=0):
     if _is_torch_cuda(g):
         import torch

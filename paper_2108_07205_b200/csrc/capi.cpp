@@ -27,6 +27,9 @@ struct sbx_update_s {
 struct sbx_els_s {
   std::unique_ptr<sbx::Els> e;
 };
+struct sbx_app_s {
+  std::shared_ptr<sbx::AppSolver> a;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -418,6 +421,59 @@ int sbx_els_build(sbx_hbs a_oo, sbx_geom old_g, sbx_geom new_g, sbx_plan plan, s
     auto e = sbx::els_build_device(H(a_oo), G(old_g), G(new_g), *plan->p, *upd->u, formulation, mu,
                                    sbx::lib_stream());
     *out = new sbx_els_s{std::move(e)};
+  });
+}
+
+int sbx_app_build(sbx_geom new_g, sbx_plan plan, int formulation, double mu, double eps, sbx_app* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    sbx::require(eps > 0.0 && eps <= 0.1, "app_build: tolerance out of range");
+    auto h = new sbx_app_s;
+    try {
+      h->a = sbx::build_app_solver(G(new_g), *plan->p, formulation, mu, eps, sbx::lib_stream());
+      SBX_CUDA(cudaStreamSynchronize(sbx::lib_stream()));
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int sbx_app_destroy(sbx_app a) {
+  delete a;
+  return SBX_OK;
+}
+
+int sbx_app_info(sbx_app a, int64_t* info) {
+  return guard([&] {
+    sbx::require(a && a->a, "null app handle");
+    info[0] = 2 * int64_t(a->a->added.size());
+    info[1] = a->a->h ? 1 : 0;
+  });
+}
+
+int sbx_app_solve(sbx_app a, const double* v, int64_t ldv, int64_t nrhs, double* out, int64_t ldo, int flags,
+                  void* stream) {
+  return guard([&] {
+    sbx::require(a && a->a, "null app handle");
+    const cudaStream_t s = stream_of(stream);
+    sbx::StreamScope scope(s);
+    const int64_t n = 2 * int64_t(a->a->added.size());
+    sbx::require(nrhs >= 0 && ldv >= n && ldo >= n, "app_solve: bad sizes");
+    if (n == 0 || nrhs == 0) return;
+    const bool tr = (flags & SBX_TRANSPOSE) != 0;
+    if (flags & SBX_DEVICE_PTRS) {
+      sbx::app_solve_device(*a->a, v, ldv, out, ldo, nrhs, s, tr);
+      return;
+    }
+    sbx::DevBuf<double> dv(size_t(n * nrhs)), dout(size_t(n * nrhs));
+    SBX_CUDA(cudaMemcpy2DAsync(dv.get(), size_t(n) * 8, v, size_t(ldv) * 8, size_t(n) * 8, size_t(nrhs),
+                               cudaMemcpyHostToDevice, s));
+    sbx::app_solve_device(*a->a, dv.get(), n, dout.get(), n, nrhs, s, tr);
+    SBX_CUDA(cudaMemcpy2DAsync(out, size_t(ldo) * 8, dout.get(), size_t(n) * 8, size_t(n) * 8, size_t(nrhs),
+                               cudaMemcpyDeviceToHost, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
   });
 }
 

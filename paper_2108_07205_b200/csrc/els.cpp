@@ -65,26 +65,32 @@ void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nr
   launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
   phase_mark("els:   a_oo sweep", s);
   if (e.n_p == 0) return;
-  const double* vp = v + nkc;
-  double* op = out + nkc;
-  if (e.app->h) {
-    HbsOp& H = *e.app->h;
+  app_solve_device(*e.app, v + nkc, ldv, out + nkc, ldo, nrhs, s, tr);
+}
+
+}  // namespace
+
+void app_solve_device(AppSolver& a, const double* vp, i64 ldv, double* op, i64 ldo, i64 nrhs, cudaStream_t s,
+                      bool tr) {
+  const i64 n_p = 2 * i64(a.added.size());
+  if (n_p == 0 || nrhs == 0) return;
+  const i64 ldw = sweep_ld(nrhs);
+  if (a.h) {
+    HbsOp& H = *a.h;
     if (!H.solve_plan.built) hbs_build_solve_plan(H);
     if (tr) hbs_ensure_transpose(H, true, false, s);
     SweepPlan& Q = H.solve_plan;
     H.ws.reserve(size_t(Q.ws_rows * ldw));
-    launch_cm_to_rm(vp, ldv, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
+    launch_cm_to_rm(vp, ldv, n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
     hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
-    launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, op, ldo, nullptr, s);
+    launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, n_p, nrhs, op, ldo, nullptr, s);
     phase_mark("els:   A_pp sweep", s);
   } else {  // explicit inverse of A_pp (els.cpp:47: app_lu.solve / app_lu.transpose().solve)
-    gemm_batched({{e.app->inv.get(), vp, op, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(ldv),
-                   int(ldo), tr ? 1 : 0, 0, 1.0, 0.0}},
+    gemm_batched({{a.inv.get(), vp, op, int(n_p), int(nrhs), int(n_p), int(n_p), int(ldv), int(ldo), tr ? 1 : 0, 0,
+                   1.0, 0.0}},
                  s);
   }
 }
-
-}  // namespace
 
 std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan, int form, double mu,
                                             double eps, cudaStream_t s) {

@@ -35,6 +35,10 @@ struct AppSolver {
 };
 std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan, int formulation,
                                             double mu, double eps, cudaStream_t s);
+// out = A_pp^{-1} v (or A_pp^{-T} v) for n_p x nrhs column-major device blocks
+// (els.cpp:47: app_lu.solve / app_h solve).
+void app_solve_device(AppSolver& a, const double* v, i64 ldv, double* out, i64 ldo, i64 nrhs, cudaStream_t s,
+                      bool transpose = false);
 
 struct Els {
   HbsOp* a_oo = nullptr;            // static wall solver (owned by the caller's handle)

@@ -18,13 +18,13 @@ def setup():
     sb.init(0)
     g = sb.panelize(sb.star(5, 0.3), 64, 16)  # 1024 nodes, 16 leaves, depth 4
     h = sb.hbs_invert(sb.hbs_compress(g, opts=sb.HbsOptions(eps=1e-10)))
-    return sb, torch, DeviceExecutor, h
+    return sb, torch, DeviceExecutor, h, g
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("nrhs", [1, 5, 64])
 def test_shard_solve_matches_full(setup, G, nrhs):
-    sb, torch, DeviceExecutor, h = setup
+    sb, torch, DeviceExecutor, h, _ = setup
     n = h.info()["n"]
     b = torch.empty((n, nrhs), dtype=torch.float64, device="cuda").uniform_(-1, 1)
     ref = sb.hbs_solve(h, b)
@@ -45,8 +45,57 @@ def test_shard_solve_matches_full(setup, G, nrhs):
 
 
 def test_shard_rejects_bad_rank_count(setup):
-    sb, torch, DeviceExecutor, h = setup
+    sb, torch, DeviceExecutor, h, _ = setup
     with pytest.raises(ValueError):
         DeviceExecutor(h, 3, 0)
     with pytest.raises(ValueError):
         DeviceExecutor(h, 64, 0)  # deeper than the tree
+
+
+@pytest.mark.parametrize("n_refine", [2, 8])
+def test_sharded_woodbury_device_matches_els(setup, n_refine):
+    """ShardedWoodbury (parallel.py) on the device pieces — the partitioned
+    HBS solve, sbx_app_solve for the added block, the update factors — on a
+    one-rank NCCL group; equals the device els_solve_raw.  The multi-rank
+    exchange is covered over gloo (test_parallel_gloo.py).  8 refined panels
+    at m = 16 put the added block on its own HBS (2 N_p > 2048)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2108_07205_b200.parallel import ShardedHbsSolver, ShardedWoodbury
+    sb, torch, DeviceExecutor, h, g = setup
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    panels = list(range(10, 10 + n_refine))
+    g1, plan = sb.refine(g, panels, 16 if n_refine == 8 else 4)
+    upd = sb.compress_update(g, g1, plan, 1e-10)
+    els = sb.els_build(h, g, g1, plan, upd)
+    app = sb.app_build(g1, plan, 1e-10)
+    assert app.info()["hbs"] == (1 if n_refine == 8 else 0)
+    L, R = upd.factors()
+    m = plan.maps()
+
+    def scal(v):
+        return np.stack([2 * v, 2 * v + 1], 1).reshape(-1)
+
+    old_of_ext = np.concatenate([scal(m["kept_old"]), scal(m["cut_old"])])
+    n_k, n_c, n_p = 2 * len(m["kept_old"]), 2 * len(m["cut_old"]), 2 * len(m["added_new"])
+    gx = torch.empty((n_k + n_c + n_p, 4), dtype=torch.float64, device="cuda").uniform_(-1, 1)
+    gx[n_k:n_k + n_c] = 0.0
+    wb = ShardedWoodbury(ShardedHbsSolver(DeviceExecutor(h, 1, 0)), torch.from_numpy(L).cuda(),
+                         torch.from_numpy(R).cuda(), old_of_ext, n_k, n_c, n_p, app_solve=app.solve)
+    y, y_p = wb.solve(wb.local_rows(gx), gx[n_k + n_c:])
+    out = torch.zeros_like(gx)
+    out[wb.own] = y[wb.pos]
+    out[n_k + n_c:] = y_p
+    ref = sb.els_solve_raw(els, gx)
+    err = (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item()
+    assert err <= 1e-10, err
