@@ -60,6 +60,17 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
   }();
+  // streaming TSQR of crowded batches: candidates per problem (the quad
+  // kernel holds n <= 128) and TSQR steps (row blocks x n) beyond which one
+  // problem's latency would set the whole round
+  static const int tsqr_max_n = [] {
+    const char* e = std::getenv("SBX_TSQR_MAXN");
+    return e ? std::atoi(e) : 128;  // measured (scripts/route_scan.sh): 129..144 on the warp kernel loses
+  }();
+  static const i64 tsqr_max_steps = [] {
+    const char* e = std::getenv("SBX_TSQR_MAXSTEPS");
+    return e ? std::atoll(e) : i64(1) << 40;
+  }();
   // Routing (measured per batch on the per-step problem mix, see
   // scripts/id_bench.cu --replay): while the whole batch fits the chip in
   // about two waves, the on-chip cooperative engine (exact CTA counts, one
@@ -87,7 +98,9 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     if (engine == 0) {
       const int g = cpqr_smem_ctas(j.M, j.n);
       const bool chip_ok = !no_coop_flag() && g > 0 && g <= sms;
-      const bool tsqr_ok = j.n <= 144 && j.M > j.n && (j.M <= tsqr_max_m || (tsqr_crowd && j.M <= 4096));
+      const bool tsqr_ok = j.n <= tsqr_max_n && j.M > j.n &&
+                           (j.M <= tsqr_max_m ||
+                            (tsqr_crowd && j.M <= 4096 && i64((j.M + 127) / 128) * j.n <= tsqr_max_steps));
       const bool one_cta = qr_smem_need(j.M, j.n) <= size_t(200 * 1024);
       int rg = 0;
       const int rc = no_reg ? -1 : cpqr_reg_config(j.M, j.n, &rg);
