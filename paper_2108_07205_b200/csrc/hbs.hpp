@@ -120,6 +120,12 @@ struct HbsOp {
   // down-sweep inputs; top_L == 0 runs every level.
   int top_L = 0;
   i64 o_top = -1, top_K = 0, top_cap = 0;
+  // smallest reciprocal condition number of each node's x and skeleton
+  // blocks seen by the inverse (hbs.cpp:429 gates); empty when unknown
+  // (an inverse loaded from HBS1).  The top only collapses over
+  // well-conditioned levels: an explicit product of ill-conditioned
+  // factors loses the accuracy the level-by-level sweep keeps.
+  std::vector<double> node_rcond;
   DevBuf<double> arena;
   i64 arena_used = 0;
   SweepPlan solve_plan, apply_plan;

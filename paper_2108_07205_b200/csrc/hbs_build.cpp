@@ -246,12 +246,19 @@ struct Gate {
   int depth = 0;
 };
 
-void check_gates(const HbsOp& op, std::vector<std::unique_ptr<Gate>>& gates, double thr, cudaStream_t s) {
+void check_gates(HbsOp& op, std::vector<std::unique_ptr<Gate>>& gates, double thr, cudaStream_t s) {
+  op.node_rcond.assign(op.nodes.size(), 1.0);
   for (const auto& gp : gates) {
     const Gate& gt = *gp;
     std::vector<double> hrc(gt.rc.size());
     gt.rc.download(hrc.data(), hrc.size(), s);
     SBX_CUDA(cudaStreamSynchronize(s));
+    for (size_t q = 0; q < gt.ids.size(); ++q) {
+      const auto& nd = op.nodes[gt.ids[q]];
+      double r = nd.c > 0 ? hrc[2 * q] : 1.0;
+      if (gt.ids[q] != 0 && nd.c > 0 && nd.k > 0) r = std::min(r, hrc[2 * q + 1]);
+      op.node_rcond[gt.ids[q]] = r;
+    }
     for (size_t q = 0; q < gt.ids.size(); ++q) {
       const auto& nd = op.nodes[gt.ids[q]];
       if (nd.c > 0 && !(hrc[2 * q] >= thr))

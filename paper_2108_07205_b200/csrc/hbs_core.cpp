@@ -84,6 +84,7 @@ void hbs_layout(HbsOp& op) {
   op.top_L = 0;
   op.o_top = -1;
   op.top_K = op.top_cap = 0;
+  op.node_rcond.clear();
   op.solve_plan.built = false;
   op.apply_plan.built = false;
 }

@@ -762,8 +762,27 @@ int choose_top(const HbsOp& op) {
   for (const auto& nd : op.nodes)
     if (nd.is_leaf()) min_leaf = std::min(min_leaf, nd.depth);
   if (env < 0 && op.max_depth < 7) return 0;  // shallow trees: few levels to save
+  static const double min_rcond = [] {
+    const char* e = std::getenv("SBX_SWEEP_TOP_RCOND");
+    return e ? std::atof(e) : 1e-6;
+  }();
+  static const bool log = std::getenv("SBX_SWEEP_TOP_LOG") != nullptr;  // diagnostics
+  if (log && op.node_rcond.size() == op.nodes.size()) {
+    std::vector<double> mn(size_t(op.max_depth + 1), 1.0);
+    for (size_t i = 0; i < op.nodes.size(); ++i)
+      mn[size_t(op.nodes[i].depth)] = std::min(mn[size_t(op.nodes[i].depth)], op.node_rcond[i]);
+    std::fprintf(stderr, "[sbx-top] n=%lld min rcond by depth:", (long long)op.n);
+    for (double r : mn) std::fprintf(stderr, " %.1e", r);
+    std::fprintf(stderr, "\n");
+  }
   int best = 0;
   for (int L = 2; L < min_leaf && (1 << L) <= kMaxDep; ++L) {
+    if (env < 0) {  // every block above depth L must be well conditioned (and known)
+      bool ok = op.node_rcond.size() == op.nodes.size();
+      for (size_t i = 0; ok && i < op.nodes.size(); ++i)
+        if (op.nodes[i].depth < L && !(op.node_rcond[i] >= min_rcond)) ok = false;
+      if (!ok) break;
+    }
     i64 K = 0;
     for (const auto& nd : op.nodes)
       if (nd.depth == L) K += nd.k;
