@@ -236,15 +236,32 @@ double Geom::panel_arclength(i64 p) const {
 
 void Geom::upload(cudaStream_t s) {
   const i64 n = n_nodes();
-  std::vector<double> h(static_cast<size_t>(8 * n));
+  // staged through a per-thread pinned buffer (a pageable copy of the 8 N
+  // doubles is a synchronous bounce through the driver's staging area)
+  struct Pinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~Pinned() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Pinned pin;
+  const size_t need = size_t(8 * n) * sizeof(double) + size_t(n) * sizeof(int);
+  if (pin.bytes < need) {
+    if (pin.p) SBX_CUDA(cudaFreeHost(pin.p));
+    pin.p = nullptr;
+    SBX_CUDA(cudaMallocHost(&pin.p, need));
+    pin.bytes = need;
+  }
+  double* h = static_cast<double*>(pin.p);
   const std::vector<double>* src[8] = {&x, &y, &nx, &ny, &w, &kappa, &tx, &ty};
-  for (int a = 0; a < 8; ++a) std::copy(src[a]->begin(), src[a]->end(), h.begin() + a * n);
-  std::vector<int> cp(static_cast<size_t>(n));
-  for (i64 i = 0; i < n; ++i) cp[size_t(i)] = int(component_of(i));
+  for (int a = 0; a < 8; ++a) std::copy(src[a]->begin(), src[a]->end(), h + a * n);
+  int* cp = reinterpret_cast<int*>(h + 8 * n);
+  for (i64 i = 0; i < n; ++i) cp[i] = int(component_of(i));
   dev.n = n;
-  dev.buf.upload(h, s);
-  dev.comp.upload(cp, s);
-  SBX_CUDA(cudaStreamSynchronize(s));
+  dev.buf.upload(h, size_t(8 * n), s);
+  dev.comp.upload(cp, size_t(n), s);
+  SBX_CUDA(cudaStreamSynchronize(s));  // the pinned buffer is reused by the next upload
 }
 
 std::vector<PanelDef> uniform_panels(int n_panels, int q) {  // geometry.cpp:112-125
