@@ -233,3 +233,25 @@ def test_fused_app_build_bitwise(po, tmp_path):
         out[mode] = np.load(tmp_path / f"{mode}.npy")
     assert np.array_equal(out["fused"], out["unfused"])
     assert np.all(np.isfinite(out["fused"]))
+
+
+def test_collapsed_top_auto(tmp_path):
+    """Default top choice on a device-compressed 32768-unknown wall: the
+    inverse's rcond gates admit the collapse (depth > 0), and the solve and
+    transposed solve agree with the level-by-level sweep (SBX_SWEEP_TOP=0)."""
+    import os
+    import subprocess
+    import sys
+    root = str(Path(__file__).resolve().parents[1])
+    out, tops = {}, {}
+    for mode in ("auto", "off"):
+        env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        if mode == "off":
+            env["SBX_SWEEP_TOP"] = "0"
+        r = subprocess.run([sys.executable, str(Path(__file__).parent / "top_auto_case.py"), str(tmp_path / f"{mode}.npy")],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        out[mode] = np.load(tmp_path / f"{mode}.npy")
+        tops[mode] = int(r.stdout.split("top")[-1])
+    assert tops["auto"] >= 2 and tops["off"] == 0, tops
+    assert rel(out["auto"], out["off"]) < 1e-12
