@@ -66,7 +66,8 @@ def test_sharded_woodbury_device_matches_els(setup, n_refine):
 
     from paper_2108_07205_b200.parallel import ShardedHbsSolver, ShardedWoodbury
     sb, torch, DeviceExecutor, h, g = setup
-    if not dist.is_initialized():
+    created = not dist.is_initialized()
+    if created:
         s = socket.socket()
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
@@ -98,4 +99,28 @@ def test_sharded_woodbury_device_matches_els(setup, n_refine):
     out[n_k + n_c:] = y_p
     ref = sb.els_solve_raw(els, gx)
     err = (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item()
+    if created and n_refine == 8:  # the last parametrisation tears the group down
+        dist.destroy_process_group()
     assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("n_refine,m", [(2, 4), (8, 16)])
+def test_app_block_solver(setup, n_refine, m):
+    """sbx_app_build / sbx_app_solve (the added block of els_build,
+    els.cpp:107-118): dense LU below 2048 scalars, its own HBS above; the
+    plain and transposed solves against a dense solve of A_pp."""
+    sb, torch, DeviceExecutor, h, g = setup
+    g1, plan = sb.refine(g, list(range(20, 20 + n_refine)), m)
+    app = sb.app_build(g1, plan, 1e-10)
+    added = plan.maps()["added_new"]
+    s = np.stack([2 * added, 2 * added + 1], 1).reshape(-1)
+    A = sb.submatrix(g1, s, s)
+    assert app.info() == {"n_p": len(s), "hbs": 1 if len(s) > 2048 else 0}
+    v = np.random.default_rng(n_refine).uniform(-1, 1, (len(s), 3))
+    tol = 1e-11 if len(s) <= 2048 else 1e-8
+    for tr in (False, True):
+        ref = np.linalg.solve(A.T if tr else A, v)
+        got = app.solve(v, transpose=tr)
+        assert np.linalg.norm(got - ref) <= tol * np.linalg.norm(ref), tr
+    vt = torch.from_numpy(v).cuda()
+    assert np.allclose(app.solve(vt).cpu().numpy(), app.solve(v), rtol=0, atol=1e-13 * np.abs(v).max() * 1e3)
