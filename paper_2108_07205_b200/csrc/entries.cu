@@ -189,7 +189,8 @@ __global__ void proxy_jobs_kernel(EntryView v, const ProxyJob* __restrict__ jobs
     const i64 node = node_of(v, cs >> 1);
     const int a = int(cs & 1);
     const double t = 2.0 * kPi * double(s) / double(jb.ns);
-    const double d0 = cos(t), d1 = sin(t);
+    double d0, d1;
+    sincos(t, &d1, &d0);  // bitwise equal to sin(t), cos(t) (scripts/sincos_check.cu), one reduction
     const double p0 = jb.cx + jb.rad * d0, p1 = jb.cy + jb.rad * d1;
     double* col = out + jb.out_off + i64(c) * jb.ld;
     double q0, q1, q2, q3;
