@@ -51,6 +51,18 @@ int guard(F&& f) {
   }
 }
 
+// Releasing a handle waits for the device, as cudaFree would: its device
+// memory returns to a stream-ordered pool while solves enqueued on caller
+// streams may still be reading it.
+template <class T>
+int destroy_handle(T* h) {
+  if (h) {
+    (void)cudaDeviceSynchronize();
+    delete h;
+  }
+  return SBX_OK;
+}
+
 cudaStream_t stream_of(void* s) {
   return s ? static_cast<cudaStream_t>(s) : sbx::lib_stream();
 }
@@ -157,10 +169,7 @@ int sbx_geom_add_holes(sbx_geom wall, int n_holes, const sbx_curve* holes, const
   });
 }
 
-int sbx_geom_destroy(sbx_geom g) {
-  delete g;
-  return SBX_OK;
-}
+int sbx_geom_destroy(sbx_geom g) { return destroy_handle(g); }
 
 int sbx_geom_info(sbx_geom g, int64_t* n_nodes, int64_t* n_panels, int64_t* n_components) {
   return guard([&] {
@@ -209,10 +218,7 @@ int sbx_coarsen(sbx_geom g, sbx_plan plan, sbx_geom* out) {
   });
 }
 
-int sbx_plan_destroy(sbx_plan p) {
-  delete p;
-  return SBX_OK;
-}
+int sbx_plan_destroy(sbx_plan p) { return destroy_handle(p); }
 
 int sbx_plan_sizes(sbx_plan p, int64_t* n_k, int64_t* n_c, int64_t* n_p) {
   return guard([&] {
@@ -282,10 +288,7 @@ int sbx_hbs_invert(sbx_hbs h) {
   return guard([&] { sbx::hbs_invert_device(H(h), sbx::lib_stream()); });
 }
 
-int sbx_hbs_destroy(sbx_hbs h) {
-  delete h;
-  return SBX_OK;
-}
+int sbx_hbs_destroy(sbx_hbs h) { return destroy_handle(h); }
 
 int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double* x, int64_t ldx,
                   int flags, void* stream) {
@@ -384,10 +387,7 @@ int sbx_update_compress(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formu
   });
 }
 
-int sbx_update_destroy(sbx_update u) {
-  delete u;
-  return SBX_OK;
-}
+int sbx_update_destroy(sbx_update u) { return destroy_handle(u); }
 
 int sbx_update_info(sbx_update u, int64_t* info) {
   return guard([&] {
@@ -440,10 +440,7 @@ int sbx_app_build(sbx_geom new_g, sbx_plan plan, int formulation, double mu, dou
   });
 }
 
-int sbx_app_destroy(sbx_app a) {
-  delete a;
-  return SBX_OK;
-}
+int sbx_app_destroy(sbx_app a) { return destroy_handle(a); }
 
 int sbx_app_info(sbx_app a, int64_t* info) {
   return guard([&] {
@@ -477,10 +474,7 @@ int sbx_app_solve(sbx_app a, const double* v, int64_t ldv, int64_t nrhs, double*
   });
 }
 
-int sbx_els_destroy(sbx_els e) {
-  delete e;
-  return SBX_OK;
-}
+int sbx_els_destroy(sbx_els e) { return destroy_handle(e); }
 
 int sbx_els_info(sbx_els e, int64_t* info) {
   return guard([&] {

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -171,6 +172,27 @@ class DevBuf {
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
+};
+
+// Per-stream scratch of a shared, immutable handle (the reference's
+// "concurrent solves with distinct right-hand sides allowed", SPEC.md:362,
+// 445): calls on one stream reuse one scratch set (stream order protects
+// it), calls on distinct streams never share one.  Entries live as long as
+// the handle, so returned references stay valid.
+template <class T>
+class PerStream {
+ public:
+  T& get(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& e : items_)
+      if (e.first == s) return *e.second;
+    items_.emplace_back(s, std::make_unique<T>());
+    return *items_.back().second;
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<cudaStream_t, std::unique_ptr<T>>> items_;
 };
 
 // Column-major host matrix (the reference's Eigen storage order; used for

@@ -53,16 +53,11 @@ double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
 void atilde_solve(Els& e, const double* v, i64 ldv, double* out, i64 ldo, i64 nrhs, cudaStream_t s,
                   bool tr = false) {
   HbsOp& A = *e.a_oo;
-  if (!A.solve_plan.built) hbs_build_solve_plan(A);
+  hbs_ensure_solve_plan(A);
   if (tr) hbs_ensure_transpose(A, true, false, s);
-  SweepPlan& P = A.solve_plan;
-  const i64 ldw = sweep_ld(nrhs);
-  A.ws.reserve(size_t(P.ws_rows * ldw));
   const i64 nkc = e.n_k + e.n_c;
-  launch_cm_to_rm(v, ldv, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
-  hbs_run_plan(A, P, A.ws.get(), nrhs, s, tr ? A.arena_t.get() : nullptr);
-  // gather: out row i <- old row map[i]
-  launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), s);
+  // scatter to old-mesh rows, sweep, gather: out row i <- old row map[i]
+  hbs_sweep_rows(A, A.solve_plan, v, ldv, nkc, nrhs, out, ldo, e.d_old_of_ext.get(), tr, s);
   phase_mark("els:   a_oo sweep", s);
   if (e.n_p == 0) return;
   app_solve_device(*e.app, v + nkc, ldv, out + nkc, ldo, nrhs, s, tr);
@@ -74,16 +69,11 @@ void app_solve_device(AppSolver& a, const double* vp, i64 ldv, double* op, i64 l
                       bool tr) {
   const i64 n_p = 2 * i64(a.added.size());
   if (n_p == 0 || nrhs == 0) return;
-  const i64 ldw = sweep_ld(nrhs);
   if (a.h) {
     HbsOp& H = *a.h;
-    if (!H.solve_plan.built) hbs_build_solve_plan(H);
+    hbs_ensure_solve_plan(H);
     if (tr) hbs_ensure_transpose(H, true, false, s);
-    SweepPlan& Q = H.solve_plan;
-    H.ws.reserve(size_t(Q.ws_rows * ldw));
-    launch_cm_to_rm(vp, ldv, n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
-    hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
-    launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, n_p, nrhs, op, ldo, nullptr, s);
+    hbs_sweep_rows(H, H.solve_plan, vp, ldv, n_p, nrhs, op, ldo, nullptr, tr, s);
     phase_mark("els:   A_pp sweep", s);
   } else {  // explicit inverse of A_pp (els.cpp:47: app_lu.solve / app_lu.transpose().solve)
     gemm_batched({{a.inv.get(), vp, op, int(n_p), int(nrhs), int(n_p), int(n_p), int(ldv), int(ldo), tr ? 1 : 0, 0,
@@ -190,24 +180,15 @@ void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cu
                               bool with_update) {
   const i64 n = e.n_ext(), nkc = e.n_k + e.n_c;
   HbsOp& A = *e.a_oo;
-  if (!A.apply_plan.built) hbs_build_apply_plan(A);
+  hbs_ensure_apply_plan(A);
   if (tr) hbs_ensure_transpose(A, false, true, s);
-  SweepPlan& P = A.apply_plan;
-  const i64 ldw = sweep_ld(nrhs);
-  A.ws.reserve(size_t(P.ws_rows * ldw));
-  launch_cm_to_rm(v, n, nkc, nrhs, A.ws.get() + P.in_row * ldw, ldw, e.d_old_of_ext.get(), s);
-  hbs_run_plan(A, P, A.ws.get(), nrhs, s, tr ? A.arena_t.get() : nullptr);
-  launch_rm_to_cm(A.ws.get() + P.out_row * ldw, ldw, nkc, nrhs, out, n, e.d_old_of_ext.get(), s);
+  hbs_sweep_rows(A, A.apply_plan, v, n, nkc, nrhs, out, n, e.d_old_of_ext.get(), tr, s);
   if (e.n_p > 0) {
     if (e.app->h) {
       HbsOp& H = *e.app->h;
-      if (!H.apply_plan.built) hbs_build_apply_plan(H);
+      hbs_ensure_apply_plan(H);
       if (tr) hbs_ensure_transpose(H, false, true, s);
-      SweepPlan& Q = H.apply_plan;
-      H.ws.reserve(size_t(Q.ws_rows * ldw));
-      launch_cm_to_rm(v + nkc, n, e.n_p, nrhs, H.ws.get() + Q.in_row * ldw, ldw, nullptr, s);
-      hbs_run_plan(H, Q, H.ws.get(), nrhs, s, tr ? H.arena_t.get() : nullptr);
-      launch_rm_to_cm(H.ws.get() + Q.out_row * ldw, ldw, e.n_p, nrhs, out + nkc, n, nullptr, s);
+      hbs_sweep_rows(H, H.apply_plan, v + nkc, n, e.n_p, nrhs, out + nkc, n, nullptr, tr, s);
     } else {
       gemm_batched({{e.app->fwd.get(), v + nkc, out + nkc, int(e.n_p), int(nrhs), int(e.n_p), int(e.n_p), int(n),
                      int(n), tr ? 1 : 0, 0, 1.0, 0.0}},
@@ -215,8 +196,7 @@ void els_apply_forward_device(Els& e, const double* v, double* out, i64 nrhs, cu
     }
   }
   if (e.k == 0 || !with_update) return;
-  e.ws2.reserve(size_t(e.k * nrhs));
-  double* t = e.ws2.get();
+  double* t = e.scratch_for(s).ws2(size_t(e.k * nrhs), s);
   if (!tr) {
     // out += L (R v)   (els.cpp:184); L is reconstructed as the update factor
     gemm_batched({{e.R.get(), v, t, int(e.k), int(nrhs), int(n), int(e.k), int(n), int(e.k), 0, 0, 1.0, 0.0}}, s);
@@ -233,8 +213,7 @@ void els_solve_ext_device(Els& e, const double* g_ext, double* y, i64 nrhs, cuda
   atilde_solve(e, g_ext, n, y, n, nrhs, s);
   if (k == 0) return;
   // y -= X W^{-1} (R y)   (els.cpp:150)
-  e.ws2.reserve(size_t(2 * k * nrhs));
-  double* t = e.ws2.get();
+  double* t = e.scratch_for(s).ws2(size_t(2 * k * nrhs), s);
   double* u = t + k * nrhs;
   gemm_batched({{e.R.get(), y, t, int(k), int(nrhs), int(n), int(k), int(n), int(k), 0, 0, 1.0, 0.0}}, s);
   gemm_batched({{e.Winv.get(), t, u, int(k), int(nrhs), int(k), int(k), int(k), int(k), 0, 0, 1.0, 0.0}}, s);
@@ -252,8 +231,7 @@ void els_solve_ext_t_device(Els& e, const double* g_ext, double* y, i64 nrhs, cu
     return;
   }
   // z = g - R^T W^{-T} (X^T g);  y = Atilde^{-T} z   (els.cpp:157-162)
-  e.ws2.reserve(size_t(2 * k * nrhs));
-  double* t = e.ws2.get();
+  double* t = e.scratch_for(s).ws2(size_t(2 * k * nrhs), s);
   double* u = t + k * nrhs;
   DevBuf<double> z(static_cast<size_t>(n * nrhs));
   SBX_CUDA(cudaMemcpyAsync(z.get(), g_ext, size_t(n * nrhs) * 8, cudaMemcpyDeviceToDevice, s));
@@ -270,8 +248,7 @@ void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, b
   const i64 rows_in = raw ? n : e.n_k + e.n_p;
   require(ldg >= rows_in && ldy >= rows_in, "els_solve: leading dimension too small");
   if (nrhs == 0) return;
-  e.ws.reserve(size_t(2 * n * nrhs));
-  double* gx = e.ws.get();
+  double* gx = e.scratch_for(s).ws(size_t(2 * n * nrhs), s);
   double* yx = gx + n * nrhs;
   const i64 nkc = e.n_k + e.n_c;
   // g_ext = (g_k, 0, g_p)  (els.cpp:167-169)

@@ -54,8 +54,23 @@ struct Els {
   DevBuf<i64> d_old_of_ext;         // ext rows [0, n_k+n_c) -> old-mesh scalar
   std::vector<i64> kept_new_s, added_s;
   i64 n_new = 0;
-  DevBuf<double> ws;                // solve workspace
-  DevBuf<double> ws2;
+  // Per-stream solve workspaces: the solver is immutable after build, so
+  // concurrent solves on distinct streams are legal.
+  struct Scratch {
+    DevBuf<double> a, b;
+    double* ws(size_t n, cudaStream_t s) {
+      StreamScope ss(s);
+      a.reserve(n);
+      return a.get();
+    }
+    double* ws2(size_t n, cudaStream_t s) {
+      StreamScope ss(s);
+      b.reserve(n);
+      return b.get();
+    }
+  };
+  PerStream<Scratch> scratch;
+  Scratch& scratch_for(cudaStream_t s) { return scratch.get(s); }
 };
 
 std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom& new_g,

@@ -13,6 +13,7 @@
 // All blocks are column-major (Eigen order) so HBS1 files map 1:1.
 #pragma once
 
+#include <atomic>
 #include <map>
 #include <memory>
 #include <string>
@@ -87,7 +88,7 @@ struct SweepPlan {
   // (tile, column-tile count) key: a step alternates block widths (the
   // Woodbury build's u columns, the solve's RHS) without rebuilding them
   std::map<int, std::unique_ptr<struct FlowCache>> flows;
-  bool built = false;
+  std::atomic<bool> built{false};
 };
 
 struct FlowCache {
@@ -97,9 +98,16 @@ struct FlowCache {
   DevBuf<int> d_needs;       // items per task and column tile (dependency counts)
   i64 partial_elems = 0;     // split-K partial tiles (doubles)
   int n_tile_cnt = 0;
-  DevBuf<double> d_partials;
   i64 n_flow_items = 0;
-  DevBuf<int> d_counters;
+};
+
+// Mutable per-call state of a sweep: the row-major workspace, host-pointer
+// staging, the dataflow completion counters and split-K partial tiles.  One
+// set per stream (HbsOp::scratch), so concurrent solves on distinct streams
+// against one operator never share any of it.
+struct SweepScratch {
+  DevBuf<double> ws, io, partials;
+  DevBuf<int> counters;
 };
 
 struct ShardPlans;
@@ -136,8 +144,14 @@ struct HbsOp {
   DevBuf<double> arena_t;
   bool t_solve = false, t_apply = false;
   std::unique_ptr<struct ShardPlans> shard;  // subtree-partitioned solve (multi-GPU)
-  DevBuf<double> ws;  // sweep workspace (grown on demand)
-  DevBuf<double> io;  // staging for host-pointer sweeps (grown on demand)
+  // Lazily built shared state (plans, flow items, transposed arena,
+  // collapsed top, shard plans) is created under `mu`; everything a call
+  // mutates lives in its stream's scratch.  After the first call on a
+  // handle, concurrent calls on distinct streams only contend for `mu`
+  // while enqueueing.
+  std::recursive_mutex mu;
+  PerStream<SweepScratch> scratch;
+  SweepScratch& scratch_for(cudaStream_t s) { return scratch.get(s); }
 
   i64 total_skeleton() const {
     i64 t = 0;
@@ -172,6 +186,12 @@ void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy
 // in `ws` row layout (the ELS path): runs the planned levels only.
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s,
                   const double* fac = nullptr);
+// Column-major rows x nrhs block through `plan` on the stream's scratch:
+// input row i goes to sweep row map[i] (identity when map is null), output
+// row i comes from sweep row map[i]; `transposed` sweeps the transposed
+// arena (hbs_ensure_transpose first).
+void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 rows, i64 nrhs, double* out,
+                    i64 ldo, const i64* map, bool transposed, cudaStream_t s);
 // hbs.cpp:627-664 / :546-587: transposed solve and apply.
 void hbs_solve_t(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev, cudaStream_t s);
 void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev, cudaStream_t s);
@@ -179,6 +199,9 @@ void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 l
 void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s);
 void hbs_build_solve_plan(HbsOp& op);
 void hbs_build_apply_plan(HbsOp& op);
+// The same, built once under op.mu on first use (thread safe).
+void hbs_ensure_solve_plan(HbsOp& op);
+void hbs_ensure_apply_plan(HbsOp& op);
 
 // Subtree-partitioned solve: rank p of G = 2^g owns the
 // subtree rooted at the p-th BFS node of depth g, i.e. old-mesh scalar rows

@@ -130,13 +130,24 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
 // ---------------------------------------------------------------- rendezvous
 IdRendezvous::IdRendezvous(int participants) : active_(participants) {}
 
-void IdRendezvous::flush_locked(cudaStream_t s) {
+void IdRendezvous::flush_locked(std::unique_lock<std::mutex>& lk, cudaStream_t s) {
   std::vector<QrJob> merged;
   for (auto* v : pending_) merged.insert(merged.end(), v->begin(), v->end());
-  launch_id_jobs(merged, 0, s);
   pending_.clear();
   waiting_ = 0;
-  ++generation_;
+  const unsigned long long gen = ++generation_;
+  // the launch runs with the lock held: the waiters' job vectors (copied
+  // above) are theirs again, but the next round must not start before this
+  // launch is enqueued (stream order of the rounds)
+  try {
+    launch_id_jobs(merged, 0, s);
+  } catch (...) {
+    err_ = std::current_exception();
+    err_gen_ = gen;
+    cv_.notify_all();
+    throw;
+  }
+  (void)lk;
   cv_.notify_all();
 }
 
@@ -146,22 +157,30 @@ void IdRendezvous::submit(std::vector<QrJob>& jobs, cudaStream_t s) {
   ++waiting_;
   last_stream_ = s;
   if (waiting_ >= active_) {
-    flush_locked(s);
+    flush_locked(lk, s);
     return;
   }
   const unsigned long long gen = generation_;
   cv_.wait(lk, [&] { return generation_ != gen; });
+  if (err_ && err_gen_ == gen + 1) std::rethrow_exception(err_);
 }
 
-void IdRendezvous::leave() {
-  std::lock_guard<std::mutex> lk(mu_);
+void IdRendezvous::leave() noexcept {
+  std::unique_lock<std::mutex> lk(mu_);
   --active_;
-  if (waiting_ > 0 && waiting_ >= active_) flush_locked(last_stream_);
+  if (waiting_ > 0 && waiting_ >= active_) {
+    try {
+      flush_locked(lk, last_stream_);
+    } catch (...) {
+      // recorded in err_ for the waiters of that round; the leaving thread
+      // is done with the rendezvous (possibly unwinding already)
+    }
+  }
 }
 
 IdRendezvousScope::IdRendezvousScope(IdRendezvous* rv) : rv_(rv), prev_(tl_rv) { tl_rv = rv; }
 IdRendezvousScope::~IdRendezvousScope() { leave(); }
-void IdRendezvousScope::leave() {
+void IdRendezvousScope::leave() noexcept {
   if (rv_) {
     rv_->leave();
     rv_ = nullptr;

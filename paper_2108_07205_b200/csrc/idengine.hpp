@@ -5,6 +5,7 @@
 #pragma once
 
 #include <condition_variable>
+#include <exception>
 #include <mutex>
 #include <vector>
 
@@ -64,17 +65,26 @@ void launch_id_jobs(const std::vector<QrJob>& jobs, int force_engine, cudaStream
 class IdRendezvous {
  public:
   explicit IdRendezvous(int participants);
+  // Throws the launch's error in every participant of the failed round.
   void submit(std::vector<QrJob>& jobs, cudaStream_t s);
-  void leave();
+  // Never throws (called during unwinding): a failed flush is handed to the
+  // waiting participants instead.
+  void leave() noexcept;
 
  private:
-  void flush_locked(cudaStream_t s);
+  // Starts a new round BEFORE launching (pending jobs moved out, generation
+  // bumped, waiters released), so a throwing launch never leaves a
+  // participant blocked or a dangling pending entry behind.
+  void flush_locked(std::unique_lock<std::mutex>& lk, cudaStream_t s);
   std::mutex mu_;
   std::condition_variable cv_;
   int active_ = 0, waiting_ = 0;
   unsigned long long generation_ = 0;
   std::vector<std::vector<QrJob>*> pending_;
   cudaStream_t last_stream_ = nullptr;
+  // error of round `err_gen_` (its generation after the bump), if its launch threw
+  std::exception_ptr err_;
+  unsigned long long err_gen_ = 0;
 };
 
 // Installs a rendezvous for the calling thread's IdBatch::factor calls;
@@ -83,7 +93,7 @@ class IdRendezvousScope {
  public:
   explicit IdRendezvousScope(IdRendezvous* rv);
   ~IdRendezvousScope();
-  void leave();
+  void leave() noexcept;
   IdRendezvousScope(const IdRendezvousScope&) = delete;
   IdRendezvousScope& operator=(const IdRendezvousScope&) = delete;
 

@@ -848,7 +848,9 @@ void hbs_build_top(HbsOp& op, int L, cudaStream_t s) {
     const i64 off = (op.arena_used + 31) / 32 * 32;
     DevBuf<double> grown(static_cast<size_t>(off + Kd * Kd));
     SBX_CUDA(cudaMemcpyAsync(grown.get(), op.arena.get(), size_t(op.arena_used) * 8, cudaMemcpyDeviceToDevice, s));
-    SBX_CUDA(cudaStreamSynchronize(s));
+    // the old arena may still be read by sweeps in flight on other streams
+    // (an apply on a caller stream): drain the device before it is recycled
+    SBX_CUDA(cudaDeviceSynchronize());
     op.arena = std::move(grown);
     op.o_top = off;
     op.top_cap = Kd * Kd;
@@ -871,6 +873,7 @@ void hbs_build_solve_plan(HbsOp& op) {
 }
 
 ShardPlans& hbs_shard(HbsOp& op, int G, int p) {
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
   require(op.has_inverse, "hbs_solve: inverse not built");
   require(G >= 1 && (G & (G - 1)) == 0, "shard: rank count must be a power of two");
   require(p >= 0 && p < G, "shard: rank out of range");
@@ -921,18 +924,24 @@ ShardPlans& hbs_shard(HbsOp& op, int G, int p) {
 
 void hbs_solve_shard_up(HbsOp& op, int G, int p, const double* b_local, i64 ldb, i64 nrhs, double* hat_out,
                         bool dev, cudaStream_t s) {
+  // the shard plans are replaced when (G, p) changes: one shard call at a time per handle
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
   ShardPlans& S = hbs_shard(op, G, p);
   const i64 rows = S.row1 - S.row0;
   require(nrhs >= 1 && ldb >= rows, "shard_up: bad sizes");
   const i64 ldw = sweep_ld(nrhs);
-  op.ws.reserve(size_t(S.up.ws_rows * ldw));
-  double* ws = op.ws.get();
+  SweepScratch& sc = op.scratch_for(s);
+  {
+    StreamScope ss(s);
+    sc.ws.reserve(size_t(S.up.ws_rows * ldw));
+    if (!dev) sc.io.reserve(size_t(rows * nrhs));
+  }
+  double* ws = sc.ws.get();
   const double* bd = b_local;
   if (!dev) {
-    op.io.reserve(size_t(rows * nrhs));
-    SBX_CUDA(cudaMemcpy2DAsync(op.io.get(), size_t(rows) * 8, b_local, size_t(ldb) * 8, size_t(rows) * 8,
+    SBX_CUDA(cudaMemcpy2DAsync(sc.io.get(), size_t(rows) * 8, b_local, size_t(ldb) * 8, size_t(rows) * 8,
                                size_t(nrhs), cudaMemcpyHostToDevice, s));
-    bd = op.io.get();
+    bd = sc.io.get();
   }
   launch_cm_to_rm(bd, dev ? ldb : rows, rows, nrhs, ws + (S.up.in_row + S.row0) * ldw, ldw, nullptr, s);
   hbs_run_plan(op, S.up, ws, nrhs, s);
@@ -952,12 +961,14 @@ void hbs_solve_shard_up(HbsOp& op, int G, int p, const double* b_local, i64 ldb,
 
 void hbs_solve_shard_down(HbsOp& op, int G, int p, const double* hats, i64 nrhs, double* x_local, i64 ldx,
                           bool dev, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
   ShardPlans& S = hbs_shard(op, G, p);
   const i64 rows = S.row1 - S.row0;
   require(nrhs >= 1 && ldx >= rows, "shard_down: bad sizes");
   const i64 ldw = sweep_ld(nrhs);
-  require(op.ws.size() >= size_t(S.up.ws_rows * ldw), "shard_down: call shard_up first");
-  double* ws = op.ws.get();
+  SweepScratch& sc = op.scratch_for(s);
+  require(sc.ws.size() >= size_t(S.up.ws_rows * ldw), "shard_down: call shard_up first (on the same stream)");
+  double* ws = sc.ws.get();
   const SolveLayout Y = solve_layout(op);
   const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if (S.g > 0)
@@ -974,9 +985,12 @@ void hbs_solve_shard_down(HbsOp& op, int G, int p, const double* hats, i64 nrhs,
   if (dev) {
     launch_rm_to_cm(ws + (S.down.out_row + S.row0) * ldw, ldw, rows, nrhs, x_local, ldx, nullptr, s);
   } else {
-    op.io.reserve(size_t(rows * nrhs));
-    launch_rm_to_cm(ws + (S.down.out_row + S.row0) * ldw, ldw, rows, nrhs, op.io.get(), rows, nullptr, s);
-    SBX_CUDA(cudaMemcpy2DAsync(x_local, size_t(ldx) * 8, op.io.get(), size_t(rows) * 8, size_t(rows) * 8,
+    {
+      StreamScope ss(s);
+      sc.io.reserve(size_t(rows * nrhs));
+    }
+    launch_rm_to_cm(ws + (S.down.out_row + S.row0) * ldw, ldw, rows, nrhs, sc.io.get(), rows, nullptr, s);
+    SBX_CUDA(cudaMemcpy2DAsync(x_local, size_t(ldx) * 8, sc.io.get(), size_t(rows) * 8, size_t(rows) * 8,
                                size_t(nrhs), cudaMemcpyDeviceToHost, s));
     SBX_CUDA(cudaStreamSynchronize(s));
   }
@@ -1113,6 +1127,9 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     return e ? std::atoi(e) : 300;
   }();
   const int key = ((ncol * 2 + (dmma ? 1 : 0)) * 2 + (target > 0 ? 1 : 0)) * 128 + TN;
+  // the flow items of this width are built once per plan under op.mu (they
+  // are immutable afterwards and shared by every stream)
+  std::unique_lock<std::recursive_mutex> lk(op.mu);
   auto& slot = plan.flows[key];
   const bool fresh = !slot;
   if (fresh) slot = std::make_unique<FlowCache>();
@@ -1134,7 +1151,9 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     }
     F.d_descs.upload(descs, s);
     F.n_flow_items = i64(fi.size());
+    SBX_CUDA(cudaStreamSynchronize(s));  // other streams may launch over these tables next
   }
+  lk.unlock();
   if (per_level) {
     for (const int2 rg : F.level_items) {
       if (rg.y == 0) continue;
@@ -1149,27 +1168,38 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     return;
   }
   if (F.n_flow_items == 0) return;
+  // completion counters and split-K partials are per call: the stream's scratch
+  SweepScratch& sc = op.scratch_for(s);
   const size_t ncount = size_t(1 + plan.n_tasks * ncol + F.n_tile_cnt);
-  F.d_counters.reserve(ncount);
-  F.d_partials.reserve(size_t(std::max<i64>(F.partial_elems, 1)));
-  SBX_CUDA(cudaMemsetAsync(F.d_counters.get(), 0, ncount * sizeof(int), s));
-  int* tile_cnt = F.d_counters.get() + 1 + plan.n_tasks * ncol;
+  {
+    StreamScope ss(s);
+    sc.counters.reserve(ncount);
+    sc.partials.reserve(size_t(std::max<i64>(F.partial_elems, 1)));
+  }
+  SBX_CUDA(cudaMemsetAsync(sc.counters.get(), 0, ncount * sizeof(int), s));
+  int* counters = sc.counters.get();
+  int* tile_cnt = counters + 1 + plan.n_tasks * ncol;
+  double* partials = sc.partials.get();
   const int grid = int(std::min<i64>(F.n_flow_items, i64(sms) * per_sm));
   static const char* trace_path = std::getenv("SBX_SWEEP_TRACE");  // diagnostics: per-item timeline
   DevBuf<unsigned long long> trace;
   if (trace_path) trace.resize(size_t(4 * F.n_flow_items));
+  unsigned long long* tr = trace.get();
+  const SweepTask* tasks = plan.d_tasks.get();
+  const FlowItem* items = F.d_flow_items.get();
+  const ItemDesc* descs = F.d_descs.get();
+  int n_items = int(F.n_flow_items), nr = int(nrhs), ldw = dmma ? int(sweep_ld(nrhs)) : 1;
+  void* args[] = {(void*)&fac, (void*)&ws, (void*)&tasks, (void*)&items, (void*)&n_items, (void*)&counters,
+                  (void*)&ncol, (void*)&nr, (void*)&ldw, (void*)&partials, (void*)&tile_cnt, (void*)&tr,
+                  (void*)&descs};
+  // Cooperative launch: the static round-robin item schedule spin-waits on
+  // items held by other CTAs, which is only deadlock-free when the whole
+  // grid is co-resident -- guaranteed here even when other streams' kernels
+  // (a concurrent solve on the same handle) occupy part of the chip.
   KernelTimer kt(dmma ? "sweep_flow_dmma" : "sweep_flow_gemv", s);
-  if (dmma)
-    sweep_flow_kernel<true, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(), F.d_flow_items.get(),
-                                                             int(F.n_flow_items), F.d_counters.get(), ncol,
-                                                             int(nrhs), int(sweep_ld(nrhs)), F.d_partials.get(),
-                                                             tile_cnt, trace.get(), F.d_descs.get());
-  else
-    sweep_flow_kernel<false, TN><<<grid, kThreads, smem, s>>>(fac, ws, plan.d_tasks.get(),
-                                                              F.d_flow_items.get(), int(F.n_flow_items),
-                                                              F.d_counters.get(), ncol, int(nrhs), 1,
-                                                              F.d_partials.get(), tile_cnt, trace.get(),
-                                                              F.d_descs.get());
+  const void* fn = dmma ? reinterpret_cast<const void*>(&sweep_flow_kernel<true, TN>)
+                        : reinterpret_cast<const void*>(&sweep_flow_kernel<false, TN>);
+  SBX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(grid)), dim3(kThreads), args, smem, s));
   SBX_LAUNCHED();
   if (trace_path) {
     std::vector<unsigned long long> h(size_t(4 * F.n_flow_items));
@@ -1198,6 +1228,33 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
 
 }  // namespace
 
+void hbs_ensure_solve_plan(HbsOp& op) {
+  if (op.solve_plan.built.load(std::memory_order_acquire)) return;
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
+  if (!op.solve_plan.built) hbs_build_solve_plan(op);
+}
+
+void hbs_ensure_apply_plan(HbsOp& op) {
+  if (op.apply_plan.built.load(std::memory_order_acquire)) return;
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
+  if (!op.apply_plan.built) hbs_build_apply_plan(op);
+}
+
+void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 rows, i64 nrhs, double* out,
+                    i64 ldo, const i64* map, bool transposed, cudaStream_t s) {
+  if (nrhs == 0 || rows == 0) return;
+  const i64 ldw = sweep_ld(nrhs);
+  SweepScratch& sc = op.scratch_for(s);
+  {
+    StreamScope ss(s);
+    sc.ws.reserve(size_t(plan.ws_rows * ldw));
+  }
+  double* ws = sc.ws.get();
+  launch_cm_to_rm(in, ldi, rows, nrhs, ws + plan.in_row * ldw, ldw, map, s);
+  hbs_run_plan(op, plan, ws, nrhs, s, transposed ? op.arena_t.get() : nullptr);
+  launch_rm_to_cm(ws + plan.out_row * ldw, ldw, rows, nrhs, out, ldo, map, s);
+}
+
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
   if (!fac) fac = op.arena.get();
   // column tile: 32 when the block is narrow enough that the tree depth
@@ -1215,26 +1272,25 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
 
 namespace {
 void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx,
-               bool dev, cudaStream_t s, const double* fac = nullptr) {
+               bool dev, cudaStream_t s, bool transposed = false) {
   require(nrhs >= 0, "sweep: negative nrhs");
   require(ldb >= op.n && ldx >= op.n, "sweep: leading dimension smaller than n");
   if (nrhs == 0) return;
-  const i64 ldw = sweep_ld(nrhs);
-  op.ws.reserve(size_t(plan.ws_rows * ldw));
-  double* ws = op.ws.get();
   const double* bd = b;
   double* xd = x;
   if (!dev) {
-    op.io.reserve(size_t(2 * op.n * nrhs));
-    double* hb = op.io.get();
+    SweepScratch& sc = op.scratch_for(s);
+    {
+      StreamScope ss(s);
+      sc.io.reserve(size_t(2 * op.n * nrhs));
+    }
+    double* hb = sc.io.get();
     SBX_CUDA(cudaMemcpy2DAsync(hb, size_t(op.n) * 8, b, size_t(ldb) * 8, size_t(op.n) * 8,
                                size_t(nrhs), cudaMemcpyHostToDevice, s));
     bd = hb;
     xd = hb + op.n * nrhs;
   }
-  launch_cm_to_rm(bd, dev ? ldb : op.n, op.n, nrhs, ws + plan.in_row * ldw, ldw, nullptr, s);
-  hbs_run_plan(op, plan, ws, nrhs, s, fac);
-  launch_rm_to_cm(ws + plan.out_row * ldw, ldw, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, s);
+  hbs_sweep_rows(op, plan, bd, dev ? ldb : op.n, op.n, nrhs, xd, dev ? ldx : op.n, nullptr, transposed, s);
   if (!dev) {
     SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, xd, size_t(op.n) * 8, size_t(op.n) * 8,
                                size_t(nrhs), cudaMemcpyDeviceToHost, s));
@@ -1245,17 +1301,18 @@ void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, d
 
 void hbs_solve(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev,
                cudaStream_t s) {
-  if (!op.solve_plan.built) hbs_build_solve_plan(op);
+  hbs_ensure_solve_plan(op);
   run_sweep(op, op.solve_plan, b, ldb, nrhs, x, ldx, dev, s);
 }
 
 void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev,
                cudaStream_t s) {
-  if (!op.apply_plan.built) hbs_build_apply_plan(op);
+  hbs_ensure_apply_plan(op);
   run_sweep(op, op.apply_plan, v, ldv, nrhs, y, ldy, dev, s);
 }
 
 void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s) {
+  std::lock_guard<std::recursive_mutex> lk(op.mu);
   solve = solve && !op.t_solve;
   apply = apply && !op.t_apply;
   if (!solve && !apply) return;
@@ -1309,16 +1366,16 @@ void hbs_ensure_transpose(HbsOp& op, bool solve, bool apply, cudaStream_t s) {
 
 void hbs_solve_t(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev,
                  cudaStream_t s) {
-  if (!op.solve_plan.built) hbs_build_solve_plan(op);
+  hbs_ensure_solve_plan(op);
   hbs_ensure_transpose(op, true, false, s);
-  run_sweep(op, op.solve_plan, b, ldb, nrhs, x, ldx, dev, s, op.arena_t.get());
+  run_sweep(op, op.solve_plan, b, ldb, nrhs, x, ldx, dev, s, true);
 }
 
 void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev,
                  cudaStream_t s) {
-  if (!op.apply_plan.built) hbs_build_apply_plan(op);
+  hbs_ensure_apply_plan(op);
   hbs_ensure_transpose(op, false, true, s);
-  run_sweep(op, op.apply_plan, v, ldv, nrhs, y, ldy, dev, s, op.arena_t.get());
+  run_sweep(op, op.apply_plan, v, ldv, nrhs, y, ldy, dev, s, true);
 }
 
 }  // namespace sbx

@@ -680,6 +680,15 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
         }
       });
     }
+    // on any exception below: main_rs leaves the rendezvous first (so the
+    // A_pp thread's pending and later factorisations launch on their own),
+    // then the thread is joined before it is destroyed -- never terminate()
+    struct JoinOnExit {
+      std::thread& t;
+      ~JoinOnExit() {
+        if (t.joinable()) t.join();
+      }
+    } join_app{app_thread};
     IdRendezvousScope main_rs(rv.get());
     // every row-ID hierarchy of the update advances in lockstep (one batched
     // CPQR per tree level across all of them)
@@ -689,6 +698,11 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
       for (size_t r = st; r < std::min(st + 128, plan.added_new.size()); ++r) l.push_back(i64(r));
       ptree.push_back(std::move(l));
     }
+    static const bool fault = [] {  // tests: a proxy violation while the A_pp thread is running
+      const char* e = std::getenv("SBX_TEST_FAULT");
+      return e && std::string(e) == "far_prepare";
+    }();
+    if (fault) throw Error(5, "far row point inside a division circle (injected by SBX_TEST_FAULT)");
     const FarPrep fk = far_prepare(ng, far_nodes, circles, true, ktree);
     FarPrep fp;
     if (!plan.added_new.empty()) fp = far_prepare(ng, plan.added_new, circles, false, ptree);
