@@ -117,6 +117,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
+def workload_config(cfg, world):
+    """The `config` object, identical in both arms (--impl ours / reference)."""
+    return {"workload": f"{cfg.name}: star r=1+0.3cos5t, 1024x16 nodes (32768 unknowns), "
+                        f"refine 16 panels m=16, 64 RHS of 8 exterior Stokeslets, eps 1e-10, leaf 64",
+            "rhs_per_step": cfg.nrhs,
+            "step": "refine -> compress_update -> els_build -> els_solve (static HBS inverse built once, excluded)",
+            "l2": "inputs re-streamed each step (per-step working set > L2)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
 def build_problem(cfg, sb):
     curve = sb.star(cfg.prongs, cfg.amplitude, cfg.a) if cfg.kind == "star" else sb.ellipse(cfg.a, cfg.b)
     g0 = sb.panelize(curve, cfg.n_panels, cfg.q)
@@ -158,8 +168,13 @@ def run_ours(args, rank, world, local_rank):
     nrhs = G.shape[1]
     stream = torch.cuda.ExternalStream(sb.api.lib().sbx_stream())
     G_dev = torch.from_numpy(np.ascontiguousarray(G)).cuda()  # rows x nrhs (C order)
-    G_pin = torch.from_numpy(np.ascontiguousarray(G)).pin_memory()
-    out_pin = torch.empty_like(G_pin).pin_memory()
+    # e2e: the drop-in caller path -- column-major HOST buffers (pinned) handed
+    # to sbx_els_solve, which copies them in, solves and copies the density
+    # back before returning (host<->device copies inside the timed region)
+    rows = G.shape[0]
+    G_host = torch.empty((nrhs, rows), dtype=torch.float64).pin_memory().numpy().T  # F-order view
+    G_host[:] = G
+    tau_host = torch.empty((nrhs, rows), dtype=torch.float64).pin_memory().numpy().T
 
     state = {}
 
@@ -167,12 +182,11 @@ def run_ours(args, rank, world, local_rank):
         g1, plan = sb.refine(g0, panels, cfg.m)
         upd = sb.compress_update(g0, g1, plan, cfg.eps, seed=cfg.seed)
         els = sb.els_build(h, g0, g1, plan, upd)
-        with torch.cuda.stream(stream):
-            if e2e:
-                gd = G_pin.to("cuda", non_blocking=True)
-                tau = sb.els_solve(els, gd)
-                out_pin.copy_(tau, non_blocking=True)
-            else:
+        if e2e:
+            sb.els_solve_into(els, G_host, tau_host)  # sbx_els_solve on host pointers (library stream)
+            tau = tau_host
+        else:
+            with torch.cuda.stream(stream):
                 tau = sb.els_solve(els, G_dev)
         state["els"], state["upd"], state["tau"] = els, upd, tau
 
@@ -224,25 +238,54 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * t_dev / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: star r=1+0.3cos5t, 1024x16 nodes (32768 unknowns), "
-                               f"refine 16 panels m=16, 64 RHS, eps 1e-10, leaf 64",
-                   "rhs_per_step": nrhs, "steps_per_s": round(world * args.steps / t_dev, 3),
-                   "t_static_s": round(t_static, 4), "phase_ms": ph,
-                   "k": state["upd"].info()["k"], "l2": "inputs re-streamed each step (> L2 per step)",
-                   "parallelism": f"replicas x{world}", "wall_s": round(wall, 3)},
-        "e2e": {"value": round(e2e_value, 3), "unit": UNIT,
-                "h2d_bytes_per_step": int(G_pin.numel() * 8),
-                "d2h_bytes_per_step": int(out_pin.numel() * 8)},
+        "config": workload_config(cfg, world),
+        "details": {"steps_per_s": round(world * args.steps / t_dev, 3), "t_static_s": round(t_static, 4),
+                    "phase_ms": ph, "k": state["upd"].info()["k"], "wall_s": round(wall, 3)},
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "path": "sbx_els_solve with host pointers",
+                "h2d_bytes_per_step": int(G_host.size * 8),
+                "d2h_bytes_per_step": int(tau_host.size * 8)},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "roofline": roof,
     }
+    if world == 1:
+        line["step_dominant"] = step_profile(sb, torch, stream, step, 1e3 * t_dev / args.steps)
     if not args.no_apply_bench and world == 1:
         line["woodbury_build"] = roofline_woodbury(sb, torch, stream, g0, h, panels, cfg)
         line["apply_microbench"] = apply_microbench(sb, torch, stream)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, G.shape[1], threads=1)
     return line
+
+
+def step_profile(sb, torch, stream, step, ms_step, reps=3):
+    """The kernel family that dominates a step: the batched CPQR launches of
+    the interpolative decompositions ("id_factor": every engine launch of
+    the update's row IDs and the A_pp HBS build, CUDA events around each
+    launch on its stream).  Algorithmic flops = 4 per trailing-block entry
+    of each pivoted Householder step actually taken (sum over problems of
+    sum_{j<steps} 4 (M - j)(n - j)); achieved = those flops / the family's
+    summed launch time; share = that time / the device step time.  The
+    step's sweep kernels are listed beside it for comparison."""
+    sb.api.kernel_timing(True)
+    for name in ("id_factor", "sweep_flow_dmma", "sweep_flow_gemv"):
+        sb.api.kernel_time(name)
+    sb.api.kernel_flops("id_factor")
+    for _ in range(reps):
+        step(False)
+    torch.cuda.synchronize()
+    ms, cnt = sb.api.kernel_time("id_factor")
+    fl = sb.api.kernel_flops("id_factor")
+    sw = {n: sb.api.kernel_time(n) for n in ("sweep_flow_dmma", "sweep_flow_gemv")}
+    sb.api.kernel_timing(False)
+    fp64 = measured_fp64_peak()["value"]
+    ach = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    return {"kernel": "id_factor (batched CPQR engines: cpqr_onchip / tsqr_quad / cpqr_reg / qr)",
+            "bound": "tensor", "achieved": round(ach, 4), "peak": fp64, "unit": "TFLOP/s",
+            "frac": round(ach / fp64, 4), "ms_per_step": round(ms / reps, 3),
+            "launches_per_step": cnt // reps, "share_of_step": round(ms / reps / ms_step, 3),
+            "algorithmic_flops_per_step": fl / reps,
+            "sweeps_ms_per_step": {n: round(v[0] / reps, 3) for n, v in sw.items()}}
 
 
 def _kernel_ms(sb, torch, stream, name, fn, reps=10):
@@ -434,9 +477,12 @@ def _oracle_step(cfg, po, o0, a0, oh, panels, srcs):
     return oe.solve(OG)
 
 
-def cpu_baseline(cfg, nrhs, threads=1, steps=1):
+def cpu_baseline(cfg, nrhs, threads=1, steps=1, warmup=0):
     """The oracle (C++ restatement of the reference's serial path) on this
-    host's cores: `threads` independent refined-wall steps in parallel."""
+    host's cores: `steps` independent refined-wall steps on a pool of
+    `threads` host threads (one step per thread at a time), after `warmup`
+    untimed steps; the static HBS inverse is built once beforehand."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import pyoracle as po
     po.build()
     o0, a0 = _oracle_problem(cfg, po)
@@ -446,40 +492,44 @@ def cpu_baseline(cfg, nrhs, threads=1, steps=1):
     panels = cfg.refine_panels(o0.nodes())
     srcs = cfg.sources()
 
-    def work():
-        for _ in range(steps):
-            _oracle_step(cfg, po, o0, a0, oh, panels, srcs)
+    def one(_):
+        _oracle_step(cfg, po, o0, a0, oh, panels, srcs)
 
-    t1 = time.perf_counter()
-    ths = [threading.Thread(target=work) for _ in range(threads)]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
-    dt = time.perf_counter() - t1
-    value = threads * steps * nrhs / dt
+    threads = max(1, min(threads, steps))
+    with ThreadPoolExecutor(max_workers=threads) as pool:
+        list(pool.map(one, range(warmup)))
+        t1 = time.perf_counter()
+        list(pool.map(one, range(steps)))
+        dt = time.perf_counter() - t1
+    value = steps * nrhs / dt
     return {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{threads * steps} full refined-wall step(s) of {cfg.name} "
-                      f"({nrhs} RHS each), {dt:.1f} s; static HBS excluded ({t_static:.1f} s)",
+            "sample": f"{steps} full refined-wall step(s) of {cfg.name} ({nrhs} RHS each) on {threads} host "
+                      f"thread(s), {warmup} warm-up step(s), {dt:.1f} s timed; static HBS excluded "
+                      f"({t_static:.1f} s)",
             "seconds": round(dt, 2), "t_static_s": round(t_static, 2)}
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU path (the oracle port; the C++ reference needs
+    Eigen3, absent here) on all host threads: --warmup untimed steps, then
+    --steps timed steps, each one full refined-wall step with 64 RHS, run
+    concurrently on a pool of min(cpu_count, steps) threads."""
     if rank != 0:
         return None
     from paper_2108_07205_b200.configs import CONFIGS
     cfg = CONFIGS[args.config]
     threads = max(1, os.cpu_count() or 1)
-    base = cpu_baseline(cfg, cfg.nrhs, threads=threads, steps=1)
-    base_per_step = base["seconds"]
+    base = cpu_baseline(cfg, cfg.nrhs, threads=threads, steps=args.steps, warmup=args.warmup)
     line = {
         "metric": METRIC, "value": base["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * base_per_step, 1), "higher_is_better": True,
+        "ms_per_step": round(1e3 * base["seconds"] / args.steps, 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name} (same as --impl ours)", "rhs_per_step": cfg.nrhs,
-                   "note": "reference C++ needs Eigen3 (absent); its CPU path is timed through "
-                           "the oracle restatement (oracle/), all host threads, one step each"},
+        "config": workload_config(cfg, world),
+        "details": {"note": "reference C++ needs Eigen3 (absent); its serial CPU path is timed through the "
+                            "oracle restatement (oracle/): independent steps on a host thread pool, "
+                            "ms_per_step = timed wall / steps (throughput, not one step's latency)",
+                    "threads": base["cores"], "t_static_s": base["t_static_s"]},
         "impl": "reference",
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": base["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

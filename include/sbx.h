@@ -239,6 +239,10 @@ int64_t sbx_kernel_launches(int reset);
  * milliseconds and launch count since the last reset. */
 int sbx_kernel_timing(int enable);
 int sbx_kernel_time(const char* name, int reset, double* total_ms, int64_t* count);
+/* Algorithmic flops attributed to a timed kernel family while timing is on
+ * ("id_factor": every CPQR launch of the interpolative decompositions, 4
+ * flops per trailing-block entry of each pivoted Householder step taken). */
+int sbx_kernel_flops(const char* name, int reset, double* flops);
 
 /* Device row ID of a host matrix W (m x n, column-major) — idlib.cpp:73-99
  * (row_id; forced >= 0 selects row_id_rank).  engine: 0 auto, 1 one CTA per

@@ -70,6 +70,7 @@ _SIGS = [
     ("sbx_kernel_launches", C.c_int64, [C.c_int]),
     ("sbx_kernel_timing", C.c_int, [C.c_int]),
     ("sbx_kernel_time", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_double), I64P]),
+    ("sbx_kernel_flops", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_double)]),
     ("sbx_row_id", C.c_int, [F64P, I64, I64, C.c_double, I64, C.c_int, I64P, I64P, F64P]),
     ("sbx_geom_create", C.c_int, [C.POINTER(sbx_curve), C.c_int, C.c_int, C.POINTER(VP)]),
     ("sbx_geom_add_holes", C.c_int,

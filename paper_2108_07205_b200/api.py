@@ -500,6 +500,23 @@ def els_solve(s: ElsSolver, g_n):
     return _els_call(lib().sbx_els_solve, s, g_n, i["n_k"] + i["n_p"])
 
 
+def els_solve_into(s: ElsSolver, g_n: np.ndarray, tau_n: np.ndarray, stream=None):
+    """sbx_els_solve on caller-owned HOST buffers (the drop-in caller path):
+    g_n, tau_n are column-major (n_k + n_p) x nrhs float64 arrays (pinned
+    memory makes the library's copies asynchronous DMA); returns once tau_n
+    holds the density."""
+    i = s.info()
+    rows = i["n_k"] + i["n_p"]
+    for a in (g_n, tau_n):
+        if a.dtype != np.float64 or a.ndim != 2 or a.shape[0] != rows or not a.flags.f_contiguous:
+            raise ValueError("els_solve_into: expected column-major float64 (n_k + n_p) x nrhs arrays")
+    if g_n.shape != tau_n.shape:
+        raise ValueError("els_solve_into: shape mismatch")
+    check(lib().sbx_els_solve(s.ptr, VP(g_n.ctypes.data), rows, g_n.shape[1], VP(tau_n.ctypes.data), rows, 0,
+                              VP(stream) if stream else VP()))
+    return tau_n
+
+
 def els_solve_raw(s: ElsSolver, g_ext, transpose: bool = False):
     """els.cpp:147-152 on extended (kept, cut, added) vectors; transpose:
     els_solve_raw_t (els.cpp:154-163)."""
@@ -590,6 +607,13 @@ def kernel_time(name: str, reset: bool = True):
     cnt = C.c_int64(0)
     check(lib().sbx_kernel_time(name.encode(), int(reset), C.byref(ms), C.byref(cnt)))
     return ms.value, cnt.value
+
+
+def kernel_flops(name: str, reset: bool = True) -> float:
+    """Algorithmic flops attributed to a timed kernel family since the last reset."""
+    f = C.c_double(0.0)
+    check(lib().sbx_kernel_flops(name.encode(), int(reset), C.byref(f)))
+    return f.value
 
 
 def gather_kept_added(plan: RefinementPlan, g_new):

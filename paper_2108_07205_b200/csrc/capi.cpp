@@ -106,6 +106,10 @@ int sbx_kernel_time(const char* name, int reset, double* total_ms, int64_t* coun
   });
 }
 
+int sbx_kernel_flops(const char* name, int reset, double* flops) {
+  return guard([&] { *flops = sbx::ktimer_flops(name, reset != 0); });
+}
+
 int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
                int64_t* k, int64_t* J, double* P) {
   return guard([&] {

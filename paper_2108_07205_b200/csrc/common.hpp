@@ -53,6 +53,10 @@ void ktimer_record(const char* name, cudaEvent_t begin, cudaEvent_t end);
 // Total milliseconds and launch count of `name` since the last reset
 // (synchronises on the recorded events).
 double ktimer_total(const char* name, bool reset, std::int64_t* count);
+// Algorithmic flops attributed to `name` while timing is on (reset with
+// ktimer_flops(name, true)).
+void ktimer_add_flops(const char* name, double flops);
+double ktimer_flops(const char* name, bool reset);
 class KernelTimer {
  public:
   KernelTimer(const char* name, cudaStream_t s);

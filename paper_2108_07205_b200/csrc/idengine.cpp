@@ -55,6 +55,7 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
+  KernelTimer kt("id_factor", s);  // every CPQR engine launch of the batch (bench: step-dominant family)
   std::vector<QrJob> jobs, big, chip, clus, reg, strm;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
@@ -233,7 +234,25 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
   std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
   if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);
   if (!hdiag.empty()) d_diag_.download(hdiag.data(), hdiag.size(), s);
+  std::vector<int> hsteps;
+  if (ktimer_on() && np) {
+    hsteps.resize(np);
+    d_steps_.download(hsteps.data(), np, s);
+  }
   SBX_CUDA(cudaStreamSynchronize(s));
+  if (!hsteps.empty()) {
+    // algorithmic work of the pivoted Householder steps actually taken:
+    // step j updates the (M-j) x (n-j) trailing block, 4 flops per entry
+    // (column dot product + rank-1 update), whatever engine ran it
+    double f = 0.0;
+    for (size_t p = 0; p < np; ++p) {
+      const auto& pr = probs[p];
+      if (pr.M == 0 || pr.n == 0) continue;
+      const int st = std::min({hsteps[p], pr.M, pr.n});
+      for (int j = 0; j < st; ++j) f += 4.0 * double(pr.M - j) * double(pr.n - j);
+    }
+    ktimer_add_flops("id_factor", f);
+  }
   diag_.assign(np, {});
   perm_.assign(np, {});
   for (size_t p = 0; p < np; ++p) {

@@ -82,6 +82,23 @@ double ktimer_total(const char* name, bool reset, std::int64_t* count) {
   return ms;
 }
 
+namespace {
+std::map<std::string, double> g_kflops;
+}
+
+void ktimer_add_flops(const char* name, double flops) {
+  if (!ktimer_on()) return;
+  std::lock_guard<std::mutex> lk(g_ktimer_mu);
+  g_kflops[name] += flops;
+}
+
+double ktimer_flops(const char* name, bool reset) {
+  std::lock_guard<std::mutex> lk(g_ktimer_mu);
+  const double f = g_kflops[name];
+  if (reset) g_kflops[name] = 0.0;
+  return f;
+}
+
 KernelTimer::KernelTimer(const char* name, cudaStream_t s) : name_(name), s_(s) {
   if (!ktimer_on()) return;
   SBX_CUDA(cudaEventCreate(&b_));
