@@ -231,6 +231,19 @@ int sbx_els_conditioning(sbx_els e, int iters, double* out);
 /* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
 int sbx_els_xw(sbx_els e, double* X, double* W);
 
+/* ---------------------------------------------------------- dense interchange
+ * dump_matrix / load_matrix (nystrom.cpp:450-477; nystrom.hpp:142-143):
+ * u32 rows, u32 cols, then the entries row by row as doubles.  Host buffers
+ * are column-major with leading dimension ld (>= rows). */
+int sbx_dump_matrix(const char* path, const double* m, int64_t rows, int64_t cols, int64_t ld);
+int sbx_load_matrix_dims(const char* path, int64_t* rows, int64_t* cols);
+int sbx_load_matrix(const char* path, double* out, int64_t ld);
+/* The update factors L (n_ext x k) and R (k x n_ext) as two dump_matrix
+ * files, and back: tier-1 hand-over of externally computed factors (e.g. the
+ * reference's) into sbx_els_build, like sbx_update_from_factors. */
+int sbx_update_dump(sbx_update u, const char* path_L, const char* path_R);
+int sbx_update_load(sbx_plan plan, const char* path_L, const char* path_R, sbx_update* out);
+
 /* ---------------------------------------------------------- diagnostics
  * Number of sbx kernels launched since the last reset (bench evidence). */
 int64_t sbx_kernel_launches(int reset);

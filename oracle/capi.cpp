@@ -334,6 +334,23 @@ int orc_update_set(void* u, const double* L, const double* R, std::int64_t n_ext
   });
 }
 
+// nystrom.cpp:450-477 interchange (column-major host buffers on this side)
+int orc_dump_matrix(const char* path, const double* m, std::int64_t rows, std::int64_t cols) {
+  return guard([&] { dump_matrix(path, from_ptr(m, rows, cols)); });
+}
+
+int orc_load_matrix_dims(const char* path, std::int64_t* rows, std::int64_t* cols) {
+  return guard([&] {
+    const Mat m = load_matrix(path);
+    *rows = m.r;
+    *cols = m.c;
+  });
+}
+
+int orc_load_matrix(const char* path, double* out) {
+  return guard([&] { to_ptr(load_matrix(path), out); });
+}
+
 int orc_block_eval_full(void* old_a, void* new_a, void* plan, int block, double* out) {
   return guard([&] {
     BlockSource src(static_cast<AsmH*>(old_a)->a, static_cast<AsmH*>(new_a)->a,

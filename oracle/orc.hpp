@@ -301,6 +301,8 @@ std::vector<StokesletSource> ring_sources(int n, V2 center, double radius);
 std::vector<double> boundary_data(const Discretization& d,
                                   const std::vector<StokesletSource>& s, double mu);
 V2 field_velocity(const std::vector<StokesletSource>& s, double mu, V2 p);
+void dump_matrix(const std::string& path, const Mat& m);  // nystrom.cpp:450-461
+Mat load_matrix(const std::string& path);                  // nystrom.cpp:463-477
 std::vector<V2> evaluate_velocity(const Discretization& d, const Formulation& f,
                                   const std::vector<double>& tau,
                                   const std::vector<V2>& targets);

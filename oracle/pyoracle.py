@@ -353,6 +353,21 @@ class Update(_Handle):
                                   L.shape[0], L.shape[1]))
 
 
+def dump_matrix(path, m):
+    """nystrom.cpp:450-461: u32 rows, u32 cols, row-major doubles."""
+    a = _fortran(np.atleast_2d(m))
+    _chk(lib().orc_dump_matrix(str(path).encode(), a.ctypes.data_as(F64P), a.shape[0], a.shape[1]))
+
+
+def load_matrix(path):
+    """nystrom.cpp:463-477."""
+    r, c = C.c_int64(), C.c_int64()
+    _chk(lib().orc_load_matrix_dims(str(path).encode(), C.byref(r), C.byref(c)))
+    out = np.zeros((r.value, c.value), order="F")
+    _chk(lib().orc_load_matrix(str(path).encode(), out.ctypes.data_as(F64P)))
+    return out
+
+
 def block_eval_full(old_asm, new_asm, plan, block):
     nk, nc, npp = plan.sizes()
     size = {"k": 2 * nk, "c": 2 * nc, "p": 2 * npp}

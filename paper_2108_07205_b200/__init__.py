@@ -11,7 +11,7 @@ from .api import (  # noqa: F401
     ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,
     evaluate_solution,
     gather_kept_added, hbs_apply, hbs_compress, hbs_invert, hbs_load, hbs_save, hbs_solve, init, kernel_launches, panelize, refine, row_id,
-    star, submatrix, update_from_factors,
+    star, submatrix, update_from_factors, update_dump, update_load, dump_matrix, load_matrix,
 )
 from ._sbx import (  # noqa: F401
     ConvergenceError, CudaError, GeometryError, ProxyViolationError, SbxError, SingularMatrixError,

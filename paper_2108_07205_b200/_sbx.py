@@ -109,6 +109,11 @@ _SIGS = [
     ("sbx_update_info", C.c_int, [VP, I64P]),
     ("sbx_update_factor", C.c_int, [VP, C.c_int, F64P]),
     ("sbx_update_from_factors", C.c_int, [VP, F64P, F64P, I64, I64, C.POINTER(VP)]),
+    ("sbx_dump_matrix", C.c_int, [C.c_char_p, F64P, I64, I64, I64]),
+    ("sbx_load_matrix_dims", C.c_int, [C.c_char_p, I64P, I64P]),
+    ("sbx_load_matrix", C.c_int, [C.c_char_p, F64P, I64]),
+    ("sbx_update_dump", C.c_int, [VP, C.c_char_p, C.c_char_p]),
+    ("sbx_update_load", C.c_int, [VP, C.c_char_p, C.c_char_p, C.POINTER(VP)]),
     ("sbx_els_build", C.c_int, [VP, VP, VP, VP, VP, C.c_int, C.c_double, C.POINTER(VP)]),
     ("sbx_els_destroy", C.c_int, [VP]),
     ("sbx_els_info", C.c_int, [VP, I64P]),

@@ -411,6 +411,34 @@ def update_from_factors(plan: RefinementPlan, L, R) -> LowRankUpdate:
     return LowRankUpdate(out)
 
 
+def update_dump(u: LowRankUpdate, path_L, path_R):
+    """L and R as dump_matrix files (nystrom.cpp:450-461)."""
+    check(lib().sbx_update_dump(u.ptr, str(path_L).encode(), str(path_R).encode()))
+
+
+def update_load(plan: RefinementPlan, path_L, path_R) -> LowRankUpdate:
+    """An update from dumped L, R (tier-1 hand-over of external factors)."""
+    out = VP()
+    check(lib().sbx_update_load(plan.ptr, str(path_L).encode(), str(path_R).encode(), C.byref(out)))
+    return LowRankUpdate(out)
+
+
+def dump_matrix(path, m):
+    """nystrom.cpp:450-461 (host; no device work)."""
+    a = np.asfortranarray(np.atleast_2d(np.asarray(m, dtype=np.float64)))
+    check(lib().sbx_dump_matrix(str(path).encode(), a.ctypes.data_as(F64P), a.shape[0], a.shape[1],
+                                max(a.shape[0], 1)))
+
+
+def load_matrix(path) -> np.ndarray:
+    """nystrom.cpp:463-477 (host; no device work)."""
+    r, c = C.c_int64(), C.c_int64()
+    check(lib().sbx_load_matrix_dims(str(path).encode(), C.byref(r), C.byref(c)))
+    out = np.zeros((r.value, c.value), order="F")
+    check(lib().sbx_load_matrix(str(path).encode(), out.ctypes.data_as(F64P), max(r.value, 1)))
+    return out
+
+
 class ElsSolver(_Handle):
     """els.hpp:17-37.  Keeps a reference to the HBS handle it solves with."""
     _destroy = "sbx_els_destroy"

@@ -9,6 +9,7 @@
 #include "hbs.hpp"
 #include "hbs_build.hpp"
 #include "idengine.hpp"
+#include "matio.hpp"
 #include "sbx.h"
 #include "update.hpp"
 
@@ -406,6 +407,52 @@ int sbx_update_factor(sbx_update u, int which, double* out) {
   return guard([&] {
     sbx::require(u && u->u, "null update handle");
     sbx::update_download(*u->u, which, out, sbx::lib_stream());
+  });
+}
+
+int sbx_dump_matrix(const char* path, const double* m, int64_t rows, int64_t cols, int64_t ld) {
+  return guard([&] { sbx::dump_matrix(path, m, rows, cols, ld); });
+}
+
+int sbx_load_matrix_dims(const char* path, int64_t* rows, int64_t* cols) {
+  return guard([&] {
+    const sbx::HMat m = sbx::load_matrix(path);
+    *rows = m.r;
+    *cols = m.c;
+  });
+}
+
+int sbx_load_matrix(const char* path, double* out, int64_t ld) {
+  return guard([&] {
+    const sbx::HMat m = sbx::load_matrix(path);
+    sbx::require(ld >= m.r, "load_matrix: leading dimension smaller than rows");
+    for (int64_t j = 0; j < m.c; ++j)
+      for (int64_t i = 0; i < m.r; ++i) out[i + j * ld] = m.a[size_t(i + j * m.r)];
+  });
+}
+
+int sbx_update_dump(sbx_update u, const char* path_L, const char* path_R) {
+  return guard([&] {
+    sbx::require(u && u->u, "null update handle");
+    const auto& x = *u->u;
+    const int64_t n = x.n_ext(), k = x.k;
+    std::vector<double> L(size_t(n * k)), R(size_t(k * n));
+    if (k > 0) {
+      sbx::update_download(x, 0, L.data(), sbx::lib_stream());
+      sbx::update_download(x, 1, R.data(), sbx::lib_stream());
+    }
+    sbx::dump_matrix(path_L, L.data(), n, k, std::max<int64_t>(n, 1));
+    sbx::dump_matrix(path_R, R.data(), k, n, std::max<int64_t>(k, 1));
+  });
+}
+
+int sbx_update_load(sbx_plan plan, const char* path_L, const char* path_R, sbx_update* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    const sbx::HMat L = sbx::load_matrix(path_L), R = sbx::load_matrix(path_R);
+    sbx::require(L.c == R.r && L.r == R.c, "update_load: L (n_ext x k) and R (k x n_ext) do not match");
+    *out = new sbx_update_s{sbx::update_from_factors(*plan->p, L.a.data(), R.a.data(), L.r, L.c,
+                                                     sbx::lib_stream())};
   });
 }
 

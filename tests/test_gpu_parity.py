@@ -255,3 +255,34 @@ def test_collapsed_top_auto(tmp_path):
         tops[mode] = int(r.stdout.split("top")[-1])
     assert tops["auto"] >= 2 and tops["off"] == 0, tops
     assert rel(out["auto"], out["off"]) < 1e-12
+
+
+def test_tier1_dumped_update_factors_match_oracle(sb, po, tmp_path):
+    """SURVEY 8(c) tier 1 for the ELS: the oracle's HBS1 inverse and its
+    update factors L, R handed over in the reference's dump_matrix format
+    (nystrom.cpp:450-477) -> device els_build / els_solve agree with the
+    oracle's els_solve to 1e-12 (identical factors, different rounding)."""
+    eps = 1e-10
+    o0 = po.Geom.create(po.STAR, 12, prongs=5, amplitude=0.3)
+    o1, op = o0.refine([3, 4], 4)
+    a0, a1 = po.Assembler.create(o0), po.Assembler.create(o1)
+    oh = po.Hbs.compress(a0, eps).invert()
+    ou = po.Update.compress(a0, a1, op, eps)
+    oe = po.Els.build(oh, a0, a1, op, ou)
+    oh.save(tmp_path / "a.hbs1")
+    f = ou.factors()
+    po.dump_matrix(tmp_path / "L.mat", f["L"])
+    po.dump_matrix(tmp_path / "R.mat", f["R"])
+    g0 = sb.panelize(sb.star(5, 0.3), 12, 16)
+    g1, plan = sb.refine(g0, [3, 4], 4)
+    h = sb.hbs_load(tmp_path / "a.hbs1")
+    u = sb.update_load(plan, tmp_path / "L.mat", tmp_path / "R.mat")
+    assert u.k == ou.info()["k"]
+    e = sb.els_build(h, g0, g1, plan, u)
+    src = po.ring_sources(4, (0, 0), 3.0)
+    G = np.stack([po.gather_kept_added(op.maps(), o1.boundary_data(s)) for s in (src, src[::-1])], 1)
+    assert rel(sb.els_solve(e, G), oe.solve(G)) < 1e-12
+    # and back out: the device's copy of the factors dumps to the same files
+    sb.update_dump(u, tmp_path / "L2.mat", tmp_path / "R2.mat")
+    assert (tmp_path / "L.mat").read_bytes() == (tmp_path / "L2.mat").read_bytes()
+    assert (tmp_path / "R.mat").read_bytes() == (tmp_path / "R2.mat").read_bytes()
