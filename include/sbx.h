@@ -58,6 +58,9 @@ typedef struct sbx_hbs_s* sbx_hbs;       /* HbsOperator (device)     */
 typedef struct sbx_update_s* sbx_update; /* LowRankUpdate (device)   */
 typedef struct sbx_els_s* sbx_els;       /* ElsSolver (device)       */
 typedef struct sbx_app_s* sbx_app;       /* A_pp inverse (device)    */
+typedef struct sbx_update_cache_s* sbx_update_cache; /* snapshot update cache */
+typedef struct sbx_comm_s* sbx_comm;     /* communicator set (multi-GPU) */
+typedef struct sbx_els_shard_s* sbx_els_shard; /* ElsSolver on a subtree partition */
 
 /* CurveParams (geometry.hpp:14-26). */
 typedef struct {
@@ -230,6 +233,58 @@ int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out);
 int sbx_els_conditioning(sbx_els e, int iters, double* out);
 /* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
 int sbx_els_xw(sbx_els e, double* X, double* W);
+
+/* ---------------------------------------------------------- snapshot update cache
+ * run_snapshot_batch's cache (scenario.cpp:836-899): updates are determined
+ * by the refinement plan alone, so identical (panel ids, m) -- at the same
+ * eps, formulation, mu and seed -- share one compression.  On a miss the
+ * update is compressed exactly as sbx_update_compress does and stored; on a
+ * hit the stored update is returned (*hit = 1).  Returned handles are
+ * independent (destroy each); the cache keeps its own reference. */
+int sbx_update_cache_create(sbx_update_cache* out);
+int sbx_update_cache_destroy(sbx_update_cache c);
+int sbx_update_cache_compress(sbx_update_cache c, sbx_geom old_g, sbx_geom new_g, sbx_plan plan,
+                              const int64_t* panel_ids, int64_t n_panels, int m, int formulation, double mu,
+                              double eps, uint64_t seed, sbx_update* out, int* hit);
+int sbx_update_cache_stats(sbx_update_cache c, int64_t* entries, int64_t* hits, int64_t* misses);
+
+/* ---------------------------------------------------------- multi-GPU
+ * One process per GPU.  A communicator set is created once per rank from a
+ * 128-byte NCCL unique id made by rank 0 and distributed by the caller (any
+ * side channel); call it with the rank's device current (sbx_init).  NCCL is
+ * loaded at run time (an NCCL already in the process, e.g. torch's, is
+ * reused).  The loopback variant makes `world` members of one in-process
+ * group (member r driven by its own host thread, exchanges by device copies):
+ * the same protocol on one GPU, for tests and emulation.
+ *
+ * Subtree partition: for world = G = 2^g, rank p owns the subtree rooted at
+ * the p-th BFS node of depth g, i.e. old-mesh rows [row0, row1) of
+ * sbx_hbs_shard_info.  sbx_hbs_solve_sharded: local up-sweep, all-gather of
+ * the G subtree-root hats (the only exchange), top levels redundantly, local
+ * down-sweep; b_local / x_local are this rank's rows (column-major). */
+int sbx_comm_unique_id(uint8_t* id128);
+int sbx_comm_create(const uint8_t* id128, int world, int rank, sbx_comm* out);
+int sbx_comm_create_loopback(int world, sbx_comm* members);
+int sbx_comm_destroy(sbx_comm c);
+int sbx_comm_info(sbx_comm c, int* world, int* rank);
+int sbx_hbs_solve_sharded(sbx_hbs h, sbx_comm c, const double* b_local, int64_t ldb, int64_t nrhs, double* x_local,
+                          int64_t ldx, int flags, void* stream);
+/* Woodbury on the same ownership (els.cpp:80-179): X = Atilde^{-1} L and the
+ * columns of R follow the row ownership, A_pp lives on rank 0, R X and R y
+ * are all-reduced, W^{-1} is formed on every rank (same rcond gate and
+ * message as sbx_els_build).  info: row0, row1, n_p on this rank (0 except
+ * rank 0), k, n_ext, world, rank.  rows: the ext row of each owned row, in
+ * old-mesh order (rows = row1 - row0).  solve: g_local / y_local are the
+ * owned rows in that order, g_p / y_p the added rows (rank 0 only; null
+ * elsewhere). */
+int sbx_els_shard_build(sbx_hbs a_oo, sbx_comm c, sbx_geom old_g, sbx_geom new_g, sbx_plan plan, sbx_update upd,
+                        int formulation, double mu, void* stream, sbx_els_shard* out);
+int sbx_els_shard_info(sbx_els_shard e, int64_t* info);
+int sbx_els_shard_rows(sbx_els_shard e, int64_t* ext_rows);
+int sbx_els_shard_solve(sbx_els_shard e, const double* g_local, int64_t ldg, const double* g_p, int64_t ldgp,
+                        int64_t nrhs, double* y_local, int64_t ldy, double* y_p, int64_t ldyp, int flags,
+                        void* stream);
+int sbx_els_shard_destroy(sbx_els_shard e);
 
 /* ---------------------------------------------------------- dense interchange
  * dump_matrix / load_matrix (nystrom.cpp:450-477; nystrom.hpp:142-143):

@@ -6,7 +6,7 @@ kernels behind the C-ABI of ``include/sbx.h``).
 """
 from .api import (  # noqa: F401
     CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR,
-    AppBlockSolver, CurveParams, Discretization, ElsSolver, HbsOperator, HbsOptions, LowRankUpdate,
+    AppBlockSolver, UpdateCache, CurveParams, Discretization, ElsSolver, HbsOperator, HbsOptions, LowRankUpdate,
     RefinementPlan, add_holes, app_build, boundary_data, circle, coarsen, compress_update, density_on_refined,
     ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,
     evaluate_solution,

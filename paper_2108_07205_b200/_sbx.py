@@ -110,6 +110,22 @@ _SIGS = [
     ("sbx_update_factor", C.c_int, [VP, C.c_int, F64P]),
     ("sbx_update_from_factors", C.c_int, [VP, F64P, F64P, I64, I64, C.POINTER(VP)]),
     ("sbx_dump_matrix", C.c_int, [C.c_char_p, F64P, I64, I64, I64]),
+    ("sbx_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("sbx_comm_create", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.POINTER(VP)]),
+    ("sbx_comm_create_loopback", C.c_int, [C.c_int, C.POINTER(VP)]),
+    ("sbx_comm_destroy", C.c_int, [VP]),
+    ("sbx_comm_info", C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("sbx_hbs_solve_sharded", C.c_int, [VP, VP, VP, I64, I64, VP, I64, C.c_int, VP]),
+    ("sbx_els_shard_build", C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int, C.c_double, VP, C.POINTER(VP)]),
+    ("sbx_els_shard_info", C.c_int, [VP, I64P]),
+    ("sbx_els_shard_rows", C.c_int, [VP, I64P]),
+    ("sbx_els_shard_solve", C.c_int, [VP, VP, I64, VP, I64, I64, VP, I64, VP, I64, C.c_int, VP]),
+    ("sbx_els_shard_destroy", C.c_int, [VP]),
+    ("sbx_update_cache_create", C.c_int, [C.POINTER(VP)]),
+    ("sbx_update_cache_destroy", C.c_int, [VP]),
+    ("sbx_update_cache_compress", C.c_int, [VP, VP, VP, VP, I64P, I64, C.c_int, C.c_int, C.c_double,
+                                            C.c_double, C.c_uint64, C.POINTER(VP), C.POINTER(C.c_int)]),
+    ("sbx_update_cache_stats", C.c_int, [VP, I64P, I64P, I64P]),
     ("sbx_load_matrix_dims", C.c_int, [C.c_char_p, I64P, I64P]),
     ("sbx_load_matrix", C.c_int, [C.c_char_p, F64P, I64]),
     ("sbx_update_dump", C.c_int, [VP, C.c_char_p, C.c_char_p]),

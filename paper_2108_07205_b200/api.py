@@ -411,6 +411,34 @@ def update_from_factors(plan: RefinementPlan, L, R) -> LowRankUpdate:
     return LowRankUpdate(out)
 
 
+class UpdateCache(_Handle):
+    """run_snapshot_batch's update cache (scenario.cpp:836-899): identical
+    (panel ids, m) at the same eps / formulation / mu / seed share one
+    compression."""
+    _destroy = "sbx_update_cache_destroy"
+
+    def __init__(self):
+        _ensure()
+        out = VP()
+        check(lib().sbx_update_cache_create(C.byref(out)))
+        super().__init__(out)
+
+    def compress(self, d_old: Discretization, d_new: Discretization, plan: RefinementPlan, panel_ids, m: int,
+                 eps: float = 1e-10, formulation=INTERIOR_DIRICHLET, mu: float = 1.0, seed: int = 0):
+        """(update, hit) -- compress_update on a miss, the cached update on a hit."""
+        ids = np.ascontiguousarray(np.asarray(panel_ids, dtype=np.int64))
+        out, hit = VP(), C.c_int(0)
+        check(lib().sbx_update_cache_compress(self.ptr, d_old.ptr, d_new.ptr, plan.ptr, ids.ctypes.data_as(I64P),
+                                              len(ids), int(m), formulation, mu, eps, C.c_uint64(seed),
+                                              C.byref(out), C.byref(hit)))
+        return LowRankUpdate(out), bool(hit.value)
+
+    def stats(self) -> dict:
+        e, h, m = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().sbx_update_cache_stats(self.ptr, C.byref(e), C.byref(h), C.byref(m)))
+        return {"entries": e.value, "hits": h.value, "misses": m.value}
+
+
 def update_dump(u: LowRankUpdate, path_L, path_R):
     """L and R as dump_matrix files (nystrom.cpp:450-461)."""
     check(lib().sbx_update_dump(u.ptr, str(path_L).encode(), str(path_R).encode()))

@@ -1,6 +1,9 @@
 // The sbx C-ABI (include/sbx.h): opaque handles over the host/device
 // objects, exceptions mapped to status codes + sbx_last_error().
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 
 #include "els.hpp"
@@ -10,6 +13,7 @@
 #include "hbs_build.hpp"
 #include "idengine.hpp"
 #include "matio.hpp"
+#include "multigpu.hpp"
 #include "sbx.h"
 #include "update.hpp"
 
@@ -23,13 +27,29 @@ struct sbx_hbs_s {
   std::unique_ptr<sbx::HbsOp> h;
 };
 struct sbx_update_s {
-  std::unique_ptr<sbx::Update> u;
+  std::shared_ptr<sbx::Update> u;  // shared with an update cache entry
+};
+// Snapshot update cache (scenario.cpp:836-899): updates are determined by the
+// refinement plan alone, so identical (panel ids, m) -- at the same
+// tolerance, formulation and seed -- share one compression.
+struct sbx_update_cache_s {
+  std::mutex mu;
+  std::map<std::tuple<std::vector<int64_t>, int, double, int, double, uint64_t>, std::shared_ptr<sbx::Update>> map;
+  int64_t hits = 0, misses = 0;
 };
 struct sbx_els_s {
   std::unique_ptr<sbx::Els> e;
 };
 struct sbx_app_s {
   std::shared_ptr<sbx::AppSolver> a;
+};
+
+struct sbx_comm_s {
+  std::unique_ptr<sbx::Collective> c;
+};
+struct sbx_els_shard_s {
+  std::unique_ptr<sbx::ElsShard> e;
+  std::shared_ptr<sbx::Update> keep_update;  // L, R read by the build only; kept for symmetry with sbx_els
 };
 
 namespace {
@@ -392,6 +412,50 @@ int sbx_update_compress(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formu
   });
 }
 
+int sbx_update_cache_create(sbx_update_cache* out) {
+  return guard([&] { *out = new sbx_update_cache_s; });
+}
+
+int sbx_update_cache_destroy(sbx_update_cache c) { return destroy_handle(c); }
+
+int sbx_update_cache_compress(sbx_update_cache c, sbx_geom old_g, sbx_geom new_g, sbx_plan plan,
+                              const int64_t* panel_ids, int64_t n_panels, int m, int formulation, double mu,
+                              double eps, uint64_t seed, sbx_update* out, int* hit) {
+  return guard([&] {
+    sbx::require(c && plan && plan->p, "null handle");
+    sbx::require(n_panels >= 0 && (n_panels == 0 || panel_ids), "update_cache: bad panel list");
+    auto key = std::make_tuple(std::vector<int64_t>(panel_ids, panel_ids + n_panels), m, eps, formulation, mu,
+                               seed);
+    {
+      std::lock_guard<std::mutex> lk(c->mu);
+      auto it = c->map.find(key);
+      if (it != c->map.end()) {
+        ++c->hits;
+        if (hit) *hit = 1;
+        *out = new sbx_update_s{it->second};
+        return;
+      }
+    }
+    std::shared_ptr<sbx::Update> u = sbx::update_compress_device(G(old_g), G(new_g), *plan->p, formulation, mu,
+                                                                 eps, seed, sbx::lib_stream());
+    std::lock_guard<std::mutex> lk(c->mu);
+    ++c->misses;
+    c->map.emplace(std::move(key), u);
+    if (hit) *hit = 0;
+    *out = new sbx_update_s{std::move(u)};
+  });
+}
+
+int sbx_update_cache_stats(sbx_update_cache c, int64_t* entries, int64_t* hits, int64_t* misses) {
+  return guard([&] {
+    sbx::require(c != nullptr, "null cache handle");
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (entries) *entries = int64_t(c->map.size());
+    if (hits) *hits = c->hits;
+    if (misses) *misses = c->misses;
+  });
+}
+
 int sbx_update_destroy(sbx_update u) { return destroy_handle(u); }
 
 int sbx_update_info(sbx_update u, int64_t* info) {
@@ -630,5 +694,135 @@ int sbx_els_xw(sbx_els e, double* X, double* W) {
     sbx::els_download_xw(*e->e, X, W, sbx::lib_stream());
   });
 }
+
+// ---------------------------------------------------------------- multi-GPU
+namespace {
+sbx::Collective& Cm(sbx_comm c) {
+  sbx::require(c && c->c, "null comm handle");
+  return *c->c;
+}
+
+// Runs f on device blocks: host inputs are staged in, host outputs copied back.
+struct Staged {
+  sbx::DevBuf<double> buf;
+  const double* in(const double* h, int64_t rows, int64_t cols, int64_t ld, bool dev, cudaStream_t s) {
+    if (dev || rows == 0 || cols == 0) return h;
+    buf.resize(size_t(rows * cols));
+    SBX_CUDA(cudaMemcpy2DAsync(buf.get(), size_t(rows) * 8, h, size_t(ld) * 8, size_t(rows) * 8, size_t(cols),
+                               cudaMemcpyHostToDevice, s));
+    return buf.get();
+  }
+  double* out(double* h, int64_t rows, int64_t cols, bool dev) {
+    if (dev || rows == 0 || cols == 0) return h;
+    buf.resize(size_t(rows * cols));
+    return buf.get();
+  }
+  void back(double* h, int64_t rows, int64_t cols, int64_t ld, bool dev, cudaStream_t s) {
+    if (dev || rows == 0 || cols == 0) return;
+    SBX_CUDA(cudaMemcpy2DAsync(h, size_t(ld) * 8, buf.get(), size_t(rows) * 8, size_t(rows) * 8, size_t(cols),
+                               cudaMemcpyDeviceToHost, s));
+  }
+};
+}  // namespace
+
+int sbx_comm_unique_id(uint8_t* id128) {
+  return guard([&] { sbx::nccl_unique_id(id128); });
+}
+
+int sbx_comm_create(const uint8_t* id128, int world, int rank, sbx_comm* out) {
+  return guard([&] { *out = new sbx_comm_s{sbx::make_nccl_collective(id128, world, rank)}; });
+}
+
+int sbx_comm_create_loopback(int world, sbx_comm* members) {
+  return guard([&] {
+    auto g = sbx::make_loopback_group(world);
+    for (int r = 0; r < world; ++r) members[r] = new sbx_comm_s{std::move(g[size_t(r)])};
+  });
+}
+
+int sbx_comm_destroy(sbx_comm c) { return destroy_handle(c); }
+
+int sbx_comm_info(sbx_comm c, int* world, int* rank) {
+  return guard([&] {
+    *world = Cm(c).world();
+    *rank = Cm(c).rank();
+  });
+}
+
+int sbx_hbs_solve_sharded(sbx_hbs h, sbx_comm c, const double* b_local, int64_t ldb, int64_t nrhs, double* x_local,
+                          int64_t ldx, int flags, void* stream) {
+  return guard([&] {
+    const cudaStream_t s = stream_of(stream);
+    sbx::StreamScope scope(s);
+    sbx::HbsOp& op = H(h);
+    sbx::Collective& cm = Cm(c);
+    const sbx::ShardPlans& S = sbx::hbs_shard(op, cm.world(), cm.rank());
+    const int64_t rows = S.row1 - S.row0;
+    sbx::require(nrhs >= 0 && ldb >= rows && ldx >= rows, "hbs_solve_sharded: bad sizes");
+    if (nrhs == 0) return;
+    const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    Staged bi, xo;
+    const double* bd = bi.in(b_local, rows, nrhs, ldb, dev, s);
+    double* xd = xo.out(x_local, rows, nrhs, dev);
+    sbx::hbs_solve_sharded(op, cm, bd, dev ? ldb : rows, nrhs, xd, dev ? ldx : rows, s);
+    xo.back(x_local, rows, nrhs, ldx, dev, s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sbx_els_shard_build(sbx_hbs a_oo, sbx_comm c, sbx_geom old_g, sbx_geom new_g, sbx_plan plan, sbx_update upd,
+                        int formulation, double mu, void* stream, sbx_els_shard* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p && upd && upd->u, "null handle");
+    const cudaStream_t s = stream_of(stream);
+    sbx::StreamScope scope(s);
+    auto e = sbx::els_shard_build(H(a_oo), Cm(c), G(old_g), G(new_g), *plan->p, *upd->u, formulation, mu, s);
+    *out = new sbx_els_shard_s{std::move(e), upd->u};
+  });
+}
+
+int sbx_els_shard_info(sbx_els_shard e, int64_t* info) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els shard handle");
+    const auto& x = *e->e;
+    const int64_t v[7] = {x.row0, x.row1, x.local_p(), x.k, x.n_k + x.n_c + x.n_p, x.G, x.p};
+    std::copy(v, v + 7, info);
+  });
+}
+
+int sbx_els_shard_rows(sbx_els_shard e, int64_t* ext_rows) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els shard handle");
+    std::copy(e->e->ext_of_local.begin(), e->e->ext_of_local.end(), ext_rows);
+  });
+}
+
+int sbx_els_shard_solve(sbx_els_shard e, const double* g_local, int64_t ldg, const double* g_p, int64_t ldgp,
+                        int64_t nrhs, double* y_local, int64_t ldy, double* y_p, int64_t ldyp, int flags,
+                        void* stream) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els shard handle");
+    sbx::ElsShard& x = *e->e;
+    const cudaStream_t s = stream_of(stream);
+    sbx::StreamScope scope(s);
+    const int64_t rows = x.rows(), np = x.local_p();
+    sbx::require(nrhs >= 0 && ldg >= rows && ldy >= rows, "els_shard_solve: bad sizes");
+    if (np > 0) sbx::require(g_p && y_p && ldgp >= np && ldyp >= np, "els_shard_solve: rank 0 needs the added rows");
+    if (nrhs == 0) return;
+    const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    Staged gi, gpi, yo, ypo;
+    const double* gd = gi.in(g_local, rows, nrhs, ldg, dev, s);
+    const double* gpd = np > 0 ? gpi.in(g_p, np, nrhs, ldgp, dev, s) : nullptr;
+    double* yd = yo.out(y_local, rows, nrhs, dev);
+    double* ypd = np > 0 ? ypo.out(y_p, np, nrhs, dev) : nullptr;
+    sbx::els_shard_solve(x, gd, dev ? ldg : rows, gpd, dev ? ldgp : std::max<int64_t>(np, 1), nrhs, yd,
+                         dev ? ldy : rows, ypd, dev ? ldyp : std::max<int64_t>(np, 1), s);
+    yo.back(y_local, rows, nrhs, ldy, dev, s);
+    if (np > 0) ypo.back(y_p, np, nrhs, ldyp, dev, s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int sbx_els_shard_destroy(sbx_els_shard e) { return destroy_handle(e); }
 
 }  // extern "C"

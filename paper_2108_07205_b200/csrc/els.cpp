@@ -25,6 +25,8 @@ std::vector<i64> scalars(const std::vector<i64>& nodes) {
   return o;
 }
 
+}  // namespace
+
 // Dense LU + explicit inverse + rcond (Eigen PartialPivLU::rcond) of an
 // n x n device matrix a (destroyed); returns rcond.
 double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
@@ -45,6 +47,8 @@ double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s) {
   SBX_CUDA(cudaStreamSynchronize(s));
   return r;
 }
+
+namespace {
 
 // out = Atilde^{-1} v for an n_ext x nrhs column-major device block
 // (els.cpp:43-65): the old-mesh part goes through the HBS sweep in old

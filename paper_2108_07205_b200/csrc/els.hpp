@@ -33,6 +33,9 @@ struct AppSolver {
     return g == &g2 && form == f && mu == m && eps == e && added == p.added_new;
   }
 };
+// Partial-pivot LU, explicit inverse into inv (ld n) and Eigen's
+// PartialPivLU::rcond() estimate of an n x n device matrix a (destroyed).
+double dense_inverse(double* a, i64 n, double* inv, cudaStream_t s);
 std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan, int formulation,
                                             double mu, double eps, cudaStream_t s);
 // out = A_pp^{-1} v (or A_pp^{-T} v) for n_p x nrhs column-major device blocks

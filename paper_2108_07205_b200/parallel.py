@@ -23,9 +23,18 @@ rows of X and y it produces) lives on rank 0, and the two u-row products
 R X (u x u) and R y (u x nrhs) are the only exchanges (all-reduce sums);
 W^{-1} is formed redundantly on every rank.
 
-The executor abstraction separates the exchange protocol (this module) from
-the per-rank compute: `DeviceExecutor` drives libsbx; tests drive the same
-protocol with a host executor over gloo.
+The device path is native: `Comm` (an NCCL communicator set owned by the
+C-ABI, sbx_comm_*), `NativeShardedSolver` (sbx_hbs_solve_sharded) and
+`NativeShardedWoodbury` (sbx_els_shard_*) run the sweeps, the GEMMs, W^{-1}
+and the NCCL collectives inside libsbx on the caller's stream -- no torch
+arithmetic.  `Comm.loopback(G)` gives G in-process members (one host thread
+each) so the same C++ protocol runs on one GPU.
+
+`ShardedHbsSolver` / `ShardedWoodbury` below restate the same exchange
+protocol over torch.distributed with a pluggable per-rank executor; the CPU
+tests drive them over gloo with host executors on the oracle's factors
+(tests/test_parallel_gloo.py), which checks the protocol itself on world
+sizes 2 and 4 where no multi-GPU box is available.
 """
 from __future__ import annotations
 
@@ -37,40 +46,162 @@ from ._sbx import check, lib
 VP = C.c_void_p
 
 
-class DeviceExecutor:
-    """Per-rank compute of the partitioned solve on this process's GPU."""
+def _stream():
+    from .api import torch_stream_handle
+    try:
+        return VP(torch_stream_handle())
+    except Exception:  # no torch CUDA context: the library stream
+        return VP()
 
-    def __init__(self, h, G: int, p: int):
+
+class Comm:
+    """A communicator set of the C-ABI (sbx_comm): NCCL for one process per
+    GPU, or a loopback member for in-process emulation."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr if isinstance(ptr, VP) else VP(ptr)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().sbx_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def create(cls, unique_id: bytes, world: int, rank: int) -> "Comm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        out = VP()
+        check(lib().sbx_comm_create(buf, world, rank, C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        """NCCL communicator over the ranks of a torch.distributed group: rank 0
+        makes the unique id, the group broadcasts it (the only use of torch)."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        return cls.create(obj[0], world, rank)
+
+    @classmethod
+    def loopback(cls, world: int):
+        arr = (VP * world)()
+        check(lib().sbx_comm_create_loopback(world, arr))
+        return [cls(VP(arr[i])) for i in range(world)]
+
+    def info(self):
+        w, r = C.c_int(), C.c_int()
+        check(lib().sbx_comm_info(self.ptr, C.byref(w), C.byref(r)))
+        return w.value, r.value
+
+    def __del__(self):
+        try:
+            if self.ptr and self.ptr.value and _sbx._lib is not None:
+                _sbx._lib.sbx_comm_destroy(self.ptr)
+                self.ptr = VP()
+        except Exception:
+            pass
+
+
+def _cm_call(x, rows):
+    """Column-major device (or host) view of a rows x m block: (keepalive, ptr, ld, m, device?)."""
+    if hasattr(x, "is_cuda") and x.is_cuda:
         import torch
-        self.torch = torch
-        self.h, self.G, self.p = h, G, p
+        x2 = x.reshape(-1, 1) if x.dim() == 1 else x
+        if x2.shape[0] != rows or x2.dtype != torch.float64:
+            raise ValueError("sharded call: expected float64 with the owned row count")
+        cm = x2.t().contiguous()
+        return cm, VP(cm.data_ptr()), rows, x2.shape[1], True
+    import numpy as np
+    a = np.asfortranarray(np.asarray(x, dtype=np.float64).reshape(rows, -1))
+    return a, VP(a.ctypes.data), rows, a.shape[1], False
+
+
+def _cm_out(like, rows, m, dev):
+    if dev:
+        import torch
+        return torch.empty((m, rows), dtype=torch.float64, device=like.device)
+    import numpy as np
+    return np.zeros((rows, m), order="F")
+
+
+def _cm_result(out, dev):
+    return out.t() if dev else out
+
+
+class NativeShardedSolver:
+    """x_local = A_oo^{-1} b on this rank's subtree rows (sbx_hbs_solve_sharded):
+    local up-sweep, NCCL all-gather of the subtree-root hats, top levels,
+    local down-sweep -- all inside libsbx on the caller's stream."""
+
+    def __init__(self, h, comm: Comm):
+        self.h, self.comm = h, comm
+        self.G, self.p = comm.info()
         r0, r1, km = C.c_int64(), C.c_int64(), C.c_int64()
-        check(lib().sbx_hbs_shard_info(h.ptr, G, p, C.byref(r0), C.byref(r1), C.byref(km)))
+        check(lib().sbx_hbs_shard_info(h.ptr, self.G, self.p, C.byref(r0), C.byref(r1), C.byref(km)))
         self.row0, self.row1, self.kmax = r0.value, r1.value, km.value
 
-    def _stream(self):
-        from .api import torch_stream_handle
-        return VP(torch_stream_handle())
+    @property
+    def rows(self):
+        return self.row0, self.row1
 
-    def up(self, b_local):
-        """b_local: CUDA float64 (rows x nrhs) -> packed hat (kmax x nrhs, row-major)."""
-        torch = self.torch
-        nrhs = b_local.shape[1]
-        bcm = b_local.t().contiguous()  # column-major storage
-        hat = torch.zeros((max(self.kmax, 1), nrhs), dtype=torch.float64, device=b_local.device)
-        check(lib().sbx_hbs_solve_shard_up(self.h.ptr, self.G, self.p, VP(bcm.data_ptr()), bcm.shape[1],
-                                           nrhs, VP(hat.data_ptr()), _sbx.SBX_DEVICE_PTRS, self._stream()))
-        return hat[: self.kmax]
+    def solve(self, b_local):
+        n = self.row1 - self.row0
+        keep, ptr, ld, m, dev = _cm_call(b_local, n)
+        out = _cm_out(keep, n, m, dev)
+        optr = VP(out.data_ptr()) if dev else VP(out.ctypes.data)
+        check(lib().sbx_hbs_solve_sharded(self.h.ptr, self.comm.ptr, ptr, ld, m, optr, n,
+                                          _sbx.SBX_DEVICE_PTRS if dev else 0, _stream() if dev else VP()))
+        return _cm_result(out, dev)
 
-    def down(self, hats, nrhs):
-        """hats: (G, kmax, nrhs) gathered blocks -> x_local (rows x nrhs)."""
-        torch = self.torch
-        rows = self.row1 - self.row0
-        out = torch.empty((nrhs, rows), dtype=torch.float64, device=hats.device)  # column-major
-        h = hats.contiguous()
-        check(lib().sbx_hbs_solve_shard_down(self.h.ptr, self.G, self.p, VP(h.data_ptr()), nrhs,
-                                             VP(out.data_ptr()), rows, _sbx.SBX_DEVICE_PTRS, self._stream()))
-        return out.t()
+
+class NativeShardedWoodbury:
+    """ELS / Woodbury on the subtree ownership inside libsbx (sbx_els_shard_*):
+    X rows and R columns by subtree, A_pp on rank 0, all-reduce of R X and
+    R y over NCCL, W^{-1} on every rank."""
+
+    def __init__(self, a_oo, comm: Comm, d_old, d_new, plan, update, formulation=0, mu=1.0, stream=None):
+        import numpy as np
+        self.comm, self._keep = comm, (a_oo, d_old, d_new, plan, update)
+        out = VP()
+        check(lib().sbx_els_shard_build(a_oo.ptr, comm.ptr, d_old.ptr, d_new.ptr, plan.ptr, update.ptr,
+                                        formulation, mu, VP(stream) if stream else VP(), C.byref(out)))
+        self.ptr = out
+        info = np.zeros(7, dtype=np.int64)
+        check(lib().sbx_els_shard_info(self.ptr, info.ctypes.data_as(_sbx.I64P)))
+        self.row0, self.row1, self.n_p_local, self.k, self.n_ext, self.G, self.p = (int(v) for v in info)
+        self.ext_rows = np.zeros(self.row1 - self.row0, dtype=np.int64)
+        check(lib().sbx_els_shard_rows(self.ptr, self.ext_rows.ctypes.data_as(_sbx.I64P)))
+
+    def local_rows(self, g_ext):
+        """This rank's owned rows (old-mesh order) of an ext-ordered block."""
+        return g_ext[self.ext_rows] if not hasattr(g_ext, "is_cuda") else g_ext[
+            __import__("torch").as_tensor(self.ext_rows, device=g_ext.device)]
+
+    def solve(self, g_local, g_p=None):
+        """(y_local, y_p): owned rows of ELS^{-1} g, and the added rows on rank 0."""
+        n = self.row1 - self.row0
+        keep, ptr, ld, m, dev = _cm_call(g_local, n)
+        out = _cm_out(keep, n, m, dev)
+        optr = VP(out.data_ptr()) if dev else VP(out.ctypes.data)
+        pk = pptr = pout = poptr = None
+        ldp = 1
+        if self.n_p_local:
+            pk, pptr, ldp, _, _ = _cm_call(g_p, self.n_p_local)
+            pout = _cm_out(keep, self.n_p_local, m, dev)
+            poptr = VP(pout.data_ptr()) if dev else VP(pout.ctypes.data)
+        check(lib().sbx_els_shard_solve(self.ptr, ptr, ld, pptr or VP(), ldp, m, optr, n, poptr or VP(), ldp,
+                                        _sbx.SBX_DEVICE_PTRS if dev else 0, _stream() if dev else VP()))
+        return _cm_result(out, dev), (_cm_result(pout, dev) if pout is not None else None)
+
+    def __del__(self):
+        try:
+            if self.ptr and self.ptr.value and _sbx._lib is not None:
+                _sbx._lib.sbx_els_shard_destroy(self.ptr)
+                self.ptr = VP()
+        except Exception:
+            pass
 
 
 class ShardedHbsSolver:

@@ -5,7 +5,7 @@
       --master-addr 127.0.0.1 --master-port 29511 scripts/shard_bench.py --nrhs 1,32,256
 
 Each rank builds the static HBS inverse of cfg3 (the same operator on every
-rank), then times `ShardedHbsSolver.solve` (local up-sweep, NCCL all-gather
+rank), then times `NativeShardedSolver.solve` (sbx_hbs_solve_sharded: local up-sweep, NCCL all-gather
 of the subtree-root hats, top levels + local down-sweep) with CUDA events on
 its stream; rank 0 prints the max over ranks and checks the gathered
 solution against a single-GPU hbs_solve.
@@ -22,7 +22,7 @@ import torch.distributed as dist
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2108_07205_b200 as sb  # noqa: E402
 from paper_2108_07205_b200.configs import CONFIGS  # noqa: E402
-from paper_2108_07205_b200.parallel import DeviceExecutor, ShardedHbsSolver  # noqa: E402
+from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver  # noqa: E402
 
 
 def main():
@@ -42,8 +42,7 @@ def main():
     g = sb.panelize(sb.star(c.prongs, c.amplitude, c.a), c.n_panels, c.q)
     h = sb.hbs_invert(sb.hbs_compress(g, opts=sb.HbsOptions(eps=c.eps, leaf_nodes=c.leaf)))
     n = h.info()["n"]
-    ex = DeviceExecutor(h, world, rank)
-    solver = ShardedHbsSolver(ex)
+    solver = NativeShardedSolver(h, Comm.from_process_group())
     r0, r1 = solver.rows
     out = []
     for nrhs in [int(x) for x in a.nrhs.split(",")]:

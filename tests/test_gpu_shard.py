@@ -1,8 +1,13 @@
-"""Device subtree-partitioned solve (sbx_hbs_solve_shard_up/down) against the
-unpartitioned device hbs_solve.  One GPU here: the G ranks run one after the
-other in this process and the all-gather is a host-side stack; the real
-exchange over NCCL is the same ShardedHbsSolver.solve call exercised over
-gloo in test_parallel_gloo.py."""
+"""Device subtree-partitioned solve and Woodbury through the native C-ABI
+path (sbx_hbs_solve_sharded, sbx_els_shard_*; multigpu.cpp) against the
+unpartitioned device solves.  One GPU here, so the G ranks are a loopback
+group (sbx_comm_create_loopback): one host thread and one stream per rank,
+each with its own copy of the HBS operator (as on separate GPUs), exchanging
+through the same Collective interface the NCCL communicator implements.  The
+NCCL communicator itself runs with world size 1; the exchange protocol at
+world sizes 2 and 4 is also covered over gloo (test_parallel_gloo.py)."""
+import threading
+
 import numpy as np
 import pytest
 
@@ -10,96 +15,130 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
-def setup():
+def setup(tmp_path_factory):
     import torch
 
     import paper_2108_07205_b200 as sb
-    from paper_2108_07205_b200.parallel import DeviceExecutor
     sb.init(0)
     g = sb.panelize(sb.star(5, 0.3), 64, 16)  # 1024 nodes, 16 leaves, depth 4
     h = sb.hbs_invert(sb.hbs_compress(g, opts=sb.HbsOptions(eps=1e-10)))
-    return sb, torch, DeviceExecutor, h, g
+    path = tmp_path_factory.mktemp("shard") / "h.hbs1"
+    sb.hbs_save(h, path)
+    return sb, torch, h, g, path
+
+
+def _ranks(G, fn):
+    """Run fn(p) for p < G in G threads (loopback ranks); re-raise the first error."""
+    errs, out = [], [None] * G
+
+    def run(p):
+        try:
+            out[p] = fn(p)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(p,)) for p in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in th), "loopback ranks did not finish"
+    if errs:
+        raise errs[0]
+    return out
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
 @pytest.mark.parametrize("nrhs", [1, 5, 64])
-def test_shard_solve_matches_full(setup, G, nrhs):
-    sb, torch, DeviceExecutor, h, _ = setup
+def test_native_sharded_solve_matches_full(setup, G, nrhs):
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver
+    sb, torch, h, _, path = setup
     n = h.info()["n"]
     b = torch.empty((n, nrhs), dtype=torch.float64, device="cuda").uniform_(-1, 1)
     ref = sb.hbs_solve(h, b)
-    exes = [DeviceExecutor(h, G, p) for p in range(G)]
-    rows = [(e.row0, e.row1) for e in exes]
-    assert rows[0][0] == 0 and rows[-1][1] == n
-    assert all(rows[p][1] == rows[p + 1][0] for p in range(G - 1))
-    hats = [exes[p].up(b[rows[p][0]:rows[p][1]]) for p in range(G)]
-    kmax = exes[0].kmax
-    gathered = (torch.stack(hats) if kmax > 0
-                else torch.zeros((G, 0, nrhs), dtype=torch.float64, device="cuda"))
-    x = torch.empty_like(b)
-    for p in range(G):
-        x[rows[p][0]:rows[p][1]] = exes[p].down(gathered, nrhs)
-    torch.cuda.synchronize()
+    comms = Comm.loopback(G)
+    ops = [sb.hbs_load(path) for _ in range(G)]  # one operator per rank, as on G GPUs
+    streams = [torch.cuda.Stream() for _ in range(G)]
+
+    def rank(p):
+        solver = NativeShardedSolver(ops[p], comms[p])
+        r0, r1 = solver.rows
+        with torch.cuda.stream(streams[p]):
+            x = solver.solve(b[r0:r1])
+            streams[p].synchronize()
+        return r0, r1, x
+
+    res = _ranks(G, rank)
+    assert res[0][0] == 0 and res[-1][1] == n
+    assert all(res[p][1] == res[p + 1][0] for p in range(G - 1))
+    x = torch.cat([r[2] for r in res])
     err = (torch.linalg.norm(x - ref) / torch.linalg.norm(ref)).item()
     assert err <= 1e-13, err
+    # host buffers through the same call
+    xh = _ranks(G, lambda p: NativeShardedSolver(ops[p], comms[p]).solve(
+        b[res[p][0]:res[p][1]].cpu().numpy()))
+    assert np.linalg.norm(np.vstack(xh) - ref.cpu().numpy()) <= 1e-13 * np.linalg.norm(ref.cpu().numpy())
+
+
+def test_nccl_communicator_world_one(setup):
+    """The NCCL communicator set of the C-ABI (world size 1 on one GPU)."""
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver
+    sb, torch, h, _, _ = setup
+    c = Comm.create(Comm.unique_id(), 1, 0)
+    assert c.info() == (1, 0)
+    b = torch.empty((h.n, 3), dtype=torch.float64, device="cuda").uniform_(-1, 1)
+    x = NativeShardedSolver(h, c).solve(b)
+    assert torch.equal(x, sb.hbs_solve(h, b))
 
 
 def test_shard_rejects_bad_rank_count(setup):
-    sb, torch, DeviceExecutor, h, _ = setup
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver
+    sb, torch, h, _, _ = setup
     with pytest.raises(ValueError):
-        DeviceExecutor(h, 3, 0)
+        NativeShardedSolver(h, Comm.loopback(3)[0])
     with pytest.raises(ValueError):
-        DeviceExecutor(h, 64, 0)  # deeper than the tree
+        NativeShardedSolver(h, Comm.loopback(64)[0])  # deeper than the tree
 
 
+@pytest.mark.parametrize("G", [1, 2, 4])
 @pytest.mark.parametrize("n_refine", [2, 8])
-def test_sharded_woodbury_device_matches_els(setup, n_refine):
-    """ShardedWoodbury (parallel.py) on the device pieces — the partitioned
-    HBS solve, sbx_app_solve for the added block, the update factors — on a
-    one-rank NCCL group; equals the device els_solve_raw.  The multi-rank
-    exchange is covered over gloo (test_parallel_gloo.py).  8 refined panels
-    at m = 16 put the added block on its own HBS (2 N_p > 2048)."""
-    import os
-    import socket
-
-    import torch.distributed as dist
-
-    from paper_2108_07205_b200.parallel import ShardedHbsSolver, ShardedWoodbury
-    sb, torch, DeviceExecutor, h, g = setup
-    if not dist.is_initialized():
-        s = socket.socket()
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-        s.close()
-        os.environ["MASTER_ADDR"] = "127.0.0.1"
-        os.environ["MASTER_PORT"] = str(port)
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+def test_native_sharded_woodbury_matches_els(setup, G, n_refine):
+    """sbx_els_shard_build / solve (X rows and R columns by subtree, A_pp on
+    rank 0, all-reduce of R X and R y, W^{-1} on every rank) against the
+    unpartitioned els_solve_raw.  8 refined panels at m = 16 put the added
+    block on its own HBS (2 N_p > 2048)."""
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedWoodbury
+    sb, torch, h, g, path = setup
     panels = list(range(10, 10 + n_refine))
     g1, plan = sb.refine(g, panels, 16 if n_refine == 8 else 4)
     upd = sb.compress_update(g, g1, plan, 1e-10)
     els = sb.els_build(h, g, g1, plan, upd)
-    app = sb.app_build(g1, plan, 1e-10)
-    assert app.info()["hbs"] == (1 if n_refine == 8 else 0)
-    L, R = upd.factors()
-    m = plan.maps()
-
-    def scal(v):
-        return np.stack([2 * v, 2 * v + 1], 1).reshape(-1)
-
-    old_of_ext = np.concatenate([scal(m["kept_old"]), scal(m["cut_old"])])
-    n_k, n_c, n_p = 2 * len(m["kept_old"]), 2 * len(m["cut_old"]), 2 * len(m["added_new"])
+    info = els.info()
+    n_k, n_c, n_p = info["n_k"], info["n_c"], info["n_p"]
     gx = torch.empty((n_k + n_c + n_p, 4), dtype=torch.float64, device="cuda").uniform_(-1, 1)
     gx[n_k:n_k + n_c] = 0.0
-    wb = ShardedWoodbury(ShardedHbsSolver(DeviceExecutor(h, 1, 0)), torch.from_numpy(L).cuda(),
-                         torch.from_numpy(R).cuda(), old_of_ext, n_k, n_c, n_p, app_solve=app.solve)
-    y, y_p = wb.solve(wb.local_rows(gx), gx[n_k + n_c:])
-    out = torch.zeros_like(gx)
-    out[wb.own] = y[wb.pos]
-    out[n_k + n_c:] = y_p
     ref = sb.els_solve_raw(els, gx)
+    comms = Comm.loopback(G)
+    ops = [sb.hbs_load(path) for _ in range(G)]
+    streams = [torch.cuda.Stream() for _ in range(G)]
+
+    def rank(p):
+        with torch.cuda.stream(streams[p]):
+            wb = NativeShardedWoodbury(ops[p], comms[p], g, g1, plan, upd, stream=streams[p].cuda_stream)
+            y, y_p = wb.solve(wb.local_rows(gx), gx[n_k + n_c:] if p == 0 else None)
+            streams[p].synchronize()
+        return wb.ext_rows, y, y_p, wb.k
+
+    res = _ranks(G, rank)
+    out = torch.zeros_like(gx)
+    for p, (rows, y, y_p, k) in enumerate(res):
+        assert k == upd.k
+        out[torch.as_tensor(rows, device="cuda")] = y
+        if p == 0 and n_p:
+            out[n_k + n_c:] = y_p
+    covered = np.sort(np.concatenate([r[0] for r in res]))
+    assert np.array_equal(covered, np.arange(n_k + n_c))
     err = (torch.linalg.norm(out - ref) / torch.linalg.norm(ref)).item()
-    if n_refine == 8 and dist.is_initialized():  # the last parametrisation tears the group down
-        dist.destroy_process_group()
     assert err <= 1e-10, err
 
 
@@ -108,7 +147,7 @@ def test_app_block_solver(setup, n_refine, m):
     """sbx_app_build / sbx_app_solve (the added block of els_build,
     els.cpp:107-118): dense LU below 2048 scalars, its own HBS above; the
     plain and transposed solves against a dense solve of A_pp."""
-    sb, torch, DeviceExecutor, h, g = setup
+    sb, torch, h, g, _ = setup
     g1, plan = sb.refine(g, list(range(20, 20 + n_refine)), m)
     app = sb.app_build(g1, plan, 1e-10)
     added = plan.maps()["added_new"]
