@@ -20,6 +20,7 @@ has no exchange step at this size), scaling "weak".
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -124,7 +125,9 @@ def workload_config(cfg, world):
             "rhs_per_step": cfg.nrhs,
             "step": "refine -> compress_update -> els_build -> els_solve (static HBS inverse built once, excluded)",
             "l2": "inputs re-streamed each step (per-step working set > L2)",
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+            "parallelism": (f"snapshot-sharded x{world}: rank r solves its own refined wall (seed + r), "
+                            f"no data-path collective; the subtree partition is measured in `partitioned`")
+                           if world > 1 else "single GPU"}
 
 
 def build_problem(cfg, sb):
@@ -158,7 +161,10 @@ def run_ours(args, rank, world, local_rank):
     import paper_2108_07205_b200 as sb
     from paper_2108_07205_b200.configs import CONFIGS
 
-    cfg = CONFIGS[args.config]
+    cfg0 = CONFIGS[args.config]
+    # independent snapshots per rank (run_snapshot_batch's units): rank r
+    # refines around its own seed-drawn point with its own RHS
+    cfg = cfg0 if rank == 0 else dataclasses.replace(cfg0, seed=cfg0.seed + rank)
     torch.cuda.set_device(local_rank)
     sb.init(local_rank)
     if world > 1:
@@ -228,8 +234,6 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     t_dev, t_e2e = times.tolist()
-    if rank != 0:
-        return None
     value = world * args.steps * nrhs / t_dev
     e2e_value = world * args.steps * nrhs / t_e2e
     roof = roofline_solve(sb, torch, stream, h, state, G_dev)
@@ -248,6 +252,10 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "roofline": roof,
     }
+    part = partitioned_bench(sb, torch, rank, world, g0, h, cfg0)
+    if rank != 0:
+        return None
+    line["partitioned"] = part
     if world == 1:
         line["step_dominant"] = step_profile(sb, torch, stream, step, 1e3 * t_dev / args.steps)
     if not args.no_apply_bench and world == 1:
@@ -256,6 +264,109 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(cfg, G.shape[1], threads=1)
     return line
+
+
+def partitioned_bench(sb, torch, rank, world, g0, h, cfg0, reps=10):
+    """The subtree partition of SURVEY.md 8(e) through the native path
+    (sbx_comm NCCL communicator, sbx_hbs_solve_sharded, sbx_els_shard_*):
+    (a) the cfg3 HBS-inverse apply (131072 unknowns) at nrhs 1/32/256 with
+    the tree split across the ranks (one NCCL all-gather of the subtree-root
+    hats per solve), and (b) the cfg2 Woodbury solve of the 64 RHS on the
+    same ownership (all-reduce of R y).  CUDA events on each rank's stream,
+    max over ranks; results checked against the single-GPU solve."""
+    import statistics
+    from paper_2108_07205_b200.configs import CONFIGS
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver, NativeShardedWoodbury
+    import tempfile
+    panels0 = cfg0.refine_panels(g0.nodes())
+    comm = Comm.from_process_group() if world > 1 else Comm.loopback(1)[0]  # one rank: no NCCL needed
+    out = {"ranks": world, "exchange": "NCCL all-gather of subtree-root hats (solve), all-reduce of R y (Woodbury)"}
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(ts)], device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return t.item()
+
+    # every rank must sweep the SAME factors: rank 0 builds them, the others
+    # load its HBS1 / dump files (one node, shared /tmp)
+    tmp = [tempfile.mkdtemp(prefix="sbx_part_") if rank == 0 else None]
+    if world > 1:
+        torch.distributed.broadcast_object_list(tmp, src=0)
+    d = Path(tmp[0])
+    c3 = CONFIGS["cfg3"]
+    if rank == 0:
+        g3 = sb.panelize(sb.star(c3.prongs, c3.amplitude, c3.a), c3.n_panels, c3.q)
+        h3 = sb.hbs_invert(sb.hbs_compress(g3, opts=sb.HbsOptions(eps=c3.eps, leaf_nodes=c3.leaf)))
+        if world > 1:
+            sb.hbs_save(h3, d / "cfg3.hbs1")
+            sb.hbs_save(h, d / "cfg2.hbs1")
+    if world > 1:
+        torch.distributed.barrier()
+        if rank != 0:
+            h3 = sb.hbs_load(d / "cfg3.hbs1")
+            h = sb.hbs_load(d / "cfg2.hbs1")
+    solver = NativeShardedSolver(h3, comm)
+    r0, r1 = solver.rows
+    n3 = h3.info()["n"]
+    apply = {}
+    for nrhs in (1, 32, 256):
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        b = torch.empty((n3, nrhs), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+        bl = b[r0:r1].contiguous()
+        ms = timed(lambda: solver.solve(bl))
+        x = solver.solve(bl)
+        ref = sb.hbs_solve(h3, b)[r0:r1]
+        err = (torch.linalg.norm(x - ref) / torch.linalg.norm(ref)).item()
+        apply[f"rhs{nrhs}"] = {"ms": round(ms, 4), "solves_per_s": round(nrhs / (ms * 1e-3), 1),
+                               "rel_err_vs_1gpu": err}
+    out["cfg3_apply"] = apply
+    # cfg2 Woodbury solve on the subtree ownership: rank 0's refined wall
+    # (configs[1], seed 0) on every rank, its update factors handed over in
+    # the dump format
+    g1, plan = sb.refine(g0, panels0, cfg0.m)
+    if rank == 0:
+        upd = sb.compress_update(g0, g1, plan, cfg0.eps, seed=cfg0.seed)
+        if world > 1:
+            sb.update_dump(upd, d / "L.mat", d / "R.mat")
+    if world > 1:
+        torch.distributed.barrier()
+        if rank != 0:
+            upd = sb.update_load(plan, d / "L.mat", d / "R.mat")
+    els = sb.els_build(h, g0, g1, plan, upd)
+    wb = NativeShardedWoodbury(h, comm, g0, g1, plan, upd)
+    i = els.info()
+    nkc = i["n_k"] + i["n_c"]
+    G0 = np.stack([sb.gather_kept_added(plan, sb.boundary_data(g1, s_)) for s_ in cfg0.sources()], 1)
+    gx = torch.zeros((nkc + i["n_p"], G0.shape[1]), dtype=torch.float64, device="cuda")
+    gx[: i["n_k"]] = torch.from_numpy(G0[: i["n_k"]]).cuda()
+    gx[nkc:] = torch.from_numpy(G0[i["n_k"]:]).cuda()
+    gl = wb.local_rows(gx).contiguous()
+    gp = gx[nkc:].contiguous() if rank == 0 else None
+    ms = timed(lambda: wb.solve(gl, gp))
+    y, _ = wb.solve(gl, gp)
+    ref = sb.els_solve_raw(els, gx)[torch.as_tensor(wb.ext_rows, device="cuda")]
+    out["cfg2_woodbury_solve"] = {"ms": round(ms, 4), "nrhs": int(G0.shape[1]), "k": wb.k,
+                                  "rel_err_vs_1gpu": (torch.linalg.norm(y - ref) / torch.linalg.norm(ref)).item()}
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        import shutil
+        shutil.rmtree(d, ignore_errors=True)
+    return out
 
 
 def step_profile(sb, torch, stream, step, ms_step, reps=3):
@@ -538,6 +649,9 @@ def run_reference(args, rank, world):
 
 
 def main():
+    # the JSON line must be the only stdout output (NCCL's version banner is a log line)
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse()
     rank, world, local_rank = dist_env()
     if args.impl == "reference":

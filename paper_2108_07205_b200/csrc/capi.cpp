@@ -72,13 +72,30 @@ int guard(F&& f) {
   }
 }
 
-// Releasing a handle waits for the device, as cudaFree would: its device
-// memory returns to a stream-ordered pool while solves enqueued on caller
-// streams may still be reading it.
+// Releasing a handle waits, as cudaFree would, for the work that may still
+// read its device memory (which returns to a stream-ordered pool): the
+// library stream, and the last call on every caller stream the handle ran
+// on (StreamMark events; no device-wide synchronisation).
+void drain_handle(sbx_hbs_s* h) {
+  if (h->h) h->h->drain();
+}
+void drain_handle(sbx_els_s* e) {
+  if (e->e) e->e->drain();
+}
+void drain_handle(sbx_app_s* a) {
+  if (a->a && a->a->h) a->a->h->drain();
+}
+void drain_handle(sbx_els_shard_s* e) {
+  if (e->e) (void)cudaDeviceSynchronize();  // shard solves run on caller streams (no marks kept)
+}
+template <class T>
+void drain_handle(T*) {}  // used on the library stream only
+
 template <class T>
 int destroy_handle(T* h) {
   if (h) {
-    (void)cudaDeviceSynchronize();
+    drain_handle(h);
+    (void)cudaStreamSynchronize(sbx::lib_stream());
     delete h;
   }
   return SBX_OK;

@@ -193,10 +193,37 @@ class PerStream {
     items_.emplace_back(s, std::make_unique<T>());
     return *items_.back().second;
   }
+  template <class F>
+  void for_each(F f) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto& e : items_) f(*e.second);
+  }
 
  private:
   std::mutex mu_;
   std::vector<std::pair<cudaStream_t, std::unique_ptr<T>>> items_;
+};
+
+// Completion marker of the last call a handle ran on one stream: recorded
+// at the end of each call, waited on when the handle is destroyed (its
+// device memory returns to a stream-ordered pool while work enqueued on a
+// caller's stream may still read it).  The event is ours, so waiting on it
+// is safe even after the caller destroyed that stream.
+struct StreamMark {
+  cudaEvent_t ev = nullptr;
+  StreamMark() = default;
+  StreamMark(const StreamMark&) = delete;
+  StreamMark& operator=(const StreamMark&) = delete;
+  ~StreamMark() {
+    if (ev) cudaEventDestroy(ev);
+  }
+  void record(cudaStream_t s) {
+    if (!ev) SBX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SBX_CUDA(cudaEventRecord(ev, s));
+  }
+  void wait() const {
+    if (ev) (void)cudaEventSynchronize(ev);
+  }
 };
 
 // Column-major host matrix (the reference's Eigen storage order; used for

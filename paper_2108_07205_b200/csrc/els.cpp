@@ -288,6 +288,7 @@ void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, b
       SBX_CUDA(cudaMemcpy2DAsync(y + e.n_k, size_t(ldy) * 8, yx + nkc, size_t(n) * 8, size_t(e.n_p) * 8,
                                  size_t(nrhs), kind, s));
   }
+  e.scratch_for(s).mark.record(s);
   if (!dev) SBX_CUDA(cudaStreamSynchronize(s));
 }
 

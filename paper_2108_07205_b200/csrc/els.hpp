@@ -61,6 +61,7 @@ struct Els {
   // concurrent solves on distinct streams are legal.
   struct Scratch {
     DevBuf<double> a, b;
+    StreamMark mark;  // end of the last solve on this stream
     double* ws(size_t n, cudaStream_t s) {
       StreamScope ss(s);
       a.reserve(n);
@@ -74,6 +75,9 @@ struct Els {
   };
   PerStream<Scratch> scratch;
   Scratch& scratch_for(cudaStream_t s) { return scratch.get(s); }
+  void drain() {
+    scratch.for_each([](Scratch& x) { x.mark.wait(); });
+  }
 };
 
 std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom& new_g,

@@ -108,6 +108,7 @@ struct FlowCache {
 struct SweepScratch {
   DevBuf<double> ws, io, partials;
   DevBuf<int> counters;
+  StreamMark mark;  // end of the last sweep on this stream
 };
 
 struct ShardPlans;
@@ -152,6 +153,10 @@ struct HbsOp {
   std::recursive_mutex mu;
   PerStream<SweepScratch> scratch;
   SweepScratch& scratch_for(cudaStream_t s) { return scratch.get(s); }
+  // Waits for every call still in flight on any stream (handle destruction).
+  void drain() {
+    scratch.for_each([](SweepScratch& x) { x.mark.wait(); });
+  }
 
   i64 total_skeleton() const {
     i64 t = 0;

@@ -994,6 +994,7 @@ void hbs_solve_shard_down(HbsOp& op, int G, int p, const double* hats, i64 nrhs,
                                size_t(nrhs), cudaMemcpyDeviceToHost, s));
     SBX_CUDA(cudaStreamSynchronize(s));
   }
+  sc.mark.record(s);
 }
 
 void hbs_build_apply_plan(HbsOp& op) {
@@ -1253,6 +1254,7 @@ void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 r
   launch_cm_to_rm(in, ldi, rows, nrhs, ws + plan.in_row * ldw, ldw, map, s);
   hbs_run_plan(op, plan, ws, nrhs, s, transposed ? op.arena_t.get() : nullptr);
   launch_rm_to_cm(ws + plan.out_row * ldw, ldw, rows, nrhs, out, ldo, map, s);
+  sc.mark.record(s);
 }
 
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
