@@ -231,8 +231,23 @@ int sbx_els_density_on_refined(sbx_els e, const double* tau_n, double* out);
  * power iteration on the device operators and their solves (linop.cpp:17-43;
  * the reference uses 80). */
 int sbx_els_conditioning(sbx_els e, int iters, double* out);
+/* conditioning_report(s, dense_oracles_allowed) (els.cpp:225-270) with the
+ * route chosen: dense != 0 takes kappa_tilde / kappa_ext from the singular
+ * values of the assembled Atilde and Atilde + L R (device Jacobi SVD,
+ * n_ext <= 12000; the meshes the ELS was built on must still be alive);
+ * dense == 0 is sbx_els_conditioning.  Same 7 outputs. */
+int sbx_els_conditioning_report(sbx_els e, int dense, int iters, double* out);
 /* Woodbury factors for inspection: X (n_ext x k), W (k x k). */
 int sbx_els_xw(sbx_els e, double* X, double* W);
+
+/* compress_update with the CompressionMode (lowrank.hpp:17, lowrank.cpp:366-373):
+ * SBX_TWO_STEP_ID is sbx_update_compress; SBX_SVD_OPTIMAL is svd_optimal
+ * (lowrank.cpp:329-362): dense truncated SVDs of the kc / kp / pk blocks
+ * re-truncated through the stacked factor (device Jacobi SVD; a diagnostic
+ * mode for small refinements, like the reference's). */
+enum { SBX_TWO_STEP_ID = 0, SBX_SVD_OPTIMAL = 1 };
+int sbx_update_compress_mode(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formulation, double mu,
+                             double eps, uint64_t seed, int mode, sbx_update* out);
 
 /* ---------------------------------------------------------- snapshot update cache
  * run_snapshot_batch's cache (scenario.cpp:836-899): updates are determined

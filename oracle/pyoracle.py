@@ -368,6 +368,42 @@ def load_matrix(path):
     return out
 
 
+def truncated_svd(w, eps):
+    """idlib.cpp:134-154 (Eigen BDCSVD there, LAPACK gesdd here): thin SVD,
+    k = #{ s_i > eps s_0 }."""
+    w = np.asarray(w, dtype=np.float64)
+    if w.size == 0:
+        return np.zeros((w.shape[0], 0)), np.zeros(0), np.zeros((w.shape[1], 0))
+    U, s, Vt = np.linalg.svd(w, full_matrices=False)
+    k = int(np.sum(s > eps * s[0])) if s[0] > 0 else 0
+    return U[:, :k], s[:k], Vt[:k].T
+
+
+def svd_optimal(old_asm, new_asm, plan, eps):
+    """lowrank.cpp:329-362 (CompressionMode::SvdOptimal) with assemble_stacked
+    (lowrank.cpp:240-251): returns dict(L, R, k, k1, kc, kp, pk)."""
+    f = {}
+    for b in ("kc", "kp", "pk"):
+        U, s, V = truncated_svd(block_eval_full(old_asm, new_asm, plan, b), eps)
+        f[b] = (U, s[:, None] * V.T)
+    nk, nc, npp = plan.sizes()
+    nk2, nc2, np2 = 2 * nk, 2 * nc, 2 * npp
+    n = nk2 + nc2 + np2
+    kpk, kkc, kkp = (f[b][0].shape[1] for b in ("pk", "kc", "kp"))
+    k1 = kpk + kkc + kkp
+    L1, R1 = np.zeros((n, k1)), np.zeros((k1, n))
+    L1[:nk2, kpk:kpk + kkc] = -f["kc"][0]
+    L1[:nk2, kpk + kkc:] = f["kp"][0]
+    L1[nk2 + nc2:, :kpk] = f["pk"][0]
+    R1[:kpk, :nk2] = f["pk"][1]
+    R1[kpk:kpk + kkc, nk2:nk2 + nc2] = f["kc"][1]
+    R1[kpk + kkc:, nk2 + nc2:] = f["kp"][1]
+    if k1 == 0:
+        return {"L": np.zeros((n, 0)), "R": np.zeros((0, n)), "k": 0, "k1": 0, "kc": 0, "kp": 0, "pk": 0}
+    U, s, V = truncated_svd(L1, eps)
+    return {"L": U, "R": (s[:, None] * V.T) @ R1, "k": U.shape[1], "k1": k1, "kc": kkc, "kp": kkp, "pk": kpk}
+
+
 def block_eval_full(old_asm, new_asm, plan, block):
     nk, nc, npp = plan.sizes()
     size = {"k": 2 * nk, "c": 2 * nc, "p": 2 * npp}

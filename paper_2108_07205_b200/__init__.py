@@ -5,7 +5,7 @@ Public API mirrors the reference C++ solver (proj/include/stokesbie): see
 kernels behind the C-ABI of ``include/sbx.h``).
 """
 from .api import (  # noqa: F401
-    CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR,
+    CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR, SVD_OPTIMAL, TWO_STEP_ID,
     AppBlockSolver, UpdateCache, CurveParams, Discretization, ElsSolver, HbsOperator, HbsOptions, LowRankUpdate,
     RefinementPlan, add_holes, app_build, boundary_data, circle, coarsen, compress_update, density_on_refined,
     ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,

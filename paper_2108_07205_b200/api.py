@@ -391,14 +391,22 @@ class LowRankUpdate(_Handle):
         return L, R
 
 
+TWO_STEP_ID, SVD_OPTIMAL = 0, 1  # CompressionMode (lowrank.hpp:17)
+
+
 def compress_update(d_old: Discretization, d_new: Discretization, plan: RefinementPlan,
                     eps: float = 1e-10, formulation=INTERIOR_DIRICHLET, mu: float = 1.0,
-                    seed: int = 0) -> LowRankUpdate:
+                    seed: int = 0, mode: int = TWO_STEP_ID) -> LowRankUpdate:
     """compress_update(BlockSource(old, new, plan), make_proxy_geometry(new, plan),
-    eps, TwoStepId, {seed}) — lowrank.cpp:366-373."""
+    eps, mode, {seed}) — lowrank.cpp:366-373 (TwoStepId, or the SvdOptimal
+    diagnostic mode of lowrank.cpp:329-362)."""
     out = VP()
-    check(lib().sbx_update_compress(d_old.ptr, d_new.ptr, plan.ptr, formulation, mu, eps,
-                                    C.c_uint64(seed), C.byref(out)))
+    if mode == TWO_STEP_ID:
+        check(lib().sbx_update_compress(d_old.ptr, d_new.ptr, plan.ptr, formulation, mu, eps,
+                                        C.c_uint64(seed), C.byref(out)))
+    else:
+        check(lib().sbx_update_compress_mode(d_old.ptr, d_new.ptr, plan.ptr, formulation, mu, eps,
+                                             C.c_uint64(seed), int(mode), C.byref(out)))
     return LowRankUpdate(out)
 
 
@@ -471,9 +479,10 @@ class ElsSolver(_Handle):
     """els.hpp:17-37.  Keeps a reference to the HBS handle it solves with."""
     _destroy = "sbx_els_destroy"
 
-    def __init__(self, ptr, a_oo):
+    def __init__(self, ptr, a_oo, meshes=()):
         super().__init__(ptr)
         self._a_oo = a_oo
+        self._meshes = meshes  # the dense conditioning route reads them
 
     def info(self) -> dict:
         out = np.zeros(6, dtype=np.int64)
@@ -499,7 +508,7 @@ def els_build(a_oo: HbsOperator, d_old: Discretization, d_new: Discretization,
     out = VP()
     check(lib().sbx_els_build(a_oo.ptr, d_old.ptr, d_new.ptr, plan.ptr, update.ptr, formulation, mu,
                               C.byref(out)))
-    return ElsSolver(out, a_oo)
+    return ElsSolver(out, a_oo, (d_old, d_new))
 
 
 class AppBlockSolver(_Handle):
@@ -591,12 +600,13 @@ def els_apply_forward(s: ElsSolver, v, transpose: bool = False) -> np.ndarray:
     return out[:, 0] if vec else out
 
 
-def els_conditioning(s: ElsSolver, iters: int = 80) -> dict:
-    """conditioning_report (els.cpp:225-270), estimator route: exact kappa_w,
-    kappa_l, kappa_r; kappa_ext, kappa_tilde by seeded power iteration on the
-    device operators and solves (linop.cpp:17-43)."""
+def els_conditioning(s: ElsSolver, iters: int = 80, dense: bool = False) -> dict:
+    """conditioning_report(s, dense) (els.cpp:225-270): exact kappa_w,
+    kappa_l, kappa_r (device Jacobi SVD); kappa_ext, kappa_tilde from the
+    dense Atilde and Atilde + L R (dense=True) or by seeded power iteration on
+    the device operators and solves (linop.cpp:17-43)."""
     out = np.zeros(7)
-    check(lib().sbx_els_conditioning(s.ptr, int(iters), out.ctypes.data_as(F64P)))
+    check(lib().sbx_els_conditioning_report(s.ptr, int(bool(dense)), int(iters), out.ctypes.data_as(F64P)))
     keys = ("kappa_w", "kappa_l", "kappa_r", "kappa_ext", "kappa_tilde", "bound")
     r = {k: float(v) for k, v in zip(keys, out[:6])}
     r["bound_holds"] = bool(out[6] != 0.0)

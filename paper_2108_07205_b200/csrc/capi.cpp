@@ -473,6 +473,20 @@ int sbx_update_cache_stats(sbx_update_cache c, int64_t* entries, int64_t* hits, 
   });
 }
 
+int sbx_update_compress_mode(sbx_geom old_g, sbx_geom new_g, sbx_plan plan, int formulation, double mu,
+                             double eps, uint64_t seed, int mode, sbx_update* out) {
+  return guard([&] {
+    sbx::require(plan && plan->p, "null plan handle");
+    sbx::require(mode == SBX_TWO_STEP_ID || mode == SBX_SVD_OPTIMAL, "compress_update: unknown compression mode");
+    std::unique_ptr<sbx::Update> u =
+        mode == SBX_SVD_OPTIMAL
+            ? sbx::update_svd_optimal_device(G(old_g), G(new_g), *plan->p, formulation, mu, eps, sbx::lib_stream())
+            : sbx::update_compress_device(G(old_g), G(new_g), *plan->p, formulation, mu, eps, seed,
+                                          sbx::lib_stream());
+    *out = new sbx_update_s{std::move(u)};
+  });
+}
+
 int sbx_update_destroy(sbx_update u) { return destroy_handle(u); }
 
 int sbx_update_info(sbx_update u, int64_t* info) {
@@ -688,6 +702,21 @@ int sbx_els_conditioning(sbx_els e, int iters, double* out) {
     sbx::require(e && e->e, "null els handle");
     sbx::require(iters >= 1, "conditioning: iteration count must be positive");
     const sbx::CondReport r = sbx::els_conditioning(*e->e, iters, sbx::lib_stream());
+    out[0] = r.kappa_w;
+    out[1] = r.kappa_l;
+    out[2] = r.kappa_r;
+    out[3] = r.kappa_ext;
+    out[4] = r.kappa_tilde;
+    out[5] = r.bound;
+    out[6] = r.bound_holds ? 1.0 : 0.0;
+  });
+}
+
+int sbx_els_conditioning_report(sbx_els e, int dense, int iters, double* out) {
+  return guard([&] {
+    sbx::require(e && e->e, "null els handle");
+    sbx::require(dense || iters >= 1, "conditioning: iteration count must be positive");
+    const sbx::CondReport r = sbx::els_conditioning(*e->e, iters, sbx::lib_stream(), dense != 0);
     out[0] = r.kappa_w;
     out[1] = r.kappa_l;
     out[2] = r.kappa_r;

@@ -7,47 +7,11 @@
 
 #include "dense.hpp"
 #include "els.hpp"
+#include "entries.hpp"
 #include "idengine.hpp"
+#include "svd.hpp"
 
 namespace sbx {
-
-std::vector<double> jacobi_singular_values(std::vector<double> a, i64 m, i64 n) {
-  require(m >= n, "jacobi_singular_values: expects m >= n");
-  const double tol = 1e-15;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    bool rotated = false;
-    for (i64 p = 0; p < n - 1; ++p)
-      for (i64 q = p + 1; q < n; ++q) {
-        double* ap = a.data() + p * m;
-        double* aq = a.data() + q * m;
-        double alpha = 0.0, beta = 0.0, gamma = 0.0;
-        for (i64 i = 0; i < m; ++i) {
-          alpha += ap[i] * ap[i];
-          beta += aq[i] * aq[i];
-          gamma += ap[i] * aq[i];
-        }
-        if (gamma == 0.0 || std::fabs(gamma) <= tol * std::sqrt(alpha * beta)) continue;
-        rotated = true;
-        const double zeta = (beta - alpha) / (2.0 * gamma);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-        for (i64 i = 0; i < m; ++i) {
-          const double x = ap[i], y = aq[i];
-          ap[i] = c * x - sn * y;
-          aq[i] = sn * x + c * y;
-        }
-      }
-    if (!rotated) break;
-  }
-  std::vector<double> sv(static_cast<size_t>(n));
-  for (i64 j = 0; j < n; ++j) {
-    double s2 = 0.0;
-    for (i64 i = 0; i < m; ++i) s2 += a[size_t(i + j * m)] * a[size_t(i + j * m)];
-    sv[size_t(j)] = std::sqrt(s2);
-  }
-  std::sort(sv.begin(), sv.end(), std::greater<double>());
-  return sv;
-}
 
 namespace {
 
@@ -61,23 +25,18 @@ double ratio(const std::vector<double>& sv, i64 k) {
   return lo > 0.0 ? sv[0] / lo : std::numeric_limits<double>::infinity();
 }
 
-// sigma_1 / sigma_k of a tall device matrix (M x k, ld M): the R factor of a
-// column-pivoted device QR carries the same singular values.
-double tall_factor_cond(const double* A, i64 M, i64 k, cudaStream_t s) {
+// sigma_1 / sigma_k of a device matrix of declared rank k (factor_cond,
+// els.cpp:216-222), by the device Jacobi SVD.
+double factor_cond_device(const double* A, i64 m, i64 n, i64 k, cudaStream_t s) {
   if (k == 0) return 1.0;
-  DevBuf<double> w(static_cast<size_t>(M * k));
-  SBX_CUDA(cudaMemcpyAsync(w.get(), A, size_t(M * k) * 8, cudaMemcpyDeviceToDevice, s));
-  IdBatch b;
-  b.factor({IdProblem{w.get(), int(M), int(k), int(M)}}, 1e-300, s);
-  std::vector<double> top(static_cast<size_t>(k * k));
-  SBX_CUDA(cudaMemcpy2DAsync(top.data(), size_t(k) * 8, w.get(), size_t(M) * 8, size_t(k) * 8, size_t(k),
-                             cudaMemcpyDeviceToHost, s));
-  SBX_CUDA(cudaStreamSynchronize(s));
-  const auto& perm = b.perm(0);
-  std::vector<double> R(static_cast<size_t>(k * k), 0.0);
-  for (i64 l = 0; l < k; ++l)
-    for (i64 i = 0; i <= l; ++i) R[size_t(i + l * k)] = top[size_t(i + i64(perm[size_t(l)]) * k)];
-  return ratio(jacobi_singular_values(std::move(R), k, k), k);
+  return ratio(singular_values_device(A, m, n, m, s), k);
+}
+
+// dense_cond (els.cpp:207-213): sigma_max / sigma_min.
+double dense_cond_device(const double* A, i64 n, cudaStream_t s) {
+  if (n == 0) return 1.0;
+  const auto sv = singular_values_device(A, n, n, n, s);
+  return sv.back() > 0.0 ? sv.front() / sv.back() : std::numeric_limits<double>::infinity();
 }
 
 // Largest singular value by power iteration on B B^T (linop.cpp:17-36).
@@ -117,18 +76,41 @@ double operator_norm(i64 n, F apply, Ft apply_t, int iters, std::uint64_t seed, 
 
 }  // namespace
 
-CondReport els_conditioning(Els& e, int iters, cudaStream_t s) {
+CondReport els_conditioning(Els& e, int iters, cudaStream_t s, bool dense) {
   CondReport r;
   const i64 k = e.k, n = e.n_ext();
   if (k > 0) {
-    std::vector<double> W(static_cast<size_t>(k * k));
-    e.Wmat.download(W.data(), W.size(), s);
-    SBX_CUDA(cudaStreamSynchronize(s));
-    r.kappa_w = ratio(jacobi_singular_values(std::move(W), k, k), k);  // dense_cond (els.cpp:207-213)
-    r.kappa_l = tall_factor_cond(e.L->get(), n, k, s);                 // factor_cond (els.cpp:216-222)
-    DevBuf<double> rt(static_cast<size_t>(n * k));                      // R^T: n x k
-    copy_batched({{e.R.get(), rt.get(), int(n), int(k), int(k), int(n), 1, 0}}, s);
-    r.kappa_r = tall_factor_cond(rt.get(), n, k, s);
+    r.kappa_w = dense_cond_device(e.Wmat.get(), k, s);          // dense_cond (els.cpp:230)
+    r.kappa_l = factor_cond_device(e.L->get(), n, k, k, s);     // factor_cond (els.cpp:231)
+    r.kappa_r = factor_cond_device(e.R.get(), k, n, k, s);      // factor_cond (els.cpp:232)
+  }
+  if (dense) {  // dense oracles (els.cpp:234-240): SVDs of Atilde and Atilde + L R
+    require(e.old_g && e.new_g, "conditioning_report: the ELS does not know its meshes");
+    require(n <= 12000, "conditioning_report: dense oracles are limited to 12000 unknowns (nystrom.cpp:13)");
+    DevBuf<double> A(static_cast<size_t>(n * n));
+    A.zero(s);
+    const i64 nkc = e.n_k + e.n_c;
+    std::vector<i64> oc = e.kept_old_s;
+    oc.insert(oc.end(), e.cut_s.begin(), e.cut_s.end());
+    DevBuf<i64> d_oc, d_p;
+    d_oc.upload(oc, s);
+    EntryOracle eo(*e.old_g, e.form, e.mu, s);
+    eo.submatrix(d_oc.get(), nkc, d_oc.get(), nkc, A.get(), n, s);
+    if (e.n_p > 0) {
+      d_p.upload(e.added_s, s);
+      EntryOracle en(*e.new_g, e.form, e.mu, s);
+      en.submatrix(d_p.get(), e.n_p, d_p.get(), e.n_p, A.get() + nkc + nkc * n, n, s);
+    }
+    DevBuf<double> X(static_cast<size_t>(n * n));
+    SBX_CUDA(cudaMemcpyAsync(X.get(), A.get(), size_t(n * n) * 8, cudaMemcpyDeviceToDevice, s));
+    r.kappa_tilde = dense_cond_device(A.get(), n, s);
+    if (k > 0)
+      gemm_batched({{e.L->get(), e.R.get(), X.get(), int(n), int(n), int(k), int(n), int(k), int(n), 0, 0, 1.0, 1.0}},
+                   s);
+    r.kappa_ext = dense_cond_device(X.get(), n, s);
+    r.bound = std::min(r.kappa_l * r.kappa_l, r.kappa_r * r.kappa_r) * r.kappa_ext * r.kappa_tilde;
+    r.bound_holds = r.kappa_w <= r.bound * 1.000001;
+    return r;
   }
   // estimator route (els.cpp:250-264): power iteration on the operators and
   // on their solves, seeds 1 and 2 (condition_estimate, linop.cpp:38-43)

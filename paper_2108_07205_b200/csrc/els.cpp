@@ -134,6 +134,12 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   const auto kept_old_s = scalars(plan.kept_old), cut_s = scalars(plan.cut_old);
   e->kept_new_s = scalars(plan.kept_new);
   e->added_s = scalars(plan.added_new);
+  e->kept_old_s = kept_old_s;
+  e->cut_s = cut_s;
+  e->old_g = &old_g;
+  e->new_g = &new_g;
+  e->form = form;
+  e->mu = mu;
   e->n_k = i64(kept_old_s.size());
   e->n_c = i64(cut_s.size());
   e->n_p = i64(e->added_s.size());

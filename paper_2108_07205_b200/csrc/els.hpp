@@ -56,6 +56,13 @@ struct Els {
   DevBuf<double> Wmat;              // k x k (I + R X), for inspection
   DevBuf<i64> d_old_of_ext;         // ext rows [0, n_k+n_c) -> old-mesh scalar
   std::vector<i64> kept_new_s, added_s;
+  std::vector<i64> kept_old_s, cut_s;
+  // the meshes and formulation it was built on (dense conditioning route);
+  // the caller keeps the geometry alive while it uses that route
+  const Geom* old_g = nullptr;
+  const Geom* new_g = nullptr;
+  int form = 0;
+  double mu = 1.0;
   i64 n_new = 0;
   // Per-stream solve workspaces: the solver is immutable after build, so
   // concurrent solves on distinct streams are legal.
@@ -109,10 +116,10 @@ struct CondReport {
   double kappa_w = 1.0, kappa_l = 1.0, kappa_r = 1.0, kappa_ext = 1.0, kappa_tilde = 1.0, bound = 1.0;
   bool bound_holds = true;
 };
-CondReport els_conditioning(Els& e, int iters, cudaStream_t s);
-// Singular values (descending) of a column-major m x n host matrix, m >= n
-// (one-sided Jacobi).
-std::vector<double> jacobi_singular_values(std::vector<double> a, i64 m, i64 n);
+// dense = true: the dense-oracle route (els.cpp:234-240): kappa_tilde and
+// kappa_ext from the singular values of the assembled Atilde and
+// Atilde + L R (device Jacobi SVD, n_ext <= 12000).
+CondReport els_conditioning(Els& e, int iters, cudaStream_t s, bool dense = false);
 
 // GMRES / PGMRES-Local on the refined system in (kept, added) unknowns
 // (gmres.cpp:14-126 driven like scenario.cpp:694-727): operator =

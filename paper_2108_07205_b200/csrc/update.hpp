@@ -36,6 +36,10 @@ std::unique_ptr<Update> update_compress_device(const Geom& old_g, const Geom& ne
                                                const Plan& plan, int formulation, double mu,
                                                double eps, std::uint64_t seed, cudaStream_t s);
 void update_download(const Update& u, int which, double* out, cudaStream_t s);
+// CompressionMode::SvdOptimal (lowrank.cpp:329-362): dense truncated SVDs of
+// the kc / kp / pk blocks, re-truncated through L1 (update_svd.cpp).
+std::unique_ptr<Update> update_svd_optimal_device(const Geom& old_g, const Geom& new_g, const Plan& plan,
+                                                  int formulation, double mu, double eps, cudaStream_t s);
 std::unique_ptr<Update> update_from_factors(const Plan& plan, const double* L, const double* R,
                                             i64 n_ext, i64 k, cudaStream_t s);
 
