@@ -132,6 +132,20 @@ int sbx_hbs_compress(sbx_geom g, int formulation, double mu, const sbx_hbs_optio
                      sbx_hbs* out);
 int sbx_hbs_compress_subset(sbx_geom g, int formulation, double mu, const int64_t* nodes,
                             int64_t n_nodes, const sbx_hbs_options* opts, sbx_hbs* out);
+/* hbs_compress over a caller-supplied entry oracle: the reference's plugin
+ * point HbsSource::entries (hbs.hpp:19-31), swapped in by its tests
+ * (test_hbs.cpp:186-245).  The geometry g still supplies the points (tree,
+ * proxy circles) and the source normals / weights / kernel roles of the
+ * proxy functionals; `entries` supplies every block the compression draws
+ * (leaf diagonal blocks, near rows of the IDs, sibling couplings): it fills
+ * the column-major nr x nc block of scalar indices (rows, cols), on the
+ * calling thread, and must not call back into the library.
+ * with_completion = 0 drops the rank-one completion functionals
+ * (HbsSource::row_null / col_null empty). */
+typedef void (*sbx_entries_fn)(void* ctx, const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                               double* out);
+int sbx_hbs_compress_custom(sbx_geom g, int formulation, double mu, sbx_entries_fn entries, void* ctx,
+                            int with_completion, const sbx_hbs_options* opts, sbx_hbs* out);
 int sbx_hbs_invert(sbx_hbs h);
 int sbx_hbs_destroy(sbx_hbs h);
 int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double* x,

@@ -110,6 +110,8 @@ _SIGS = [
     ("sbx_update_factor", C.c_int, [VP, C.c_int, F64P]),
     ("sbx_update_from_factors", C.c_int, [VP, F64P, F64P, I64, I64, C.POINTER(VP)]),
     ("sbx_dump_matrix", C.c_int, [C.c_char_p, F64P, I64, I64, I64]),
+    ("sbx_hbs_compress_custom", C.c_int, [VP, C.c_int, C.c_double, VP, VP, C.c_int,
+                                          C.POINTER(sbx_hbs_options), C.POINTER(VP)]),
     ("sbx_update_compress_mode", C.c_int, [VP, VP, VP, C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int,
                                            C.POINTER(VP)]),
     ("sbx_els_conditioning_report", C.c_int, [VP, C.c_int, C.c_int, F64P]),

@@ -288,10 +288,40 @@ class HbsOperator(_Handle):
         return out
 
 
+ENTRIES_FN = C.CFUNCTYPE(None, C.c_void_p, I64P, C.c_int64, I64P, C.c_int64, F64P)
+
+
 def hbs_compress(d: Discretization, formulation=INTERIOR_DIRICHLET, opts: HbsOptions | None = None,
-                 mu: float = 1.0, subset=None) -> HbsOperator:
+                 mu: float = 1.0, subset=None, entries=None, with_completion: bool = True) -> HbsOperator:
+    """hbs_compress(make_hbs_source(a), opts) (hbs.cpp:349-425).  entries:
+    the HbsSource::entries plugin (hbs.hpp:19-31) -- a callable
+    (rows, cols) -> (len(rows) x len(cols)) array over scalar indices that
+    replaces the kernel entries of every block the compression draws;
+    with_completion=False drops the completion functionals (row_null /
+    col_null empty)."""
     o = (opts or HbsOptions()).to_c()
     out = VP()
+    if entries is not None:
+        if subset is not None:
+            raise ValueError("hbs_compress: a custom entry oracle covers the whole discretization")
+        errs = []
+
+        def cb(_ctx, rows, nr, cols, nc, outp):
+            try:
+                r = np.ctypeslib.as_array(rows, shape=(nr,)).copy()
+                c = np.ctypeslib.as_array(cols, shape=(nc,)).copy()
+                blk = np.asarray(entries(r, c), dtype=np.float64).reshape(nr, nc)
+                np.ctypeslib.as_array(outp, shape=(nc, nr))[:] = blk.T  # column-major out
+            except BaseException as e:  # noqa: BLE001  (re-raised after the C call)
+                errs.append(e)
+
+        fn = ENTRIES_FN(cb)
+        code = lib().sbx_hbs_compress_custom(d.ptr, formulation, mu, C.cast(fn, VP), None, int(bool(with_completion)),
+                                             C.byref(o), C.byref(out))
+        if errs:
+            raise errs[0]
+        check(code)
+        return HbsOperator(out)
     if subset is None:
         check(lib().sbx_hbs_compress(d.ptr, formulation, mu, C.byref(o), C.byref(out)))
     else:

@@ -326,6 +326,22 @@ int sbx_hbs_compress_subset(sbx_geom g, int formulation, double mu, const int64_
   });
 }
 
+int sbx_hbs_compress_custom(sbx_geom g, int formulation, double mu, sbx_entries_fn entries, void* ctx,
+                            int with_completion, const sbx_hbs_options* opts, sbx_hbs* out) {
+  return guard([&] {
+    sbx::require(entries != nullptr, "hbs_compress_custom: null entry oracle");
+    sbx::HostEntries he;
+    he.fn = reinterpret_cast<decltype(he.fn)>(entries);
+    he.ctx = ctx;
+    he.with_completion = with_completion != 0;
+    sbx::HbsBuildOptions o;
+    if (opts) o = sbx::HbsBuildOptions::from(*opts);
+    o.entries = &he;
+    auto h = sbx::hbs_compress_device(G(g), formulation, mu, nullptr, 0, o, sbx::lib_stream());
+    *out = new sbx_hbs_s{std::move(h)};
+  });
+}
+
 int sbx_hbs_invert(sbx_hbs h) {
   return guard([&] { sbx::hbs_invert_device(H(h), sbx::lib_stream()); });
 }

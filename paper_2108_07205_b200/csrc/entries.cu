@@ -505,4 +505,44 @@ void launch_near_jobs(const EntryView& v, const NearJob* d_jobs, int n_jobs, i64
   SBX_LAUNCHED();
 }
 
+std::vector<double> HostEntries::block(const i64* rows, i64 nr, const i64* cols, i64 nc) const {
+  std::vector<double> b(static_cast<size_t>(nr * nc), 0.0);
+  if (nr > 0 && nc > 0) fn(ctx, rows, nr, cols, nc, b.data());
+  return b;
+}
+
+void host_block_jobs(const HostEntries& h, const std::vector<BlockJob>& jobs, const std::vector<i64>& rows,
+                     const std::vector<i64>& cols, double* out, cudaStream_t s) {
+  for (const auto& j : jobs) {
+    require(j.dst_col_off < 0, "custom entries: scattered block columns are not supported");
+    if (j.nr == 0 || j.nc == 0) continue;
+    const auto b = h.block(rows.data() + j.row_off, j.nr, cols.data() + j.col_off, j.nc);
+    SBX_CUDA(cudaMemcpy2DAsync(out + j.out_off, size_t(j.ld) * 8, b.data(), size_t(j.nr) * 8, size_t(j.nr) * 8,
+                               size_t(j.nc), cudaMemcpyHostToDevice, s));
+    SBX_CUDA(cudaStreamSynchronize(s));  // b is a temporary
+  }
+}
+
+void host_near_jobs(const HostEntries& h, const std::vector<NearJob>& jobs, const std::vector<i64>& cand,
+                    const std::vector<i64>& near, double* out, cudaStream_t s) {
+  for (const auto& j : jobs) {
+    if (j.n == 0 || j.n_near == 0) continue;
+    const i64* c = cand.data() + j.cand_off;
+    const i64* nv = near.data() + j.near_off;
+    // W^T rows [out_off, out_off + n_near) x the n candidate columns:
+    // row ID (transpose 0): A(cand, near)^T; column ID: A(near, cand)
+    std::vector<double> wt(static_cast<size_t>(j.n_near) * j.n);
+    if (j.transpose == 0) {
+      const auto b = h.block(c, j.n, nv, j.n_near);  // n x n_near
+      for (int r = 0; r < j.n_near; ++r)
+        for (int q = 0; q < j.n; ++q) wt[size_t(r) + size_t(q) * j.n_near] = b[size_t(q) + size_t(r) * j.n];
+    } else {
+      wt = h.block(nv, j.n_near, c, j.n);
+    }
+    SBX_CUDA(cudaMemcpy2DAsync(out + j.out_off, size_t(j.ld) * 8, wt.data(), size_t(j.n_near) * 8,
+                               size_t(j.n_near) * 8, size_t(j.n), cudaMemcpyHostToDevice, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
 }  // namespace sbx

@@ -24,6 +24,19 @@ struct EntryView {
   int sl_qmax;
 };
 
+// A caller-supplied entry oracle (the reference's HbsSource::entries plugin,
+// hbs.hpp:19-31): fn fills the column-major nr x nc block of the scalar
+// indices (rows, cols) on the host.  with_completion = false drops the
+// rank-one completion functionals of the compression (HbsSource::row_null /
+// col_null left empty).
+struct HostEntries {
+  void (*fn)(void* ctx, const i64* rows, i64 nr, const i64* cols, i64 nc, double* out) = nullptr;
+  void* ctx = nullptr;
+  bool with_completion = true;
+  // column-major nr x nc block (host)
+  std::vector<double> block(const i64* rows, i64 nr, const i64* cols, i64 nc) const;
+};
+
 class EntryOracle {
  public:
   EntryOracle(const Geom& g, int formulation, double mu, cudaStream_t s,
@@ -99,5 +112,12 @@ struct NearJob {
 };
 void launch_near_jobs(const EntryView& v, const NearJob* d_jobs, int n_jobs, i64 max_entries,
                       const i64* d_cand, const i64* d_near, double* out, cudaStream_t s);
+
+// The same jobs through a caller-supplied entry oracle: blocks evaluated on
+// the host, copied into place (host index arrays of the jobs).
+void host_block_jobs(const HostEntries& h, const std::vector<BlockJob>& jobs, const std::vector<i64>& rows,
+                     const std::vector<i64>& cols, double* out, cudaStream_t s);
+void host_near_jobs(const HostEntries& h, const std::vector<NearJob>& jobs, const std::vector<i64>& cand,
+                    const std::vector<i64>& near, double* out, cudaStream_t s);
 
 }  // namespace sbx

@@ -215,8 +215,11 @@ void build_round(Builder& B, const std::vector<i64>& ids, const std::vector<int>
   dpj.upload(pj, B.s);
   dnj.upload(nj, B.s);
   launch_proxy_jobs(B.eo.view(), dpj.get(), int(pj.size()), max_rows, max_n, dcand.get(), R.wt.get(), B.s);
-  launch_near_jobs(B.eo.view(), dnj.get(), int(nj.size()), max_near, dcand.get(), dnear.get(),
-                   R.wt.get(), B.s);
+  if (B.o.entries)
+    host_near_jobs(*B.o.entries, nj, cand, nearv, R.wt.get(), B.s);
+  else
+    launch_near_jobs(B.eo.view(), dnj.get(), int(nj.size()), max_near, dcand.get(), dnear.get(),
+                     R.wt.get(), B.s);
   R.ids.factor(R.probs, 1e-15, B.s);  // keeps every row the forced-rank rule can use
 }
 
@@ -480,7 +483,9 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
   op->n = 2 * N;
   op->leaf_nodes = o.leaf_nodes;
   op->eps = o.eps;
-  Builder B{g, o, s, *op, eo, eo.has_nullspace(), {}, {}, {}, {}, 0};
+  require(!o.entries || !nodes, "hbs_compress: a custom entry oracle covers the whole discretization");
+  const bool with_null = eo.has_nullspace() && (!o.entries || o.entries->with_completion);
+  Builder B{g, o, s, *op, eo, with_null, {}, {}, {}, {}, 0};
   B.px.resize(size_t(N));
   B.py.resize(size_t(N));
   for (i64 i = 0; i < N; ++i) {
@@ -569,8 +574,10 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
     DevBuf<BlockJob> djobs;
     didx.upload(idx, s);
     djobs.upload(jobs, s);
-    launch_block_jobs(eo.view(), djobs.get(), int(jobs.size()), mx, didx.get(), didx.get(),
-                      dstore.get(), s);
+    if (o.entries)
+      host_block_jobs(*o.entries, jobs, idx, idx, dstore.get(), s);
+    else
+      launch_block_jobs(eo.view(), djobs.get(), int(jobs.size()), mx, didx.get(), didx.get(), dstore.get(), s);
     SBX_CUDA(cudaStreamSynchronize(s));
   }
 
@@ -776,8 +783,10 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
       dri.upload(ri, s);
       dci.upload(ci, s);
       dj.upload(jobs, s);
-      launch_block_jobs(eo.view(), dj.get(), int(jobs.size()), mx, dri.get(), dci.get(),
-                        st->buf.get(), s);
+      if (o.entries)
+        host_block_jobs(*o.entries, jobs, ri, ci, st->buf.get(), s);
+      else
+        launch_block_jobs(eo.view(), dj.get(), int(jobs.size()), mx, dri.get(), dci.get(), st->buf.get(), s);
       SBX_CUDA(cudaStreamSynchronize(s));
     }
     if (fz) {  // this level's inverse inputs are complete: hand it to the inversion thread

@@ -3,6 +3,7 @@
 // per-step path.
 #pragma once
 
+#include "entries.hpp"
 #include "geometry.hpp"
 #include "hbs.hpp"
 #include "sbx.h"
@@ -14,6 +15,9 @@ struct HbsBuildOptions {
   i64 leaf_nodes = 64;
   double bas_factor = 1.5;
   double div_factor = 3.0;
+  // caller-supplied entry oracle (HbsSource::entries plugin); null: the
+  // formulation's kernel entries on the device
+  const HostEntries* entries = nullptr;
   static HbsBuildOptions from(const sbx_hbs_options& o) {
     HbsBuildOptions b;
     b.eps = o.eps;
