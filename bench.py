@@ -648,6 +648,170 @@ def run_reference(args, rank, world):
     return line
 
 
+# ------------------------------------------------------------------ cfg4: transient channel
+def stokeslet_field(src, tg, mu=1.0):
+    """Velocity of Stokeslets (x, y, fx, fy) at targets (the exact solution the
+    boundary data come from; kernels.hpp Stokeslet, 1/(4 pi mu) normalisation)."""
+    out = np.zeros((len(tg), 2))
+    for x, y, fx, fy in src:
+        r = tg - np.array([x, y])
+        r2 = np.sum(r * r, 1)
+        lg = -0.5 * np.log(r2)
+        rf = r[:, 0] * fx + r[:, 1] * fy
+        out[:, 0] += (lg * fx + r[:, 0] * rf / r2) / (4 * np.pi * mu)
+        out[:, 1] += (lg * fy + r[:, 1] * rf / r2) / (4 * np.pi * mu)
+    return out
+
+
+def transient_schedule(cfg, steps):
+    """Indices into the 200-gap schedule: all of them, or `steps` evenly spaced."""
+    n = len(cfg.gaps())
+    if steps >= n:
+        return list(range(n))
+    return sorted(set(int(round(x)) for x in np.linspace(0, n - 1, steps)))
+
+
+def run_transient(args, rank, world, local_rank):
+    """BASELINE configs[3] (cfg4): one step = one time step of the transient on
+    the closed wavy channel (SBX_CHANNEL, 32768 nodes): the disk's proximity
+    picks the base panels to refine (m = ceil(max length / gap)); m = 1 is the
+    identity plan (plain hbs_solve); else refine -> compress_update ->
+    els_build -> els_solve with one Stokeslet RHS (scenario.cpp:844-915
+    without its cache).  Timed steps: the whole 200-gap schedule for
+    --steps >= 200, else --steps evenly spaced gaps.  Replicas for N > 1."""
+    import torch
+    import paper_2108_07205_b200 as sb
+    from paper_2108_07205_b200.configs import CONFIGS
+    cfg = CONFIGS["cfg4"]
+    torch.cuda.set_device(local_rank)
+    sb.init(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    base = sb.panelize(cfg.curve(sb), cfg.n_panels, cfg.q)
+    t0 = time.perf_counter()
+    h = sb.hbs_invert(sb.hbs_compress(base, opts=sb.HbsOptions(eps=cfg.eps, leaf_nodes=cfg.leaf)))
+    sb.api.lib().sbx_sync()
+    t_static = time.perf_counter() - t0
+    nd = base.nodes()
+    plen = np.zeros(cfg.n_panels)
+    np.add.at(plen, nd["panel_of"], nd["w"])
+    src, tg = cfg.sources(), cfg.targets()
+    gaps = cfg.gaps()
+    g_base = sb.boundary_data(base, src)
+    g_base_dev = torch.from_numpy(g_base).cuda()
+    plans = [cfg.step_plan(nd, plen, g) for g in gaps]
+    stream = torch.cuda.ExternalStream(sb.api.lib().sbx_stream())
+
+    def step(i, dev=True):
+        near, m = plans[i]
+        if m <= 1:
+            with torch.cuda.stream(stream):
+                tau = sb.hbs_solve(h, g_base_dev if dev else g_base)
+            return base, tau, None, 0
+        g1, plan = sb.refine(base, near, m)
+        upd = sb.compress_update(base, g1, plan, cfg.eps)
+        els = sb.els_build(h, base, g1, plan, upd)
+        gn = sb.gather_kept_added(plan, sb.boundary_data(g1, src))
+        with torch.cuda.stream(stream):
+            tau = sb.els_solve(els, torch.from_numpy(gn).cuda() if dev else gn)
+        return g1, tau, els, upd.k
+
+    sched = transient_schedule(cfg, args.steps)
+    for i in range(min(args.warmup, len(gaps))):
+        step(i)
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in sched:
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    f0 = time.perf_counter()  # e2e: host RHS in, density out (library copies)
+    for i in sched:
+        _, tau, _, _ = step(i, dev=False)
+    e2e_s = time.perf_counter() - f0
+    # verification (untimed): velocity at fluid targets vs the generating Stokeslets
+    exact = stokeslet_field(src, tg)
+    worst, ks, n_ref = 0.0, [], 0
+    for i in sched:
+        geom, tau, els, k = step(i)
+        tau = tau.cpu().numpy() if hasattr(tau, "cpu") else tau
+        dens = sb.density_on_refined(els, tau) if els is not None else tau
+        vel, _, _ = sb.evaluate_solution(geom, sb.INTERIOR_DIRICHLET, dens, tg)
+        worst = max(worst, float(np.max(np.linalg.norm(vel - exact, axis=1) / np.linalg.norm(exact, axis=1))))
+        ks.append(k)
+        n_ref += els is not None
+    times = torch.tensor([ms / 1e3, e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    t_dev, t_e2e = times.tolist()
+    if rank != 0:
+        return None
+    K = len(sched)
+    line = {
+        "metric": METRIC, "value": round(world * K / t_dev, 3), "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / K, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg4: closed wavy channel y=+/-(1+0.2 sin(2 pi x/4)), x in [0,8], polynomial "
+                               "caps (SBX_CHANNEL), 2048x16 nodes, eps 1e-10, leaf 64; disk r=0.1 rising to "
+                               "the crest, gap 0.5 -> 0.005 over 200 steps, 1 Stokeslet RHS per step",
+                   "timed_gaps": f"{K} of the 200-step schedule", "refined_steps": n_ref,
+                   "l2": "each refined step streams new factors (> L2)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "details": {"t_static_s": round(t_static, 3), "max_k": int(max(ks)),
+                    "max_rel_velocity_error": worst},
+        "e2e": {"value": round(world * K / t_e2e, 3), "unit": UNIT, "path": "host RHS in / density out",
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_transient(cfg, sb, plans, sched)
+    return line
+
+
+def cpu_baseline_transient(cfg, sb, plans, sched, n_ref=2, n_id=4):
+    """The oracle on 1 host core over a bounded sample of the schedule: n_ref
+    refined steps (the smallest gaps) and n_id identity-plan steps, each
+    timed; the schedule's time is extrapolated from the two means."""
+    from oracle import pyoracle as po
+    po.build()
+    cv = cfg.curve(sb)
+    o0 = po.Geom.create(po.CHANNEL, cfg.n_panels, cfg.q, center=cv.center, scale=cv.scale, prongs=cv.n_prongs,
+                        amplitude=cv.amplitude, aspect=cv.aspect, cos_coef=cv.cos_coef, sin_coef=cv.sin_coef)
+    a0 = po.Assembler.create(o0)
+    t0 = time.perf_counter()
+    oh = po.Hbs.compress(a0, cfg.eps).invert()
+    t_static = time.perf_counter() - t0
+    src = cfg.sources()
+    g0 = o0.boundary_data(src)
+    ref = [i for i in sched if plans[i][1] > 1][-n_ref:]
+    ids = [i for i in sched if plans[i][1] <= 1][:n_id]
+    tr, ti = [], []
+    for i in ref:
+        near, m = plans[i]
+        s0 = time.perf_counter()
+        o1, op = o0.refine(near, m)
+        a1 = po.Assembler.create(o1)
+        ou = po.Update.compress(a0, a1, op, cfg.eps)
+        oe = po.Els.build(oh, a0, a1, op, ou)
+        oe.solve(po.gather_kept_added(op.maps(), o1.boundary_data(src)))
+        tr.append(time.perf_counter() - s0)
+    for _ in ids:
+        s0 = time.perf_counter()
+        oh.solve(g0)
+        ti.append(time.perf_counter() - s0)
+    n_r = sum(1 for i in sched if plans[i][1] > 1)
+    total = n_r * (np.mean(tr) if tr else 0.0) + (len(sched) - n_r) * (np.mean(ti) if ti else 0.0)
+    return {"value": round(len(sched) / total, 4), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{len(tr)} refined + {len(ti)} identity-plan steps timed on 1 core "
+                      f"(means {np.mean(tr):.2f} s / {np.mean(ti) * 1e3:.1f} ms), extrapolated to the "
+                      f"{len(sched)} timed steps ({n_r} refined); static HBS excluded ({t_static:.1f} s)"}
+
+
 def main():
     # the JSON line must be the only stdout output (NCCL's version banner is a log line)
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
@@ -656,6 +820,8 @@ def main():
     rank, world, local_rank = dist_env()
     if args.impl == "reference":
         line = run_reference(args, rank, world)
+    elif args.config == "cfg4":
+        line = run_transient(args, rank, world, local_rank)
     else:
         line = run_ours(args, rank, world, local_rank)
     if line is not None:

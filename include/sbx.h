@@ -41,8 +41,18 @@ enum {
   SBX_RUNTIME_ERROR = 7       /* any other std::runtime_error (e.g. HBS1 I/O) */
 };
 
-/* Curve kinds (geometry.hpp:10 CurveKind) and formulations (kernels.hpp:35). */
-enum { SBX_CIRCLE = 0, SBX_ELLIPSE = 1, SBX_STAR = 2, SBX_FOURIER = 3 };
+/* Curve kinds (geometry.hpp:10 CurveKind) and formulations (kernels.hpp:35).
+ * SBX_CHANNEL extends the reference's radial kinds with the closed wavy
+ * channel of BASELINE configs[3] (in units of h = scale, shifted by center):
+ * walls Y = -/+(1 + a sin(k X)), X in [0, Lam] (a = amplitude, Lam = aspect,
+ * k = 2 pi n_prongs / Lam), closed by two degree-9 polynomial caps whose
+ * coefficients are cos_coef[0..9] (X) and [10..19] (Y) of the right cap,
+ * [20..29] / [30..39] of the left cap (chosen so the caps join the walls
+ * with matching derivatives up to the fourth).  t in [0, 2 pi) runs bottom
+ * wall, right cap, top wall, left cap over the fractions sin_coef[0],
+ * sin_coef[1], sin_coef[0], 1 - 2 sin_coef[0] - sin_coef[1] (multiples of
+ * 1/n_panels put the joins on panel ends). */
+enum { SBX_CIRCLE = 0, SBX_ELLIPSE = 1, SBX_STAR = 2, SBX_FOURIER = 3, SBX_CHANNEL = 4 };
 enum { SBX_INTERIOR_DIRICHLET = 0, SBX_EXTERIOR_COMBINED = 1, SBX_MIXED = 2 };
 
 /* Sweep flags. */

@@ -91,6 +91,19 @@ int orc_geom_create(int kind, double cx, double cy, double scale, int prongs, do
   });
 }
 
+// Any curve kind with its coefficient lists (Fourier / Channel).
+int orc_geom_create_curve(int kind, double cx, double cy, double scale, int prongs, double amp, double aspect,
+                          int n_cos, const double* cos_coef, int n_sin, const double* sin_coef, int n_panels, int q,
+                          void** out) {
+  return guard([&] {
+    CurveParams cp = curve_params(kind, cx, cy, scale, prongs, amp, aspect, 0);
+    cp.cos_coef.assign(cos_coef, cos_coef + n_cos);
+    cp.sin_coef.assign(sin_coef, sin_coef + n_sin);
+    Curve c(cp);
+    *out = new GeomH{std::make_shared<Discretization>(panelize(c, n_panels, q))};
+  });
+}
+
 // holes: per hole (cx, cy, radius, n_panels, q) as doubles.
 int orc_geom_add_holes(void* wall, int nh, const double* holes, void** out_geom, void** out_plan) {
   return guard([&] {

@@ -127,7 +127,9 @@ inline V2 operator*(double s, V2 a) { return {s * a.x, s * a.y}; }
 inline double dot(V2 a, V2 b) { return a.x * b.x + a.y * b.y; }
 inline double norm(V2 a) { return std::sqrt(a.x * a.x + a.y * a.y); }
 
-enum class CurveKind { Circle = 0, Ellipse = 1, Star = 2, Fourier = 3 };
+// Channel (4): the closed wavy channel of BASELINE configs[3] (sbx.h SBX_CHANNEL;
+// the reference has no such kind).
+enum class CurveKind { Circle = 0, Ellipse = 1, Star = 2, Fourier = 3, Channel = 4 };
 
 struct CurveParams {  // geometry.hpp:14-26
   CurveKind kind = CurveKind::Circle;
@@ -144,6 +146,7 @@ struct Curve {  // geometry.cpp:11-110
   CurveParams p;
   explicit Curve(CurveParams params);
   void radial(double t, double& r, double& dr, double& ddr) const;
+  void channel(double t, double& px, double& py, double& dx, double& dy, double& ddx, double& ddy) const;
   V2 position(double t) const;
   V2 derivative(double t) const;
   V2 second_derivative(double t) const;

@@ -22,7 +22,7 @@ I64P = C.POINTER(C.c_int64)
 F64P = C.POINTER(C.c_double)
 VPP = C.POINTER(C.c_void_p)
 
-CIRCLE, ELLIPSE, STAR, FOURIER = 0, 1, 2, 3
+CIRCLE, ELLIPSE, STAR, FOURIER, CHANNEL = 0, 1, 2, 3, 4
 INTERIOR, EXTERIOR, MIXED = 0, 1, 2
 BLOCKS = {"kk": 0, "kc": 1, "ck": 2, "cc": 3, "kp": 4, "pk": 5, "pp": 6}
 
@@ -91,8 +91,15 @@ class Geom(_Handle):
 
     @staticmethod
     def create(kind, n_panels, q=16, center=(0.0, 0.0), scale=1.0, prongs=0, amplitude=0.0,
-               aspect=1.0):
+               aspect=1.0, cos_coef=(), sin_coef=()):
         p = C.c_void_p()
+        if cos_coef or sin_coef:
+            cc, cp = _f(np.asarray(cos_coef, dtype=np.float64).reshape(-1))
+            ss, sp = _f(np.asarray(sin_coef, dtype=np.float64).reshape(-1))
+            _chk(lib().orc_geom_create_curve(kind, C.c_double(center[0]), C.c_double(center[1]),
+                                             C.c_double(scale), prongs, C.c_double(amplitude), C.c_double(aspect),
+                                             len(cc), cp, len(ss), sp, n_panels, q, C.byref(p)))
+            return Geom(p)
         _chk(lib().orc_geom_create(kind, C.c_double(center[0]), C.c_double(center[1]),
                                    C.c_double(scale), prongs, C.c_double(amplitude),
                                    C.c_double(aspect), n_panels, q, C.byref(p)))

@@ -5,10 +5,10 @@ Public API mirrors the reference C++ solver (proj/include/stokesbie): see
 kernels behind the C-ABI of ``include/sbx.h``).
 """
 from .api import (  # noqa: F401
-    CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR, SVD_OPTIMAL, TWO_STEP_ID,
+    CHANNEL, CIRCLE, ELLIPSE, EXTERIOR_COMBINED, FOURIER, INTERIOR_DIRICHLET, MIXED, STAR, SVD_OPTIMAL, TWO_STEP_ID,
     AppBlockSolver, UpdateCache, CurveParams, Discretization, ElsSolver, HbsOperator, HbsOptions, LowRankUpdate,
     RefinementPlan, add_holes, app_build, boundary_data, circle, coarsen, compress_update, density_on_refined,
-    ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,
+    channel, ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,
     evaluate_solution,
     gather_kept_added, hbs_apply, hbs_compress, hbs_invert, hbs_load, hbs_save, hbs_solve, init, kernel_launches, panelize, refine, row_id,
     star, submatrix, update_from_factors, update_dump, update_load, dump_matrix, load_matrix,

@@ -34,7 +34,7 @@ import numpy as np
 from . import _sbx
 from ._sbx import F64P, I64P, VP, check, lib
 
-CIRCLE, ELLIPSE, STAR, FOURIER = 0, 1, 2, 3
+CIRCLE, ELLIPSE, STAR, FOURIER, CHANNEL = 0, 1, 2, 3, 4
 INTERIOR_DIRICHLET, EXTERIOR_COMBINED, MIXED = 0, 1, 2
 
 _initialized = False
@@ -87,6 +87,45 @@ def ellipse(a: float, b: float, center=(0.0, 0.0)) -> CurveParams:
 
 def star(n_prongs: int, amplitude: float, scale=1.0, center=(0.0, 0.0)) -> CurveParams:
     return CurveParams(kind=STAR, center=center, scale=scale, n_prongs=n_prongs, amplitude=amplitude)
+
+
+def channel(length: float = 8.0, half_width: float = 1.0, amplitude: float = 0.2, periods: int = 2,
+            cap_speed: float = 3.0, fractions=(45 / 128, 21 / 128), center=(0.0, 0.0)) -> CurveParams:
+    """The closed wavy channel of BASELINE configs[3] (sbx.h SBX_CHANNEL):
+    walls y = -/+ h (1 + a sin(2 pi periods x / length)), x in [0, length],
+    closed by degree-9 polynomial caps that continue the walls with matching
+    derivatives up to the fourth (position, tangent, curvature and its first
+    two derivatives are continuous).  cap_speed scales the caps' parameter
+    speed against the walls' (their bulge); fractions (bottom / top wall,
+    right cap) of the parameter circle are multiples of 1/128, so any panel
+    count divisible by 128 puts the four joins on panel ends."""
+    from math import factorial
+    lam_len = length / half_width
+    k = 2 * np.pi * periods / lam_len
+
+    def wall(top, x, d):  # d-th x-derivative of (X, Y) on the scaled top / bottom wall
+        X = x if d == 0 else (1.0 if d == 1 else 0.0)
+        ph = (np.sin, np.cos, lambda z: -np.sin(z), lambda z: -np.cos(z))[d % 4]
+        Y = (1.0 + amplitude * np.sin(k * x)) if d == 0 else amplitude * k ** d * ph(k * x)
+        return np.array([X, Y if top else -Y])
+
+    def cap(P0, P1):  # degree-9 polynomial with 5 derivative conditions at u = 0 and u = 1
+        A, b = [], []
+        for u, P in ((0.0, P0), (1.0, P1)):
+            for d in range(5):
+                A.append([factorial(j) / factorial(j - d) * u ** (j - d) if j >= d else 0.0 for j in range(10)])
+                b.append(P[d])
+        return np.linalg.solve(np.array(A), np.array(b))  # (10, 2)
+
+    lam = cap_speed
+    right = cap([wall(False, lam_len, d) * lam ** d for d in range(5)],
+                [wall(True, lam_len, d) * (-lam) ** d for d in range(5)])
+    left = cap([wall(True, 0.0, d) * (-lam) ** d for d in range(5)],
+               [wall(False, 0.0, d) * lam ** d for d in range(5)])
+    coef = np.concatenate([right[:, 0], right[:, 1], left[:, 0], left[:, 1]])
+    return CurveParams(kind=CHANNEL, center=center, scale=half_width, n_prongs=int(periods),
+                       amplitude=amplitude, aspect=lam_len, cos_coef=[float(c) for c in coef],
+                       sin_coef=[float(fractions[0]), float(fractions[1])])
 
 
 def circle(radius=1.0, center=(0.0, 0.0)) -> CurveParams:

@@ -162,64 +162,40 @@ class HolesConfig:
 
 @dataclass
 class ChannelConfig:
-    """configs[3]: transient sequence on a wavy channel closed into a smooth
-    curve.  The reference has no general parametric curve,
-    so the channel y = +/-(1 + 0.2 sin(2 pi x / 4)), x in [0, 8], with round
-    end caps is represented as a radial Fourier curve about (4, 0) (the
-    reference's CurveKind::Fourier, geometry.cpp:49-63): 64 sigma-smoothed
-    modes of the polar radius of that shape.  2048 panels x 16 nodes.  A disk
-    of radius 0.1 (a proximity trigger only, never discretized, as in
-    scenario.cpp:773-788) approaches the right end cap along y = 0 (where the
-    equal-parameter panels of the radial curve are longest, ~0.015), the gap
+    """configs[3]: transient sequence on the wavy channel y = +/-(1 + 0.2
+    sin(2 pi x / 4)), x in [0, 8], closed by smooth end caps -- the curve
+    kind SBX_CHANNEL (api.channel: degree-9 polynomial caps continuing the
+    walls with matching derivatives up to the fourth; the reference has only
+    radial curves, geometry.cpp:36-69, so this kind is added to the oracle
+    and the device alike).  2048 panels x 16 nodes (32768 nodes), the four
+    joins on panel ends.  A disk of radius 0.1 (a proximity trigger only,
+    never discretized, as in scenario.cpp:773-788) rises along x = 5 towards
+    the crest of the top wall (y = 1.2, horizontal tangent), the gap
     shrinking geometrically from 0.5 to 0.005 over 200 steps; each step
     refines the base panels within 5 gaps of the disk so panel length is at
-    most the gap (m = ceil(max length / gap)) and solves one Stokeslet RHS."""
+    most the gap (m = ceil(max length / gap); m = 1 keeps the base mesh:
+    identity plan, plain hbs_solve) and solves one Stokeslet RHS."""
     name: str = "cfg4"
     n_panels: int = 2048
     q: int = 16
-    modes: int = 64
     eps: float = 1e-10
     leaf: int = 64
     steps: int = 200
     gap0: float = 0.5
     gap1: float = 0.005
     disk_radius: float = 0.1
+    disk_x: float = 5.0
+    crest_y: float = 1.2
     seed: int = 0
 
-    def shape_inside(self, x, y):
-        h = 1.0 + 0.2 * np.sin(2 * np.pi * x / 4.0)
-        if 0.0 <= x <= 8.0:
-            return abs(y) < h
-        if x < 0.0:
-            return x * x + y * y < 1.0
-        return (x - 8.0) ** 2 + y * y < 1.0
-
-    def fourier(self):
-        """(scale, cos_coef, sin_coef) of the radial curve about (4, 0)."""
-        m = 2048
-        th = 2 * np.pi * np.arange(m) / m
-        r = np.empty(m)
-        for i, t in enumerate(th):
-            c, s_ = np.cos(t), np.sin(t)
-            lo = 0.0
-            while self.shape_inside(4 + (lo + 0.002) * c, (lo + 0.002) * s_):
-                lo += 0.002
-            hi = lo + 0.002
-            for _ in range(50):
-                mid = 0.5 * (lo + hi)
-                if self.shape_inside(4 + mid * c, mid * s_):
-                    lo = mid
-                else:
-                    hi = mid
-            r[i] = 0.5 * (lo + hi)
-        F = np.fft.rfft(r) / m
-        a0 = F[0].real
-        k = np.arange(1, self.modes + 1)
-        sig = np.sinc(k / (self.modes + 1))  # Lanczos sigma factors against Gibbs ringing
-        return a0, list(2 * F[1:self.modes + 1].real * sig / a0), list(-2 * F[1:self.modes + 1].imag * sig / a0)
+    def curve(self, sb):
+        return sb.channel(length=8.0, half_width=1.0, amplitude=0.2, periods=2)
 
     def gaps(self):
         return self.gap0 * (self.gap1 / self.gap0) ** (np.arange(self.steps) / (self.steps - 1))
+
+    def disk_center(self, gap):
+        return np.array([self.disk_x, self.crest_y - self.disk_radius - gap])
 
     def sources(self):
         rng = np.random.default_rng(self.seed)
@@ -228,8 +204,15 @@ class ChannelConfig:
         return np.column_stack([pts, rng.standard_normal((len(pts), 2))])
 
     def targets(self):
-        xs = np.linspace(1.5, 6.5, 6)
-        return np.array([(x, y) for x in xs for y in (-0.3, 0.0, 0.3)])
+        return np.array([(x, y) for x in (1.5, 2.5, 3.5, 6.5) for y in (-0.5, 0.0, 0.5)])
+
+    def step_plan(self, nodes, plen, gap):
+        """(base panels to refine, m) for the disk at this gap."""
+        c = self.disk_center(gap)
+        d = np.hypot(nodes["x"] - c[0], nodes["y"] - c[1]) - self.disk_radius
+        near = np.unique(nodes["panel_of"][d < 5 * gap])
+        m = int(np.ceil(np.max(plen[near]) / gap)) if len(near) else 1
+        return near, m
 
 
 CONFIGS = {

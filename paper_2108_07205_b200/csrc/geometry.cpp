@@ -62,7 +62,15 @@ void check_curve(const sbx_curve& p) {  // geometry.cpp:11-34
     if (std::fabs(p.amplitude) >= 1.0) throw Error(3, "star amplitude must keep radius positive");
   }
   if (p.kind == SBX_ELLIPSE && p.aspect <= 0) throw Error(3, "ellipse aspect must be positive");
-  if (p.kind < 0 || p.kind > 3) throw Error(1, "unknown curve kind");
+  if (p.kind == SBX_CHANNEL) {
+    if (p.n_prongs < 1) throw Error(3, "channel needs at least one wave period");
+    if (std::fabs(p.amplitude) >= 1.0) throw Error(3, "channel amplitude must keep the width positive");
+    if (p.aspect <= 0) throw Error(3, "channel length must be positive");
+    if (p.n_cos != 40) throw Error(3, "channel needs its two degree-9 cap polynomials (40 coefficients)");
+    if (p.n_sin != 2 || !(p.sin_coef[0] > 0.0 && p.sin_coef[1] > 0.0 && 2.0 * p.sin_coef[0] + p.sin_coef[1] < 1.0))
+      throw Error(3, "channel parameter fractions must be positive and sum below 1");
+  }
+  if (p.kind < 0 || p.kind > 4) throw Error(1, "unknown curve kind");
   if (p.n_cos < 0 || p.n_cos > 64 || p.n_sin < 0 || p.n_sin > 64)
     throw Error(1, "fourier coefficient count out of range");
 }
@@ -80,6 +88,10 @@ const GaussTable& gauss_table(int q) {
 
 void CurveDef::eval(double t, double& px, double& py, double& dx, double& dy, double& ddx,
                     double& ddy) const {
+  if (p.kind == SBX_CHANNEL) {
+    channel_eval(t, px, py, dx, dy, ddx, ddy);
+    return;
+  }
   const double c = std::cos(t), s = std::sin(t);
   if (p.kind == SBX_ELLIPSE) {
     px = p.center_x + p.scale * c;
@@ -120,6 +132,63 @@ void CurveDef::eval(double t, double& px, double& py, double& dx, double& dy, do
   ddy = p.scale * (ddr * s + 2 * dr * c - r * s);
 }
 
+// The closed wavy channel (sbx.h SBX_CHANNEL), piecewise in t; the same
+// operations as the oracle's Curve::channel (oracle/geom.cpp), so nodes agree
+// bit for bit.
+void CurveDef::channel_eval(double t, double& px, double& py, double& dx, double& dy, double& ddx,
+                            double& ddy) const {
+  const double F = 2.0 * kPi, fw = p.sin_coef[0], fr = p.sin_coef[1], fl = 1.0 - 2.0 * fw - fr;
+  const double h = p.scale, Lam = p.aspect, a = p.amplitude, k = 2.0 * kPi * double(p.n_prongs) / Lam;
+  const double T0 = F * fw, T1 = T0 + F * fr, T2 = T1 + F * fw;
+  // scaled coordinates (X, Y), derivatives in t
+  double X, Y, X1, Y1, X2, Y2;
+  auto cap = [&](const double* cx, const double* cy, double u, double ud) {  // degree-9 polynomial piece
+    X = 0.0, Y = 0.0, X1 = 0.0, Y1 = 0.0, X2 = 0.0, Y2 = 0.0;
+    for (int j = 9; j >= 0; --j) {  // Horner for the value and both derivatives
+      X2 = X2 * u + 2.0 * X1;
+      Y2 = Y2 * u + 2.0 * Y1;
+      X1 = X1 * u + X;
+      Y1 = Y1 * u + Y;
+      X = X * u + cx[j];
+      Y = Y * u + cy[j];
+    }
+    X1 *= ud;
+    Y1 *= ud;
+    X2 *= ud * ud;
+    Y2 *= ud * ud;
+  };
+  if (t < T0 || t >= T2 + F * fl) {  // bottom wall, left to right (t >= 2 pi wraps)
+    const double tt = t < T0 ? t : t - F;
+    const double xd = Lam / (F * fw);
+    X = tt * xd;
+    const double sn = std::sin(k * X), cs = std::cos(k * X);
+    Y = -(1.0 + a * sn);
+    X1 = xd;
+    Y1 = -a * k * cs * xd;
+    X2 = 0.0;
+    Y2 = a * k * k * sn * xd * xd;
+  } else if (t < T1) {  // right cap, bottom to top
+    cap(p.cos_coef, p.cos_coef + 10, (t - T0) / (F * fr), 1.0 / (F * fr));
+  } else if (t < T2) {  // top wall, right to left
+    const double xd = -Lam / (F * fw);
+    X = Lam + (t - T1) * xd;
+    const double sn = std::sin(k * X), cs = std::cos(k * X);
+    Y = 1.0 + a * sn;
+    X1 = xd;
+    Y1 = a * k * cs * xd;
+    X2 = 0.0;
+    Y2 = -a * k * k * sn * xd * xd;
+  } else {  // left cap, top to bottom
+    cap(p.cos_coef + 20, p.cos_coef + 30, (t - T2) / (F * fl), 1.0 / (F * fl));
+  }
+  px = p.center_x + h * X;
+  py = p.center_y + h * Y;
+  dx = h * X1;
+  dy = h * Y1;
+  ddx = h * X2;
+  ddy = h * Y2;
+}
+
 namespace {
 
 void curve_checks(const CurveDef& cv) {  // positive radius / nonvanishing speed (geometry.cpp:20-33)
@@ -128,7 +197,7 @@ void curve_checks(const CurveDef& cv) {  // positive radius / nonvanishing speed
     const double t = 2 * kPi * i / 2048.0;
     double px, py, dx, dy, ddx, ddy;
     cv.eval(t, px, py, dx, dy, ddx, ddy);
-    if (cv.p.kind != SBX_ELLIPSE) {
+    if (cv.p.kind != SBX_ELLIPSE && cv.p.kind != SBX_CHANNEL) {
       const double rr = std::hypot(px - cv.p.center_x, py - cv.p.center_y) / cv.p.scale;
       if (rr <= 1e-6) throw Error(3, "curve radius vanishes");
     }

@@ -21,6 +21,8 @@ struct CurveDef {
   sbx_curve p;
   void eval(double t, double& px, double& py, double& dx, double& dy, double& ddx,
             double& ddy) const;
+  void channel_eval(double t, double& px, double& py, double& dx, double& dy, double& ddx,
+                    double& ddy) const;
 };
 
 struct PanelDef {

@@ -379,3 +379,49 @@ def test_els_holes_match_dense_mixed_oracle(po):  # test_els.cpp:168-197
     vel = g1.evaluate_velocity(po.MIXED, density_on_refined(maps, g1.n_nodes, tau), HOLE_TARGETS)
     exact = po.field_velocity(srcs, HOLE_TARGETS)
     assert max(np.linalg.norm(vel[i] - exact[i]) / np.linalg.norm(exact[i]) for i in range(3)) < 1e-8
+
+
+def _channel_geom(po, n_panels):
+    import paper_2108_07205_b200 as sb  # host-only helper: the cap polynomials (numpy)
+    cv = sb.channel()
+    return cv, po.Geom.create(po.CHANNEL, n_panels, center=cv.center, scale=cv.scale, prongs=cv.n_prongs,
+                              amplitude=cv.amplitude, aspect=cv.aspect, cos_coef=cv.cos_coef,
+                              sin_coef=cv.sin_coef)
+
+
+def test_channel_curve_geometry(po):
+    """BASELINE configs[3]'s closed wavy channel (SBX_CHANNEL): wall nodes lie on
+    y = -/+(1 + 0.2 sin(2 pi x / 4)), the caps stay outside x in [0, 8], the
+    four joins sit on panel ends, and tangent, curvature and its derivative
+    are continuous across them."""
+    cv, o = _channel_geom(po, 256)
+    nd = o.nodes()
+    x, y, kap, pan = nd["x"], nd["y"], nd["curvature"], nd["panel_of"]
+    # panel ranges of the four pieces (fractions 45/128, 21/128, 45/128, 17/128)
+    n = 256
+    b0, b1, b2 = 45 * n // 128, (45 + 21) * n // 128, (90 + 21) * n // 128
+    wall = (pan < b0) | ((pan >= b1) & (pan < b2))
+    assert np.max(np.abs(np.abs(y[wall]) - (1 + 0.2 * np.sin(np.pi * x[wall] / 2)))) < 1e-14
+    assert np.all((x[wall] > 0) & (x[wall] < 8))
+    caps = ~wall
+    assert np.all((x[caps] < 1e-12) | (x[caps] > 8 - 1e-12))
+    # curvature is smooth across each join: the nodes either side extrapolate to the same value
+    for bj in (b0, b1, b2, n):
+        left = kap[pan == (bj - 1) % n][-3:]
+        right = kap[pan == bj % n][:3]
+        jump = abs((2 * left[-1] - left[-2]) - (2 * right[0] - right[1]))
+        assert jump < 5e-3 * (1 + abs(left[-1])), (bj, left, right)
+
+
+def test_channel_hbs_manufactured_field(po):  # test_hbs.cpp:159-184 on the channel
+    _, o = _channel_geom(po, 256)
+    a = po.Assembler.create(o)
+    h = po.Hbs.compress(a, 1e-10).invert()
+    src = np.array([[x, yy, f1, f2] for (x, yy), (f1, f2) in
+                    zip([(1.0, -2.6), (3.0, 2.6), (5.0, -2.6), (7.0, 2.6), (-2.5, 0.3), (10.5, -0.4)],
+                        [(1.0, 0.5), (-0.3, 1.2), (0.7, -0.8), (-1.1, 0.2), (0.4, 0.9), (0.6, -0.5)])])
+    tau = h.solve(o.boundary_data(src))
+    tg = np.array([(x, yy) for x in (1.5, 3.5, 6.5) for yy in (-0.5, 0.0, 0.5)] + [(-0.4, 0.0), (8.5, 0.1)])
+    u = o.evaluate_velocity(po.INTERIOR, tau, tg)
+    ref = po.field_velocity(src, tg)
+    assert np.max(np.linalg.norm(u - ref, axis=1) / np.linalg.norm(ref, axis=1)) < 1e-9
