@@ -59,6 +59,12 @@ void cpqr_cluster_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // M <= 1088): returns the layout index (G set) or -1 when it does not apply.
 int cpqr_reg_config(int M, int n, int* G);
 void cpqr_reg_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Row-split cluster CPQR (engine 7, cpqr_rows.cu): one tall problem (M >= 2n)
+// per cluster of G <= 8 CTAs, each holding a row slab in shared memory; the
+// column norms are replicated, so a step needs two O(n) DSMEM exchanges.
+// cpqr_rows_cluster gives the smallest G that fits (0: not applicable).
+int cpqr_rows_cluster(int M, int n);
+void cpqr_rows_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // Streaming one-CTA CPQR (M <= 1088): columns beyond the shared-memory slab
 // are updated in place in global memory (L2).
 bool cpqr_stream_ok(int M, int n);

@@ -56,7 +56,7 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
   KernelTimer kt("id_factor", s);  // every CPQR engine launch of the batch (bench: step-dominant family)
-  std::vector<QrJob> jobs, big, chip, clus, reg, strm;
+  std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
@@ -93,9 +93,17 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   static const bool log = std::getenv("SBX_ID_LOG") != nullptr;  // diagnostics
   static const bool no_cluster = std::getenv("SBX_NO_CLUSTER") != nullptr;  // diagnostics
   static const bool no_reg = std::getenv("SBX_NO_REG") != nullptr;          // diagnostics
+  // Few tall problems (the late rounds of the lockstep hierarchies): the
+  // row-split cluster engine (two O(n) DSMEM exchanges per step) beats the
+  // grid-barrier engine's per-step latency (measured on the replayed cfg2
+  // rounds of <= 19 problems: 0.65 -> 0.42 ms, 0.74 -> 0.39 ms, 0.85 -> 0.77 ms)
+  static const bool no_rows = std::getenv("SBX_NO_ROWS") != nullptr;  // diagnostics
+  bool rows_all = !no_rows && !crowded && !all.empty() && all.size() <= 24;
+  for (const auto& j : all) rows_all = rows_all && cpqr_rows_cluster(j.M, j.n) > 0;
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
+    if (engine == 0 && rows_all) engine = 7;
     if (engine == 0) {
       const int g = cpqr_smem_ctas(j.M, j.n);
       const bool chip_ok = !no_coop_flag() && g > 0 && g <= sms;
@@ -116,7 +124,13 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
       else engine = 1;
     }
     if (log) line += " " + std::to_string(j.M) + "x" + std::to_string(j.n) + "/e" + std::to_string(engine);
-    (engine == 2 ? big : engine == 3 ? chip : engine == 4 ? clus : engine == 5 ? reg : engine == 6 ? strm : jobs)
+    (engine == 2   ? big
+     : engine == 3 ? chip
+     : engine == 4 ? clus
+     : engine == 5 ? reg
+     : engine == 6 ? strm
+     : engine == 7 ? rows
+                   : jobs)
         .push_back(j);
   }
   if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
@@ -126,6 +140,7 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   cpqr_cluster_batched(clus, s);
   cpqr_reg_batched(reg, s);
   cpqr_stream_batched(strm, s);
+  cpqr_rows_batched(rows, s);
 }
 
 // ---------------------------------------------------------------- rendezvous

@@ -23,6 +23,7 @@ using namespace sbx;
 #ifdef SBX_CPQR_PROF
 namespace sbx {
 void cpqr_prof_dump();
+void cpqr_rows_prof_dump();
 }
 #endif
 
@@ -113,6 +114,12 @@ int replay(const char* dir, const std::vector<int>& engines) {
       int k0 = -1;
       std::string err;
       const float ms = time_batch(probs, engines[q], s, &k0, &err);
+#ifdef SBX_CPQR_PROF
+      std::printf("\n[first problem %dx%d]\n", probs[0].M, probs[0].n);
+      std::fflush(stdout);
+      if (engines[q] == 7) cpqr_rows_prof_dump();
+      else cpqr_prof_dump();
+#endif
       if (ms < 0) {
         std::printf("  e%d    n/a  ", engines[q]);
         total[q] = 1e30;

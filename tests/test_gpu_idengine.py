@@ -173,3 +173,25 @@ def test_row_id_tall_quad_tsqr(sb, po, shape):
     assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
     kf, Jf, Pf = sb.row_id(w, forced=min(k + 3, m), engine=1)
     assert np.array_equal(Jf[:kk], Jo[:kk])
+
+
+@pytest.mark.parametrize("shape", [(30, 257), (97, 257), (57, 513), (98, 513), (28, 1088), (112, 369),
+                                   (128, 767), (8, 64), (4, 9), (64, 3000)])
+def test_row_id_rows_engine(sb, po, shape):
+    """Row-split cluster CPQR (engine 7, cpqr_rows.cu) on tall W^T (functionals
+    >= 2 x candidates): same pivots and ranks as the oracle, exact skeleton
+    identity, forced-rank extension keeps the eps skeleton."""
+    m, n = shape
+    rng = np.random.default_rng(3 * m + n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=7)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    if k + 3 <= r:
+        kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=7)
+        assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
