@@ -134,13 +134,39 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
         .push_back(j);
   }
   if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
+  // The register-resident cluster engine and the one-CTA / TSQR engines
+  // hold no grid-wide barriers, so when a round has both they run side by
+  // side (the register engine on a forked stream) and share the chip's
+  // tail instead of following each other.
+  static const int fork_env = [] {
+    const char* e = std::getenv("SBX_ID_FORK");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool fork = fork_env != 0 && !reg.empty() && !jobs.empty();
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (fork) {
+    if (!side) {
+      SBX_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      SBX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      SBX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    SBX_CUDA(cudaEventRecord(ev_fork, s));
+    SBX_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+    {
+      StreamScope ss(side);
+      cpqr_reg_batched(reg, side);
+    }
+    SBX_CUDA(cudaEventRecord(ev_join, side));
+  }
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
   cpqr_smem_batched(chip, s);
   cpqr_cluster_batched(clus, s);
-  cpqr_reg_batched(reg, s);
+  if (!fork) cpqr_reg_batched(reg, s);
   cpqr_stream_batched(strm, s);
   cpqr_rows_batched(rows, s);
+  if (fork) SBX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
 }
 
 // ---------------------------------------------------------------- rendezvous
