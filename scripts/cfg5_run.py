@@ -37,8 +37,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--check-rhs", type=int, default=2)
+    ap.add_argument("--wall-panels", type=int, default=0, help="override the wall panel count")
+    ap.add_argument("--hole-panels", type=int, default=0, help="override the panels per hole")
+    ap.add_argument("--ppr", type=int, default=0, help="override the refined panels per region")
+    ap.add_argument("--m", type=int, default=0, help="override the split factor")
+    ap.add_argument("--arclength", action="store_true", help="BASELINE's equal arc-length split 9216 + 16 x 448")
     a = ap.parse_args()
+    import dataclasses
     c = CONFIGS["cfg5"]
+    if a.arclength:
+        c = dataclasses.replace(c, wall_panels=9216, hole_panels=448)
+    over = {k: v for k, v in (("wall_panels", a.wall_panels), ("hole_panels", a.hole_panels),
+                              ("panels_per_region", a.ppr), ("m", a.m)) if v}
+    if over:
+        c = dataclasses.replace(c, **over)
     sb.init(0)
     t0 = t()
     wall = sb.panelize(sb.ellipse(c.a, c.b), c.wall_panels, c.q)
@@ -53,6 +65,14 @@ def main():
           flush=True)
     panels = c.refine_panels(base.nodes())
     srcs = c.sources()
+    if a.check_rhs:  # the static inverse alone on the base mesh
+        tg = c.targets(20)
+        for j in range(a.check_rhs):
+            tau0 = sb.hbs_solve(h, sb.boundary_data(base, srcs[j]))
+            vel, _, _ = sb.evaluate_solution(base, sb.MIXED, tau0, tg)
+            ex = stokeslet_field(srcs[j], tg)
+            err = np.max(np.linalg.norm(vel - ex, axis=1) / np.linalg.norm(ex, axis=1))
+            print(f"  static rhs {j}: max relative velocity error {err:.2e}", flush=True)
     for step in range(a.steps):
         s0 = t()
         g1, plan = sb.refine(base, panels, c.m)
