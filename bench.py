@@ -268,15 +268,17 @@ def run_ours(args, rank, world, local_rank):
 
 def partitioned_bench(sb, torch, rank, world, g0, h, cfg0, reps=10):
     """The subtree partition of SURVEY.md 8(e) through the native path
-    (sbx_comm NCCL communicator, sbx_hbs_solve_sharded, sbx_els_shard_*):
-    (a) the cfg3 HBS-inverse apply (131072 unknowns) at nrhs 1/32/256 with
-    the tree split across the ranks (one NCCL all-gather of the subtree-root
-    hats per solve), and (b) the cfg2 Woodbury solve of the 64 RHS on the
-    same ownership (all-reduce of R y).  CUDA events on each rank's stream,
+    (sbx_comm NCCL communicator, sbx_hbs_compress_sharded,
+    sbx_hbs_solve_sharded, sbx_els_shard_*): (a) the cfg3 operator
+    (131072 unknowns) compressed, inverted and stored by subtree, and its
+    inverse applied at nrhs 1/32/256 with the tree split across the ranks
+    (one NCCL all-gather of the subtree-root hats per solve), and (b) the
+    cfg2 Woodbury solve of the 64 RHS on the same ownership (all-reduce of
+    R y).  CUDA events on each rank's stream,
     max over ranks; results checked against the single-GPU solve."""
     import statistics
     from paper_2108_07205_b200.configs import CONFIGS
-    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver, NativeShardedWoodbury
+    from paper_2108_07205_b200.parallel import Comm, NativeShardedSolver, NativeShardedWoodbury, compress_sharded
     import tempfile
     panels0 = cfg0.refine_panels(g0.nodes())
     comm = Comm.from_process_group() if world > 1 else Comm.loopback(1)[0]  # one rank: no NCCL needed
@@ -308,16 +310,26 @@ def partitioned_bench(sb, torch, rank, world, g0, h, cfg0, reps=10):
         torch.distributed.broadcast_object_list(tmp, src=0)
     d = Path(tmp[0])
     c3 = CONFIGS["cfg3"]
-    if rank == 0:
-        g3 = sb.panelize(sb.star(c3.prongs, c3.amplitude, c3.a), c3.n_panels, c3.q)
-        h3 = sb.hbs_invert(sb.hbs_compress(g3, opts=sb.HbsOptions(eps=c3.eps, leaf_nodes=c3.leaf)))
-        if world > 1:
-            sb.hbs_save(h3, d / "cfg3.hbs1")
-            sb.hbs_save(h, d / "cfg2.hbs1")
+    g3 = sb.panelize(sb.star(c3.prongs, c3.amplitude, c3.a), c3.n_panels, c3.q)
+    o3 = sb.HbsOptions(eps=c3.eps, leaf_nodes=c3.leaf)
+    # the cfg3 operator is compressed, inverted and stored by subtree
+    # (sbx_hbs_compress_sharded); the unsharded one is the reference answer
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    h3 = sb.hbs_invert(compress_sharded(g3, comm, opts=o3)) if world > 1 else sb.hbs_invert(sb.hbs_compress(g3, opts=o3))
+    torch.cuda.synchronize()
+    tb = torch.tensor([time.perf_counter() - t0], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(tb, op=torch.distributed.ReduceOp.MAX)
+    out["cfg3_build"] = {"s": round(tb.item(), 3), "arena_MB_per_rank": round(8e-6 * h3.info()["arena_doubles"], 1),
+                         "sharded": bool(h3.info()["sharded"])}
+    h3_full = sb.hbs_invert(sb.hbs_compress(g3, opts=o3)) if world > 1 else h3
+    if rank == 0 and world > 1:
+        sb.hbs_save(h, d / "cfg2.hbs1")
     if world > 1:
         torch.distributed.barrier()
         if rank != 0:
-            h3 = sb.hbs_load(d / "cfg3.hbs1")
             h = sb.hbs_load(d / "cfg2.hbs1")
     solver = NativeShardedSolver(h3, comm)
     r0, r1 = solver.rows
@@ -329,7 +341,7 @@ def partitioned_bench(sb, torch, rank, world, g0, h, cfg0, reps=10):
         bl = b[r0:r1].contiguous()
         ms = timed(lambda: solver.solve(bl))
         x = solver.solve(bl)
-        ref = sb.hbs_solve(h3, b)[r0:r1]
+        ref = sb.hbs_solve(h3_full, b)[r0:r1]
         err = (torch.linalg.norm(x - ref) / torch.linalg.norm(ref)).item()
         apply[f"rhs{nrhs}"] = {"ms": round(ms, 4), "solves_per_s": round(nrhs / (ms * 1e-3), 1),
                                "rel_err_vs_1gpu": err}

@@ -181,10 +181,12 @@ int sbx_hbs_solve_shard_down(sbx_hbs h, int G, int p, const double* hats, int64_
                              double* x_local, int64_t ldx, int flags, void* stream);
 int sbx_hbs_save_hbs1(sbx_hbs h, const char* path);
 int sbx_hbs_load_hbs1(const char* path, sbx_hbs* out);
-/* info[0..11]: n, nodes, total_skeleton, max_block_drawn, has_inverse,
+/* info[0..13]: n, nodes, total_skeleton, max_block_drawn, has_inverse,
  * solve_factor_doubles, max_depth, max_k, apply_factor_doubles, leaf_nodes,
  * top_depth, top_size (the solve's collapsed top: depth and K of the dense
- * map, 0 when every level runs; set once a solve plan exists) */
+ * map, 0 when every level runs; set once a solve plan exists),
+ * arena_doubles (the factors this handle stores on the device), sharded
+ * (1: a subtree-sharded operator, sbx_hbs_compress_sharded) */
 int sbx_hbs_info(sbx_hbs h, int64_t* info);
 int sbx_hbs_node_ranks(sbx_hbs h, int64_t* k, int64_t cap);
 
@@ -302,6 +304,15 @@ int sbx_update_cache_stats(sbx_update_cache c, int64_t* entries, int64_t* hits, 
  * the G subtree-root hats (the only exchange), top levels redundantly, local
  * down-sweep; b_local / x_local are this rank's rows (column-major). */
 int sbx_comm_unique_id(uint8_t* id128);
+/* hbs_compress over the subtree partition: every rank of
+ * the communicator set calls it; rank p compresses the nodes of its subtree
+ * and, redundantly, the top levels, exchanging each level's skeleton lists
+ * (and the subtree roots' couplings) through the communicator, and keeps
+ * only those factors.  sbx_hbs_invert then inverts the subtree and the top
+ * (the subtree roots' dhat blocks exchanged); the operator solves through
+ * sbx_hbs_solve_sharded on the same communicator, which must outlive it. */
+int sbx_hbs_compress_sharded(sbx_geom g, int formulation, double mu, const sbx_hbs_options* opts, sbx_comm c,
+                             sbx_hbs* out);
 int sbx_comm_create(const uint8_t* id128, int world, int rank, sbx_comm* out);
 int sbx_comm_create_loopback(int world, sbx_comm* members);
 int sbx_comm_destroy(sbx_comm c);

@@ -116,6 +116,8 @@ _SIGS = [
                                            C.POINTER(VP)]),
     ("sbx_els_conditioning_report", C.c_int, [VP, C.c_int, C.c_int, F64P]),
     ("sbx_comm_unique_id", C.c_int, [C.POINTER(C.c_uint8)]),
+    ("sbx_hbs_compress_sharded", C.c_int, [VP, C.c_int, C.c_double, C.POINTER(sbx_hbs_options), VP,
+                                           C.POINTER(VP)]),
     ("sbx_comm_create", C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.POINTER(VP)]),
     ("sbx_comm_create_loopback", C.c_int, [C.c_int, C.POINTER(VP)]),
     ("sbx_comm_destroy", C.c_int, [VP]),

@@ -309,11 +309,11 @@ class HbsOperator(_Handle):
     _destroy = "sbx_hbs_destroy"
 
     def info(self) -> dict:
-        out = np.zeros(12, dtype=np.int64)
+        out = np.zeros(14, dtype=np.int64)
         check(lib().sbx_hbs_info(self.ptr, out.ctypes.data_as(I64P)))
         keys = ("n", "nodes", "total_skeleton", "max_block_drawn", "has_inverse",
                 "factor_doubles", "max_depth", "max_k", "apply_factor_doubles", "leaf_nodes",
-                "top_L", "top_K")
+                "top_L", "top_K", "arena_doubles", "sharded")
         return dict(zip(keys, (int(v) for v in out)))
 
     @property

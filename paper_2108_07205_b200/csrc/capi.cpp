@@ -109,6 +109,10 @@ sbx::Geom& G(sbx_geom g) {
   sbx::require(g && g->g, "null geometry handle");
   return *g->g;
 }
+sbx::Collective& Cm(sbx_comm c) {
+  sbx::require(c && c->c, "null comm handle");
+  return *c->c;
+}
 sbx::HbsOp& H(sbx_hbs h) {
   sbx::require(h && h->h, "null hbs handle");
   return *h->h;
@@ -326,6 +330,17 @@ int sbx_hbs_compress_subset(sbx_geom g, int formulation, double mu, const int64_
   });
 }
 
+int sbx_hbs_compress_sharded(sbx_geom g, int formulation, double mu, const sbx_hbs_options* opts, sbx_comm c,
+                             sbx_hbs* out) {
+  return guard([&] {
+    sbx::HbsBuildOptions o;
+    if (opts) o = sbx::HbsBuildOptions::from(*opts);
+    o.comm = Cm(c).world() > 1 ? &Cm(c) : nullptr;
+    auto h = sbx::hbs_compress_device(G(g), formulation, mu, nullptr, 0, o, sbx::lib_stream());
+    *out = new sbx_hbs_s{std::move(h)};
+  });
+}
+
 int sbx_hbs_compress_custom(sbx_geom g, int formulation, double mu, sbx_entries_fn entries, void* ctx,
                             int with_completion, const sbx_hbs_options* opts, sbx_hbs* out) {
   return guard([&] {
@@ -424,6 +439,8 @@ int sbx_hbs_info(sbx_hbs h, int64_t* info) {
     info[9] = op.leaf_nodes;
     info[10] = op.top_L;
     info[11] = op.top_K;
+    info[12] = op.arena_used;
+    info[13] = op.sharded() ? 1 : 0;
   });
 }
 
@@ -759,10 +776,6 @@ int sbx_els_xw(sbx_els e, double* X, double* W) {
 
 // ---------------------------------------------------------------- multi-GPU
 namespace {
-sbx::Collective& Cm(sbx_comm c) {
-  sbx::require(c && c->c, "null comm handle");
-  return *c->c;
-}
 
 // Runs f on device blocks: host inputs are staged in, host outputs copied back.
 struct Staged {

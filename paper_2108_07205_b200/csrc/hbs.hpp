@@ -112,6 +112,7 @@ struct SweepScratch {
 };
 
 struct ShardPlans;
+class Collective;
 
 struct HbsOp {
   i64 n = 0, leaf_nodes = 64;
@@ -145,6 +146,17 @@ struct HbsOp {
   DevBuf<double> arena_t;
   bool t_solve = false, t_apply = false;
   std::unique_ptr<struct ShardPlans> shard;  // subtree-partitioned solve (multi-GPU)
+  // Subtree-sharded build and storage (multi-GPU): rank
+  // shard_p of shard_G = 2^shard_g compresses and inverts the nodes of its
+  // subtree (depth >= shard_g) and, redundantly, the top levels; `stored`
+  // marks the nodes whose factors live in this arena (its subtree, the top,
+  // and the G subtree roots' coupling / dhat blocks the top inverse reads).
+  // Empty: an unsharded operator.  `comm` carries the build's exchanges.
+  int shard_G = 1, shard_p = 0, shard_g = 0;
+  std::vector<char> stored;
+  Collective* comm = nullptr;
+  bool sharded() const { return !stored.empty(); }
+  bool has(size_t i) const { return stored.empty() || stored[i] != 0; }
   // Lazily built shared state (plans, flow items, transposed arena,
   // collapsed top, shard plans) is created under `mu`; everything a call
   // mutates lives in its stream's scratch.  After the first call on a

@@ -19,6 +19,7 @@
 #include "entries.hpp"
 #include "hbs_build.hpp"
 #include "idengine.hpp"
+#include "multigpu.hpp"
 
 namespace sbx {
 
@@ -541,11 +542,42 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
   }
   B.levels.assign(size_t(max_depth + 1), {});
   for (size_t i = 0; i < nn; ++i) B.levels[size_t(op->nodes[i].depth)].push_back(i64(i));
+  // subtree-sharded build (multi-GPU): rank p of G = 2^g compresses the nodes
+  // of depth >= g under the p-th depth-g node, and every node above, itself
+  std::vector<char> mine(nn, 1);
+  Collective* comm = o.comm;
+  int G = 1, P = 0, gdep = 0;
+  if (comm && comm->world() > 1) {
+    require(!with_inverse, "hbs_compress: the fused build is not sharded");
+    require(!nodes && !o.entries, "hbs_compress: a sharded build covers the whole discretization");
+    G = comm->world();
+    P = comm->rank();
+    while ((1 << gdep) < G) ++gdep;
+    require((1 << gdep) == G, "hbs_compress: sharded builds need a power-of-two rank count");
+    std::vector<i64> owner(nn, -1);
+    i64 q = 0;
+    for (size_t i = 0; i < nn; ++i) {
+      if (op->nodes[i].is_leaf())
+        require(op->nodes[i].depth >= gdep, "hbs_compress: tree has a leaf above the partition depth");
+      if (op->nodes[i].depth == gdep) owner[i] = q++;
+      else if (op->nodes[i].depth > gdep) owner[i] = owner[size_t(op->nodes[i].parent)];
+    }
+    require(q == G, "hbs_compress: tree has fewer subtrees than ranks");
+    op->stored.assign(nn, 0);
+    for (size_t i = 0; i < nn; ++i) {
+      mine[i] = owner[i] < 0 || owner[i] == P;
+      op->stored[i] = mine[i] || op->nodes[i].depth == gdep;  // subtree roots: coupling + dhat slots everywhere
+    }
+    op->shard_G = G;
+    op->shard_p = P;
+    op->shard_g = gdep;
+    op->comm = comm;
+  }
 
   // leaf diagonal blocks
   std::vector<i64> leaf_ids;
   for (size_t i = 0; i < nn; ++i)
-    if (op->nodes[i].is_leaf()) leaf_ids.push_back(i64(i));
+    if (op->nodes[i].is_leaf() && mine[i]) leaf_ids.push_back(i64(i));
   std::vector<i64> d_off(nn, -1);
   DevBuf<double> dstore;
   {
@@ -618,8 +650,12 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
   // bottom-up skeletonisation; the root keeps no factors (hbs.cpp:411-421)
   std::vector<std::unique_ptr<LevelStore>> stores(static_cast<size_t>(max_depth + 1));
   std::vector<i64> pos_in_level(nn, 0);
+  std::vector<double> remote_b;  // sharded: the other subtree roots' couplings (gathered)
+  std::vector<i64> remote_b_off(nn, -1);
   for (int depth = max_depth; depth >= 1; --depth) {
-    const auto& ids = B.levels[size_t(depth)];
+    std::vector<i64> ids;
+    for (i64 id : B.levels[size_t(depth)])
+      if (mine[size_t(id)]) ids.push_back(id);
     const size_t L = ids.size();
     for (size_t q = 0; q < L; ++q) pos_in_level[size_t(ids[q])] = i64(q);
     std::vector<std::vector<i64>> rc(L), cc(L), nc, nr;
@@ -705,6 +741,48 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
       k = std::min(kr, kc);
       kfin[q] = k;
     }
+    // skeletons (idlib.cpp:55-62: J[:k] of each ID)
+    for (size_t q = 0; q < L; ++q) {
+      HbsNodeH& nd = op->nodes[size_t(ids[q])];
+      const IdBatch& RB = rounds[size_t(row_round[q])]->ids;
+      const IdBatch& CB = rounds[size_t(col_round[q])]->ids;
+      nd.k = kfin[q];
+      nd.row_skel.resize(size_t(nd.k));
+      nd.col_skel.resize(size_t(nd.k));
+      for (i64 i = 0; i < nd.k; ++i) {
+        nd.row_skel[size_t(i)] = rc[q][size_t(RB.perm(row_pi[q])[size_t(i)])];
+        nd.col_skel[size_t(i)] = cc[q][size_t(CB.perm(col_pi[q])[size_t(i)])];
+      }
+      if (nd.k == i64(rc[q].size()))
+        op->notes.push_back("node [" + std::to_string(nd.begin) + "," + std::to_string(nd.end) +
+                            ") kept at full rank (stored dense)");
+    }
+    if (G > 1 && depth >= gdep) {  // the other subtrees' skeletons of this depth (near sets, couplings above)
+      std::vector<double> pk;
+      for (i64 id : ids) {
+        const auto& nd = op->nodes[size_t(id)];
+        pk.push_back(double(id));
+        pk.push_back(double(nd.k));
+        for (i64 v : nd.row_skel) pk.push_back(double(v));
+        for (i64 v : nd.col_skel) pk.push_back(double(v));
+      }
+      const auto all = gather_host(*comm, pk, s);
+      for (int r = 0; r < G; ++r) {
+        if (r == P) continue;
+        const auto& v = all[size_t(r)];
+        for (size_t at = 0; at < v.size();) {
+          HbsNodeH& nd = op->nodes[size_t(v[at])];
+          nd.k = i64(v[at + 1]);
+          nd.row_skel.assign(size_t(nd.k), 0);
+          nd.col_skel.assign(size_t(nd.k), 0);
+          for (i64 i = 0; i < nd.k; ++i) {
+            nd.row_skel[size_t(i)] = i64(v[at + 2 + size_t(i)]);
+            nd.col_skel[size_t(i)] = i64(v[at + 2 + size_t(nd.k + i)]);
+          }
+          at += 2 + size_t(2 * nd.k);
+        }
+      }
+    }
     // interpolation matrices u (row) and v (col), c x k each, then b_sib
     auto st = std::make_unique<LevelStore>();
     st->o_u.resize(L);
@@ -718,11 +796,11 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
       st->o_v[q] = tot;
       tot += i64(cc[q].size()) * kfin[q];
     }
-    for (size_t q = 0; q < L; ++q) {  // b_sib sizes need the sibling's k
+    for (size_t q = 0; q < L; ++q) {  // b_sib sizes need the sibling's k (remote when sharded)
       const i64 id = ids[q];
       const i64 sib = op->sib(id);
       st->o_b[q] = tot;
-      tot += kfin[q] * kfin[size_t(pos_in_level[size_t(sib)])];
+      tot += kfin[q] * op->nodes[size_t(sib)].k;
     }
     st->buf.resize(size_t(std::max<i64>(tot, 1)));
     for (size_t r = 0; r < rounds.size(); ++r) {
@@ -742,21 +820,6 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
         }
       }
       rounds[r]->ids.interp(ks, P, ldp, s);
-    }
-    for (size_t q = 0; q < L; ++q) {
-      HbsNodeH& nd = op->nodes[size_t(ids[q])];
-      const IdBatch& RB = rounds[size_t(row_round[q])]->ids;
-      const IdBatch& CB = rounds[size_t(col_round[q])]->ids;
-      nd.k = kfin[q];
-      nd.row_skel.resize(size_t(nd.k));
-      nd.col_skel.resize(size_t(nd.k));
-      for (i64 i = 0; i < nd.k; ++i) {
-        nd.row_skel[size_t(i)] = rc[q][size_t(RB.perm(row_pi[q])[size_t(i)])];
-        nd.col_skel[size_t(i)] = cc[q][size_t(CB.perm(col_pi[q])[size_t(i)])];
-      }
-      if (nd.k == i64(rc[q].size()))
-        op->notes.push_back("node [" + std::to_string(nd.begin) + "," + std::to_string(nd.end) +
-                            ") kept at full rank (stored dense)");
     }
     {  // b_sib = entries(row_skel, sibling col_skel)
       std::vector<i64> ri, ci;
@@ -788,6 +851,32 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
       else
         launch_block_jobs(eo.view(), dj.get(), int(jobs.size()), mx, dri.get(), dci.get(), st->buf.get(), s);
       SBX_CUDA(cudaStreamSynchronize(s));
+    }
+    if (G > 1 && depth == gdep) {  // the subtree roots' couplings, for the top levels' inverse on every rank
+      std::vector<double> pk;
+      for (size_t q = 0; q < L; ++q) {
+        const auto& nd = op->nodes[size_t(ids[q])];
+        const i64 ks = op->nodes[size_t(op->sib(ids[q]))].k;
+        std::vector<double> b(static_cast<size_t>(nd.k * ks));
+        if (!b.empty()) {
+          SBX_CUDA(cudaMemcpyAsync(b.data(), st->buf.get() + st->o_b[q], b.size() * 8, cudaMemcpyDeviceToHost, s));
+          SBX_CUDA(cudaStreamSynchronize(s));
+        }
+        pk.push_back(double(ids[q]));
+        pk.insert(pk.end(), b.begin(), b.end());
+      }
+      const auto all = gather_host(*comm, pk, s);
+      for (int r = 0; r < G; ++r) {
+        if (r == P) continue;
+        const auto& v = all[size_t(r)];
+        for (size_t at = 0; at < v.size();) {
+          const i64 id = i64(v[at]);
+          const i64 cnt = op->nodes[size_t(id)].k * op->nodes[size_t(op->sib(id))].k;
+          remote_b_off[size_t(id)] = i64(remote_b.size());
+          remote_b.insert(remote_b.end(), v.begin() + i64(at) + 1, v.begin() + i64(at) + 1 + cnt);
+          at += 1 + size_t(cnt);
+        }
+      }
     }
     if (fz) {  // this level's inverse inputs are complete: hand it to the inversion thread
       const LevelStore& S = *st;
@@ -835,9 +924,17 @@ std::unique_ptr<HbsOp> compress_impl(const Geom& g, int formulation, double mu, 
   hbs_layout(*op);
   std::vector<CopyJob> cj;
   double* A = op->arena.get();
+  DevBuf<double> d_remote_b;
+  if (!remote_b.empty()) d_remote_b.upload(remote_b, s);
   for (size_t i = 0; i < nn; ++i) {
     const auto& nd = op->nodes[i];
     const int k = int(nd.k), c = int(nd.c);
+    if (!mine[i]) {  // sharded: another rank's subtree; its root's coupling block only
+      const i64 ks = i ? op->nodes[size_t(op->sib(i64(i)))].k : 0;
+      if (op->has(i) && remote_b_off[i] >= 0 && k > 0 && ks > 0)
+        cj.push_back({d_remote_b.get() + remote_b_off[i], A + nd.o_b, k, int(ks), k, k, 0, 0});
+      continue;
+    }
     if (nd.is_leaf()) {  // d below v^T in vd
       const int vld = (i == 0) ? c : k + c;
       cj.push_back({dstore.get() + d_off[i], A + nd.o_vd + (i == 0 ? 0 : k), c, c, c, vld, 0, 0});
@@ -917,12 +1014,51 @@ void hbs_invert_device(HbsOp& op, cudaStream_t s) {
     p.e = A + nd.o_e;
     p.fg = A + nd.o_fg;
   }
+  // sharded operator: this rank inverts its subtree, then (after the subtree
+  // roots' dhat blocks are exchanged) the top levels like every other rank
+  std::vector<char> own(nn, 1);
+  if (op.sharded()) {
+    require(op.comm != nullptr, "hbs_invert: sharded operator without its communicator");
+    std::vector<i64> owner(nn, -1);
+    i64 q = 0;
+    for (size_t i = 0; i < nn; ++i) {
+      if (op.nodes[i].depth == op.shard_g) owner[i] = q++;
+      else if (op.nodes[i].depth > op.shard_g) owner[i] = owner[size_t(op.nodes[i].parent)];
+      own[i] = owner[i] < 0 || owner[i] == op.shard_p;
+    }
+  }
   std::vector<std::unique_ptr<Gate>> gates;
   for (int depth = op.max_depth; depth >= 0; --depth) {
     std::vector<size_t> ids;
     for (size_t i = 0; i < nn; ++i)
-      if (op.nodes[i].depth == depth) ids.push_back(i);
+      if (op.nodes[i].depth == depth && own[i]) ids.push_back(i);
     invert_level(op, ids, P, A + op.o_root_g, gates, s);
+    if (op.sharded() && op.shard_G > 1 && depth == op.shard_g) {
+      std::vector<double> pk;
+      for (size_t i : ids) {
+        const i64 k = op.nodes[i].k;
+        std::vector<double> d(static_cast<size_t>(k * k));
+        if (!d.empty()) {
+          SBX_CUDA(cudaMemcpyAsync(d.data(), A + op.nodes[i].o_dhat, d.size() * 8, cudaMemcpyDeviceToHost, s));
+          SBX_CUDA(cudaStreamSynchronize(s));
+        }
+        pk.push_back(double(i));
+        pk.insert(pk.end(), d.begin(), d.end());
+      }
+      const auto all = gather_host(*op.comm, pk, s);
+      for (int r = 0; r < op.shard_G; ++r) {
+        if (r == op.shard_p) continue;
+        const auto& v = all[size_t(r)];
+        for (size_t at = 0; at < v.size();) {
+          const auto& nd = op.nodes[size_t(v[at])];
+          const size_t cnt = size_t(nd.k * nd.k);
+          if (cnt)
+            SBX_CUDA(cudaMemcpyAsync(A + nd.o_dhat, v.data() + at + 1, cnt * 8, cudaMemcpyHostToDevice, s));
+          at += 1 + cnt;
+        }
+      }
+      SBX_CUDA(cudaStreamSynchronize(s));
+    }
   }
   check_gates(op, gates, thr, s);
   phase_mark("inv: done", s);

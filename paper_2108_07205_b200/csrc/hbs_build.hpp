@@ -18,6 +18,9 @@ struct HbsBuildOptions {
   // caller-supplied entry oracle (HbsSource::entries plugin); null: the
   // formulation's kernel entries on the device
   const HostEntries* entries = nullptr;
+  // subtree-sharded build (multi-GPU): this rank's subtree and the top
+  // levels only, skeletons exchanged level by level through `comm`
+  class Collective* comm = nullptr;
   static HbsBuildOptions from(const sbx_hbs_options& o) {
     HbsBuildOptions b;
     b.eps = o.eps;

@@ -51,7 +51,7 @@ void hbs_layout(HbsOp& op) {
     for (int d = op.max_depth; d >= 0; --d)
       for (size_t i = 0; i < nn; ++i) {
         auto& nd = op.nodes[i];
-        if (nd.depth != d) continue;
+        if (nd.depth != d || !op.has(i)) continue;  // sharded: this rank's nodes only
         const bool root = i == 0;
         const i64 k = nd.k, c = nd.c;
         switch (kind) {
@@ -246,6 +246,7 @@ std::unique_ptr<HbsOp> hbs_load_hbs1(const std::string& path, cudaStream_t s) {
 }
 
 void hbs_save_hbs1(const HbsOp& op, const std::string& path, cudaStream_t s) {
+  require(!op.sharded(), "hbs_save: a subtree-sharded operator holds only its subtree's factors");
   std::vector<double> host(op.arena.size());
   op.arena.download(host.data(), host.size(), s);
   SBX_CUDA(cudaStreamSynchronize(s));

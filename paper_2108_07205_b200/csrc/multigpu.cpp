@@ -225,6 +225,33 @@ std::vector<std::unique_ptr<Collective>> make_loopback_group(int world) {
   return out;
 }
 
+std::vector<std::vector<double>> gather_host(Collective& c, const std::vector<double>& mine, cudaStream_t s) {
+  const int G = c.world(), p = c.rank();
+  DevBuf<double> sz(static_cast<size_t>(G));
+  sz.zero(s);
+  const double me = double(mine.size());
+  SBX_CUDA(cudaMemcpyAsync(sz.get() + p, &me, sizeof(double), cudaMemcpyHostToDevice, s));
+  c.all_gather(sz.get(), 1, s);
+  std::vector<double> hs(static_cast<size_t>(G));
+  sz.download(hs.data(), hs.size(), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  size_t mx = 1;
+  for (double v : hs) mx = std::max(mx, size_t(v));
+  DevBuf<double> buf(static_cast<size_t>(G) * mx);
+  buf.zero(s);
+  if (!mine.empty())
+    SBX_CUDA(cudaMemcpyAsync(buf.get() + size_t(p) * mx, mine.data(), mine.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, s));
+  c.all_gather(buf.get(), mx, s);
+  std::vector<double> all(static_cast<size_t>(G) * mx);
+  buf.download(all.data(), all.size(), s);
+  SBX_CUDA(cudaStreamSynchronize(s));
+  std::vector<std::vector<double>> out(static_cast<size_t>(G));
+  for (int q = 0; q < G; ++q)
+    out[size_t(q)].assign(all.begin() + i64(q) * i64(mx), all.begin() + i64(q) * i64(mx) + i64(hs[size_t(q)]));
+  return out;
+}
+
 // ---------------------------------------------------------------- sharded solve
 void hbs_solve_sharded(HbsOp& op, Collective& c, const double* b_local, i64 ldb, i64 nrhs, double* x_local,
                        i64 ldx, cudaStream_t s) {

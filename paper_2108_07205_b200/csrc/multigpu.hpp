@@ -38,6 +38,11 @@ class Collective {
   virtual void all_reduce_sum(double* buf, size_t count, cudaStream_t s) = 0;
 };
 
+// All-gather of one variable-length host vector per rank (sizes, then the
+// payload padded to the longest), through the collective on stream s;
+// integers travel exactly as doubles (< 2^53).
+std::vector<std::vector<double>> gather_host(Collective& c, const std::vector<double>& mine, cudaStream_t s);
+
 // 128-byte NCCL unique id (rank 0 creates it, the caller distributes it).
 void nccl_unique_id(unsigned char out[128]);
 std::unique_ptr<Collective> make_nccl_collective(const unsigned char id[128], int world, int rank);

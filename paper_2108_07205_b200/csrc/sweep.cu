@@ -875,6 +875,8 @@ void hbs_build_solve_plan(HbsOp& op) {
 ShardPlans& hbs_shard(HbsOp& op, int G, int p) {
   std::lock_guard<std::recursive_mutex> lk(op.mu);
   require(op.has_inverse, "hbs_solve: inverse not built");
+  require(!op.sharded() || (op.shard_G == G && op.shard_p == p),
+          "shard: a subtree-sharded operator solves only on the partition it was built for");
   require(G >= 1 && (G & (G - 1)) == 0, "shard: rank count must be a power of two");
   require(p >= 0 && p < G, "shard: rank out of range");
   if (op.shard && op.shard->G == G && op.shard->p == p) return *op.shard;
@@ -1230,12 +1232,14 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
 }  // namespace
 
 void hbs_ensure_solve_plan(HbsOp& op) {
+  require(!op.sharded(), "hbs_solve: a subtree-sharded operator solves through sbx_hbs_solve_sharded");
   if (op.solve_plan.built.load(std::memory_order_acquire)) return;
   std::lock_guard<std::recursive_mutex> lk(op.mu);
   if (!op.solve_plan.built) hbs_build_solve_plan(op);
 }
 
 void hbs_ensure_apply_plan(HbsOp& op) {
+  require(!op.sharded(), "hbs_apply: a subtree-sharded operator holds only its subtree's factors");
   if (op.apply_plan.built.load(std::memory_order_acquire)) return;
   std::lock_guard<std::recursive_mutex> lk(op.mu);
   if (!op.apply_plan.built) hbs_build_apply_plan(op);

@@ -104,6 +104,20 @@ class Comm:
             pass
 
 
+def compress_sharded(d, comm: Comm, formulation=0, opts=None, mu: float = 1.0):
+    """hbs_compress over the subtree partition of `comm` (sbx_hbs_compress_sharded):
+    this rank's subtree and the top levels only; invert with api.hbs_invert,
+    solve with NativeShardedSolver on the same communicator (which must
+    outlive the operator)."""
+    from .api import HbsOperator, HbsOptions
+    o = (opts or HbsOptions()).to_c()
+    out = VP()
+    check(lib().sbx_hbs_compress_sharded(d.ptr, formulation, mu, C.byref(o), comm.ptr, C.byref(out)))
+    h = HbsOperator(out)
+    h._comm = comm  # keep the communicator alive as long as the operator
+    return h
+
+
 def _cm_call(x, rows):
     """Column-major device (or host) view of a rows x m block: (keepalive, ptr, ld, m, device?)."""
     if hasattr(x, "is_cuda") and x.is_cuda:
