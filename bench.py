@@ -346,6 +346,16 @@ def partitioned_bench(sb, torch, rank, world, g0, h, cfg0, reps=10):
         apply[f"rhs{nrhs}"] = {"ms": round(ms, 4), "solves_per_s": round(nrhs / (ms * 1e-3), 1),
                                "rel_err_vs_1gpu": err}
     out["cfg3_apply"] = apply
+    # the same 256 right-hand sides split by column instead (no exchange; every
+    # rank holds the whole operator): parallel.solve_columns
+    from paper_2108_07205_b200.parallel import column_range
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    b = torch.empty((n3, 256), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=gen)
+    c0, c1 = column_range(256, world, rank)
+    bc = b[:, c0:c1].contiguous()
+    ms = timed(lambda: sb.hbs_solve(h3_full, bc))
+    out["cfg3_columns"] = {"rhs": 256, "ms": round(ms, 4), "solves_per_s": round(256 / (ms * 1e-3), 1),
+                           "columns_per_rank": c1 - c0}
     # cfg2 Woodbury solve on the subtree ownership: rank 0's refined wall
     # (configs[1], seed 0) on every rank, its update factors handed over in
     # the dump format

@@ -247,15 +247,21 @@ class ShardedHbsSolver:
         return self.ex.down(flat.view(self.G, kmax, nrhs), nrhs)
 
 
-def solve_columns(h, b, group=None):
-    """Batched RHS split by column across ranks (no exchange): rank p solves
-    its contiguous block of columns of b with the full local operator."""
+def column_range(ncols: int, world: int, rank: int):
+    """Rank `rank`'s contiguous block of `ncols` right-hand sides."""
+    return ncols * rank // world, ncols * (rank + 1) // world
+
+
+def solve_columns(h, b, group=None, solve=None):
+    """Batched RHS split by column across ranks (no
+    exchange): rank p solves its contiguous block of columns of b with the
+    full local operator (`solve(h, block)`, default api.hbs_solve).  Returns
+    ((c0, c1), x block)."""
     import torch.distributed as dist
     from .api import hbs_solve
     G, p = dist.get_world_size(group), dist.get_rank(group)
-    n = b.shape[1]
-    c0, c1 = n * p // G, n * (p + 1) // G
-    return (c0, c1), hbs_solve(h, b[:, c0:c1])
+    c0, c1 = column_range(b.shape[1], G, p)
+    return (c0, c1), (solve or hbs_solve)(h, b[:, c0:c1])
 
 
 class ShardedWoodbury:
