@@ -58,8 +58,13 @@ enum { SBX_INTERIOR_DIRICHLET = 0, SBX_EXTERIOR_COMBINED = 1, SBX_MIXED = 2 };
 /* Sweep flags. */
 enum {
   SBX_TRANSPOSE = 1,     /* hbs_solve_t / hbs_apply_t                        */
-  SBX_DEVICE_PTRS = 2    /* b / x are device pointers (else host, pinned or
+  SBX_DEVICE_PTRS = 2,   /* b / x are device pointers (else host, pinned or
                             pageable; copies are issued on the stream)     */
+  SBX_ROW_MAJOR = 4      /* with SBX_DEVICE_PTRS, sbx_hbs_solve / _apply only:
+                            b / x are n x nrhs ROW-major (ld = row stride
+                            >= nrhs), the sweep workspace's own layout, so
+                            they move by strided copies instead of
+                            transposes (a C-contiguous torch tensor)       */
 };
 
 typedef struct sbx_geom_s* sbx_geom;     /* Discretization           */

@@ -30,6 +30,7 @@ SBX_RUNTIME_ERROR = 7
 
 SBX_TRANSPOSE = 1
 SBX_DEVICE_PTRS = 2
+SBX_ROW_MAJOR = 4
 
 
 class sbx_curve(C.Structure):

@@ -390,7 +390,7 @@ def torch_stream_handle():
     return s if s else CUDA_STREAM_LEGACY
 
 
-def _sweep(fn, op_ptr, b, n, stream=None, flags=0):
+def _sweep(fn, op_ptr, b, n, stream=None, flags=0, row_major_ok=False):
     """Column-major n x nrhs sweep through the C-ABI (host numpy or CUDA torch)."""
     if _is_torch_cuda(b):
         import torch
@@ -398,9 +398,16 @@ def _sweep(fn, op_ptr, b, n, stream=None, flags=0):
         bt = b.reshape(-1, 1) if vec else b
         if bt.dtype != torch.float64 or bt.shape[0] != n:
             raise ValueError("sweep: expected float64 with n rows")
+        s = stream if stream is not None else torch_stream_handle()
+        if row_major_ok and bt.stride(1) == 1 and bt.stride(0) >= bt.shape[1]:
+            # row-major rows (a C-contiguous tensor) are the sweep workspace's
+            # own layout: strided copies in and out, no transposes (SBX_ROW_MAJOR)
+            out = torch.empty((n, bt.shape[1]), dtype=torch.float64, device=bt.device)
+            check(fn(op_ptr, VP(bt.data_ptr()), bt.stride(0), bt.shape[1], VP(out.data_ptr()), bt.shape[1],
+                     _sbx.SBX_DEVICE_PTRS | _sbx.SBX_ROW_MAJOR | flags, VP(s)))
+            return out.reshape(-1) if vec else out
         bcm = bt.t().contiguous()  # column-major storage = transposed row-major
         out = torch.empty_like(bcm)
-        s = stream if stream is not None else torch_stream_handle()
         check(fn(op_ptr, VP(bcm.data_ptr()), n, bt.shape[1], VP(out.data_ptr()), n,
                  _sbx.SBX_DEVICE_PTRS | flags, VP(s)))
         res = out.t()
@@ -417,12 +424,14 @@ def _sweep(fn, op_ptr, b, n, stream=None, flags=0):
 
 def hbs_solve(op: HbsOperator, b, transpose: bool = False):
     """hbs.cpp:589-625; transpose: hbs_solve_t (hbs.cpp:627-664)."""
-    return _sweep(lib().sbx_hbs_solve, op.ptr, b, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0)
+    return _sweep(lib().sbx_hbs_solve, op.ptr, b, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0,
+                  row_major_ok=True)
 
 
 def hbs_apply(op: HbsOperator, v, transpose: bool = False):
     """hbs.cpp:511-544; transpose: hbs_apply_t (hbs.cpp:546-587)."""
-    return _sweep(lib().sbx_hbs_apply, op.ptr, v, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0)
+    return _sweep(lib().sbx_hbs_apply, op.ptr, v, op.n, flags=_sbx.SBX_TRANSPOSE if transpose else 0,
+                  row_major_ok=True)
 
 
 def hbs_save(op: HbsOperator, path):

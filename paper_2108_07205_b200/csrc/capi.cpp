@@ -368,6 +368,11 @@ int sbx_hbs_solve(sbx_hbs h, const double* b, int64_t ldb, int64_t nrhs, double*
   return guard([&] {
     sbx::StreamScope scope(stream_of(stream));
     const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    if (flags & SBX_ROW_MAJOR) {
+      sbx::require(dev, "hbs_solve: row-major blocks must be device pointers");
+      sbx::hbs_sweep_rm(H(h), false, (flags & SBX_TRANSPOSE) != 0, b, ldb, nrhs, x, ldx, stream_of(stream));
+      return;
+    }
     if (flags & SBX_TRANSPOSE)
       sbx::hbs_solve_t(H(h), b, ldb, nrhs, x, ldx, dev, stream_of(stream));
     else
@@ -380,6 +385,11 @@ int sbx_hbs_apply(sbx_hbs h, const double* v, int64_t ldv, int64_t nrhs, double*
   return guard([&] {
     sbx::StreamScope scope(stream_of(stream));
     const bool dev = (flags & SBX_DEVICE_PTRS) != 0;
+    if (flags & SBX_ROW_MAJOR) {
+      sbx::require(dev, "hbs_apply: row-major blocks must be device pointers");
+      sbx::hbs_sweep_rm(H(h), true, (flags & SBX_TRANSPOSE) != 0, v, ldv, nrhs, y, ldy, stream_of(stream));
+      return;
+    }
     if (flags & SBX_TRANSPOSE)
       sbx::hbs_apply_t(H(h), v, ldv, nrhs, y, ldy, dev, stream_of(stream));
     else

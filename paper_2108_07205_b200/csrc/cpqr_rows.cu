@@ -30,6 +30,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cfloat>
+#include <functional>
+#include <map>
 #include <mutex>
 
 #include "dense.hpp"
@@ -360,29 +362,39 @@ void cpqr_rows_batched(const std::vector<QrJob>& all, cudaStream_t s) {
   int dev = 0, sms = 148;
   SBX_CUDA(cudaGetDevice(&dev));
   SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // spread few problems over more CTAs (shorter per-step work), never past one wave
-  std::vector<std::pair<int, QrJob>> sized;
+  // spread few problems over more CTAs (shorter per-step work), never past
+  // one wave.  The cluster size sets the rank order of every partial sum, so
+  // it must depend on the batch's multiset of shapes only, not on the order
+  // the rendezvous participants arrived in: problems of one (M, n) class
+  // grow together, classes taken tallest first.
+  std::vector<QrJob> jobs_in(all);
+  std::map<std::pair<int, int>, std::pair<int, int>, std::greater<std::pair<int, int>>> cls;  // (M, n) -> (count, G)
   i64 ctas = 0;
-  for (const auto& j : all) {
+  for (const auto& j : jobs_in) {
     const int g = cpqr_rows_cluster(j.M, j.n);
     require(g > 0, "cpqr_rows: problem does not fit one cluster");
-    sized.push_back({g, j});
+    auto& c = cls[{j.M, j.n}];
+    c.first += 1;
+    c.second = g;
     ctas += g;
   }
   static const int force_g = [] {  // diagnostics: fixed cluster size
     const char* e = std::getenv("SBX_ROWS_G");
     return e ? std::atoi(e) : 0;
   }();
-  for (auto& sj : sized) {
+  for (auto& kv : cls) {
+    auto& c = kv.second;
     if (force_g > 0) {
-      sj.first = std::max(sj.first, force_g);
+      c.second = std::max(c.second, force_g);
       continue;
     }
-    while (sj.first < kRMaxG && (sj.second.M / (2 * sj.first)) >= 32 && ctas + sj.first <= sms) {
-      ctas += sj.first;
-      sj.first *= 2;
+    while (c.second < kRMaxG && (kv.first.first / (2 * c.second)) >= 32 && ctas + i64(c.first) * c.second <= sms) {
+      ctas += i64(c.first) * c.second;
+      c.second *= 2;
     }
   }
+  std::vector<std::pair<int, QrJob>> sized;
+  for (const auto& j : jobs_in) sized.push_back({cls[{j.M, j.n}].second, j});
   std::stable_sort(sized.begin(), sized.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
   std::vector<QrJob> jobs;
   for (const auto& sj : sized) jobs.push_back(sj.second);

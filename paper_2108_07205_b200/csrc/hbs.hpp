@@ -209,6 +209,11 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
 // arena (hbs_ensure_transpose first).
 void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 rows, i64 nrhs, double* out,
                     i64 ldo, const i64* map, bool transposed, cudaStream_t s);
+// Device blocks already in the workspace layout (n x nrhs row-major, row
+// stride ldb / ldx >= nrhs): solve (apply = false) or apply, plain or
+// transposed, with strided copies in and out (sbx.h SBX_ROW_MAJOR).
+void hbs_sweep_rm(HbsOp& op, bool apply, bool transpose, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx,
+                  cudaStream_t s);
 // hbs.cpp:627-664 / :546-587: transposed solve and apply.
 void hbs_solve_t(HbsOp& op, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx, bool dev, cudaStream_t s);
 void hbs_apply_t(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy, bool dev, cudaStream_t s);

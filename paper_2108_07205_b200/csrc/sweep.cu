@@ -486,25 +486,53 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------- layout moves
-__global__ void cm_to_rm_kernel(const double* __restrict__ src, i64 ld, i64 n, i64 nrhs,
-                                double* __restrict__ dst, i64 ldw, const i64* __restrict__ map) {
-  const i64 total = n * nrhs;
-  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
-       idx += i64(gridDim.x) * blockDim.x) {
-    const i64 i = idx % n, c = idx / n;  // coalesced read along columns
-    const i64 r = map ? map[i] : i;
-    dst[r * ldw + c] = src[i + c * ld];
+// Layout conversions between the caller's column-major blocks and the
+// row-major sweep workspace (RHS fastest), with an optional row map.  Blocks
+// of several RHS go through 32 x 32 shared-memory tiles, so the column-major
+// side moves along its rows and the row-major side along its RHS (both
+// coalesced, no 64-bit index divisions); a single RHS is a plain (gathered)
+// copy.
+template <bool kToRm>
+__global__ void __launch_bounds__(256) transpose_tiles_kernel(const double* __restrict__ src, i64 lds,
+                                                              double* __restrict__ dst, i64 ldd, i64 n, i64 nrhs,
+                                                              const i64* __restrict__ map) {
+  __shared__ double t[32][33];
+  const i64 i0 = i64(blockIdx.x) * 32, c0 = i64(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  if (kToRm) {  // src column-major (i, c); dst row map(i), column c
+#pragma unroll
+    for (int k = ty; k < 32; k += 8) {
+      const i64 c = c0 + k, i = i0 + tx;
+      if (i < n && c < nrhs) t[k][tx] = src[i + c * lds];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = ty; k < 32; k += 8) {
+      const i64 i = i0 + k, c = c0 + tx;
+      if (i < n && c < nrhs) dst[(map ? map[i] : i) * ldd + c] = t[tx][k];
+    }
+  } else {  // src row map(i), column c; dst column-major (i, c)
+#pragma unroll
+    for (int k = ty; k < 32; k += 8) {
+      const i64 i = i0 + k, c = c0 + tx;
+      if (i < n && c < nrhs) t[k][tx] = src[(map ? map[i] : i) * lds + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = ty; k < 32; k += 8) {
+      const i64 c = c0 + k, i = i0 + tx;
+      if (i < n && c < nrhs) dst[i + c * ldd] = t[tx][k];
+    }
   }
 }
 
-__global__ void rm_to_cm_kernel(const double* __restrict__ src, i64 ldw, i64 n, i64 nrhs,
-                                double* __restrict__ dst, i64 ld, const i64* __restrict__ map) {
-  const i64 total = n * nrhs;
-  for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
-       idx += i64(gridDim.x) * blockDim.x) {
-    const i64 i = idx % n, c = idx / n;
+template <bool kToRm>
+__global__ void copy_rows_kernel(const double* __restrict__ src, i64 lds, double* __restrict__ dst, i64 ldd, i64 n,
+                                 const i64* __restrict__ map) {
+  for (i64 i = blockIdx.x * i64(blockDim.x) + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) {
     const i64 r = map ? map[i] : i;
-    dst[i + c * ld] = src[r * ldw + c];
+    if (kToRm) dst[r * ldd] = src[i];
+    else dst[i] = src[r * lds];
   }
 }
 
@@ -517,14 +545,22 @@ int grid_for(i64 total) {
 void launch_cm_to_rm(const double* src, i64 ld, i64 n, i64 nrhs, double* dst, i64 ldw, const i64* map,
                      cudaStream_t s) {
   if (n * nrhs == 0) return;
-  cm_to_rm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, ld, n, nrhs, dst, ldw, map);
+  if (nrhs == 1)
+    copy_rows_kernel<true><<<grid_for(n), 256, 0, s>>>(src, ld, dst, ldw, n, map);
+  else
+    transpose_tiles_kernel<true><<<dim3(unsigned((n + 31) / 32), unsigned((nrhs + 31) / 32)), 256, 0, s>>>(
+        src, ld, dst, ldw, n, nrhs, map);
   SBX_LAUNCHED();
 }
 
 void launch_rm_to_cm(const double* src, i64 ldw, i64 n, i64 nrhs, double* dst, i64 ld, const i64* map,
                      cudaStream_t s) {
   if (n * nrhs == 0) return;
-  rm_to_cm_kernel<<<grid_for(n * nrhs), 256, 0, s>>>(src, ldw, n, nrhs, dst, ld, map);
+  if (nrhs == 1)
+    copy_rows_kernel<false><<<grid_for(n), 256, 0, s>>>(src, ldw, dst, ld, n, map);
+  else
+    transpose_tiles_kernel<false><<<dim3(unsigned((n + 31) / 32), unsigned((nrhs + 31) / 32)), 256, 0, s>>>(
+        src, ldw, dst, ld, n, nrhs, map);
   SBX_LAUNCHED();
 }
 
@@ -1258,6 +1294,38 @@ void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 r
   launch_cm_to_rm(in, ldi, rows, nrhs, ws + plan.in_row * ldw, ldw, map, s);
   hbs_run_plan(op, plan, ws, nrhs, s, transposed ? op.arena_t.get() : nullptr);
   launch_rm_to_cm(ws + plan.out_row * ldw, ldw, rows, nrhs, out, ldo, map, s);
+  sc.mark.record(s);
+}
+
+void hbs_sweep_rm(HbsOp& op, bool apply, bool transpose, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx,
+                  cudaStream_t s) {
+  require(nrhs >= 0 && ldb >= std::max<i64>(nrhs, 1) && ldx >= std::max<i64>(nrhs, 1),
+          "sweep: row-major leading dimension smaller than nrhs");
+  if (apply) hbs_ensure_apply_plan(op);
+  else hbs_ensure_solve_plan(op);
+  if (transpose) hbs_ensure_transpose(op, !apply, apply, s);
+  if (nrhs == 0) return;
+  SweepPlan& plan = apply ? op.apply_plan : op.solve_plan;
+  const i64 ldw = sweep_ld(nrhs);
+  SweepScratch& sc = op.scratch_for(s);
+  {
+    StreamScope ss(s);
+    sc.ws.reserve(size_t(plan.ws_rows * ldw));
+  }
+  double* ws = sc.ws.get();
+  // dense rows (ld == nrhs == the workspace pitch): one linear copy; a 2D
+  // copy of 8-byte rows runs at a fraction of the bandwidth
+  if (ldb == nrhs && ldw == nrhs)
+    SBX_CUDA(cudaMemcpyAsync(ws + plan.in_row * ldw, b, size_t(op.n * nrhs) * 8, cudaMemcpyDeviceToDevice, s));
+  else
+    SBX_CUDA(cudaMemcpy2DAsync(ws + plan.in_row * ldw, size_t(ldw) * 8, b, size_t(ldb) * 8, size_t(nrhs) * 8,
+                               size_t(op.n), cudaMemcpyDeviceToDevice, s));
+  hbs_run_plan(op, plan, ws, nrhs, s, transpose ? op.arena_t.get() : nullptr);
+  if (ldx == nrhs && ldw == nrhs)
+    SBX_CUDA(cudaMemcpyAsync(x, ws + plan.out_row * ldw, size_t(op.n * nrhs) * 8, cudaMemcpyDeviceToDevice, s));
+  else
+    SBX_CUDA(cudaMemcpy2DAsync(x, size_t(ldx) * 8, ws + plan.out_row * ldw, size_t(ldw) * 8, size_t(nrhs) * 8,
+                               size_t(op.n), cudaMemcpyDeviceToDevice, s));
   sc.mark.record(s);
 }
 

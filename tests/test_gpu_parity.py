@@ -217,13 +217,15 @@ def test_collapsed_top_matches_oracle(po, tmp_path, top):
 def test_fused_app_build_bitwise(po, tmp_path):
     """The added block's HBS built with each level's inverse overlapping the
     next level's compression (hbs_compress_invert_device) gives the same
-    refined solve, bit for bit, as compress-then-invert."""
+    refined solve, bit for bit, as compress-then-invert -- and a second
+    fused run repeats the first (the ID rounds of the two concurrent builds
+    are merged in arrival order; no engine choice may depend on it)."""
     import os
     import subprocess
     import sys
     root = str(Path(__file__).resolve().parents[1])
     out = {}
-    for mode in ("fused", "unfused"):
+    for mode in ("fused", "unfused", "fused_again"):
         env = dict(os.environ, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
         if mode == "unfused":
             env["SBX_APP_UNFUSED"] = "1"
@@ -232,6 +234,7 @@ def test_fused_app_build_bitwise(po, tmp_path):
         assert r.returncode == 0, r.stdout + r.stderr
         out[mode] = np.load(tmp_path / f"{mode}.npy")
     assert np.array_equal(out["fused"], out["unfused"])
+    assert np.array_equal(out["fused"], out["fused_again"])
     assert np.all(np.isfinite(out["fused"]))
 
 

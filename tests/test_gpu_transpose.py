@@ -144,3 +144,28 @@ def test_conditioning_report(sb, po):  # test_els.cpp:268-291
     ke, kt = cond(At + L @ R), cond(At)
     assert 0.3 * ke <= rep["kappa_ext"] <= 3.0 * ke
     assert 0.3 * kt <= rep["kappa_tilde"] <= 3.0 * kt
+
+
+@pytest.mark.parametrize("nrhs", [1, 7, 32, 256])
+def test_row_major_layout_bitwise(sb, nrhs):
+    """SBX_ROW_MAJOR (row-major device blocks, the sweep workspace's own
+    layout) gives the same bits as the column-major host path, for solves
+    and applies, plain and transposed, dense and strided rows."""
+    import torch
+    g = sb.panelize(sb.star(5, 0.3), 64, 16)
+    h = sb.hbs_invert(sb.hbs_compress(g, opts=sb.HbsOptions(eps=1e-10)))
+    n = h.n
+    B = rng_mat(n, nrhs, 21)
+    wide = torch.zeros((n, nrhs + 3), dtype=torch.float64, device="cuda")
+    wide[:, :nrhs] = torch.from_numpy(B)
+    for fn in (sb.hbs_solve, sb.hbs_apply):
+        for tr in (False, True):
+            want = fn(h, B, transpose=tr)
+            dense = fn(h, torch.from_numpy(B).cuda(), transpose=tr)          # ld == nrhs
+            strided = fn(h, wide[:, :nrhs], transpose=tr)                     # ld = nrhs + 3
+            colmajor = fn(h, torch.from_numpy(np.asfortranarray(B)).cuda().t().contiguous().t(), transpose=tr)
+            for got in (dense, strided, colmajor):
+                assert np.array_equal(got.cpu().numpy(), want), (fn.__name__, tr)
+            if nrhs == 1:
+                vec = fn(h, torch.from_numpy(B[:, 0]).cuda(), transpose=tr)
+                assert np.array_equal(vec.cpu().numpy(), want[:, 0])
