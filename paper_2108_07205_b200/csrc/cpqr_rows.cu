@@ -89,6 +89,19 @@ __device__ __forceinline__ double group_sum(double v, int gsz) {
   return v;
 }
 
+// Rank-ordered sum of one slot over the cluster's G CTAs: all G DSMEM loads
+// are issued before the first add (a remote load costs hundreds of cycles).
+__device__ __forceinline__ double cluster_sum(cg::cluster_group& cl, double* slot, int G) {
+  double part[kRMaxG];
+#pragma unroll
+  for (int q = 0; q < kRMaxG; ++q) part[q] = q < G ? *cl.map_shared_rank(slot, q) : 0.0;
+  double d = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRMaxG; ++q)
+    if (q < G) d += part[q];
+  return d;
+}
+
 __global__ void __launch_bounds__(kRT, 1) cpqr_rows_kernel(const QrJob* __restrict__ jobs) {
   extern __shared__ __align__(16) double sm[];
   cg::cluster_group cl = cg::this_cluster();
@@ -133,8 +146,7 @@ __global__ void __launch_bounds__(kRT, 1) cpqr_rows_kernel(const QrJob* __restri
   }
   cl.sync();
   if (has_col && sub == 0) {
-    double s2 = 0.0;
-    for (int q = 0; q < G; ++q) s2 += cl.map_shared_rank(xch3, q)[gc];
+    const double s2 = cluster_sum(cl, xch3 + gc, G);
     upd[gc] = dir[gc] = sqrt(s2);
   }
   cl.sync();  // peers done reading xch3[0]; upd visible CTA-wide
@@ -236,6 +248,7 @@ __global__ void __launch_bounds__(kRT, 1) cpqr_rows_kernel(const QrJob* __restri
     {
       double d = 0.0;
       if (live && tau != 0.0)
+#pragma unroll 4
         for (int i = i0 + sub; i < ml; i += gsz) d = fma(pc[i] * rd, col[i], d);
       d = group_sum(d, gsz);
       if (live && sub == 0) {
@@ -250,15 +263,14 @@ __global__ void __launch_bounds__(kRT, 1) cpqr_rows_kernel(const QrJob* __restri
     // group leaders gather their column's dot (rank order) and the owner's row j
     double tw = 0.0, rj = 0.0;
     if (live && sub == 0) {
-      double d = 0.0;
-      for (int q = 0; q < G; ++q) d += cl.map_shared_rank(x2, q)[gc];
-      tw = tau * d;
       rj = cl.map_shared_rank(x2, owner)[n + gc];
+      tw = tau * cluster_sum(cl, x2 + gc, G);
     }
     tw = __shfl_sync(0xffffffffu, tw, lane & ~(gsz - 1));
     // ---- apply the reflector to the local rows of the column
     if (live) {
       if (tw != 0.0)
+#pragma unroll 4
         for (int i = i0 + sub; i < ml; i += gsz) col[i] = fma(-(pc[i] * rd), tw, col[i]);
       if (own_j && sub == 0) col[j - r0] -= tw;
     }
@@ -291,8 +303,7 @@ __global__ void __launch_bounds__(kRT, 1) cpqr_rows_kernel(const QrJob* __restri
       if (recompute && sub == 0) x3[gc] = s2;
       cl.sync();
       if (recompute && sub == 0) {
-        double t = 0.0;
-        for (int q = 0; q < G; ++q) t += cl.map_shared_rank(x3, q)[gc];
+        const double t = cluster_sum(cl, x3 + gc, G);
         upd[gc] = dir[gc] = sqrt(t);
       }
       __syncthreads();

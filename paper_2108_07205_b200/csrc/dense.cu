@@ -1117,19 +1117,28 @@ __device__ void coop_pick(const CoopPart* cur, int G, double* red, int* ired, in
     ired[64 + warp] = bo;
   }
   __syncthreads();
-  double v0 = -1.0;
-  int p0 = 0x7fffffff, q0 = -1, o0 = -1;
-  for (int w = 0; w < nw; ++w)
-    if (better(red[w], ired[w], v0, p0)) {
-      v0 = red[w];
-      p0 = ired[w];
-      q0 = ired[32 + w];
-      o0 = ired[64 + w];
+  if (warp == 0) {  // first max over the warps' winners (ascending warp order on ties)
+    double v0 = -1.0;
+    int p0 = 0x7fffffff, q0 = -1, o0 = -1;
+    for (int w = 0; w < nw; ++w)
+      if (better(red[w], ired[w], v0, p0)) {
+        v0 = red[w];
+        p0 = ired[w];
+        q0 = ired[32 + w];
+        o0 = ired[64 + w];
+      }
+    __syncwarp();
+    if (lane == 0) {
+      ired[0] = q0;
+      ired[1] = p0;
+      ired[2] = o0;
     }
-  out_phys = q0;
-  out_pos = p0;
-  out_own = o0;
-  __syncthreads();  // everyone has read red / ired
+  }
+  __syncthreads();
+  out_phys = ired[0];
+  out_pos = ired[1];
+  out_own = ired[2];
+  __syncthreads();  // everyone has read ired
 }
 
 struct CoopArgs {
@@ -1346,6 +1355,88 @@ __device__ long long g_cpqr_prof[64 * 8];
   do {             \
   } while (0)
 #endif
+// The whole CTA applies step j's reflector to U slab columns cb.. (tall
+// slabs with few columns per CTA): rows split over all threads, the column
+// pointers and liveness hoisted out of the row loops; then the xGEQPF norm
+// downdate of each live column (uniform decisions: every thread reads the
+// same values).
+template <int U>
+__device__ __forceinline__ void tall_cols(double* S, int ldS, int cb, int nown, const int* mypos, const double* v,
+                                          int j, int M, double tau, double* upd, double* dir, double thr,
+                                          double* red) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* col[U];
+  bool live[U];
+  double d[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    live[u] = cb + u < nown && mypos[cb + u] >= 0;
+    col[u] = S + size_t(cb + u) * ldS;
+    d[u] = 0.0;
+  }
+  if (tau != 0.0 && M - j > 1) {
+#pragma unroll 4
+    for (int i = j + 1 + tid; i < M; i += kOT) {
+      const double vi = v[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (live[u]) d[u] += vi * col[u][i];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[u] = warp_sum(d[u]);
+    if (lane == 0)
+#pragma unroll
+      for (int u = 0; u < U; ++u) red[warp * U + u] = d[u];
+    __syncthreads();
+    double tw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double t = 0.0;
+      for (int w = 0; w < kOWarps; ++w) t += red[w * U + u];
+      tw[u] = live[u] ? tau * (t + col[u][j]) : 0.0;
+    }
+    __syncthreads();  // everyone has read S[j, :] and red[]
+#pragma unroll 4
+    for (int i = j + 1 + tid; i < M; i += kOT) {
+      const double vi = v[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (live[u]) col[u][i] -= vi * tw[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (tid == u && live[u]) col[u][j] -= tw[u];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!live[u]) continue;
+    const int c = cb + u;
+    const double uu = upd[c];
+    if (uu == 0.0) continue;
+    double t = fabs(col[u][j]) / uu;
+    t = (1.0 + t) * (1.0 - t);
+    t = t < 0.0 ? 0.0 : t;
+    const double rr = uu / dir[c];
+    __syncthreads();  // all threads read upd[c] before it changes
+    if (t * rr * rr <= thr) {
+      double sacc = 0.0;
+      for (int i = j + 1 + tid; i < M; i += kOT) sacc += col[u][i] * col[u][i];
+      sacc = warp_sum(sacc);
+      if (lane == 0) red[warp] = sacc;
+      __syncthreads();
+      if (tid == 0) {
+        double s2 = 0.0;
+        for (int w = 0; w < kOWarps; ++w) s2 += red[w];
+        upd[c] = dir[c] = sqrt(s2);
+      }
+    } else if (tid == 0) {
+      upd[c] = uu * sqrt(t);
+    }
+    __syncthreads();
+  }
+}
+
 template <bool kCl>
 __global__ void __launch_bounds__(kOT) cpqr_onchip_kernel(SmemCoopArgs args) {
   extern __shared__ double sm[];
@@ -1533,8 +1624,11 @@ __global__ void __launch_bounds__(kOT) cpqr_onchip_kernel(SmemCoopArgs args) {
           for (int i = j + tid; i < M; i += kOT) __stcg(dst + i, src[i]);
         }
       }
+      CPQR_T(6);
       group_barrier(ctl, unsigned(G));
+      CPQR_T(1);
       coop_pick(parts + (j & 1) * G, G, red, ired, p, lp, own);
+      CPQR_T(2);
     }
     for (int c = tid; c < nown; c += kOT) {
       if (c0 + c == p) {
@@ -1556,10 +1650,25 @@ __global__ void __launch_bounds__(kOT) cpqr_onchip_kernel(SmemCoopArgs args) {
     }
     auto ldp = [&](int i) { return kCl ? pc[i] : __ldcg(pc + i); };
     double part = 0.0;
-    for (int i = j + 1 + tid; i < M; i += kOT) {
-      const double x = ldp(i);
-      v[i] = x;
-      part += x * x;
+    {
+      // the pivot column comes from L2 (or a peer's shared memory): keep 8
+      // loads in flight per thread; the sum keeps its ascending row order
+      int i = j + 1 + tid;
+      for (; i + 7 * kOT < M; i += 8 * kOT) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = ldp(i + u * kOT);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[i + u * kOT] = x[u];
+          part += x[u] * x[u];
+        }
+      }
+      for (; i < M; i += kOT) {
+        const double x = ldp(i);
+        v[i] = x;
+        part += x * x;
+      }
     }
     part = warp_sum(part);
     if (lane == 0) red[warp] = part;
@@ -1627,74 +1736,14 @@ __global__ void __launch_bounds__(kOT) cpqr_onchip_kernel(SmemCoopArgs args) {
         reflect_cols<4>(cols, slot, v, j, M, tau, true, upd, dir, thr, lane);
       }
     } else {
-      for (int cb = 0; cb < nown; cb += kSmemCoopU) {
-        double d[kSmemCoopU];
-        bool live[kSmemCoopU];
-#pragma unroll
-        for (int u = 0; u < kSmemCoopU; ++u) {
-          live[u] = cb + u < nown && mypos[cb + u] >= 0;
-          d[u] = 0.0;
-        }
-        if (tau != 0.0 && M - j > 1) {
-          for (int i = j + 1 + tid; i < M; i += kOT) {
-            const double vi = v[i];
-#pragma unroll
-            for (int u = 0; u < kSmemCoopU; ++u)
-              if (live[u]) d[u] += vi * S[i + size_t(cb + u) * ldS];
-          }
-#pragma unroll
-          for (int u = 0; u < kSmemCoopU; ++u) d[u] = warp_sum(d[u]);
-          if (lane == 0)
-#pragma unroll
-            for (int u = 0; u < kSmemCoopU; ++u) red[warp * kSmemCoopU + u] = d[u];
-          __syncthreads();
-          double tw[kSmemCoopU];
-#pragma unroll
-          for (int u = 0; u < kSmemCoopU; ++u) {
-            double t = 0.0;
-            for (int w = 0; w < kOWarps; ++w) t += red[w * kSmemCoopU + u];
-            tw[u] = live[u] ? tau * (t + S[j + size_t(cb + u) * ldS]) : 0.0;
-          }
-          __syncthreads();  // everyone has read S[j, :] and red[]
-          for (int i = j + 1 + tid; i < M; i += kOT) {
-            const double vi = v[i];
-#pragma unroll
-            for (int u = 0; u < kSmemCoopU; ++u)
-              if (live[u]) S[i + size_t(cb + u) * ldS] -= vi * tw[u];
-          }
-#pragma unroll
-          for (int u = 0; u < kSmemCoopU; ++u)
-            if (tid == u && live[u]) S[j + size_t(cb + u) * ldS] -= tw[u];
-          __syncthreads();
-        }
-        // norm downdating (uniform decisions: every thread reads the same values)
-#pragma unroll
-        for (int u = 0; u < kSmemCoopU; ++u) {
-          if (!live[u]) continue;
-          const int c = cb + u;
-          const double uu = upd[c];
-          if (uu == 0.0) continue;
-          double t = fabs(S[j + size_t(c) * ldS]) / uu;
-          t = (1.0 + t) * (1.0 - t);
-          t = t < 0.0 ? 0.0 : t;
-          const double rr = uu / dir[c];
-          __syncthreads();  // all threads read upd[c] before it changes
-          if (t * rr * rr <= thr) {
-            double sacc = 0.0;
-            for (int i = j + 1 + tid; i < M; i += kOT) sacc += S[i + size_t(c) * ldS] * S[i + size_t(c) * ldS];
-            sacc = warp_sum(sacc);
-            if (lane == 0) red[warp] = sacc;
-            __syncthreads();
-            if (tid == 0) {
-              double s2 = 0.0;
-              for (int w = 0; w < kOWarps; ++w) s2 += red[w];
-              upd[c] = dir[c] = sqrt(s2);
-            }
-          } else if (tid == 0) {
-            upd[c] = uu * sqrt(t);
-          }
-          __syncthreads();
-        }
+      for (int cb = 0; cb < nown;) {
+        const int rem = nown - cb;
+        const int U = rem <= 1 ? 1 : rem <= 2 ? 2 : rem <= 4 ? 4 : 8;
+        if (U == 1) tall_cols<1>(S, ldS, cb, nown, mypos, v, j, M, tau, upd, dir, thr, red);
+        else if (U == 2) tall_cols<2>(S, ldS, cb, nown, mypos, v, j, M, tau, upd, dir, thr, red);
+        else if (U == 4) tall_cols<4>(S, ldS, cb, nown, mypos, v, j, M, tau, upd, dir, thr, red);
+        else tall_cols<8>(S, ldS, cb, nown, mypos, v, j, M, tau, upd, dir, thr, red);
+        cb += U;
       }
     }
     __syncthreads();
@@ -3544,11 +3593,9 @@ void cpqr_prof_dump() {
   SBX_CUDA(cudaMemcpyFromSymbol(h, g_cpqr_prof, sizeof(h)));
   for (int j = 0; j < 64; ++j) {
     if (h[j * 8 + 5] == 0) break;
-    std::fprintf(stderr, "step %2d:", j);
-    int last = 5;
-    while (last < 7 && h[j * 8 + last + 1]) ++last;
-    for (int q = 1; q <= last; ++q) std::fprintf(stderr, " %6lld", h[j * 8 + q] - h[j * 8 + q - 1]);
-    std::fprintf(stderr, "  | next %lld\n", j < 63 && h[j * 8 + 8] ? h[j * 8 + 8] - h[j * 8 + last] : 0LL);
+    std::fprintf(stderr, "step %2d: (rel. to slot 0)", j);
+    for (int q = 1; q < 8; ++q) std::fprintf(stderr, " %8lld", h[j * 8 + q] ? h[j * 8 + q] - h[j * 8] : 0LL);
+    std::fprintf(stderr, "  | next %lld\n", j < 63 && h[j * 8 + 8] ? h[j * 8 + 8] - h[j * 8] : 0LL);
   }
 }
 #endif

@@ -133,7 +133,12 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
                    : jobs)
         .push_back(j);
   }
-  if (log) std::fprintf(stderr, "[sbx-id]%s\n", line.c_str());
+  cudaEvent_t lg0 = nullptr, lg1 = nullptr;
+  if (log) {
+    SBX_CUDA(cudaEventCreate(&lg0));
+    SBX_CUDA(cudaEventCreate(&lg1));
+    SBX_CUDA(cudaEventRecord(lg0, s));
+  }
   // The register-resident cluster engine and the one-CTA / TSQR engines
   // hold no grid-wide barriers, so when a round has both they run side by
   // side (the register engine on a forked stream) and share the chip's
@@ -167,6 +172,15 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   cpqr_stream_batched(strm, s);
   cpqr_rows_batched(rows, s);
   if (fork) SBX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  if (log) {  // diagnostics: the batch's device time (serialises the stream)
+    float ms = 0.f;
+    SBX_CUDA(cudaEventRecord(lg1, s));
+    SBX_CUDA(cudaEventSynchronize(lg1));
+    SBX_CUDA(cudaEventElapsedTime(&ms, lg0, lg1));
+    std::fprintf(stderr, "[sbx-id %.3f ms]%s\n", double(ms), line.c_str());
+    SBX_CUDA(cudaEventDestroy(lg0));
+    SBX_CUDA(cudaEventDestroy(lg1));
+  }
 }
 
 // ---------------------------------------------------------------- rendezvous

@@ -109,6 +109,35 @@ int replay(const char* dir, const std::vector<int>& engines) {
       if (shown++ < 4) desc += kv.first + "*" + std::to_string(kv.second) + " ";
     if (shapes.size() > 4) desc += "...";
     std::printf("batch %3d (%3lld probs) %-44s", seq, np, desc.c_str());
+    if (std::getenv("ID_STATS")) {  // per problem class: count, steps taken (auto routing)
+      i64 tot = 0;
+      for (const auto& p : probs) tot += i64(p.M) * p.n;
+      DevBuf<double> work(static_cast<size_t>(tot));
+      std::vector<IdProblem> ps;
+      i64 o = 0;
+      for (const auto& p : probs) {
+        SBX_CUDA(cudaMemcpy(work.get() + o, p.w.data(), p.w.size() * 8, cudaMemcpyHostToDevice));
+        ps.push_back({work.get() + o, p.M, p.n, p.M});
+        o += i64(p.M) * p.n;
+      }
+      IdBatch b;
+      b.factor(ps, probs[0].eps, s);
+      std::map<std::pair<int, int>, std::vector<i64>> cls;
+      double fl = 0;
+      for (size_t q = 0; q < probs.size(); ++q) {
+        const i64 k = b.eps_rank(q, 1e-300);
+        cls[{probs[q].M, probs[q].n}].push_back(k);
+        for (i64 j = 0; j < k; ++j) fl += 4.0 * double(probs[q].M - j) * double(probs[q].n - j);
+      }
+      std::printf("\n  flops %.3g; classes:", fl);
+      for (const auto& kv : cls) {
+        i64 mx = 0, sm = 0;
+        for (i64 k : kv.second) mx = std::max(mx, k), sm += k;
+        std::printf(" %dx%d*%zu(k avg %.0f max %lld)", kv.first.first, kv.first.second, kv.second.size(),
+                    double(sm) / kv.second.size(), (long long)mx);
+      }
+      std::printf("\n  ");
+    }
     double b = 1e30;
     for (size_t q = 0; q < engines.size(); ++q) {
       int k0 = -1;
@@ -162,6 +191,12 @@ int main(int argc, char** argv) {
       {"upd leaves 513x256 r12 x151", {{513, 256, 12, 151}}},
       {"upd leaves 1088x256 r25 x32", {{1088, 256, 25, 32}}},
       {"upd near 8192x256 r80 x4", {{8192, 256, 80, 4}}},
+      {"upd near 8192x256 r16 x1", {{8192, 256, 16, 1}}},
+      {"upd tall 511/767x128 r55 x240", {{511, 128, 55, 120}, {767, 128, 55, 120}}},
+      {"upd tall 511/767x128 r55 x60", {{511, 128, 55, 30}, {767, 128, 55, 30}}},
+      {"upd tall 767x128 r55 x1", {{767, 128, 55, 1}}},
+      {"upd near 8192x256 r16 x4", {{8192, 256, 16, 4}}},
+      {"upd near 2048x256 r16 x1", {{2048, 256, 16, 1}}},
       {"upd leaves all", {{257, 256, 12, 151}, {513, 256, 12, 151}, {1088, 256, 25, 32}}},
       {"upd leaves 257x256 r12 x1", {{257, 256, 12, 1}}},
       {"upd leaves 257x256 r12 x32", {{257, 256, 12, 32}}},
@@ -239,7 +274,8 @@ int main(int argc, char** argv) {
       if (ok) std::printf("  e%d %8.3f ms (k0 %d)", e, best, rank0);
 #ifdef SBX_CPQR_PROF
       std::fflush(stdout);
-      cpqr_prof_dump();
+      if (e == 7) cpqr_rows_prof_dump();
+      else cpqr_prof_dump();
 #endif
     }
     std::printf("\n");
