@@ -65,6 +65,16 @@ void cpqr_reg_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // cpqr_rows_cluster gives the smallest G that fits (0: not applicable).
 int cpqr_rows_cluster(int M, int n);
 void cpqr_rows_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// One-exchange row-split cluster CPQR (engine 8, cpqr_push.cu): the same
+// slab split, but one pushed exchange per step (unscaled pivot-column dots
+// and row j, st.async into every CTA's slot, mbarrier transaction counts).
+int cpqr_push_cluster(int M, int n);
+void cpqr_push_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Register-resident row-split cluster CPQR (engine 9, cpqr_push.cu): the
+// slab in registers (<= 32 rows per thread), one pushed exchange and two CTA
+// barriers per step, next pivot chosen before the update.
+int cpqr_regrows_cluster(int M, int n);
+void cpqr_regrows_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // Streaming one-CTA CPQR (M <= 1088): columns beyond the shared-memory slab
 // are updated in place in global memory (L2).
 bool cpqr_stream_ok(int M, int n);

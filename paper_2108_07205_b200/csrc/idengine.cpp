@@ -56,7 +56,7 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
   KernelTimer kt("id_factor", s);  // every CPQR engine launch of the batch (bench: step-dominant family)
-  std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows;
+  std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows, push, rrow;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
@@ -100,9 +100,29 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   static const bool no_rows = std::getenv("SBX_NO_ROWS") != nullptr;  // diagnostics
   bool rows_all = !no_rows && !crowded && !all.empty() && all.size() <= 24;
   for (const auto& j : all) rows_all = rows_all && cpqr_rows_cluster(j.M, j.n) > 0;
+  // The register-resident row-split engine (engine 9: one pushed exchange
+  // per step, no serial section) takes every tall problem it holds while
+  // their clusters fit the chip in about two waves (measured on the replayed
+  // cfg2 rounds of <= 151 problems: 2.09 -> 1.86, 1.40 -> 1.10, 1.00 -> 0.45,
+  // 0.78 -> 0.33, 0.43 -> 0.24, 0.40 -> 0.21 ms); crowded rounds keep the
+  // throughput engines below.
+  static const bool no_rr = std::getenv("SBX_NO_RR") != nullptr;  // diagnostics
+  static const i64 rr_cap = [] {
+    const char* e = std::getenv("SBX_RR_CAP");
+    return e ? std::atoll(e) : i64(-1);
+  }();
+  i64 rr_ctas = 0;
+  for (const auto& j : all) {
+    const int g = cpqr_regrows_cluster(j.M, j.n);
+    rr_ctas += g > 0 ? g : 0;
+  }
+  const bool rr_route = !no_rr && rr_ctas > 0 && rr_ctas <= (rr_cap >= 0 ? rr_cap : 2 * i64(sms));
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
+    if (engine == 8 && cpqr_push_cluster(j.M, j.n) == 0) engine = 0;  // does not fit: auto route
+    if (engine == 9 && cpqr_regrows_cluster(j.M, j.n) == 0) engine = 0;
+    if (engine == 0 && rr_route && cpqr_regrows_cluster(j.M, j.n) > 0) engine = 9;
     if (engine == 0 && rows_all) engine = 7;
     if (engine == 0) {
       const int g = cpqr_smem_ctas(j.M, j.n);
@@ -130,6 +150,8 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
      : engine == 5 ? reg
      : engine == 6 ? strm
      : engine == 7 ? rows
+     : engine == 8 ? push
+     : engine == 9 ? rrow
                    : jobs)
         .push_back(j);
   }
@@ -164,6 +186,31 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     }
     SBX_CUDA(cudaEventRecord(ev_join, side));
   }
+  // engine 9 (clusters, no grid-wide barriers) likewise runs beside the
+  // other engines of the round on its own forked stream
+  static const int fork_rr_env = [] {
+    const char* e = std::getenv("SBX_RR_FORK");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool fork_rr = fork_rr_env != 0 && !rrow.empty() &&
+                       !(jobs.empty() && big.empty() && chip.empty() && clus.empty() && reg.empty() && strm.empty() &&
+                         rows.empty() && push.empty());
+  static thread_local cudaStream_t side_rr = nullptr;
+  static thread_local cudaEvent_t ev_fork_rr = nullptr, ev_join_rr = nullptr;
+  if (fork_rr) {
+    if (!side_rr) {
+      SBX_CUDA(cudaStreamCreateWithFlags(&side_rr, cudaStreamNonBlocking));
+      SBX_CUDA(cudaEventCreateWithFlags(&ev_fork_rr, cudaEventDisableTiming));
+      SBX_CUDA(cudaEventCreateWithFlags(&ev_join_rr, cudaEventDisableTiming));
+    }
+    SBX_CUDA(cudaEventRecord(ev_fork_rr, s));
+    SBX_CUDA(cudaStreamWaitEvent(side_rr, ev_fork_rr, 0));
+    {
+      StreamScope ss(side_rr);
+      cpqr_regrows_batched(rrow, side_rr);
+    }
+    SBX_CUDA(cudaEventRecord(ev_join_rr, side_rr));
+  }
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
   cpqr_smem_batched(chip, s);
@@ -171,6 +218,9 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   if (!fork) cpqr_reg_batched(reg, s);
   cpqr_stream_batched(strm, s);
   cpqr_rows_batched(rows, s);
+  cpqr_push_batched(push, s);
+  if (!fork_rr) cpqr_regrows_batched(rrow, s);
+  if (fork_rr) SBX_CUDA(cudaStreamWaitEvent(s, ev_join_rr, 0));
   if (fork) SBX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
   if (log) {  // diagnostics: the batch's device time (serialises the stream)
     float ms = 0.f;

@@ -24,6 +24,7 @@ using namespace sbx;
 namespace sbx {
 void cpqr_prof_dump();
 void cpqr_rows_prof_dump();
+void cpqr_push_prof_dump();
 }
 #endif
 
@@ -147,6 +148,7 @@ int replay(const char* dir, const std::vector<int>& engines) {
       std::printf("\n[first problem %dx%d]\n", probs[0].M, probs[0].n);
       std::fflush(stdout);
       if (engines[q] == 7) cpqr_rows_prof_dump();
+      else if (engines[q] == 8 || engines[q] == 9) cpqr_push_prof_dump();
       else cpqr_prof_dump();
 #endif
       if (ms < 0) {

@@ -195,3 +195,39 @@ def test_row_id_rows_engine(sb, po, shape):
     if k + 3 <= r:
         kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=7)
         assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
+
+
+@pytest.mark.parametrize("engine", [8, 9])
+@pytest.mark.parametrize("shape", [(30, 257), (97, 257), (57, 513), (98, 513), (28, 1088), (112, 369),
+                                   (128, 767), (8, 64), (4, 9), (64, 3000), (200, 600), (1, 40), (116, 861),
+                                   (250, 1000)])
+def test_row_id_push_engine(sb, po, shape, engine):
+    """One-exchange row-split cluster CPQR (engines 8 and 9, cpqr_push.cu:
+    pivot-column dots pushed with st.async, mbarrier transaction counts; slab
+    in shared memory / in registers): same pivots and ranks as the oracle,
+    exact skeleton identity, forced-rank extension keeps the eps skeleton."""
+    m, n = shape
+    rng = np.random.default_rng(5 * m + n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=engine)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    if k + 3 <= r:
+        kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=engine)
+        assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
+
+
+@pytest.mark.parametrize("engine", [8, 9])
+def test_row_id_push_engine_deterministic(sb, engine):
+    rng = np.random.default_rng(19)
+    w = spectrum_matrix(116, 861, 10.0 ** (-12 * np.arange(116) / 116), rng)
+    first = sb.row_id(w, 1e-10, engine=engine)
+    for _ in range(3):
+        again = sb.row_id(w, 1e-10, engine=engine)
+        assert again[0] == first[0]
+        assert np.array_equal(again[1], first[1]) and np.array_equal(again[2], first[2])
