@@ -125,7 +125,16 @@ const char* sbx_last_error(void) { return g_err.c_str(); }
 
 int sbx_init(int device) {
   return guard([&] {
+    // The per-step path waits on the device between its ID rounds (perm /
+    // diag come back to the host): spin-wait so a waiting host thread is not
+    // descheduled (SBX_SCHEDULE=yield|block|auto restores the driver's choice).
+    static const char* sched = std::getenv("SBX_SCHEDULE");
+    const unsigned flag = !sched ? cudaDeviceScheduleSpin
+                          : std::strcmp(sched, "yield") == 0 ? cudaDeviceScheduleYield
+                          : std::strcmp(sched, "block") == 0 ? cudaDeviceScheduleBlockingSync
+                          : cudaDeviceScheduleAuto;
     SBX_CUDA(cudaSetDevice(device));
+    if (cudaSetDeviceFlags(flag) != cudaSuccess) (void)cudaGetLastError();  // context already set up: keep its flags
     (void)sbx::lib_stream();
   });
 }

@@ -93,6 +93,27 @@ class StreamScope {
   cudaStream_t prev_;
 };
 
+// A stream forked from `parent` (its work starts after the parent's queued
+// work) for launches that should run beside the parent's next ones; join()
+// makes the parent wait for it.  Streams and their fork/join events come
+// from a process-wide pool: the per-step host threads are short-lived, so
+// thread-local streams would be created (a driver call that can stall for
+// tens of milliseconds under contention) and leaked every step.
+class SideStream {
+ public:
+  SideStream(cudaStream_t parent, bool high_priority = false);
+  ~SideStream();
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
+  cudaStream_t get() const { return s_; }
+  void join(cudaStream_t parent);
+
+ private:
+  cudaStream_t s_ = nullptr;
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
+  bool high_ = false;
+};
+
 // Thread-local switch: while set, the ID engines avoid cooperative launches
 // (grid-wide co-residency), which other streams' kernels can starve.
 bool& no_coop_flag();

@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -979,28 +980,16 @@ void cpqr_regrows_batched(const std::vector<QrJob>& all, cudaStream_t s) {
   }
   static thread_local JobTablePush tab;
   const QrJob* dj = tab.upload(jobs, s);
-  static thread_local std::vector<cudaStream_t> side;
-  static thread_local std::vector<cudaEvent_t> evs;
-  static thread_local cudaEvent_t ev_fork = nullptr;
+  // every (G, RPT, gsz) group launches on its own stream forked from s, so
+  // the groups run side by side
   const size_t ng = groups.size();
-  if (ng > 1) {
-    if (!ev_fork) SBX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    while (side.size() < ng - 1) {
-      cudaStream_t st;
-      cudaEvent_t ev;
-      SBX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-      SBX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      side.push_back(st);
-      evs.push_back(ev);
-    }
-    SBX_CUDA(cudaEventRecord(ev_fork, s));
-    for (size_t g = 0; g + 1 < ng; ++g) SBX_CUDA(cudaStreamWaitEvent(side[g], ev_fork, 0));
-  }
+  std::vector<std::unique_ptr<SideStream>> side;
+  for (size_t g = 0; g < ng; ++g) side.emplace_back(new SideStream(s));
   size_t gi = 0;
   for (const auto& kv : groups) {
     const int C = kv.first.first, R = kv.first.second & 0xff;
     const auto sp = spans[gi];
-    cudaStream_t st = gi == 0 ? s : side[gi - 1];
+    cudaStream_t st = side[gi]->get();
     size_t smem = 0;
     int threads = 32;
     for (size_t q = sp.first; q < sp.second; ++q) {
@@ -1022,10 +1011,9 @@ void cpqr_regrows_batched(const std::vector<QrJob>& all, cudaStream_t s) {
     const QrJob* jp = dj + sp.first;
     SBX_CUDA(cudaLaunchKernelEx(&cfg, rr_kernel(R, rr_gsz(jobs[sp.first].n)), jp));
     SBX_LAUNCHED();
-    if (gi > 0) SBX_CUDA(cudaEventRecord(evs[gi - 1], st));
+    side[gi]->join(s);
     ++gi;
   }
-  for (size_t g = 0; g + 1 < ng; ++g) SBX_CUDA(cudaStreamWaitEvent(s, evs[g], 0));
 }
 
 }  // namespace sbx

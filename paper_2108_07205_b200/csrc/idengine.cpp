@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <string>
 #include <condition_variable>
+#include <memory>
 #include <mutex>
 
 namespace sbx {
@@ -170,21 +171,11 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     return e ? std::atoi(e) : 1;
   }();
   const bool fork = fork_env != 0 && !reg.empty() && !jobs.empty();
-  static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::unique_ptr<SideStream> side;
   if (fork) {
-    if (!side) {
-      SBX_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      SBX_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      SBX_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
-    SBX_CUDA(cudaEventRecord(ev_fork, s));
-    SBX_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    {
-      StreamScope ss(side);
-      cpqr_reg_batched(reg, side);
-    }
-    SBX_CUDA(cudaEventRecord(ev_join, side));
+    side.reset(new SideStream(s));
+    StreamScope ss(side->get());
+    cpqr_reg_batched(reg, side->get());
   }
   // engine 9 (clusters, no grid-wide barriers) likewise runs beside the
   // other engines of the round on its own forked stream
@@ -195,21 +186,11 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   const bool fork_rr = fork_rr_env != 0 && !rrow.empty() &&
                        !(jobs.empty() && big.empty() && chip.empty() && clus.empty() && reg.empty() && strm.empty() &&
                          rows.empty() && push.empty());
-  static thread_local cudaStream_t side_rr = nullptr;
-  static thread_local cudaEvent_t ev_fork_rr = nullptr, ev_join_rr = nullptr;
+  std::unique_ptr<SideStream> side_rr;
   if (fork_rr) {
-    if (!side_rr) {
-      SBX_CUDA(cudaStreamCreateWithFlags(&side_rr, cudaStreamNonBlocking));
-      SBX_CUDA(cudaEventCreateWithFlags(&ev_fork_rr, cudaEventDisableTiming));
-      SBX_CUDA(cudaEventCreateWithFlags(&ev_join_rr, cudaEventDisableTiming));
-    }
-    SBX_CUDA(cudaEventRecord(ev_fork_rr, s));
-    SBX_CUDA(cudaStreamWaitEvent(side_rr, ev_fork_rr, 0));
-    {
-      StreamScope ss(side_rr);
-      cpqr_regrows_batched(rrow, side_rr);
-    }
-    SBX_CUDA(cudaEventRecord(ev_join_rr, side_rr));
+    side_rr.reset(new SideStream(s));
+    StreamScope ss(side_rr->get());
+    cpqr_regrows_batched(rrow, side_rr->get());
   }
   qr_batched(jobs, s);
   cpqr_coop_batched(big, s);
@@ -220,8 +201,8 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   cpqr_rows_batched(rows, s);
   cpqr_push_batched(push, s);
   if (!fork_rr) cpqr_regrows_batched(rrow, s);
-  if (fork_rr) SBX_CUDA(cudaStreamWaitEvent(s, ev_join_rr, 0));
-  if (fork) SBX_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+  if (side_rr) side_rr->join(s);
+  if (side) side->join(s);
   if (log) {  // diagnostics: the batch's device time (serialises the stream)
     float ms = 0.f;
     SBX_CUDA(cudaEventRecord(lg1, s));

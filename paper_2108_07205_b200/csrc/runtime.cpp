@@ -153,7 +153,12 @@ void* dev_alloc(size_t bytes) {
     }
   }
   void* p = nullptr;
+  static const bool alloc_log = std::getenv("SBX_ALLOC_LOG") != nullptr;  // diagnostics
+  const auto ta = alloc_log ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
   cudaError_t e = cudaMalloc(&p, c);
+  if (alloc_log)
+    std::fprintf(stderr, "[sbx-alloc] %zu bytes %.3f ms\n", c,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count());
   if (e != cudaSuccess) {  // release cached blocks and retry once
     (void)cudaGetLastError();
     std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -172,6 +177,56 @@ void dev_free(void* p, size_t bytes) {
   const cudaStream_t st = cur_stream();
   std::lock_guard<std::mutex> lk(g_pool_mu);
   g_pool[st][size_class(bytes)].push_back(p);
+}
+
+namespace {
+struct SidePool {
+  std::mutex mu;
+  struct Entry {
+    cudaStream_t s;
+    cudaEvent_t fork, join;
+  };
+  std::vector<Entry> free[2];
+};
+SidePool& side_pool() {
+  static SidePool* p = new SidePool;  // never destroyed (streams outlive static destruction order)
+  return *p;
+}
+}  // namespace
+
+SideStream::SideStream(cudaStream_t parent, bool high_priority) : high_(high_priority) {
+  auto& pool = side_pool();
+  {
+    std::lock_guard<std::mutex> lk(pool.mu);
+    auto& fl = pool.free[high_ ? 1 : 0];
+    if (!fl.empty()) {
+      s_ = fl.back().s;
+      fork_ = fl.back().fork;
+      join_ = fl.back().join;
+      fl.pop_back();
+    }
+  }
+  if (!s_) {
+    int least = 0, greatest = 0;
+    SBX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SBX_CUDA(cudaStreamCreateWithPriority(&s_, cudaStreamNonBlocking, high_ ? greatest : least));
+    SBX_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    SBX_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
+  }
+  SBX_CUDA(cudaEventRecord(fork_, parent));
+  SBX_CUDA(cudaStreamWaitEvent(s_, fork_, 0));
+}
+
+void SideStream::join(cudaStream_t parent) {
+  SBX_CUDA(cudaEventRecord(join_, s_));
+  SBX_CUDA(cudaStreamWaitEvent(parent, join_, 0));
+}
+
+SideStream::~SideStream() {
+  if (!s_) return;
+  auto& pool = side_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  pool.free[high_ ? 1 : 0].push_back({s_, fork_, join_});
 }
 
 void parallel_tasks(const std::vector<std::function<void(cudaStream_t)>>& tasks, cudaStream_t main,

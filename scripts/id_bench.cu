@@ -51,8 +51,9 @@ float time_batch(const std::vector<Prob>& probs, int e, cudaStream_t s, int* k0,
     SBX_CUDA(cudaMemcpy(pristine.get() + off[q], probs[q].w.data(), probs[q].w.size() * 8, cudaMemcpyHostToDevice));
   std::vector<IdProblem> ps;
   for (size_t q = 0; q < probs.size(); ++q) ps.push_back({work.get() + off[q], probs[q].M, probs[q].n, probs[q].M});
-  float best = 1e30f;
-  for (int rep = 0; rep < 3; ++rep) {
+  float best = 1e30f, worst = 0.f;
+  static const int reps = std::getenv("ID_REPS") ? std::atoi(std::getenv("ID_REPS")) : 3;
+  for (int rep = 0; rep < reps; ++rep) {
     SBX_CUDA(cudaMemcpyAsync(work.get(), pristine.get(), size_t(tot) * 8, cudaMemcpyDeviceToDevice, s));
     IdBatch b;
     b.force_engine = e;
@@ -71,8 +72,10 @@ float time_batch(const std::vector<Prob>& probs, int e, cudaStream_t s, int* k0,
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     best = std::min(best, ms);
+    worst = std::max(worst, ms);
     *k0 = int(b.eps_rank(0, 1e-10));
   }
+  if (reps > 3) std::printf(" [worst %.3f]", worst);
   return best;
 }
 
