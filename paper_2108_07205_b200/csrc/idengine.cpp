@@ -103,21 +103,23 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   for (const auto& j : all) rows_all = rows_all && cpqr_rows_cluster(j.M, j.n) > 0;
   // The register-resident row-split engine (engine 9: one pushed exchange
   // per step, no serial section) takes every tall problem it holds while
-  // their clusters fit the chip in about two waves (measured on the replayed
-  // cfg2 rounds of <= 151 problems: 2.09 -> 1.86, 1.40 -> 1.10, 1.00 -> 0.45,
-  // 0.78 -> 0.33, 0.43 -> 0.24, 0.40 -> 0.21 ms); crowded rounds keep the
-  // throughput engines below.
+  // their minimal clusters need at most ~4.75 waves of SMs (replayed cfg2
+  // rounds, routing cap 296 / 700 / 1000 / 3000 CTAs: step median 20.9 /
+  // 19.9 / 19.8 / 22.8 ms; the 151- and 75-problem rounds 2.09 -> 1.06 and
+  // 1.40 -> 0.83 ms, the <= 38-problem rounds 1.00 -> 0.46, 0.78 -> 0.34,
+  // 0.43 -> 0.24, 0.40 -> 0.21 ms); crowded rounds keep the throughput
+  // engines below.
   static const bool no_rr = std::getenv("SBX_NO_RR") != nullptr;  // diagnostics
   static const i64 rr_cap = [] {
     const char* e = std::getenv("SBX_RR_CAP");
-    return e ? std::atoll(e) : i64(-1);
+    return e ? std::atoll(e) : i64(-1);  // default: 19/4 of the SM count (replayed cfg2 rounds)
   }();
   i64 rr_ctas = 0;
   for (const auto& j : all) {
     const int g = cpqr_regrows_cluster(j.M, j.n);
     rr_ctas += g > 0 ? g : 0;
   }
-  const bool rr_route = !no_rr && rr_ctas > 0 && rr_ctas <= (rr_cap >= 0 ? rr_cap : 2 * i64(sms));
+  const bool rr_route = !no_rr && rr_ctas > 0 && rr_ctas <= (rr_cap >= 0 ? rr_cap : 19 * i64(sms) / 4);
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
