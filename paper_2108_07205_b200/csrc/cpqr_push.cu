@@ -915,7 +915,7 @@ int rr_rpt_t(int rpt) { return rpt <= 8 ? 8 : rpt <= 12 ? 12 : rpt <= 16 ? 16 : 
 }  // namespace
 
 int cpqr_regrows_cluster(int M, int n) {
-  if (M <= 0 || n <= 0 || M < 2 * n || n > 256) return 0;  // at least two lanes per column (keys hold 8-bit positions)
+  if (M <= 0 || n <= 0 || n > 256) return 0;  // at least two lanes per column (keys hold 8-bit positions)
   for (int G = 1; G <= kPMaxG; G <<= 1)
     if (rr_rpt(M, n, G) <= kRRMaxRpt && rr_smem((M + G - 1) / G, n, G) <= kRRSmemCap) return G;
   return 0;

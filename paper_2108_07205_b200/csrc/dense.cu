@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <memory>
 #include <mutex>
 
 #include "dense.hpp"
@@ -3333,7 +3334,26 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   static const bool old_tsqr = std::getenv("SBX_TSQR_WARP") != nullptr;  // diagnostics: warp-layout kernel
   std::vector<QrJob> quad, wide;
   for (const auto& j : tall) (!old_tsqr && j.n <= kQBm ? quad : wide).push_back(j);
+  // the three launches (quad TSQR, warp TSQR, one-CTA CPQR) run side by side:
+  // all but the first on streams forked from s
+  const cudaStream_t s0 = s;
+  std::vector<std::unique_ptr<SideStream>> sides;
+  int used = 0;
+  static const bool no_fork = std::getenv("SBX_QR_NOFORK") != nullptr;  // diagnostics
+  auto next_stream = [&]() -> cudaStream_t {
+    if (used++ == 0 || no_fork) return s0;
+    sides.emplace_back(new SideStream(s0));
+    return sides.back()->get();
+  };
+  struct Join {
+    std::vector<std::unique_ptr<SideStream>>& v;
+    cudaStream_t p;
+    ~Join() {
+      for (auto& x : v) x->join(p);
+    }
+  } join{sides, s0};
   if (!quad.empty()) {
+    s = next_stream();
     int nmax = 0;
     for (const auto& j : quad) nmax = std::max(nmax, j.n);
     const QrJob* d = qtab.upload(quad, s);
@@ -3341,6 +3361,7 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     SBX_LAUNCHED();
   }
   if (!wide.empty()) {
+    s = next_stream();
     int nmax = 0;
     for (const auto& j : wide) nmax = std::max(nmax, j.n);
     const size_t smem = tsqr_smem(nmax);
@@ -3364,6 +3385,7 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
     base = std::max(base, size_t(blk ? cpqr_blocked_head(j.n) : 3 * j.n + 72) * sizeof(double));
   need = std::max(need, base);
   require(base <= kSmemCap, "qr_batched: too many columns for the norm tables");
+  s = next_stream();
   const QrJob* d = tab.upload(plain, s);
   qr_kernel<<<unsigned(plain.size()), kT, need, s>>>(d, int(need / sizeof(double)), blk);
   SBX_LAUNCHED();

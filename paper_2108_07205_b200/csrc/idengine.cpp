@@ -114,18 +114,20 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     const char* e = std::getenv("SBX_RR_CAP");
     return e ? std::atoll(e) : i64(-1);  // default: 19/4 of the SM count (replayed cfg2 rounds)
   }();
+  // (tall problems only: on W^T with M < 2n it loses to the throughput engines)
+  auto rr_fit = [](const QrJob& j) { return j.M >= 2 * j.n ? cpqr_regrows_cluster(j.M, j.n) : 0; };
   i64 rr_ctas = 0;
-  for (const auto& j : all) {
-    const int g = cpqr_regrows_cluster(j.M, j.n);
-    rr_ctas += g > 0 ? g : 0;
-  }
+  for (const auto& j : all) rr_ctas += rr_fit(j);
   const bool rr_route = !no_rr && rr_ctas > 0 && rr_ctas <= (rr_cap >= 0 ? rr_cap : 19 * i64(sms) / 4);
+  // in crowded rounds engine 9 still takes the problems the register
+  // cluster engine would (wide-ish W^T stopping after a few steps)
+  static const bool rr_e5 = !no_rr && std::getenv("SBX_RR_E5") != nullptr;  // measured: slower (off)
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
     if (engine == 8 && cpqr_push_cluster(j.M, j.n) == 0) engine = 0;  // does not fit: auto route
     if (engine == 9 && cpqr_regrows_cluster(j.M, j.n) == 0) engine = 0;
-    if (engine == 0 && rr_route && cpqr_regrows_cluster(j.M, j.n) > 0) engine = 9;
+    if (engine == 0 && rr_route && rr_fit(j) > 0) engine = 9;
     if (engine == 0 && rows_all) engine = 7;
     if (engine == 0) {
       const int g = cpqr_smem_ctas(j.M, j.n);
@@ -139,7 +141,7 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
       const int cs = cpqr_cluster_size(j.M, j.n);
       if (!crowded && chip_ok) engine = 3;
       else if (tsqr_ok) engine = 1;
-      else if (rc >= 0 && !(rc >= 3 && cs > 0 && cs < rg)) engine = 5;
+      else if (rc >= 0 && !(rc >= 3 && cs > 0 && cs < rg)) engine = (rr_e5 && rr_fit(j) > 0) ? 9 : 5;
       else if (one_cta) engine = 1;
       else if (!no_cluster && cs > 0) engine = 4;
       else if (chip_ok) engine = 3;
@@ -164,47 +166,35 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     SBX_CUDA(cudaEventCreate(&lg1));
     SBX_CUDA(cudaEventRecord(lg0, s));
   }
-  // The register-resident cluster engine and the one-CTA / TSQR engines
-  // hold no grid-wide barriers, so when a round has both they run side by
-  // side (the register engine on a forked stream) and share the chip's
-  // tail instead of following each other.
+  // The engine groups of a round hold no grid-wide barriers between each
+  // other, so they run side by side: the first non-empty group on s, every
+  // other one on a stream forked from s (pooled), all joined back into s.
   static const int fork_env = [] {
     const char* e = std::getenv("SBX_ID_FORK");
     return e ? std::atoi(e) : 1;
   }();
-  const bool fork = fork_env != 0 && !reg.empty() && !jobs.empty();
-  std::unique_ptr<SideStream> side;
-  if (fork) {
-    side.reset(new SideStream(s));
-    StreamScope ss(side->get());
-    cpqr_reg_batched(reg, side->get());
+  struct Group {
+    std::vector<QrJob>* v;
+    void (*fn)(const std::vector<QrJob>&, cudaStream_t);
+  };
+  const Group groups[] = {{&jobs, qr_batched},          {&rrow, cpqr_regrows_batched}, {&reg, cpqr_reg_batched},
+                          {&big, cpqr_coop_batched},    {&chip, cpqr_smem_batched},    {&clus, cpqr_cluster_batched},
+                          {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},    {&push, cpqr_push_batched}};
+  std::vector<std::unique_ptr<SideStream>> sides;
+  bool first = true;
+  for (const auto& g : groups) {
+    if (g.v->empty()) continue;
+    const bool forkable = fork_env == 1 || (fork_env == 2 && (g.v == &rrow || g.v == &reg));
+    if (first || !forkable) {
+      g.fn(*g.v, s);
+      first = false;
+      continue;
+    }
+    sides.emplace_back(new SideStream(s));
+    StreamScope ss(sides.back()->get());
+    g.fn(*g.v, sides.back()->get());
   }
-  // engine 9 (clusters, no grid-wide barriers) likewise runs beside the
-  // other engines of the round on its own forked stream
-  static const int fork_rr_env = [] {
-    const char* e = std::getenv("SBX_RR_FORK");
-    return e ? std::atoi(e) : 1;
-  }();
-  const bool fork_rr = fork_rr_env != 0 && !rrow.empty() &&
-                       !(jobs.empty() && big.empty() && chip.empty() && clus.empty() && reg.empty() && strm.empty() &&
-                         rows.empty() && push.empty());
-  std::unique_ptr<SideStream> side_rr;
-  if (fork_rr) {
-    side_rr.reset(new SideStream(s));
-    StreamScope ss(side_rr->get());
-    cpqr_regrows_batched(rrow, side_rr->get());
-  }
-  qr_batched(jobs, s);
-  cpqr_coop_batched(big, s);
-  cpqr_smem_batched(chip, s);
-  cpqr_cluster_batched(clus, s);
-  if (!fork) cpqr_reg_batched(reg, s);
-  cpqr_stream_batched(strm, s);
-  cpqr_rows_batched(rows, s);
-  cpqr_push_batched(push, s);
-  if (!fork_rr) cpqr_regrows_batched(rrow, s);
-  if (side_rr) side_rr->join(s);
-  if (side) side->join(s);
+  for (auto& sd : sides) sd->join(s);
   if (log) {  // diagnostics: the batch's device time (serialises the stream)
     float ms = 0.f;
     SBX_CUDA(cudaEventRecord(lg1, s));

@@ -151,6 +151,26 @@ void* dev_alloc(size_t bytes) {
       it->second.pop_back();
       return p;
     }
+    // Another stream's pool has a free block of this class (blocks migrate
+    // between pools when a host thread frees on a different stream than it
+    // allocated on): take it, ordered after every use queued on that stream
+    // so far (an event recorded there now).  A cudaMalloc in steady state
+    // can stall the host for tens of milliseconds.
+    for (auto& sp : g_pool) {
+      if (sp.first == st) continue;
+      auto jt = sp.second.find(c);
+      if (jt == sp.second.end() || jt->second.empty()) continue;
+      void* p = jt->second.back();
+      jt->second.pop_back();
+      static cudaEvent_t ev = [] {
+        cudaEvent_t e = nullptr;
+        SBX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return e;
+      }();
+      SBX_CUDA(cudaEventRecord(ev, sp.first));
+      SBX_CUDA(cudaStreamWaitEvent(st, ev, 0));
+      return p;
+    }
   }
   void* p = nullptr;
   static const bool alloc_log = std::getenv("SBX_ALLOC_LOG") != nullptr;  // diagnostics

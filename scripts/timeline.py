@@ -57,6 +57,14 @@ def main():
     ev.sort(key=lambda e: e["ts"])
     walls = [1e3 * (b - a) for a, b in marks]
     print("step wall ms:", " ".join(f"{w:.1f}" for w in walls))
+    # the slowest step: every runtime call / kernel longer than 1 ms in it
+    # (trace timestamps are microseconds on the profiler's clock; the steps
+    # are located by the gaps between them, so take the longest busy window)
+    cpu = [e for e in allev if e.get("ph") == "X" and "dur" in e and e["dur"] > 1000.0]
+    cpu.sort(key=lambda e: e["ts"])
+    print("events > 1 ms (all steps):")
+    for e in cpu[:80]:
+        print(f"  ts {e['ts']:.0f} dur {1e-3 * e['dur']:8.3f} ms  cat {e.get('cat')}  tid {e.get('tid')}  {e['name'][:60]}")
     # split kernels into steps by gaps > 0.3 ms with no kernel running (host sync)
     groups, cur, end = [], [], -1.0
     for e in ev:
