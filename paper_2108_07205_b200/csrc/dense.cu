@@ -697,31 +697,35 @@ __global__ void __launch_bounds__(kT, 1) tsqr_cpqr_kernel(const QrJob* __restric
 //   two barriers per step (pivot partials; reflector).
 // Output contract as tsqr_cpqr_kernel: R0's CPQR factor in the first n rows
 // of the job matrix, columns in place (perm[l] = physical column at l).
-constexpr int kQT = 256;               // threads
+#ifndef SBX_QL
+#define SBX_QL 8
+#endif
+constexpr int kQL = SBX_QL;            // lanes per column group ("quad"); 4 or 8
+constexpr int kQT = 64 * kQL;          // threads: 64 groups, two columns each
 constexpr int kQWarps = kQT / 32;
-constexpr int kQRows = 32;             // rows per thread and column
-constexpr int kQBm = 4 * kQRows;       // rows per block; also the largest n
-constexpr int kQHalf = kQT / 4;        // column offset of a quad's second column
-constexpr int kQPad = kQRows + 2;      // padded quarter stride of v
+constexpr int kQRows = 128 / kQL;      // rows per thread and column
+constexpr int kQBm = kQL * kQRows;     // rows per block; also the largest n
+constexpr int kQHalf = kQT / kQL;      // column offset of a group's second column
+constexpr int kQPad = kQRows + 2;      // padded per-lane stride of v
 
 // quad-local shuffles: the callers branch per column pair (quad-uniformly)
-__device__ __forceinline__ unsigned quad_mask() { return 0xFu << (threadIdx.x & 28); }
+__device__ __forceinline__ unsigned quad_mask() { return ((1u << kQL) - 1u) << (threadIdx.x & (32 - kQL)); }
 
 __device__ __forceinline__ double quad_sum(double v) {
   const unsigned m = quad_mask();
-  v += __shfl_xor_sync(m, v, 1);
-  v += __shfl_xor_sync(m, v, 2);
+#pragma unroll
+  for (int o = 1; o < kQL; o <<= 1) v += __shfl_xor_sync(m, v, o);
   return v;
 }
 
 // register b[i] of the quad thread holding row `row` (quad-uniform result)
 __device__ __forceinline__ double quad_row(const double (&b)[kQRows], int row) {
   double x = 0.0;
-  const int ir = row >> 2;
+  const int ir = row / kQL;
 #pragma unroll
   for (int i = 0; i < kQRows; ++i)
     if (i == ir) x = b[i];
-  return __shfl_sync(quad_mask(), x, (threadIdx.x & 28) | (row & 3));
+  return __shfl_sync(quad_mask(), x, (threadIdx.x & (32 - kQL)) | (row & (kQL - 1)));
 }
 
 // shared-memory 16-byte load the compiler may not cache in registers across
@@ -814,7 +818,7 @@ __device__ __forceinline__ void quad_cpqr_reflector(double (&b)[kQRows], int j, 
   double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < kQRows; ++i)
-    if (q + 4 * i > j) s4[i & 3] = fma(b[i], b[i], s4[i & 3]);
+    if (q + kQL * i > j) s4[i & 3] = fma(b[i], b[i], s4[i & 3]);
   const double s = quad_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
   const double c0 = quad_row(b, j);
   double tau = 0.0, beta = c0, inv = 0.0;
@@ -830,7 +834,7 @@ __device__ __forceinline__ void quad_cpqr_reflector(double (&b)[kQRows], int j, 
     double e[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int row = q + 4 * (i + h);
+      const int row = q + kQL * (i + h);
       if (row > j) {
         b[i + h] *= inv;
         e[h] = b[i + h];
@@ -861,82 +865,29 @@ __device__ __forceinline__ void quad_downdate(const double (&b)[kQRows], int j, 
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < kQRows; ++i)
-      if (q + 4 * i > j) s = fma(b[i], b[i], s);
+      if (q + kQL * i > j) s = fma(b[i], b[i], s);
     upd = dirn = sqrt(quad_sum(s));
   } else {
     upd *= sqrt(t);
   }
 }
 
-size_t tsqr_quad_smem(int n) {
-  return size_t(n) * size_t(n + 1) * sizeof(double) + size_t(2 * 4 * kQPad + 16 + 2 * kQWarps) * sizeof(double) +
-         size_t(2 * kQWarps) * sizeof(int);
-}
-
-__global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restrict__ jobs, int phases) {
-  extern __shared__ double sm[];
-  const QrJob jb = jobs[blockIdx.x];
-  const int M = jb.M, n = jb.n, ldr = n + 1;
+// CPQR of the n x n upper-triangular R0 (Eigen ColPivHouseholderQR
+// semantics) held row-major in shared memory (ld ldr), quad layout (each
+// quad of 4 threads owns two columns, 32 rows each in registers): the
+// second phase of the TSQR and blocked-QR engines.  Writes the pivoted R
+// into the top n rows of jb.a, perm, diag and steps.
+__device__ __forceinline__ void quad_cpqr_r0(const QrJob& jb, const double* R, int ldr, double* vq, double* sc,
+                                             double* red, int* ired, int phases) {
+  const int n = jb.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = tid >> 2, q = tid & 3;
-  const int c0 = g, c1 = g + kQHalf;         // owned columns
+  const int g = tid / kQL, q = tid % kQL;
+  const int c0 = g, c1 = g + kQHalf;
   const bool h0 = c0 < n, h1 = c1 < n;
-  double* R = sm;                                  // n x n, row-major, ld n + 1
-  double* vq = R + n * ldr;                        // 2 x (4 x kQPad) reflector buffers
-  double* taus = vq + 2 * 4 * kQPad;               // 2 (+pad)
-  double* sc = taus + 8;                           // tau, beta
-  double* red = sc + 8;                            // kQWarps pivot partials
-  int* ired = reinterpret_cast<int*>(red + 2 * kQWarps);
-  for (int idx = tid; idx < n * ldr; idx += kQT) R[idx] = 0.0;
   double b[2][kQRows];
-  // ---------------- TSQR: R0 of W^T
-  for (int r0 = 0; r0 < ((phases & 4) ? 0 : M); r0 += kQBm) {
-    const int rb = min(kQBm, M - r0);
-    const double* s0 = jb.a + r0 + size_t(h0 ? c0 : 0) * jb.lda;
-    const double* s1 = jb.a + r0 + size_t(h1 ? c1 : 0) * jb.lda;
-#pragma unroll
-    for (int i = 0; i < kQRows; ++i) {
-      const int row = q + 4 * i;
-      b[0][i] = (h0 && row < rb) ? __ldg(s0 + row) : 0.0;
-      b[1][i] = (h1 && row < rb) ? __ldg(s1 + row) : 0.0;
-    }
-    __syncthreads();  // R of the previous block complete, buffers free
-    if (g == 0) quad_tsqr_reflector(b[0], R, ldr, 0, vq, taus, q);
-    __syncthreads();
-    for (int j = 0; j < n; ++j) {
-      const int cur = j & 1;
-      const bool a0 = h0 && c0 > j, a1 = h1 && c1 > j;
-      if (a0 || a1) {
-        const double tau = taus[cur];
-        if (tau != 0.0) {
-          const double e0 = a0 ? R[j * ldr + c0] : 0.0, e1 = a1 ? R[j * ldr + c1] : 0.0;
-          double tw0, tw1;
-          quad_apply_any(a0, a1, b, vq + cur * (4 * kQPad) + q * kQPad, tau, e0, e1, tw0, tw1);
-          if (q == 0) {
-            if (a0) R[j * ldr + c0] = e0 - tw0;
-            if (a1) R[j * ldr + c1] = e1 - tw1;
-          }
-        }
-        const int jn = j + 1;
-        if (jn < n && (jn & (kQHalf - 1)) == g) {  // look-ahead: next reflector
-          if (jn < kQHalf)
-            quad_tsqr_reflector(b[0], R, ldr, jn, vq + (cur ^ 1) * (4 * kQPad), taus + (cur ^ 1), q);
-          else
-            quad_tsqr_reflector(b[1], R, ldr, jn, vq + (cur ^ 1) * (4 * kQPad), taus + (cur ^ 1), q);
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // ---------------- CPQR of R0 (Eigen ColPivHouseholderQR semantics)
-  if (phases & 4) {  // diagnostics: CPQR of the top n x n block alone
-    __syncthreads();
-    for (int idx = tid; idx < n * n; idx += kQT) R[(idx % n) * ldr + idx / n] = jb.a[(idx % n) + size_t(idx / n) * jb.lda];
-    __syncthreads();
-  }
 #pragma unroll
   for (int i = 0; i < kQRows; ++i) {
-    const int row = q + 4 * i;
+    const int row = q + kQL * i;
     b[0][i] = (h0 && row < n) ? R[row * ldr + c0] : 0.0;
     b[1][i] = (h1 && row < n) ? R[row * ldr + c1] : 0.0;
   }
@@ -972,7 +923,7 @@ __global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restri
       bq = c1;
     }
 #pragma unroll
-    for (int o = 16; o >= 4; o >>= 1) {
+    for (int o = 16; o >= kQL; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int op = __shfl_xor_sync(0xffffffffu, bp, o);
       const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
@@ -1001,7 +952,7 @@ __global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restri
       }
     }
     const int p = bq, lp = bp;
-    double* v = vq + (j & 1) * (4 * kQPad);
+    double* v = vq + (j & 1) * (kQL * kQPad);
     // (2) Householder vector of the pivot column over rows >= j
     if (p == c0)
       quad_cpqr_reflector(b[0], j, v, sc, q);
@@ -1035,10 +986,378 @@ __global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restri
     if (q == 0) jb.perm[u ? pos1 : pos0] = cu;
 #pragma unroll
     for (int i = 0; i < kQRows; ++i) {
-      const int row = q + 4 * i;
+      const int row = q + kQL * i;
       if (row < n) jb.a[row + size_t(cu) * jb.lda] = b[u][i];
     }
   }
+}
+
+size_t tsqr_quad_smem(int n) {
+  return size_t(n) * size_t(n + 1) * sizeof(double) + size_t(2 * kQL * kQPad + 16 + 2 * kQWarps) * sizeof(double) +
+         size_t(2 * kQWarps) * sizeof(int);
+}
+
+__global__ void __launch_bounds__(kQT, 1) tsqr_quad_kernel(const QrJob* __restrict__ jobs, int phases) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n, ldr = n + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = tid / kQL, q = tid % kQL;
+  const int c0 = g, c1 = g + kQHalf;         // owned columns
+  const bool h0 = c0 < n, h1 = c1 < n;
+  double* R = sm;                                  // n x n, row-major, ld n + 1
+  double* vq = R + n * ldr;                        // 2 x (4 x kQPad) reflector buffers
+  double* taus = vq + 2 * kQL * kQPad;               // 2 (+pad)
+  double* sc = taus + 8;                           // tau, beta
+  double* red = sc + 8;                            // kQWarps pivot partials
+  int* ired = reinterpret_cast<int*>(red + 2 * kQWarps);
+  for (int idx = tid; idx < n * ldr; idx += kQT) R[idx] = 0.0;
+  double b[2][kQRows];
+  // ---------------- TSQR: R0 of W^T
+  for (int r0 = 0; r0 < ((phases & 4) ? 0 : M); r0 += kQBm) {
+    const int rb = min(kQBm, M - r0);
+    const double* s0 = jb.a + r0 + size_t(h0 ? c0 : 0) * jb.lda;
+    const double* s1 = jb.a + r0 + size_t(h1 ? c1 : 0) * jb.lda;
+#pragma unroll
+    for (int i = 0; i < kQRows; ++i) {
+      const int row = q + kQL * i;
+      b[0][i] = (h0 && row < rb) ? __ldg(s0 + row) : 0.0;
+      b[1][i] = (h1 && row < rb) ? __ldg(s1 + row) : 0.0;
+    }
+    __syncthreads();  // R of the previous block complete, buffers free
+    if (g == 0) quad_tsqr_reflector(b[0], R, ldr, 0, vq, taus, q);
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+      const int cur = j & 1;
+      const bool a0 = h0 && c0 > j, a1 = h1 && c1 > j;
+      if (a0 || a1) {
+        const double tau = taus[cur];
+        if (tau != 0.0) {
+          const double e0 = a0 ? R[j * ldr + c0] : 0.0, e1 = a1 ? R[j * ldr + c1] : 0.0;
+          double tw0, tw1;
+          quad_apply_any(a0, a1, b, vq + cur * (kQL * kQPad) + q * kQPad, tau, e0, e1, tw0, tw1);
+          if (q == 0) {
+            if (a0) R[j * ldr + c0] = e0 - tw0;
+            if (a1) R[j * ldr + c1] = e1 - tw1;
+          }
+        }
+        const int jn = j + 1;
+        if (jn < n && (jn & (kQHalf - 1)) == g) {  // look-ahead: next reflector
+          if (jn < kQHalf)
+            quad_tsqr_reflector(b[0], R, ldr, jn, vq + (cur ^ 1) * (kQL * kQPad), taus + (cur ^ 1), q);
+          else
+            quad_tsqr_reflector(b[1], R, ldr, jn, vq + (cur ^ 1) * (kQL * kQPad), taus + (cur ^ 1), q);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (phases & 4) {  // diagnostics: CPQR of the top n x n block alone
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += kQT) R[(idx % n) * ldr + idx / n] = jb.a[(idx % n) + size_t(idx / n) * jb.lda];
+    __syncthreads();
+  }
+  quad_cpqr_r0(jb, R, ldr, vq, sc, red, ired, phases);
+}
+
+// D = A B + C on the FP64 tensor cores (m8n8k4: lane l holds A[l/4][l%4],
+// B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- blocked QR (engine 10)
+// Tall W^T (M <= kBMaxM, n <= 128), one CTA per problem.  Phase 1 reduces
+// W^T to R0 by a blocked Householder QR (LAPACK dgeqrf/dlarft/dlarfb,
+// forward, columnwise): 16-column panels factored in shared memory (one
+// CTA barrier per column), the trailing matrix updated in place in global
+// memory (L2) by A <- A - V (T^T (V^T A)) on the FP64 tensor cores
+// (mma.sync.m8n8k4.f64 -> DMMA).  Phase 2 is the CPQR of R0 of the TSQR
+// engine (quad_cpqr_r0): same pivots as the CPQR of W^T in exact arithmetic
+// (R0 has W^T's column space geometry).
+constexpr int kBW = 16;           // panel width
+constexpr int kBMaxM = 1280;      // rows (panel in shared memory)
+constexpr int kBT = kQT;          // threads (the CPQR phase's quad layout)
+constexpr int kBWarps = kBT / 32;
+constexpr int kBLdW = 128 + 4;    // row stride of the W / W2 buffers
+constexpr int kBRpl = (kBMaxM + 32 * (kQT / 32) - 1) / (32 * (kQT / 32));  // panel rows per lane
+
+#ifdef SBX_CPQR_PROF
+__device__ long long g_bqr_prof[16 * 8];
+#define BQR_T(ph)                                                                               \
+  do {                                                                                          \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && c0 / kBW < 16) g_bqr_prof[(c0 / kBW) * 8 + (ph)] = clock64(); \
+  } while (0)
+#else
+#define BQR_T(ph) \
+  do {            \
+  } while (0)
+#endif
+size_t bqr_smem(int M, int n) {
+  const size_t ldp = size_t((M + 3) / 4 * 4);
+  const size_t p1 = ldp * kBW + 2 * size_t(kBW) * kBLdW + 2 * kBW * kBW + 2 * kBW;  // P, W, W2, G, T, tau
+  const size_t p2 = size_t(n) * size_t(n + 1) + 2 * kQL * kQPad + 16 + 2 * kQWarps + kQWarps;  // R, vq, sc, red, ired
+  return std::max(p1, p2) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(kBT, 1) bqr_kernel(const QrJob* __restrict__ jobs, int phases) {
+  extern __shared__ double sm[];
+  const QrJob jb = jobs[blockIdx.x];
+  const int M = jb.M, n = jb.n, lda = jb.lda;
+  double* const A = jb.a;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int ldp = (M + 3) / 4 * 4;
+  double* P = sm;                         // ldp x 16 (column-major): panel, then V
+  double* W = P + size_t(ldp) * kBW;      // 16 x kBLdW: V^T A_trail
+  double* W2 = W + kBW * kBLdW;           // 16 x kBLdW: T^T W
+  double* Gm = W2 + kBW * kBLdW;          // 16 x 16: V^T V (column-major)
+  double* T = Gm + kBW * kBW;             // 16 x 16 (column-major)
+  double* tau = T + kBW * kBW;            // 16
+  for (int c0 = 0; c0 < ((phases & 4) ? 0 : n); c0 += kBW) {
+    const int w = min(kBW, n - c0), ml = M - c0, kp = (ml + 3) / 4 * 4, nt = n - c0 - w;
+    BQR_T(0);
+    // ---- (1) the panel: rows c0.., columns c0..c0+w (zero padded to kp x 16)
+    for (int k = warp; k < kBW; k += kBWarps) {
+      const double* src = A + c0 + size_t(c0 + (k < w ? k : 0)) * lda;
+      for (int i0 = 0; i0 < kp; i0 += 128) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + lane + 32 * u;
+          v[u] = (k < w && i < ml) ? src[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + lane + 32 * u;
+          if (i < kp) P[i + size_t(ldp) * k] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    BQR_T(1);
+    // ---- (2) panel QR, rows split over the warps (warp w owns panel rows
+    // [w rpw, (w + 1) rpw), lane rows w rpw + lane + 32 t): per column, the
+    // partial sums x^T a_k of every warp (two CTA barriers per column)
+    {
+      const int rpw = (kp + kBWarps - 1) / kBWarps;
+      const int rb0 = warp * rpw, rb1 = min(kp, rb0 + rpw);
+      double* part = W;   // kBWarps x 16 partial sums (W is free until step 4)
+      double* scv = W2;   // tw_k / (alpha - beta) per column, scale, beta
+      for (int j = 0; j < w; ++j) {
+        double acc[kBW];
+#pragma unroll
+        for (int k = 0; k < kBW; ++k) acc[k] = 0.0;
+#pragma unroll
+        for (int t = 0; t < kBRpl; ++t) {
+          const int i = rb0 + lane + 32 * t;
+          if (i < rb1 && i > j && i < ml) {
+            const double x = P[i + size_t(ldp) * j];
+#pragma unroll
+            for (int k = 0; k < kBW; ++k) acc[k] = fma(x, P[i + size_t(ldp) * k], acc[k]);
+          }
+        }
+        // reduce-scatter over the warp (16 + 8 + 4 + 2 + 1 shuffles): lane l
+        // ends with the warp sum of value l >> 1
+#pragma unroll
+        for (int h = kBW / 2; h >= 1; h >>= 1) {
+          const bool up = (lane & (2 * h)) != 0;  // keep the upper h values
+#pragma unroll
+          for (int k = 0; k < h; ++k) {
+            const double send = up ? acc[k] : acc[k + h];
+            const double keep = up ? acc[k + h] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+          }
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        if ((lane & 1) == 0) part[warp * kBW + (lane >> 1)] = acc[0];
+        __syncthreads();
+        if (warp == 0) {  // (the whole warp: the shuffle below)
+          double tot = 0.0;
+          if (lane < kBW)
+            for (int v = 0; v < kBWarps; ++v) tot += part[v * kBW + lane];  // warp order
+          const double s2 = __shfl_sync(0xffffffffu, tot, j);
+          const double alpha = P[j + size_t(ldp) * j];
+          double t = 0.0, beta = alpha, sc = 0.0;
+          if (s2 > DBL_MIN) {
+            beta = sqrt(fma(alpha, alpha, s2));
+            if (alpha >= 0.0) beta = -beta;
+            sc = 1.0 / (alpha - beta);
+            t = (beta - alpha) / beta;
+          }
+          if (lane > j && lane < w) {
+            const double tw = t * (P[j + size_t(ldp) * lane] + sc * tot);
+            scv[lane] = tw * sc;
+            P[j + size_t(ldp) * lane] -= tw;  // R(j, k)
+          }
+          if (lane == 0) {
+            scv[kBW] = sc;
+            tau[j] = t;
+            P[j + size_t(ldp) * j] = beta;
+          }
+        }
+        __syncthreads();
+        const double sc = scv[kBW];
+#pragma unroll
+        for (int t = 0; t < kBRpl; ++t) {
+          const int i = rb0 + lane + 32 * t;
+          if (i < rb1 && i > j && i < ml) {
+            double* xr = P + i;
+            const double x = xr[size_t(ldp) * j];
+#pragma unroll
+            for (int k = 0; k < kBW; ++k)
+              if (k > j && k < w) xr[size_t(ldp) * k] = fma(-x, scv[k], xr[size_t(ldp) * k]);
+            xr[size_t(ldp) * j] = x * sc;
+          }
+        }
+        // (each warp updates only its own rows, which its next partial sums
+        // read; the scalars' buffers are rewritten after the next barrier)
+      }
+    }
+    __syncthreads();
+    BQR_T(2);
+    // ---- (3) R rows of the panel to global memory; V gets its unit diagonal
+    for (int k = warp; k < w; k += kBWarps)
+      for (int i = lane; i <= k; i += 32) A[(c0 + i) + size_t(c0 + k) * lda] = P[i + size_t(ldp) * k];
+    __syncthreads();
+    for (int idx = tid; idx < kBW * kBW; idx += kBT) {
+      const int i = idx % kBW, k = idx / kBW;
+      if (i <= k) P[i + size_t(ldp) * k] = (i == k && k < w) ? 1.0 : 0.0;
+    }
+    if (nt <= 0) {
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    BQR_T(3);
+    // ---- (4) G = V^T V (warps 0-3: one 8 x 8 tile each) and W = V^T A_trail
+    if (warp < 4) {
+      const int ti = warp >> 1, tj2 = warp & 1;
+      double g0 = 0.0, g1 = 0.0;
+      for (int k0 = 0; k0 < kp; k0 += 4) {
+        const double a = P[(k0 + tig) + size_t(ldp) * (ti * 8 + gid)];
+        const double b = P[(k0 + tig) + size_t(ldp) * (tj2 * 8 + gid)];
+        dmma(g0, g1, a, b);
+      }
+      Gm[(ti * 8 + gid) + kBW * (tj2 * 8 + 2 * tig)] = g0;
+      Gm[(ti * 8 + gid) + kBW * (tj2 * 8 + 2 * tig + 1)] = g1;
+    }
+    {
+      // W = V^T A_trail: a warp per 8-column tile of A_trail (both 8-row
+      // tiles of W share its B fragments = A_trail(k0 + tig, cj * 8 + gid),
+      // streamed from L2 with 8 loads in flight)
+      const int ctiles = (nt + 7) / 8;
+      for (int cj = warp; cj < ctiles; cj += kBWarps) {
+        const bool cok = cj * 8 + gid < nt;
+        const double* ac = A + c0 + size_t(cok ? c0 + w + cj * 8 + gid : c0 + w) * lda;
+        double w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0;
+        for (int k0 = 0; k0 < kp; k0 += 32) {
+          double bb[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = k0 + 4 * u + tig;
+            bb[u] = (cok && r < ml) ? ac[r] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = k0 + 4 * u + tig;
+            if (k0 + 4 * u < kp) {
+              dmma(w00, w01, P[r + size_t(ldp) * gid], bb[u]);
+              dmma(w10, w11, P[r + size_t(ldp) * (8 + gid)], bb[u]);
+            }
+          }
+        }
+        W[gid * kBLdW + cj * 8 + 2 * tig] = w00;
+        W[gid * kBLdW + cj * 8 + 2 * tig + 1] = w01;
+        W[(8 + gid) * kBLdW + cj * 8 + 2 * tig] = w10;
+        W[(8 + gid) * kBLdW + cj * 8 + 2 * tig + 1] = w11;
+      }
+    }
+    __syncthreads();
+    BQR_T(4);
+    // ---- (5) T (dlarft, forward columnwise): T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j)
+    if (warp == 0) {
+      for (int j = 0; j < kBW; ++j) {
+        const double tj = j < w ? tau[j] : 0.0;
+        double v = 0.0;
+        if (lane < j) {
+          double s2 = 0.0;
+          for (int l = lane; l < j; ++l) s2 = fma(T[lane + kBW * l], Gm[l + kBW * j], s2);
+          v = -tj * s2;
+        }
+        __syncwarp();
+        if (lane < kBW) T[lane + kBW * j] = lane < j ? v : (lane == j ? tj : 0.0);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    BQR_T(5);
+    // ---- (6) W2 = T^T W
+    for (int idx = tid; idx < kBW * nt; idx += kBT) {
+      const int a = idx / nt, c = idx % nt;
+      double s2 = 0.0;
+      for (int b = 0; b <= a; ++b) s2 = fma(T[b + kBW * a], W[b * kBLdW + c], s2);
+      W2[a * kBLdW + c] = s2;
+    }
+    __syncthreads();
+    BQR_T(6);
+    // ---- (7) A_trail -= V W2 (8 x 8 tiles, K = 16: four DMMA each); a warp
+    // takes four row tiles of one column tile at a time (8 loads in flight)
+    {
+      const int rtiles = (kp + 7) / 8, ctiles = (nt + 7) / 8, rgroups = (rtiles + 3) / 4;
+      for (int t = warp; t < rgroups * ctiles; t += kBWarps) {
+        const int rg = t % rgroups, cj = t / rgroups;
+        const int cc = cj * 8 + 2 * tig;
+        const bool c0ok = cc < nt, c1ok = cc + 1 < nt;
+        double wb[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) wb[kk] = (cj * 8 + gid < nt) ? W2[(4 * kk + tig) * kBLdW + cj * 8 + gid] : 0.0;
+        double d[4][2];
+        double* ap[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = (rg * 4 + u) * 8 + gid;
+          const bool rok = r < ml;
+          ap[u] = A + (c0 + (rok ? r : 0)) + size_t(c0 + w + (c0ok ? cc : 0)) * lda;
+          d[u][0] = (rok && c0ok) ? ap[u][0] : 0.0;
+          d[u][1] = (rok && c1ok) ? ap[u][lda] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rt = rg * 4 + u;
+          if (rt >= rtiles) continue;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const double va = (rt * 8 + gid < kp) ? -P[(rt * 8 + gid) + size_t(ldp) * (4 * kk + tig)] : 0.0;
+            dmma(d[u][0], d[u][1], va, wb[kk]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = (rg * 4 + u) * 8 + gid;
+          if (r < ml && c0ok) ap[u][0] = d[u][0];
+          if (r < ml && c1ok) ap[u][lda] = d[u][1];
+        }
+      }
+    }
+    __syncthreads();
+    BQR_T(7);
+  }
+  // ---- phase 2: CPQR of R0 (the top n rows' upper triangle)
+  double* R = sm;
+  const int ldr = n + 1;
+  double* vq = R + n * ldr;
+  double* sc = vq + 2 * kQL * kQPad;
+  double* red = sc + 8;
+  int* ired = reinterpret_cast<int*>(red + 2 * kQWarps);
+  for (int idx = tid; idx < n * n; idx += kBT) {
+    const int i = idx % n, k = idx / n;
+    R[i * ldr + k] = i <= k ? A[i + size_t(k) * lda] : 0.0;
+  }
+  __syncthreads();
+  quad_cpqr_r0(jb, R, ldr, vq, sc, red, ired, phases);
 }
 
 // ---------------------------------------------------------------- cooperative CPQR
@@ -2382,11 +2701,6 @@ __global__ void __launch_bounds__(kIWarps * 32) interp_warp_kernel(const InterpJ
 // ---------------------------------------------------------------- GEMM (DMMA)
 constexpr int gTM = 64, gTN = 64, gKC = 16, gPad = 8;
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 // 8-byte asynchronous global -> shared copy; src_bytes 0 zero-fills
 __device__ __forceinline__ void gcp_async8(double* dst, const double* src, bool pred) {
@@ -3391,6 +3705,45 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   SBX_LAUNCHED();
 }
 
+constexpr size_t kBSmemCap = 225 * 1024;
+bool bqr_ok(int M, int n) {
+  return n >= 1 && n <= kQBm && M > n && M <= kBMaxM && bqr_smem(M, n) <= kBSmemCap;
+}
+
+#ifdef SBX_CPQR_PROF
+void bqr_prof_dump() {
+  long long h[16 * 8];
+  SBX_CUDA(cudaMemcpyFromSymbol(h, g_bqr_prof, sizeof(h)));
+  for (int p = 0; p < 16; ++p) {
+    if (h[p * 8 + 7] == 0) break;
+    std::fprintf(stderr, "bqr panel %2d:", p);
+    for (int q = 1; q < 8; ++q) std::fprintf(stderr, " %7lld", h[p * 8 + q] - h[p * 8 + q - 1]);
+    std::fprintf(stderr, "\n");
+  }
+}
+#endif
+
+void bqr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
+  if (jobs.empty()) return;
+  static std::once_flag attr;
+  std::call_once(attr, [] {
+    SBX_CUDA(cudaFuncSetAttribute(bqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBSmemCap)));
+  });
+  size_t smem = 0;
+  for (const auto& j : jobs) {
+    require(bqr_ok(j.M, j.n), "bqr: problem outside the blocked-QR engine's range");
+    smem = std::max(smem, bqr_smem(j.M, j.n));
+  }
+  static thread_local JobTable<QrJob> tab;
+  const QrJob* d = tab.upload(jobs, s);
+  static const int phases = [] {  // diagnostics: bit 2 skips phase 1, bit 3 the CPQR of R0
+    const char* e = std::getenv("SBX_BQR_PHASES");
+    return e ? std::atoi(e) : 0;
+  }();
+  bqr_kernel<<<unsigned(jobs.size()), kBT, smem, s>>>(d, phases);
+  SBX_LAUNCHED();
+}
+
 void cpqr_coop_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   if (jobs.empty()) return;
   int dev = 0, sms = 148;
@@ -3811,6 +4164,10 @@ void cpqr_reg_batched(const std::vector<QrJob>& all, cudaStream_t s) {
   for (const auto& o : order) jobs.push_back(all[o.second]);
   static thread_local JobTable<QrJob> tjobs;
   const QrJob* dj = tjobs.upload(jobs, s);
+  // the launches (one per layout / cluster size) run side by side: all but
+  // the first on streams forked from s
+  static const bool no_fork = std::getenv("SBX_REG_NOFORK") != nullptr;  // diagnostics
+  std::vector<std::unique_ptr<SideStream>> sides;
   for (size_t g0 = 0; g0 < jobs.size();) {
     const int key = order[g0].first;
     size_t g1 = g0;
@@ -3820,15 +4177,21 @@ void cpqr_reg_batched(const std::vector<QrJob>& all, cudaStream_t s) {
       ++g1;
     }
     const int c = key / 64, G = key % 64, np = int(g1 - g0);
+    cudaStream_t st = s;
+    if (g0 > 0 && !no_fork) {
+      sides.emplace_back(new SideStream(s));
+      st = sides.back()->get();
+    }
     switch (c) {
-      case 0: launch_reg<9, 4>(dj + g0, np, G, size_max, s); break;
-      case 1: launch_reg<17, 2>(dj + g0, np, G, size_max, s); break;
-      case 2: launch_reg<20, 2>(dj + g0, np, G, size_max, s); break;
-      case 3: launch_reg<27, 1>(dj + g0, np, G, size_max, s); break;
-      default: launch_reg<34, 1>(dj + g0, np, G, size_max, s); break;
+      case 0: launch_reg<9, 4>(dj + g0, np, G, size_max, st); break;
+      case 1: launch_reg<17, 2>(dj + g0, np, G, size_max, st); break;
+      case 2: launch_reg<20, 2>(dj + g0, np, G, size_max, st); break;
+      case 3: launch_reg<27, 1>(dj + g0, np, G, size_max, st); break;
+      default: launch_reg<34, 1>(dj + g0, np, G, size_max, st); break;
     }
     g0 = g1;
   }
+  for (auto& sd : sides) sd->join(s);
 }
 
 void interp_batched(const std::vector<InterpJob>& all, cudaStream_t s) {

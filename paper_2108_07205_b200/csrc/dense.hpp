@@ -75,6 +75,11 @@ void cpqr_push_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // barriers per step, next pivot chosen before the update.
 int cpqr_regrows_cluster(int M, int n);
 void cpqr_regrows_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
+// Blocked QR (engine 10): tall W^T (M <= 1280, n <= 128), one CTA per
+// problem; 16-column Householder panels in shared memory, the trailing
+// matrix updated in global memory on DMMA, then the CPQR of R0 on chip.
+bool bqr_ok(int M, int n);
+void bqr_batched(const std::vector<QrJob>& jobs, cudaStream_t s);
 // Streaming one-CTA CPQR (M <= 1088): columns beyond the shared-memory slab
 // are updated in place in global memory (L2).
 bool cpqr_stream_ok(int M, int n);

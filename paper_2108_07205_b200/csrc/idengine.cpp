@@ -57,7 +57,7 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
   KernelTimer kt("id_factor", s);  // every CPQR engine launch of the batch (bench: step-dominant family)
-  std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows, push, rrow;
+  std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows, push, rrow, bq;
   static const int tsqr_max_m = [] {
     const char* e = std::getenv("SBX_TSQR_MAXM");
     return e ? std::atoi(e) : 0;
@@ -122,11 +122,17 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   // in crowded rounds engine 9 still takes the problems the register
   // cluster engine would (wide-ish W^T stopping after a few steps)
   static const bool rr_e5 = !no_rr && std::getenv("SBX_RR_E5") != nullptr;  // measured: slower (off)
+  static const bool rr_tsqr = !no_rr && std::getenv("SBX_RR_TSQR") != nullptr;
+  // crowded tall problems: the blocked DMMA QR (engine 10) instead of the
+  // streaming TSQR where it holds them (replayed cfg2 batches: 8.3 -> 6.6,
+  // 4.4 -> 3.7, 1.54 -> 1.22 ms)
+  static const bool use_bqr = std::getenv("SBX_NO_BQR") == nullptr;
   std::string line;
   for (const auto& j : all) {
     int engine = force_engine;
     if (engine == 8 && cpqr_push_cluster(j.M, j.n) == 0) engine = 0;  // does not fit: auto route
     if (engine == 9 && cpqr_regrows_cluster(j.M, j.n) == 0) engine = 0;
+    if (engine == 10 && !bqr_ok(j.M, j.n)) engine = 0;
     if (engine == 0 && rr_route && rr_fit(j) > 0) engine = 9;
     if (engine == 0 && rows_all) engine = 7;
     if (engine == 0) {
@@ -140,7 +146,7 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
       const int rc = no_reg ? -1 : cpqr_reg_config(j.M, j.n, &rg);
       const int cs = cpqr_cluster_size(j.M, j.n);
       if (!crowded && chip_ok) engine = 3;
-      else if (tsqr_ok) engine = 1;
+      else if (tsqr_ok) engine = (rr_tsqr && rr_fit(j) > 0) ? 9 : (use_bqr && bqr_ok(j.M, j.n)) ? 10 : 1;
       else if (rc >= 0 && !(rc >= 3 && cs > 0 && cs < rg)) engine = (rr_e5 && rr_fit(j) > 0) ? 9 : 5;
       else if (one_cta) engine = 1;
       else if (!no_cluster && cs > 0) engine = 4;
@@ -157,6 +163,7 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
      : engine == 7 ? rows
      : engine == 8 ? push
      : engine == 9 ? rrow
+     : engine == 10 ? bq
                    : jobs)
         .push_back(j);
   }
@@ -179,7 +186,8 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
   };
   const Group groups[] = {{&jobs, qr_batched},          {&rrow, cpqr_regrows_batched}, {&reg, cpqr_reg_batched},
                           {&big, cpqr_coop_batched},    {&chip, cpqr_smem_batched},    {&clus, cpqr_cluster_batched},
-                          {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},    {&push, cpqr_push_batched}};
+                          {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},    {&push, cpqr_push_batched},
+                          {&bq, bqr_batched}};
   std::vector<std::unique_ptr<SideStream>> sides;
   bool first = true;
   for (const auto& g : groups) {

@@ -25,6 +25,7 @@ namespace sbx {
 void cpqr_prof_dump();
 void cpqr_rows_prof_dump();
 void cpqr_push_prof_dump();
+void bqr_prof_dump();
 }
 #endif
 
@@ -152,6 +153,7 @@ int replay(const char* dir, const std::vector<int>& engines) {
       std::fflush(stdout);
       if (engines[q] == 7) cpqr_rows_prof_dump();
       else if (engines[q] == 8 || engines[q] == 9) cpqr_push_prof_dump();
+      else if (engines[q] == 10) bqr_prof_dump();
       else cpqr_prof_dump();
 #endif
       if (ms < 0) {

@@ -231,3 +231,25 @@ def test_row_id_push_engine_deterministic(sb, engine):
         again = sb.row_id(w, 1e-10, engine=engine)
         assert again[0] == first[0]
         assert np.array_equal(again[1], first[1]) and np.array_equal(again[2], first[2])
+
+
+@pytest.mark.parametrize("shape", [(30, 257), (97, 257), (57, 513), (98, 513), (112, 369), (128, 767),
+                                   (8, 64), (116, 861), (110, 1172), (128, 1250), (17, 40), (1, 9)])
+def test_row_id_blocked_qr_engine(sb, po, shape):
+    """Blocked DMMA QR + CPQR of R0 (engine 10, bqr_kernel) on tall W^T: same
+    pivots and ranks as the oracle's CPQR of W^T, exact skeleton identity,
+    forced-rank extension keeps the eps skeleton."""
+    m, n = shape
+    rng = np.random.default_rng(7 * m + n)
+    r = min(m, n)
+    w = spectrum_matrix(m, n, 10.0 ** (-14 * np.arange(r) / r), rng)
+    k, J, P = sb.row_id(w, 1e-10, engine=10)
+    ko, Jo, Po = po.row_id(w, 1e-10)
+    assert abs(k - ko) <= 1
+    kk = min(k, ko) - 2
+    assert np.array_equal(J[:kk], Jo[:kk])
+    assert skeleton_identity_exact(k, J, P)
+    assert np.linalg.norm(w - P @ w[J[:k]], 2) <= 10 * 1e-10 * np.linalg.norm(w, 2)
+    if k + 3 <= r:
+        kw, Jw, Pw = sb.row_id(w, forced=k + 3, engine=10)
+        assert kw == k + 3 and np.array_equal(Jw[:k], J[:k])
