@@ -413,7 +413,7 @@ def step_profile(sb, torch, stream, step, ms_step, reps=3):
     sb.api.kernel_timing(False)
     fp64 = measured_fp64_peak()["value"]
     ach = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    return {"kernel": "id_factor (batched CPQR engines: cpqr_onchip / tsqr_quad / cpqr_reg / qr)",
+    return {"kernel": "id_factor (batched CPQR engines: cpqr_regrows / bqr / cpqr_onchip / tsqr_quad / cpqr_reg / qr)",
             "bound": "tensor", "achieved": round(ach, 4), "peak": fp64, "unit": "TFLOP/s",
             "frac": round(ach / fp64, 4), "ms_per_step": round(ms / reps, 3),
             "launches_per_step": cnt // reps, "share_of_step": round(ms / reps / ms_step, 3),
