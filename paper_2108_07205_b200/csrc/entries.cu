@@ -4,6 +4,7 @@
 // no FMA contraction, IEEE division.  Stores are coalesced along the
 // leading dimension of the column-major destination.
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "entries.hpp"
@@ -108,6 +109,147 @@ __device__ double entry(const EntryView& v, i64 rs, i64 cs) {
   return out;
 }
 
+// The whole 2 x 2 block A(2i + a, 2j + b) of `entry` with the geometry,
+// the division and the logarithms formed once: every output is
+// produced by exactly the operations entry() uses for it, so the bits agree.
+__device__ void entry_block(const EntryView& v, i64 i, i64 j, double (&o)[2][2]) {
+  const int ci = v.comp[i];
+  const double c4 = 1.0 / (4.0 * kPi * v.mu);
+  if (i == j) {
+    const double wi = v.w[i];
+    const double dl = -v.kappa[i] / (2.0 * kPi) * wi;
+    const double tx = v.tx[i], ty = v.ty[i];
+    const bool sl = single_layer(v, ci), nul = in_null(v, ci);
+    double corr = 0.0;
+    if (sl) {
+      const i64 n = v.sl_n;
+      const int loc = v.sl_i[i], q = v.sl_i[n + i];
+      const double jac = v.sl_d[n + i];
+      const double lam = v.sl_tab[v.sl_i[4 * n + i] + loc * q + loc];
+      corr = c4 * (-lam * jac - wi * log(jac));
+    }
+    const double sm = wi * c4;
+    const double nx = v.nx[i], ny = v.ny[i];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double ta = (a == 0 || a != b) ? tx : ty;
+        const double tb = (b == 1 || a != b) ? ty : tx;
+        double out = dl * ta * tb;
+        if (a == b) out = v.jump + out;
+        if (sl) {
+          out += sm * ta * tb;
+          if (a == b) out += corr;
+        }
+        if (nul) {
+          const double na = a == 0 ? nx : ny;
+          const double nb = b == 0 ? nx : ny;
+          out += wi * na * nb;
+        }
+        o[a][b] = out;
+      }
+    return;
+  }
+  const int cj = v.comp[j];
+  const double rx = v.x[i] - v.x[j];
+  const double ry = v.y[i] - v.y[j];
+  const double r2 = rx * rx + ry * ry;
+  const double wj = v.w[j];
+  const double dn = (rx * v.nx[j] + ry * v.ny[j]) / (kPi * r2 * r2);
+  const double c = wj * dn;
+  const bool slj = single_layer(v, cj), nul = in_null(v, ci) && in_null(v, cj);
+  double sc = 0.0, lg = 0.0;
+  if (slj) {
+    sc = wj * c4 / r2;
+    bool corrected = false;
+    if (ci == cj) {
+      const i64 n = v.sl_n;
+      const int np = v.sl_i[3 * n + i];
+      int diff = v.sl_i[2 * n + i] - v.sl_i[2 * n + j];
+      if (diff < 0) diff += np;
+      const int locj = v.sl_i[j];
+      const double xj = v.sl_d[j], jacj = v.sl_d[n + j];
+      double lam = 0.0, xi = 0.0;
+      if (diff == 0) {
+        const int q = v.sl_i[n + i];
+        lam = v.sl_tab[v.sl_i[4 * n + i] + v.sl_i[i] * q + locj];
+        xi = v.sl_d[i];
+        corrected = true;
+      } else if (diff == 1 || diff == np - 1) {
+        const int dir = diff == 1 ? 0 : 1;
+        lam = v.sl_lam[(dir * n + i) * v.sl_qmax + locj];
+        xi = v.sl_d[(2 + dir) * n + i];
+        corrected = true;
+      }
+      if (corrected) lg = c4 * (-lam * jacj - wj * (0.5 * log(r2) - log(fabs(xj - xi))));
+    }
+    if (!corrected) lg = c4 * wj * (-0.5 * log(r2));
+  }
+  const double nxi = v.nx[i], nyi = v.ny[i], nxj = v.nx[j], nyj = v.ny[j];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double ra = (a == 0 || a != b) ? rx : ry;
+      const double rb = (b == 1 || a != b) ? ry : rx;
+      double out = c * ra * rb;
+      if (slj) {
+        out += sc * ra * rb;
+        if (a == b) out += lg;
+      }
+      if (nul) {
+        const double na = a == 0 ? nxi : nyi;
+        const double nb = b == 0 ? nxj : nyj;
+        out += wj * na * nb;
+      }
+      o[a][b] = out;
+    }
+}
+
+// A 2 x 2 output tile (rows r, r + 1 of columns c, c + 1 of a column-major
+// block with leading dimension ld): when both index pairs are the two
+// components of one node each, one entry_block; otherwise entry by entry.
+// Adjacent rows leave as one 16-byte store when aligned.
+__device__ __forceinline__ void tile_2x2(const EntryView& v, const i64* rl, const i64* cl, int r, int c, int nr,
+                                         int nc, bool transpose, double* col0, double* col1) {
+  const bool r2ok = r + 1 < nr, c2ok = c + 1 < nc;
+  const i64 ra = rl[r], rb = r2ok ? rl[r + 1] : -1;
+  const i64 ca = cl[c], cb = c2ok ? cl[c + 1] : -1;
+  double o[2][2];
+  const bool rpair = r2ok && (ra & 1) == 0 && rb == ra + 1;
+  const bool cpair = c2ok && (ca & 1) == 0 && cb == ca + 1;
+  if (rpair && cpair) {
+    double e[2][2];
+    if (!transpose) {
+      entry_block(v, node_of(v, ra >> 1), node_of(v, ca >> 1), e);
+      o[0][0] = e[0][0], o[0][1] = e[0][1], o[1][0] = e[1][0], o[1][1] = e[1][1];
+    } else {  // tile (r, c) of A(cols, rows)^T: o[x][y] = A(cl[c + y], rl[r + x])
+      entry_block(v, node_of(v, ca >> 1), node_of(v, ra >> 1), e);
+      o[0][0] = e[0][0], o[0][1] = e[1][0], o[1][0] = e[0][1], o[1][1] = e[1][1];
+    }
+  } else {
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) {
+        const i64 ri = x ? rb : ra, cj = y ? cb : ca;
+        o[x][y] = (ri >= 0 && cj >= 0) ? (transpose ? entry(v, cj, ri) : entry(v, ri, cj)) : 0.0;
+      }
+  }
+#pragma unroll
+  for (int y = 0; y < 2; ++y) {
+    if (y == 1 && !c2ok) break;
+    double* dst = (y ? col1 : col0) + r;
+    if (r2ok && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      *reinterpret_cast<double2*>(dst) = make_double2(o[0][y], o[1][y]);
+    } else {
+      dst[0] = o[0][y];
+      if (r2ok) dst[1] = o[1][y];
+    }
+  }
+}
+
 struct M2d {
   double a00, a01, a10, a11;
   __device__ double at(int i, int j) const {
@@ -158,12 +300,15 @@ __global__ void block_jobs_kernel(EntryView v, const BlockJob* __restrict__ jobs
                                   const i64* __restrict__ rows, const i64* __restrict__ cols,
                                   double* __restrict__ out, const i64* __restrict__ dst_cols) {
   const BlockJob jb = jobs[blockIdx.y];
-  const i64 total = i64(jb.nr) * jb.nc;
+  const int tr = (jb.nr + 1) / 2, tc = (jb.nc + 1) / 2;  // 2 x 2 tiles
+  const i64 total = i64(tr) * tc;
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
-    const int r = int(idx % jb.nr), c = int(idx / jb.nr);
-    const i64 oc = jb.dst_col_off >= 0 ? dst_cols[jb.dst_col_off + c] : c;
-    out[jb.out_off + r + oc * jb.ld] = entry(v, rows[jb.row_off + r], cols[jb.col_off + c]);
+    const int r = 2 * int(idx % tr), c = 2 * int(idx / tr);
+    const i64 oc0 = jb.dst_col_off >= 0 ? dst_cols[jb.dst_col_off + c] : c;
+    const i64 oc1 = c + 1 < jb.nc ? (jb.dst_col_off >= 0 ? dst_cols[jb.dst_col_off + c + 1] : c + 1) : oc0;
+    tile_2x2(v, rows + jb.row_off, cols + jb.col_off, r, c, jb.nr, jb.nc, false, out + jb.out_off + oc0 * jb.ld,
+             out + jb.out_off + oc1 * jb.ld);
   }
 }
 
@@ -233,12 +378,15 @@ __global__ void near_jobs_kernel(EntryView v, const NearJob* __restrict__ jobs,
                                  const i64* __restrict__ cand, const i64* __restrict__ nearv,
                                  double* __restrict__ out) {
   const NearJob jb = jobs[blockIdx.y];
-  const i64 total = i64(jb.n_near) * jb.n;
+  const int tr = (jb.n_near + 1) / 2, tc = (jb.n + 1) / 2;  // 2 x 2 tiles
+  const i64 total = i64(tr) * tc;
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
-    const int r = int(idx % jb.n_near), c = int(idx / jb.n_near);
-    const i64 cs = cand[jb.cand_off + c], ns = nearv[jb.near_off + r];
-    out[jb.out_off + r + i64(c) * jb.ld] = jb.transpose ? entry(v, ns, cs) : entry(v, cs, ns);
+    const int r = 2 * int(idx % tr), c = 2 * int(idx / tr);
+    // output (r, c) = transpose ? A(near_r, cand_c) : A(cand_c, near_r)
+    double* base = out + jb.out_off;
+    tile_2x2(v, nearv + jb.near_off, cand + jb.cand_off, r, c, jb.n_near, jb.n, !jb.transpose,
+             base + i64(c) * jb.ld, base + i64(c + 1 < jb.n ? c + 1 : c) * jb.ld);
   }
 }
 

@@ -103,4 +103,21 @@ def test_evaluate_solution_matches_oracle(sb, po):  # nystrom.cpp:408-448
         ref = o1.evaluate_velocity(po.MIXED, tau[:, r], tg)
         assert np.max(np.abs(vel[:, :, r] - ref)) <= 1e-12 * np.max(np.abs(ref))
     assert list(near) == [False, False, False, True, True]
-    assert np.all(np.isfinite(pre))
+    # pressure: numpy restatement of evaluate_solution's pressure sum
+    # (nystrom.cpp:437-440 with kernels.cpp:37-48: pressure_double on every
+    # node, pressure_single on the single-layer components -- the holes under
+    # MIXED), mu = 1
+    nd = o1.nodes()
+    x, y, nx, ny, w = nd["x"], nd["y"], nd["nx"], nd["ny"], nd["w"]
+    n_wall = 20 * 16  # the wall's nodes come first; the holes carry the single layer
+    sl = np.arange(o1.n_nodes) >= n_wall
+    for r in range(3):
+        t0, t1 = tau[0::2, r], tau[1::2, r]
+        for k, (px, py) in enumerate(tg):
+            rx, ry = px - x, py - y
+            r2 = rx * rx + ry * ry
+            rn = rx * nx + ry * ny
+            pd0 = (1.0 / np.pi) * (-nx / r2 + rx * (2.0 * rn / (r2 * r2)))
+            pd1 = (1.0 / np.pi) * (-ny / r2 + ry * (2.0 * rn / (r2 * r2)))
+            terms = w * (pd0 * t0 + pd1 * t1) + np.where(sl, w * (rx * t0 + ry * t1) / (2.0 * np.pi * r2), 0.0)
+            assert abs(pre[k, r] - terms.sum()) <= 1e-12 * np.abs(terms).sum()
