@@ -323,53 +323,87 @@ __global__ void submatrix_kernel(EntryView v, const i64* __restrict__ rows, i64 
   }
 }
 
+// The four proxy functionals of one candidate node for both of its
+// components (q[a][.] for component a): the kernel matrices formed once.
+__device__ __forceinline__ void proxy_node(const EntryView& v, const ProxyJob& jb, i64 node, double d0, double d1,
+                                           double p0, double p1, double (&q)[2][4]) {
+  if (jb.kind != 1) {  // outgoing: fields at the candidate from circle sources
+    const double mu = jb.kind == 2 ? 1.0 : v.mu;
+    const M2d sl = stokeslet(v.x[node], v.y[node], p0, p1, mu);
+    const M2d dl = double_layer(v.x[node], v.y[node], p0, p1, d0, d1);
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      q[a][0] = sl.at(a, 0);
+      q[a][1] = sl.at(a, 1);
+      q[a][2] = dl.at(a, 0);
+      q[a][3] = dl.at(a, 1);
+    }
+  } else {  // incoming: candidate source evaluated on the circle
+    const double nj0 = v.nx[node], nj1 = v.ny[node], wj = v.w[node];
+    M2d val = double_layer(p0, p1, v.x[node], v.y[node], nj0, nj1);
+    M2d grad = double_layer_gradient(p0, p1, v.x[node], v.y[node], nj0, nj1, d0, d1);
+    if (single_layer(v, v.comp[node])) {
+      const M2d s1 = stokeslet(p0, p1, v.x[node], v.y[node], v.mu);
+      const M2d g1 = stokeslet_gradient(p0, p1, v.x[node], v.y[node], v.mu, d0, d1);
+      val = {val.a00 + s1.a00, val.a01 + s1.a01, val.a10 + s1.a10, val.a11 + s1.a11};
+      grad = {grad.a00 + g1.a00, grad.a01 + g1.a01, grad.a10 + g1.a10, grad.a11 + g1.a11};
+    }
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      q[a][0] = wj * val.at(0, a);
+      q[a][1] = wj * val.at(1, a);
+      q[a][2] = wj * grad.at(0, a);
+      q[a][3] = wj * grad.at(1, a);
+    }
+  }
+}
+
+__device__ __forceinline__ void proxy_store(const EntryView& v, const ProxyJob& jb, double* col, int s, i64 node,
+                                            int a, const double (&q)[4]) {
+  double* dst = col + 4 * s;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    reinterpret_cast<double2*>(dst)[0] = make_double2(q[0], q[1]);
+    reinterpret_cast<double2*>(dst)[1] = make_double2(q[2], q[3]);
+  } else {
+    dst[0] = q[0];
+    dst[1] = q[1];
+    dst[2] = q[2];
+    dst[3] = q[3];
+  }
+  if (s == 0 && jb.with_null) {
+    const bool nul = in_null(v, v.comp[node]);
+    const double nn = a == 0 ? v.nx[node] : v.ny[node];
+    col[4 * jb.ns] = nul ? (jb.kind == 1 ? v.w[node] * nn : nn) : 0.0;
+  }
+}
+
+// One thread per (proxy point, candidate pair): when the two candidates are
+// the components of one node, its kernel matrices serve both columns.
 __global__ void proxy_jobs_kernel(EntryView v, const ProxyJob* __restrict__ jobs,
                                   const i64* __restrict__ cand, double* __restrict__ out) {
   const ProxyJob jb = jobs[blockIdx.y];
-  const i64 total = i64(jb.ns) * jb.n;
+  const int np = (jb.n + 1) / 2;
+  const i64 total = i64(jb.ns) * np;
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
-    const int s = int(idx % jb.ns), c = int(idx / jb.ns);
-    const i64 cs = cand[jb.cand_off + c];
-    const i64 node = node_of(v, cs >> 1);
-    const int a = int(cs & 1);
+    const int s = int(idx % jb.ns), c = 2 * int(idx / jb.ns);
     const double t = 2.0 * kPi * double(s) / double(jb.ns);
     double d0, d1;
     sincos(t, &d1, &d0);  // bitwise equal to sin(t), cos(t) (scripts/sincos_check.cu), one reduction
     const double p0 = jb.cx + jb.rad * d0, p1 = jb.cy + jb.rad * d1;
-    double* col = out + jb.out_off + i64(c) * jb.ld;
-    double q0, q1, q2, q3;
-    if (jb.kind != 1) {  // outgoing: fields at the candidate from circle sources
-      const double mu = jb.kind == 2 ? 1.0 : v.mu;
-      const M2d sl = stokeslet(v.x[node], v.y[node], p0, p1, mu);
-      const M2d dl = double_layer(v.x[node], v.y[node], p0, p1, d0, d1);
-      q0 = sl.at(a, 0);
-      q1 = sl.at(a, 1);
-      q2 = dl.at(a, 0);
-      q3 = dl.at(a, 1);
-    } else {  // incoming: candidate source evaluated on the circle
-      const double nj0 = v.nx[node], nj1 = v.ny[node], wj = v.w[node];
-      M2d val = double_layer(p0, p1, v.x[node], v.y[node], nj0, nj1);
-      M2d grad = double_layer_gradient(p0, p1, v.x[node], v.y[node], nj0, nj1, d0, d1);
-      if (single_layer(v, v.comp[node])) {
-        const M2d s1 = stokeslet(p0, p1, v.x[node], v.y[node], v.mu);
-        const M2d g1 = stokeslet_gradient(p0, p1, v.x[node], v.y[node], v.mu, d0, d1);
-        val = {val.a00 + s1.a00, val.a01 + s1.a01, val.a10 + s1.a10, val.a11 + s1.a11};
-        grad = {grad.a00 + g1.a00, grad.a01 + g1.a01, grad.a10 + g1.a10, grad.a11 + g1.a11};
-      }
-      q0 = wj * val.at(0, a);
-      q1 = wj * val.at(1, a);
-      q2 = wj * grad.at(0, a);
-      q3 = wj * grad.at(1, a);
-    }
-    col[4 * s + 0] = q0;
-    col[4 * s + 1] = q1;
-    col[4 * s + 2] = q2;
-    col[4 * s + 3] = q3;
-    if (s == 0 && jb.with_null) {
-      const bool nul = in_null(v, v.comp[node]);
-      const double nn = a == 0 ? v.nx[node] : v.ny[node];
-      col[4 * jb.ns] = nul ? (jb.kind == 1 ? v.w[node] * nn : nn) : 0.0;
+    const i64 cs0 = cand[jb.cand_off + c];
+    const bool two = c + 1 < jb.n;
+    const i64 cs1 = two ? cand[jb.cand_off + c + 1] : -1;
+    const i64 node0 = node_of(v, cs0 >> 1);
+    double q[2][4];
+    proxy_node(v, jb, node0, d0, d1, p0, p1, q);
+    const int a0 = int(cs0 & 1);
+    proxy_store(v, jb, out + jb.out_off + i64(c) * jb.ld, s, node0, a0, q[a0]);
+    if (two) {
+      const i64 node1 = node_of(v, cs1 >> 1);
+      const int a1 = int(cs1 & 1);
+      if (node1 != node0) proxy_node(v, jb, node1, d0, d1, p0, p1, q);
+      proxy_store(v, jb, out + jb.out_off + i64(c + 1) * jb.ld, s, node1, a1, q[a1]);
     }
   }
 }
