@@ -3654,10 +3654,13 @@ void qr_batched(const std::vector<QrJob>& jobs, cudaStream_t s) {
   std::vector<std::unique_ptr<SideStream>> sides;
   int used = 0;
   static const bool no_fork = std::getenv("SBX_QR_NOFORK") != nullptr;  // diagnostics
+  // side streams fork from s before the first launch (no launch waits for another)
+  const int nlaunch = int(!quad.empty()) + int(!wide.empty()) + int(!plain.empty());
+  if (!no_fork)
+    for (int q = 1; q < nlaunch; ++q) sides.emplace_back(new SideStream(s0));
   auto next_stream = [&]() -> cudaStream_t {
-    if (used++ == 0 || no_fork) return s0;
-    sides.emplace_back(new SideStream(s0));
-    return sides.back()->get();
+    const int u = used++;
+    return (u == 0 || no_fork) ? s0 : sides[size_t(u - 1)]->get();
   };
   struct Join {
     std::vector<std::unique_ptr<SideStream>>& v;
@@ -4168,6 +4171,13 @@ void cpqr_reg_batched(const std::vector<QrJob>& all, cudaStream_t s) {
   // the first on streams forked from s
   static const bool no_fork = std::getenv("SBX_REG_NOFORK") != nullptr;  // diagnostics
   std::vector<std::unique_ptr<SideStream>> sides;
+  {  // side streams fork from s before the first launch
+    int nl = 0;
+    for (size_t q = 0; q < order.size(); ++q) nl += (q == 0 || order[q].first != order[q - 1].first) ? 1 : 0;
+    if (!no_fork)
+      for (int q = 1; q < nl; ++q) sides.emplace_back(new SideStream(s));
+  }
+  size_t used = 0;
   for (size_t g0 = 0; g0 < jobs.size();) {
     const int key = order[g0].first;
     size_t g1 = g0;
@@ -4177,11 +4187,7 @@ void cpqr_reg_batched(const std::vector<QrJob>& all, cudaStream_t s) {
       ++g1;
     }
     const int c = key / 64, G = key % 64, np = int(g1 - g0);
-    cudaStream_t st = s;
-    if (g0 > 0 && !no_fork) {
-      sides.emplace_back(new SideStream(s));
-      st = sides.back()->get();
-    }
+    cudaStream_t st = (g0 > 0 && !no_fork) ? sides[used++]->get() : s;
     switch (c) {
       case 0: launch_reg<9, 4>(dj + g0, np, G, size_max, st); break;
       case 1: launch_reg<17, 2>(dj + g0, np, G, size_max, st); break;

@@ -188,19 +188,25 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
                           {&big, cpqr_coop_batched},    {&chip, cpqr_smem_batched},    {&clus, cpqr_cluster_batched},
                           {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},    {&push, cpqr_push_batched},
                           {&bq, bqr_batched}};
+  // (every side stream forks from s BEFORE anything of this round is
+  // launched on s, so no group waits for another)
   std::vector<std::unique_ptr<SideStream>> sides;
+  std::vector<std::pair<const Group*, cudaStream_t>> plan;
   bool first = true;
   for (const auto& g : groups) {
     if (g.v->empty()) continue;
     const bool forkable = fork_env == 1 || (fork_env == 2 && (g.v == &rrow || g.v == &reg));
     if (first || !forkable) {
-      g.fn(*g.v, s);
+      plan.push_back({&g, s});
       first = false;
       continue;
     }
     sides.emplace_back(new SideStream(s));
-    StreamScope ss(sides.back()->get());
-    g.fn(*g.v, sides.back()->get());
+    plan.push_back({&g, sides.back()->get()});
+  }
+  for (const auto& pl : plan) {
+    StreamScope ss(pl.second);
+    pl.first->fn(*pl.first->v, pl.second);
   }
   for (auto& sd : sides) sd->join(s);
   if (log) {  // diagnostics: the batch's device time (serialises the stream)
