@@ -188,6 +188,18 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
     keep.push_back(std::move(pb));
   }
   std::vector<RowIdResult> outs(H);
+  // the roots' interpolation matrices scattered into the m-row outputs: all
+  // hierarchies in one launch (one upload of the concatenated row maps)
+  std::vector<i64> maps;
+  std::vector<std::pair<size_t, i64>> map_off(H, {0, -1});
+  for (size_t h = 0; h < H; ++h) {
+    if (level[h].empty() || level[h].front().k <= 0) continue;
+    map_off[h] = {maps.size(), 0};
+    maps.insert(maps.end(), level[h].front().rows.begin(), level[h].front().rows.end());
+  }
+  DevBuf<i64> d_maps;
+  if (!maps.empty()) d_maps.upload(maps, s);
+  std::vector<ScatterJob> root_jobs;
   for (size_t h = 0; h < H; ++h) {
     RowIdResult& out = outs[h];
     const i64 m = specs[h].m;
@@ -202,11 +214,8 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
     out.P.resize(size_t(std::max<i64>(m * out.k, 1)));
     if (out.k > 0) {
       SBX_CUDA(cudaMemsetAsync(out.P.get(), 0, size_t(m * out.k) * 8, s));
-      DevBuf<i64> map;
-      map.upload(root.rows, s);
-      scatter_batched({{root.P, out.P.get(), map.get(), int(root.rows.size()), int(out.k),
-                        std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0}},
-                      s);
+      root_jobs.push_back({root.P, out.P.get(), d_maps.get() + map_off[h].first, int(root.rows.size()), int(out.k),
+                           std::max<int>(1, int(root.rows.size())), int(m), 0, 0, 1.0});
     }
     out.J = root.skel;
     std::vector<char> in(size_t(m), 0);
@@ -214,6 +223,7 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
     for (i64 x : root.rows)
       if (!in[size_t(x)]) out.J.push_back(x);
   }
+  scatter_batched(root_jobs, s);
   return outs;
 }
 
