@@ -60,13 +60,17 @@ def dist_env():
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region (NVML every
-    10 ms; nvidia-smi as the fallback)."""
+    20 ms; nvidia-smi as the fallback)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
         self.device = device
+        # one NVML query pair costs ~1 ms of driver time that the per-step
+        # host syncs can wait behind: sample every 20 ms (the recipe's
+        # nvidia-smi loop uses 200 ms)
+        self.period = float(os.environ.get("SBX_CLOCK_MS", "20")) / 1e3
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -82,11 +86,11 @@ class ClockSampler:
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append([str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(mx)]
                                     + ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.01)
+                self._stop.wait(self.period)
             return
         except Exception:
             self.samples.clear()
-        while not self._stop.is_set():
+        while not self._stop.is_set():  # nvidia-smi fallback
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
