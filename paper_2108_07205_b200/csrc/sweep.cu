@@ -592,15 +592,18 @@ std::vector<FlowItem> make_items(SweepPlan& plan, int tile0, int ncol, int tile_
     const int lsplit = L.ksplit > 0 ? int((L.max_k + kcap - 1) / kcap)
                        : lsplit_ok && target > 0 && base > 0 ? int(std::min<i64>(8, (target + base - 1) / base))
                                                                : 1;
-    for (int ct = 0; ct < ncol; ++ct)
-      for (size_t t = 0; t < L.tasks.size(); ++t) {
+    // (column tiles innermost: the items reading the same factor rows run
+    // side by side, so the second column tile finds them in L2)
+    for (size_t t = 0; t < L.tasks.size(); ++t)
+      for (int r0 = 0; r0 < L.tasks[t].m; r0 += tile)
+        for (int ct = 0; ct < ncol; ++ct) {
         const auto& tk = L.tasks[t];
         const int ns = L.ksplit > 0 ? lsplit : std::max(1, std::min(lsplit, tk.K / 32));
         // split boundaries on multiples of 16 (the DMMA K chunk)
         const int per = ((tk.K + ns - 1) / ns + 15) / 16 * 16;
         const int nsplit = std::max(1, (tk.K + per - 1) / std::max(per, 1));
         (*needs)[size_t(L.first_task + i64(t))] = (tk.m + tile - 1) / tile;
-        for (int r0 = 0; r0 < tk.m; r0 += tile) {
+        {
           for (int ks = 0; ks < nsplit; ++ks) {
             FlowItem f{};
             f.task = int(L.first_task + i64(t));
