@@ -184,10 +184,12 @@ void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_
     std::vector<QrJob>* v;
     void (*fn)(const std::vector<QrJob>&, cudaStream_t);
   };
-  const Group groups[] = {{&jobs, qr_batched},          {&rrow, cpqr_regrows_batched}, {&reg, cpqr_reg_batched},
-                          {&big, cpqr_coop_batched},    {&chip, cpqr_smem_batched},    {&clus, cpqr_cluster_batched},
-                          {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},    {&push, cpqr_push_batched},
-                          {&bq, bqr_batched}};
+  // (launch order = the block scheduler's order: the longest-running
+  // throughput engines first, so the shorter ones fill their tail waves)
+  const Group groups[] = {{&bq, bqr_batched},           {&jobs, qr_batched},          {&rrow, cpqr_regrows_batched},
+                          {&reg, cpqr_reg_batched},     {&big, cpqr_coop_batched},    {&chip, cpqr_smem_batched},
+                          {&clus, cpqr_cluster_batched}, {&strm, cpqr_stream_batched}, {&rows, cpqr_rows_batched},
+                          {&push, cpqr_push_batched}};
   // (every side stream forks from s BEFORE anything of this round is
   // launched on s, so no group waits for another)
   std::vector<std::unique_ptr<SideStream>> sides;
