@@ -114,6 +114,22 @@ class SideStream {
   bool high_ = false;
 };
 
+// A pinned host buffer of at least `bytes` from a process-wide pool (returned
+// on destruction): small device-to-host reads the host waits for anyway go
+// through it as one async copy + sync instead of a pageable staged copy.
+class PinnedLease {
+ public:
+  explicit PinnedLease(size_t bytes);
+  ~PinnedLease();
+  PinnedLease(const PinnedLease&) = delete;
+  PinnedLease& operator=(const PinnedLease&) = delete;
+  void* get() const { return p_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
 // Thread-local switch: while set, the ID engines avoid cooperative launches
 // (grid-wide co-residency), which other streams' kernels can starve.
 bool& no_coop_flag();

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <condition_variable>
 #include <memory>
@@ -326,14 +327,21 @@ void IdBatch::factor(const std::vector<IdProblem>& probs, double stop_eps, cudaS
     launch_id_jobs(jobs, force_engine, s);
   std::vector<int> hperm(static_cast<size_t>(perm_off_[np]));
   std::vector<double> hdiag(static_cast<size_t>(diag_off[np]));
-  if (!hperm.empty()) d_perm_.download(hperm.data(), hperm.size(), s);
-  if (!hdiag.empty()) d_diag_.download(hdiag.data(), hdiag.size(), s);
   std::vector<int> hsteps;
-  if (ktimer_on() && np) {
-    hsteps.resize(np);
-    d_steps_.download(hsteps.data(), np, s);
+  if (ktimer_on() && np) hsteps.resize(np);
+  {  // pivots, |r_jj| (and steps) through one pinned buffer: async copies, one sync
+    const size_t b_diag = hdiag.size() * sizeof(double), b_perm = hperm.size() * sizeof(int),
+                 b_steps = hsteps.size() * sizeof(int);
+    PinnedLease pin(b_diag + b_perm + b_steps);
+    char* h = static_cast<char*>(pin.get());
+    if (b_diag) SBX_CUDA(cudaMemcpyAsync(h, d_diag_.get(), b_diag, cudaMemcpyDeviceToHost, s));
+    if (b_perm) SBX_CUDA(cudaMemcpyAsync(h + b_diag, d_perm_.get(), b_perm, cudaMemcpyDeviceToHost, s));
+    if (b_steps) SBX_CUDA(cudaMemcpyAsync(h + b_diag + b_perm, d_steps_.get(), b_steps, cudaMemcpyDeviceToHost, s));
+    SBX_CUDA(cudaStreamSynchronize(s));
+    if (b_diag) std::memcpy(hdiag.data(), h, b_diag);
+    if (b_perm) std::memcpy(hperm.data(), h + b_diag, b_perm);
+    if (b_steps) std::memcpy(hsteps.data(), h + b_diag + b_perm, b_steps);
   }
-  SBX_CUDA(cudaStreamSynchronize(s));
   if (!hsteps.empty()) {
     // algorithmic work of the pivoted Householder steps actually taken:
     // step j updates the (M-j) x (n-j) trailing block, 4 flops per entry

@@ -1,5 +1,6 @@
 // Library runtime: device selection, the library stream, launch counting,
 // the caching device allocator and the optional phase timer.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -247,6 +248,43 @@ SideStream::~SideStream() {
   auto& pool = side_pool();
   std::lock_guard<std::mutex> lk(pool.mu);
   pool.free[high_ ? 1 : 0].push_back({s_, fork_, join_});
+}
+
+namespace {
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool;  // never destroyed
+  return *p;
+}
+}  // namespace
+
+PinnedLease::PinnedLease(size_t bytes) {
+  bytes = std::max<size_t>(bytes, 4096);
+  auto& pool = pinned_pool();
+  {
+    std::lock_guard<std::mutex> lk(pool.mu);
+    for (size_t i = 0; i < pool.free.size(); ++i)
+      if (pool.free[i].second >= bytes) {
+        p_ = pool.free[i].first;
+        bytes_ = pool.free[i].second;
+        pool.free.erase(pool.free.begin() + long(i));
+        return;
+      }
+  }
+  size_t sz = 4096;
+  while (sz < bytes) sz <<= 1;
+  SBX_CUDA(cudaMallocHost(&p_, sz));
+  bytes_ = sz;
+}
+
+PinnedLease::~PinnedLease() {
+  if (!p_) return;
+  auto& pool = pinned_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  pool.free.push_back({p_, bytes_});
 }
 
 void parallel_tasks(const std::vector<std::function<void(cudaStream_t)>>& tasks, cudaStream_t main,
