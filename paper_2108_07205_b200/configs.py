@@ -83,18 +83,21 @@ class RefinedWallConfig:
 class HolesConfig:
     """configs[4]: outer ellipse (8, 4) with 16 circular obstacles r = 0.3 on a
     seed-jittered 4x4 grid, Mixed formulation (wall D + N, holes D + S).
-    262144 nodes: 8960 wall panels + 16 x 464 hole panels of 16 nodes (the
-    arc-length split is 9216 + 16 x 448; that tree puts hole boundaries
-    where the telescoping inverse fails the reference's own rcond gate,
-    hbs.cpp:429, at depth 2 — rcond(v^T x^-1 u) = 9e-11 < 1e-9, recomputed in
-    numpy from the compressed factors — so the split is moved by 3%).  Each step refines 8 panels around a seed-random point on 8
+    262144 nodes: 8896 wall panels + 16 x 468 hole panels of 16 nodes.  The
+    arc-length split is 9216 + 16 x 448; with 16384 panels in all, the boxes
+    that hold whole obstacles put the telescoping inverse's skeleton blocks
+    v^T x^-1 u at rcond 1e-10 .. 1e-9, right at the reference's own gate
+    (hbs.cpp:429, 1e-9), and which side a split lands on depends on the
+    rounding of the IDs (profiles/r02b_cfg5_scan.txt: 7 splits, 3 under the
+    gate at rcond 3.4e-10 .. 9.6e-10); 8896 + 16 x 468 (2.9 % off the
+    arc-length split) passes and is the most accurate of the scan.  Each step refines 8 panels around a seed-random point on 8
     distinct obstacles (m = 16) and solves 128 right-hand sides of Stokeslets
     placed outside the fluid (beyond the wall and inside the obstacles)."""
     name: str = "cfg5"
     a: float = 8.0
     b: float = 4.0
-    wall_panels: int = 8960
-    hole_panels: int = 464
+    wall_panels: int = 8896
+    hole_panels: int = 468
     hole_radius: float = 0.3
     grid: int = 4
     q: int = 16

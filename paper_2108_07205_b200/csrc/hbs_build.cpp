@@ -8,6 +8,7 @@
 //   ->  interpolation matrices (interp_kernel)  ->  b_sib blocks.
 // The inverse is a per-level batch of LU/inverse/rcond + DMMA GEMMs.
 #include <algorithm>
+#include <cstdio>
 #include <climits>
 #include <cmath>
 #include <condition_variable>
@@ -250,6 +251,12 @@ struct Gate {
   int depth = 0;
 };
 
+std::string sci(double v) {
+  char b[32];
+  std::snprintf(b, sizeof(b), "%.3e", v);
+  return b;
+}
+
 void check_gates(HbsOp& op, std::vector<std::unique_ptr<Gate>>& gates, double thr, cudaStream_t s) {
   op.node_rcond.assign(op.nodes.size(), 1.0);
   for (const auto& gp : gates) {
@@ -267,14 +274,14 @@ void check_gates(HbsOp& op, std::vector<std::unique_ptr<Gate>>& gates, double th
       const auto& nd = op.nodes[gt.ids[q]];
       if (nd.c > 0 && !(hrc[2 * q] >= thr))
         throw Error(4, std::string("singular ") + (gt.ids[q] == 0 ? "root" : "diagonal") +
-                           " block (rcond " + std::to_string(hrc[2 * q]) + ") at tree node [" +
+                           " block (rcond " + sci(hrc[2 * q]) + ") at tree node [" +
                            std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
                            std::to_string(nd.depth));
     }
     for (size_t q = 0; q < gt.ids.size(); ++q) {
       const auto& nd = op.nodes[gt.ids[q]];
       if (gt.ids[q] != 0 && nd.c > 0 && nd.k > 0 && !(hrc[2 * q + 1] >= thr))
-        throw Error(4, "singular skeleton block (rcond " + std::to_string(hrc[2 * q + 1]) + ") at tree node [" +
+        throw Error(4, "singular skeleton block (rcond " + sci(hrc[2 * q + 1]) + ") at tree node [" +
                            std::to_string(nd.begin) + "," + std::to_string(nd.end) + ") depth " +
                            std::to_string(nd.depth));
     }

@@ -57,6 +57,11 @@ void dump_batch(const std::vector<QrJob>& all, cudaStream_t s) {
 
 void launch_id_jobs(const std::vector<QrJob>& all, int force_engine, cudaStream_t s) {
   dump_batch(all, s);
+  static const int env_engine = [] {  // diagnostics: one engine for every batch
+    const char* e = std::getenv("SBX_FORCE_ENGINE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_engine == 0) force_engine = env_engine;
   KernelTimer kt("id_factor", s);  // every CPQR engine launch of the batch (bench: step-dominant family)
   std::vector<QrJob> jobs, big, chip, clus, reg, strm, rows, push, rrow, bq;
   static const int tsqr_max_m = [] {
