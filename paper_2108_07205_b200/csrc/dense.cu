@@ -1102,6 +1102,94 @@ size_t bqr_smem(int M, int n) {
   return std::max(p1, p2) * sizeof(double);
 }
 
+// One column step of the panel QR (rows split over the warps): partial
+// sums x^T a_k of the live panel columns k >= K0, reduce-scatter per warp,
+// warp 0 forms the Householder scalars and R row j, every warp updates its
+// rows.  Two CTA barriers.
+template <int K0>
+__device__ __forceinline__ void bqr_panel_column(double* P, int ldp, int j, int w, int ml, int rb0, int rb1, int lane,
+                                                 int warp, double* part, double* scv, double* tau) {
+  constexpr int NV = kBW - K0;  // values per lane (16 or 8)
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int t = 0; t < kBRpl; ++t) {
+    const int i = rb0 + lane + 32 * t;
+    if (i < rb1 && i > j && i < ml) {
+      const double x = P[i + size_t(ldp) * j];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] = fma(x, P[i + size_t(ldp) * (K0 + k)], acc[k]);
+    }
+  }
+  // reduce-scatter: after the halving steps lane l holds value (l >> 1) mod NV
+  // summed over the lanes that differ in bits 1 .. log2(NV); the remaining
+  // lane bits are summed by plain butterflies
+#pragma unroll
+  for (int h = NV / 2; h >= 1; h >>= 1) {
+    const bool up = (lane & (2 * h)) != 0;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? acc[k] : acc[k + h];
+      const double keep = up ? acc[k + h] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
+    }
+  }
+#pragma unroll
+  for (int o = 2 * NV; o < 32; o <<= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+  acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+  if ((lane & ~(2 * NV - 2)) == 0) part[warp * kBW + K0 + (lane >> 1)] = acc[0];
+  __syncthreads();
+  if (warp == 0) {  // (the whole warp: the shuffle below)
+    double tot = 0.0;
+    if (lane >= K0 && lane < kBW) {
+      double v[kBWarps];
+#pragma unroll
+      for (int q = 0; q < kBWarps; ++q) v[q] = part[q * kBW + lane];
+#pragma unroll
+      for (int q = 1; q < kBWarps; q <<= 1)  // fixed tree over the warps
+#pragma unroll
+        for (int r = 0; r + q < kBWarps; r += 2 * q) v[r] += v[r + q];
+      tot = v[0];
+    }
+    const double s2 = __shfl_sync(0xffffffffu, tot, j);
+    const double alpha = P[j + size_t(ldp) * j];
+    double t = 0.0, beta = alpha, sc = 0.0;
+    if (s2 > DBL_MIN) {
+      beta = sqrt(fma(alpha, alpha, s2));
+      if (alpha >= 0.0) beta = -beta;
+      sc = 1.0 / (alpha - beta);
+      t = (beta - alpha) / beta;
+    }
+    if (lane > j && lane < w) {
+      const double tw = t * (P[j + size_t(ldp) * lane] + sc * tot);
+      scv[lane] = tw * sc;
+      P[j + size_t(ldp) * lane] -= tw;  // R(j, k)
+    }
+    if (lane == 0) {
+      scv[kBW] = sc;
+      tau[j] = t;
+      P[j + size_t(ldp) * j] = beta;
+    }
+  }
+  __syncthreads();
+  const double sc = scv[kBW];
+#pragma unroll
+  for (int t = 0; t < kBRpl; ++t) {
+    const int i = rb0 + lane + 32 * t;
+    if (i < rb1 && i > j && i < ml) {
+      double* xr = P + i;
+      const double x = xr[size_t(ldp) * j];
+#pragma unroll
+      for (int k = K0; k < kBW; ++k)
+        if (k > j && k < w) xr[size_t(ldp) * k] = fma(-x, scv[k], xr[size_t(ldp) * k]);
+      xr[size_t(ldp) * j] = x * sc;
+    }
+  }
+  // (each warp updates only its own rows, which its next partial sums read;
+  // the scalars' buffers are rewritten after the next barrier)
+}
+
 __global__ void __launch_bounds__(kBT, 1) bqr_kernel(const QrJob* __restrict__ jobs, int phases) {
   extern __shared__ double sm[];
   const QrJob jb = jobs[blockIdx.x];
@@ -1147,73 +1235,12 @@ __global__ void __launch_bounds__(kBT, 1) bqr_kernel(const QrJob* __restrict__ j
       double* part = W;   // kBWarps x 16 partial sums (W is free until step 4)
       double* scv = W2;   // tw_k / (alpha - beta) per column, scale, beta
       for (int j = 0; j < w; ++j) {
-        double acc[kBW];
-#pragma unroll
-        for (int k = 0; k < kBW; ++k) acc[k] = 0.0;
-#pragma unroll
-        for (int t = 0; t < kBRpl; ++t) {
-          const int i = rb0 + lane + 32 * t;
-          if (i < rb1 && i > j && i < ml) {
-            const double x = P[i + size_t(ldp) * j];
-#pragma unroll
-            for (int k = 0; k < kBW; ++k) acc[k] = fma(x, P[i + size_t(ldp) * k], acc[k]);
-          }
-        }
-        // reduce-scatter over the warp (16 + 8 + 4 + 2 + 1 shuffles): lane l
-        // ends with the warp sum of value l >> 1
-#pragma unroll
-        for (int h = kBW / 2; h >= 1; h >>= 1) {
-          const bool up = (lane & (2 * h)) != 0;  // keep the upper h values
-#pragma unroll
-          for (int k = 0; k < h; ++k) {
-            const double send = up ? acc[k] : acc[k + h];
-            const double keep = up ? acc[k + h] : acc[k];
-            acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2 * h);
-          }
-        }
-        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-        if ((lane & 1) == 0) part[warp * kBW + (lane >> 1)] = acc[0];
-        __syncthreads();
-        if (warp == 0) {  // (the whole warp: the shuffle below)
-          double tot = 0.0;
-          if (lane < kBW)
-            for (int v = 0; v < kBWarps; ++v) tot += part[v * kBW + lane];  // warp order
-          const double s2 = __shfl_sync(0xffffffffu, tot, j);
-          const double alpha = P[j + size_t(ldp) * j];
-          double t = 0.0, beta = alpha, sc = 0.0;
-          if (s2 > DBL_MIN) {
-            beta = sqrt(fma(alpha, alpha, s2));
-            if (alpha >= 0.0) beta = -beta;
-            sc = 1.0 / (alpha - beta);
-            t = (beta - alpha) / beta;
-          }
-          if (lane > j && lane < w) {
-            const double tw = t * (P[j + size_t(ldp) * lane] + sc * tot);
-            scv[lane] = tw * sc;
-            P[j + size_t(ldp) * lane] -= tw;  // R(j, k)
-          }
-          if (lane == 0) {
-            scv[kBW] = sc;
-            tau[j] = t;
-            P[j + size_t(ldp) * j] = beta;
-          }
-        }
-        __syncthreads();
-        const double sc = scv[kBW];
-#pragma unroll
-        for (int t = 0; t < kBRpl; ++t) {
-          const int i = rb0 + lane + 32 * t;
-          if (i < rb1 && i > j && i < ml) {
-            double* xr = P + i;
-            const double x = xr[size_t(ldp) * j];
-#pragma unroll
-            for (int k = 0; k < kBW; ++k)
-              if (k > j && k < w) xr[size_t(ldp) * k] = fma(-x, scv[k], xr[size_t(ldp) * k]);
-            xr[size_t(ldp) * j] = x * sc;
-          }
-        }
-        // (each warp updates only its own rows, which its next partial sums
-        // read; the scalars' buffers are rewritten after the next barrier)
+        // columns below K0 are all pivoted once j >= 8: the second half of
+        // the panel runs with the 8 live columns only
+        if (j < kBW / 2)
+          bqr_panel_column<0>(P, ldp, j, w, ml, rb0, rb1, lane, warp, part, scv, tau);
+        else
+          bqr_panel_column<kBW / 2>(P, ldp, j, w, ml, rb0, rb1, lane, warp, part, scv, tau);
       }
     }
     __syncthreads();
