@@ -376,6 +376,12 @@ int sbx_kernel_flops(const char* name, int reset, double* flops);
 int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced, int engine,
                int64_t* k, int64_t* J, double* P);
 
+/* Explicit inverse and Eigen-style reciprocal condition estimate of a dense
+ * host matrix a (n x n, column-major, n <= 2048) through the device path the
+ * Woodbury operator W and the dense A_pp use — els.cpp:111-127
+ * (PartialPivLU + rcond()).  inv: n*n doubles. */
+int sbx_dense_inverse(const double* a, int64_t n, double* inv, double* rcond);
+
 #ifdef __cplusplus
 }
 #endif

@@ -736,6 +736,19 @@ def row_id(w, eps=1e-10, forced=None, engine=0):
     return kk, J, P[: m * kk].reshape((m, kk), order="F")
 
 
+def dense_inverse(a):
+    """Explicit inverse and reciprocal condition estimate of a dense matrix on
+    the device (els.cpp:111-127: PartialPivLU + rcond()).  Returns inv, rcond."""
+    _ensure()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    n = a.shape[0]
+    assert a.shape == (n, n)
+    inv = np.zeros((n, n), order="F")
+    rc = C.c_double(0.0)
+    check(lib().sbx_dense_inverse(a.ctypes.data_as(F64P), n, inv.ctypes.data_as(F64P), C.byref(rc)))
+    return inv, rc.value
+
+
 def kernel_launches(reset: bool = False) -> int:
     return int(lib().sbx_kernel_launches(int(reset)))
 

@@ -193,6 +193,19 @@ int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced
   });
 }
 
+int sbx_dense_inverse(const double* a, int64_t n, double* inv, double* rcond) {
+  return guard([&] {
+    sbx::require(n >= 1, "dense_inverse: empty matrix");
+    cudaStream_t s = sbx::lib_stream();
+    sbx::DevBuf<double> d(size_t(n * n)), di(size_t(n * n));
+    SBX_CUDA(cudaMemcpyAsync(d.get(), a, size_t(n * n) * 8, cudaMemcpyHostToDevice, s));
+    const double rc = sbx::dense_inverse(d.get(), n, di.get(), s);
+    di.download(inv, size_t(n * n), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+    if (rcond) *rcond = rc;
+  });
+}
+
 void* sbx_stream(void) {
   try {
     return static_cast<void*>(sbx::lib_stream());

@@ -2937,7 +2937,10 @@ __device__ void warp_lu_solve_t(const double* lu, int n, int lda, double (&x)[kM
 
 // Reciprocal 1-norm condition estimate (Eigen ConditionEstimator.h,
 // Hager/Higham) of a matrix with 1-norm l1 from its explicit inverse X
-// (n x n, ld n), CTA-wide.  work: 4n doubles; red/ired: block scratch.
+// (n x n, ld n), CTA-wide (NT threads; with NT < kT the caller presets
+// red[NT/32..] = 0 and ired likewise beyond the live warps' slots: the block
+// reductions read kWarps slots).  work: 4n doubles; red/ired: block scratch.
+template <int NT = kT>
 __device__ double rcond_from_inverse(const double* X, int n, double l1, double* work, double* red, int* ired) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   {
@@ -2948,13 +2951,13 @@ __device__ double rcond_from_inverse(const double* X, int n, double l1, double* 
     double* tmp = work + 3 * n;  // n
     auto gemv = [&](const double* x, double* y, bool trans) {  // y = X x or X^T x
       if (!trans) {
-        for (int i = tid; i < n; i += kT) {
+        for (int i = tid; i < n; i += NT) {
           double a = 0.0;
           for (int c = 0; c < n; ++c) a += X[i + size_t(c) * n] * x[c];
           y[i] = a;
         }
       } else {
-        for (int c = warp; c < n; c += kWarps) {
+        for (int c = warp; c < n; c += NT / 32) {
           double a = 0.0;
           for (int i = lane; i < n; i += 32) a += X[i + size_t(c) * n] * x[i];
           a = warp_sum(a);
@@ -2965,7 +2968,7 @@ __device__ double rcond_from_inverse(const double* X, int n, double l1, double* 
     };
     auto l1sum = [&](const double* x) {
       double a = 0.0;
-      for (int i = tid; i < n; i += kT) a += fabs(x[i]);
+      for (int i = tid; i < n; i += NT) a += fabs(x[i]);
       return block_sum(a, red);
     };
     double result;
@@ -2974,14 +2977,14 @@ __device__ double rcond_from_inverse(const double* X, int n, double l1, double* 
     } else if (n == 1) {
       result = 1.0;
     } else {
-      for (int i = tid; i < n; i += kT) tmp[i] = 1.0 / double(n);
+      for (int i = tid; i < n; i += NT) tmp[i] = 1.0 / double(n);
       __syncthreads();
       gemv(tmp, v, false);
       double lower = l1sum(v), old_lower = lower;
       int old_vmax = -1;
       for (int it = 0; it < 4; ++it) {
         int differs = 0;
-        for (int i = tid; i < n; i += kT) {
+        for (int i = tid; i < n; i += NT) {
           sg[i] = v[i] < 0.0 ? -1.0 : 1.0;
           if (it > 0 && sg[i] != osg[i]) differs = 1;
         }
@@ -2993,7 +2996,7 @@ __device__ double rcond_from_inverse(const double* X, int n, double l1, double* 
         gemv(sg, tmp, true);
         double bv = -1.0;
         int bi = 0x7fffffff;
-        for (int i = tid; i < n; i += kT)
+        for (int i = tid; i < n; i += NT)
           if (fabs(tmp[i]) > bv) {
             bv = fabs(tmp[i]);
             bi = i;
@@ -3002,16 +3005,16 @@ __device__ double rcond_from_inverse(const double* X, int n, double l1, double* 
         int vmax;
         block_argmax(bv, bi, red, ired, mv, vmax);
         if (vmax == old_vmax) break;
-        for (int i = tid; i < n; i += kT) v[i] = X[i + size_t(vmax) * n];
+        for (int i = tid; i < n; i += NT) v[i] = X[i + size_t(vmax) * n];
         __syncthreads();
         lower = l1sum(v);
         if (lower <= old_lower) break;
-        for (int i = tid; i < n; i += kT) osg[i] = sg[i];
+        for (int i = tid; i < n; i += NT) osg[i] = sg[i];
         __syncthreads();
         old_vmax = vmax;
         old_lower = lower;
       }
-      for (int i = tid; i < n; i += kT)
+      for (int i = tid; i < n; i += NT)
         tmp[i] = (i % 2 == 0 ? 1.0 : -1.0) * (1.0 + double(i) / double(n - 1));
       __syncthreads();
       gemv(tmp, v, false);
@@ -3398,6 +3401,323 @@ __global__ void __launch_bounds__(kT) gj_inverse_smem_kernel(const LuJob* __rest
     const double r = s_sing ? 0.0 : rcond_from_inverse(jb.inv, n, s_l1, jb.work, red, ired);
     if (tid == 0) *jb.rcond = r;
   }
+}
+
+// ---------------------------------------------------------------- Gauss-Jordan inverse on DMMA accumulators
+// Explicit inverse (n <= 32 TA) by BLOCKED in-place Gauss-Jordan with the
+// matrix held in registers as m8n8k4 accumulator tiles: 4 x 4 warps, each
+// owning TA x TA tiles of 8 x 8 (the matrix is padded with the identity to
+// NP = 32 TA).  Steps go in blocks of 4 pivot columns:
+//   1. the block's 4 columns are copied out of the tiles (shared memory);
+//   2. ONE warp factors that n x 4 panel in its registers, four pivoted
+//      Gauss-Jordan steps with no CTA barrier (pivot = first largest
+//      |M[i, k]| over the unused rows, found by a warp reduction);
+//   3. the 4 pivot rows are copied out of the tiles and brought up to date
+//      by one thread per column (a 4-term recurrence in registers);
+//   4. everything else is updated by ONE DMMA per tile,  M <- M - U R  with
+//      U = the four pivot columns (zero at their own pivot rows) and R = the
+//      four scaled pivot rows; pivot rows and the block's columns are then
+//      rewritten from their step-by-step values.
+// Four CTA barriers per block of four steps.  Same pivot rule, no row
+// movement and the same unscrambling as gj_inverse_kernel; results agree
+// with it up to the summation order of the four products of a block.
+// els.cpp:124-127 (PartialPivLU of W and rcond()).
+constexpr int kGjNb = 4;
+template <int TA>
+constexpr int gj_dmma_ld() { return 32 * TA + 4; }
+template <int TA>
+size_t gj_dmma_smem(int n) {
+  const size_t head = (64 + 32 + 2 * 16 * TA) * sizeof(double);  // red, ired, pivrow/rowstep
+  const size_t panels = (5 * kGjNb * size_t(gj_dmma_ld<TA>()) + 32) * sizeof(double);
+  return head + std::max(panels, size_t(n) * n * sizeof(double));
+}
+
+#ifdef SBX_GJ_PROFILE  // diagnostics: cycles per phase (thread 0), printed at the end
+#define GJP_DECL long long gjp_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}, gjp_last = clock64()
+#define GJP(i)                          \
+  do {                                  \
+    const long long now_ = clock64();   \
+    gjp_t[i] += now_ - gjp_last;        \
+    gjp_last = now_;                    \
+  } while (0)
+#define GJP_PRINT                                                                                   \
+  if (tid == 0)                                                                                     \
+  printf("[gj n=%d] load %lld extract %lld panel %lld rows %lld fix %lld dmma %lld out %lld rcond %lld\n", n, \
+         gjp_t[0], gjp_t[1], gjp_t[2], gjp_t[3], gjp_t[4], gjp_t[5], gjp_t[6], gjp_t[7])
+#else
+#define GJP_DECL
+#define GJP(i)
+#define GJP_PRINT
+#endif
+
+constexpr int kGjT = 256;  // 8 warps: 4 row groups x 2 column groups, up to 255 registers per thread
+template <int TA>
+__global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* __restrict__ jobs) {
+  constexpr int NP = 32 * TA, LD = gj_dmma_ld<TA>(), NB = kGjNb, TB = 2 * TA;
+  static_assert(NB == 4, "one m8n8k4 per tile and block");
+  static_assert(NP <= kGjT, "one thread per column in the row phase");
+  extern __shared__ double sm[];
+  const LuJob jb = jobs[blockIdx.x];
+  const int n = jb.n;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp & 3, wc = warp >> 2;
+  double* red = sm;                                  // 64
+  int* ired = reinterpret_cast<int*>(red + 64);      // 64
+  int* pivrow = ired + 64;                           // NP
+  int* rowstep = pivrow + NP;                        // NP
+  double* body = sm + 64 + 32 + 2 * 16 * TA;
+  double* Cm = body;                // 2 x NB x LD: the block's columns (double buffered)
+  double* U = Cm + 2 * NB * LD;     // NB x LD: pivot columns (0 at the step's pivot row)
+  double* Rm = U + NB * LD;         // NB x LD: scaled pivot rows; before that the raw rows
+  double* Fm = Rm + NB * LD;        // NB x LD: pivot rows as they stand at the end of the block
+  double* rblk = Fm + NB * LD;      // NB x NB: the pivot rows inside the block's columns
+  double* rinvs = rblk + NB * NB;   // NB
+  double* X = body;                 // n x n: the inverse, for rcond (after the last block)
+  __shared__ int s_sing;
+  __shared__ double s_l1;
+  if (tid == 0) {
+    s_sing = 0;
+    s_l1 = 0.0;
+  }
+  if (tid < 64) {  // the block reductions of rcond read kWarps slots; the dead warps' stay neutral
+    red[tid] = 0.0;
+    ired[tid] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int c = warp; c < n; c += kGjT / 32) {
+    double cs = 0.0;
+    for (int i = lane; i < n; i += 32) cs += fabs(jb.a[i + size_t(c) * jb.lda]);
+    cs = warp_sum(cs);
+    if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_l1), __double_as_longlong(cs));
+  }
+  GJP_DECL;
+  double acc[TA][TB][2];
+#pragma unroll
+  for (int a = 0; a < TA; ++a)
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * (TA * wr + a) + gid, col = 8 * (TB * wc + b) + 2 * tig + e;
+        acc[a][b][e] = (row < n && col < n) ? jb.a[row + size_t(col) * jb.lda] : (row == col ? 1.0 : 0.0);
+      }
+  unsigned usedmask = 0;  // warp 0: bit q set when row lane + 32 q has been a pivot
+  GJP(0);
+  for (int k0 = 0, blk = 0; k0 < n; k0 += NB, ++blk) {
+    const int nb = min(NB, n - k0);
+    const int tc0 = k0 >> 3, half = (k0 >> 2) & 1;
+    const bool own_cols = wc == tc0 / TB && (tig >> 1) == half;
+    const int bsel = tc0 % TB, cloc = (2 * tig) & 3;
+    double* Cb = Cm + (blk & 1) * NB * LD;
+    if (own_cols) {
+#pragma unroll
+      for (int a = 0; a < TA; ++a)
+#pragma unroll
+        for (int b = 0; b < TB; ++b)
+          if (b == bsel) {
+            const int row = 8 * (TA * wr + a) + gid;
+            Cb[cloc * LD + row] = acc[a][b][0];
+            Cb[(cloc + 1) * LD + row] = acc[a][b][1];
+          }
+    }
+    __syncthreads();
+    GJP(1);
+    if (warp == 0) {  // the n x 4 panel, in place in shared memory: lane owns rows lane + 32 q
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        if (s < nb) {
+          double cs[TA];
+          double bv = -1.0;
+          int bi = 0x7fffffff;
+#pragma unroll
+          for (int q = 0; q < TA; ++q) cs[q] = Cb[s * LD + lane + 32 * q];
+#pragma unroll
+          for (int q = 0; q < TA; ++q) {
+            double v = fabs(cs[q]);
+            if (!(v == v)) v = DBL_MAX;  // a NaN column still yields a definite row
+            const int i = lane + 32 * q;
+            if (i < n && !((usedmask >> q) & 1u) && v > bv) {
+              bv = v;
+              bi = i;
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          const int p = bi;
+          double r[NB];  // the scaled pivot row inside the block's columns
+#pragma unroll
+          for (int c = 0; c < NB; ++c) r[c] = Cb[c * LD + p];
+          const double piv = r[s];
+          const double rinv = piv != 0.0 ? 1.0 / piv : 0.0;
+#pragma unroll
+          for (int c = 0; c < NB; ++c) r[c] = c == s ? rinv : r[c] * rinv;
+          __syncwarp();  // row p read by every lane before its owner rewrites it
+          double u[TA];
+#pragma unroll
+          for (int q = 0; q < TA; ++q) {
+            const int i = lane + 32 * q;
+            u[q] = i == p ? 0.0 : cs[q];
+            U[s * LD + i] = u[q];
+          }
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            double x[TA];
+#pragma unroll
+            for (int q = 0; q < TA; ++q) x[q] = c == s ? 0.0 : Cb[c * LD + lane + 32 * q];
+#pragma unroll
+            for (int q = 0; q < TA; ++q) {
+              const int i = lane + 32 * q;
+              Cb[c * LD + i] = i == p ? r[c] : x[q] - u[q] * r[c];
+            }
+          }
+          if (lane == (p & 31)) usedmask |= 1u << (p >> 5);
+          if (lane == 0) {
+            pivrow[k0 + s] = p;
+            rowstep[p] = k0 + s;
+            rinvs[s] = rinv;
+            if (!(bv > 0.0)) s_sing = 1;
+          }
+          if (lane < NB) {
+            double t = r[0];
+#pragma unroll
+            for (int c = 1; c < NB; ++c)
+              if (lane == c) t = r[c];
+            rblk[s * NB + lane] = t;
+          }
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int q = 0; q < TA; ++q) U[s * LD + lane + 32 * q] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    GJP(2);
+    for (int s = 0; s < nb; ++s) {  // the pivot rows as they stood at the start of the block
+      const int ps = pivrow[k0 + s], tr = ps >> 3;
+      if (wr == tr / TA && gid == (ps & 7)) {
+        const int asel = tr % TA;
+#pragma unroll
+        for (int a = 0; a < TA; ++a)
+          if (a == asel) {
+#pragma unroll
+            for (int b = 0; b < TB; ++b) {
+              const int col = 8 * (TB * wc + b) + 2 * tig;
+              Rm[s * LD + col] = acc[a][b][0];
+              Rm[s * LD + col + 1] = acc[a][b][1];
+            }
+          }
+      }
+    }
+    __syncthreads();
+    GJP(3);
+    if (tid < NP) {  // one thread per column: rows up to date and scaled, then as at the end of the block
+      const int j = tid;
+      const bool inblk = j >= k0 && j < k0 + NB;
+      double r[NB], upp[NB][NB];
+      int ps[NB];
+#pragma unroll
+      for (int s = 0; s < NB; ++s) ps[s] = s < nb ? pivrow[k0 + s] : 0;
+#pragma unroll
+      for (int s = 0; s < NB; ++s)
+#pragma unroll
+        for (int t = 0; t < NB; ++t) upp[t][s] = t != s ? U[t * LD + ps[s]] : 0.0;  // U[t][p_s] (0 for t >= nb)
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        r[s] = 0.0;
+        if (s < nb) {
+          if (inblk) {
+            r[s] = rblk[s * NB + (j - k0)];
+          } else {
+            double v = Rm[s * LD + j];
+#pragma unroll
+            for (int t = 0; t < s; ++t) v -= upp[t][s] * r[t];
+            r[s] = v * rinvs[s];
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        double f = r[s];
+#pragma unroll
+        for (int t = s + 1; t < NB; ++t) f -= upp[t][s] * r[t];
+        Rm[s * LD + j] = r[s];
+        Fm[s * LD + j] = f;
+      }
+    }
+    __syncthreads();
+    GJP(4);
+    {
+      double af[TA];
+#pragma unroll
+      for (int a = 0; a < TA; ++a) af[a] = -U[tig * LD + 8 * (TA * wr + a) + gid];
+#pragma unroll
+      for (int b = 0; b < TB; ++b) {
+        const double bf = Rm[tig * LD + 8 * (TB * wc + b) + gid];
+#pragma unroll
+        for (int a = 0; a < TA; ++a) dmma(acc[a][b][0], acc[a][b][1], af[a], bf);
+      }
+    }
+    for (int s = 0; s < nb; ++s) {
+      const int ps = pivrow[k0 + s], tr = ps >> 3;
+      if (wr == tr / TA && gid == (ps & 7)) {
+        const int asel = tr % TA;
+#pragma unroll
+        for (int a = 0; a < TA; ++a)
+          if (a == asel) {
+#pragma unroll
+            for (int b = 0; b < TB; ++b) {
+              const int col = 8 * (TB * wc + b) + 2 * tig;
+              acc[a][b][0] = Fm[s * LD + col];
+              acc[a][b][1] = Fm[s * LD + col + 1];
+            }
+          }
+      }
+    }
+    if (own_cols) {
+#pragma unroll
+      for (int a = 0; a < TA; ++a)
+#pragma unroll
+        for (int b = 0; b < TB; ++b)
+          if (b == bsel) {
+            const int row = 8 * (TA * wr + a) + gid;
+            acc[a][b][0] = Cb[cloc * LD + row];
+            acc[a][b][1] = Cb[(cloc + 1) * LD + row];
+          }
+    }
+    GJP(5);
+    // no barrier: the next block writes the other Cm buffer, and U / Rm / Fm
+    // only after its first barrier
+  }
+  __syncthreads();
+  // unscramble into X (shared, over the dead panels), then out
+#pragma unroll
+  for (int a = 0; a < TA; ++a)
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * (TA * wr + a) + gid, col = 8 * (TB * wc + b) + 2 * tig + e;
+        if (row < n && col < n) X[rowstep[row] + size_t(pivrow[col]) * n] = acc[a][b][e];
+      }
+  for (int q = tid; q < n; q += kGjT) jb.piv[q] = pivrow[q];
+  __syncthreads();
+  for (int e = tid; e < n * n; e += kGjT) jb.inv[e] = X[e];
+  GJP(6);
+  if (jb.rcond) {
+    const double r = s_sing ? 0.0 : rcond_from_inverse<kGjT>(X, n, s_l1, jb.work, red, ired);
+    if (tid == 0) *jb.rcond = r;
+  }
+  GJP(7);
+  GJP_PRINT;
 }
 
 constexpr int kGjSmemMax = 160;
@@ -4441,6 +4761,7 @@ void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
       }
       const LuJob* d = gtab[c].upload(gj[c], s);
       const unsigned g = unsigned(gj[c].size());
+      KernelTimer kt("gj_inverse", s);
       const size_t sm = gj_smem(nmax);
       if (c == 0)
         gj_inverse_kernel<1, 2><<<g, kT, sm, s>>>(d);
@@ -4450,9 +4771,30 @@ void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
         gj_inverse_kernel<4, 8><<<g, kT, sm, s>>>(d);
       SBX_LAUNCHED();
     }
-    // 128 < n <= 160: shared-memory Gauss-Jordan
+    // 128 < n <= 160: blocked Gauss-Jordan on DMMA accumulator tiles
+    // (SBX_GJ_SMEM=1: the unblocked shared-memory kernel, diagnostics)
     std::vector<LuJob> mid, rest2;
     for (const auto& j : rest) (j.n <= kGjSmemMax ? mid : rest2).push_back(j);
+    static const bool gj_smem_only = std::getenv("SBX_GJ_SMEM") != nullptr;
+    if (!mid.empty() && !gj_smem_only) {
+      int nmax = 1;
+      for (const auto& j : mid) {
+        require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+        require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
+        nmax = std::max(nmax, j.n);
+      }
+      static std::once_flag dattr;
+      std::call_once(dattr, [] {
+        SBX_CUDA(cudaFuncSetAttribute(gj_inverse_dmma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(gj_dmma_smem<5>(kGjSmemMax))));
+      });
+      static thread_local JobTable<LuJob> dtab;
+      const LuJob* d = dtab.upload(mid, s);
+      KernelTimer kt("gj_inverse_dmma", s);
+      gj_inverse_dmma_kernel<5><<<unsigned(mid.size()), kGjT, gj_dmma_smem<5>(nmax), s>>>(d);
+      SBX_LAUNCHED();
+      mid.clear();
+    }
     if (!mid.empty()) {
       int nmax = 1;
       for (const auto& j : mid) {
