@@ -262,7 +262,10 @@ def run_ours(args, rank, world, local_rank):
     line["partitioned"] = part
     if world == 1:
         line["step_dominant"] = step_profile(sb, torch, stream, step, 1e3 * t_dev / args.steps)
+    if world == 1:
+        line["verification"] = field_check(sb, g0, panels, cfg, state)
     if not args.no_apply_bench and world == 1:
+        line["other_configs"] = {"cfg1": small_config_bench(sb, torch, stream, "cfg1")}
         line["woodbury_build"] = roofline_woodbury(sb, torch, stream, g0, h, panels, cfg)
         line["apply_microbench"] = apply_microbench(sb, torch, stream)
     if not args.no_cpu_baseline and world == 1:
@@ -431,14 +434,19 @@ def _kernel_ms(sb, torch, stream, name, fn, reps=10):
     with torch.cuda.stream(stream):
         for _ in range(3):
             fn()
-        sb.api.kernel_timing(True)
-        sb.api.kernel_time(name)
+        # whole calls back to back, without the per-launch timer events
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(reps):
             fn()
         e1.record(stream)
+        torch.cuda.synchronize()
+        # the kernel alone: CUDA events around each launch on its stream
+        sb.api.kernel_timing(True)
+        sb.api.kernel_time(name)
+        for _ in range(reps):
+            fn()
     torch.cuda.synchronize()
     kms, kcnt = sb.api.kernel_time(name)
     sb.api.kernel_timing(False)
@@ -476,6 +484,7 @@ def apply_microbench(sb, torch, stream):
             ach = byts / (ms * 1e-3) / 1e9
             out["rhs1"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                            "frac": round(ach / hbm, 4), "launch_ms": round(ms, 4), "call_ms": round(call_ms, 4),
+                           "call_frac": round(byts / (call_ms * 1e-3) / 1e9 / hbm, 4),
                            "algorithmic_bytes": byts, "traffic": measured_traffic("sweep_gemv")}
         else:
             fl = 2.0 * nrhs * fd
@@ -484,6 +493,64 @@ def apply_microbench(sb, torch, stream):
                                  "frac": round(ach / fp64, 4), "launch_ms": round(ms, 4),
                                  "call_ms": round(call_ms, 4), "algorithmic_flops": fl}
     return out
+
+
+def field_check(sb, g0, panels, cfg, state, cols=(0, 17, 63), n_targets=25):
+    """Untimed check of the timed step's result: the velocity the last timed
+    step's densities induce at interior targets against the Stokeslets that
+    generated the boundary data (the same test the gpu suite asserts at 1e-8)."""
+    g1, _ = sb.refine(g0, panels, cfg.m)
+    tau = state["tau"]
+    tau = tau.cpu().numpy() if hasattr(tau, "cpu") else np.asarray(tau)
+    tg = cfg.interior_targets()[:n_targets]
+    srcs = cfg.sources()
+    worst = 0.0
+    cols = [c for c in cols if c < tau.shape[1]]
+    for j in cols:
+        dens = sb.density_on_refined(state["els"], np.ascontiguousarray(tau[:, j]))
+        vel, _, _ = sb.evaluate_solution(g1, sb.INTERIOR_DIRICHLET, dens, tg)
+        ex = stokeslet_field(srcs[j], tg)
+        worst = max(worst, float(np.max(np.linalg.norm(vel - ex, axis=1) / np.linalg.norm(ex, axis=1))))
+    return {"what": "max relative velocity error of the last timed step's densities vs the generating "
+                    "Stokeslets", "rhs_columns": cols, "targets": len(tg), "max_rel_err": worst}
+
+
+def small_config_bench(sb, torch, stream, name, steps=5, warmup=3):
+    """BASELINE configs[0] (the reference's CPU-runnable case) through the same
+    step on the device: device ms per step (CUDA events on the library
+    stream) and the analytic field error at all its targets."""
+    from paper_2108_07205_b200.configs import CONFIGS
+    cfg = CONFIGS[name]
+    g0, h, panels, G, t_static = build_problem(cfg, sb)
+    G_dev = torch.from_numpy(np.ascontiguousarray(G)).cuda()
+    st = {}
+
+    def step():
+        g1, plan = sb.refine(g0, panels, cfg.m)
+        upd = sb.compress_update(g0, g1, plan, cfg.eps, seed=cfg.seed)
+        els = sb.els_build(h, g0, g1, plan, upd)
+        with torch.cuda.stream(stream):
+            st["tau"] = sb.els_solve(els, G_dev)
+        st["els"], st["upd"] = els, upd
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    info = st["els"].info()
+    chk = field_check(sb, g0, panels, cfg, st, cols=tuple(range(G.shape[1])), n_targets=cfg.targets)
+    return {"workload": f"{name}: {cfg.kind} {cfg.n_panels}x{cfg.q} nodes ({2 * cfg.n_panels * cfg.q} unknowns), "
+                        f"refine {cfg.n_refine} panels m={cfg.m}, {G.shape[1]} RHS, eps {cfg.eps:g}",
+            "ms_per_step": round(ms, 3), "solves_per_s": round(1e3 * G.shape[1] / ms, 2), "steps": steps,
+            "t_static_s": round(t_static, 4), "k": info["k"], "app_hbs": info.get("app_hbs"),
+            "field_max_rel_err": chk["max_rel_err"], "targets": chk["targets"]}
 
 
 def roofline_woodbury(sb, torch, stream, g0, h, panels, cfg):

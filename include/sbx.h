@@ -382,6 +382,13 @@ int sbx_row_id(const double* w, int64_t m, int64_t n, double eps, int64_t forced
  * (PartialPivLU + rcond()).  inv: n*n doubles. */
 int sbx_dense_inverse(const double* a, int64_t n, double* inv, double* rcond);
 
+/* C = A B for host column-major operands (A m x k, B k x n) through the
+ * device GEMM dispatcher the ELS uses (W = I + R X, els.cpp:124; R y and
+ * X z of the Woodbury solve, els.cpp:150) — DMMA tiles, split-K with a
+ * fixed-order reduction, the thin-product kernel for small outputs over a
+ * long inner dimension. */
+int sbx_matmul(const double* a, int64_t m, int64_t k, const double* b, int64_t n, double* c);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     RefinementPlan, add_holes, app_build, boundary_data, circle, coarsen, compress_update, density_on_refined,
     channel, ellipse, els_apply_forward, els_build, els_conditioning, els_gmres, els_solve, els_solve_into, els_solve_raw,
     evaluate_solution,
-    gather_kept_added, hbs_apply, hbs_compress, hbs_invert, hbs_load, hbs_save, hbs_solve, init, kernel_launches, panelize, refine, row_id, dense_inverse,
+    gather_kept_added, hbs_apply, hbs_compress, hbs_invert, hbs_load, hbs_save, hbs_solve, init, kernel_launches, panelize, refine, row_id, dense_inverse, matmul,
     star, submatrix, update_from_factors, update_dump, update_load, dump_matrix, load_matrix,
 )
 from ._sbx import (  # noqa: F401

@@ -74,6 +74,7 @@ _SIGS = [
     ("sbx_kernel_flops", C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_double)]),
     ("sbx_row_id", C.c_int, [F64P, I64, I64, C.c_double, I64, C.c_int, I64P, I64P, F64P]),
     ("sbx_dense_inverse", C.c_int, [F64P, I64, F64P, C.POINTER(C.c_double)]),
+    ("sbx_matmul", C.c_int, [F64P, I64, I64, F64P, I64, F64P]),
     ("sbx_geom_create", C.c_int, [C.POINTER(sbx_curve), C.c_int, C.c_int, C.POINTER(VP)]),
     ("sbx_geom_add_holes", C.c_int,
      [VP, C.c_int, C.POINTER(sbx_curve), C.POINTER(C.c_int32), C.POINTER(C.c_int32),

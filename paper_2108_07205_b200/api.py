@@ -749,6 +749,19 @@ def dense_inverse(a):
     return inv, rc.value
 
 
+def matmul(a, b):
+    """A @ B through the device GEMM dispatcher of the ELS (els.cpp:124, 150)."""
+    _ensure()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    b = np.asfortranarray(np.asarray(b, dtype=np.float64))
+    m, k = a.shape
+    assert b.shape[0] == k
+    n = b.shape[1]
+    c = np.zeros((m, n), order="F")
+    check(lib().sbx_matmul(a.ctypes.data_as(F64P), m, k, b.ctypes.data_as(F64P), n, c.ctypes.data_as(F64P)))
+    return c
+
+
 def kernel_launches(reset: bool = False) -> int:
     return int(lib().sbx_kernel_launches(int(reset)))
 

@@ -206,6 +206,20 @@ int sbx_dense_inverse(const double* a, int64_t n, double* inv, double* rcond) {
   });
 }
 
+int sbx_matmul(const double* a, int64_t m, int64_t k, const double* b, int64_t n, double* c) {
+  return guard([&] {
+    sbx::require(m >= 1 && n >= 1 && k >= 1, "matmul: empty operand");
+    cudaStream_t s = sbx::lib_stream();
+    sbx::DevBuf<double> da(size_t(m * k)), db(size_t(k * n)), dc(size_t(m * n));
+    SBX_CUDA(cudaMemcpyAsync(da.get(), a, size_t(m * k) * 8, cudaMemcpyHostToDevice, s));
+    SBX_CUDA(cudaMemcpyAsync(db.get(), b, size_t(k * n) * 8, cudaMemcpyHostToDevice, s));
+    sbx::gemm_batched({{da.get(), db.get(), dc.get(), int(m), int(n), int(k), int(m), int(k), int(m), 0, 0, 1.0, 0.0}},
+                      s);
+    dc.download(c, size_t(m * n), s);
+    SBX_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 void* sbx_stream(void) {
   try {
     return static_cast<void*>(sbx::lib_stream());

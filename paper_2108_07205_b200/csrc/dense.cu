@@ -2846,6 +2846,135 @@ __global__ void __launch_bounds__(256) gemm_kernel(const GemmJob* __restrict__ j
   }
 }
 
+// ---------------------------------------------------------------- thin product (m, n <= 160, long K)
+// C = A B with a small output and a long inner dimension (the Woodbury
+// operator's R X, els.cpp:124: 146 x 40960 x 146): one CTA per K range
+// computes the WHOLE output block as DMMA accumulator tiles in registers
+// (8 warps, 4 x 2, each 5 x 10 tiles of 8 x 8), so no output-tile padding to
+// 64 and every operand element is read once; A (column-major, rows
+// contiguous) and B (column-major, k contiguous) move through a 4-stage
+// 16-byte cp.async pipeline into layouts whose fragment loads are
+// bank-conflict free.  After a grid barrier (cooperative launch, one CTA per
+// SM) every CTA sums its slice of the output over all partials in a fixed
+// order (deterministic).
+constexpr int kThinKC = 16, kThinStages = 4, kThinTA = 5;
+constexpr int kThinMP = 160;            // 4 warp rows x 5 tiles x 8 = 2 warp columns x 10 tiles x 8
+constexpr int kThinLdA = kThinMP + 4;   // As[k][row]: (tig * ld + gid) distinct mod 16
+constexpr int kThinLdB = kThinKC + 4;   // Bs[col][k]: (gid * ld + tig) distinct mod 16
+struct ThinSmem {
+  double As[kThinStages][kThinKC][kThinLdA];
+  double Bs[kThinStages][kThinMP][kThinLdB];
+};
+
+__device__ __forceinline__ void gcp_async16(double* dst, const double* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+
+template <int WC>  // warp columns: 2 (8 warps, 5 x 10 tiles each) or 4 (16 warps, 5 x 5 tiles each)
+__global__ void __launch_bounds__(128 * WC, 1) thin_gemm_kernel(const GemmJob* __restrict__ jobs) {
+  constexpr int NT = 128 * WC, kThinTB = 20 / WC;
+  extern __shared__ __align__(16) double gsm[];
+  ThinSmem& S = *reinterpret_cast<ThinSmem*>(gsm);
+  const GemmJob jb = jobs[0];
+  const int m = jb.m, n = jb.n;
+  const int kb = int(blockIdx.x) * jb.kchunk, ke = min(jb.k, kb + jb.kchunk);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int mp = (m + 1) / 2;  // 16-byte pairs per A column
+  auto issue = [&](int st, int k0) {
+    for (int e = tid; e < kThinKC * mp; e += NT) {  // A: rows contiguous
+      const int kk = e / mp, r = (e - kk * mp) * 2;
+      const int gk = k0 + kk;
+      const int bytes = gk < ke ? (r + 1 < m ? 16 : 8) : 0;
+      gcp_async16(&S.As[st][kk][r], bytes ? jb.A + r + size_t(gk) * jb.lda : jb.A, bytes);
+    }
+    for (int e = tid; e < n * (kThinKC / 2); e += NT) {  // B: k contiguous
+      const int c = e / (kThinKC / 2), kk = (e - c * (kThinKC / 2)) * 2;
+      const int gk = k0 + kk;
+      const int bytes = gk + 1 < ke ? 16 : (gk < ke ? 8 : 0);
+      gcp_async16(&S.Bs[st][c][kk], bytes ? jb.B + gk + size_t(c) * jb.ldb : jb.B, bytes);
+    }
+  };
+  double acc[kThinTA][kThinTB][2];
+#pragma unroll
+  for (int a = 0; a < kThinTA; ++a)
+#pragma unroll
+    for (int b = 0; b < kThinTB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nch = (ke - kb + kThinKC - 1) / kThinKC;
+#pragma unroll
+  for (int c = 0; c < kThinStages - 1; ++c) {
+    if (c < nch) issue(c, kb + c * kThinKC);
+    gcp_commit();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % kThinStages;
+    gcp_wait<kThinStages - 2>();
+    __syncthreads();  // chunk ch visible; the stage of chunk ch - 1 is free
+    const int nx = ch + kThinStages - 1;
+    if (nx < nch) issue(nx % kThinStages, kb + nx * kThinKC);
+    gcp_commit();
+#pragma unroll
+    for (int k4 = 0; k4 < kThinKC; k4 += 4) {
+      double af[kThinTA];
+#pragma unroll
+      for (int a = 0; a < kThinTA; ++a) af[a] = S.As[st][k4 + tig][8 * (kThinTA * wr + a) + gid];
+#pragma unroll
+      for (int b = 0; b < kThinTB; ++b) {
+        const double bf = S.Bs[st][8 * (kThinTB * wc + b) + gid][k4 + tig];
+#pragma unroll
+        for (int a = 0; a < kThinTA; ++a) dmma(acc[a][b][0], acc[a][b][1], af[a], bf);
+      }
+    }
+  }
+  gcp_wait<0>();
+  double* part = jb.part + size_t(blockIdx.x) * m * n;
+#pragma unroll
+  for (int a = 0; a < kThinTA; ++a)
+#pragma unroll
+    for (int b = 0; b < kThinTB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * (kThinTA * wr + a) + gid, col = 8 * (kThinTB * wc + b) + 2 * tig + e;
+        if (row < m && col < n) part[row + size_t(col) * m] = acc[a][b][e];
+      }
+  // every CTA then reduces its own slice of the output over all partials, in a
+  // fixed order (cooperative launch: the grid is co-resident)
+  cooperative_groups::this_grid().sync();
+  const int total = m * n, G = int(gridDim.x);
+  const int per = (total + G - 1) / G, o0 = int(blockIdx.x) * per;
+  const int cnt = min(per, total - o0);
+  auto store = [&](int o, double v) {
+    const int idx = o0 + o, row = idx % m, col = idx / m;
+    double* dst = jb.C + row + size_t(col) * jb.ldc;
+    v *= jb.alpha;
+    *dst = jb.beta == 0.0 ? v : v + jb.beta * *dst;
+  };
+  if (per <= NT) {  // NT / per groups of threads take interleaved partials; combined in group order
+    const int groups = min(NT / per, 8);
+    const int g = tid / per, o = tid - g * per;
+    double* sred = gsm;
+    if (g < groups && o < cnt) {
+      double v = 0.0;
+      for (int q = g; q < G; q += groups) v += __ldcg(jb.part + size_t(q) * total + o0 + o);
+      sred[g * per + o] = v;
+    }
+    __syncthreads();
+    if (tid < cnt) {
+      double v = sred[tid];
+      for (int q = 1; q < groups; ++q) v += sred[q * per + tid];
+      store(tid, v);
+    }
+  } else {
+    for (int o = tid; o < cnt; o += NT) {
+      double v = 0.0;
+      for (int q = 0; q < G; ++q) v += __ldcg(jb.part + size_t(q) * total + o0 + o);
+      store(o, v);
+    }
+  }
+}
+
 // fixed-order reduction of split-K partials: C = alpha * sum_s part_s + beta * C
 __global__ void splitk_reduce_kernel(const GemmJob* __restrict__ jobs) {
   const GemmJob jb = jobs[blockIdx.y];
@@ -2854,7 +2983,15 @@ __global__ void splitk_reduce_kernel(const GemmJob* __restrict__ jobs) {
   for (i64 idx = blockIdx.x * i64(blockDim.x) + threadIdx.x; idx < total;
        idx += i64(gridDim.x) * blockDim.x) {
     double acc = 0.0;
-    for (int s = 0; s < jb.splitk; ++s) acc += jb.part[size_t(s) * total + idx];
+    int s = 0;
+    for (; s + 16 <= jb.splitk; s += 16) {  // 16 loads in flight, summed in split order
+      double v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __ldcg(jb.part + size_t(s + q) * total + idx);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc += v[q];
+    }
+    for (; s < jb.splitk; ++s) acc += __ldcg(jb.part + size_t(s) * total + idx);
     const i64 row = idx % jb.m, col = idx / jb.m;
     double* dst = jb.C + row + col * jb.ldc;
     const double v = jb.alpha * acc;
@@ -4600,6 +4737,45 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
   static thread_local JobTable<int4> ttab;
   static thread_local DevBuf<double> parts;
   std::vector<GemmJob> js = jobs;
+  // one small output block over a long inner dimension: the thin-product kernel
+  static const bool no_thin = std::getenv("SBX_NO_THIN_GEMM") != nullptr;  // diagnostics
+  if (!no_thin && js.size() == 1) {
+    GemmJob& j = js[0];
+    const bool aligned = (reinterpret_cast<uintptr_t>(j.A) % 16 == 0) && j.lda % 2 == 0 &&
+                         (reinterpret_cast<uintptr_t>(j.B) % 16 == 0) && j.ldb % 2 == 0;
+    if (!j.ta && !j.tb && j.m > 64 && j.n > 64 && j.m <= kThinMP && j.n <= kThinMP && j.k >= 8192 && aligned) {
+      int sms = 148;
+      {
+        int dev = 0;
+        SBX_CUDA(cudaGetDevice(&dev));
+        SBX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      j.kchunk = ((j.k + sms - 1) / sms + kThinKC - 1) / kThinKC * kThinKC;
+      j.splitk = std::max(2, (j.k + j.kchunk - 1) / j.kchunk);  // k >= 8192: always several ranges
+      parts.reserve(size_t(j.splitk) * j.m * j.n);
+      j.part = parts.get();
+      const GemmJob* d = tab.upload(js, s);
+      static std::once_flag tattr;
+      std::call_once(tattr, [] {
+        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sizeof(ThinSmem))));
+        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sizeof(ThinSmem))));
+      });
+      static const int thin_wc = [] {  // diagnostics: SBX_THIN_WC=2 selects the 8-warp variant
+        const char* e = std::getenv("SBX_THIN_WC");
+        return e && std::atoi(e) == 2 ? 2 : 4;
+      }();
+      KernelTimer kt("thin_gemm", s);
+      void* args[] = {(void*)&d};
+      const void* fn = thin_wc == 2 ? reinterpret_cast<const void*>(&thin_gemm_kernel<2>)
+                                    : reinterpret_cast<const void*>(&thin_gemm_kernel<4>);
+      SBX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(j.splitk)), dim3(thin_wc == 2 ? 256 : 512), args,
+                                           sizeof(ThinSmem), s));
+      SBX_LAUNCHED();
+      return;
+    }
+  }
   // split K when a product has few output tiles but a long inner dimension
   i64 out_tiles = 0;
   for (const auto& j : js) out_tiles += i64((j.m + gTM - 1) / gTM) * ((j.n + gTN - 1) / gTN);

@@ -108,6 +108,10 @@ struct FlowCache {
 struct SweepScratch {
   DevBuf<double> ws, io, partials;
   DevBuf<int> counters;
+  // the dataflow kernel zeroes the counters it used before it exits, so a
+  // memset is only needed for memory it has not run over yet
+  const int* counters_zeroed = nullptr;
+  size_t counters_zeroed_n = 0;
   StreamMark mark;  // end of the last sweep on this stream
 };
 
@@ -201,8 +205,16 @@ void hbs_apply(HbsOp& op, const double* v, i64 ldv, i64 nrhs, double* y, i64 ldy
 
 // Row-major workspace form, for callers that already hold the sweep input
 // in `ws` row layout (the ELS path): runs the planned levels only.
+// One right-hand side may be read from / written to the caller's vectors
+// directly (no copy into the workspace's input / output regions).
+struct SweepDirectIo {
+  const double* in = nullptr;
+  double* out = nullptr;
+  i64 in_row = 0, out_row = 0, n = 0;
+};
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s,
-                  const double* fac = nullptr);
+                  const double* fac = nullptr,
+                  const SweepDirectIo* io = nullptr);
 // Column-major rows x nrhs block through `plan` on the stream's scratch:
 // input row i goes to sweep row map[i] (identity when map is null), output
 // row i comes from sweep row map[i]; `transposed` sweeps the transposed

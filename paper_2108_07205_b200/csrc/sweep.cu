@@ -80,7 +80,7 @@ __device__ __forceinline__ void gemv_prefetch(const double* __restrict__ fac, co
 template <int GR>
 __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, double* __restrict__ ws,
                                             const SweepTask& t, int row0, int kb, int ke, const GemvRegs& g,
-                                            double* sm, double* partial) {
+                                            double* sm, double* partial, const SweepDirectIo& io) {
   constexpr int kGS = GemvShape<GR>::kGS, kGV = GemvShape<GR>::kGV;
   const int K = t.K;
   double* xs = sm;                    // K doubles
@@ -90,7 +90,12 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
   // the P row is fetched together with the input vector (one round trip on
   // the critical path instead of two)
   const double pv = (slice == 0 && row < t.m && t.p_row >= 0 && !partial) ? __ldcg(ws + t.p_row + row) : 0.0;
-  for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(ws + t.b_row + j);
+  {
+    // the caller's vector stands in for the workspace's input region
+    const bool direct = io.in && t.b_row >= io.in_row && t.b_row < io.in_row + io.n;
+    const double* xsrc = direct ? io.in + (t.b_row - io.in_row) : ws + t.b_row;
+    for (int j = kb + threadIdx.x; j < ke; j += kThreads) xs[j] = __ldcg(xsrc + j);
+  }
   __syncthreads();
   double acc = 0.0, acc1 = 0.0;
 #pragma unroll
@@ -136,7 +141,10 @@ __device__ __forceinline__ void gemv_finish(const double* __restrict__ fac, doub
     }
     if (t.p_row >= 0) s += pv;
     const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
-    ws[dst] = s;
+    if (io.out && dst >= io.out_row && dst < io.out_row + io.n)
+      io.out[dst - io.out_row] = s;
+    else
+      ws[dst] = s;
   }
 }
 
@@ -337,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
                       const SweepTask* __restrict__ tasks, const FlowItem* __restrict__ items,
                       int n_items, int* __restrict__ counters, int ncol, int nrhs, int ldw,
                       double* __restrict__ partials, int* __restrict__ tile_cnt,
-                      unsigned long long* __restrict__ trace, const ItemDesc* __restrict__ descs) {
+                      unsigned long long* __restrict__ trace, const ItemDesc* __restrict__ descs,
+                      SweepDirectIo io, int ncount) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int s_last;
   __shared__ __align__(16) ItemDesc sdesc[2];
@@ -401,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
                       *reinterpret_cast<DmmaSmem<TN>*>(dsm), part);
     }
     else if (small)
-      gemv_finish<kGRs>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
+      gemv_finish<kGRs>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part, io);
     else
-      gemv_finish<kGR>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part);
+      gemv_finish<kGR>(fac, ws, t, it.row0, it.kb, it.ke, g, dsm, part, io);
     __syncthreads();  // the item's stores happen-before thread 0's release below
     bool done = true;
     if (it.nsplit > 1) {  // last split of the tile reduces the partials in split order
@@ -435,7 +444,10 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
             for (int q = 0; q < it.nsplit; ++q) v += __ldcg(pb + i64(q) * tile_elems + r);
             if (t.p_row >= 0) v += __ldcg(ws + t.p_row + row);
             const i64 dst = row < t.split ? t.d1_row + row : t.d2_row + (row - t.split);
-            ws[dst] = v;
+            if (io.out && dst >= io.out_row && dst < io.out_row + io.n)
+              io.out[dst - io.out_row] = v;
+            else
+              ws[dst] = v;
           }
         }
         __syncthreads();
@@ -456,6 +468,15 @@ __global__ void __launch_bounds__(kThreads, kDmma ? 3 : 4)
       }
     }
   }
+  // The last CTA out zeroes the counters for the next launch on this stream's
+  // scratch (every other CTA has passed its last wait): no memset per call.
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(counters, 1) == G - 1;
+  }
+  __syncthreads();
+  if (s_last)
+    for (int i = threadIdx.x; i < ncount; i += kThreads) counters[i] = 0;
 }
 
 // Per-level launches (diagnostic path, SBX_SWEEP_LEVELS=1).
@@ -468,7 +489,7 @@ __global__ void __launch_bounds__(kThreads)
   const SweepTask t = tasks[it.x];
   GemvRegs g;
   gemv_prefetch<kGR>(fac, t, it.y, 0, t.K, g);
-  gemv_finish<kGR>(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr);
+  gemv_finish<kGR>(fac, ws, t, it.y, 0, t.K, g, dsm, nullptr, SweepDirectIo{});
 }
 
 template <int TN>
@@ -1120,7 +1141,8 @@ void hbs_build_apply_plan(HbsOp& op) {
 
 namespace {
 template <int TN>
-void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
+void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
+              const SweepDirectIo* dio) {
   const bool dmma = nrhs > 1;
   static const bool per_level = std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
   int max_k = 0;
@@ -1218,7 +1240,12 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     sc.counters.reserve(ncount);
     sc.partials.reserve(size_t(std::max<i64>(F.partial_elems, 1)));
   }
-  SBX_CUDA(cudaMemsetAsync(sc.counters.get(), 0, ncount * sizeof(int), s));
+  if (sc.counters_zeroed != sc.counters.get() || sc.counters_zeroed_n < ncount) {
+    // fresh (or regrown) memory; afterwards every launch leaves its counters zero
+    SBX_CUDA(cudaMemsetAsync(sc.counters.get(), 0, sc.counters.size() * sizeof(int), s));
+    sc.counters_zeroed = sc.counters.get();
+    sc.counters_zeroed_n = sc.counters.size();
+  }
   int* counters = sc.counters.get();
   int* tile_cnt = counters + 1 + plan.n_tasks * ncol;
   double* partials = sc.partials.get();
@@ -1231,9 +1258,11 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
   const FlowItem* items = F.d_flow_items.get();
   const ItemDesc* descs = F.d_descs.get();
   int n_items = int(F.n_flow_items), nr = int(nrhs), ldw = dmma ? int(sweep_ld(nrhs)) : 1;
+  SweepDirectIo io = (dio && !dmma) ? *dio : SweepDirectIo{};
+  int ncount_i = int(ncount);
   void* args[] = {(void*)&fac, (void*)&ws, (void*)&tasks, (void*)&items, (void*)&n_items, (void*)&counters,
                   (void*)&ncol, (void*)&nr, (void*)&ldw, (void*)&partials, (void*)&tile_cnt, (void*)&tr,
-                  (void*)&descs};
+                  (void*)&descs, (void*)&io, (void*)&ncount_i};
   // Cooperative launch: the static round-robin item schedule spin-waits on
   // items held by other CTAs, which is only deadlock-free when the whole
   // grid is co-resident -- guaranteed here even when other streams' kernels
@@ -1294,6 +1323,22 @@ void hbs_sweep_rows(HbsOp& op, SweepPlan& plan, const double* in, i64 ldi, i64 r
     sc.ws.reserve(size_t(plan.ws_rows * ldw));
   }
   double* ws = sc.ws.get();
+  // one right-hand side in natural order: the leaf items read the caller's
+  // vector and the last items write the caller's result (no layout kernels)
+  static const bool no_direct = std::getenv("SBX_SWEEP_NO_DIRECT") != nullptr ||
+                                std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
+  const bool disjoint = in + rows <= out || out + rows <= in;
+  if (nrhs == 1 && !map && !no_direct && disjoint && rows == op.n) {
+    SweepDirectIo io;
+    io.in = in;
+    io.out = out;
+    io.in_row = plan.in_row;
+    io.out_row = plan.out_row;
+    io.n = rows;
+    hbs_run_plan(op, plan, ws, nrhs, s, transposed ? op.arena_t.get() : nullptr, &io);
+    sc.mark.record(s);
+    return;
+  }
   launch_cm_to_rm(in, ldi, rows, nrhs, ws + plan.in_row * ldw, ldw, map, s);
   hbs_run_plan(op, plan, ws, nrhs, s, transposed ? op.arena_t.get() : nullptr);
   launch_rm_to_cm(ws + plan.out_row * ldw, ldw, rows, nrhs, out, ldo, map, s);
@@ -1316,6 +1361,24 @@ void hbs_sweep_rm(HbsOp& op, bool apply, bool transpose, const double* b, i64 ld
     sc.ws.reserve(size_t(plan.ws_rows * ldw));
   }
   double* ws = sc.ws.get();
+  {
+    // one dense right-hand side: the sweep reads b and writes x in place of
+    // the workspace's input / output regions (no copies)
+    static const bool no_direct = std::getenv("SBX_SWEEP_NO_DIRECT") != nullptr ||
+                                  std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
+    const bool disjoint = b + op.n <= x || x + op.n <= b;
+    if (nrhs == 1 && ldb == 1 && ldx == 1 && disjoint && !no_direct) {
+      SweepDirectIo io;
+      io.in = b;
+      io.out = x;
+      io.in_row = plan.in_row;
+      io.out_row = plan.out_row;
+      io.n = op.n;
+      hbs_run_plan(op, plan, ws, nrhs, s, transpose ? op.arena_t.get() : nullptr, &io);
+      sc.mark.record(s);
+      return;
+    }
+  }
   // dense rows (ld == nrhs == the workspace pitch): one linear copy; a 2D
   // copy of 8-byte rows runs at a fraction of the bandwidth
   if (ldb == nrhs && ldw == nrhs)
@@ -1332,7 +1395,8 @@ void hbs_sweep_rm(HbsOp& op, bool apply, bool transpose, const double* b, i64 ld
   sc.mark.record(s);
 }
 
-void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac) {
+void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
+                  const SweepDirectIo* io) {
   if (!fac) fac = op.arena.get();
   // column tile: 32 when the block is narrow enough that the tree depth
   // (not the tensor throughput) bounds the sweep (SBX_SWEEP_TN overrides)
@@ -1342,9 +1406,9 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
   }();
   const int tn = tn_env == 32 || tn_env == 64 ? tn_env : (nrhs <= 192 ? 32 : 64);
   if (tn == 32)
-    run_flow<32>(op, plan, ws, nrhs, s, fac);
+    run_flow<32>(op, plan, ws, nrhs, s, fac, io);
   else
-    run_flow<64>(op, plan, ws, nrhs, s, fac);
+    run_flow<64>(op, plan, ws, nrhs, s, fac, io);
 }
 
 namespace {
