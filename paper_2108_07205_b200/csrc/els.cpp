@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include "idengine.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <limits>
 
@@ -15,12 +17,17 @@ namespace sbx {
 
 namespace {
 
+// widths (columns) of the last Woodbury build / solve sweeps: hints for
+// build_app_solver's item-table prebuild
+std::atomic<i64> g_hint_build_cols{0}, g_hint_solve_cols{0};
+
 std::vector<i64> scalars(const std::vector<i64>& nodes) {
-  std::vector<i64> o;
-  o.reserve(2 * nodes.size());
-  for (i64 n : nodes) {
-    o.push_back(2 * n);
-    o.push_back(2 * n + 1);
+  std::vector<i64> o(2 * nodes.size());
+  i64* d = o.data();
+  const i64* n = nodes.data();
+  for (size_t i = 0, e = nodes.size(); i < e; ++i) {  // indexed stores: this runs on the step's critical path
+    d[2 * i] = 2 * n[i];
+    d[2 * i + 1] = 2 * n[i] + 1;
   }
   return o;
 }
@@ -121,6 +128,14 @@ std::shared_ptr<AppSolver> build_app_solver(const Geom& new_g, const Plan& plan,
       id_rendezvous_leave();
     }
     hbs_build_solve_plan(*a->h);
+    // this runs beside the update compression (update.cpp: A_pp thread); the
+    // sweeps over the new A_pp come right after it, at the widths of the
+    // previous step's Woodbury build and solve: build their item tables here
+    // rather than on the critical path
+    for (const auto* hint : {&g_hint_build_cols, &g_hint_solve_cols}) {
+      const i64 w = hint->load(std::memory_order_relaxed);
+      if (w > 0) hbs_prebuild_flow(*a->h, a->h->solve_plan, w, s);
+    }
   }
   return a;
 }
@@ -131,24 +146,36 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
   require(a_oo.has_inverse, "els_build: diagonal solver lacks inverse");
   auto e = std::make_unique<Els>();
   e->a_oo = &a_oo;
-  const auto kept_old_s = scalars(plan.kept_old), cut_s = scalars(plan.cut_old);
-  e->kept_new_s = scalars(plan.kept_new);
-  e->added_s = scalars(plan.added_new);
-  e->kept_old_s = kept_old_s;
-  e->cut_s = cut_s;
   e->old_g = &old_g;
   e->new_g = &new_g;
   e->form = form;
   e->mu = mu;
-  e->n_k = i64(kept_old_s.size());
-  e->n_c = i64(cut_s.size());
-  e->n_p = i64(e->added_s.size());
+  e->n_k = 2 * i64(plan.kept_old.size());
+  e->n_c = 2 * i64(plan.cut_old.size());
+  e->n_p = 2 * i64(plan.added_new.size());
   e->n_new = new_g.n_nodes();
   require(a_oo.n == e->n_k + e->n_c, "els_build: diagonal solver size does not match the old mesh");
   require(upd.n_ext() == e->n_ext(), "els_build: update factor size does not match the plan");
-  std::vector<i64> old_of_ext = kept_old_s;
-  old_of_ext.insert(old_of_ext.end(), cut_s.begin(), cut_s.end());
-  e->d_old_of_ext.upload(old_of_ext, s);
+  {  // ext rows (kept, cut) -> old-mesh scalars: all the first sweep needs from the host
+    std::vector<i64> old_of_ext(size_t(e->n_k + e->n_c));
+    i64* d = old_of_ext.data();
+    for (const i64 nd : plan.kept_old) {
+      *d++ = 2 * nd;
+      *d++ = 2 * nd + 1;
+    }
+    for (const i64 nd : plan.cut_old) {
+      *d++ = 2 * nd;
+      *d++ = 2 * nd + 1;
+    }
+    e->d_old_of_ext.upload(old_of_ext, s);
+  }
+  // the host-side index maps of the handle are filled while the device works
+  auto fill_host_maps = [&] {
+    e->kept_old_s = scalars(plan.kept_old);
+    e->cut_s = scalars(plan.cut_old);
+    e->kept_new_s = scalars(plan.kept_new);
+    e->added_s = scalars(plan.added_new);
+  };
   if (e->n_p > 0) {
     if (upd.app && upd.app->matches(new_g, plan, form, mu, a_oo.eps))
       e->app = upd.app;
@@ -163,6 +190,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
     SBX_CUDA(cudaMemcpyAsync(e->R.get(), upd.R.get(), size_t(k * n) * 8, cudaMemcpyDeviceToDevice, s));
     e->X.resize(size_t(n * k));
     e->L = upd.L;
+    g_hint_build_cols.store(k, std::memory_order_relaxed);
     atilde_solve(*e, upd.L->get(), n, e->X.get(), n, k, s);
     phase_mark("els: X = Atilde^-1 L", s);
     // W = I + R X  (els.cpp:124)
@@ -172,6 +200,7 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
                  s);
     launch_add_identity(e->Wmat.get(), k, k, s);
     phase_mark("els:   W = I + R X", s);
+    fill_host_maps();
     DevBuf<double> wlu(static_cast<size_t>(k * k));
     SBX_CUDA(cudaMemcpyAsync(wlu.get(), e->Wmat.get(), size_t(k * k) * 8, cudaMemcpyDeviceToDevice, s));
     e->Winv.resize(size_t(k * k));
@@ -180,6 +209,8 @@ std::unique_ptr<Els> els_build_device(HbsOp& a_oo, const Geom& old_g, const Geom
       throw Error(4,
                   "woodbury operator numerically singular; consider the optimal-basis compression "
                   "mode at woodbury solve");
+  } else {
+    fill_host_maps();
   }
   SBX_CUDA(cudaStreamSynchronize(s));
   phase_mark("els: W, LU(W)", s);
@@ -258,6 +289,7 @@ void els_solve(Els& e, const double* g, i64 ldg, i64 nrhs, double* y, i64 ldy, b
   const i64 rows_in = raw ? n : e.n_k + e.n_p;
   require(ldg >= rows_in && ldy >= rows_in, "els_solve: leading dimension too small");
   if (nrhs == 0) return;
+  if (!tr) g_hint_solve_cols.store(nrhs, std::memory_order_relaxed);
   double* gx = e.scratch_for(s).ws(size_t(2 * n * nrhs), s);
   double* yx = gx + n * nrhs;
   const i64 nkc = e.n_k + e.n_c;

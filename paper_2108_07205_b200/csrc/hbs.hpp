@@ -215,6 +215,9 @@ struct SweepDirectIo {
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s,
                   const double* fac = nullptr,
                   const SweepDirectIo* io = nullptr);
+// Builds (and uploads) the dataflow item tables of `plan` for blocks of nrhs
+// right-hand sides ahead of the first sweep of that width.
+void hbs_prebuild_flow(HbsOp& op, SweepPlan& plan, i64 nrhs, cudaStream_t s);
 // Column-major rows x nrhs block through `plan` on the stream's scratch:
 // input row i goes to sweep row map[i] (identity when map is null), output
 // row i comes from sweep row map[i]; `transposed` sweeps the transposed

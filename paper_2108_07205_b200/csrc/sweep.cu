@@ -1142,7 +1142,7 @@ void hbs_build_apply_plan(HbsOp& op) {
 namespace {
 template <int TN>
 void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
-              const SweepDirectIo* dio) {
+              const SweepDirectIo* dio, bool build_only) {
   const bool dmma = nrhs > 1;
   static const bool per_level = std::getenv("SBX_SWEEP_LEVELS") != nullptr;  // diagnostics
   int max_k = 0;
@@ -1218,6 +1218,7 @@ void run_flow(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, 
     SBX_CUDA(cudaStreamSynchronize(s));  // other streams may launch over these tables next
   }
   lk.unlock();
+  if (build_only) return;  // hbs_prebuild_flow: the item tables of this width now exist
   if (per_level) {
     for (const int2 rg : F.level_items) {
       if (rg.y == 0) continue;
@@ -1395,8 +1396,23 @@ void hbs_sweep_rm(HbsOp& op, bool apply, bool transpose, const double* b, i64 ld
   sc.mark.record(s);
 }
 
+namespace {
+void run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
+              const SweepDirectIo* io, bool build_only);
+}
+
 void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
                   const SweepDirectIo* io) {
+  run_plan(op, plan, ws, nrhs, s, fac, io, false);
+}
+
+void hbs_prebuild_flow(HbsOp& op, SweepPlan& plan, i64 nrhs, cudaStream_t s) {
+  if (nrhs >= 1) run_plan(op, plan, nullptr, nrhs, s, nullptr, nullptr, true);
+}
+
+namespace {
+void run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t s, const double* fac,
+              const SweepDirectIo* io, bool build_only) {
   if (!fac) fac = op.arena.get();
   // column tile: 32 when the block is narrow enough that the tree depth
   // (not the tensor throughput) bounds the sweep (SBX_SWEEP_TN overrides)
@@ -1406,10 +1422,11 @@ void hbs_run_plan(HbsOp& op, SweepPlan& plan, double* ws, i64 nrhs, cudaStream_t
   }();
   const int tn = tn_env == 32 || tn_env == 64 ? tn_env : (nrhs <= 192 ? 32 : 64);
   if (tn == 32)
-    run_flow<32>(op, plan, ws, nrhs, s, fac, io);
+    run_flow<32>(op, plan, ws, nrhs, s, fac, io, build_only);
   else
-    run_flow<64>(op, plan, ws, nrhs, s, fac, io);
+    run_flow<64>(op, plan, ws, nrhs, s, fac, io, build_only);
 }
+}  // namespace
 
 namespace {
 void run_sweep(HbsOp& op, SweepPlan& plan, const double* b, i64 ldb, i64 nrhs, double* x, i64 ldx,
