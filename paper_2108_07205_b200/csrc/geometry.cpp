@@ -256,41 +256,43 @@ bool inside(const CurveDef& cv, double qx, double qy, int samples = 512) {  // g
   return crossings % 2 == 1;
 }
 
-// skip (optional, per panel of the component): leave the node arrays of
-// those panels zero for the caller to fill (refine copies kept nodes bit for
-// bit, so evaluating the curve there is wasted work).
-void append_nodes(Geom& g, i64 ci, const std::vector<char>* skip = nullptr) {  // geometry.cpp:149-179
+// One Gauss node of panel pd appended to the node arrays (geometry.cpp:149-179).
+inline void push_node(Geom& g, const Component& comp, const GaussTable& gt, const PanelDef& pd, double half,
+                      int j, double sgn, i64 pid) {
+  const double t = pd.a + half * (gt.x[size_t(j)] + 1.0);
+  double px, py, dx, dy, ddx, ddy;
+  comp.curve.eval(t, px, py, dx, dy, ddx, ddy);
+  const double sp = std::sqrt(dx * dx + dy * dy);
+  const double nn = std::sqrt(dy * dy + dx * dx);  // |(dy, -dx)|
+  g.x.push_back(px);
+  g.y.push_back(py);
+  g.nx.push_back(sgn * (dy / nn));
+  g.ny.push_back(sgn * (-dx / nn));
+  g.tx.push_back(dx / sp);
+  g.ty.push_back(dy / sp);
+  g.w.push_back(gt.w[size_t(j)] * sp * half);
+  g.kappa.push_back(sgn * ((dx * ddy - dy * ddx) / (sp * sp * sp)));
+  g.t.push_back(t);
+  g.panel_of.push_back(pid);
+}
+
+inline void reserve_nodes(Geom& g, size_t total) {
+  for (auto* v : {&g.x, &g.y, &g.nx, &g.ny, &g.tx, &g.ty, &g.w, &g.kappa, &g.t}) v->reserve(total);
+  g.panel_of.reserve(total);
+}
+
+void append_nodes(Geom& g, i64 ci) {  // geometry.cpp:149-179
   Component& comp = g.comps[size_t(ci)];
   const GaussTable& gt = gauss_table(comp.q);
   const int q = comp.q;
   const double sgn = comp.curve.p.flip_normal ? -1.0 : 1.0;
+  reserve_nodes(g, size_t(g.n_nodes()) + comp.panels.size() * size_t(q));
   for (size_t pl = 0; pl < comp.panels.size(); ++pl) {
     const PanelDef& pd = comp.panels[pl];
     const i64 pid = i64(g.panels.size());
     g.panels.push_back({ci, i64(pl), pd.a, pd.b, pd.level, g.n_nodes(), q});
     const double half = 0.5 * (pd.b - pd.a);
-    if (skip && (*skip)[pl]) {
-      for (auto* v : {&g.x, &g.y, &g.nx, &g.ny, &g.tx, &g.ty, &g.w, &g.kappa, &g.t}) v->resize(v->size() + size_t(q));
-      g.panel_of.insert(g.panel_of.end(), size_t(q), pid);
-      continue;
-    }
-    for (int j = 0; j < q; ++j) {
-      const double t = pd.a + half * (gt.x[size_t(j)] + 1.0);
-      double px, py, dx, dy, ddx, ddy;
-      comp.curve.eval(t, px, py, dx, dy, ddx, ddy);
-      const double sp = std::sqrt(dx * dx + dy * dy);
-      const double nn = std::sqrt(dy * dy + dx * dx);  // |(dy, -dx)|
-      g.x.push_back(px);
-      g.y.push_back(py);
-      g.nx.push_back(sgn * (dy / nn));
-      g.ny.push_back(sgn * (-dx / nn));
-      g.tx.push_back(dx / sp);
-      g.ty.push_back(dy / sp);
-      g.w.push_back(gt.w[size_t(j)] * sp * half);
-      g.kappa.push_back(sgn * ((dx * ddy - dy * ddx) / (sp * sp * sp)));
-      g.t.push_back(t);
-      g.panel_of.push_back(pid);
-    }
+    for (int j = 0; j < q; ++j) push_node(g, comp, gt, pd, half, j, sgn, pid);
   }
 }
 
@@ -412,59 +414,75 @@ std::pair<std::unique_ptr<Geom>, std::unique_ptr<Plan>> geom_refine(const Geom& 
   plan->panel_ids = ids;
   plan->m = m;
   auto ng = std::make_unique<Geom>();
+  // Unrefined panels keep their nodes bit for bit: runs of them are copied
+  // from the old arrays in bulk; only the m sub-panels of a refined panel
+  // evaluate the curve (this is the per-step path of a moving refinement).
+  size_t total = 0;
+  for (const auto& o : g.panels) total += size_t(o.q) * (refined[size_t(&o - g.panels.data())] ? size_t(m) : 1);
+  reserve_nodes(*ng, total);
+  ng->panels.reserve(g.panels.size() + ids.size() * size_t(m - 1));
+  plan->kept_old.reserve(size_t(g.n_nodes()));
+  plan->kept_new.reserve(size_t(g.n_nodes()));
+  const std::vector<double>* src[9] = {&g.x, &g.y, &g.nx, &g.ny, &g.tx, &g.ty, &g.w, &g.kappa, &g.t};
+  std::vector<double>* dst[9] = {&ng->x, &ng->y, &ng->nx, &ng->ny, &ng->tx, &ng->ty, &ng->w, &ng->kappa, &ng->t};
   for (size_t ci = 0; ci < g.comps.size(); ++ci) {
     const Component& comp = g.comps[ci];
     plan->old_panels.push_back(comp.panels);
     plan->old_q.push_back(comp.q);
+    const GaussTable& gt = gauss_table(comp.q);
+    const int q = comp.q;
+    const double sgn = comp.curve.p.flip_normal ? -1.0 : 1.0;
     std::vector<PanelDef> mesh;
-    std::vector<char> kept;  // new panels that are unrefined copies
+    mesh.reserve(comp.panels.size() + ids.size() * size_t(m - 1));
+    const i64 node_offset = ng->n_nodes(), panel_offset = i64(ng->panels.size());
+    i64 run_a = -1, run_b = -1;  // pending run of kept old nodes [run_a, run_b)
+    auto flush = [&] {
+      if (run_a < 0) return;
+      for (int a = 0; a < 9; ++a) dst[a]->insert(dst[a]->end(), src[a]->begin() + run_a, src[a]->begin() + run_b);
+      run_a = run_b = -1;
+    };
     for (size_t pl = 0; pl < comp.panels.size(); ++pl) {
       const PanelDef& p = comp.panels[pl];
+      const PanelRow& o = g.panels[size_t(comp.panel_offset + i64(pl))];
       if (refined[size_t(comp.panel_offset + i64(pl))]) {
+        flush();
+        for (int j = 0; j < o.q; ++j) plan->cut_old.push_back(o.node_begin + j);
         double prev = p.a;
-        for (int j = 1; j <= m; ++j) {
-          const double next = (j == m) ? p.b : p.a + (p.b - p.a) * j / m;
-          mesh.push_back({prev, next, p.level + 1});
-          kept.push_back(0);
+        for (int sp = 1; sp <= m; ++sp) {
+          const double next = (sp == m) ? p.b : p.a + (p.b - p.a) * sp / m;
+          const PanelDef pd{prev, next, p.level + 1};
+          const i64 pid = i64(ng->panels.size());
+          ng->panels.push_back({i64(ci), i64(mesh.size()), pd.a, pd.b, pd.level, ng->n_nodes(), q});
+          mesh.push_back(pd);
+          const double half = 0.5 * (pd.b - pd.a);
+          for (int j = 0; j < q; ++j) {
+            plan->added_new.push_back(ng->n_nodes());
+            push_node(*ng, comp, gt, pd, half, j, sgn, pid);
+          }
           prev = next;
         }
       } else {
+        const i64 pid = i64(ng->panels.size());
+        // nodes already appended plus the pending run = this panel's first node
+        const i64 nb = ng->n_nodes() + (run_a < 0 ? 0 : run_b - run_a);
+        ng->panels.push_back({i64(ci), i64(mesh.size()), p.a, p.b, p.level, nb, q});
         mesh.push_back(p);
-        kept.push_back(1);
+        if (run_a >= 0 && run_b == o.node_begin) {
+          run_b += o.q;
+        } else {
+          flush();
+          run_a = o.node_begin;
+          run_b = o.node_begin + o.q;
+        }
+        for (int j = 0; j < o.q; ++j) {
+          plan->kept_old.push_back(o.node_begin + j);
+          plan->kept_new.push_back(nb + j);
+        }
+        ng->panel_of.insert(ng->panel_of.end(), size_t(o.q), pid);
       }
     }
-    ng->comps.push_back({comp.curve, std::move(mesh), comp.q, ng->n_nodes(), i64(ng->panels.size()),
-                         comp.is_hole});
-    append_nodes(*ng, i64(ci), &kept);
-  }
-  i64 new_panel = 0;
-  for (i64 op = 0; op < np; ++op) {
-    const PanelRow& o = g.panels[size_t(op)];
-    if (refined[size_t(op)]) {
-      for (int j = 0; j < o.q; ++j) plan->cut_old.push_back(o.node_begin + j);
-      for (int sp = 0; sp < m; ++sp) {
-        const PanelRow& nr = ng->panels[size_t(new_panel + sp)];
-        for (int j = 0; j < nr.q; ++j) plan->added_new.push_back(nr.node_begin + j);
-      }
-      new_panel += m;
-    } else {
-      const PanelRow& nr = ng->panels[size_t(new_panel)];
-      for (int j = 0; j < o.q; ++j) {  // kept nodes copied bit for bit
-        const size_t a = size_t(o.node_begin + j), b = size_t(nr.node_begin + j);
-        plan->kept_old.push_back(i64(a));
-        plan->kept_new.push_back(i64(b));
-        ng->x[b] = g.x[a];
-        ng->y[b] = g.y[a];
-        ng->nx[b] = g.nx[a];
-        ng->ny[b] = g.ny[a];
-        ng->tx[b] = g.tx[a];
-        ng->ty[b] = g.ty[a];
-        ng->w[b] = g.w[a];
-        ng->kappa[b] = g.kappa[a];
-        ng->t[b] = g.t[a];
-      }
-      new_panel += 1;
-    }
+    flush();
+    ng->comps.push_back({comp.curve, std::move(mesh), comp.q, node_offset, panel_offset, comp.is_hole});
   }
   return {std::move(ng), std::move(plan)};
 }

@@ -1,5 +1,6 @@
 // Library runtime: device selection, the library stream, launch counting,
 // the caching device allocator and the optional phase timer.
+#include <malloc.h>
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -117,8 +118,25 @@ std::int64_t launches(bool reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }
 
+namespace {
+// The per-step host path builds multi-megabyte index and node vectors; with
+// glibc's defaults every one of them is a fresh mmap (page faults on first
+// touch, munmap on free: ~0.6 ms of a 0.75 ms refine).  Keep blocks up to
+// 32 MB on the heap and do not trim it between steps.  SBX_NO_MALLOPT=1
+// leaves the host process's allocator alone.
+void tune_host_allocator() {
+#if defined(__GLIBC__)
+  if (std::getenv("SBX_NO_MALLOPT")) return;
+  mallopt(M_MMAP_THRESHOLD, 32 << 20);
+  mallopt(M_TRIM_THRESHOLD, 512 << 20);
+  mallopt(M_TOP_PAD, 64 << 20);
+#endif
+}
+}  // namespace
+
 cudaStream_t lib_stream() {
   std::call_once(g_once, [] {
+    tune_host_allocator();
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
       throw Error(6, "no CUDA device visible: the sbx library has no CPU fallback");
