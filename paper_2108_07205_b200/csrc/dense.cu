@@ -2957,7 +2957,16 @@ __global__ void __launch_bounds__(128 * WC, 1) thin_gemm_kernel(const GemmJob* _
     double* sred = gsm;
     if (g < groups && o < cnt) {
       double v = 0.0;
-      for (int q = g; q < G; q += groups) v += __ldcg(jb.part + size_t(q) * total + o0 + o);
+      const double* src = jb.part + o0 + o;
+      int q = g;
+      for (; q + 15 * groups < G; q += 16 * groups) {  // 16 loads in flight, summed in split order
+        double t[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) t[i] = __ldcg(src + size_t(q + i * groups) * total);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v += t[i];
+      }
+      for (; q < G; q += groups) v += __ldcg(src + size_t(q) * total);
       sred[g * per + o] = v;
     }
     __syncthreads();
@@ -3565,7 +3574,7 @@ constexpr int gj_dmma_ld() { return 32 * TA + 4; }
 template <int TA>
 size_t gj_dmma_smem(int n) {
   const size_t head = (64 + 32 + 2 * 16 * TA) * sizeof(double);  // red, ired, pivrow/rowstep
-  const size_t panels = (5 * kGjNb * size_t(gj_dmma_ld<TA>()) + 32) * sizeof(double);
+  const size_t panels = (7 * kGjNb * size_t(gj_dmma_ld<TA>()) + 32) * sizeof(double);
   return head + std::max(panels, size_t(n) * n * sizeof(double));
 }
 
@@ -3604,8 +3613,9 @@ __global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* _
   int* pivrow = ired + 64;                           // NP
   int* rowstep = pivrow + NP;                        // NP
   double* body = sm + 64 + 32 + 2 * 16 * TA;
-  double* Cm = body;                // 2 x NB x LD: the block's columns (double buffered)
-  double* U = Cm + 2 * NB * LD;     // NB x LD: pivot columns (0 at the step's pivot row)
+  double* Cm = body;                // 2 x 2 x NB x LD: the block's columns (double buffered across blocks,
+                                    // and ping-pong between the steps of a panel)
+  double* U = Cm + 4 * NB * LD;     // NB x LD: pivot columns (0 at the step's pivot row)
   double* Rm = U + NB * LD;         // NB x LD: scaled pivot rows; before that the raw rows
   double* Fm = Rm + NB * LD;        // NB x LD: pivot rows as they stand at the end of the block
   double* rblk = Fm + NB * LD;      // NB x NB: the pivot rows inside the block's columns
@@ -3646,7 +3656,8 @@ __global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* _
     const int tc0 = k0 >> 3, half = (k0 >> 2) & 1;
     const bool own_cols = wc == tc0 / TB && (tig >> 1) == half;
     const int bsel = tc0 % TB, cloc = (2 * tig) & 3;
-    double* Cb = Cm + (blk & 1) * NB * LD;
+    double* Cb = Cm + (blk & 1) * 2 * NB * LD;         // panel input (step 0 reads it)
+    double* Cfin = Cb + (nb & 1) * NB * LD;            // where the panel's last step leaves the columns
     if (own_cols) {
 #pragma unroll
       for (int a = 0; a < TA; ++a)
@@ -3660,59 +3671,58 @@ __global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* _
     }
     __syncthreads();
     GJP(1);
-    if (warp == 0) {  // the n x 4 panel, in place in shared memory: lane owns rows lane + 32 q
+    if (warp == 0) {  // the n x 4 panel in shared memory: lane owns rows lane + 32 q
 #pragma unroll
       for (int s = 0; s < NB; ++s) {
+        // step s reads one buffer and writes the other (no load waits on a store)
+        const double* __restrict__ pin = Cb + (s & 1) * NB * LD;
+        double* __restrict__ pout = Cb + ((s + 1) & 1) * NB * LD;
         if (s < nb) {
           double cs[TA];
-          double bv = -1.0;
+#pragma unroll
+          for (int q = 0; q < TA; ++q) cs[q] = pin[s * LD + lane + 32 * q];
+          // pivot: first largest |x| over the unused rows, compared as integers
+          // (the bit pattern of |x| is monotone; NaN counts as the largest)
+          long long bk = -1;
           int bi = 0x7fffffff;
 #pragma unroll
-          for (int q = 0; q < TA; ++q) cs[q] = Cb[s * LD + lane + 32 * q];
-#pragma unroll
           for (int q = 0; q < TA; ++q) {
-            double v = fabs(cs[q]);
-            if (!(v == v)) v = DBL_MAX;  // a NaN column still yields a definite row
             const int i = lane + 32 * q;
-            if (i < n && !((usedmask >> q) & 1u) && v > bv) {
-              bv = v;
+            long long key = __double_as_longlong(fabs(cs[q]));
+            if (key > 0x7ff0000000000000ll) key = 0x7ff0000000000000ll;
+            if (i < n && !((usedmask >> q) & 1u) && key > bk) {
+              bk = key;
               bi = i;
             }
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-              bv = ov;
-              bi = oi;
-            }
-          }
-          const int p = bi;
+          const int hi = int(bk >> 32);
+          const unsigned lo = unsigned(bk);
+          const int mh = __reduce_max_sync(0xffffffffu, hi);
+          const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+          const int p = int(__reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? unsigned(bi) : 0x7fffffffu));
+          const bool nonzero = mh > 0 || (mh == 0 && ml > 0);
           double r[NB];  // the scaled pivot row inside the block's columns
 #pragma unroll
-          for (int c = 0; c < NB; ++c) r[c] = Cb[c * LD + p];
+          for (int c = 0; c < NB; ++c) r[c] = pin[c * LD + p];
           const double piv = r[s];
           const double rinv = piv != 0.0 ? 1.0 / piv : 0.0;
 #pragma unroll
           for (int c = 0; c < NB; ++c) r[c] = c == s ? rinv : r[c] * rinv;
-          __syncwarp();  // row p read by every lane before its owner rewrites it
-          double u[TA];
 #pragma unroll
           for (int q = 0; q < TA; ++q) {
             const int i = lane + 32 * q;
-            u[q] = i == p ? 0.0 : cs[q];
-            U[s * LD + i] = u[q];
+            if (i == p) cs[q] = 0.0;  // u: the pivot column, zero at the pivot row
+            U[s * LD + i] = cs[q];
           }
 #pragma unroll
           for (int c = 0; c < NB; ++c) {
             double x[TA];
 #pragma unroll
-            for (int q = 0; q < TA; ++q) x[q] = c == s ? 0.0 : Cb[c * LD + lane + 32 * q];
+            for (int q = 0; q < TA; ++q) x[q] = c == s ? 0.0 : pin[c * LD + lane + 32 * q];
 #pragma unroll
             for (int q = 0; q < TA; ++q) {
               const int i = lane + 32 * q;
-              Cb[c * LD + i] = i == p ? r[c] : x[q] - u[q] * r[c];
+              pout[c * LD + i] = i == p ? r[c] : x[q] - cs[q] * r[c];
             }
           }
           if (lane == (p & 31)) usedmask |= 1u << (p >> 5);
@@ -3720,7 +3730,7 @@ __global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* _
             pivrow[k0 + s] = p;
             rowstep[p] = k0 + s;
             rinvs[s] = rinv;
-            if (!(bv > 0.0)) s_sing = 1;
+            if (!nonzero) s_sing = 1;
           }
           if (lane < NB) {
             double t = r[0];
@@ -3826,8 +3836,8 @@ __global__ void __launch_bounds__(kGjT, 1) gj_inverse_dmma_kernel(const LuJob* _
         for (int b = 0; b < TB; ++b)
           if (b == bsel) {
             const int row = 8 * (TA * wr + a) + gid;
-            acc[a][b][0] = Cb[cloc * LD + row];
-            acc[a][b][1] = Cb[(cloc + 1) * LD + row];
+            acc[a][b][0] = Cfin[cloc * LD + row];
+            acc[a][b][1] = Cfin[(cloc + 1) * LD + row];
           }
     }
     GJP(5);
@@ -4917,6 +4927,31 @@ void lu_batched(const std::vector<LuJob>& all, cudaStream_t s) {
   if (!no_gj) {
     std::vector<LuJob> gj[3], rest;
     for (const auto& j : jobs) (j.n <= 32 ? gj[0] : j.n <= 64 ? gj[1] : j.n <= kGjMax ? gj[2] : rest).push_back(j);
+    // 64 < n <= 128 on the DMMA-tile kernel too (4 x 8 tiles per warp): 133 us at n = 96, 170 us at
+    // n = 128 against 207 / 302 us of the register kernel below (SBX_GJ_DMMA128=0 restores it)
+    static const bool dmma128 = [] {
+      const char* e = std::getenv("SBX_GJ_DMMA128");
+      return !e || std::atoi(e) != 0;
+    }();
+    if (dmma128 && !gj[2].empty()) {
+      int nmax = 1;
+      for (const auto& j : gj[2]) {
+        require(j.inv != nullptr, "lu_batched: the explicit inverse output is required");
+        require(!j.rcond || j.work != nullptr, "lu_batched: rcond needs 4n scratch");
+        nmax = std::max(nmax, j.n);
+      }
+      static std::once_flag d4attr;
+      std::call_once(d4attr, [] {
+        SBX_CUDA(cudaFuncSetAttribute(gj_inverse_dmma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(gj_dmma_smem<4>(kGjMax))));
+      });
+      static thread_local JobTable<LuJob> d4tab;
+      const LuJob* d = d4tab.upload(gj[2], s);
+      KernelTimer kt("gj_inverse", s);
+      gj_inverse_dmma_kernel<4><<<unsigned(gj[2].size()), kGjT, gj_dmma_smem<4>(nmax), s>>>(d);
+      SBX_LAUNCHED();
+      gj[2].clear();
+    }
     static thread_local JobTable<LuJob> gtab[3];
     static std::once_flag gattr;
     std::call_once(gattr, [] {
