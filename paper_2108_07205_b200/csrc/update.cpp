@@ -547,8 +547,58 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   u->nc2 = 2 * i64(plan.cut_old.size());
   u->np2 = 2 * i64(plan.added_new.size());
   if (u->nc2 == 0 && u->np2 == 0) return u;
+  // (the entry oracles first: they build the meshes' lazily shared single-layer
+  // tables, which the A_pp thread's own oracle must find in place)
   EntryOracle eold(og, form, mu, s), enew(ng, form, mu, s);
   const bool with_null = enew.has_nullspace();
+  const double app_eps = eps;  // els_build adopts it when a_oo was built at this eps
+  auto t_app = [&](cudaStream_t w) {
+    if (plan.added_new.empty()) return;
+    try {
+      u->app = build_app_solver(ng, plan, form, mu, app_eps, w);
+    } catch (const Error&) {
+      u->app.reset();  // els_build rebuilds it and reports the error there
+    }
+    phase_mark("update: A_pp inverse (for els_build)", w);
+  };
+  static const int par_mode = [] {
+    const char* e = std::getenv("SBX_PAR_MODE");
+    return e ? std::atoi(e) : 4;
+  }();
+  // mode 4: the A_pp HBS build runs in a second host thread on the SAME
+  // stream; its factorisations and the update's share joint CPQR launches
+  // through a rendezvous until one side has no more of them.  The thread
+  // starts before the host-side setup below (proxy circles, far / near
+  // split, partition trees: ~0.8 ms during which the device would idle).
+  std::unique_ptr<IdRendezvous> rv;
+  std::thread app_thread;
+  std::exception_ptr app_err;
+  if (par_mode == 4 && !plan.added_new.empty()) {
+    rv = std::make_unique<IdRendezvous>(2);
+    int dev = 0;
+    SBX_CUDA(cudaGetDevice(&dev));
+    app_thread = std::thread([&, dev] {
+      try {
+        SBX_CUDA(cudaSetDevice(dev));
+        StreamScope ss(s);
+        IdRendezvousScope rs(rv.get());
+        phase_mark(nullptr, s);
+        t_app(s);
+      } catch (...) {
+        app_err = std::current_exception();
+      }
+    });
+  }
+  // on any exception below: main_rs leaves the rendezvous first (so the
+  // A_pp thread's pending and later factorisations launch on their own),
+  // then the thread is joined before it is destroyed -- never terminate()
+  struct JoinOnExit {
+    std::thread& t;
+    ~JoinOnExit() {
+      if (t.joinable()) t.join();
+    }
+  } join_app{app_thread};
+  IdRendezvousScope main_rs(rv.get());
   const auto circles = make_proxy_circles(ng, plan);
   const double div = 3.0;
   // shared far-field ID over the kept rows (lowrank.cpp:275-287)
@@ -640,16 +690,6 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     pk_near = near_row_id(enew.view(), added_s, mapped(kept_new_s, near_s), eps, notes_pk, "pk", w);
     phase_mark("update: pk near ID", w);
   };
-  const double app_eps = eps;  // els_build adopts it when a_oo was built at this eps
-  auto t_app = [&](cudaStream_t w) {
-    if (plan.added_new.empty()) return;
-    try {
-      u->app = build_app_solver(ng, plan, form, mu, app_eps, w);
-    } catch (const Error&) {
-      u->app.reset();  // els_build rebuilds it and reports the error there
-    }
-    phase_mark("update: A_pp inverse (for els_build)", w);
-  };
   // SBX_PAR_MODE:
   //   4 (default) the row-ID hierarchies of the update in lockstep on the
   //     library stream, and the A_pp HBS build in a second host thread on
@@ -663,43 +703,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   // Measured on cfg2 (bench, 10 steps): mode 4 32-33 ms, mode 2 35 ms;
   // modes 0/1/3 vary widely from run to run (co-scheduling of the
   // large-smem CPQR kernels of two streams is not stable).
-  static const int par_mode = [] {
-    const char* e = std::getenv("SBX_PAR_MODE");
-    return e ? std::atoi(e) : 4;
-  }();
   if (par_mode == 2 || par_mode == 4) {
-    // mode 4: the A_pp HBS build runs in a second host thread on the SAME
-    // stream; its factorisations and the update's share joint CPQR launches
-    // through a rendezvous until one side has no more of them
-    std::unique_ptr<IdRendezvous> rv;
-    std::thread app_thread;
-    std::exception_ptr app_err;
-    if (par_mode == 4 && !plan.added_new.empty()) {
-      rv = std::make_unique<IdRendezvous>(2);
-      int dev = 0;
-      SBX_CUDA(cudaGetDevice(&dev));
-      app_thread = std::thread([&, dev] {
-        try {
-          SBX_CUDA(cudaSetDevice(dev));
-          StreamScope ss(s);
-          IdRendezvousScope rs(rv.get());
-          phase_mark(nullptr, s);
-          t_app(s);
-        } catch (...) {
-          app_err = std::current_exception();
-        }
-      });
-    }
-    // on any exception below: main_rs leaves the rendezvous first (so the
-    // A_pp thread's pending and later factorisations launch on their own),
-    // then the thread is joined before it is destroyed -- never terminate()
-    struct JoinOnExit {
-      std::thread& t;
-      ~JoinOnExit() {
-        if (t.joinable()) t.join();
-      }
-    } join_app{app_thread};
-    IdRendezvousScope main_rs(rv.get());
     // every row-ID hierarchy of the update advances in lockstep (one batched
     // CPQR per tree level across all of them)
     std::vector<std::vector<i64>> ptree;
