@@ -489,11 +489,12 @@ HierSpec near_spec(const EntryView& v, const std::vector<i64>& rowsc, const std:
 }
 
 std::vector<i64> scalars(const std::vector<i64>& nodes) {
-  std::vector<i64> o;
-  o.reserve(2 * nodes.size());
-  for (i64 n : nodes) {
-    o.push_back(2 * n);
-    o.push_back(2 * n + 1);
+  std::vector<i64> o(2 * nodes.size());
+  i64* d = o.data();
+  const i64* n = nodes.data();
+  for (size_t i = 0, e = nodes.size(); i < e; ++i) {  // indexed stores: per-step host path
+    d[2 * i] = 2 * n[i];
+    d[2 * i + 1] = 2 * n[i] + 1;
   }
   return o;
 }
@@ -623,7 +624,13 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
         const double x = ng.x[size_t(far_nodes[size_t(i)])], y = ng.y[size_t(far_nodes[size_t(i)])];
         for (const auto& c : circles)
           best = std::min(best, std::sqrt((x - c.cx) * (x - c.cx) + (y - c.cy) * (y - c.cy)) / c.r0);
-        band[size_t(i)] = int(std::floor(std::log2(std::max(1.0, best))));
+        // floor(log2(max(1, best))) (proxy.cpp:91-129) through the binary exponent;
+        // log2 itself only within 1e-14 of the next power of two, where its
+        // rounding decides the band
+        const double bb = std::max(1.0, best);
+        int e2 = std::ilogb(bb);
+        if (bb >= std::ldexp(1.0, e2 + 1) * (1.0 - 1e-14)) e2 = int(std::floor(std::log2(bb)));
+        band[size_t(i)] = e2;
       }
       std::stable_sort(order.begin(), order.end(),
                        [&](i64 a, i64 b) { return band[size_t(a)] < band[size_t(b)]; });
