@@ -13,7 +13,9 @@
 #include "update.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <numeric>
@@ -501,16 +503,39 @@ std::vector<i64> scalars(const std::vector<i64>& nodes) {
 
 }  // namespace
 
+namespace {
+// Diagnostics (SBX_HOST_TIMING): host wall time between marks of the update's
+// setup, without device synchronisation.
+struct HostMarks {
+  bool on = std::getenv("SBX_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sbx-host] %-28s %8.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+};
+}  // namespace
+
 std::vector<ProxyCircleH> make_proxy_circles(const Geom& g, const Plan& plan) {
   std::vector<ProxyCircleH> out;
   if (plan.added_new.empty()) return out;
   const size_t nc = g.comps.size();
   std::vector<std::vector<std::pair<double, double>>> pts(nc);
-  std::vector<std::set<i64>> pans(nc);
+  std::vector<std::vector<i64>> pans(nc);  // the panels of the added nodes, ascending and unique per component
+  for (auto& p : pts) p.reserve(plan.added_new.size() + 2 * 64);
   for (i64 node : plan.added_new) {
-    const i64 c = g.component_of(node);
+    const i64 pid = g.panel_of[size_t(node)];
+    const i64 c = g.panels[size_t(pid)].component;
     pts[size_t(c)].push_back({g.x[size_t(node)], g.y[size_t(node)]});
-    pans[size_t(c)].insert(g.panel_of[size_t(node)]);
+    auto& pc = pans[size_t(c)];
+    if (pc.empty() || pc.back() != pid) pc.push_back(pid);  // nodes come panel by panel
+  }
+  for (auto& pc : pans) {
+    std::sort(pc.begin(), pc.end());
+    pc.erase(std::unique(pc.begin(), pc.end()), pc.end());
   }
   for (size_t c = 0; c < nc; ++c) {
     auto& p = pts[c];
@@ -600,7 +625,9 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     }
   } join_app{app_thread};
   IdRendezvousScope main_rs(rv.get());
+  HostMarks hm;
   const auto circles = make_proxy_circles(ng, plan);
+  hm("circles");
   const double div = 3.0;
   // shared far-field ID over the kept rows (lowrank.cpp:275-287)
   std::vector<i64> far_pos, near_pos;
@@ -611,6 +638,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   }
   std::vector<i64> far_nodes;
   for (i64 p : far_pos) far_nodes.push_back(plan.kept_new[size_t(p)]);
+  hm("far/near split");
   // dyadic-by-distance partition (proxy.cpp:91-129)
   std::vector<std::vector<i64>> ktree;
   {
@@ -632,8 +660,13 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
         if (bb >= std::ldexp(1.0, e2 + 1) * (1.0 - 1e-14)) e2 = int(std::floor(std::log2(bb)));
         band[size_t(i)] = e2;
       }
-      std::stable_sort(order.begin(), order.end(),
-                       [&](i64 a, i64 b) { return band[size_t(a)] < band[size_t(b)]; });
+      // stable order by band: a counting sort (bands are a handful of small integers)
+      int bmax = 0;
+      for (int b : band) bmax = std::max(bmax, b);
+      std::vector<i64> start(size_t(bmax) + 2, 0);
+      for (int b : band) ++start[size_t(b) + 1];
+      for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+      for (i64 i = 0; i < n; ++i) order[size_t(start[size_t(band[size_t(i)])]++)] = i;
     }
     size_t pos = 0;
     while (pos < order.size()) {
@@ -647,10 +680,12 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     }
   }
   phase_mark("update: setup", s);
+  hm("bands + ktree");
   const std::vector<i64> far_s = scalars(far_pos), near_s = scalars(near_pos);
   // kept-row blocks kc (old oracle) and kp (new oracle)  (lowrank.cpp:130-180)
   const std::vector<i64> kept_old_s = scalars(plan.kept_old), kept_new_s = scalars(plan.kept_new);
   const std::vector<i64> cut_s = scalars(plan.cut_old), added_s = scalars(plan.added_new);
+  hm("scalars");
   auto mapped = [](const std::vector<i64>& map, const std::vector<i64>& idx) {
     std::vector<i64> o;
     o.reserve(idx.size());
@@ -727,9 +762,11 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     const FarPrep fk = far_prepare(ng, far_nodes, circles, true, ktree);
     FarPrep fp;
     if (!plan.added_new.empty()) fp = far_prepare(ng, plan.added_new, circles, false, ptree);
+  hm("far_prepare");
     const std::vector<i64> kc_rows = do_kc ? mapped(kept_old_s, near_s) : std::vector<i64>{};
     const std::vector<i64> kp_rows = do_kp ? mapped(kept_new_s, near_s) : std::vector<i64>{};
     const std::vector<i64> pk_cols = do_pk_near ? mapped(kept_new_s, near_s) : std::vector<i64>{};
+  hm("mapped");
     std::vector<HierSpec> specs;
     specs.push_back({fk.m, fk.leaves, proxy_builder(enew.view(), far_nodes, circles, fk.factor, 64, with_null, s)});
     specs.push_back({fk.m, fk.leaves, proxy_builder(enew.view(), far_nodes, circles, fk.factor, 128, with_null, s)});
@@ -740,6 +777,7 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     specs.push_back(near_spec(eold.view(), kc_rows, cut_s, notes_kc, "kc", s));
     specs.push_back(near_spec(enew.view(), kp_rows, added_s, notes_kp, "kp", s));
     specs.push_back(near_spec(enew.view(), added_s, pk_cols, notes_pk, "pk", s));
+  hm("specs");
     auto res = hierarchical_id_multi(specs, eps, s);
     phase_mark("update: lockstep row IDs", s);
     far = far_settle(enew.view(), far_nodes, circles, with_null, fk, std::move(res[0]), std::move(res[1]), eps, s);
