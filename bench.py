@@ -831,7 +831,9 @@ def run_transient(args, rank, world, local_rank):
     worst, ks, n_ref = 0.0, [], 0
     for i in sched:
         geom, tau, els, k = step(i)
-        tau = tau.cpu().numpy() if hasattr(tau, "cpu") else tau
+        if hasattr(tau, "cpu"):  # the result is ordered on the library stream: read it there
+            with torch.cuda.stream(stream):
+                tau = tau.cpu().numpy()
         dens = sb.density_on_refined(els, tau) if els is not None else tau
         vel, _, _ = sb.evaluate_solution(geom, sb.INTERIOR_DIRICHLET, dens, tg)
         worst = max(worst, float(np.max(np.linalg.norm(vel - exact, axis=1) / np.linalg.norm(exact, axis=1))))
