@@ -2871,9 +2871,11 @@ __device__ __forceinline__ void gcp_async16(double* dst, const double* src, int 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
 }
 
-template <int WC>  // warp columns: 2 (8 warps, 5 x 10 tiles each) or 4 (16 warps, 5 x 5 tiles each)
+// WC warp columns x TB tile columns per warp: <2, 10> (8 warps) or <4, 5> (16 warps) cover 160 output
+// columns, <4, 2> covers 64 (R y of a 64-RHS Woodbury solve)
+template <int WC, int TB>
 __global__ void __launch_bounds__(128 * WC, 1) thin_gemm_kernel(const GemmJob* __restrict__ jobs) {
-  constexpr int NT = 128 * WC, kThinTB = 20 / WC;
+  constexpr int NT = 128 * WC, kThinTB = TB;
   extern __shared__ __align__(16) double gsm[];
   ThinSmem& S = *reinterpret_cast<ThinSmem*>(gsm);
   const GemmJob jb = jobs[0];
@@ -4753,7 +4755,7 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
     GemmJob& j = js[0];
     const bool aligned = (reinterpret_cast<uintptr_t>(j.A) % 16 == 0) && j.lda % 2 == 0 &&
                          (reinterpret_cast<uintptr_t>(j.B) % 16 == 0) && j.ldb % 2 == 0;
-    if (!j.ta && !j.tb && j.m > 64 && j.n > 64 && j.m <= kThinMP && j.n <= kThinMP && j.k >= 8192 && aligned) {
+    if (!j.ta && !j.tb && j.m > 64 && j.n >= 32 && j.m <= kThinMP && j.n <= kThinMP && j.k >= 8192 && aligned) {
       int sms = 148;
       {
         int dev = 0;
@@ -4767,9 +4769,11 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
       const GemmJob* d = tab.upload(js, s);
       static std::once_flag tattr;
       std::call_once(tattr, [] {
-        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(sizeof(ThinSmem))));
-        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(sizeof(ThinSmem))));
+        SBX_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(sizeof(ThinSmem))));
       });
       static const int thin_wc = [] {  // diagnostics: SBX_THIN_WC=2 selects the 8-warp variant
@@ -4778,10 +4782,12 @@ void gemm_batched(const std::vector<GemmJob>& jobs, cudaStream_t s) {
       }();
       KernelTimer kt("thin_gemm", s);
       void* args[] = {(void*)&d};
-      const void* fn = thin_wc == 2 ? reinterpret_cast<const void*>(&thin_gemm_kernel<2>)
-                                    : reinterpret_cast<const void*>(&thin_gemm_kernel<4>);
-      SBX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(j.splitk)), dim3(thin_wc == 2 ? 256 : 512), args,
-                                           sizeof(ThinSmem), s));
+      const bool narrow = j.n <= 64;
+      const void* fn = narrow         ? reinterpret_cast<const void*>(&thin_gemm_kernel<4, 2>)
+                       : thin_wc == 2 ? reinterpret_cast<const void*>(&thin_gemm_kernel<2, 10>)
+                                      : reinterpret_cast<const void*>(&thin_gemm_kernel<4, 5>);
+      SBX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(j.splitk)), dim3(!narrow && thin_wc == 2 ? 256 : 512),
+                                           args, sizeof(ThinSmem), s));
       SBX_LAUNCHED();
       return;
     }

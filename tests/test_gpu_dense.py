@@ -71,7 +71,7 @@ def test_dense_inverse_singular_reports_zero_rcond():
 
 
 @pytest.mark.parametrize("m,k,n", [(146, 40960, 146), (160, 8192, 65), (65, 9000, 160), (129, 20002, 131),
-                                   (146, 40960, 64), (64, 4096, 64), (200, 10000, 100), (7, 100, 5)])
+                                   (146, 40960, 64), (100, 16384, 40), (64, 4096, 64), (200, 10000, 100), (7, 100, 5)])
 def test_matmul_matches_numpy(m, k, n):
     """The GEMM dispatcher across its routes (64 x 64 DMMA tiles, split-K,
     the thin-product kernel for W = I + R X: els.cpp:124)."""
