@@ -279,7 +279,15 @@ void IdRendezvous::leave() noexcept {
   }
 }
 
-IdRendezvousScope::IdRendezvousScope(IdRendezvous* rv) : rv_(rv), prev_(tl_rv) { tl_rv = rv; }
+void IdRendezvous::enter() {
+  std::lock_guard<std::mutex> lk(mu_);
+  ++active_;
+}
+
+IdRendezvousScope::IdRendezvousScope(IdRendezvous* rv, bool enter) : rv_(rv), prev_(tl_rv) {
+  if (rv && enter) rv->enter();
+  tl_rv = rv;
+}
 IdRendezvousScope::~IdRendezvousScope() { leave(); }
 void IdRendezvousScope::leave() noexcept {
   if (rv_) {

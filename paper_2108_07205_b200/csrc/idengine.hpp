@@ -70,6 +70,9 @@ class IdRendezvous {
   // Never throws (called during unwinding): a failed flush is handed to the
   // waiting participants instead.
   void leave() noexcept;
+  // A participant that was not counted at construction joins (its rounds are
+  // joint from its first submit on; the others never waited for it before).
+  void enter();
 
  private:
   // Starts a new round BEFORE launching (pending jobs moved out, generation
@@ -91,7 +94,8 @@ class IdRendezvous {
 // leaves it (at the latest) on destruction.
 class IdRendezvousScope {
  public:
-  explicit IdRendezvousScope(IdRendezvous* rv);
+  // enter: the thread was not counted in the rendezvous' participants yet
+  explicit IdRendezvousScope(IdRendezvous* rv, bool enter = false);
   ~IdRendezvousScope();
   void leave() noexcept;
   IdRendezvousScope(const IdRendezvousScope&) = delete;

@@ -597,10 +597,16 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
   // starts before the host-side setup below (proxy circles, far / near
   // split, partition trees: ~0.8 ms during which the device would idle).
   std::unique_ptr<IdRendezvous> rv;
+  bool rv_entered = true;  // false: the main thread still has to enter the rendezvous
   std::thread app_thread;
   std::exception_ptr app_err;
   if (par_mode == 4 && !plan.added_new.empty()) {
-    rv = std::make_unique<IdRendezvous>(2);
+    // the A_pp thread alone at first: its rounds launch on their own until the
+    // main thread has finished the setup below and enters with its first batch
+    // (SBX_RV_WAIT=1: both counted from the start, the A_pp thread waits)
+    static const bool rv_wait = std::getenv("SBX_RV_WAIT") != nullptr;
+    rv = std::make_unique<IdRendezvous>(rv_wait ? 2 : 1);
+    rv_entered = rv_wait;
     int dev = 0;
     SBX_CUDA(cudaGetDevice(&dev));
     app_thread = std::thread([&, dev] {
@@ -624,7 +630,9 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
       if (t.joinable()) t.join();
     }
   } join_app{app_thread};
-  IdRendezvousScope main_rs(rv.get());
+  // (counted from the start only with SBX_RV_WAIT; else it enters below)
+  std::unique_ptr<IdRendezvousScope> main_rs_early;
+  if (rv && rv_entered) main_rs_early = std::make_unique<IdRendezvousScope>(rv.get());
   HostMarks hm;
   const auto circles = make_proxy_circles(ng, plan);
   hm("circles");
@@ -778,6 +786,8 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     specs.push_back(near_spec(enew.view(), kp_rows, added_s, notes_kp, "kp", s));
     specs.push_back(near_spec(enew.view(), added_s, pk_cols, notes_pk, "pk", s));
   hm("specs");
+    std::unique_ptr<IdRendezvousScope> main_rs_late;
+    if (rv && !rv_entered) main_rs_late = std::make_unique<IdRendezvousScope>(rv.get(), true);
     auto res = hierarchical_id_multi(specs, eps, s);
     phase_mark("update: lockstep row IDs", s);
     far = far_settle(enew.view(), far_nodes, circles, with_null, fk, std::move(res[0]), std::move(res[1]), eps, s);
@@ -787,7 +797,8 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
     kc_near = std::move(res[4]);
     kp_near = std::move(res[5]);
     pk_near = std::move(res[6]);
-    main_rs.leave();
+    if (main_rs_late) main_rs_late->leave();
+    if (main_rs_early) main_rs_early->leave();
     if (app_thread.joinable()) {
       app_thread.join();
       if (app_err) std::rethrow_exception(app_err);
