@@ -177,7 +177,8 @@ def run_ours(args, rank, world, local_rank):
     g0, h, panels, G, t_static = build_problem(cfg, sb)
     nrhs = G.shape[1]
     stream = torch.cuda.ExternalStream(sb.api.lib().sbx_stream())
-    G_dev = torch.from_numpy(np.ascontiguousarray(G)).cuda()  # rows x nrhs (C order)
+    # rows x nrhs, resident in HBM in the C-ABI's column-major layout (a transposed view of nrhs x rows)
+    G_dev = torch.from_numpy(np.ascontiguousarray(G.T)).cuda().t()
     # e2e: the drop-in caller path -- column-major HOST buffers (pinned) handed
     # to sbx_els_solve, which copies them in, solves and copies the density
     # back before returning (host<->device copies inside the timed region)
