@@ -16,7 +16,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <numeric>
 #include <set>
@@ -446,10 +448,10 @@ FarPrep far_prepare(const Geom& g, const std::vector<i64>& nodes, const std::vec
   f.m = 2 * i64(nodes.size());
   if (nodes.empty()) return f;
   for (const auto& lf : tree_leaves) {
-    std::vector<i64> rows;
-    for (i64 p : lf) {
-      rows.push_back(2 * p);
-      rows.push_back(2 * p + 1);
+    std::vector<i64> rows(2 * lf.size());
+    for (size_t i = 0; i < lf.size(); ++i) {
+      rows[2 * i] = 2 * lf[i];
+      rows[2 * i + 1] = 2 * lf[i] + 1;
     }
     f.leaves.push_back(std::move(rows));
   }
@@ -661,11 +663,14 @@ std::unique_ptr<Update> update_compress_device(const Geom& og, const Geom& ng, c
         for (const auto& c : circles)
           best = std::min(best, std::sqrt((x - c.cx) * (x - c.cx) + (y - c.cy) * (y - c.cy)) / c.r0);
         // floor(log2(max(1, best))) (proxy.cpp:91-129) through the binary exponent;
-        // log2 itself only within 1e-14 of the next power of two, where its
-        // rounding decides the band
+        // log2 itself only within 64 ulp (1.4e-14) of the next power of two,
+        // where its rounding decides the band
         const double bb = std::max(1.0, best);
-        int e2 = std::ilogb(bb);
-        if (bb >= std::ldexp(1.0, e2 + 1) * (1.0 - 1e-14)) e2 = int(std::floor(std::log2(bb)));
+        std::uint64_t bits;
+        std::memcpy(&bits, &bb, sizeof bits);
+        int e2 = int((bits >> 52) & 0x7ff) - 1023;  // bb >= 1: a normal number
+        const std::uint64_t frac = bits & 0xfffffffffffffull;
+        if (frac >= 0xfffffffffffffull - 64 || !std::isfinite(bb)) e2 = int(std::floor(std::log2(bb)));
         band[size_t(i)] = e2;
       }
       // stable order by band: a counting sort (bands are a handful of small integers)
