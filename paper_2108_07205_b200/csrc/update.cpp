@@ -33,6 +33,23 @@
 namespace sbx {
 
 namespace {
+// Diagnostics (SBX_HOST_TIMING): host wall time between marks of the update's
+// setup, without device synchronisation.
+struct HostMarks {
+  bool on = std::getenv("SBX_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  void operator()(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sbx-host] %-28s %8.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+  }
+};
+}  // namespace
+
+
+namespace {
 
 struct RowIdResult {
   i64 m = 0, k = 0;
@@ -82,7 +99,9 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       keep.push_back(std::move(buf));
     }
     IdBatch ids;
+    HostMarks hm;
     ids.factor(all, eps, s);
+    hm("  leaves: factor (host+sync)");
     std::vector<i64> ks(all.size()), off(all.size());
     i64 tot = 0;
     for (size_t p = 0; p < all.size(); ++p) {
@@ -97,7 +116,9 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       P[p] = pb->get() + off[p];
       ldp[p] = std::max<int>(1, int(specs[who[p].first].leaves[who[p].second].size()));
     }
+    hm("  leaves: ranks + alloc");
     ids.interp(ks, P, ldp, s);
+    hm("  leaves: interp launch");
     for (size_t p = 0; p < all.size(); ++p) {
       const auto& lf = specs[who[p].first].leaves[who[p].second];
       Chunk c;
@@ -108,6 +129,7 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       level[who[p].first].push_back(std::move(c));
     }
     keep.push_back(std::move(pb));
+    hm("  leaves: chunks");
     phase_mark("  hier: leaves", s);
   }
   for (;;) {
@@ -503,22 +525,6 @@ std::vector<i64> scalars(const std::vector<i64>& nodes) {
   return o;
 }
 
-}  // namespace
-
-namespace {
-// Diagnostics (SBX_HOST_TIMING): host wall time between marks of the update's
-// setup, without device synchronisation.
-struct HostMarks {
-  bool on = std::getenv("SBX_HOST_TIMING") != nullptr;
-  std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
-  void operator()(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[sbx-host] %-28s %8.1f us\n", what,
-                 std::chrono::duration<double, std::micro>(now - last).count());
-    last = now;
-  }
-};
 }  // namespace
 
 std::vector<ProxyCircleH> make_proxy_circles(const Geom& g, const Plan& plan) {
