@@ -575,6 +575,19 @@ def roofline_woodbury(sb, torch, stream, g0, h, panels, cfg):
         if rep:
             ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
+    # one more build with the per-launch timers on: where the build's device time goes
+    sb.api.kernel_timing(True)
+    names = ("sweep_flow_dmma", "thin_gemm", "gj_inverse_dmma")
+    for nm in names:
+        sb.api.kernel_time(nm)
+    with torch.cuda.stream(stream):
+        els = sb.els_build(h, g0, g1, plan, upd)
+    torch.cuda.synchronize()
+    parts = {}
+    for nm in names:
+        t, c = sb.api.kernel_time(nm)
+        parts[nm] = {"ms": round(t, 4), "launches": int(c)}
+    sb.api.kernel_timing(False)
     e = els.info()
     u = e["k"]
     n_ext = e["n_k"] + e["n_c"] + e["n_p"]
@@ -584,7 +597,8 @@ def roofline_woodbury(sb, torch, stream, g0, h, panels, cfg):
     ach = fl / (ms * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(ach, 3), "peak": fp64, "unit": "TFLOP/s",
             "frac": round(ach / fp64, 4), "ms": round(ms, 4), "u": u, "n_ext": n_ext,
-            "algorithmic_flops": fl}
+            "algorithmic_flops": fl,
+            "kernels": parts}  # the two Atilde^-1 sweeps over the u columns, R X, the inverse of W
 
 
 def phase_split(sb, torch, stream, g0, h, panels, cfg, G_dev):
