@@ -85,6 +85,15 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
   const size_t H = specs.size();
   std::vector<std::unique_ptr<DevBuf<double>>> keep;
   std::vector<std::vector<Chunk>> level(H);
+  static const bool no_defer = std::getenv("SBX_NO_DEFER") != nullptr;  // diagnostics
+  std::function<void()> deferred;  // the previous round's interpolation / merge launches
+  auto run_deferred = [&] {
+    if (deferred) {
+      auto f = std::move(deferred);
+      deferred = nullptr;
+      f();
+    }
+  };
   // leaves
   {
     std::vector<IdProblem> all;
@@ -98,7 +107,8 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       all.insert(all.end(), probs.begin(), probs.end());
       keep.push_back(std::move(buf));
     }
-    IdBatch ids;
+    auto idsp = std::make_shared<IdBatch>();
+    IdBatch& ids = *idsp;
     HostMarks hm;
     ids.factor(all, eps, s);
     hm("  leaves: factor (host+sync)");
@@ -117,7 +127,12 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       ldp[p] = std::max<int>(1, int(specs[who[p].first].leaves[who[p].second].size()));
     }
     hm("  leaves: ranks + alloc");
-    ids.interp(ks, P, ldp, s);
+    // the interpolation matrices are not needed by the next round's W^T
+    // assembly or its factorization: their launch (and its host-side job
+    // tables) is queued after that assembly's launches, so the device
+    // assembles while the host prepares them (SBX_NO_DEFER: at once)
+    deferred = [idsp, ks, P, ldp, s] { idsp->interp(ks, P, ldp, s); };
+    if (no_defer) run_deferred();
     hm("  leaves: interp launch");
     for (size_t p = 0; p < all.size(); ++p) {
       const auto& lf = specs[who[p].first].leaves[who[p].second];
@@ -155,7 +170,9 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       all.insert(all.end(), probs.begin(), probs.end());
       keep.push_back(std::move(buf));
     }
-    IdBatch ids;
+    run_deferred();  // behind this round's W^T assembly launches
+    auto idsp = std::make_shared<IdBatch>();
+    IdBatch& ids = *idsp;
     ids.factor(all, eps, s);
     std::vector<i64> ks(all.size()), ioff(all.size()), poff(all.size());
     i64 itot = 0, ptot = 0;
@@ -178,7 +195,6 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
         IP[p] = ib->get() + ioff[p];
         ldi[p] = std::max<int>(1, int(unis[h][q].size()));
       }
-    ids.interp(ks, IP, ldi, s);
     std::vector<GemmJob> gj;
     for (size_t h = 0; h < H; ++h) {
       std::vector<Chunk> next;
@@ -208,11 +224,16 @@ std::vector<RowIdResult> hierarchical_id_multi(const std::vector<HierSpec>& spec
       if (level[h].size() % 2 == 1) next.push_back(level[h].back());
       if (!unis[h].empty()) level[h] = std::move(next);
     }
-    gemm_batched(gj, s);
+    deferred = [idsp, ks, IP, ldi, gj, s] {
+      idsp->interp(ks, IP, ldi, s);
+      gemm_batched(gj, s);
+    };
+    if (no_defer) run_deferred();
     phase_mark("  hier: merge level", s);
     keep.push_back(std::move(ib));
     keep.push_back(std::move(pb));
   }
+  run_deferred();
   std::vector<RowIdResult> outs(H);
   // the roots' interpolation matrices scattered into the m-row outputs: all
   // hierarchies in one launch (one upload of the concatenated row maps)
